@@ -1,0 +1,476 @@
+#!/usr/bin/env python
+"""bench.py -- MTL-par GNN training-step throughput on B200 (contract: DESIGN.md "Measurement").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+  (N>1: launched by torchrun, one rank per GPU; NCCL data path, gloo plumbing)
+
+Workload "mtl5-weak" (BASELINE.json metric: train structures/sec, 5-head MTL,
+1/2/4/8 B200, weak scaling): the reference's default5_specs() five-source mix
+(src/dataset.cpp:213-239), ModelHyper{L=4, H=W=128, head_depth=3, rc=5},
+model seed 7.  Per-GPU work is fixed: a per-GPU edge budget split over heads
+in proportion {1,1,1,2,3} (GPUs per head at 8 ranks), so the 1-GPU batch is
+{102,58,74,24,18} structures and at N GPUs every rank serves its heads'
+shares from hmtl_head_placement (each rank samples only its heads' sources).
+One step = device batch assembly -> neighbour list -> forward -> SPEC loss ->
+backward -> head-group + global allreduce (N>1) -> AdamW, one CUDA graph.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+for _p in (ROOT, os.path.join(ROOT, "oracle")):
+    if _p not in sys.path:
+        sys.path.insert(0, _p)
+
+HEADS = 5
+WEIGHTS = (1, 1, 1, 2, 3)
+# mean edges/structure of the default5 sources at rc 5
+EDGES_PER_STRUCT = (59, 104, 81, 488, 989)
+UNIT_EDGES = 48000  # per-GPU edge budget of one step
+HYPER = dict(n_species=20, layers=4, hidden=128, head_width=128, head_depth=3, n_heads=5, cutoff=5.0)
+N_BATCHES = 4  # distinct batches cycled per rank
+WORKLOAD = "mtl5-weak"
+
+
+def batch_counts():
+    from paper_2506_21788_b200.data import mtl_batch_counts
+
+    return mtl_batch_counts(EDGES_PER_STRUCT, UNIT_EDGES, WEIGHTS)
+
+
+def arena_bytes(G, N):
+    a16 = lambda x: (x + 15) & ~15
+    go = 16
+    ds = a16(go + 4 * (G + 1))
+    sp = a16(ds + G)
+    pos = a16(sp + N)
+    le = pos + 24 * N
+    lf = le + 8 * G
+    return a16(lf + 24 * N)
+
+
+def rank_batches(rank, world, nb=N_BATCHES):
+    """This rank's batches: for each owned head k, world*n_k*share[rank,k]
+    structures per step, drawn from head k's source (seed 1234+k), the group
+    members taking disjoint slices (the taskpar routing rule of
+    src/datastore.cpp:57-81)."""
+    from paper_2506_21788_b200 import data
+    from paper_2506_21788_b200.model import Samples
+
+    share = data.head_placement(world, WEIGHTS)
+    counts = batch_counts()
+    specs = data.default5_specs()
+    heads = [k for k in range(HEADS) if share[rank, k] > 0]
+    parts = {}
+    for k in heads:
+        members = [r for r in range(world) if share[r, k] > 0]
+        per_step = int(round(world * counts[k] * share[rank, k]))
+        slot = members.index(rank)
+        pool = data.generate_dataset(specs[k], 1234 + k, count=per_step * nb * len(members))
+        parts[k] = (pool, per_step, slot)
+    batches = []
+    for b in range(nb):
+        sel = []
+        for k in heads:
+            pool, per_step, slot = parts[k]
+            start = (slot * nb + b) * per_step
+            sel.append(pool.take(range(start, start + per_step)))
+        batches.append(Samples.concat(sel))
+    return heads, batches, share
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.device), "-lms", "20"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        rows = [r for t, r in self.rows if t0 - 0.05 <= t <= t1 + 0.05] or [r for _, r in self.rows[-5:]]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ roofline
+def kernel_work(name, E, N, G, H, W, L, S):
+    """Algorithmic (flops, bytes) of ONE launch of a profiled kernel scope."""
+    f4 = 4
+    table = {
+        # forward, per encoder layer
+        "fwd.node_P": (2 * N * H * 2 * H, f4 * (N * H + N * 2 * H + 2 * H * H)),
+        "fwd.edge_msg_gemm": (2 * E * H * H, f4 * (2 * N * H + E * H + H * H) + 24 * E),
+        "fwd.agg_segsum": (E * H, f4 * (E * H + N * H) + 4 * (N + 1)),
+        "fwd.node_mlp1": (2 * N * 2 * H * H, f4 * (3 * N * H + 2 * H * H)),
+        "fwd.node_mlp2": (2 * N * H * H, f4 * (3 * N * H + H * H)),
+        "fwd.force_edge_gemm": (2 * E * W * W, f4 * (N * W + E * W) + 12 * E),
+        "fwd.forces_segsum": (6 * E, 20 * E + 12 * N),
+        # backward, per encoder layer
+        "bwd.edge_dz2_gather": (E * H, f4 * (2 * E * H + N * H) + 4 * E),
+        "bwd.edge_w2grad": (2 * E * (H + 1) * H, f4 * (2 * N * H + E * H + H * H) + 24 * E),
+        "bwd.edge_dz1_gemm": (2 * E * H * H, f4 * (2 * N * H + 2 * E * H + H * H) + 24 * E),
+        "bwd.segsum_dst_src": (2 * E * H, f4 * (2 * E * H + 2 * N * H) + 4 * E),
+        "bwd.edge_w1ab_grad": (2 * N * H * 2 * H, f4 * (3 * N * H + 2 * H * H)),
+        "bwd.edge_dh_gemm": (2 * N * 2 * H * H, f4 * (4 * N * H + 2 * H * H)),
+    }
+    return table.get(name)
+
+
+GATHER_SCATTER = ("fwd.agg_segsum", "bwd.segsum_dst_src", "bwd.edge_dz2_gather", "fwd.forces_segsum")
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1400.0, "fallback"
+
+
+def profile(model, cfg, slots, E, N, G, steps=3):
+    """Eager steps with per-kernel CUDA events (outside the timed region)."""
+    import ctypes as C
+
+    from paper_2506_21788_b200._lib import check, lib
+
+    check(lib().hmtl_profile_enable(model.ctx, 1))
+    eager = type(cfg)(**{**cfg.__dict__, "use_graph": False})
+    for i in range(steps):
+        check(lib().hmtl_pool_bind(model.ctx, slots[i % len(slots)], None))
+        check(lib().hmtl_train_step(model.ctx, C.byref(eager.c()), None))
+    buf = C.create_string_buffer(1 << 16)
+    check(lib().hmtl_profile_report(model.ctx, buf, len(buf)))
+    check(lib().hmtl_profile_enable(model.ctx, 0))
+    rep = json.loads(buf.value.decode())
+    for r in rep:
+        r["calls"] /= steps
+        r["ms"] /= steps
+    return rep
+
+
+def roofline(rep, E, N, G, step_ms):
+    H, W, L = HYPER["hidden"], HYPER["head_width"], HYPER["layers"]
+    hbm, bf16, src = load_peaks()
+    total = sum(r["ms"] for r in rep)
+    dom = max(rep, key=lambda r: r["ms"])
+    out = {"kernel": dom["name"], "share_of_step": round(dom["ms"] / total, 4), "peak_source": src}
+    w = kernel_work(dom["name"], E, N, G, H, W, L, HEADS)
+    per_launch_ms = dom["ms"] / max(dom["calls"], 1)
+    if w:
+        flops, byts = w
+        tf = flops / (per_launch_ms * 1e-3) / 1e12
+        gbs = byts / (per_launch_ms * 1e-3) / 1e9
+        if tf / bf16 >= gbs / hbm:
+            out.update(bound="tensor", achieved=round(tf, 3), peak=bf16, unit="TFLOP/s", frac=round(tf / bf16, 5))
+        else:
+            out.update(bound="hbm", achieved=round(gbs, 1), peak=hbm, unit="GB/s", frac=round(gbs / hbm, 4))
+        out["fp32_simt_peak_tflops"] = round(148 * 128 * 2 * 1.965e9 / 1e12, 1)
+        out["algorithmic_per_launch"] = {"flops": flops, "bytes": byts, "ms": round(per_launch_ms, 5)}
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(dom["name"])
+    out["traffic"] = traffic
+    # gather/scatter message-passing kernels against the HBM roofline (north star >= 50%)
+    gs_ms, gs_bytes = 0.0, 0.0
+    for r in rep:
+        if r["name"] in GATHER_SCATTER:
+            w = kernel_work(r["name"], E, N, G, H, W, L, HEADS)
+            gs_ms += r["ms"]
+            gs_bytes += w[1] * r["calls"]
+    gs = None
+    if gs_ms > 0:
+        a = gs_bytes / (gs_ms * 1e-3) / 1e9
+        gs = {"bound": "hbm", "achieved": round(a, 1), "peak": hbm, "unit": "GB/s", "frac": round(a / hbm, 4),
+              "kernels": list(GATHER_SCATTER), "share_of_step": round(gs_ms / total, 4)}
+    return out, gs
+
+
+# ------------------------------------------------------------------ arms
+def cpu_sample_rate(batch, seconds=12.0, threads=None):
+    """Reference CPU path (oracle/_ref: build_batch + ModelT<float> fwd/bwd + SPEC
+    loss/AdamW), thread-parallel over structures, on a bounded sample."""
+    import oracle as O
+
+    ref = O.Ref()
+    threads = threads or os.cpu_count() or 1
+    h = O.Hyper(**HYPER)
+    m = O.RefModel(ref, h, 7, list(range(HEADS)), dbl=False)
+    tr = O.RefTrainer(ref, m)
+    smp = {"n_atoms": batch.n_atoms, "species": batch.species, "pos": batch.positions, "forces": batch.forces,
+           "energy": batch.energy, "dsid": batch.dataset_id}
+    t0 = time.perf_counter()
+    tr.step(smp, threads)
+    t1 = time.perf_counter()
+    n_steps, structs = 1, batch.G
+    # keep going until the sample reaches `seconds` of host time
+    while time.perf_counter() - t0 < seconds:
+        tr.step(smp, threads)
+        n_steps += 1
+        structs += batch.G
+    dt = time.perf_counter() - t0
+    return structs / dt, threads, n_steps, t1 - t0
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    _, batches, _ = rank_batches(0, 1)
+    import oracle as O
+
+    ref = O.Ref()
+    threads = os.cpu_count() or 1
+    h = O.Hyper(**HYPER)
+    m = O.RefModel(ref, h, 7, list(range(HEADS)), dbl=False)
+    tr = O.RefTrainer(ref, m)
+    sm = lambda b: {"n_atoms": b.n_atoms, "species": b.species, "pos": b.positions, "forces": b.forces,
+                    "energy": b.energy, "dsid": b.dataset_id}
+    full = batches[0]
+    # bound the per-step sample so the whole run stays within a few minutes
+    t0 = time.perf_counter()
+    tr.step(sm(full), threads)
+    one = time.perf_counter() - t0
+    budget = 120.0 / max(args.steps + args.warmup, 1)
+    frac = min(1.0, budget / one)
+    samples = []
+    for b in batches:
+        n = max(HEADS, int(b.G * frac))
+        idx = np.linspace(0, b.G - 1, n).astype(int)  # proportional over the head-ordered batch
+        samples.append(b.take(sorted(set(idx.tolist()))))
+    for i in range(args.warmup):
+        tr.step(sm(samples[i % len(samples)]), threads)
+    t0 = time.perf_counter()
+    structs = 0
+    for i in range(args.steps):
+        s = samples[i % len(samples)]
+        tr.step(sm(s), threads)
+        structs += s.G
+    dt = time.perf_counter() - t0
+    v = structs / dt
+    line = {"impl": "reference", "metric": "train structures/sec (5-head MTL)", "value": round(v, 3),
+            "unit": "structures/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference default5 generator)",
+            "config": {"workload": WORKLOAD, **HYPER, "structures_per_gpu_step": full.G,
+                       "sampled_structures_per_step": int(np.mean([s.G for s in samples]))},
+            "cpu_baseline": {"value": round(v, 3), "unit": "structures/s", "cores": threads, "kind": "reference",
+                             "sample": f"{args.steps} steps x ~{int(np.mean([s.G for s in samples]))} structures "
+                                       f"({frac:.2f} of the per-GPU batch), reference ModelT<float> + SPEC AdamW, "
+                                       f"{threads} threads"},
+            "e2e": {"value": round(v, 3), "unit": "structures/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, rank, world, local_rank, dist):
+    import ctypes as C
+
+    import torch
+
+    import paper_2506_21788_b200 as P
+    from paper_2506_21788_b200._lib import check, lib
+
+    heads, batches, share = rank_batches(rank, world)
+    caps = P.Caps.for_samples(batches[0])
+    for b in batches[1:]:
+        caps = caps.union(P.Caps.for_samples(b))
+    hp = P.ModelHyper(**HYPER)
+    torch.cuda.set_device(local_rank)
+    model = P.ModelT(hp, 7, heads, caps=caps, device=local_rank)
+    slots = []
+    for b in batches:
+        sl = C.c_int()
+        check(lib().hmtl_pool_add(model.ctx, C.byref(b.as_c()), C.byref(sl)))
+        slots.append(sl.value)
+    if world > 1:
+        idb = (C.c_uint8 * 128)()
+        if rank == 0:
+            check(lib().hmtl_comm_unique_id(idb))
+        t = torch.tensor(list(bytes(idb)), dtype=torch.uint8)
+        dist.broadcast(t, 0)
+        idb = (C.c_uint8 * 128)(*t.tolist())
+        check(lib().hmtl_comm_init(model.ctx, idb, world, rank))
+    cfg = P.TrainConfig(use_graph=True)
+    stream_ptr = lib().hmtl_ctx_stream(model.ctx)
+    ext = torch.cuda.ExternalStream(stream_ptr, device=local_rank)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")  # > 126 MB L2
+
+    def step(i):
+        check(lib().hmtl_pool_bind(model.ctx, slots[i % len(slots)], None))
+        check(lib().hmtl_train_step(model.ctx, C.byref(cfg.c()), None))
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    L = C.c_float()
+    check(lib().hmtl_read_loss(model.ctx, C.byref(L)))  # surfaces any device-side error flag
+    E = C.c_int()
+    check(lib().hmtl_batch_edges(model.ctx, C.byref(E), None, None, None))
+
+    # ---- timed region: device-resident inputs, L2 flushed between steps
+    clk = ClockSampler(local_rank)
+    clk.start()
+    time.sleep(0.1)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.time()
+    with torch.cuda.stream(ext):
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(ext)
+            step(args.warmup + i)
+            evs[i][1].record(ext)
+    torch.cuda.synchronize()
+    t_wall1 = time.time()
+    if dist:
+        dist.barrier()
+    time.sleep(0.05)
+    clk.stop()
+    dev_ms = sum(a.elapsed_time(b) for a, b in evs)
+    check(lib().hmtl_read_loss(model.ctx, C.byref(L)))
+    final_loss = float(L.value)
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    dev_ms = max_over_ranks(dev_ms)
+    counts = batch_counts()
+    structs_per_step = world * sum(counts)  # sum over ranks of their batches
+    value = structs_per_step * args.steps / (dev_ms / 1e3)
+
+    # ---- e2e through the public API: host samples -> pinned arena -> H2D -> step -> D2H loss
+    e2e_s = 0.0
+    h2d = 0
+    for i in range(args.steps):
+        b = batches[i % len(batches)]
+        with torch.cuda.stream(ext):
+            flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        model.train_step(b, cfg, read_loss=True)
+        e2e_s += time.perf_counter() - t0
+        h2d += arena_bytes(b.G, b.N)
+    e2e_s = max_over_ranks(e2e_s)
+    e2e = structs_per_step * args.steps / e2e_s
+
+    # ---- per-kernel profile (eager, instrumented; outside the timed region)
+    rep = profile(model, cfg, slots, E.value, batches[0].N, batches[0].G)
+    launches_per_step = sum(r["calls"] * (2 if ("grad" in r["name"]) else 1) for r in rep) + 1  # + adam_tick
+    roof, roof_gs = roofline(rep, E.value, batches[0].N, batches[0].G, dev_ms / args.steps)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, cores, n, first = cpu_sample_rate(batches[0], seconds=args.cpu_seconds)
+            cpu = {"value": round(v, 3), "unit": "structures/s", "cores": cores, "kind": "reference",
+                   "sample": f"{n} reference CPU steps on the 1-GPU batch ({batches[0].G} structures, "
+                             f"{E.value} edges), ModelT<float> + SPEC AdamW, {cores} threads, "
+                             f"~{args.cpu_seconds:.0f} s"}
+        except Exception as e:  # the reference .so may be absent on a box without the checkers
+            cpu = {"value": None, "unit": "structures/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    clocks = clk.summary(t_wall0, t_wall1)
+    nb = {}
+    if world > 1:
+        ub = (C.c_uint64 * 2)()
+        lib().hmtl_comm_bytes(model.ctx, ub)
+        nb = {"encoder_sync_bytes_per_step": model.shared_size() * 4,
+              "head_sync_bytes_per_step": int(sum(model.head_size() * 4 for k in heads if (share[:, k] > 0).sum() > 1))}
+    if rank == 0:
+        par = "mtl-par" if world > 1 else "mtl-base(1 rank, 5 heads)"
+        line = {
+            "metric": "train structures/sec (5-head MTL)", "value": round(value, 2), "unit": "structures/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dev_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference default5 generator, seeds 1234+k)",
+            "config": {"workload": WORKLOAD, **HYPER, "per_gpu_batch": {"structures": batches[0].G,
+                                                                        "edges": E.value, "nodes": batches[0].N},
+                       "batch_counts_1gpu": counts, "head_weights": list(WEIGHTS), "parallelism": par,
+                       "l2": "flushed (256 MB write) between timed steps", "cuda_graph": True,
+                       "final_loss": final_loss},
+            "e2e": {"value": round(e2e, 2), "unit": "structures/s",
+                    "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": 240},
+            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "roofline": roof, "roofline_gather_scatter": roof_gs, "clocks": clocks,
+            "cpu_baseline": cpu, **({"comm": nb} if nb else {}),
+            "kernel_ms_per_step": {r["name"]: round(r["ms"], 4) for r in sorted(rep, key=lambda r: -r["ms"])},
+        }
+        print(json.dumps(line), flush=True)
+    model.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world)
+        else:
+            run_b200(args, rank, world, local_rank, dist)
+    finally:
+        if dist:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

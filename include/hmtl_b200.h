@@ -1,0 +1,197 @@
+/*
+ * hmtl_b200.h -- C ABI of the B200-native multi-task-parallel GNN training step.
+ *
+ * Drop-in boundary for the reference's hot path (/root/reference/proj, namespace
+ * hmtl).  The reference is a header-only C++ template API with no FFI; this
+ * C ABI is what its C++ types bind to (see include/hmtl_b200.hpp for the
+ * C++ drop-in mirror and INTEGRATION.md for the binding).  Each entry point
+ * names the reference interface it replaces.
+ *
+ * Conventions
+ *   - Return value: 0 = ok, 1..6 = hmtl::ErrorCode (hmtl/error.hpp:8-15:
+ *     contract=1, io=2, comm=3, data=4, config=5, internal=6).  The message of
+ *     the last failure on the calling thread is hmtl_last_error().
+ *   - Plain pointers and sizes only.  `stream` is a cudaStream_t passed as
+ *     void* (NULL = the context's own stream).  Every device call is
+ *     stream-ordered; functions that return data to the host synchronise.
+ *   - Parameter blocks use the reference's flat BlockLayout offsets
+ *     (hmtl/model.hpp:40-90), so host<->device copies are 1:1 with
+ *     ModelT::shared_block()/head_block(k).
+ *   - Contexts are not thread-safe: one host thread per GPU.
+ *   - There is no CPU fallback: without a CUDA device every device entry
+ *     point fails with HMTL_ERR_INTERNAL.
+ */
+#ifndef HMTL_B200_H
+#define HMTL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HMTL_ABI_VERSION 1
+
+enum {
+  HMTL_OK = 0,
+  HMTL_ERR_CONTRACT = 1,
+  HMTL_ERR_IO = 2,
+  HMTL_ERR_COMM = 3,
+  HMTL_ERR_DATA = 4,
+  HMTL_ERR_CONFIG = 5,
+  HMTL_ERR_INTERNAL = 6
+};
+
+/* ModelHyper, hmtl/model.hpp:17-37 (field for field). */
+typedef struct hmtl_hyper {
+  int n_species, layers, hidden, head_width, head_depth, n_heads;
+  double cutoff;
+} hmtl_hyper;
+
+/* data::DatasetSpec, hmtl/dataset.hpp:20-32. */
+typedef struct hmtl_dataset_spec {
+  int dataset_id;
+  int n_elements;
+  uint8_t elements[32];
+  int n_min, n_max;
+  double alpha, sigma;
+  double mu[20];
+  uint64_t count;
+  int64_t structure_seed;
+} hmtl_dataset_spec;
+
+/* A batch of AtomisticSample (hmtl/graph.hpp:13-21) in host memory, the
+ * input of build_batch (hmtl/graph.hpp:46-48).  n_atoms[G]; species[N];
+ * positions[3N]; forces[3N]; energy_per_atom[G]; dataset_id[G]. */
+typedef struct hmtl_samples {
+  int G, N;
+  const int* n_atoms;
+  const uint8_t* species;
+  const double* positions;
+  const double* forces;
+  const double* energy_per_atom;
+  const uint8_t* dataset_id;
+} hmtl_samples;
+
+/* Capacity of one context's device buffers (capacity-padded so a whole step
+ * can be captured once in a CUDA graph and replayed for any batch that fits). */
+typedef struct hmtl_caps {
+  int max_graphs, max_nodes;
+  long long max_edges;
+} hmtl_caps;
+
+/* SPEC trainer knobs. */
+typedef struct hmtl_train_cfg {
+  float lr, beta1, beta2, eps, weight_decay, w_energy, w_force;
+  int use_graph; /* capture the step in a CUDA graph and replay it */
+} hmtl_train_cfg;
+
+typedef struct hmtl_ctx hmtl_ctx;
+
+/* ------------------------------------------------------------ host-only */
+int hmtl_abi_version(void);
+const char* hmtl_last_error(void);
+int hmtl_device_count(void);
+
+/* shared_layout / head_layout, hmtl/model.hpp:56-90: total sizes, entries. */
+size_t hmtl_shared_size(const hmtl_hyper* hp);
+size_t hmtl_head_size(const hmtl_hyper* hp);
+int hmtl_layout_entry(const hmtl_hyper* hp, int shared, int i, char* name, size_t name_cap,
+                      size_t* rows, size_t* cols, size_t* offset); /* returns #entries */
+/* ModelT ctor init (hmtl/model.hpp:158-167, 211-225): which=-1 shared, k head k. */
+int hmtl_init_block(const hmtl_hyper* hp, uint64_t seed, int which, float* out);
+/* classify_regime / memory_footprint, hmtl/model.hpp:246-263 (mode 0 serial 1 base 2 taskpar) */
+int hmtl_classify_regime(size_t p_s, size_t p_h, int n_h);
+size_t hmtl_memory_footprint(size_t p_s, size_t p_h, int n_h, int mode);
+
+/* Synthetic multi-source generator (host input source; data::default5_specs and
+ * data::generate_dataset, src/dataset.cpp:106-161, 213-239).  Two-call:
+ * with out arrays NULL it reports *G and *N; then fill. */
+int hmtl_default5_spec(int id, hmtl_dataset_spec* out);
+int hmtl_generate(const hmtl_dataset_spec* spec, uint64_t seed, int* G, int* N, int* n_atoms,
+                  uint8_t* species, double* positions, double* forces, double* energy,
+                  uint8_t* dataset_id);
+
+/* Head -> rank placement for MTL-par on `world` ranks (generalises
+ * Mesh{N x M}, hmtl/mesh.hpp:21-31, to uneven groups).  share[r*n_heads+k]
+ * receives the fraction of head k's per-step global batch served by rank r.
+ * weights[k] = relative per-head work (e.g. GPUs-per-head at world 8).
+ * Returns 0 or HMTL_ERR_CONFIG when the heads cannot be balanced. */
+int hmtl_head_placement(int world, int n_heads, const double* weights, double* share);
+
+/* ------------------------------------------------------------ device */
+/* ModelT<float>(hp, seed, owned_heads), hmtl/model.hpp:158: creates the device
+ * context on `device`, allocates capacity-padded buffers and initialises the
+ * parameters exactly as the reference does. */
+int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* owned_heads,
+                    int n_owned, const hmtl_caps* caps, hmtl_ctx** out);
+void hmtl_ctx_destroy(hmtl_ctx* ctx);
+void* hmtl_ctx_stream(hmtl_ctx* ctx);
+
+/* shared_block()/head_block(k) (hmtl/model.hpp:182-187): host <-> device. */
+int hmtl_set_block(hmtl_ctx* ctx, int which, const float* host);
+int hmtl_get_block(hmtl_ctx* ctx, int which, float* host);
+/* GradientBufferT (hmtl/model.hpp:98-115) of the last backward. */
+int hmtl_get_grad(hmtl_ctx* ctx, int which, float* host);
+
+/* Batch upload: the samples are packed into one pinned staging arena and
+ * copied with one cudaMemcpyAsync (build_batch input, hmtl/graph.hpp:46). */
+int hmtl_batch_upload(hmtl_ctx* ctx, const hmtl_samples* s, void* stream);
+/* Device-resident batch pool: pack samples once into device memory ... */
+int hmtl_pool_add(hmtl_ctx* ctx, const hmtl_samples* s, int* slot);
+/* ... and bind pool slot `slot` as the current batch (device-to-device). */
+int hmtl_pool_bind(hmtl_ctx* ctx, int slot, void* stream);
+
+/* build_batch<float> on the device (hmtl/graph.hpp:46-83): bit-exact FP64
+ * cutoff test, dst-major CSR, reverse-edge permutation, per-graph edge offsets. */
+int hmtl_build_batch(hmtl_ctx* ctx, void* stream);
+/* GraphBatchT edge view (syncs): *E, and optionally edge_dst/edge_src[E], edge_offset[G+1]. */
+int hmtl_batch_edges(hmtl_ctx* ctx, int* E, int* edge_dst, int* edge_src, int* edge_offset);
+
+/* ModelT::forward, hmtl/model.hpp:338-488 (cache kept on the device). */
+int hmtl_forward(hmtl_ctx* ctx, void* stream);
+/* PredictionT (hmtl/model.hpp:92-96), syncs: energy_per_atom[G], forces[3N]. */
+int hmtl_predictions(hmtl_ctx* ctx, float* energy, float* forces);
+/* SPEC loss: loss on device + upstreams dE[G], dF[3N]. */
+int hmtl_loss(hmtl_ctx* ctx, float w_energy, float w_force, void* stream);
+int hmtl_read_loss(hmtl_ctx* ctx, float* loss); /* syncs */
+/* ModelT::backward, hmtl/model.hpp:490-625.  d_energy/d_forces are HOST
+ * upstreams [G], [3N]; pass NULL for both to use the device upstreams of
+ * hmtl_loss. */
+int hmtl_backward(hmtl_ctx* ctx, const float* d_energy, const float* d_forces, void* stream);
+/* SPEC AdamW over every owned block; step counter internal. */
+int hmtl_adamw(hmtl_ctx* ctx, const hmtl_train_cfg* cfg, void* stream);
+/* train_step: build_batch -> forward -> loss -> backward
+ * -> head-group + global gradient allreduce_mean (when a communicator is
+ * attached) -> AdamW.  Stream-ordered; read the loss with hmtl_read_loss. */
+int hmtl_train_step(hmtl_ctx* ctx, const hmtl_train_cfg* cfg, void* stream);
+
+/* Per-layer parity probe: copies a named device cache tensor to the host
+ * (syncs). names: "h" (layer 0..L: input of layer l, L = final), "P", "z1",
+ * "z2", "agg", "vz1", "pooled", "ez" (layer = MLP layer), "Qf", "zf" (layer =
+ * MLP layer >= 1), "s", "dE", "dF".  Returns #floats written in *n. */
+int hmtl_debug_fetch(hmtl_ctx* ctx, const char* name, int layer, float* host, size_t cap, size_t* n);
+
+/* Benchmark instrumentation: when enabled, every kernel launch site records
+ * CUDA events on its stream (eager steps only; do not combine with graphs).
+ * report (syncs) writes a JSON array [{"name","calls","ms"}] and resets. */
+int hmtl_profile_enable(hmtl_ctx* ctx, int on);
+int hmtl_profile_report(hmtl_ctx* ctx, char* json, size_t cap);
+
+/* ------------------------------------------------------------ comm (NCCL) */
+/* collective::allreduce_mean over RankGroup (hmtl/mesh.hpp:276-278, 312-342),
+ * re-implemented as NCCL communicators: one world communicator and one per
+ * head split by ncclCommSplit(color = head).  share[] as from
+ * hmtl_head_placement decides which heads this rank owns. */
+int hmtl_comm_unique_id(uint8_t out[128]);
+int hmtl_comm_init(hmtl_ctx* ctx, const uint8_t id[128], int world, int rank);
+/* Allreduce the last gradients (head groups, then global) on `stream`. */
+int hmtl_comm_sync_grads(hmtl_ctx* ctx, void* stream);
+/* Per-category byte counters (CommStats, hmtl/mesh.hpp:102-131): [encoder_sync, head_sync]. */
+int hmtl_comm_bytes(hmtl_ctx* ctx, uint64_t out[2]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

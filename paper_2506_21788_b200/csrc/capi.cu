@@ -1,0 +1,526 @@
+// capi.cu -- the C ABI (include/hmtl_b200.h): device context, batch upload,
+// and the stream-ordered training step.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ctx.cuh"
+
+using namespace hmtl_b200;
+
+namespace {
+
+template <class T>
+int dalloc(T** p, size_t n) {
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+  if (e != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+cudaStream_t pick(Ctx& c, void* s) { return s ? static_cast<cudaStream_t>(s) : c.stream; }
+
+int check_hdr(Ctx& c) {
+  DevHdr h;
+  HMTL_CUDA(cudaMemcpy(&h, c.hdr, sizeof(DevHdr), cudaMemcpyDeviceToHost));
+  if (h.err & kErrUnowned) return fail(HMTL_ERR_CONTRACT, "model: unknown dataset id (head not owned by this rank)");
+  if (h.err & kErrEmptyGraph) return fail(HMTL_ERR_CONTRACT, "build_batch: empty graph rejected");
+  if (h.err & kErrEdgeOverflow) return fail(HMTL_ERR_CONTRACT, "build_batch: edge capacity exceeded");
+  if (h.err & kErrNonFinite) return fail(HMTL_ERR_CONTRACT, "model: non-finite prediction");
+  return 0;
+}
+
+// pack AtomisticSamples into the batch arena format (common.cuh: arena_layout)
+int pack(Ctx& c, const hmtl_samples* s, uint8_t* dst, size_t cap, size_t* bytes) {
+  if (!s || s->G <= 0 || s->N <= 0) return fail(HMTL_ERR_CONTRACT, "model: empty batch rejected");
+  if (s->G > c.Gc || s->N > c.Nc) return fail(HMTL_ERR_CONTRACT, "batch exceeds context capacity (graphs/nodes)");
+  const ArenaLayout al = arena_layout(s->G, s->N);
+  if (al.total > cap) return fail(HMTL_ERR_INTERNAL, "arena too small");
+  long long bound = 0, n_sum = 0;
+  for (int g = 0; g < s->G; ++g) {
+    const long long n = s->n_atoms[g];
+    if (n < 1) return fail(HMTL_ERR_CONTRACT, "build_batch: empty graph rejected");
+    bound += n * (n - 1);
+    n_sum += n;
+    if (s->dataset_id[g] >= 255 || c.slot_of[s->dataset_id[g]] < 0)
+      return fail(HMTL_ERR_CONTRACT, "model: unknown dataset id " + std::to_string(s->dataset_id[g]) +
+                                         " (head not owned by this rank)");
+  }
+  if (n_sum != s->N) return fail(HMTL_ERR_CONTRACT, "samples: sum(n_atoms) != N");
+  if (bound > c.Ec) return fail(HMTL_ERR_CONTRACT, "batch may exceed the context's edge capacity");
+  int* hdr = reinterpret_cast<int*>(dst);
+  hdr[0] = s->G;
+  hdr[1] = s->N;
+  hdr[2] = hdr[3] = 0;
+  int* go = reinterpret_cast<int*>(dst + al.go);
+  go[0] = 0;
+  for (int g = 0; g < s->G; ++g) go[g + 1] = go[g] + s->n_atoms[g];
+  std::memcpy(dst + al.ds, s->dataset_id, s->G);
+  std::memcpy(dst + al.sp, s->species, s->N);
+  std::memcpy(dst + al.pos, s->positions, 24 * size_t(s->N));
+  if (s->energy_per_atom) std::memcpy(dst + al.le, s->energy_per_atom, 8 * size_t(s->G));
+  else std::memset(dst + al.le, 0, 8 * size_t(s->G));
+  if (s->forces) std::memcpy(dst + al.lf, s->forces, 24 * size_t(s->N));
+  else std::memset(dst + al.lf, 0, 24 * size_t(s->N));
+  *bytes = al.total;
+  c.host_G = s->G;
+  c.host_N = s->N;
+  return 0;
+}
+
+void free_ctx(Ctx& c) {
+  void* ptrs[] = {c.params, c.grads, c.adam_m, c.adam_v, c.hdr, c.d_slot_of, c.arena, c.graph_offset, c.node_graph,
+                  c.deg, c.row_ptr, c.edge_src, c.edge_dst, c.rev, c.edge_offset, c.pos32, c.geo, c.dist,
+                  c.species, c.gslot, c.gperm, c.gnode_base, c.gedge_base, c.node_perm, c.edge_perm, c.hs, c.P,
+                  c.z2, c.agg, c.vz1, c.pooled, c.ez, c.energy, c.Qf, c.zf, c.s, c.forces, c.dE, c.dF, c.dh,
+                  c.dh2, c.dagg, c.dvz1, c.dzA, c.dzB, c.Sbuf, c.ds, c.dpooled, c.edA, c.edB, c.scratch,
+                  c.partial};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto* p : c.pool) cudaFree(p);
+  if (c.h_arena) cudaFreeHost(c.h_arena);
+  if (c.step_exec) cudaGraphExecDestroy(c.step_exec);
+  comm_destroy(c.comm);
+  c.comm = nullptr;
+  if (c.stream) cudaStreamDestroy(c.stream);
+}
+
+int enqueue_step(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st) {
+  launch_prep(c, st);
+  launch_nbr(c, st);
+  launch_forward(c, st);
+  launch_loss(c, cfg.w_energy, cfg.w_force, st);
+  launch_backward(c, st);
+  if (c.comm) {
+    int rc = comm_sync_grads(c, st);
+    if (rc) return rc;
+  }
+  launch_adamw(c, cfg, st);
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hmtl_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* owned, int n_owned,
+                    const hmtl_caps* caps, hmtl_ctx** out) {
+  if (!hp || !caps || !out) return fail(HMTL_ERR_CONTRACT, "ctx_create: null argument");
+  if (hp->hidden < 1 || hp->head_width < 1 || hp->layers < 1 || hp->n_species < 1 || hp->n_heads < 1 ||
+      hp->n_heads > 255)
+    return fail(HMTL_ERR_CONFIG, "ctx_create: invalid hyperparameters");
+  if (hp->head_depth < 2) return fail(HMTL_ERR_CONFIG, "ctx_create: head_depth >= 2 required on the GPU path");
+  if (n_owned < 1 || n_owned > kMaxSlots) return fail(HMTL_ERR_CONFIG, "ctx_create: 1..16 owned heads per rank");
+  if (caps->max_graphs < 1 || caps->max_nodes < 1 || caps->max_edges < 1)
+    return fail(HMTL_ERR_CONFIG, "ctx_create: capacities must be positive");
+  int ndev = hmtl_device_count();
+  if (device < 0 || device >= ndev)
+    return fail(HMTL_ERR_INTERNAL, "ctx_create: no CUDA device " + std::to_string(device) +
+                                       " (the B200 path has no CPU fallback)");
+  HMTL_CUDA(cudaSetDevice(device));
+  auto* h = new hmtl_ctx;
+  Ctx& c = h->c;
+  c.device = device;
+  c.hp = *hp;
+  c.H = hp->hidden;
+  c.W = hp->head_width;
+  c.L = hp->layers;
+  c.D = hp->head_depth;
+  c.NS = hp->n_species;
+  c.rc2 = hp->cutoff * hp->cutoff;
+  std::fill(c.slot_of, c.slot_of + 256, -1);
+  c.owned.assign(owned, owned + n_owned);
+  std::sort(c.owned.begin(), c.owned.end());
+  for (size_t s = 0; s < c.owned.size(); ++s) {
+    const int k = c.owned[s];
+    if (k < 0 || k >= hp->n_heads || (s && c.owned[s - 1] == k)) {
+      delete h;
+      return fail(HMTL_ERR_CONTRACT, "model: head index out of range");
+    }
+    c.slot_of[k] = int(s);
+  }
+  c.S = int(c.owned.size());
+  c.shared_lay = make_layout(*hp, true);
+  c.head_lay = make_layout(*hp, false);
+  c.PS = c.shared_lay.total;
+  c.PH = c.head_lay.total;
+  c.PT = c.PS + size_t(c.S) * c.PH;
+  c.Gc = caps->max_graphs;
+  c.Nc = caps->max_nodes;
+  c.Ec = caps->max_edges;
+  cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, device);
+  int rc = 0;
+  auto A = [&](auto** p, size_t n) {
+    if (!rc) rc = dalloc(p, n);
+  };
+  const size_t H = c.H, W = c.W, L = c.L, D = c.D;
+  const size_t N = c.Nc, E = c.Ec, G = c.Gc;
+  if (cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking) != cudaSuccess) rc = HMTL_ERR_INTERNAL;
+  A(&c.params, c.PT);
+  A(&c.grads, c.PT);
+  A(&c.adam_m, c.PT);
+  A(&c.adam_v, c.PT);
+  A(&c.hdr, 1);
+  A(&c.d_slot_of, 256);
+  c.arena_cap = arena_layout(c.Gc, c.Nc).total;
+  A(&c.arena, c.arena_cap);
+  A(&c.graph_offset, G + 1);
+  A(&c.node_graph, N);
+  A(&c.deg, N);
+  A(&c.row_ptr, N + 1);
+  A(&c.edge_src, E);
+  A(&c.edge_dst, E);
+  A(&c.rev, E);
+  A(&c.edge_offset, G + 1);
+  A(&c.pos32, N);
+  A(&c.geo, E);
+  A(&c.dist, E);
+  A(&c.species, N);
+  A(&c.gslot, G);
+  A(&c.gperm, G);
+  A(&c.gnode_base, G);
+  A(&c.gedge_base, G);
+  A(&c.node_perm, N);
+  A(&c.edge_perm, E);
+  A(&c.hs, (L + 1) * N * H);
+  A(&c.P, L * N * 2 * H);
+  A(&c.z2, L * E * H);
+  A(&c.agg, L * N * H);
+  A(&c.vz1, L * N * H);
+  A(&c.pooled, G * H);
+  A(&c.ez, D * G * W);
+  A(&c.energy, G);
+  A(&c.Qf, N * W);
+  A(&c.zf, std::max<size_t>(D - 2, 1) * E * W);
+  A(&c.s, E);
+  A(&c.forces, 3 * N);
+  A(&c.dE, G);
+  A(&c.dF, 3 * N);
+  A(&c.dh, N * H);
+  A(&c.dh2, N * H);
+  A(&c.dagg, N * H);
+  A(&c.dvz1, N * H);
+  A(&c.dzA, E * std::max(H, W));
+  A(&c.dzB, E * std::max(H, W));
+  A(&c.Sbuf, N * 2 * std::max(H, W));
+  A(&c.ds, E);
+  A(&c.dpooled, G * H);
+  A(&c.edA, G * W);
+  A(&c.edB, G * W);
+  A(&c.scratch, E * std::max(H, W));
+  auto clampi = [](long long v, long long lo, long long hi) { return int(std::min(std::max(v, lo), hi)); };
+  c.nsplit_node = clampi((c.Nc + 63) / 64, 1, 64);
+  c.nsplit_edge = clampi((c.Ec + 127) / 128, 1, 64);
+  c.nsplit_graph = clampi((c.Gc + 15) / 16, 1, 16);
+  const size_t kn_shared = (2 * H + 1) * H;
+  const size_t kn_head = std::max({(H + 1) * W, (W + 1) * W, H * W, 2 * W});
+  c.partial_cap = std::max(size_t(64) * kn_shared, size_t(c.S) * 64 * kn_head);
+  A(&c.partial, c.partial_cap);
+  if (rc) {
+    free_ctx(c);
+    delete h;
+    return rc;
+  }
+  // parameters exactly as ModelT's ctor (hmtl/model.hpp:162-166)
+  std::vector<float> host(c.PT);
+  init_block(*hp, seed, -1, host.data());
+  for (int s = 0; s < c.S; ++s) init_block(*hp, seed, c.owned[s], host.data() + c.PS + size_t(s) * c.PH);
+  cudaMemcpy(c.params, host.data(), c.PT * sizeof(float), cudaMemcpyHostToDevice);
+  cudaMemset(c.adam_m, 0, c.PT * sizeof(float));
+  cudaMemset(c.adam_v, 0, c.PT * sizeof(float));
+  cudaMemset(c.grads, 0, c.PT * sizeof(float));
+  cudaMemset(c.hdr, 0, sizeof(DevHdr));
+  cudaMemcpy(c.d_slot_of, c.slot_of, 256 * sizeof(int), cudaMemcpyHostToDevice);
+  c.h_arena_cap = c.arena_cap;
+  if (cudaMallocHost(&c.h_arena, c.h_arena_cap) != cudaSuccess) {
+    free_ctx(c);
+    delete h;
+    return fail(HMTL_ERR_INTERNAL, "cudaMallocHost failed");
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    free_ctx(c);
+    delete h;
+    return fail(HMTL_ERR_INTERNAL, std::string("ctx_create: ") + cudaGetErrorString(e));
+  }
+  *out = h;
+  return 0;
+}
+
+void hmtl_ctx_destroy(hmtl_ctx* h) {
+  if (!h) return;
+  cudaSetDevice(h->c.device);
+  cudaDeviceSynchronize();
+  free_ctx(h->c);
+  delete h;
+}
+
+void* hmtl_ctx_stream(hmtl_ctx* h) { return h ? h->c.stream : nullptr; }
+
+static int block_span(Ctx& c, int which, size_t* off, size_t* n) {
+  if (which < 0) {
+    *off = 0;
+    *n = c.PS;
+    return 0;
+  }
+  if (which >= 256 || c.slot_of[which] < 0) return fail(HMTL_ERR_CONTRACT, "head not owned by this rank");
+  *off = c.PS + size_t(c.slot_of[which]) * c.PH;
+  *n = c.PH;
+  return 0;
+}
+
+int hmtl_set_block(hmtl_ctx* h, int which, const float* host) {
+  size_t off, n;
+  if (int rc = block_span(h->c, which, &off, &n)) return rc;
+  cudaSetDevice(h->c.device);
+  HMTL_CUDA(cudaMemcpy(h->c.params + off, host, n * sizeof(float), cudaMemcpyHostToDevice));
+  return 0;
+}
+int hmtl_get_block(hmtl_ctx* h, int which, float* host) {
+  size_t off, n;
+  if (int rc = block_span(h->c, which, &off, &n)) return rc;
+  cudaSetDevice(h->c.device);
+  HMTL_CUDA(cudaStreamSynchronize(h->c.stream));
+  HMTL_CUDA(cudaMemcpy(host, h->c.params + off, n * sizeof(float), cudaMemcpyDeviceToHost));
+  return 0;
+}
+int hmtl_get_grad(hmtl_ctx* h, int which, float* host) {
+  size_t off, n;
+  if (int rc = block_span(h->c, which, &off, &n)) return rc;
+  cudaSetDevice(h->c.device);
+  HMTL_CUDA(cudaStreamSynchronize(h->c.stream));
+  HMTL_CUDA(cudaMemcpy(host, h->c.grads + off, n * sizeof(float), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int hmtl_batch_upload(hmtl_ctx* h, const hmtl_samples* s, void* stream) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  cudaStream_t st = pick(c, stream);
+  // the pinned staging buffer may still be read by a previous async copy
+  HMTL_CUDA(cudaStreamSynchronize(st));
+  size_t bytes = 0;
+  if (int rc = pack(c, s, c.h_arena, c.h_arena_cap, &bytes)) return rc;
+  HMTL_CUDA(cudaMemcpyAsync(c.arena, c.h_arena, bytes, cudaMemcpyHostToDevice, st));
+  return 0;
+}
+
+int hmtl_pool_add(hmtl_ctx* h, const hmtl_samples* s, int* slot) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  std::vector<uint8_t> tmp(c.arena_cap);
+  size_t bytes = 0;
+  if (int rc = pack(c, s, tmp.data(), tmp.size(), &bytes)) return rc;
+  uint8_t* d = nullptr;
+  HMTL_CUDA(cudaMalloc(&d, bytes));
+  HMTL_CUDA(cudaMemcpy(d, tmp.data(), bytes, cudaMemcpyHostToDevice));
+  c.pool.push_back(d);
+  c.pool_bytes.push_back(bytes);
+  if (slot) *slot = int(c.pool.size()) - 1;
+  return 0;
+}
+
+int hmtl_pool_bind(hmtl_ctx* h, int slot, void* stream) {
+  Ctx& c = h->c;
+  if (slot < 0 || slot >= int(c.pool.size())) return fail(HMTL_ERR_CONTRACT, "pool_bind: bad slot");
+  cudaSetDevice(c.device);
+  HMTL_CUDA(cudaMemcpyAsync(c.arena, c.pool[slot], c.pool_bytes[slot], cudaMemcpyDeviceToDevice, pick(c, stream)));
+  return 0;
+}
+
+int hmtl_build_batch(hmtl_ctx* h, void* stream) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  cudaStream_t st = pick(c, stream);
+  launch_prep(c, st);
+  launch_nbr(c, st);
+  HMTL_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int hmtl_batch_edges(hmtl_ctx* h, int* E, int* edge_dst, int* edge_src, int* edge_offset) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  HMTL_CUDA(cudaStreamSynchronize(c.stream));
+  HMTL_CUDA(cudaDeviceSynchronize());
+  if (int rc = check_hdr(c)) return rc;
+  DevHdr hd;
+  HMTL_CUDA(cudaMemcpy(&hd, c.hdr, sizeof hd, cudaMemcpyDeviceToHost));
+  if (E) *E = hd.E;
+  if (edge_dst) HMTL_CUDA(cudaMemcpy(edge_dst, c.edge_dst, size_t(hd.E) * 4, cudaMemcpyDeviceToHost));
+  if (edge_src) HMTL_CUDA(cudaMemcpy(edge_src, c.edge_src, size_t(hd.E) * 4, cudaMemcpyDeviceToHost));
+  if (edge_offset) HMTL_CUDA(cudaMemcpy(edge_offset, c.edge_offset, size_t(hd.G + 1) * 4, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int hmtl_forward(hmtl_ctx* h, void* stream) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  launch_forward(c, pick(c, stream));
+  HMTL_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int hmtl_predictions(hmtl_ctx* h, float* energy, float* forces) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  HMTL_CUDA(cudaDeviceSynchronize());
+  if (int rc = check_hdr(c)) return rc;
+  DevHdr hd;
+  HMTL_CUDA(cudaMemcpy(&hd, c.hdr, sizeof hd, cudaMemcpyDeviceToHost));
+  if (energy) HMTL_CUDA(cudaMemcpy(energy, c.energy, size_t(hd.G) * 4, cudaMemcpyDeviceToHost));
+  if (forces) HMTL_CUDA(cudaMemcpy(forces, c.forces, size_t(hd.N) * 12, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int hmtl_loss(hmtl_ctx* h, float w_e, float w_f, void* stream) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  launch_loss(c, w_e, w_f, pick(c, stream));
+  HMTL_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int hmtl_read_loss(hmtl_ctx* h, float* loss) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  HMTL_CUDA(cudaDeviceSynchronize());
+  if (int rc = check_hdr(c)) return rc;
+  DevHdr hd;
+  HMTL_CUDA(cudaMemcpy(&hd, c.hdr, sizeof hd, cudaMemcpyDeviceToHost));
+  *loss = float(hd.loss);
+  return 0;
+}
+
+int hmtl_backward(hmtl_ctx* h, const float* dE, const float* dF, void* stream) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  cudaStream_t st = pick(c, stream);
+  if ((dE == nullptr) != (dF == nullptr)) return fail(HMTL_ERR_CONTRACT, "model: upstream shape mismatch");
+  if (dE) {
+    HMTL_CUDA(cudaMemcpyAsync(c.dE, dE, size_t(c.host_G) * 4, cudaMemcpyHostToDevice, st));
+    HMTL_CUDA(cudaMemcpyAsync(c.dF, dF, size_t(c.host_N) * 12, cudaMemcpyHostToDevice, st));
+  }
+  launch_backward(c, st);
+  HMTL_CUDA(cudaGetLastError());
+  if (dE) HMTL_CUDA(cudaStreamSynchronize(st));  // host upstreams must outlive the copy
+  return 0;
+}
+
+int hmtl_adamw(hmtl_ctx* h, const hmtl_train_cfg* cfg, void* stream) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  launch_adamw(c, *cfg, pick(c, stream));
+  HMTL_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int hmtl_train_step(hmtl_ctx* h, const hmtl_train_cfg* cfg, void* stream) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  cudaStream_t st = pick(c, stream);
+  if (!cfg->use_graph) {
+    if (int rc = enqueue_step(c, *cfg, st)) return rc;
+    HMTL_CUDA(cudaGetLastError());
+    return 0;
+  }
+  if (c.step_exec && std::memcmp(&c.graph_cfg, cfg, sizeof *cfg) != 0) {
+    cudaGraphExecDestroy(c.step_exec);
+    c.step_exec = nullptr;
+  }
+  if (!c.step_exec) {
+    cudaGraph_t g;
+    HMTL_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_step(c, *cfg, st);
+    cudaError_t e = cudaStreamEndCapture(st, &g);
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("graph capture: ") + cudaGetErrorString(e));
+    HMTL_CUDA(cudaGraphInstantiate(&c.step_exec, g, 0));
+    cudaGraphDestroy(g);
+    c.graph_cfg = *cfg;
+  }
+  HMTL_CUDA(cudaGraphLaunch(c.step_exec, st));
+  return 0;
+}
+
+int hmtl_debug_fetch(hmtl_ctx* h, const char* name, int layer, float* host, size_t cap, size_t* n) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  HMTL_CUDA(cudaDeviceSynchronize());
+  DevHdr hd;
+  HMTL_CUDA(cudaMemcpy(&hd, c.hdr, sizeof hd, cudaMemcpyDeviceToHost));
+  const size_t H = c.H, W = c.W, N = hd.N, E = hd.E, G = hd.G;
+  const size_t NH = size_t(c.Nc) * H, EH = size_t(c.Ec) * H;
+  const std::string nm(name);
+  const float* src = nullptr;
+  size_t cnt = 0;
+  auto lay_ok = [&](int lo, int hi) { return layer >= lo && layer <= hi; };
+  if (nm == "h" && lay_ok(0, c.L)) src = c.hs + layer * NH, cnt = N * H;
+  else if (nm == "P" && lay_ok(0, c.L - 1)) src = c.P + layer * 2 * NH, cnt = N * 2 * H;
+  else if (nm == "z2" && lay_ok(0, c.L - 1)) src = c.z2 + layer * EH, cnt = E * H;
+  else if (nm == "agg" && lay_ok(0, c.L - 1)) src = c.agg + layer * NH, cnt = N * H;
+  else if (nm == "vz1" && lay_ok(0, c.L - 1)) src = c.vz1 + layer * NH, cnt = N * H;
+  else if (nm == "pooled") src = c.pooled, cnt = G * H;
+  else if (nm == "ez" && lay_ok(0, c.D - 1)) src = c.ez + layer * size_t(c.Gc) * W, cnt = G * W;
+  else if (nm == "Qf") src = c.Qf, cnt = N * W;
+  else if (nm == "zf" && lay_ok(1, c.D - 2)) src = c.zf + (layer - 1) * size_t(c.Ec) * W, cnt = E * W;
+  else if (nm == "s") src = c.s, cnt = E;
+  else if (nm == "dE") src = c.dE, cnt = G;
+  else if (nm == "dF") src = c.dF, cnt = 3 * N;
+  else if (nm == "z1" && lay_ok(0, c.L - 1)) {
+    launch_debug_z1(c, layer, c.scratch, c.stream);
+    HMTL_CUDA(cudaStreamSynchronize(c.stream));
+    src = c.scratch, cnt = E * H;
+  } else {
+    return fail(HMTL_ERR_CONTRACT, "debug_fetch: unknown tensor/layer " + nm);
+  }
+  if (n) *n = cnt;
+  if (!host) return 0;
+  if (cap < cnt) return fail(HMTL_ERR_CONTRACT, "debug_fetch: buffer too small");
+  HMTL_CUDA(cudaMemcpy(host, src, cnt * 4, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int hmtl_profile_enable(hmtl_ctx* h, int on) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  HMTL_CUDA(cudaDeviceSynchronize());
+  c.prof_on = on != 0;
+  for (auto& r : c.prof) r.used = 0;
+  return 0;
+}
+
+int hmtl_profile_report(hmtl_ctx* h, char* json, size_t cap) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  HMTL_CUDA(cudaDeviceSynchronize());
+  std::string out = "[";
+  for (auto& r : c.prof) {
+    double ms = 0.0;
+    for (size_t i = 0; i + 1 < r.used; i += 2) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, r.ev[i], r.ev[i + 1]);
+      ms += t;
+    }
+    if (out.size() > 1) out += ",";
+    out += "{\"name\":\"" + r.name + "\",\"calls\":" + std::to_string(r.used / 2) + ",\"ms\":" +
+           std::to_string(ms) + "}";
+    r.used = 0;
+  }
+  out += "]";
+  if (out.size() + 1 > cap) return fail(HMTL_ERR_CONTRACT, "profile_report: buffer too small");
+  std::memcpy(json, out.c_str(), out.size() + 1);
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,142 @@
+// ctx.cuh -- the per-GPU device context behind hmtl_ctx (one host thread per GPU).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace hmtl_b200 {
+
+struct Comm;  // comm.cu (NCCL)
+
+// Optional per-launch CUDA-event timing (hmtl_profile); off in timed steps.
+struct ProfRec {
+  std::string name;
+  std::vector<cudaEvent_t> ev;  // pairs (start, end)
+  size_t used = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  hmtl_hyper hp{};
+  int H = 0, W = 0, L = 0, D = 0, S = 0, NS = 0;
+  std::vector<int> owned;  // head id per slot (ascending)
+  int slot_of[256];
+  Layout shared_lay, head_lay;
+  size_t PS = 0, PH = 0, PT = 0;  // shared, head, total owned parameter counts
+  int Gc = 0, Nc = 0;
+  long long Ec = 0;
+  double rc2 = 0.0;  // cutoff^2 in FP64, as build_batch (hmtl/graph.hpp:53)
+
+  // parameters / optimiser state: [shared | slot0 head | slot1 head | ...]
+  float *params = nullptr, *grads = nullptr, *adam_m = nullptr, *adam_v = nullptr;
+  DevHdr* hdr = nullptr;
+  int* d_slot_of = nullptr;
+
+  // batch arena (device) + pinned staging + device pool
+  uint8_t* arena = nullptr;
+  size_t arena_cap = 0;
+  uint8_t* h_arena = nullptr;
+  size_t h_arena_cap = 0;
+  std::vector<uint8_t*> pool;
+  std::vector<size_t> pool_bytes;
+  int host_G = 0, host_N = 0;  // last bound batch (host view)
+
+  // derived batch structure
+  int *graph_offset = nullptr, *node_graph = nullptr, *deg = nullptr, *row_ptr = nullptr;
+  int *edge_src = nullptr, *edge_dst = nullptr, *rev = nullptr, *edge_offset = nullptr;
+  float4 *pos32 = nullptr, *geo = nullptr;  // geo = (dx, dy, dz, d2) per edge, FP32
+  float* dist = nullptr;
+  uint8_t* species = nullptr;
+  int *gslot = nullptr, *gperm = nullptr, *gnode_base = nullptr, *gedge_base = nullptr;
+  int *node_perm = nullptr, *edge_perm = nullptr;
+
+  // forward cache (device)
+  float *hs = nullptr, *P = nullptr, *z2 = nullptr, *agg = nullptr, *vz1 = nullptr;
+  float *pooled = nullptr, *ez = nullptr, *energy = nullptr, *Qf = nullptr, *zf = nullptr;
+  float *s = nullptr, *forces = nullptr;
+  // backward workspace
+  float *dE = nullptr, *dF = nullptr, *dh = nullptr, *dh2 = nullptr, *dagg = nullptr, *dvz1 = nullptr;
+  float *dzA = nullptr, *dzB = nullptr, *Sbuf = nullptr, *ds = nullptr, *dpooled = nullptr;
+  float *edA = nullptr, *edB = nullptr, *scratch = nullptr;
+  float* partial = nullptr;
+  size_t partial_cap = 0;
+  int nsplit_node = 1, nsplit_edge = 1, nsplit_graph = 1;
+
+  // CUDA graph of a whole training step
+  cudaGraphExec_t step_exec = nullptr;
+  hmtl_train_cfg graph_cfg{};
+
+  Comm* comm = nullptr;
+  int sm_count = 148;
+  bool prof_on = false;
+  std::vector<ProfRec> prof;
+
+  // helpers
+  float* shared_param(const char* name) const { return params + shared_lay.at(name).offset; }
+  float* shared_grad(const char* name) const { return grads + shared_lay.at(name).offset; }
+  size_t shared_off(const std::string& name) const { return shared_lay.at(name).offset; }
+  size_t head_off(const std::string& name) const { return head_lay.at(name).offset; }
+  float* head_params() const { return params + PS; }
+  float* head_grads() const { return grads + PS; }
+};
+
+// launchers (stream-ordered; sizes come from the device header)
+void launch_prep(Ctx& c, cudaStream_t st);      // arena -> node/graph tables, routing
+void launch_nbr(Ctx& c, cudaStream_t st);       // neighbour list, CSR, rev, edge offsets
+void launch_forward(Ctx& c, cudaStream_t st);   // ModelT::forward
+void launch_loss(Ctx& c, float w_e, float w_f, cudaStream_t st);
+void launch_backward(Ctx& c, cudaStream_t st);  // ModelT::backward (upstreams in c.dE/c.dF)
+void launch_adamw(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st);
+void launch_debug_z1(Ctx& c, int layer, float* out, cudaStream_t st);
+
+int comm_sync_grads(Ctx& c, cudaStream_t st);
+
+// RAII timing scope: records start/end events on `st` when profiling is on.
+struct Prof {
+  Ctx& c;
+  cudaStream_t st;
+  cudaEvent_t end = nullptr;
+  Prof(Ctx& c_, const char* name, cudaStream_t s) : c(c_), st(s) {
+    if (!c.prof_on) return;
+    ProfRec* r = nullptr;
+    for (auto& x : c.prof)
+      if (x.name == name) r = &x;
+    if (!r) {
+      c.prof.push_back(ProfRec{name, {}, 0});
+      r = &c.prof.back();
+    }
+    if (r->used + 2 > r->ev.size()) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      r->ev.push_back(a);
+      r->ev.push_back(b);
+    }
+    cudaEventRecord(r->ev[r->used], st);
+    end = r->ev[r->used + 1];
+    r->used += 2;
+  }
+  ~Prof() {
+    if (end) cudaEventRecord(end, st);
+  }
+};
+void comm_destroy(Comm* m);
+
+#define HMTL_CUDA(call)                                                                 \
+  do {                                                                                  \
+    cudaError_t e__ = (call);                                                           \
+    if (e__ != cudaSuccess)                                                             \
+      return ::hmtl_b200::fail(HMTL_ERR_INTERNAL, std::string("CUDA: ") + #call + ": " + \
+                                                      cudaGetErrorString(e__));         \
+  } while (0)
+
+}  // namespace hmtl_b200
+
+struct hmtl_ctx {
+  hmtl_b200::Ctx c;
+};

@@ -1,0 +1,394 @@
+// host.cpp -- host-side pieces of the B200 step (no device code):
+//   * flat parameter layouts (shared_layout / head_layout, hmtl/model.hpp:56-90)
+//   * parameter init identical to ModelT's ctor (hmtl/model.hpp:158-167, 211-225)
+//   * the synthetic multi-source generator used as the INPUT SOURCE
+//     (src/dataset.cpp:21-161, 213-239) -- re-stated here so the product never
+//     touches oracle/ or the reference; bit-identical by construction
+//     (std::mt19937_64 is standard-specified, distributions hand-rolled as in
+//     hmtl/rng.hpp) and checked against tests/golden/dataset5.npz
+//   * MTL-par head placement for uneven meshes (generalises hmtl/mesh.hpp:21-31)
+// Compiled with -ffp-contract=off: the reference is built without -march, so
+// it never contracts a*b+c into an FMA.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <numeric>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "hmtl_b200.h"
+#include "internal.h"
+
+namespace hmtl_b200 {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+// ----------------------------------------------------------------- layouts
+Layout make_layout(const hmtl_hyper& hp, bool shared) {
+  Layout L;
+  auto add = [&](const std::string& n, size_t r, size_t c) {
+    L.entries.push_back({n, r, c, L.total});
+    L.total += r * c;
+  };
+  const size_t H = hp.hidden;
+  if (shared) {
+    add("embed", hp.n_species, H);
+    for (int l = 0; l < hp.layers; ++l) {
+      const std::string p = "layer" + std::to_string(l) + ".";
+      add(p + "edge.W1", 2 * H + 1, H);
+      add(p + "edge.b1", 1, H);
+      add(p + "edge.W2", H, H);
+      add(p + "edge.b2", 1, H);
+      add(p + "node.W1", 2 * H, H);
+      add(p + "node.b1", 1, H);
+      add(p + "node.W2", H, H);
+      add(p + "node.b2", 1, H);
+    }
+  } else {
+    auto mlp = [&](const std::string& p, size_t in) {
+      for (int i = 0; i < hp.head_depth; ++i) {
+        size_t out = (i == hp.head_depth - 1) ? 1 : size_t(hp.head_width);
+        add(p + ".W" + std::to_string(i), in, out);
+        add(p + ".b" + std::to_string(i), 1, out);
+        in = out;
+      }
+    };
+    mlp("energy", H);
+    mlp("force", H + 1);
+  }
+  return L;
+}
+
+// ------------------------------------------------------------------- RNG
+uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+uint64_t seed_stream(uint64_t master, uint64_t id) {
+  return splitmix64(splitmix64(master) ^ splitmix64(id + 1));
+}
+
+namespace {
+// Same sequence contract as hmtl::Rng (hmtl/rng.hpp:19-77).
+struct Rng {
+  std::mt19937_64 eng;
+  double spare = 0.0;
+  bool have = false;
+  explicit Rng(uint64_t s) : eng(s) {}
+  uint64_t u64() { return eng(); }
+  double uniform() { return double(u64() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+  uint64_t uniform_int(uint64_t n) { return uint64_t((__uint128_t(u64()) * n) >> 64); }
+  double normal() {
+    if (have) {
+      have = false;
+      return spare;
+    }
+    double u1 = uniform(), u2 = uniform();
+    while (u1 <= 0.0) u1 = uniform();
+    double r = std::sqrt(-2.0 * std::log(u1));
+    double a = 6.283185307179586476925286766559 * u2;
+    spare = r * std::sin(a);
+    have = true;
+    return r * std::cos(a);
+  }
+  double normal(double m, double s) { return m + s * normal(); }
+};
+
+// ---- synthetic Morse-potential corpus (src/dataset.cpp:16-161)
+constexpr double kDmin = 0.8;
+constexpr uint64_t kMorseSeed = 0x4d4f525345ull;
+
+struct Morse {
+  double depth, width, r0;
+};
+Morse morse_params(uint8_t a, uint8_t b) {
+  if (a > b) std::swap(a, b);
+  Rng r(splitmix64(kMorseSeed ^ (uint64_t(a) * 131 + b)));
+  Morse p;
+  p.depth = r.uniform(0.4, 1.2);
+  p.width = r.uniform(0.8, 1.3);
+  p.r0 = r.uniform(1.0, 1.4);
+  return p;
+}
+
+void morse_labels(const std::vector<uint8_t>& sp, const std::vector<double>& x, double* e_out,
+                  std::vector<double>* f) {
+  const size_t n = sp.size();
+  double e = 0.0;
+  f->assign(3 * n, 0.0);
+  for (size_t i = 0; i < n; ++i)
+    for (size_t j = i + 1; j < n; ++j) {
+      const double dx = x[3 * i] - x[3 * j], dy = x[3 * i + 1] - x[3 * j + 1],
+                   dz = x[3 * i + 2] - x[3 * j + 2];
+      const double r = std::sqrt(dx * dx + dy * dy + dz * dz);
+      const Morse p = morse_params(sp[i], sp[j]);
+      const double ex = std::exp(-p.width * (r - p.r0));
+      const double om = 1.0 - ex;
+      e += p.depth * (om * om - 1.0);
+      const double ex2 = std::exp(-p.width * (r - p.r0));
+      const double g = (2.0 * p.width * p.depth * ex2 * (1.0 - ex2)) / r;
+      (*f)[3 * i] -= g * dx;
+      (*f)[3 * i + 1] -= g * dy;
+      (*f)[3 * i + 2] -= g * dz;
+      (*f)[3 * j] += g * dx;
+      (*f)[3 * j + 1] += g * dy;
+      (*f)[3 * j + 2] += g * dz;
+    }
+  *e_out = e;
+}
+
+bool place(Rng& r, size_t n, std::vector<double>* x) {
+  const double side = 1.6 * std::cbrt(double(n)) + 0.8;
+  x->assign(3 * n, 0.0);
+  for (size_t i = 0; i < n; ++i) {
+    bool ok = false;
+    for (int t = 0; t < 200 && !ok; ++t) {
+      const double a = r.uniform(0.0, side), b = r.uniform(0.0, side), c = r.uniform(0.0, side);
+      ok = true;
+      for (size_t j = 0; j < i; ++j) {
+        const double dx = a - (*x)[3 * j], dy = b - (*x)[3 * j + 1], dz = c - (*x)[3 * j + 2];
+        if (dx * dx + dy * dy + dz * dz < kDmin * kDmin) {
+          ok = false;
+          break;
+        }
+      }
+      if (ok) {
+        (*x)[3 * i] = a;
+        (*x)[3 * i + 1] = b;
+        (*x)[3 * i + 2] = c;
+      }
+    }
+    if (!ok) return false;
+  }
+  return true;
+}
+}  // namespace
+
+// ---------------------------------------------------------------- init
+void init_block(const hmtl_hyper& hp, uint64_t seed, int which, float* out) {
+  const bool shared = which < 0;
+  Layout L = make_layout(hp, shared);
+  Rng r(seed_stream(seed, shared ? 0 : uint64_t(1 + which)));
+  std::fill(out, out + L.total, 0.0f);
+  for (const auto& e : L.entries) {
+    if (e.name.find(".b") != std::string::npos) continue;
+    const double s = (shared && e.name == "embed") ? 0.5 : 1.0 / std::sqrt(double(e.rows));
+    for (size_t i = 0; i < e.rows * e.cols; ++i) out[e.offset + i] = float(r.uniform(-s, s));
+  }
+}
+
+}  // namespace hmtl_b200
+
+using namespace hmtl_b200;
+
+extern "C" {
+
+int hmtl_abi_version(void) { return HMTL_ABI_VERSION; }
+const char* hmtl_last_error(void) { return g_last_error.c_str(); }
+
+size_t hmtl_shared_size(const hmtl_hyper* hp) { return make_layout(*hp, true).total; }
+size_t hmtl_head_size(const hmtl_hyper* hp) { return make_layout(*hp, false).total; }
+
+int hmtl_layout_entry(const hmtl_hyper* hp, int shared, int i, char* name, size_t cap,
+                      size_t* rows, size_t* cols, size_t* offset) {
+  Layout L = make_layout(*hp, shared != 0);
+  const int n = int(L.entries.size());
+  if (i >= 0 && i < n) {
+    const auto& e = L.entries[i];
+    if (name && cap) std::snprintf(name, cap, "%s", e.name.c_str());
+    if (rows) *rows = e.rows;
+    if (cols) *cols = e.cols;
+    if (offset) *offset = e.offset;
+  }
+  return n;
+}
+
+int hmtl_init_block(const hmtl_hyper* hp, uint64_t seed, int which, float* out) {
+  if (!hp || !out) return fail(HMTL_ERR_CONTRACT, "init_block: null argument");
+  if (which >= hp->n_heads) return fail(HMTL_ERR_CONTRACT, "model: head index out of range");
+  init_block(*hp, seed, which, out);
+  return HMTL_OK;
+}
+
+// classify_regime, hmtl/model.hpp:249-255 (x10 threshold)
+int hmtl_classify_regime(size_t p_s, size_t p_h, int n_h) {
+  if (!(p_s > 0 && p_h > 0 && n_h > 0)) return -fail(HMTL_ERR_CONTRACT, "classify_regime: positive counts");
+  const double nhph = double(n_h) * double(p_h);
+  if (double(p_s) >= 10.0 * nhph) return 1;
+  if (nhph >= 10.0 * double(p_s)) return 2;
+  return 3;
+}
+// memory_footprint, hmtl/model.hpp:260-263
+size_t hmtl_memory_footprint(size_t p_s, size_t p_h, int n_h, int mode) {
+  if (mode == 2) return p_s + p_h;
+  return p_s + size_t(n_h) * p_h;
+}
+
+// default5_specs, src/dataset.cpp:213-239
+int hmtl_default5_spec(int id, hmtl_dataset_spec* s) {
+  struct Row {
+    const char* name;
+    std::vector<uint8_t> el;
+    int nmin, nmax;
+    double alpha, sigma;
+  };
+  static const Row rows[5] = {
+      {"organicA", {0, 1, 2, 3}, 4, 12, 1.00, 0.01},
+      {"organicB", {0, 2, 3, 4, 5}, 4, 16, 0.70, 0.02},
+      {"organicC", {0, 1, 3, 5, 6, 7}, 4, 14, 1.35, 0.01},
+      {"inorganicA", {2, 5, 8, 9, 10, 11, 12, 13, 14, 15}, 8, 40, 0.55, 0.03},
+      {"inorganicB", {3, 6, 9, 12, 14, 16, 17, 18, 19}, 8, 64, 1.60, 0.02},
+  };
+  if (id < 0 || id >= 5 || !s) return fail(HMTL_ERR_DATA, "default5: id out of range");
+  std::memset(s, 0, sizeof(*s));
+  const Row& r = rows[id];
+  s->dataset_id = id;
+  s->n_elements = int(r.el.size());
+  for (size_t i = 0; i < r.el.size(); ++i) s->elements[i] = r.el[i];
+  s->n_min = r.nmin;
+  s->n_max = r.nmax;
+  s->alpha = r.alpha;
+  s->sigma = r.sigma;
+  s->count = 10000;
+  s->structure_seed = -1;
+  Rng m(seed_stream(0x0FF5E75, uint64_t(id)));
+  for (uint8_t e : r.el) s->mu[e] = m.uniform(-3.0, 3.0);
+  return HMTL_OK;
+}
+
+// generate_dataset, src/dataset.cpp:106-161
+int hmtl_generate(const hmtl_dataset_spec* spec, uint64_t seed, int* G, int* N, int* n_atoms,
+                  uint8_t* species, double* positions, double* forces, double* energy,
+                  uint8_t* dataset_id) {
+  if (!spec || spec->n_min < 2 || spec->n_max < spec->n_min)
+    return fail(HMTL_ERR_DATA, "dataset spec: need n_min >= 2");
+  if (!(spec->alpha > 0.0)) return fail(HMTL_ERR_DATA, "dataset spec: alpha must be positive");
+  if (spec->n_elements < 1) return fail(HMTL_ERR_DATA, "dataset spec: empty element set");
+  for (int i = 0; i < spec->n_elements; ++i)
+    if (spec->elements[i] >= 20) return fail(HMTL_ERR_DATA, "dataset spec: element index out of range");
+  const uint64_t sseed = spec->structure_seed >= 0
+                             ? seed_stream(uint64_t(spec->structure_seed), 0xA)
+                             : seed_stream(seed, 0xA00 + uint64_t(spec->dataset_id));
+  Rng sr(sseed), nr(seed_stream(seed, 0xB00 + uint64_t(spec->dataset_id)));
+  size_t at = 0;
+  for (uint64_t k = 0; k < spec->count; ++k) {
+    const size_t n = size_t(spec->n_min) + sr.uniform_int(uint64_t(spec->n_max - spec->n_min + 1));
+    std::vector<uint8_t> sp(n);
+    for (size_t i = 0; i < n; ++i) sp[i] = spec->elements[sr.uniform_int(uint64_t(spec->n_elements))];
+    std::vector<double> x;
+    bool ok = false;
+    for (int t = 0; t < 20 && !ok; ++t) ok = place(sr, n, &x);
+    if (!ok) return fail(HMTL_ERR_DATA, "generate_dataset: rejection sampling failed (box too dense)");
+    double e_true;
+    std::vector<double> f_true;
+    morse_labels(sp, x, &e_true, &f_true);
+    double off = 0.0;
+    for (size_t i = 0; i < n; ++i) off += spec->mu[sp[i]];
+    double epa = spec->alpha * e_true / double(n) + off / double(n);
+    if (spec->sigma > 0.0) epa += nr.normal(0.0, spec->sigma);
+    if (n_atoms) {
+      n_atoms[k] = int(n);
+      std::memcpy(species + at, sp.data(), n);
+      std::memcpy(positions + 3 * at, x.data(), 3 * n * sizeof(double));
+      energy[k] = epa;
+      dataset_id[k] = uint8_t(spec->dataset_id);
+    }
+    for (size_t i = 0; i < 3 * n; ++i) {
+      double v = spec->alpha * f_true[i];
+      if (spec->sigma > 0.0) v += nr.normal(0.0, spec->sigma);
+      if (n_atoms) forces[3 * at + i] = v;
+    }
+    at += n;
+  }
+  if (G) *G = int(spec->count);
+  if (N) *N = int(at);
+  return HMTL_OK;
+}
+
+// Head placement for MTL-par on uneven meshes.  Head k is split evenly over
+// m_k replicas (sub-group of size m_k); the pieces (size w_k/m_k) are packed
+// into `world` ranks of equal load, each replica of a head on a distinct rank.
+// The search enumerates replica vectors by increasing piece count (fewest
+// pieces = most task-parallel, least communication) and packs by backtracking.
+int hmtl_head_placement(int world, int n_heads, const double* w, double* share) {
+  if (world < 1 || n_heads < 1 || !w || !share) return fail(HMTL_ERR_CONTRACT, "head_placement: bad args");
+  double total = 0.0;
+  for (int k = 0; k < n_heads; ++k) {
+    if (!(w[k] > 0.0)) return fail(HMTL_ERR_CONFIG, "head_placement: weights must be positive");
+    total += w[k];
+  }
+  const double cap = total / world;
+  std::fill(share, share + size_t(world) * n_heads, 0.0);
+  if (world == 1) {
+    for (int k = 0; k < n_heads; ++k) share[k] = 1.0;
+    return HMTL_OK;
+  }
+  std::vector<int> m(n_heads, 1);
+  for (int pieces = n_heads; pieces <= world * n_heads; ++pieces) {
+    // enumerate m with sum == pieces, each 1..world
+    std::function<bool(int, int)> rec_m = [&](int k, int left) -> bool {
+      if (k == n_heads) {
+        if (left != 0) return false;
+        struct Piece {
+          int head;
+          double size;
+        };
+        std::vector<Piece> ps;
+        for (int h = 0; h < n_heads; ++h)
+          for (int r = 0; r < m[h]; ++r) ps.push_back({h, w[h] / m[h]});
+        std::sort(ps.begin(), ps.end(), [](const Piece& a, const Piece& b) {
+          return a.size > b.size || (a.size == b.size && a.head < b.head);
+        });
+        std::vector<double> load(world, 0.0);
+        std::vector<std::vector<int>> has(world, std::vector<int>(n_heads, 0));
+        std::function<bool(size_t)> pack = [&](size_t i) -> bool {
+          if (i == ps.size()) {
+            for (int r = 0; r < world; ++r)
+              if (std::fabs(load[r] - cap) > 1e-9 * total) return false;
+            return true;
+          }
+          double prev = -1.0;
+          for (int r = 0; r < world; ++r) {
+            if (has[r][ps[i].head]) continue;
+            if (load[r] + ps[i].size > cap + 1e-9 * total) continue;
+            if (load[r] == prev) continue;  // symmetric bins
+            prev = load[r];
+            load[r] += ps[i].size;
+            has[r][ps[i].head] = 1;
+            if (pack(i + 1)) return true;
+            load[r] -= ps[i].size;
+            has[r][ps[i].head] = 0;
+          }
+          return false;
+        };
+        if (!pack(0)) return false;
+        for (int r = 0; r < world; ++r)
+          for (int h = 0; h < n_heads; ++h)
+            if (has[r][h]) share[size_t(r) * n_heads + h] = 1.0 / m[h];
+        return true;
+      }
+      const int rest = n_heads - k - 1;
+      for (int v = 1; v <= world && v <= left - rest; ++v) {
+        m[k] = v;
+        if (rec_m(k + 1, left - v)) return true;
+      }
+      return false;
+    };
+    if (rec_m(0, pieces)) return HMTL_OK;
+  }
+  return fail(HMTL_ERR_CONFIG, "head_placement: no balanced placement of the heads on this mesh");
+}
+
+}  // extern "C"

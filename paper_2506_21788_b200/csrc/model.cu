@@ -1,0 +1,898 @@
+// model.cu -- ModelT<float>::forward/backward on the GPU (FP32 parity path).
+//
+// Math: /root/reference/proj/include/hmtl/model.hpp:338-625 (restated in
+// SURVEY.md Appendix A).  Dataflow changes (exact in real arithmetic):
+//   * first edge layer factorised: z1_e = (h W1a)[dst] + (h W1b)[src] + d2_e w + b1
+//     -- a node GEMM (N x H x 2H) plus an L2-resident gather instead of an
+//     E x (2H+1) x H GEMM; its backward uses two CSR segment sums
+//     (S_dst, S_src via the reverse-edge permutation) and node GEMMs;
+//   * force-MLP layer 0 factorised the same way over h_i + h_j;
+//   * a1 / z1 / zf0 are recomputed from node tables instead of stored
+//     (saved per layer: z2 [E x H] only);
+//   * every scatter-add is a destination-sorted CSR segment reduction in
+//     ascending edge order (no float atomics, bit-reproducible), and every
+//     weight gradient is a split-row A^T B with a fixed-order reduction.
+// Head-specific weights: rows are grouped per owned head (head-sorted
+// permutations built by route_kernel); GEMM tiles never straddle heads.
+#include "ctx.cuh"
+
+namespace hmtl_b200 {
+
+namespace {
+
+int gridn(long long n, int threads, int cap) {
+  long long b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  return int(b < cap ? b : cap);
+}
+
+// first edge layer pre-activation z1(e, k), factorised (see header)
+__device__ __forceinline__ float z1_of(const float* __restrict__ P, int H, int d, int s, float d2,
+                                       const float* __restrict__ wd, const float* __restrict__ b1, int k) {
+  return __fadd_rn(__fadd_rn(__fadd_rn(P[size_t(d) * 2 * H + k], P[size_t(s) * 2 * H + H + k]), __fmul_rn(d2, wd[k])),
+                   b1[k]);
+}
+
+// force-MLP layer 0 pre-activation: psi_in = [h_i + h_j, d_ij] (hmtl/model.hpp:466-473)
+__device__ __forceinline__ float zf0_of(const float* __restrict__ Qf, int W, int d, int s, float dist,
+                                        const float* __restrict__ wdist, const float* __restrict__ b0, int k) {
+  return __fadd_rn(__fadd_rn(__fadd_rn(Qf[size_t(d) * W + k], Qf[size_t(s) * W + k]), __fmul_rn(dist, wdist[k])),
+                   b0[k]);
+}
+
+struct HeadW {  // a head-block tensor of slot `seg`: base + seg*PH + off
+  const float* base;
+  size_t PH, off;
+  __device__ __forceinline__ const float* at(int seg) const { return base + size_t(seg) * PH + off; }
+};
+struct HeadG {
+  float* base;
+  size_t PH, off;
+  __device__ __forceinline__ float* at(int seg) const { return base + size_t(seg) * PH + off; }
+};
+
+// ================================================================ forward
+// P = h [W1a | W1b]
+struct PProb {
+  static constexpr const char* kName = "fwd.node_P";
+  RowSet rows;
+  int K, Ncols, H;
+  const float *h, *W1;
+  float* P;
+  __device__ float a(int, int r, int k) const { return h[size_t(r) * H + k]; }
+  __device__ float b(int, int k, int n) const { return n < H ? W1[size_t(k) * H + n] : W1[size_t(H + k) * H + n - H]; }
+  __device__ void epi(int, int r, int n, float acc) const { P[size_t(r) * 2 * H + n] = acc; }
+};
+
+// z2 = silu(z1) W2 + b2   (hmtl/model.hpp:398-404)
+struct MsgProb {
+  static constexpr const char* kName = "fwd.edge_msg_gemm";
+  RowSet rows;
+  int K, Ncols, H;
+  const float *P, *wd, *b1, *W2, *b2;
+  const int *dst, *src;
+  const float4* geo;
+  float* z2;
+  __device__ float a(int, int e, int k) const { return silu(z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, k)); }
+  __device__ float b(int, int k, int n) const { return W2[size_t(k) * H + n]; }
+  __device__ void epi(int, int e, int n, float acc) const { z2[size_t(e) * H + n] = acc + b2[n]; }
+};
+
+// vz1 = [h, agg] nW1 + nb1   (hmtl/model.hpp:412-420)
+struct Node1Prob {
+  static constexpr const char* kName = "fwd.node_mlp1";
+  RowSet rows;
+  int K, Ncols, H;
+  const float *h, *agg, *W, *bias;
+  float* vz1;
+  __device__ float a(int, int r, int k) const { return k < H ? h[size_t(r) * H + k] : agg[size_t(r) * H + k - H]; }
+  __device__ float b(int, int k, int n) const { return W[size_t(k) * H + n]; }
+  __device__ void epi(int, int r, int n, float acc) const { vz1[size_t(r) * H + n] = acc + bias[n]; }
+};
+
+// h' = h + (silu(vz1) nW2 + nb2)   (hmtl/model.hpp:421-426, residual)
+struct Node2Prob {
+  static constexpr const char* kName = "fwd.node_mlp2";
+  RowSet rows;
+  int K, Ncols, H;
+  const float *vz1, *W, *bias, *h;
+  float* hn;
+  __device__ float a(int, int r, int k) const { return silu(vz1[size_t(r) * H + k]); }
+  __device__ float b(int, int k, int n) const { return W[size_t(k) * H + n]; }
+  __device__ void epi(int, int r, int n, float acc) const {
+    hn[size_t(r) * H + n] = h[size_t(r) * H + n] + (acc + bias[n]);
+  }
+};
+
+// energy MLP layer i over graph rows of each head (mlp_forward_, :282-306)
+struct EnergyProb {
+  static constexpr const char* kName = "fwd.energy_mlp";
+  RowSet rows;
+  int K, Ncols, H, W, layer, last;
+  const float *pooled, *ezp;  // ezp = ez of layer-1
+  HeadW Wt, Bt;
+  float *ez, *energy;
+  __device__ float a(int, int g, int k) const {
+    return layer == 0 ? pooled[size_t(g) * H + k] : silu(ezp[size_t(g) * W + k]);
+  }
+  __device__ float b(int seg, int k, int n) const { return Wt.at(seg)[size_t(k) * Ncols + n]; }
+  __device__ void epi(int seg, int g, int n, float acc) const {
+    const float z = acc + Bt.at(seg)[n];
+    ez[size_t(g) * W + n] = z;
+    if (last) energy[g] = z;
+  }
+};
+
+// Qf = h_L Wf0[:H]  (node rows per head)
+struct QfProb {
+  static constexpr const char* kName = "fwd.force_Qf";
+  RowSet rows;
+  int K, Ncols, H, W;
+  const float* h;
+  HeadW Wt;
+  float* Qf;
+  __device__ float a(int, int r, int k) const { return h[size_t(r) * H + k]; }
+  __device__ float b(int seg, int k, int n) const { return Wt.at(seg)[size_t(k) * W + n]; }
+  __device__ void epi(int, int r, int n, float acc) const { Qf[size_t(r) * W + n] = acc; }
+};
+
+// force MLP layer i >= 1 over edge rows per head; last layer writes s_e
+struct ForceProb {
+  static constexpr const char* kName = "fwd.force_edge_gemm";
+  RowSet rows;
+  int K, Ncols, H, W, layer, last;
+  long long Ec;
+  const float *Qf, *zf, *dist;
+  const int *dst, *src;
+  HeadW Wd, B0, Wt, Bt;  // Wd = row H of Wf0 (distance weight), B0 = bf0
+  float *zf_out, *s;
+  __device__ float a(int seg, int e, int k) const {
+    if (layer == 1) return silu(zf0_of(Qf, W, dst[e], src[e], dist[e], Wd.at(seg), B0.at(seg), k));
+    return silu(zf[size_t(layer - 2) * Ec * W + size_t(e) * W + k]);
+  }
+  __device__ float b(int seg, int k, int n) const { return Wt.at(seg)[size_t(k) * Ncols + n]; }
+  __device__ void epi(int seg, int e, int n, float acc) const {
+    const float z = acc + Bt.at(seg)[n];
+    if (last) s[e] = z;
+    else zf_out[size_t(layer - 1) * Ec * W + size_t(e) * W + n] = z;
+  }
+};
+
+__global__ void embed_kernel(const DevHdr* hdr, const uint8_t* __restrict__ species, const float* __restrict__ embed,
+                             float* __restrict__ h, int H) {
+  const long long total = (long long)hdr->N * H;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int i = int(t / H), k = int(t % H);
+    h[t] = embed[size_t(species[i]) * H + k];
+  }
+}
+
+// agg_i = sum_{e: dst(e)=i, ascending e} silu(z2_e)   (segment_sum, hmtl/kernels.hpp:97-108)
+__global__ void agg_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const float* __restrict__ z2,
+                           float* __restrict__ agg, int H) {
+  const int N = hdr->N;
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += (gridDim.x * blockDim.x) >> 5) {
+    const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
+    for (int c = lane; c < H; c += 32) {
+      float acc = 0.f;
+      for (int e = e0; e < e1; ++e) acc += silu(z2[size_t(e) * H + c]);
+      agg[size_t(i) * H + c] = acc;
+    }
+  }
+}
+
+// mean pool: (sum_i h_i) * (S(1)/S(n))   (hmtl/model.hpp:444-453)
+__global__ void pool_kernel(const DevHdr* hdr, const int* __restrict__ graph_offset, const float* __restrict__ h,
+                            float* __restrict__ pooled, int H) {
+  const int G = hdr->G;
+  const int lane = threadIdx.x & 31;
+  for (int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < G; g += (gridDim.x * blockDim.x) >> 5) {
+    const int lo = graph_offset[g], hi = graph_offset[g + 1];
+    const float inv = 1.f / float(hi - lo);
+    for (int c = lane; c < H; c += 32) {
+      float acc = 0.f;
+      for (int i = lo; i < hi; ++i) acc += h[size_t(i) * H + c];
+      pooled[size_t(g) * H + c] = acc * inv;
+    }
+  }
+}
+
+// F_i = sum_{e in row i} dvec_e * s_e   (hmtl/model.hpp:475-480)
+__global__ void forces_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const float4* __restrict__ geo,
+                              const float* __restrict__ s, float* __restrict__ F) {
+  const int N = hdr->N;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    float fx = 0.f, fy = 0.f, fz = 0.f;
+    for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+      const float4 g = geo[e];
+      const float se = s[e];
+      fx += g.x * se;
+      fy += g.y * se;
+      fz += g.z * se;
+    }
+    F[3 * i] = fx;
+    F[3 * i + 1] = fy;
+    F[3 * i + 2] = fz;
+  }
+}
+
+__global__ void finite_kernel(DevHdr* hdr, const float* __restrict__ energy, const float* __restrict__ F) {
+  const int G = hdr->G, N = hdr->N;
+  bool bad = false;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < G + 3 * N; t += gridDim.x * blockDim.x) {
+    const float v = t < G ? energy[t] : F[t - G];
+    if (!isfinite(v)) bad = true;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&hdr->err, kErrNonFinite);
+}
+
+template <class P>
+void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& c) {
+  Prof pr(c, P::kName, st);
+  const long long tiles = ((rows_cap + 63) / 64 + nseg) * ((p.Ncols + 63) / 64);
+  gemm_ab_kernel<P><<<gridn(tiles, 1, sm * 8), 256, 0, st>>>(p);
+}
+
+template <class P>
+void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st) {
+  Prof pr(c, P::kName, st);
+  const int tiles = ((p.K + 63) / 64) * ((p.Ncols + 63) / 64);
+  dim3 grid(tiles, nsplit, p.rows.nseg);
+  gemm_atb_kernel<P><<<grid, 256, 0, st>>>(p, c.partial, nsplit);
+  const long long total = (long long)p.K * p.Ncols * p.rows.nseg;
+  gemm_atb_reduce<P><<<gridn(total, 256, c.sm_count * 8), 256, 0, st>>>(p, c.partial, nsplit);
+}
+
+RowSet node_rows(Ctx& c) {
+  RowSet r;
+  r.count = &c.hdr->N;
+  return r;
+}
+RowSet edge_rows(Ctx& c) {
+  RowSet r;
+  r.count = &c.hdr->E;
+  return r;
+}
+RowSet node_rows_by_head(Ctx& c) {
+  RowSet r;
+  r.perm = c.node_perm;
+  r.seg_off = c.hdr->seg_node;
+  r.nseg = c.S;
+  return r;
+}
+RowSet edge_rows_by_head(Ctx& c) {
+  RowSet r;
+  r.perm = c.edge_perm;
+  r.seg_off = c.hdr->seg_edge;
+  r.nseg = c.S;
+  return r;
+}
+RowSet graph_rows_by_head(Ctx& c) {
+  RowSet r;
+  r.perm = c.gperm;
+  r.seg_off = c.hdr->seg_graph;
+  r.nseg = c.S;
+  return r;
+}
+
+}  // namespace
+
+void launch_forward(Ctx& c, cudaStream_t st) {
+  const int H = c.H, W = c.W, L = c.L, D = c.D, sm = c.sm_count;
+  const size_t NH = size_t(c.Nc) * H, EH = size_t(c.Ec) * H;
+  {
+    Prof pr(c, "fwd.embed", st);
+    embed_kernel<<<gridn(NH, 256, sm * 16), 256, 0, st>>>(c.hdr, c.species, c.shared_param("embed"), c.hs, H);
+  }
+  for (int l = 0; l < L; ++l) {
+    const std::string p = "layer" + std::to_string(l) + ".";
+    const float* h = c.hs + size_t(l) * NH;
+    float* hn = c.hs + size_t(l + 1) * NH;
+    float* P = c.P + size_t(l) * 2 * NH;
+    float* z2 = c.z2 + size_t(l) * EH;
+    float* agg = c.agg + size_t(l) * NH;
+    float* vz1 = c.vz1 + size_t(l) * NH;
+    const float* W1 = c.params + c.shared_off(p + "edge.W1");
+    {
+      PProb q{node_rows(c), H, 2 * H, H, h, W1, P};
+      ab(q, c.Nc, 1, st, sm, c);
+    }
+    {
+      MsgProb q{edge_rows(c), H, H, H, P, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
+                c.params + c.shared_off(p + "edge.W2"), c.params + c.shared_off(p + "edge.b2"), c.edge_dst,
+                c.edge_src, c.geo, z2};
+      ab(q, c.Ec, 1, st, sm, c);
+    }
+    {
+      Prof pr(c, "fwd.agg_segsum", st);
+      agg_kernel<<<gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st>>>(c.hdr, c.row_ptr, z2, agg, H);
+    }
+    {
+      Node1Prob q{node_rows(c), 2 * H, H, H, h, agg, c.params + c.shared_off(p + "node.W1"),
+                  c.params + c.shared_off(p + "node.b1"), vz1};
+      ab(q, c.Nc, 1, st, sm, c);
+    }
+    {
+      Node2Prob q{node_rows(c), H, H, H, vz1, c.params + c.shared_off(p + "node.W2"),
+                  c.params + c.shared_off(p + "node.b2"), h, hn};
+      ab(q, c.Nc, 1, st, sm, c);
+    }
+  }
+  const float* hL = c.hs + size_t(L) * NH;
+  // energy branch
+  {
+    Prof pr(c, "fwd.pool", st);
+    pool_kernel<<<gridn((long long)c.Gc * 32, 256, sm * 8), 256, 0, st>>>(c.hdr, c.graph_offset, hL, c.pooled, H);
+  }
+  for (int i = 0; i < D; ++i) {
+    const int last = i == D - 1;
+    EnergyProb q{graph_rows_by_head(c), i == 0 ? H : W, last ? 1 : W, H, W, i, last, c.pooled,
+                 i ? c.ez + size_t(i - 1) * c.Gc * W : nullptr,
+                 HeadW{c.head_params(), c.PH, c.head_off("energy.W" + std::to_string(i))},
+                 HeadW{c.head_params(), c.PH, c.head_off("energy.b" + std::to_string(i))},
+                 c.ez + size_t(i) * c.Gc * W, c.energy};
+    ab(q, c.Gc, c.S, st, sm, c);
+  }
+  // force branch
+  {
+    QfProb q{node_rows_by_head(c), H, W, H, W, hL, HeadW{c.head_params(), c.PH, c.head_off("force.W0")}, c.Qf};
+    ab(q, c.Nc, c.S, st, sm, c);
+  }
+  const size_t wf0 = c.head_off("force.W0");
+  for (int i = 1; i < D; ++i) {
+    const int last = i == D - 1;
+    ForceProb q{edge_rows_by_head(c), W, last ? 1 : W, H, W, i, last, c.Ec, c.Qf, c.zf, c.dist, c.edge_dst,
+                c.edge_src, HeadW{c.head_params(), c.PH, wf0 + size_t(H) * W},
+                HeadW{c.head_params(), c.PH, c.head_off("force.b0")},
+                HeadW{c.head_params(), c.PH, c.head_off("force.W" + std::to_string(i))},
+                HeadW{c.head_params(), c.PH, c.head_off("force.b" + std::to_string(i))}, c.zf, c.s};
+    ab(q, c.Ec, c.S, st, sm, c);
+  }
+  {
+    Prof pr(c, "fwd.forces_segsum", st);
+    forces_kernel<<<gridn(c.Nc, 256, sm * 8), 256, 0, st>>>(c.hdr, c.row_ptr, c.geo, c.s, c.forces);
+  }
+  {
+    Prof pr(c, "fwd.finite", st);
+    finite_kernel<<<gridn(c.Gc + 3LL * c.Nc, 256, sm * 4), 256, 0, st>>>(c.hdr, c.energy, c.forces);
+  }
+}
+
+// ----------------------------------------------------------------- loss
+// SPEC.md:383-391; one CTA, warp per graph, fixed-order reductions.
+namespace {
+__global__ void __launch_bounds__(1024) loss_kernel(DevHdr* hdr, const uint8_t* __restrict__ arena,
+                                                    const int* __restrict__ graph_offset,
+                                                    const float* __restrict__ energy, const float* __restrict__ F,
+                                                    float* __restrict__ dE, float* __restrict__ dF, float w_e,
+                                                    float w_f) {
+  __shared__ double wsum[32];
+  const int G = hdr->G, N = hdr->N;
+  const ArenaLayout al = arena_layout(G, N);
+  const double* le = reinterpret_cast<const double*>(arena + al.le);
+  const double* lf = reinterpret_cast<const double*>(arena + al.lf);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double acc = 0.0;
+  for (int g = wid; g < G; g += 32) {
+    const int lo = graph_offset[g], hi = graph_offset[g + 1];
+    const double n = double(hi - lo);
+    double fe = 0.0;
+    for (int t = 3 * lo + lane; t < 3 * hi; t += 32) {
+      const double r = double(F[t]) - lf[t];
+      fe += r * r;
+      dF[t] = float(2.0 * double(w_f) * r / (n * double(G)));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) fe += __shfl_xor_sync(0xffffffffu, fe, o);
+    const double de = double(energy[g]) - le[g];
+    if (lane == 0) {
+      acc += double(w_e) * de * de + double(w_f) * fe / n;
+      dE[g] = float(2.0 * double(w_e) * de / double(G));
+    }
+  }
+  if (lane == 0) wsum[wid] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 32; ++w) s += wsum[w];
+    hdr->loss = s / double(G);
+  }
+}
+}  // namespace
+
+void launch_loss(Ctx& c, float w_e, float w_f, cudaStream_t st) {
+  {
+    Prof pr(c, "loss", st);
+    loss_kernel<<<1, 1024, 0, st>>>(c.hdr, c.arena, c.graph_offset, c.energy, c.forces, c.dE, c.dF, w_e, w_f);
+  }
+}
+
+// ================================================================ backward
+namespace {
+
+// A^T B problems: store(seg, k, n, v) writes the gradient element
+struct EGradProb {  // energy MLP layer i weight+bias
+  static constexpr const char* kName = "bwd.energy_wgrad";
+  RowSet rows;
+  int K, Ncols, H, W, layer;  // K = in + 1
+  const float *pooled, *ezp, *dz;
+  int ldz;
+  HeadG G;
+  __device__ float a(int, int g, int k) const {
+    if (k == K - 1) return 1.f;
+    return layer == 0 ? pooled[size_t(g) * H + k] : silu(ezp[size_t(g) * W + k]);
+  }
+  __device__ float b(int, int g, int n) const { return dz[size_t(g) * ldz + n]; }
+  __device__ void store(int seg, int k, int n, float v) const { G.at(seg)[size_t(k) * Ncols + n] = v; }
+};
+// dx = dz W^T, epilogue dz_prev = dx * silu'(z_prev) (or plain dpooled)
+struct EDxProb {
+  static constexpr const char* kName = "bwd.energy_dx";
+  RowSet rows;
+  int K, Ncols, W, H;  // K = out_i, Ncols = in_i
+  const float *dz, *zprev;
+  int ldz;
+  HeadW Wt;
+  float* out;
+  int ldo, act;
+  __device__ float a(int, int g, int k) const { return dz[size_t(g) * ldz + k]; }
+  __device__ float b(int seg, int k, int n) const { return Wt.at(seg)[size_t(n) * K + k]; }
+  __device__ void epi(int, int g, int n, float acc) const {
+    out[size_t(g) * ldo + n] = act ? acc * silu_grad(zprev[size_t(g) * W + n]) : acc;
+  }
+};
+
+struct FGradProb {  // force MLP layer i >= 1 weight+bias (edge rows per head)
+  static constexpr const char* kName = "bwd.force_edge_wgrad";
+  RowSet rows;
+  int K, Ncols, H, W, layer;
+  long long Ec;
+  const float *Qf, *zf, *dist, *dz;
+  int ldz;
+  const int *dst, *src;
+  HeadW Wd, B0;
+  HeadG G;
+  __device__ float a(int seg, int e, int k) const {
+    if (k == K - 1) return 1.f;
+    if (layer == 1) return silu(zf0_of(Qf, W, dst[e], src[e], dist[e], Wd.at(seg), B0.at(seg), k));
+    return silu(zf[size_t(layer - 2) * Ec * W + size_t(e) * W + k]);
+  }
+  __device__ float b(int, int e, int n) const { return dz[size_t(e) * ldz + n]; }
+  __device__ void store(int seg, int k, int n, float v) const { G.at(seg)[size_t(k) * Ncols + n] = v; }
+};
+struct FDxProb {  // dz_{i-1} = (dz_i W_i^T) * silu'(z_{i-1})
+  static constexpr const char* kName = "bwd.force_edge_dx";
+  RowSet rows;
+  int K, Ncols, H, W, layer;  // layer = i
+  long long Ec;
+  const float *Qf, *zf, *dist, *dz;
+  int ldz;
+  const int *dst, *src;
+  HeadW Wd, B0, Wt;
+  float* out;
+  __device__ float a(int, int e, int k) const { return dz[size_t(e) * ldz + k]; }
+  __device__ float b(int seg, int k, int n) const { return Wt.at(seg)[size_t(n) * K + k]; }
+  __device__ void epi(int seg, int e, int n, float acc) const {
+    const float zp = layer == 1 ? zf0_of(Qf, W, dst[e], src[e], dist[e], Wd.at(seg), B0.at(seg), n)
+                                : zf[size_t(layer - 2) * Ec * W + size_t(e) * W + n];
+    out[size_t(e) * W + n] = acc * silu_grad(zp);
+  }
+};
+struct F0NodeGrad {  // g_Wf0[:H] = h^T T  (node rows per head)
+  static constexpr const char* kName = "bwd.force0_node_wgrad";
+  RowSet rows;
+  int K, Ncols, H, W;
+  const float *h, *T;
+  HeadG G;
+  __device__ float a(int, int r, int k) const { return h[size_t(r) * H + k]; }
+  __device__ float b(int, int r, int n) const { return T[size_t(r) * W + n]; }
+  __device__ void store(int seg, int k, int n, float v) const { G.at(seg)[size_t(k) * W + n] = v; }
+};
+struct F0EdgeGrad {  // g_Wf0[H] (distance row) and g_bf0 (edge rows per head)
+  static constexpr const char* kName = "bwd.force0_edge_wgrad";
+  RowSet rows;
+  int K, Ncols, H, W;
+  const float *dist, *dz;
+  HeadG G;  // points at row H of Wf0
+  __device__ float a(int, int e, int k) const { return k == 0 ? dist[e] : 1.f; }
+  __device__ float b(int, int e, int n) const { return dz[size_t(e) * W + n]; }
+  __device__ void store(int seg, int k, int n, float v) const { G.at(seg)[size_t(k) * W + n] = v; }
+};
+struct F0Dh {  // dh += T Wf0[:H]^T  (node rows per head)
+  static constexpr const char* kName = "bwd.force0_dh";
+  RowSet rows;
+  int K, Ncols, H, W;
+  const float* T;
+  HeadW Wt;
+  float* dh;
+  __device__ float a(int, int r, int k) const { return T[size_t(r) * W + k]; }
+  __device__ float b(int seg, int k, int n) const { return Wt.at(seg)[size_t(n) * W + k]; }
+  __device__ void epi(int, int r, int n, float acc) const { dh[size_t(r) * H + n] += acc; }
+};
+
+// ---- encoder layer backward problems (shared weights, identity rows)
+struct L1Prob {  // dvz1 = (dh nW2^T) * silu'(vz1)
+  static constexpr const char* kName = "bwd.node_dvz1";
+  RowSet rows;
+  int K, Ncols, H;
+  const float *dh, *W, *vz1;
+  float* dvz1;
+  __device__ float a(int, int r, int k) const { return dh[size_t(r) * H + k]; }
+  __device__ float b(int, int k, int n) const { return W[size_t(n) * H + k]; }
+  __device__ void epi(int, int r, int n, float acc) const {
+    dvz1[size_t(r) * H + n] = acc * silu_grad(vz1[size_t(r) * H + n]);
+  }
+};
+struct L2Prob {  // [g_nW2; g_nb2] = [silu(vz1), 1]^T dh
+  static constexpr const char* kName = "bwd.node_w2grad";
+  RowSet rows;
+  int K, Ncols, H;
+  const float *vz1, *dh;
+  float* G;
+  __device__ float a(int, int r, int k) const { return k < H ? silu(vz1[size_t(r) * H + k]) : 1.f; }
+  __device__ float b(int, int r, int n) const { return dh[size_t(r) * H + n]; }
+  __device__ void store(int, int k, int n, float v) const { G[size_t(k) * H + n] = v; }
+};
+struct L3Prob {  // [g_nW1; g_nb1] = [h, agg, 1]^T dvz1
+  static constexpr const char* kName = "bwd.node_w1grad";
+  RowSet rows;
+  int K, Ncols, H;
+  const float *h, *agg, *dvz1;
+  float* G;
+  __device__ float a(int, int r, int k) const {
+    return k < H ? h[size_t(r) * H + k] : (k < 2 * H ? agg[size_t(r) * H + k - H] : 1.f);
+  }
+  __device__ float b(int, int r, int n) const { return dvz1[size_t(r) * H + n]; }
+  __device__ void store(int, int k, int n, float v) const { G[size_t(k) * H + n] = v; }
+};
+struct L4Prob {  // dv = dvz1 nW1^T ; dh2 = dh + dv[:, :H] ; dagg = dv[:, H:]
+  static constexpr const char* kName = "bwd.node_dv";
+  RowSet rows;
+  int K, Ncols, H;
+  const float *dvz1, *W, *dh;
+  float *dh2, *dagg;
+  __device__ float a(int, int r, int k) const { return dvz1[size_t(r) * H + k]; }
+  __device__ float b(int, int k, int n) const { return W[size_t(n) * H + k]; }
+  __device__ void epi(int, int r, int n, float acc) const {
+    if (n < H) dh2[size_t(r) * H + n] = dh[size_t(r) * H + n] + acc;
+    else dagg[size_t(r) * H + n - H] = acc;
+  }
+};
+struct L6Prob {  // [g_eW2; g_eb2] = [silu(z1), 1]^T dz2   (E rows)
+  static constexpr const char* kName = "bwd.edge_w2grad";
+  RowSet rows;
+  int K, Ncols, H;
+  const float *P, *wd, *b1, *dz2;
+  const int *dst, *src;
+  const float4* geo;
+  float* G;
+  __device__ float a(int, int e, int k) const {
+    return k < H ? silu(z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, k)) : 1.f;
+  }
+  __device__ float b(int, int e, int n) const { return dz2[size_t(e) * H + n]; }
+  __device__ void store(int, int k, int n, float v) const { G[size_t(k) * H + n] = v; }
+};
+struct L7Prob {  // dz1 = (dz2 eW2^T) * silu'(z1)
+  static constexpr const char* kName = "bwd.edge_dz1_gemm";
+  RowSet rows;
+  int K, Ncols, H;
+  const float *dz2, *W, *P, *wd, *b1;
+  const int *dst, *src;
+  const float4* geo;
+  float* dz1;
+  __device__ float a(int, int e, int k) const { return dz2[size_t(e) * H + k]; }
+  __device__ float b(int, int k, int n) const { return W[size_t(n) * H + k]; }
+  __device__ void epi(int, int e, int n, float acc) const {
+    dz1[size_t(e) * H + n] = acc * silu_grad(z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, n));
+  }
+};
+struct L9Prob {  // [g_W1[2H]; g_b1] = [d2, 1]^T dz1   (E rows)
+  static constexpr const char* kName = "bwd.edge_w1tail_grad";
+  RowSet rows;
+  int K, Ncols, H;
+  const float4* geo;
+  const float* dz1;
+  float* G;  // row 2H of g_eW1
+  __device__ float a(int, int e, int k) const { return k == 0 ? geo[e].w : 1.f; }
+  __device__ float b(int, int e, int n) const { return dz1[size_t(e) * H + n]; }
+  __device__ void store(int, int k, int n, float v) const { G[size_t(k) * H + n] = v; }
+};
+struct L10Prob {  // g_W1a = h^T S_dst, g_W1b = h^T S_src
+  static constexpr const char* kName = "bwd.edge_w1ab_grad";
+  RowSet rows;
+  int K, Ncols, H;
+  const float *h, *S;
+  float* G;  // g_eW1
+  __device__ float a(int, int r, int k) const { return h[size_t(r) * H + k]; }
+  __device__ float b(int, int r, int n) const { return S[size_t(r) * 2 * H + n]; }
+  __device__ void store(int, int k, int n, float v) const {
+    if (n < H) G[size_t(k) * H + n] = v;
+    else G[size_t(H + k) * H + n - H] = v;
+  }
+};
+struct L11Prob {  // dh2 += S_dst W1a^T + S_src W1b^T
+  static constexpr const char* kName = "bwd.edge_dh_gemm";
+  RowSet rows;
+  int K, Ncols, H;
+  const float *S, *W1;
+  float* dh2;
+  __device__ float a(int, int r, int k) const { return S[size_t(r) * 2 * H + k]; }
+  __device__ float b(int, int k, int n) const {
+    return k < H ? W1[size_t(n) * H + k] : W1[size_t(H + n) * H + k - H];
+  }
+  __device__ void epi(int, int r, int n, float acc) const { dh2[size_t(r) * H + n] += acc; }
+};
+
+// dh_i = dpooled_g * (1/n)  (first contribution; hmtl/model.hpp:517-524)
+__global__ void dh_pool_kernel(const DevHdr* hdr, const int* __restrict__ node_graph,
+                               const int* __restrict__ graph_offset, const float* __restrict__ dpooled,
+                               float* __restrict__ dh, int H) {
+  const long long total = (long long)hdr->N * H;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int i = int(t / H), k = int(t % H);
+    const int g = node_graph[i];
+    const float inv = 1.f / float(graph_offset[g + 1] - graph_offset[g]);
+    dh[t] = dpooled[size_t(g) * H + k] * inv;
+  }
+}
+
+// ds_e = sum_c dF[dst,c] * dvec[e,c]  (hmtl/model.hpp:528-536)
+__global__ void ds_kernel(const DevHdr* hdr, const int* __restrict__ dst, const float4* __restrict__ geo,
+                          const float* __restrict__ dF, float* __restrict__ ds) {
+  const int E = hdr->E;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    const int i = dst[e];
+    const float4 g = geo[e];
+    float acc = 0.f;
+    acc += dF[3 * i] * g.x;
+    acc += dF[3 * i + 1] * g.y;
+    acc += dF[3 * i + 2] * g.z;
+    ds[e] = acc;
+  }
+}
+
+// dz2 = dagg[dst] * silu'(z2)  (hmtl/model.hpp:590-597)
+__global__ void dz2_kernel(const DevHdr* hdr, const int* __restrict__ dst, const float* __restrict__ dagg,
+                           const float* __restrict__ z2, float* __restrict__ dz2, int H) {
+  const long long total = (long long)hdr->E * H;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int e = int(t / H), k = int(t % H);
+    dz2[t] = dagg[size_t(dst[e]) * H + k] * silu_grad(z2[t]);
+  }
+}
+
+// S[i] = [ sum_{e in row i} x_e | sum_{e in row i} x_{rev(e)} ]; x is [E x C].
+// The second half is the src-segment sum: edges with src == i are exactly the
+// reverses of row i.  If `fold`, the two halves are added (force head: T).
+__global__ void seg2_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const int* __restrict__ rev,
+                            const float* __restrict__ x, float* __restrict__ S, int C, int fold) {
+  const int N = hdr->N;
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += (gridDim.x * blockDim.x) >> 5) {
+    const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
+    for (int c = lane; c < C; c += 32) {
+      float a = 0.f, b = 0.f;
+      for (int e = e0; e < e1; ++e) {
+        a += x[size_t(e) * C + c];
+        b += x[size_t(rev[e]) * C + c];
+      }
+      if (fold) S[size_t(i) * C + c] = a + b;
+      else {
+        S[size_t(i) * 2 * C + c] = a;
+        S[size_t(i) * 2 * C + C + c] = b;
+      }
+    }
+  }
+}
+
+// g_embed[s] = sum_{i: species_i = s} dh_i (ascending i; hmtl/model.hpp:619-622)
+__global__ void embed_grad_kernel(const DevHdr* hdr, const uint8_t* __restrict__ species, const float* __restrict__ dh,
+                                  float* __restrict__ G, int H, int NS) {
+  const int N = hdr->N;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < NS * H; t += gridDim.x * blockDim.x) {
+    const int s = t / H, k = t % H;
+    float acc = 0.f;
+    for (int i = 0; i < N; ++i)
+      if (species[i] == s) acc += dh[size_t(i) * H + k];
+    G[t] = acc;
+  }
+}
+
+}  // namespace
+
+void launch_backward(Ctx& c, cudaStream_t st) {
+  const int H = c.H, W = c.W, L = c.L, D = c.D, sm = c.sm_count;
+  const size_t NH = size_t(c.Nc) * H, EH = size_t(c.Ec) * H;
+  const float* hL = c.hs + size_t(L) * NH;
+  const size_t GW = size_t(c.Gc) * W;
+
+  // ---------------- energy heads (hmtl/model.hpp:512-524)
+  {
+    const float* dz = c.dE;
+    int ldz = 1;
+    float* bufs[2] = {c.edA, c.edB};
+    for (int i = D - 1; i >= 0; --i) {
+      const int in = i == 0 ? H : W, out = i == D - 1 ? 1 : W;
+      EGradProb gq{graph_rows_by_head(c), in + 1, out, H, W, i, c.pooled,
+                   i ? c.ez + size_t(i - 1) * GW : nullptr, dz, ldz,
+                   HeadG{c.head_grads(), c.PH, c.head_off("energy.W" + std::to_string(i))}};
+      atb(gq, c, c.nsplit_graph, st);
+      float* nxt = i ? bufs[i & 1] : c.dpooled;
+      EDxProb dq{graph_rows_by_head(c), out, in, W, H, dz, i ? c.ez + size_t(i - 1) * GW : nullptr, ldz,
+                 HeadW{c.head_params(), c.PH, c.head_off("energy.W" + std::to_string(i))}, nxt, i ? W : H,
+                 i ? 1 : 0};
+      ab(dq, c.Gc, c.S, st, sm, c);
+      dz = nxt;
+      ldz = W;
+    }
+    {
+      Prof pr(c, "bwd.pool", st);
+      dh_pool_kernel<<<gridn(NH, 256, sm * 16), 256, 0, st>>>(c.hdr, c.node_graph, c.graph_offset, c.dpooled, c.dh, H);
+    }
+  }
+  // ---------------- force heads (hmtl/model.hpp:526-549)
+  {
+    {
+      Prof pr(c, "bwd.force_ds", st);
+      ds_kernel<<<gridn(c.Ec, 256, sm * 8), 256, 0, st>>>(c.hdr, c.edge_dst, c.geo, c.dF, c.ds);
+    }
+    const size_t wf0 = c.head_off("force.W0");
+    const HeadW Wd{c.head_params(), c.PH, wf0 + size_t(H) * W};
+    const HeadW B0{c.head_params(), c.PH, c.head_off("force.b0")};
+    const float* dz = c.ds;
+    int ldz = 1;
+    float* bufs[2] = {c.dzA, c.dzB};
+    for (int i = D - 1; i >= 1; --i) {
+      const int out = i == D - 1 ? 1 : W;
+      FGradProb gq{edge_rows_by_head(c), W + 1, out, H, W, i, c.Ec, c.Qf, c.zf, c.dist, dz, ldz, c.edge_dst,
+                   c.edge_src, Wd, B0, HeadG{c.head_grads(), c.PH, c.head_off("force.W" + std::to_string(i))}};
+      atb(gq, c, c.nsplit_edge, st);
+      float* nxt = bufs[i & 1];
+      FDxProb dq{edge_rows_by_head(c), out, W, H, W, i, c.Ec, c.Qf, c.zf, c.dist, dz, ldz, c.edge_dst, c.edge_src,
+                 Wd, B0, HeadW{c.head_params(), c.PH, c.head_off("force.W" + std::to_string(i))}, nxt};
+      ab(dq, c.Ec, c.S, st, sm, c);
+      dz = nxt;
+      ldz = W;
+    }
+    // layer 0 (factorised): T = S_dst(dz0) + S_src(dz0)
+    {
+      Prof pr(c, "bwd.segsum_dst_src", st);
+      seg2_kernel<<<gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st>>>(c.hdr, c.row_ptr, c.rev, dz, c.Sbuf, W,
+                                                                            1);
+    }
+    F0NodeGrad ng{node_rows_by_head(c), H, W, H, W, hL, c.Sbuf, HeadG{c.head_grads(), c.PH, wf0}};
+    atb(ng, c, c.nsplit_node, st);
+    F0EdgeGrad eg{edge_rows_by_head(c), 2, W, H, W, c.dist, dz, HeadG{c.head_grads(), c.PH, wf0 + size_t(H) * W}};
+    atb(eg, c, c.nsplit_edge, st);
+    F0Dh dhq{node_rows_by_head(c), W, H, H, W, c.Sbuf, HeadW{c.head_params(), c.PH, wf0}, c.dh};
+    ab(dhq, c.Nc, c.S, st, sm, c);
+  }
+  // ---------------- encoder layers in reverse (hmtl/model.hpp:552-617)
+  float* dh = c.dh;
+  float* dh2 = c.dh2;
+  for (int l = L - 1; l >= 0; --l) {
+    const std::string p = "layer" + std::to_string(l) + ".";
+    const float* h = c.hs + size_t(l) * NH;
+    const float* P = c.P + size_t(l) * 2 * NH;
+    const float* z2 = c.z2 + size_t(l) * EH;
+    const float* agg = c.agg + size_t(l) * NH;
+    const float* vz1 = c.vz1 + size_t(l) * NH;
+    const float* eW1 = c.params + c.shared_off(p + "edge.W1");
+    const float* wd = eW1 + size_t(2) * H * H;
+    const float* b1 = c.params + c.shared_off(p + "edge.b1");
+    float* geW1 = c.grads + c.shared_off(p + "edge.W1");
+    {
+      L1Prob q{node_rows(c), H, H, H, dh, c.params + c.shared_off(p + "node.W2"), vz1, c.dvz1};
+      ab(q, c.Nc, 1, st, sm, c);
+    }
+    {
+      L2Prob q{node_rows(c), H + 1, H, H, vz1, dh, c.grads + c.shared_off(p + "node.W2")};
+      atb(q, c, c.nsplit_node, st);
+    }
+    {
+      L3Prob q{node_rows(c), 2 * H + 1, H, H, h, agg, c.dvz1, c.grads + c.shared_off(p + "node.W1")};
+      atb(q, c, c.nsplit_node, st);
+    }
+    {
+      L4Prob q{node_rows(c), H, 2 * H, H, c.dvz1, c.params + c.shared_off(p + "node.W1"), dh, dh2, c.dagg};
+      ab(q, c.Nc, 1, st, sm, c);
+    }
+    {
+      Prof pr(c, "bwd.edge_dz2_gather", st);
+      dz2_kernel<<<gridn(EH, 256, sm * 16), 256, 0, st>>>(c.hdr, c.edge_dst, c.dagg, z2, c.dzA, H);
+    }
+    {
+      L6Prob q{edge_rows(c), H + 1, H, H, P, wd, b1, c.dzA, c.edge_dst, c.edge_src, c.geo,
+               c.grads + c.shared_off(p + "edge.W2")};
+      atb(q, c, c.nsplit_edge, st);
+    }
+    {
+      L7Prob q{edge_rows(c), H, H, H, c.dzA, c.params + c.shared_off(p + "edge.W2"), P, wd, b1, c.edge_dst,
+               c.edge_src, c.geo, c.dzB};
+      ab(q, c.Ec, 1, st, sm, c);
+    }
+    {
+      Prof pr(c, "bwd.segsum_dst_src", st);
+      seg2_kernel<<<gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st>>>(c.hdr, c.row_ptr, c.rev, c.dzB, c.Sbuf,
+                                                                            H, 0);
+    }
+    {
+      L9Prob q{edge_rows(c), 2, H, H, c.geo, c.dzB, geW1 + size_t(2) * H * H};
+      atb(q, c, c.nsplit_edge, st);
+    }
+    {
+      L10Prob q{node_rows(c), H, 2 * H, H, h, c.Sbuf, geW1};
+      atb(q, c, c.nsplit_node, st);
+    }
+    {
+      L11Prob q{node_rows(c), 2 * H, H, H, c.Sbuf, eW1, dh2};
+      ab(q, c.Nc, 1, st, sm, c);
+    }
+    std::swap(dh, dh2);
+  }
+  {
+    Prof pr(c, "bwd.embed_grad", st);
+    embed_grad_kernel<<<gridn((long long)c.NS * H, 128, sm * 8), 128, 0, st>>>(c.hdr, c.species, dh,
+                                                                                 c.grads + c.shared_off("embed"), H,
+                                                                                 c.NS);
+  }
+}
+
+// debug probe: z1 of layer l (the factorised pre-activation), [E x H]
+namespace {
+__global__ void z1_kernel(const DevHdr* hdr, const float* __restrict__ P, const int* __restrict__ dst,
+                          const int* __restrict__ src, const float4* __restrict__ geo, const float* __restrict__ wd,
+                          const float* __restrict__ b1, float* __restrict__ out, int H) {
+  const long long total = (long long)hdr->E * H;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int e = int(t / H), k = int(t % H);
+    out[t] = z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, k);
+  }
+}
+}  // namespace
+
+void launch_debug_z1(Ctx& c, int l, float* out, cudaStream_t st) {
+  const std::string p = "layer" + std::to_string(l) + ".";
+  const float* W1 = c.params + c.shared_off(p + "edge.W1");
+  z1_kernel<<<gridn((long long)c.Ec * c.H, 256, c.sm_count * 16), 256, 0, st>>>(
+      c.hdr, c.P + size_t(l) * 2 * c.Nc * c.H, c.edge_dst, c.edge_src, c.geo, W1 + size_t(2) * c.H * c.H,
+      c.params + c.shared_off(p + "edge.b1"), out, c.H);
+}
+
+// ---------------------------------------------------------------- AdamW
+namespace {
+__global__ void adam_tick(DevHdr* hdr) { hdr->step += 1; }
+// torch.optim.AdamW ordering (decision recorded in DESIGN.md)
+__global__ void adamw_kernel(const DevHdr* hdr, float* __restrict__ p, const float* __restrict__ g,
+                             float* __restrict__ m, float* __restrict__ v, size_t n, float lr, float b1, float b2,
+                             float eps, float wd) {
+  const int t = hdr->step;
+  const float bc1 = float(1.0 - pow(double(b1), double(t)));
+  const float bc2s = float(sqrt(1.0 - pow(double(b2), double(t))));
+  const float step_size = lr / bc1;
+  const float decay = float(1.0 - double(lr) * double(wd));
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    float pi = p[i] * decay;
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float denom = sqrtf(vi) / bc2s + eps;
+    p[i] = pi - step_size * mi / denom;
+  }
+}
+}  // namespace
+
+void launch_adamw(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st) {
+  adam_tick<<<1, 1, 0, st>>>(c.hdr);
+  {
+    Prof pr(c, "adamw", st);
+    adamw_kernel<<<gridn(c.PT, 256, c.sm_count * 8), 256, 0, st>>>(c.hdr, c.params, c.grads, c.adam_m, c.adam_v, c.PT,
+                                                                   cfg.lr, cfg.beta1, cfg.beta2, cfg.eps,
+                                                                   cfg.weight_decay);
+  }
+}
+
+}  // namespace hmtl_b200

@@ -1,0 +1,365 @@
+"""Python mirror of the reference's C++ API for the hot path, backed by the
+B200 C ABI (include/hmtl_b200.h).  Names follow the reference:
+
+  ModelHyper            hmtl/model.hpp:17-37
+  shared_layout/head_layout  hmtl/model.hpp:56-90
+  ModelT (float)        hmtl/model.hpp:155-242  (forward :196-197, backward :198-201)
+  build_batch           hmtl/graph.hpp:46-83    (runs on the GPU)
+  PredictionT / GradientBufferT  hmtl/model.hpp:92-115
+  classify_regime / memory_footprint  hmtl/model.hpp:246-263
+
+Host numpy arrays in, host numpy arrays out; the device keeps the batch, the
+forward cache and the parameters.  Errors raise HmtlError with the
+reference's ErrorCode.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import CCaps, CHyper, CSamples, CTrainCfg, HmtlError, check, lib
+
+__all__ = [
+    "ModelHyper", "Samples", "Caps", "ModelT", "PredictionT", "GradientBufferT", "GraphBatch", "TrainConfig",
+    "shared_layout", "head_layout", "classify_regime", "memory_footprint", "HmtlError",
+]
+
+
+@dataclass
+class ModelHyper:
+    n_species: int = 20
+    layers: int = 2
+    hidden: int = 32
+    head_width: int = 32
+    head_depth: int = 3
+    n_heads: int = 1
+    cutoff: float = 5.0
+
+    @staticmethod
+    def paper_preset(n_heads: int) -> "ModelHyper":
+        """4 x 866 encoder, 3-layer 889-unit heads (hmtl/model.hpp:28-36)."""
+        return ModelHyper(layers=4, hidden=866, head_width=889, head_depth=3, n_heads=n_heads)
+
+    def c(self) -> CHyper:
+        return CHyper(self.n_species, self.layers, self.hidden, self.head_width, self.head_depth, self.n_heads,
+                      self.cutoff)
+
+
+def _layout(hp: ModelHyper, shared: bool):
+    ch = hp.c()
+    n = lib().hmtl_layout_entry(C.byref(ch), int(shared), -1, None, 0, None, None, None)
+    out = []
+    for i in range(n):
+        nm = C.create_string_buffer(64)
+        r, c, o = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        lib().hmtl_layout_entry(C.byref(ch), int(shared), i, nm, 64, C.byref(r), C.byref(c), C.byref(o))
+        out.append((nm.value.decode(), r.value, c.value, o.value))
+    return out
+
+
+def shared_layout(hp: ModelHyper):
+    return _layout(hp, True)
+
+
+def head_layout(hp: ModelHyper):
+    return _layout(hp, False)
+
+
+def classify_regime(p_s: int, p_h: int, n_h: int) -> int:
+    """1, 2, 3 = ParallelRegime::case1..case3 (hmtl/model.hpp:249-255)."""
+    r = lib().hmtl_classify_regime(p_s, p_h, n_h)
+    if r < 0:
+        raise HmtlError(-r, lib().hmtl_last_error().decode())
+    return r
+
+
+def memory_footprint(p_s: int, p_h: int, n_h: int, mode: str) -> int:
+    return lib().hmtl_memory_footprint(p_s, p_h, n_h, {"serial": 0, "base": 1, "taskpar": 2}[mode])
+
+
+@dataclass
+class Samples:
+    """A list of AtomisticSample (hmtl/graph.hpp:13-21), struct-of-arrays."""
+
+    n_atoms: np.ndarray  # [G] int32
+    species: np.ndarray  # [N] uint8
+    positions: np.ndarray  # [N,3] float64
+    forces: np.ndarray  # [N,3] float64
+    energy: np.ndarray  # [G] float64 (energy per atom)
+    dataset_id: np.ndarray  # [G] uint8
+
+    def __post_init__(self):
+        self.n_atoms = np.ascontiguousarray(self.n_atoms, np.int32)
+        self.species = np.ascontiguousarray(self.species, np.uint8)
+        self.positions = np.ascontiguousarray(self.positions, np.float64).reshape(-1, 3)
+        self.forces = np.ascontiguousarray(self.forces, np.float64).reshape(-1, 3)
+        self.energy = np.ascontiguousarray(self.energy, np.float64)
+        self.dataset_id = np.ascontiguousarray(self.dataset_id, np.uint8)
+
+    @property
+    def G(self) -> int:
+        return len(self.n_atoms)
+
+    @property
+    def N(self) -> int:
+        return len(self.species)
+
+    def edge_bound(self) -> int:
+        n = self.n_atoms.astype(np.int64)
+        return int((n * (n - 1)).sum())
+
+    def offsets(self) -> np.ndarray:
+        return np.concatenate([[0], np.cumsum(self.n_atoms)]).astype(np.int64)
+
+    def take(self, idx) -> "Samples":
+        off = self.offsets()
+        idx = list(idx)
+        cat = lambda a: np.concatenate([a[off[i]:off[i + 1]] for i in idx]) if idx else a[:0]
+        return Samples(self.n_atoms[idx], cat(self.species), cat(self.positions), cat(self.forces), self.energy[idx],
+                       self.dataset_id[idx])
+
+    @staticmethod
+    def concat(parts) -> "Samples":
+        return Samples(*[np.concatenate([getattr(p, f) for p in parts]) for f in
+                         ("n_atoms", "species", "positions", "forces", "energy", "dataset_id")])
+
+    def as_c(self) -> CSamples:
+        P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
+        return CSamples(self.G, self.N, P(self.n_atoms, C.c_int), P(self.species, C.c_uint8),
+                        P(self.positions, C.c_double), P(self.forces, C.c_double), P(self.energy, C.c_double),
+                        P(self.dataset_id, C.c_uint8))
+
+
+@dataclass
+class Caps:
+    max_graphs: int
+    max_nodes: int
+    max_edges: int
+
+    @staticmethod
+    def for_samples(s: Samples, slack: float = 1.0) -> "Caps":
+        return Caps(max(1, int(s.G * slack)), max(1, int(s.N * slack)), max(1, int(s.edge_bound() * slack)))
+
+    def covers(self, s: Samples) -> bool:
+        return s.G <= self.max_graphs and s.N <= self.max_nodes and s.edge_bound() <= self.max_edges
+
+    def union(self, o: "Caps") -> "Caps":
+        return Caps(max(self.max_graphs, o.max_graphs), max(self.max_nodes, o.max_nodes),
+                    max(self.max_edges, o.max_edges))
+
+
+@dataclass
+class PredictionT:
+    energy_per_atom: np.ndarray  # [G]
+    forces: np.ndarray  # [N,3]
+
+
+@dataclass
+class GradientBufferT:
+    shared: np.ndarray
+    heads: dict = field(default_factory=dict)
+
+
+@dataclass
+class GraphBatch:
+    """Edge view of GraphBatchT (hmtl/graph.hpp:27-42) as built on the device."""
+
+    n_graphs: int
+    graph_offset: np.ndarray
+    edge_offset: np.ndarray
+    edge_dst: np.ndarray
+    edge_src: np.ndarray
+
+    def n_edges(self) -> int:
+        return len(self.edge_dst)
+
+
+@dataclass
+class TrainConfig:
+    """TrainConfig + AdamW defaults."""
+
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.01
+    w_energy: float = 1.0
+    w_force: float = 1.0
+    use_graph: bool = True
+
+    def c(self) -> CTrainCfg:
+        return CTrainCfg(self.lr, self.beta1, self.beta2, self.eps, self.weight_decay, self.w_energy, self.w_force,
+                         int(self.use_graph))
+
+
+class ModelT:
+    """ModelT<float> living on one B200 (hmtl/model.hpp:155-242)."""
+
+    def __init__(self, hp: ModelHyper, seed: int, owned_heads, caps: Caps | None = None, device: int = 0):
+        self.hp, self.seed, self.device = hp, int(seed), int(device)
+        self.owned = sorted(int(k) for k in owned_heads)
+        self.caps = caps or Caps(64, 4096, 1 << 17)
+        self._ctx = None
+        self._create(self.caps)
+        self._G = self._N = 0
+
+    # ---- context management
+    def _create(self, caps: Caps, params=None):
+        ctx = C.c_void_p()
+        owned = (C.c_int * len(self.owned))(*self.owned)
+        cc = CCaps(caps.max_graphs, caps.max_nodes, caps.max_edges)
+        check(lib().hmtl_ctx_create(self.device, C.byref(self.hp.c()), self.seed, owned, len(self.owned),
+                                    C.byref(cc), C.byref(ctx)))
+        self._ctx = ctx
+        self.caps = caps
+        if params is not None:
+            for k, v in params.items():
+                check(lib().hmtl_set_block(self._ctx, k, _fp(v)))
+
+    def reserve(self, s: Samples) -> None:
+        """Grow the device capacities to fit `s` (keeps parameters, drops optimiser state)."""
+        if self.caps.covers(s):
+            return
+        params = {-1: self.shared_block(), **{k: self.head_block(k) for k in self.owned}}
+        self.close()
+        self._create(self.caps.union(Caps.for_samples(s, 1.25)), params)
+
+    def close(self):
+        if self._ctx is not None:
+            lib().hmtl_ctx_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def ctx(self):
+        return self._ctx
+
+    # ---- census (hmtl/model.hpp:169-180)
+    def shared_size(self) -> int:
+        return lib().hmtl_shared_size(C.byref(self.hp.c()))
+
+    def head_size(self) -> int:
+        return lib().hmtl_head_size(C.byref(self.hp.c()))
+
+    def owns_head(self, k: int) -> bool:
+        return k in self.owned
+
+    def n_owned_heads(self) -> int:
+        return len(self.owned)
+
+    def param_count(self) -> int:
+        return self.shared_size() + len(self.owned) * self.head_size()
+
+    # ---- blocks (hmtl/model.hpp:182-187)
+    def _get(self, fn, which, n):
+        out = np.zeros(n, np.float32)
+        check(fn(self._ctx, which, _fp(out)))
+        return out
+
+    def shared_block(self) -> np.ndarray:
+        return self._get(lib().hmtl_get_block, -1, self.shared_size())
+
+    def head_block(self, k: int) -> np.ndarray:
+        return self._get(lib().hmtl_get_block, k, self.head_size())
+
+    def set_shared_block(self, v) -> None:
+        check(lib().hmtl_set_block(self._ctx, -1, _fp(np.ascontiguousarray(v, np.float32))))
+
+    def set_head_block(self, k: int, v) -> None:
+        check(lib().hmtl_set_block(self._ctx, k, _fp(np.ascontiguousarray(v, np.float32))))
+
+    # ---- step pieces
+    def upload(self, s: Samples, stream=None) -> None:
+        self.reserve(s)
+        self._keep = s
+        check(lib().hmtl_batch_upload(self._ctx, C.byref(s.as_c()), stream))
+        self._G, self._N = s.G, s.N
+
+    def build_batch(self, s: Samples) -> GraphBatch:
+        """build_batch<float> on the device; returns the edge view (syncs)."""
+        self.upload(s)
+        check(lib().hmtl_build_batch(self._ctx, None))
+        return self.edges()
+
+    def edges(self) -> GraphBatch:
+        E = C.c_int()
+        check(lib().hmtl_batch_edges(self._ctx, C.byref(E), None, None, None))
+        dst = np.zeros(max(E.value, 1), np.int32)
+        src = np.zeros(max(E.value, 1), np.int32)
+        eo = np.zeros(self._G + 1, np.int32)
+        check(lib().hmtl_batch_edges(self._ctx, C.byref(E), _ip(dst), _ip(src), _ip(eo)))
+        go = np.concatenate([[0], np.cumsum(self._keep.n_atoms)]).astype(np.int32)
+        return GraphBatch(self._G, go, eo, dst[:E.value], src[:E.value])
+
+    def forward(self, s: Samples | None = None) -> PredictionT:
+        """ModelT::forward (hmtl/model.hpp:338-488).  With `s`, uploads and builds the batch first."""
+        if s is not None:
+            self.upload(s)
+            check(lib().hmtl_build_batch(self._ctx, None))
+        check(lib().hmtl_forward(self._ctx, None))
+        e = np.zeros(self._G, np.float32)
+        f = np.zeros(3 * self._N, np.float32)
+        check(lib().hmtl_predictions(self._ctx, _fp(e), _fp(f)))
+        return PredictionT(e, f.reshape(-1, 3))
+
+    def loss(self, w_energy: float = 1.0, w_force: float = 1.0) -> float:
+        """SPEC loss on the device (also leaves dE/dF on the device for backward(None, None))."""
+        check(lib().hmtl_loss(self._ctx, w_energy, w_force, None))
+        L = C.c_float()
+        check(lib().hmtl_read_loss(self._ctx, C.byref(L)))
+        return float(L.value)
+
+    def backward(self, d_energy=None, d_forces=None) -> GradientBufferT:
+        """ModelT::backward (hmtl/model.hpp:490-625) for the last forward."""
+        if d_energy is None:
+            check(lib().hmtl_backward(self._ctx, None, None, None))
+        else:
+            de = np.ascontiguousarray(d_energy, np.float32)
+            df = np.ascontiguousarray(d_forces, np.float32).reshape(-1)
+            if de.size != self._G or df.size != 3 * self._N:
+                raise HmtlError(1, "model: upstream shape mismatch")
+            check(lib().hmtl_backward(self._ctx, _fp(de), _fp(df), None))
+        return self.grads()
+
+    def grads(self) -> GradientBufferT:
+        g = GradientBufferT(self._get(lib().hmtl_get_grad, -1, self.shared_size()))
+        for k in self.owned:
+            g.heads[k] = self._get(lib().hmtl_get_grad, k, self.head_size())
+        return g
+
+    def debug(self, name: str, layer: int = 0) -> np.ndarray:
+        n = C.c_size_t()
+        check(lib().hmtl_debug_fetch(self._ctx, name.encode(), layer, None, 0, C.byref(n)))
+        out = np.zeros(max(n.value, 1), np.float32)
+        check(lib().hmtl_debug_fetch(self._ctx, name.encode(), layer, _fp(out), out.size, C.byref(n)))
+        return out[: n.value]
+
+    def adamw(self, cfg: TrainConfig) -> None:
+        check(lib().hmtl_adamw(self._ctx, C.byref(cfg.c()), None))
+
+    def train_step(self, s: Samples | None, cfg: TrainConfig, stream=None, read_loss: bool = True):
+        """train_step -- uploads `s` (if given) and runs the whole
+        stream-ordered step; returns the loss (syncs) when read_loss."""
+        if s is not None:
+            self.upload(s, stream)
+        check(lib().hmtl_train_step(self._ctx, C.byref(cfg.c()), stream))
+        if read_loss:
+            L = C.c_float()
+            check(lib().hmtl_read_loss(self._ctx, C.byref(L)))
+            return float(L.value)
+        return None
+
+
+def _fp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _ip(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int))

@@ -1,0 +1,103 @@
+"""Training-step parity: SPEC loss/AdamW on the B200 vs the
+FP64 oracle trainer, including the 100-step loss curve (north star)."""
+import numpy as np
+import pytest
+
+import oracle as O
+
+import paper_2506_21788_b200 as P
+from paper_2506_21788_b200 import data
+from paper_2506_21788_b200.model import Samples
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    P.build()
+    O.build(ref=False)
+    if P.lib().hmtl_device_count() < 1:
+        pytest.skip("no CUDA device")
+
+
+def batch(counts, seed=1234):
+    specs = data.default5_specs()
+    return Samples.concat([data.generate_dataset(sp, seed + k, count=c) for k, (sp, c) in enumerate(zip(specs, counts)) if c])
+
+
+class OracleTrainer:
+    def __init__(self, o, oh, seed, owned):
+        self.o, self.oh = o, oh
+        self.sh = o.init_block(oh, seed, -1)
+        self.heads = {k: o.init_block(oh, seed, k) for k in owned}
+        self.st = {"s": (np.zeros_like(self.sh), np.zeros_like(self.sh))}
+        for k in owned:
+            self.st[k] = (np.zeros_like(self.heads[k]), np.zeros_like(self.heads[k]))
+        self.t = 0
+
+    def step(self, s: Samples, cutoff=5.0):
+        b = O.batch_from_samples(dict(n_atoms=s.n_atoms, species=s.species, pos=s.positions, forces=s.forces,
+                                      energy=s.energy, dsid=s.dataset_id), cutoff, self.o.build_edges)
+        E, F, c = self.o.forward(self.oh, self.sh, self.heads, b)
+        L, dE, dF = self.o.loss(b, E, F)
+        gs, gh = self.o.backward(self.oh, self.sh, self.heads, b, c, dE, dF)
+        self.t += 1
+        self.o.adamw(self.sh, gs, *self.st["s"], self.t)
+        for k in self.heads:
+            self.o.adamw(self.heads[k], gh[k], *self.st[k], self.t)
+        return L
+
+
+def test_adamw_one_step_matches_oracle():
+    o = O.Oracle()
+    hp = P.ModelHyper(20, 2, 16, 16, 3, 5, 5.0)
+    oh = O.Hyper(20, 2, 16, 16, 3, 5, 5.0)
+    s = batch((3, 2, 2, 1, 1))
+    m = P.ModelT(hp, 7, range(5))
+    ot = OracleTrainer(o, oh, 7, range(5))
+    cfg = P.TrainConfig(use_graph=False)
+    L = m.train_step(s, cfg)
+    Lo = ot.step(s)
+    assert abs(L - Lo) / Lo < 1e-5
+    assert O.rel_vec_error(m.shared_block(), ot.sh) < 1e-6
+    for k in range(5):
+        assert O.rel_vec_error(m.head_block(k), ot.heads[k]) < 1e-6
+
+
+def test_cuda_graph_step_equals_eager_step():
+    hp = P.ModelHyper(20, 2, 32, 32, 3, 5, 5.0)
+    s1, s2 = batch((3, 2, 2, 1, 1), 1), batch((4, 1, 3, 2, 1), 2)
+    caps = P.Caps.for_samples(s1).union(P.Caps.for_samples(s2))
+    res = []
+    for g in (False, True):
+        m = P.ModelT(hp, 7, range(5), caps=caps)
+        cfg = P.TrainConfig(use_graph=g)
+        Ls = [m.train_step(x, cfg) for x in (s1, s2, s1, s2)]
+        res.append((Ls, m.shared_block()))
+        m.close()
+    assert res[0][0] == res[1][0]
+    assert np.array_equal(res[0][1], res[1][1])
+
+
+def test_loss_curve_100_steps_matches_fp64_oracle():
+    """Loss curves over 100 steps (north star).  Same batches, same seeds; the
+    FP32 B200 path vs the FP64 restatement of the reference."""
+    o = O.Oracle()
+    hp = P.ModelHyper(20, 2, 32, 32, 3, 5, 5.0)
+    oh = O.Hyper(20, 2, 32, 32, 3, 5, 5.0)
+    batches = [batch((3, 2, 2, 1, 1), 100 + i) for i in range(4)]
+    caps = P.Caps(64, 1024, max(b.edge_bound() for b in batches))
+    m = P.ModelT(hp, 7, range(5), caps=caps)
+    ot = OracleTrainer(o, oh, 7, range(5))
+    cfg = P.TrainConfig(use_graph=True)
+    g, ref = [], []
+    for step in range(100):
+        b = batches[step % 4]
+        g.append(m.train_step(b, cfg))
+        ref.append(ot.step(b))
+    g, ref = np.array(g), np.array(ref)
+    relerr = np.abs(g - ref) / np.abs(ref)
+    print("max rel loss deviation over 100 steps:", relerr.max(), "final", g[-1], ref[-1])
+    assert ref[-1] < ref[0]  # it trains
+    assert relerr.max() < 1e-3
+    assert O.rel_vec_error(m.shared_block(), ot.sh) < 1e-3
