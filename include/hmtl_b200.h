@@ -179,6 +179,11 @@ int hmtl_debug_fetch(hmtl_ctx* ctx, const char* name, int layer, float* host, si
 int hmtl_profile_enable(hmtl_ctx* ctx, int on);
 int hmtl_profile_report(hmtl_ctx* ctx, char* json, size_t cap);
 
+/* Engine self-test (not on the training path): runs the tcgen05 engines on
+ * plain row-major matrices on device 0.  mode 0: C[rows x N] = X[rows x K] B[K x N]
+ * (Y = B); mode 1: C[K x N] = X[rows x K]^T Y[rows x N].  variant: debug bits. */
+int hmtl_selftest_gemm(int mode, int variant, int rows, int K, int N, const float* X, const float* Y, float* C);
+
 /* ------------------------------------------------------------ comm (NCCL) */
 /* collective::allreduce_mean over RankGroup (hmtl/mesh.hpp:276-278, 312-342),
  * re-implemented as NCCL communicators: one world communicator and one per

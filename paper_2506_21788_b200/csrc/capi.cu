@@ -1,6 +1,7 @@
 // capi.cu -- the C ABI (include/hmtl_b200.h): device context, batch upload,
 // and the stream-ordered training step.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -75,7 +76,7 @@ void free_ctx(Ctx& c) {
                   c.species, c.gslot, c.gperm, c.gnode_base, c.gedge_base, c.node_perm, c.edge_perm, c.hs, c.P,
                   c.z2, c.agg, c.vz1, c.pooled, c.ez, c.energy, c.Qf, c.zf, c.s, c.forces, c.dE, c.dF, c.dh,
                   c.dh2, c.dagg, c.dvz1, c.dzA, c.dzB, c.Sbuf, c.ds, c.dpooled, c.edA, c.edB, c.scratch,
-                  c.partial};
+                  c.partial, c.bimg, c.a1, c.af0};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto* p : c.pool) cudaFree(p);
@@ -225,7 +226,15 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   const size_t kn_shared = (2 * H + 1) * H;
   const size_t kn_head = std::max({(H + 1) * W, (W + 1) * W, H * W, 2 * W});
   c.partial_cap = std::max(size_t(64) * kn_shared, size_t(c.S) * 64 * kn_head);
+  c.partial_cap = std::max(c.partial_cap, size_t(std::max(c.S, 1)) * 128 * (2 * std::max(H, W) + 1) * std::max(H, W));
   A(&c.partial, c.partial_cap);
+  c.bimg_cap = size_t(std::max(c.S, 2)) * 2 * (2 * std::max(H, W)) * (2 * std::max(H, W));
+  A(&c.bimg, c.bimg_cap);
+  if (const char* e = std::getenv("HMTL_NO_TC")) c.use_tc = e[0] == '0';
+  c.store_a1 = c.use_tc && H % 32 == 0;
+  c.store_af0 = c.use_tc && W % 32 == 0;
+  A(&c.a1, c.store_a1 ? L * E * H : 1);
+  A(&c.af0, c.store_af0 ? E * W : 1);
   if (rc) {
     free_ctx(c);
     delete h;

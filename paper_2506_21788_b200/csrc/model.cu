@@ -14,7 +14,12 @@
 //     weight gradient is a split-row A^T B with a fixed-order reduction.
 // Head-specific weights: rows are grouped per owned head (head-sorted
 // permutations built by route_kernel); GEMM tiles never straddle heads.
+#include <algorithm>
+#include <type_traits>
+#include <utility>
+
 #include "ctx.cuh"
+#include "tc.cuh"
 
 namespace hmtl_b200 {
 
@@ -40,6 +45,25 @@ __device__ __forceinline__ float zf0_of(const float* __restrict__ Qf, int W, int
                    b0[k]);
 }
 
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ float4 silu4(float4 a) { return make_float4(silu(a.x), silu(a.y), silu(a.z), silu(a.w)); }
+__device__ __forceinline__ float4 mul4(float4 a, float4 b) { return make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w); }
+__device__ __forceinline__ float4 sgrad4(float4 a) {
+  return make_float4(silu_grad(a.x), silu_grad(a.y), silu_grad(a.z), silu_grad(a.w));
+}
+// factorised pre-activation for 4 consecutive columns (same op order as z1_of/zf0_of)
+__device__ __forceinline__ float4 pre4(float4 a, float4 b, float s, float4 w, float4 bias) {
+  return make_float4(__fadd_rn(__fadd_rn(__fadd_rn(a.x, b.x), __fmul_rn(s, w.x)), bias.x),
+                     __fadd_rn(__fadd_rn(__fadd_rn(a.y, b.y), __fmul_rn(s, w.y)), bias.y),
+                     __fadd_rn(__fadd_rn(__fadd_rn(a.z, b.z), __fmul_rn(s, w.z)), bias.z),
+                     __fadd_rn(__fadd_rn(__fadd_rn(a.w, b.w), __fmul_rn(s, w.w)), bias.w));
+}
+
+// head-block vectors are not 16 B aligned (reference layout: energy.b2 is one float)
+__device__ __forceinline__ float4 ldu4(const float* p) { return make_float4(p[0], p[1], p[2], p[3]); }
+
 struct HeadW {  // a head-block tensor of slot `seg`: base + seg*PH + off
   const float* base;
   size_t PH, off;
@@ -55,6 +79,8 @@ struct HeadG {
 // P = h [W1a | W1b]
 struct PProb {
   static constexpr const char* kName = "fwd.node_P";
+  __device__ float4 a4(int, int r, int k) const { return ld4(h + size_t(r) * H + k); }
+  __device__ void epi4(int, int r, int n, float4 acc) const { st4(P + size_t(r) * 2 * H + n, acc); }
   RowSet rows;
   int K, Ncols, H;
   const float *h, *W1;
@@ -67,12 +93,33 @@ struct PProb {
 // z2 = silu(z1) W2 + b2   (hmtl/model.hpp:398-404)
 struct MsgProb {
   static constexpr const char* kName = "fwd.edge_msg_gemm";
+  struct RC {
+    int d, s;
+    float w;
+  };
+  __device__ RC rctx(int, int e) const { return RC{dst[e], src[e], geo[e].w}; }
+  __device__ float4 a4c(int, int e, const RC& r, int k) const {
+    const float4 a = silu4(pre4(ld4(P + size_t(r.d) * 2 * H + k), ld4(P + size_t(r.s) * 2 * H + H + k), r.w,
+                                ld4(wd + k), ld4(b1 + k)));
+    if (a1out) st4(a1out + size_t(e) * H + k, a);  // materialise a1 for the dW2 reduce GEMM
+    return a;
+  }
+  __device__ void epi4c(int, int e, const RC&, int n, float4 acc) const {
+    st4(z2 + size_t(e) * H + n, add4(acc, ld4(b2 + n)));
+  }
+  __device__ float4 a4(int, int e, int k) const {
+    const int d = dst[e], s = src[e];
+    return silu4(pre4(ld4(P + size_t(d) * 2 * H + k), ld4(P + size_t(s) * 2 * H + H + k), geo[e].w, ld4(wd + k),
+                      ld4(b1 + k)));
+  }
+  __device__ void epi4(int, int e, int n, float4 acc) const { st4(z2 + size_t(e) * H + n, add4(acc, ld4(b2 + n))); }
   RowSet rows;
   int K, Ncols, H;
   const float *P, *wd, *b1, *W2, *b2;
   const int *dst, *src;
   const float4* geo;
   float* z2;
+  float* a1out;
   __device__ float a(int, int e, int k) const { return silu(z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, k)); }
   __device__ float b(int, int k, int n) const { return W2[size_t(k) * H + n]; }
   __device__ void epi(int, int e, int n, float acc) const { z2[size_t(e) * H + n] = acc + b2[n]; }
@@ -81,6 +128,10 @@ struct MsgProb {
 // vz1 = [h, agg] nW1 + nb1   (hmtl/model.hpp:412-420)
 struct Node1Prob {
   static constexpr const char* kName = "fwd.node_mlp1";
+  __device__ float4 a4(int, int r, int k) const {
+    return k < H ? ld4(h + size_t(r) * H + k) : ld4(agg + size_t(r) * H + k - H);
+  }
+  __device__ void epi4(int, int r, int n, float4 acc) const { st4(vz1 + size_t(r) * H + n, add4(acc, ld4(bias + n))); }
   RowSet rows;
   int K, Ncols, H;
   const float *h, *agg, *W, *bias;
@@ -93,6 +144,10 @@ struct Node1Prob {
 // h' = h + (silu(vz1) nW2 + nb2)   (hmtl/model.hpp:421-426, residual)
 struct Node2Prob {
   static constexpr const char* kName = "fwd.node_mlp2";
+  __device__ float4 a4(int, int r, int k) const { return silu4(ld4(vz1 + size_t(r) * H + k)); }
+  __device__ void epi4(int, int r, int n, float4 acc) const {
+    st4(hn + size_t(r) * H + n, add4(ld4(h + size_t(r) * H + n), add4(acc, ld4(bias + n))));
+  }
   RowSet rows;
   int K, Ncols, H;
   const float *vz1, *W, *bias, *h;
@@ -126,6 +181,8 @@ struct EnergyProb {
 // Qf = h_L Wf0[:H]  (node rows per head)
 struct QfProb {
   static constexpr const char* kName = "fwd.force_Qf";
+  __device__ float4 a4(int, int r, int k) const { return ld4(h + size_t(r) * H + k); }
+  __device__ void epi4(int, int r, int n, float4 acc) const { st4(Qf + size_t(r) * W + n, acc); }
   RowSet rows;
   int K, Ncols, H, W;
   const float* h;
@@ -139,6 +196,35 @@ struct QfProb {
 // force MLP layer i >= 1 over edge rows per head; last layer writes s_e
 struct ForceProb {
   static constexpr const char* kName = "fwd.force_edge_gemm";
+  struct RC {
+    int d, s;
+    float dist;
+  };
+  __device__ RC rctx(int, int e) const { return RC{dst[e], src[e], dist[e]}; }
+  __device__ float4 a4c(int seg, int e, const RC& r, int k) const {
+    if (layer == 1) {
+      const float4 a = silu4(pre4(ld4(Qf + size_t(r.d) * W + k), ld4(Qf + size_t(r.s) * W + k), r.dist,
+                                  ldu4(Wd.at(seg) + k), ldu4(B0.at(seg) + k)));
+      if (af0out) st4(af0out + size_t(e) * W + k, a);  // materialise silu(zf0) for the dWf1 reduce GEMM
+      return a;
+    }
+    return silu4(ld4(zf + size_t(layer - 2) * Ec * W + size_t(e) * W + k));
+  }
+  __device__ void epi4c(int seg, int e, const RC&, int n, float4 acc) const { epi4(seg, e, n, acc); }
+  __device__ float4 a4(int seg, int e, int k) const {
+    if (layer == 1)
+      return silu4(pre4(ld4(Qf + size_t(dst[e]) * W + k), ld4(Qf + size_t(src[e]) * W + k), dist[e],
+                        ldu4(Wd.at(seg) + k), ldu4(B0.at(seg) + k)));
+    return silu4(ld4(zf + size_t(layer - 2) * Ec * W + size_t(e) * W + k));
+  }
+  __device__ void epi4(int seg, int e, int n, float4 acc) const {
+    const float4 z = add4(acc, ldu4(Bt.at(seg) + n));
+    if (last) {
+      s[e] = z.x;  // Ncols == 1 never reaches the tensor-core path
+    } else {
+      st4(zf_out + size_t(layer - 1) * Ec * W + size_t(e) * W + n, z);
+    }
+  }
   RowSet rows;
   int K, Ncols, H, W, layer, last;
   long long Ec;
@@ -146,6 +232,7 @@ struct ForceProb {
   const int *dst, *src;
   HeadW Wd, B0, Wt, Bt;  // Wd = row H of Wf0 (distance weight), B0 = bf0
   float *zf_out, *s;
+  float* af0out;
   __device__ float a(int seg, int e, int k) const {
     if (layer == 1) return silu(zf0_of(Qf, W, dst[e], src[e], dist[e], Wd.at(seg), B0.at(seg), k));
     return silu(zf[size_t(layer - 2) * Ec * W + size_t(e) * W + k]);
@@ -227,16 +314,148 @@ __global__ void finite_kernel(DevHdr* hdr, const float* __restrict__ energy, con
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&hdr->err, kErrNonFinite);
 }
 
+// ---- tcgen05 adapters over the SIMT problem functors (same math, same epilogues)
+template <class P, class = void>
+struct HasA4 : std::false_type {};
+template <class P>
+struct HasA4<P, std::void_t<decltype(std::declval<const P&>().a4(0, 0, 0))>> : std::true_type {};
+template <class P, class = void>
+struct HasEpi4 : std::false_type {};
+template <class P>
+struct HasEpi4<P, std::void_t<decltype(std::declval<const P&>().epi4(0, 0, 0, float4{}))>> : std::true_type {};
+
+struct NoRC {};
+template <class P, class = void>
+struct RCOf {
+  using type = NoRC;
+  static constexpr bool has = false;
+};
+template <class P>
+struct RCOf<P, std::void_t<typename P::RC>> {
+  using type = typename P::RC;
+  static constexpr bool has = true;
+};
+
+template <class P>
+struct TcRow {
+  using RC = typename RCOf<P>::type;
+  RowSet rows;
+  int K, Ncols;
+  const float* bimg;
+  size_t bimg_seg;
+  P p;
+  __device__ __forceinline__ RC rctx(int seg, int row) const {
+    if constexpr (RCOf<P>::has) return p.rctx(seg, row);
+    else return RC{};
+  }
+  __device__ __forceinline__ float4 a4(int seg, int row, const RC& rc, int k) const {
+    if constexpr (RCOf<P>::has) return p.a4c(seg, row, rc, k);
+    else if constexpr (HasA4<P>::value) return p.a4(seg, row, k);
+    else return make_float4(p.a(seg, row, k), p.a(seg, row, k + 1), p.a(seg, row, k + 2), p.a(seg, row, k + 3));
+  }
+  __device__ __forceinline__ void epi4(int seg, int row, const RC& rc, int n, float4 acc) const {
+    if constexpr (RCOf<P>::has) {
+      p.epi4c(seg, row, rc, n, acc);
+    } else if constexpr (HasEpi4<P>::value) {
+      p.epi4(seg, row, n, acc);
+    } else {
+      p.epi(seg, row, n, acc.x);
+      p.epi(seg, row, n + 1, acc.y);
+      p.epi(seg, row, n + 2, acc.z);
+      p.epi(seg, row, n + 3, acc.w);
+    }
+  }
+};
+template <class P, class = void>
+struct HasX4 : std::false_type {};
+template <class P>
+struct HasX4<P, std::void_t<decltype(std::declval<const P&>().x4(0, 0, 0))>> : std::true_type {};
+template <class P, class = void>
+struct HasY4 : std::false_type {};
+template <class P>
+struct HasY4<P, std::void_t<decltype(std::declval<const P&>().y4(0, 0, 0))>> : std::true_type {};
+// B image of problem P: B(n, k) = p.b(seg, k, n), layout of tc::bimg_kernel
+template <class P>
+__global__ void bimg_prob_kernel(P p, float* __restrict__ out, int nseg) {
+  const int K = p.K, N = p.Ncols;
+  const size_t total = size_t(nseg) * K * N;
+  for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < total; t += size_t(gridDim.x) * blockDim.x) {
+    const int seg = int(t / (size_t(K) * N));
+    const int rem = int(t % (size_t(K) * N));
+    const int n = rem % N, k = rem / N;
+    const float x = p.b(seg, k, n);
+    const float h = tc::tf32_hi(x);
+    const int ch = k / tc::KC, g = (k % tc::KC) / 4, q = k % 4;
+    float* o = out + size_t(seg) * 2 * K * N + size_t(ch) * 2 * tc::KC * N;
+    o[(size_t(g) * N + n) * 4 + q] = h;
+    o[size_t(tc::KC) * N + (size_t(g) * N + n) * 4 + q] = x - h;
+  }
+}
+template <class P>
+struct TcRed {
+  RowSet rows;
+  int M, Ncols, colsum;
+  P p;
+  __device__ __forceinline__ float4 x4(int seg, int row, int m) const {
+    if constexpr (HasX4<P>::value) return p.x4(seg, row, m);
+    else return make_float4(p.a(seg, row, m), p.a(seg, row, m + 1), p.a(seg, row, m + 2), p.a(seg, row, m + 3));
+  }
+  __device__ __forceinline__ float4 y4(int seg, int row, int n) const {
+    if constexpr (HasY4<P>::value) return p.y4(seg, row, n);
+    else return make_float4(p.b(seg, row, n), p.b(seg, row, n + 1), p.b(seg, row, n + 2), p.b(seg, row, n + 3));
+  }
+  __device__ __forceinline__ void store(int seg, int k, int n, float v) const { p.store(seg, k, n, v); }
+};
+
+template <class Kern>
+void set_smem(Kern k, size_t bytes) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+}
+
 template <class P>
 void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& c) {
   Prof pr(c, P::kName, st);
+  const bool use_tc = c.use_tc && p.K % tc::KC == 0 && p.Ncols % 32 == 0 && p.Ncols <= 256 &&
+                      size_t(nseg) * 2 * p.K * p.Ncols <= c.bimg_cap;
+  if (use_tc) {
+    bimg_prob_kernel<P><<<gridn((long long)nseg * p.K * p.Ncols, 256, sm * 4), 256, 0, st>>>(p, c.bimg, nseg);
+    TcRow<P> q{p.rows, p.K, p.Ncols, c.bimg, size_t(2) * p.K * p.Ncols, p};
+    const long long mtiles = (rows_cap + 127) / 128 + nseg;
+    // split N when there are too few row tiles to fill the GPU (node-row GEMMs)
+    int Nt = p.Ncols;
+    while (Nt > 32 && mtiles * (p.Ncols / Nt) < sm && (Nt / 2) % 32 == 0) Nt /= 2;
+    const tc::RowPlan plan = tc::row_plan(p.K, Nt);
+    set_smem(tc::tc_row_kernel<TcRow<P>>, plan.smem);
+    tc::tc_row_kernel<TcRow<P>><<<gridn(mtiles * (p.Ncols / Nt), 1, sm), tc::kRowThreads, plan.smem, st>>>(q, plan);
+    return;
+  }
   const long long tiles = ((rows_cap + 63) / 64 + nseg) * ((p.Ncols + 63) / 64);
   gemm_ab_kernel<P><<<gridn(tiles, 1, sm * 8), 256, 0, st>>>(p);
 }
 
 template <class P>
-void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st) {
+void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0) {
   Prof pr(c, P::kName, st);
+  const int M = p.K - P::kBias;
+  if (c.use_tc && P::kTc && p.Ncols % 32 == 0 && p.Ncols <= 256 && M % 4 == 0) {
+    const int mtiles = (M + 127) / 128;
+    const long long chunks = (rows_cap > 0 ? rows_cap : (long long)c.Ec) / tc::KC + 1;
+    // enough CTAs to fill the GPU, >= 4 chunks each (bounded partial traffic)
+    long long want = std::max<long long>(1, (long long)c.sm_count * 2 / (mtiles * p.rows.nseg));
+    int ns = int(std::max<long long>(1, std::min<long long>(want, chunks / 4)));
+    while (ns > 1 && size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * p.Ncols > c.partial_cap) ns /= 2;
+    if (size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * p.Ncols <= c.partial_cap) {
+      TcRed<P> q{p.rows, M, p.Ncols, P::kBias, p};
+      const size_t smem = tc::tc_red_smem(p.Ncols);
+      set_smem(tc::tc_red_kernel<TcRed<P>>, smem);
+      dim3 grid(mtiles, ns, p.rows.nseg);
+      tc::tc_red_kernel<TcRed<P>><<<grid, tc::kRedThreads, smem, st>>>(q, c.partial, ns,
+                                                                        tc::red_stages(p.Ncols));
+      const long long total = (long long)(M + P::kBias) * p.Ncols * p.rows.nseg;
+      tc::tc_red_reduce<TcRed<P>><<<gridn(total, 256, c.sm_count * 8), 256, 0, st>>>(q, c.partial, ns);
+      return;
+    }
+  }
   const int tiles = ((p.K + 63) / 64) * ((p.Ncols + 63) / 64);
   dim3 grid(tiles, nsplit, p.rows.nseg);
   gemm_atb_kernel<P><<<grid, 256, 0, st>>>(p, c.partial, nsplit);
@@ -301,7 +520,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     {
       MsgProb q{edge_rows(c), H, H, H, P, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
                 c.params + c.shared_off(p + "edge.W2"), c.params + c.shared_off(p + "edge.b2"), c.edge_dst,
-                c.edge_src, c.geo, z2};
+                c.edge_src, c.geo, z2, c.store_a1 ? c.a1 + size_t(l) * EH : nullptr};
       ab(q, c.Ec, 1, st, sm, c);
     }
     {
@@ -346,7 +565,8 @@ void launch_forward(Ctx& c, cudaStream_t st) {
                 c.edge_src, HeadW{c.head_params(), c.PH, wf0 + size_t(H) * W},
                 HeadW{c.head_params(), c.PH, c.head_off("force.b0")},
                 HeadW{c.head_params(), c.PH, c.head_off("force.W" + std::to_string(i))},
-                HeadW{c.head_params(), c.PH, c.head_off("force.b" + std::to_string(i))}, c.zf, c.s};
+                HeadW{c.head_params(), c.PH, c.head_off("force.b" + std::to_string(i))}, c.zf, c.s,
+                c.store_af0 ? c.af0 : nullptr};
     ab(q, c.Ec, c.S, st, sm, c);
   }
   {
@@ -414,6 +634,12 @@ namespace {
 // A^T B problems: store(seg, k, n, v) writes the gradient element
 struct EGradProb {  // energy MLP layer i weight+bias
   static constexpr const char* kName = "bwd.energy_wgrad";
+  static constexpr int kBias = 1;
+  static constexpr bool kTc = true;
+  __device__ float4 x4(int, int g, int m) const {
+    return layer == 0 ? ld4(pooled + size_t(g) * H + m) : silu4(ld4(ezp + size_t(g) * W + m));
+  }
+  __device__ float4 y4(int, int g, int n) const { return ld4(dz + size_t(g) * ldz + n); }
   RowSet rows;
   int K, Ncols, H, W, layer;  // K = in + 1
   const float *pooled, *ezp, *dz;
@@ -445,6 +671,17 @@ struct EDxProb {
 
 struct FGradProb {  // force MLP layer i >= 1 weight+bias (edge rows per head)
   static constexpr const char* kName = "bwd.force_edge_wgrad";
+  static constexpr int kBias = 1;
+  static constexpr bool kTc = true;
+  __device__ float4 x4(int seg, int e, int m) const {
+    if (layer == 1) {
+      if (af0s) return ld4(af0s + size_t(e) * W + m);
+      return silu4(pre4(ld4(Qf + size_t(dst[e]) * W + m), ld4(Qf + size_t(src[e]) * W + m), dist[e],
+                        ldu4(Wd.at(seg) + m), ldu4(B0.at(seg) + m)));
+    }
+    return silu4(ld4(zf + size_t(layer - 2) * Ec * W + size_t(e) * W + m));
+  }
+  __device__ float4 y4(int, int e, int n) const { return ld4(dz + size_t(e) * ldz + n); }
   RowSet rows;
   int K, Ncols, H, W, layer;
   long long Ec;
@@ -453,6 +690,7 @@ struct FGradProb {  // force MLP layer i >= 1 weight+bias (edge rows per head)
   const int *dst, *src;
   HeadW Wd, B0;
   HeadG G;
+  const float* af0s;  // silu(zf0) materialised by the forward producer (nullable)
   __device__ float a(int seg, int e, int k) const {
     if (k == K - 1) return 1.f;
     if (layer == 1) return silu(zf0_of(Qf, W, dst[e], src[e], dist[e], Wd.at(seg), B0.at(seg), k));
@@ -463,6 +701,25 @@ struct FGradProb {  // force MLP layer i >= 1 weight+bias (edge rows per head)
 };
 struct FDxProb {  // dz_{i-1} = (dz_i W_i^T) * silu'(z_{i-1})
   static constexpr const char* kName = "bwd.force_edge_dx";
+  struct RC {
+    int d, s;
+    float dist;
+  };
+  __device__ RC rctx(int, int e) const { return RC{dst[e], src[e], dist[e]}; }
+  __device__ float4 a4c(int, int e, const RC&, int k) const { return ld4(dz + size_t(e) * ldz + k); }
+  __device__ void epi4c(int seg, int e, const RC& r, int n, float4 acc) const {
+    const float4 zp = layer == 1 ? pre4(ld4(Qf + size_t(r.d) * W + n), ld4(Qf + size_t(r.s) * W + n), r.dist,
+                                        ldu4(Wd.at(seg) + n), ldu4(B0.at(seg) + n))
+                                 : ld4(zf + size_t(layer - 2) * Ec * W + size_t(e) * W + n);
+    st4(out + size_t(e) * W + n, mul4(acc, sgrad4(zp)));
+  }
+  __device__ float4 a4(int, int e, int k) const { return ld4(dz + size_t(e) * ldz + k); }
+  __device__ void epi4(int seg, int e, int n, float4 acc) const {
+    const float4 zp = layer == 1 ? pre4(ld4(Qf + size_t(dst[e]) * W + n), ld4(Qf + size_t(src[e]) * W + n), dist[e],
+                                        ldu4(Wd.at(seg) + n), ldu4(B0.at(seg) + n))
+                                 : ld4(zf + size_t(layer - 2) * Ec * W + size_t(e) * W + n);
+    st4(out + size_t(e) * W + n, mul4(acc, sgrad4(zp)));
+  }
   RowSet rows;
   int K, Ncols, H, W, layer;  // layer = i
   long long Ec;
@@ -481,6 +738,10 @@ struct FDxProb {  // dz_{i-1} = (dz_i W_i^T) * silu'(z_{i-1})
 };
 struct F0NodeGrad {  // g_Wf0[:H] = h^T T  (node rows per head)
   static constexpr const char* kName = "bwd.force0_node_wgrad";
+  static constexpr int kBias = 0;
+  static constexpr bool kTc = true;
+  __device__ float4 x4(int, int r, int m) const { return ld4(h + size_t(r) * H + m); }
+  __device__ float4 y4(int, int r, int n) const { return ld4(T + size_t(r) * W + n); }
   RowSet rows;
   int K, Ncols, H, W;
   const float *h, *T;
@@ -491,6 +752,8 @@ struct F0NodeGrad {  // g_Wf0[:H] = h^T T  (node rows per head)
 };
 struct F0EdgeGrad {  // g_Wf0[H] (distance row) and g_bf0 (edge rows per head)
   static constexpr const char* kName = "bwd.force0_edge_wgrad";
+  static constexpr int kBias = 0;
+  static constexpr bool kTc = false;
   RowSet rows;
   int K, Ncols, H, W;
   const float *dist, *dz;
@@ -501,6 +764,11 @@ struct F0EdgeGrad {  // g_Wf0[H] (distance row) and g_bf0 (edge rows per head)
 };
 struct F0Dh {  // dh += T Wf0[:H]^T  (node rows per head)
   static constexpr const char* kName = "bwd.force0_dh";
+  __device__ float4 a4(int, int r, int k) const { return ld4(T + size_t(r) * W + k); }
+  __device__ void epi4(int, int r, int n, float4 acc) const {
+    float* o = dh + size_t(r) * H + n;
+    st4(o, add4(ld4(o), acc));
+  }
   RowSet rows;
   int K, Ncols, H, W;
   const float* T;
@@ -514,6 +782,10 @@ struct F0Dh {  // dh += T Wf0[:H]^T  (node rows per head)
 // ---- encoder layer backward problems (shared weights, identity rows)
 struct L1Prob {  // dvz1 = (dh nW2^T) * silu'(vz1)
   static constexpr const char* kName = "bwd.node_dvz1";
+  __device__ float4 a4(int, int r, int k) const { return ld4(dh + size_t(r) * H + k); }
+  __device__ void epi4(int, int r, int n, float4 acc) const {
+    st4(dvz1 + size_t(r) * H + n, mul4(acc, sgrad4(ld4(vz1 + size_t(r) * H + n))));
+  }
   RowSet rows;
   int K, Ncols, H;
   const float *dh, *W, *vz1;
@@ -526,6 +798,10 @@ struct L1Prob {  // dvz1 = (dh nW2^T) * silu'(vz1)
 };
 struct L2Prob {  // [g_nW2; g_nb2] = [silu(vz1), 1]^T dh
   static constexpr const char* kName = "bwd.node_w2grad";
+  static constexpr int kBias = 1;
+  static constexpr bool kTc = true;
+  __device__ float4 x4(int, int r, int m) const { return silu4(ld4(vz1 + size_t(r) * H + m)); }
+  __device__ float4 y4(int, int r, int n) const { return ld4(dh + size_t(r) * H + n); }
   RowSet rows;
   int K, Ncols, H;
   const float *vz1, *dh;
@@ -536,6 +812,12 @@ struct L2Prob {  // [g_nW2; g_nb2] = [silu(vz1), 1]^T dh
 };
 struct L3Prob {  // [g_nW1; g_nb1] = [h, agg, 1]^T dvz1
   static constexpr const char* kName = "bwd.node_w1grad";
+  static constexpr int kBias = 1;
+  static constexpr bool kTc = true;
+  __device__ float4 x4(int, int r, int m) const {
+    return m < H ? ld4(h + size_t(r) * H + m) : ld4(agg + size_t(r) * H + m - H);
+  }
+  __device__ float4 y4(int, int r, int n) const { return ld4(dvz1 + size_t(r) * H + n); }
   RowSet rows;
   int K, Ncols, H;
   const float *h, *agg, *dvz1;
@@ -548,6 +830,11 @@ struct L3Prob {  // [g_nW1; g_nb1] = [h, agg, 1]^T dvz1
 };
 struct L4Prob {  // dv = dvz1 nW1^T ; dh2 = dh + dv[:, :H] ; dagg = dv[:, H:]
   static constexpr const char* kName = "bwd.node_dv";
+  __device__ float4 a4(int, int r, int k) const { return ld4(dvz1 + size_t(r) * H + k); }
+  __device__ void epi4(int, int r, int n, float4 acc) const {
+    if (n < H) st4(dh2 + size_t(r) * H + n, add4(ld4(dh + size_t(r) * H + n), acc));
+    else st4(dagg + size_t(r) * H + n - H, acc);
+  }
   RowSet rows;
   int K, Ncols, H;
   const float *dvz1, *W, *dh;
@@ -561,12 +848,21 @@ struct L4Prob {  // dv = dvz1 nW1^T ; dh2 = dh + dv[:, :H] ; dagg = dv[:, H:]
 };
 struct L6Prob {  // [g_eW2; g_eb2] = [silu(z1), 1]^T dz2   (E rows)
   static constexpr const char* kName = "bwd.edge_w2grad";
+  static constexpr int kBias = 1;
+  static constexpr bool kTc = true;
+  __device__ float4 x4(int, int e, int m) const {
+    if (a1s) return ld4(a1s + size_t(e) * H + m);
+    return silu4(pre4(ld4(P + size_t(dst[e]) * 2 * H + m), ld4(P + size_t(src[e]) * 2 * H + H + m), geo[e].w,
+                      ld4(wd + m), ld4(b1 + m)));
+  }
+  __device__ float4 y4(int, int e, int n) const { return ld4(dz2 + size_t(e) * H + n); }
   RowSet rows;
   int K, Ncols, H;
   const float *P, *wd, *b1, *dz2;
   const int *dst, *src;
   const float4* geo;
   float* G;
+  const float* a1s;  // a1 materialised by the forward producer (nullable)
   __device__ float a(int, int e, int k) const {
     return k < H ? silu(z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, k)) : 1.f;
   }
@@ -575,6 +871,23 @@ struct L6Prob {  // [g_eW2; g_eb2] = [silu(z1), 1]^T dz2   (E rows)
 };
 struct L7Prob {  // dz1 = (dz2 eW2^T) * silu'(z1)
   static constexpr const char* kName = "bwd.edge_dz1_gemm";
+  struct RC {
+    int d, s;
+    float w;
+  };
+  __device__ RC rctx(int, int e) const { return RC{dst[e], src[e], geo[e].w}; }
+  __device__ float4 a4c(int, int e, const RC&, int k) const { return ld4(dz2 + size_t(e) * H + k); }
+  __device__ void epi4c(int, int e, const RC& r, int n, float4 acc) const {
+    const float4 z = pre4(ld4(P + size_t(r.d) * 2 * H + n), ld4(P + size_t(r.s) * 2 * H + H + n), r.w, ld4(wd + n),
+                          ld4(b1 + n));
+    st4(dz1 + size_t(e) * H + n, mul4(acc, sgrad4(z)));
+  }
+  __device__ float4 a4(int, int e, int k) const { return ld4(dz2 + size_t(e) * H + k); }
+  __device__ void epi4(int, int e, int n, float4 acc) const {
+    const float4 z = pre4(ld4(P + size_t(dst[e]) * 2 * H + n), ld4(P + size_t(src[e]) * 2 * H + H + n), geo[e].w,
+                          ld4(wd + n), ld4(b1 + n));
+    st4(dz1 + size_t(e) * H + n, mul4(acc, sgrad4(z)));
+  }
   RowSet rows;
   int K, Ncols, H;
   const float *dz2, *W, *P, *wd, *b1;
@@ -589,6 +902,8 @@ struct L7Prob {  // dz1 = (dz2 eW2^T) * silu'(z1)
 };
 struct L9Prob {  // [g_W1[2H]; g_b1] = [d2, 1]^T dz1   (E rows)
   static constexpr const char* kName = "bwd.edge_w1tail_grad";
+  static constexpr int kBias = 0;
+  static constexpr bool kTc = false;
   RowSet rows;
   int K, Ncols, H;
   const float4* geo;
@@ -600,6 +915,10 @@ struct L9Prob {  // [g_W1[2H]; g_b1] = [d2, 1]^T dz1   (E rows)
 };
 struct L10Prob {  // g_W1a = h^T S_dst, g_W1b = h^T S_src
   static constexpr const char* kName = "bwd.edge_w1ab_grad";
+  static constexpr int kBias = 0;
+  static constexpr bool kTc = true;
+  __device__ float4 x4(int, int r, int m) const { return ld4(h + size_t(r) * H + m); }
+  __device__ float4 y4(int, int r, int n) const { return ld4(S + size_t(r) * 2 * H + n); }
   RowSet rows;
   int K, Ncols, H;
   const float *h, *S;
@@ -613,6 +932,11 @@ struct L10Prob {  // g_W1a = h^T S_dst, g_W1b = h^T S_src
 };
 struct L11Prob {  // dh2 += S_dst W1a^T + S_src W1b^T
   static constexpr const char* kName = "bwd.edge_dh_gemm";
+  __device__ float4 a4(int, int r, int k) const { return ld4(S + size_t(r) * 2 * H + k); }
+  __device__ void epi4(int, int r, int n, float4 acc) const {
+    float* o = dh2 + size_t(r) * H + n;
+    st4(o, add4(ld4(o), acc));
+  }
   RowSet rows;
   int K, Ncols, H;
   const float *S, *W1;
@@ -717,7 +1041,7 @@ void launch_backward(Ctx& c, cudaStream_t st) {
       EGradProb gq{graph_rows_by_head(c), in + 1, out, H, W, i, c.pooled,
                    i ? c.ez + size_t(i - 1) * GW : nullptr, dz, ldz,
                    HeadG{c.head_grads(), c.PH, c.head_off("energy.W" + std::to_string(i))}};
-      atb(gq, c, c.nsplit_graph, st);
+      atb(gq, c, c.nsplit_graph, st, c.Gc);
       float* nxt = i ? bufs[i & 1] : c.dpooled;
       EDxProb dq{graph_rows_by_head(c), out, in, W, H, dz, i ? c.ez + size_t(i - 1) * GW : nullptr, ldz,
                  HeadW{c.head_params(), c.PH, c.head_off("energy.W" + std::to_string(i))}, nxt, i ? W : H,
@@ -746,8 +1070,9 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     for (int i = D - 1; i >= 1; --i) {
       const int out = i == D - 1 ? 1 : W;
       FGradProb gq{edge_rows_by_head(c), W + 1, out, H, W, i, c.Ec, c.Qf, c.zf, c.dist, dz, ldz, c.edge_dst,
-                   c.edge_src, Wd, B0, HeadG{c.head_grads(), c.PH, c.head_off("force.W" + std::to_string(i))}};
-      atb(gq, c, c.nsplit_edge, st);
+                   c.edge_src, Wd, B0, HeadG{c.head_grads(), c.PH, c.head_off("force.W" + std::to_string(i))},
+                   c.store_af0 ? c.af0 : nullptr};
+      atb(gq, c, c.nsplit_edge, st, c.Ec);
       float* nxt = bufs[i & 1];
       FDxProb dq{edge_rows_by_head(c), out, W, H, W, i, c.Ec, c.Qf, c.zf, c.dist, dz, ldz, c.edge_dst, c.edge_src,
                  Wd, B0, HeadW{c.head_params(), c.PH, c.head_off("force.W" + std::to_string(i))}, nxt};
@@ -762,9 +1087,9 @@ void launch_backward(Ctx& c, cudaStream_t st) {
                                                                             1);
     }
     F0NodeGrad ng{node_rows_by_head(c), H, W, H, W, hL, c.Sbuf, HeadG{c.head_grads(), c.PH, wf0}};
-    atb(ng, c, c.nsplit_node, st);
+    atb(ng, c, c.nsplit_node, st, c.Nc);
     F0EdgeGrad eg{edge_rows_by_head(c), 2, W, H, W, c.dist, dz, HeadG{c.head_grads(), c.PH, wf0 + size_t(H) * W}};
-    atb(eg, c, c.nsplit_edge, st);
+    atb(eg, c, c.nsplit_edge, st, c.Ec);
     F0Dh dhq{node_rows_by_head(c), W, H, H, W, c.Sbuf, HeadW{c.head_params(), c.PH, wf0}, c.dh};
     ab(dhq, c.Nc, c.S, st, sm, c);
   }
@@ -788,11 +1113,11 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     }
     {
       L2Prob q{node_rows(c), H + 1, H, H, vz1, dh, c.grads + c.shared_off(p + "node.W2")};
-      atb(q, c, c.nsplit_node, st);
+      atb(q, c, c.nsplit_node, st, c.Nc);
     }
     {
       L3Prob q{node_rows(c), 2 * H + 1, H, H, h, agg, c.dvz1, c.grads + c.shared_off(p + "node.W1")};
-      atb(q, c, c.nsplit_node, st);
+      atb(q, c, c.nsplit_node, st, c.Nc);
     }
     {
       L4Prob q{node_rows(c), H, 2 * H, H, c.dvz1, c.params + c.shared_off(p + "node.W1"), dh, dh2, c.dagg};
@@ -804,8 +1129,8 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     }
     {
       L6Prob q{edge_rows(c), H + 1, H, H, P, wd, b1, c.dzA, c.edge_dst, c.edge_src, c.geo,
-               c.grads + c.shared_off(p + "edge.W2")};
-      atb(q, c, c.nsplit_edge, st);
+               c.grads + c.shared_off(p + "edge.W2"), c.store_a1 ? c.a1 + size_t(l) * EH : nullptr};
+      atb(q, c, c.nsplit_edge, st, c.Ec);
     }
     {
       L7Prob q{edge_rows(c), H, H, H, c.dzA, c.params + c.shared_off(p + "edge.W2"), P, wd, b1, c.edge_dst,
@@ -819,11 +1144,11 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     }
     {
       L9Prob q{edge_rows(c), 2, H, H, c.geo, c.dzB, geW1 + size_t(2) * H * H};
-      atb(q, c, c.nsplit_edge, st);
+      atb(q, c, c.nsplit_edge, st, c.Ec);
     }
     {
       L10Prob q{node_rows(c), H, 2 * H, H, h, c.Sbuf, geW1};
-      atb(q, c, c.nsplit_node, st);
+      atb(q, c, c.nsplit_node, st, c.Nc);
     }
     {
       L11Prob q{node_rows(c), 2 * H, H, H, c.Sbuf, eW1, dh2};

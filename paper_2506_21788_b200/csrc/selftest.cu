@@ -1,0 +1,98 @@
+// selftest.cu -- direct checks of the tcgen05 engines on plain matrices
+// (hmtl_selftest_gemm, used by tests/test_gpu_tc.py; not on the training path).
+#include <cstring>
+#include <string>
+
+#include "ctx.cuh"
+#include "tc.cuh"
+
+namespace hmtl_b200 {
+namespace {
+
+// row GEMM: C[r][n] = sum_k X[r][k] * B[k][n]
+struct StRow {
+  RowSet rows;
+  int K, Ncols;
+  const float* bimg;
+  size_t bimg_seg;
+  const float* X;
+  float* C;
+  struct RC {};
+  __device__ RC rctx(int, int) const { return RC{}; }
+  __device__ float4 a4(int, int r, const RC&, int k) const {
+    return *reinterpret_cast<const float4*>(X + size_t(r) * K + k);
+  }
+  __device__ void epi4(int, int r, const RC&, int n, float4 acc) const {
+    *reinterpret_cast<float4*>(C + size_t(r) * Ncols + n) = acc;
+  }
+};
+// reduce GEMM: C[m][n] = sum_r X[r][m] * Y[r][n]
+struct StRed {
+  RowSet rows;
+  int M, Ncols, colsum;
+  const float *X, *Y;
+  float* C;
+  __device__ float4 x4(int, int r, int m) const { return *reinterpret_cast<const float4*>(X + size_t(r) * M + m); }
+  __device__ float4 y4(int, int r, int n) const {
+    return *reinterpret_cast<const float4*>(Y + size_t(r) * Ncols + n);
+  }
+  __device__ void store(int, int m, int n, float v) const { C[size_t(m) * Ncols + n] = v; }
+};
+
+__global__ void st_bimg(const float* B, int K, int N, float* out) {  // B is [K][N]
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < K * N; t += gridDim.x * blockDim.x) {
+    const int n = t % N, k = t / N;
+    const float x = B[size_t(k) * N + n], h = tc::tf32_hi(x);
+    const int ch = k / tc::KC, g = (k % tc::KC) / 4, q = k % 4;
+    float* o = out + size_t(ch) * 2 * tc::KC * N;
+    o[(size_t(g) * N + n) * 4 + q] = h;
+    o[size_t(tc::KC) * N + (size_t(g) * N + n) * 4 + q] = x - h;
+  }
+}
+
+}  // namespace
+}  // namespace hmtl_b200
+
+using namespace hmtl_b200;
+
+extern "C" int hmtl_selftest_gemm(int mode, int variant, int rows, int K, int N, const float* X, const float* Y,
+                                  float* C) {
+  cudaSetDevice(0);
+  float *dX, *dY, *dC, *img, *part;
+  int* dcnt;
+  const size_t nx = size_t(rows) * K, ny = mode == 0 ? size_t(K) * N : size_t(rows) * N;
+  const size_t nc = mode == 0 ? size_t(rows) * N : size_t(K + 1) * N;
+  HMTL_CUDA(cudaMalloc(&dX, nx * 4));
+  HMTL_CUDA(cudaMalloc(&dY, ny * 4));
+  HMTL_CUDA(cudaMalloc(&dC, nc * 4));
+  HMTL_CUDA(cudaMalloc(&img, 2 * size_t(K) * N * 4));
+  HMTL_CUDA(cudaMalloc(&part, size_t(64) * (K + 1) * N * 4));
+  HMTL_CUDA(cudaMalloc(&dcnt, 4));
+  cudaMemcpy(dX, X, nx * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dY, Y, ny * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dcnt, &rows, 4, cudaMemcpyHostToDevice);
+  cudaMemset(dC, 0, nc * 4);
+  (void)variant;
+  RowSet rs;
+  rs.count = dcnt;
+  if (mode == 0) {
+    st_bimg<<<64, 256>>>(dY, K, N, img);
+    StRow p{rs, K, N, img, 0, dX, dC};
+    const tc::RowPlan plan = tc::row_plan(K, N);
+    cudaFuncSetAttribute(tc::tc_row_kernel<StRow>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan.smem));
+    tc::tc_row_kernel<StRow><<<(rows + 127) / 128, tc::kRowThreads, plan.smem>>>(p, plan);
+  } else {
+    StRed p{rs, K, N, 0, dX, dY, dC};
+    const int ns = 4;
+    const size_t smem = tc::tc_red_smem(N);
+    cudaFuncSetAttribute(tc::tc_red_kernel<StRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    dim3 grid((K + 127) / 128, ns, 1);
+    tc::tc_red_kernel<StRed><<<grid, tc::kRedThreads, smem>>>(p, part, ns, tc::red_stages(N));
+    tc::tc_red_reduce<StRed><<<64, 256>>>(p, part, ns);
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) cudaMemcpy(C, dC, (mode == 0 ? nc : size_t(K) * N) * 4, cudaMemcpyDeviceToHost);
+  cudaFree(dX), cudaFree(dY), cudaFree(dC), cudaFree(img), cudaFree(part), cudaFree(dcnt);
+  if (e != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("selftest: ") + cudaGetErrorString(e));
+  return 0;
+}

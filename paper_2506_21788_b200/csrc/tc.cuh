@@ -1,0 +1,545 @@
+// tc.cuh -- tcgen05 (5th-gen tensor core) GEMM engine for the FP32 path.
+//
+// Precision: kind::tf32 with the 3xTF32 split (x = hi + lo, hi = x with the
+// low 13 mantissa bits cleared; D += A_lo*B_hi + A_hi*B_lo + A_hi*B_hi,
+// FP32 accumulation in TMEM) -> ~FP32 accuracy (error ~2^-22 |a||b|), which
+// keeps the rel 1e-4 parity bar of the FP32 path.
+//
+// Operands live in shared memory in the canonical K-major SWIZZLE_NONE UMMA
+// layout: a K-chunk of 32 values is 8 "k-groups" of 4 fp32 (16 B); group g of
+// an R-row operand starts at g*R*16 B and row r sits at +r*16 B.  One MMA
+// (K = 8) covers two k-groups: LBO = R*16 B (k-group stride), SBO = 128 B
+// (8-row core-matrix stride).  Producer threads write A rows (thread t = row t,
+// 16 B stores, conflict-free); B comes from a pre-split global image with the
+// same byte layout (plain coalesced 16 B copies, L2-resident, shared by all CTAs).
+//
+// Two engines, both templated on a problem functor:
+//   tc_row_kernel : C[row, n] = epi(sum_k A(row,k) B(k,n)), 128-row tiles of a
+//                   RowSet (tiles never straddle head segments), N <= 256.
+//   tc_red_kernel : C_seg[m, n] = sum_rows A(row,m) B(row,n) for weight
+//                   gradients: M-tile 128 features, the ROWS are the reduction
+//                   dim (K), statically split over CTAs; fixed-order reduce after.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace hmtl_b200 {
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {  // warp-wide
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {  // warp-wide
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// 32 consecutive TMEM columns of this warp's 32 lanes -> 32 registers / thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// K-major, SWIZZLE_NONE shared-memory matrix descriptor (sm100 "version 1").
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46);
+}
+// instruction descriptor: kind::tf32, D f32, A/B tf32 K-major, M = 128, N
+__host__ __device__ constexpr uint32_t idesc_tf32(int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+
+// write 4 consecutive k-values of row r into the hi/lo chunk images
+__device__ __forceinline__ void put4(float* hi, float* lo, int R, int g, int r, float4 v) {
+  float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+  float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+  reinterpret_cast<float4*>(hi)[g * R + r] = h;
+  reinterpret_cast<float4*>(lo)[g * R + r] = l;
+}
+
+constexpr int KC = 32;  // k values per chunk (4 MMAs of K=8)
+
+// issue the 3xTF32 MMAs of one chunk (single thread)
+__device__ __forceinline__ void issue_chunk(uint32_t tmem, const float* a_hi, const float* a_lo, int RA,
+                                            const float* b_hi, const float* b_lo, int RB, uint32_t idesc,
+                                            bool first) {
+  const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+  const uint32_t la = RA * 16, lb = RB * 16;
+#pragma unroll
+  for (int j = 0; j < KC / 8; ++j) {
+    const uint32_t oa = j * 2 * RA * 16, ob = j * 2 * RB * 16;
+    const uint64_t dah = sdesc(ah + oa, la, 128), dal = sdesc(al + oa, la, 128);
+    const uint64_t dbh = sdesc(bh + ob, lb, 128), dbl = sdesc(bl + ob, lb, 128);
+    mma_tf32(tmem, dal, dbh, idesc, (first && j == 0) ? 0u : 1u);
+    mma_tf32(tmem, dah, dbl, idesc, 1u);
+    mma_tf32(tmem, dah, dbh, idesc, 1u);
+  }
+}
+
+// B images (weights) are built per problem by bimg_prob_kernel (model.cu):
+// per 32-k chunk c, [hi | lo], each [8 k-groups][N rows][4] fp32.
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// ================================================================ row GEMM
+// Warp-specialised, persistent.  Warps 0-3 produce A (8 lanes per row ->
+// coalesced 128 B row segments; the per-row gather context is loaded once per
+// tile, not per K-chunk) into a ring of smem stages; warp 4 allocates TMEM and
+// one lane issues the 3xTF32 MMAs; warps 5-8 drain a double-buffered TMEM
+// accumulator through the epilogue (warp w reads TMEM lanes 32*(w%4)..+31,
+// transposes each 32x32 slab through padded smem so stores are row-coalesced),
+// overlapping tile t's epilogue with tile t+1's MMAs.  When the whole B image
+// (hi+lo, K x Nt) fits next to two A stages it is loaded once per CTA
+// ("resident"), otherwise each stage carries its B slice.
+// P must provide: RowSet rows; int K, Ncols; const float* bimg; size_t bimg_seg;
+//   typename P::RC rctx(int seg, int row) const;                    // per-row gather context
+//   float4 a4(int seg, int row, const RC&, int k) const;           // A(row, k..k+3)
+//   void epi4(int seg, int row, const RC&, int n, float4 acc) const;  // C(row, n..n+3)
+constexpr int kMaxStages = 4;
+constexpr int kRowThreads = 288;
+constexpr size_t kSmemLimit = 227 * 1024;
+constexpr int kEpiLd = 36;  // padded row stride (floats) of the epilogue transpose slab
+constexpr size_t kEpiBytes = size_t(128) * kEpiLd * 4;
+
+struct RowPlan {
+  int Nt, stages, resident;
+  size_t a_stage, b_stage, b_res, smem;
+};
+inline RowPlan row_plan(int K, int Nt) {
+  RowPlan r;
+  r.Nt = Nt;
+  r.a_stage = size_t(2 * 128 * KC) * 4;  // hi + lo
+  const size_t b_chunk = size_t(2 * Nt * KC) * 4;
+  const size_t b_all = b_chunk * (K / KC);
+  r.resident = (b_all + 2 * r.a_stage + kEpiBytes + 256 <= kSmemLimit) ? 1 : 0;
+  r.b_res = r.resident ? b_all : 0;
+  r.b_stage = r.resident ? 0 : b_chunk;
+  const size_t per = r.a_stage + r.b_stage;
+  int st = int((kSmemLimit - 256 - kEpiBytes - r.b_res) / per);
+  r.stages = st < 2 ? 2 : (st > kMaxStages ? kMaxStages : st);
+  r.smem = r.b_res + r.stages * per + kEpiBytes + 128;
+  return r;
+}
+
+template <class P>
+__global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan plan) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int Nt = plan.Nt, kStages = plan.stages;
+  const size_t SB = plan.a_stage + plan.b_stage;
+  float* bres = reinterpret_cast<float*>(smem_raw);  // resident B (hi/lo per chunk)
+  uint8_t* stages = smem_raw + plan.b_res;
+  float* epi_smem = reinterpret_cast<float*>(stages + kStages * SB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kStages * SB + kEpiBytes);
+  uint64_t* full = bars;                        // [kStages], count 128
+  uint64_t* empty = bars + kStages;             // [kStages], count 1 (MMA commit)
+  uint64_t* accfull = bars + 2 * kStages;       // [2], count 1
+  uint64_t* accempty = bars + 2 * kStages + 2;  // [2], count 128
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t acc_cols = Nt <= 32 ? 32 : (Nt <= 64 ? 64 : (Nt <= 128 ? 128 : 256));
+  if (warp == 4) tmem_alloc(tmem_slot, 2 * acc_cols);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accfull[b], 1);
+      mbar_init(&accempty[b], 128);
+    }
+    fence_mbar_init();
+  }
+  int mt_seg[kMaxSlots + 1];
+  int total_m = 0;
+  for (int s = 0; s < p.rows.nseg; ++s) {
+    mt_seg[s] = total_m;
+    total_m += (p.rows.end(s) - p.rows.begin(s) + 127) / 128;
+  }
+  mt_seg[p.rows.nseg] = total_m;
+  const int ntn = p.Ncols / Nt;
+  const int total = total_m * ntn;
+  const int nchunks = p.K / KC;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {  // ---------------------------------------------- producers
+    int stage = 0;
+    uint32_t phase = 0;
+    int res_key = -1;  // (seg, n0) of the resident B image
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const int tm = t / ntn, n0 = (t % ntn) * Nt;
+      int seg = 0;
+      while (tm >= mt_seg[seg + 1]) ++seg;
+      const int g8 = lane & 7, rbase = warp * 32 + (lane >> 3);
+      int rows_it[8];
+      typename P::RC rc[8];
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int v = p.rows.begin(seg) + (tm - mt_seg[seg]) * 128 + rbase + it * 4;
+        rows_it[it] = v < p.rows.end(seg) ? p.rows.row(v) : -1;
+        if (rows_it[it] >= 0) rc[it] = p.rctx(seg, rows_it[it]);
+      }
+      const float4* bsrc = reinterpret_cast<const float4*>(p.bimg + seg * p.bimg_seg);
+      if (plan.resident && res_key != seg * 4096 + n0) {
+        // (re)load the whole B slice for (seg, n0): wait until every stage is idle
+        // is unnecessary -- MMAs only read B after `full`, and the previous tile's
+        // MMAs completed before its epilogue; guard with a CTA-wide named barrier.
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (res_key >= 0) {
+          // drain: the last chunk of the previous tile must have been consumed
+          // (its `empty` phase) before B is overwritten
+          int ps = stage == 0 ? kStages - 1 : stage - 1;
+          uint32_t pph = stage == 0 ? (phase ^ 1) : phase;
+          mbar_wait(&empty[ps], pph);
+        }
+        float4* bd = reinterpret_cast<float4*>(bres);
+        for (int c = 0; c < nchunks; ++c) {
+          const float4* bc = bsrc + size_t(c) * 2 * KC * p.Ncols / 4;
+          for (int i = tid; i < 2 * (KC / 4) * Nt; i += 128) {
+            const int part = i / ((KC / 4) * Nt), rem = i % ((KC / 4) * Nt);
+            const int g = rem / Nt, n = rem % Nt;
+            bd[size_t(c) * 2 * (KC / 4) * Nt + i] = bc[size_t(part) * (KC / 4) * p.Ncols + size_t(g) * p.Ncols + n0 + n];
+          }
+        }
+        fence_proxy_async();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        res_key = seg * 4096 + n0;
+      }
+      for (int c = 0; c < nchunks; ++c) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        float* a_hi = reinterpret_cast<float*>(stages + stage * SB);
+        float* a_lo = a_hi + 128 * KC;
+        float4 x[8];
+#pragma unroll
+        for (int it = 0; it < 8; ++it)
+          x[it] = rows_it[it] >= 0 ? p.a4(seg, rows_it[it], rc[it], c * KC + 4 * g8) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int it = 0; it < 8; ++it) put4(a_hi, a_lo, 128, g8, rbase + it * 4, x[it]);
+        if (!plan.resident) {
+          float4* b_st = reinterpret_cast<float4*>(a_lo + 128 * KC);
+          const float4* bc = bsrc + size_t(c) * 2 * KC * p.Ncols / 4;
+          for (int i = tid; i < 2 * (KC / 4) * Nt; i += 128) {
+            const int part = i / ((KC / 4) * Nt), rem = i % ((KC / 4) * Nt);
+            const int g = rem / Nt, n = rem % Nt;
+            b_st[i] = bc[size_t(part) * (KC / 4) * p.Ncols + size_t(g) * p.Ncols + n0 + n];
+          }
+        }
+        fence_proxy_async();
+        mbar_arrive(&full[stage]);
+        if (++stage == kStages) stage = 0, phase ^= 1;
+      }
+    }
+  } else if (warp == 4) {  // ---------------------------------------- MMA issuer
+    int stage = 0;
+    uint32_t phase = 0;
+    int ab = 0;
+    uint32_t aphase = 0;
+    const uint32_t idesc = idesc_tf32(Nt);
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      mbar_wait(&accempty[ab], aphase ^ 1);
+      tc_fence_after();
+      for (int c = 0; c < nchunks; ++c) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          float* a_hi = reinterpret_cast<float*>(stages + stage * SB);
+          float* a_lo = a_hi + 128 * KC;
+          float* b_hi = plan.resident ? bres + size_t(c) * 2 * KC * Nt : a_lo + 128 * KC;
+          float* b_lo = b_hi + Nt * KC;
+          issue_chunk(tmem + ab * acc_cols, a_hi, a_lo, 128, b_hi, b_lo, Nt, idesc, c == 0);
+          mma_commit(&empty[stage]);
+          if (c == nchunks - 1) mma_commit(&accfull[ab]);
+        }
+        __syncwarp();
+        if (++stage == kStages) stage = 0, phase ^= 1;
+      }
+      if (++ab == 2) ab = 0, aphase ^= 1;
+    }
+  } else {  // ------------------------------------------------------- epilogue
+    const int q = warp & 3;
+    int ab = 0;
+    uint32_t aphase = 0;
+    float* slab = epi_smem + q * 32 * kEpiLd;  // this warp's 32 rows x 32 cols (padded)
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const int tm = t / ntn, n0 = (t % ntn) * Nt;
+      int seg = 0;
+      while (tm >= mt_seg[seg + 1]) ++seg;
+      int rows_it[8];
+      typename P::RC rc[8];
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int v = p.rows.begin(seg) + (tm - mt_seg[seg]) * 128 + q * 32 + it * 4 + (lane >> 3);
+        rows_it[it] = v < p.rows.end(seg) ? p.rows.row(v) : -1;
+        if (rows_it[it] >= 0) rc[it] = p.rctx(seg, rows_it[it]);
+      }
+      mbar_wait(&accfull[ab], aphase);
+      tc_fence_after();
+      for (int j = 0; j < Nt; j += 32) {
+        float acc[32];
+        __syncwarp();
+        tmem_ld32(tmem + ab * acc_cols + (uint32_t(q * 32) << 16) + j, acc);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          reinterpret_cast<float4*>(slab + lane * kEpiLd)[i] =
+              make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int rl = it * 4 + (lane >> 3), c4 = (lane & 7) * 4;
+          const float4 a = reinterpret_cast<const float4*>(slab + rl * kEpiLd)[lane & 7];
+          if (rows_it[it] >= 0) p.epi4(seg, rows_it[it], rc[it], n0 + j + c4, a);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&accempty[ab]);
+      if (++ab == 2) ab = 0, aphase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) tmem_dealloc(tmem, 2 * acc_cols);
+}
+
+// ================================================================ reduce GEMM
+// Weight gradients C_seg[m, n] = sum over rows r of segment seg of X(r, m) Y(r, n)
+// with X, Y ROW-MAJOR per row (features contiguous).  K-chunk = 32 rows.  A
+// producer lane loads a 4-row x 4-feature block (4 coalesced float4 row
+// segments), transposes it in registers, and stores 4 k-values per feature
+// into the K-major SWIZZLE_NONE layout (lane-rotated store order ->
+// conflict-free).  CTA (mtile, split, seg) owns chunks split, split+nsplit, ...
+// (static -> the fixed-order reduce is deterministic).  Warps 0-3 produce
+// (warp w = rows 8w..8w+7 of the chunk), warp 4 issues MMAs; the producers run
+// the epilogue.  If p.colsum, m-tile 0 also accumulates sum_rows Y(r, n).
+// P must provide: RowSet rows; int M, Ncols, colsum;
+//   float4 x4(int seg, int row, int m) const;  float4 y4(int seg, int row, int n) const;
+// Output partial: [seg][split][Ncols][M + colsum] (transposed: coalesced stores).
+constexpr int kRedThreads = 160;
+__host__ __device__ inline size_t red_stage_bytes(int N) { return size_t(2 * 128 * KC + 2 * N * KC) * 4; }
+inline int red_stages(int N) {
+  int s = int((kSmemLimit - 2048 - 8192) / red_stage_bytes(N));
+  return s < 2 ? 2 : (s > kMaxStages ? kMaxStages : s);
+}
+inline size_t tc_red_smem(int N) { return red_stages(N) * red_stage_bytes(N) + 8192 + 2048; }
+
+__device__ __forceinline__ float4 col4(const float4* v, int j) {  // column j of a 4x4 block
+  return j == 0 ? make_float4(v[0].x, v[1].x, v[2].x, v[3].x)
+       : j == 1 ? make_float4(v[0].y, v[1].y, v[2].y, v[3].y)
+       : j == 2 ? make_float4(v[0].z, v[1].z, v[2].z, v[3].z)
+                : make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
+}
+
+template <class P>
+__global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __restrict__ partial, int nsplit,
+                                                                int kStages) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int N = p.Ncols;
+  const size_t SB = red_stage_bytes(N);
+  float* csum_smem = reinterpret_cast<float*>(smem_raw + kStages * SB);  // [4 warps][N]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + kStages * SB + 8192);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages;
+  uint64_t* accfull = bars + 2 * kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int mtile = blockIdx.x, split = blockIdx.y, seg = blockIdx.z;
+  const uint32_t acc_cols = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
+  if (warp == 4) tmem_alloc(tmem_slot, acc_cols);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&accfull[0], 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int rb = p.rows.begin(seg), re = p.rows.end(seg);
+  const int nchunks = (re - rb + KC - 1) / KC;
+  int my_chunks = 0;
+  for (int c = split; c < nchunks; c += nsplit) ++my_chunks;
+  const int Mo = p.M + (p.colsum ? 1 : 0);
+  float* out = partial + (size_t(seg) * nsplit + split) * size_t(Mo) * N;
+  const int m0 = mtile * 128;
+  const int Mt = p.M - m0 < 128 ? p.M - m0 : 128;  // features of this m-tile (mult of 4)
+  const bool do_colsum = p.colsum && mtile == 0;
+
+  if (warp < 4) {
+    float4 cs[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+    int stage = 0;
+    uint32_t phase = 0;
+    const int f = lane * 4;
+    for (int c = split; c < nchunks; c += nsplit) {
+      // this warp's 8 rows of the chunk; lane j < 8 resolves row j, broadcast by shuffle
+      const int vj = rb + c * KC + warp * 8 + (lane & 7);
+      const int rj = vj < re ? p.rows.row(vj) : -1;
+      int rows[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) rows[j] = __shfl_sync(0xffffffffu, rj, j);
+      float4 xa[8], yb[2][8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        xa[j] = (rows[j] >= 0 && f < Mt) ? p.x4(seg, rows[j], m0 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int n = f + 128 * u;
+          yb[u][j] = (rows[j] >= 0 && n < N) ? p.y4(seg, rows[j], n) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      if (do_colsum)
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            cs[u] = make_float4(cs[u].x + yb[u][j].x, cs[u].y + yb[u][j].y, cs[u].z + yb[u][j].z,
+                                cs[u].w + yb[u][j].w);
+      mbar_wait(&empty[stage], phase ^ 1);
+      float* a_hi = reinterpret_cast<float*>(smem_raw + stage * SB);
+      float* a_lo = a_hi + 128 * KC;
+      float* b_hi = a_lo + 128 * KC;
+      float* b_lo = b_hi + N * KC;
+#pragma unroll
+      for (int qd = 0; qd < 2; ++qd) {  // row quads of this warp: k-group g = 2*warp + qd
+        const int g = 2 * warp + qd;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int jj = (i + lane) & 3;
+          put4(a_hi, a_lo, 128, g, f + jj, col4(&xa[4 * qd], jj));
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            if (f + 128 * u < N) put4(b_hi, b_lo, N, g, f + 128 * u + jj, col4(&yb[u][4 * qd], jj));
+        }
+      }
+      fence_proxy_async();
+      mbar_arrive(&full[stage]);
+      if (++stage == kStages) stage = 0, phase ^= 1;
+    }
+    if (do_colsum) {  // per-warp partial column sums -> fixed-order combine below
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (f + 128 * u < N) *reinterpret_cast<float4*>(csum_smem + warp * N + f + 128 * u) = cs[u];
+    }
+    // epilogue: TMEM lane = feature m0 + tid; the partial is stored transposed ([n][m])
+    if (my_chunks > 0) {
+      mbar_wait(&accfull[0], 0);
+      tc_fence_after();
+    }
+    for (int n0 = 0; n0 < N; n0 += 32) {
+      float acc[32];
+      __syncwarp();
+      tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + n0, acc);
+      if (tid < Mt) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (n0 + i < N) out[size_t(n0 + i) * Mo + m0 + tid] = my_chunks ? acc[i] : 0.f;
+      }
+    }
+    if (do_colsum) {
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      for (int n = tid; n < N; n += 128) {
+        const float v = ((csum_smem[n] + csum_smem[N + n]) + csum_smem[2 * N + n]) + csum_smem[3 * N + n];
+        out[size_t(n) * Mo + p.M] = v;
+      }
+    }
+  } else {  // warp 4: MMA issuer
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t idesc = idesc_tf32(N);
+    int i = 0;
+    for (int c = split; c < nchunks; c += nsplit, ++i) {
+      mbar_wait(&full[stage], phase);
+      tc_fence_after();
+      if (lane == 0) {
+        float* a_hi = reinterpret_cast<float*>(smem_raw + stage * SB);
+        float* a_lo = a_hi + 128 * KC;
+        float* b_hi = a_lo + 128 * KC;
+        float* b_lo = b_hi + N * KC;
+        issue_chunk(tmem, a_hi, a_lo, 128, b_hi, b_lo, N, idesc, i == 0);
+        mma_commit(&empty[stage]);
+        if (i == my_chunks - 1) mma_commit(&accfull[0]);
+      }
+      __syncwarp();
+      if (++stage == kStages) stage = 0, phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) tmem_dealloc(tmem, acc_cols);
+}
+
+// partial is [seg][split][n][Mo] (transposed); store C[m][n]
+template <class P>
+__global__ void tc_red_reduce(P p, const float* __restrict__ partial, int nsplit) {
+  const int Mo = p.M + (p.colsum ? 1 : 0);
+  const size_t KN = size_t(Mo) * p.Ncols;
+  const size_t total = KN * p.rows.nseg;
+  for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += size_t(gridDim.x) * blockDim.x) {
+    const int seg = int(idx / KN);
+    const size_t nm = idx % KN;
+    const float* src = partial + size_t(seg) * nsplit * KN + nm;
+    float s = 0.f;
+    for (int q = 0; q < nsplit; ++q) s += src[size_t(q) * KN];
+    p.store(seg, int(nm % Mo), int(nm / Mo), s);
+  }
+}
+
+}  // namespace tc
+}  // namespace hmtl_b200
