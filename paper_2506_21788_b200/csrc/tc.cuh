@@ -149,7 +149,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 //   float4 a4(int seg, int row, const RC&, int k) const;           // A(row, k..k+3)
 //   void epi4(int seg, int row, const RC&, int n, float4 acc) const;  // C(row, n..n+3)
 constexpr int kMaxStages = 4;
-constexpr int kRowThreads = 288;
+constexpr int kProdWarps = 8;
+constexpr int kRowThreads = (kProdWarps + 5) * 32;  // producers, 1 MMA warp, 4 epilogue warps
 constexpr size_t kSmemLimit = 227 * 1024;
 constexpr int kEpiLd = 36;  // padded row stride (floats) of the epilogue transpose slab
 constexpr size_t kEpiBytes = size_t(128) * kEpiLd * 4;
@@ -183,17 +184,18 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   uint8_t* stages = smem_raw + plan.b_res;
   float* epi_smem = reinterpret_cast<float*>(stages + kStages * SB);
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kStages * SB + kEpiBytes);
-  uint64_t* full = bars;                        // [kStages], count 128
+  uint64_t* full = bars;                        // [kStages], count = producer threads
   uint64_t* empty = bars + kStages;             // [kStages], count 1 (MMA commit)
   uint64_t* accfull = bars + 2 * kStages;       // [2], count 1
   uint64_t* accempty = bars + 2 * kStages + 2;  // [2], count 128
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t acc_cols = Nt <= 32 ? 32 : (Nt <= 64 ? 64 : (Nt <= 128 ? 128 : 256));
-  if (warp == 4) tmem_alloc(tmem_slot, 2 * acc_cols);
+  constexpr int kMmaWarp = kProdWarps, kProdThreads = kProdWarps * 32;
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, 2 * acc_cols);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 128);
+      mbar_init(&full[s], kProdThreads);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -217,32 +219,29 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 4) {  // ---------------------------------------------- producers
+  if (warp < kProdWarps) {  // ------------------------------------- producers
+    // 4 lanes per row, each lane two k-groups (32 contiguous bytes of the row):
+    // 8 consecutive rows per store instruction -> all 8 16B bank groups, no conflicts
     int stage = 0;
     uint32_t phase = 0;
     int res_key = -1;  // (seg, n0) of the resident B image
+    const int kq = lane & 3, rsub = lane >> 2;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const int tm = t / ntn, n0 = (t % ntn) * Nt;
       int seg = 0;
       while (tm >= mt_seg[seg + 1]) ++seg;
-      const int g8 = lane & 7, rbase = warp * 32 + (lane >> 3);
-      int rows_it[8];
-      typename P::RC rc[8];
+      int rows_it[2];
+      typename P::RC rc[2];
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const int v = p.rows.begin(seg) + (tm - mt_seg[seg]) * 128 + rbase + it * 4;
+      for (int it = 0; it < 2; ++it) {  // rows warp*16 + it*8 + rsub
+        const int v = p.rows.begin(seg) + (tm - mt_seg[seg]) * 128 + warp * 16 + it * 8 + rsub;
         rows_it[it] = v < p.rows.end(seg) ? p.rows.row(v) : -1;
         if (rows_it[it] >= 0) rc[it] = p.rctx(seg, rows_it[it]);
       }
       const float4* bsrc = reinterpret_cast<const float4*>(p.bimg + seg * p.bimg_seg);
       if (plan.resident && res_key != seg * 4096 + n0) {
-        // (re)load the whole B slice for (seg, n0): wait until every stage is idle
-        // is unnecessary -- MMAs only read B after `full`, and the previous tile's
-        // MMAs completed before its epilogue; guard with a CTA-wide named barrier.
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (res_key >= 0) {
-          // drain: the last chunk of the previous tile must have been consumed
-          // (its `empty` phase) before B is overwritten
+        asm volatile("bar.sync 1, %0;" ::"r"(kProdThreads) : "memory");
+        if (res_key >= 0) {  // the previous tile's last chunk must be consumed first
           int ps = stage == 0 ? kStages - 1 : stage - 1;
           uint32_t pph = stage == 0 ? (phase ^ 1) : phase;
           mbar_wait(&empty[ps], pph);
@@ -250,30 +249,35 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
         float4* bd = reinterpret_cast<float4*>(bres);
         for (int c = 0; c < nchunks; ++c) {
           const float4* bc = bsrc + size_t(c) * 2 * KC * p.Ncols / 4;
-          for (int i = tid; i < 2 * (KC / 4) * Nt; i += 128) {
+          for (int i = tid; i < 2 * (KC / 4) * Nt; i += kProdThreads) {
             const int part = i / ((KC / 4) * Nt), rem = i % ((KC / 4) * Nt);
             const int g = rem / Nt, n = rem % Nt;
             bd[size_t(c) * 2 * (KC / 4) * Nt + i] = bc[size_t(part) * (KC / 4) * p.Ncols + size_t(g) * p.Ncols + n0 + n];
           }
         }
         fence_proxy_async();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(kProdThreads) : "memory");
         res_key = seg * 4096 + n0;
       }
       for (int c = 0; c < nchunks; ++c) {
+        float4 x[2][2];  // [row it][k-group half]
+#pragma unroll
+        for (int it = 0; it < 2; ++it)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            x[it][h] = rows_it[it] >= 0 ? p.a4(seg, rows_it[it], rc[it], c * KC + 8 * kq + 4 * h)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
         mbar_wait(&empty[stage], phase ^ 1);
         float* a_hi = reinterpret_cast<float*>(stages + stage * SB);
         float* a_lo = a_hi + 128 * KC;
-        float4 x[8];
 #pragma unroll
-        for (int it = 0; it < 8; ++it)
-          x[it] = rows_it[it] >= 0 ? p.a4(seg, rows_it[it], rc[it], c * KC + 4 * g8) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int it = 0; it < 2; ++it)
 #pragma unroll
-        for (int it = 0; it < 8; ++it) put4(a_hi, a_lo, 128, g8, rbase + it * 4, x[it]);
+          for (int h = 0; h < 2; ++h) put4(a_hi, a_lo, 128, 2 * kq + h, warp * 16 + it * 8 + rsub, x[it][h]);
         if (!plan.resident) {
           float4* b_st = reinterpret_cast<float4*>(a_lo + 128 * KC);
           const float4* bc = bsrc + size_t(c) * 2 * KC * p.Ncols / 4;
-          for (int i = tid; i < 2 * (KC / 4) * Nt; i += 128) {
+          for (int i = tid; i < 2 * (KC / 4) * Nt; i += kProdThreads) {
             const int part = i / ((KC / 4) * Nt), rem = i % ((KC / 4) * Nt);
             const int g = rem / Nt, n = rem % Nt;
             b_st[i] = bc[size_t(part) * (KC / 4) * p.Ncols + size_t(g) * p.Ncols + n0 + n];
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
         if (++stage == kStages) stage = 0, phase ^= 1;
       }
     }
-  } else if (warp == 4) {  // ---------------------------------------- MMA issuer
+  } else if (warp == kMmaWarp) {  // --------------------------------- MMA issuer
     int stage = 0;
     uint32_t phase = 0;
     int ab = 0;
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) tmem_dealloc(tmem, 2 * acc_cols);
+  if (warp == kMmaWarp) tmem_dealloc(tmem, 2 * acc_cols);
 }
 
 // ================================================================ reduce GEMM
