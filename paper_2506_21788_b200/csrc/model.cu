@@ -497,6 +497,11 @@ RowSet graph_rows_by_head(Ctx& c) {
 
 }  // namespace
 
+namespace {
+__global__ void agg4_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const float* __restrict__ z2,
+                            float* __restrict__ agg, int H);
+}
+
 void launch_forward(Ctx& c, cudaStream_t st) {
   const int H = c.H, W = c.W, L = c.L, D = c.D, sm = c.sm_count;
   const size_t NH = size_t(c.Nc) * H, EH = size_t(c.Ec) * H;
@@ -525,7 +530,8 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     }
     {
       Prof pr(c, "fwd.agg_segsum", st);
-      agg_kernel<<<gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st>>>(c.hdr, c.row_ptr, z2, agg, H);
+      if (H % 4 == 0) agg4_kernel<<<gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st>>>(c.hdr, c.row_ptr, z2, agg, H);
+      else agg_kernel<<<gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st>>>(c.hdr, c.row_ptr, z2, agg, H);
     }
     {
       Node1Prob q{node_rows(c), 2 * H, H, H, h, agg, c.params + c.shared_off(p + "node.W1"),
@@ -855,7 +861,10 @@ struct L6Prob {  // [g_eW2; g_eb2] = [silu(z1), 1]^T dz2   (E rows)
     return silu4(pre4(ld4(P + size_t(dst[e]) * 2 * H + m), ld4(P + size_t(src[e]) * 2 * H + H + m), geo[e].w,
                       ld4(wd + m), ld4(b1 + m)));
   }
-  __device__ float4 y4(int, int e, int n) const { return ld4(dz2 + size_t(e) * H + n); }
+  __device__ float4 y4(int, int e, int n) const {
+    if (dagg) return mul4(ld4(dagg + size_t(dst[e]) * H + n), sgrad4(ld4(z2s + size_t(e) * H + n)));
+    return ld4(dz2 + size_t(e) * H + n);
+  }
   RowSet rows;
   int K, Ncols, H;
   const float *P, *wd, *b1, *dz2;
@@ -863,6 +872,7 @@ struct L6Prob {  // [g_eW2; g_eb2] = [silu(z1), 1]^T dz2   (E rows)
   const float4* geo;
   float* G;
   const float* a1s;  // a1 materialised by the forward producer (nullable)
+  const float *dagg, *z2s;  // non-null: dz2 = dagg[dst] * silu'(z2) computed on the fly
   __device__ float a(int, int e, int k) const {
     return k < H ? silu(z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, k)) : 1.f;
   }
@@ -876,7 +886,10 @@ struct L7Prob {  // dz1 = (dz2 eW2^T) * silu'(z1)
     float w;
   };
   __device__ RC rctx(int, int e) const { return RC{dst[e], src[e], geo[e].w}; }
-  __device__ float4 a4c(int, int e, const RC&, int k) const { return ld4(dz2 + size_t(e) * H + k); }
+  __device__ float4 a4c(int, int e, const RC& r, int k) const {
+    if (dagg) return mul4(ld4(dagg + size_t(r.d) * H + k), sgrad4(ld4(z2s + size_t(e) * H + k)));
+    return ld4(dz2 + size_t(e) * H + k);
+  }
   __device__ void epi4c(int, int e, const RC& r, int n, float4 acc) const {
     const float4 z = pre4(ld4(P + size_t(r.d) * 2 * H + n), ld4(P + size_t(r.s) * 2 * H + H + n), r.w, ld4(wd + n),
                           ld4(b1 + n));
@@ -894,6 +907,7 @@ struct L7Prob {  // dz1 = (dz2 eW2^T) * silu'(z1)
   const int *dst, *src;
   const float4* geo;
   float* dz1;
+  const float *dagg, *z2s;  // non-null: dz2 computed on the fly (tensor-core path)
   __device__ float a(int, int e, int k) const { return dz2[size_t(e) * H + k]; }
   __device__ float b(int, int k, int n) const { return W[size_t(n) * H + k]; }
   __device__ void epi(int, int e, int n, float acc) const {
@@ -1010,6 +1024,136 @@ __global__ void seg2_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, 
   }
 }
 
+// ---- vectorised CSR segment sums: warp per node, lane = float4 column group,
+// 4 independent edge loads in flight; ascending-edge accumulation per column.
+__device__ __forceinline__ float4 f4z() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+
+// agg_i = sum_{e in row i} silu(z2_e)
+__global__ void agg4_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const float* __restrict__ z2,
+                            float* __restrict__ agg, int H) {
+  const int N = hdr->N, lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += (gridDim.x * blockDim.x) >> 5) {
+    const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
+    for (int c = lane * 4; c < H; c += 128) {
+      float4 acc = f4z();
+      int e = e0;
+      for (; e + 4 <= e1; e += 4) {
+        const float4 v0 = ld4(z2 + size_t(e) * H + c), v1 = ld4(z2 + size_t(e + 1) * H + c);
+        const float4 v2 = ld4(z2 + size_t(e + 2) * H + c), v3 = ld4(z2 + size_t(e + 3) * H + c);
+        acc = add4(acc, silu4(v0));
+        acc = add4(acc, silu4(v1));
+        acc = add4(acc, silu4(v2));
+        acc = add4(acc, silu4(v3));
+      }
+      for (; e < e1; ++e) acc = add4(acc, silu4(ld4(z2 + size_t(e) * H + c)));
+      st4(agg + size_t(i) * H + c, acc);
+    }
+  }
+}
+
+// S[i] = [sum_{e in row i} x_e | sum_{e in row i} x_{rev(e)}] (or folded a + b)
+__global__ void seg2v_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const int* __restrict__ rev,
+                             const float* __restrict__ x, float* __restrict__ S, int C, int fold) {
+  const int N = hdr->N, lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += (gridDim.x * blockDim.x) >> 5) {
+    const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
+    for (int c = lane * 4; c < C; c += 128) {
+      float4 a = f4z(), b = f4z();
+      int e = e0;
+      for (; e + 2 <= e1; e += 2) {
+        const int r0 = rev[e], r1 = rev[e + 1];
+        const float4 a0 = ld4(x + size_t(e) * C + c), a1 = ld4(x + size_t(e + 1) * C + c);
+        const float4 b0 = ld4(x + size_t(r0) * C + c), b1 = ld4(x + size_t(r1) * C + c);
+        a = add4(add4(a, a0), a1);
+        b = add4(add4(b, b0), b1);
+      }
+      for (; e < e1; ++e) {
+        a = add4(a, ld4(x + size_t(e) * C + c));
+        b = add4(b, ld4(x + size_t(rev[e]) * C + c));
+      }
+      if (fold) {
+        st4(S + size_t(i) * C + c, add4(a, b));
+      } else {
+        st4(S + size_t(i) * 2 * C + c, a);
+        st4(S + size_t(i) * 2 * C + C + c, b);
+      }
+    }
+  }
+}
+
+// Column sums over the rows of each head segment: out[seg] = [sum_r w(r) x_r ; sum_r x_r]
+// (the [distance-or-d2 ; bias] rows of a factorised first layer's gradient).
+// Deterministic: CTA (chunk, seg) owns a fixed row range, 8 warps split it in
+// fixed sub-ranges, smem combine in warp order; colsum2_reduce sums chunks in order.
+constexpr int kCs2Rows = 512;
+__global__ void __launch_bounds__(256) colsum2_kernel(RowSet rows, const float* __restrict__ wvec, int wstride,
+                                                      const float* __restrict__ x, int C,
+                                                      float* __restrict__ partial, int nchunk_cap) {
+  __shared__ float4 red[8][2][64];
+  const int seg = blockIdx.y, chunk = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rb = rows.begin(seg), re = rows.end(seg);
+  const int r0 = rb + chunk * kCs2Rows;
+  const int sub = kCs2Rows / 8;
+  const int w0 = r0 + warp * sub, w1 = min(w0 + sub, re);
+  for (int c = lane * 4, u = 0; c < C; c += 128, ++u) {
+    float4 sw = f4z(), sx = f4z();
+    for (int v = w0; v < w1; ++v) {
+      const int r = rows.row(v);
+      const float4 xv = ld4(x + size_t(r) * C + c);
+      const float w = wvec[size_t(r) * wstride];
+      sw = make_float4(sw.x + w * xv.x, sw.y + w * xv.y, sw.z + w * xv.z, sw.w + w * xv.w);
+      sx = add4(sx, xv);
+    }
+    red[warp][0][lane + 32 * u] = sw;
+    red[warp][1][lane + 32 * u] = sx;
+  }
+  __syncthreads();
+  float* out = partial + (size_t(seg) * nchunk_cap + chunk) * 2 * C;
+  for (int t = threadIdx.x; t < 2 * (C / 4); t += blockDim.x) {
+    const int which = t / (C / 4), cg = t % (C / 4);
+    float4 acc = f4z();
+    for (int w = 0; w < 8; ++w) acc = add4(acc, red[w][which][cg]);
+    st4(out + which * C + cg * 4, acc);
+  }
+}
+__global__ void colsum2_reduce(RowSet rows, const float* __restrict__ partial, int nchunk_cap, int C,
+                               float* __restrict__ G, size_t seg_stride) {
+  const int seg = blockIdx.y;
+  const int nchunks = (rows.end(seg) - rows.begin(seg) + kCs2Rows - 1) / kCs2Rows;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 2 * C; t += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int k = 0; k < nchunks; ++k) acc += partial[(size_t(seg) * nchunk_cap + k) * 2 * C + t];
+    G[seg * seg_stride + t] = acc;  // rows [w; bias] are contiguous in the layout
+  }
+}
+
+// g_embed[s] = sum_{i: species_i = s} dh_i: CTA = 128-node chunk, thread = column,
+// smem accumulator [species][H] updated in ascending node order; chunks summed in order.
+constexpr int kEmbChunk = 128;
+__global__ void embed_grad_part(const DevHdr* hdr, const uint8_t* __restrict__ species, const float* __restrict__ dh,
+                                float* __restrict__ partial, int H, int NS) {
+  extern __shared__ float acc[];  // [NS][H]
+  const int N = hdr->N, chunk = blockIdx.x;
+  const int i0 = chunk * kEmbChunk;
+  if (i0 >= N) return;
+  for (int t = threadIdx.x; t < NS * H; t += blockDim.x) acc[t] = 0.f;
+  __syncthreads();
+  const int i1 = min(i0 + kEmbChunk, N);
+  for (int c = threadIdx.x; c < H; c += blockDim.x)
+    for (int i = i0; i < i1; ++i) acc[species[i] * H + c] += dh[size_t(i) * H + c];
+  __syncthreads();
+  for (int t = threadIdx.x; t < NS * H; t += blockDim.x) partial[size_t(chunk) * NS * H + t] = acc[t];
+}
+__global__ void embed_grad_reduce(const DevHdr* hdr, const float* __restrict__ partial, float* __restrict__ G, int H,
+                                  int NS) {
+  const int nchunks = (hdr->N + kEmbChunk - 1) / kEmbChunk;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < NS * H; t += gridDim.x * blockDim.x) {
+    float a = 0.f;
+    for (int k = 0; k < nchunks; ++k) a += partial[size_t(k) * NS * H + t];
+    G[t] = a;
+  }
+}
+
 // g_embed[s] = sum_{i: species_i = s} dh_i (ascending i; hmtl/model.hpp:619-622)
 __global__ void embed_grad_kernel(const DevHdr* hdr, const uint8_t* __restrict__ species, const float* __restrict__ dh,
                                   float* __restrict__ G, int H, int NS) {
@@ -1023,6 +1167,24 @@ __global__ void embed_grad_kernel(const DevHdr* hdr, const uint8_t* __restrict__
   }
 }
 
+}  // namespace
+
+namespace {
+void segsum2(Ctx& c, const float* x, int C, int fold, cudaStream_t st) {
+  Prof pr(c, "bwd.segsum_dst_src", st);
+  const int blocks = gridn((long long)c.Nc * 32, 256, c.sm_count * 16);
+  if (C % 4 == 0) seg2v_kernel<<<blocks, 256, 0, st>>>(c.hdr, c.row_ptr, c.rev, x, c.Sbuf, C, fold);
+  else seg2_kernel<<<blocks, 256, 0, st>>>(c.hdr, c.row_ptr, c.rev, x, c.Sbuf, C, fold);
+}
+// [sum w*x ; sum x] per head segment into G + seg*seg_stride (rows are contiguous)
+void colsum2(Ctx& c, RowSet rows, const float* w, int wstride, const float* x, int C, float* G, size_t seg_stride,
+             cudaStream_t st) {
+  Prof pr(c, "bwd.colsum_tail", st);
+  const int chunk_cap = int((c.Ec + kCs2Rows - 1) / kCs2Rows);
+  dim3 grid(chunk_cap, rows.nseg);
+  colsum2_kernel<<<grid, 256, 0, st>>>(rows, w, wstride, x, C, c.partial, chunk_cap);
+  colsum2_reduce<<<dim3(1, rows.nseg), 256, 0, st>>>(rows, c.partial, chunk_cap, C, G, seg_stride);
+}
 }  // namespace
 
 void launch_backward(Ctx& c, cudaStream_t st) {
@@ -1081,15 +1243,15 @@ void launch_backward(Ctx& c, cudaStream_t st) {
       ldz = W;
     }
     // layer 0 (factorised): T = S_dst(dz0) + S_src(dz0)
-    {
-      Prof pr(c, "bwd.segsum_dst_src", st);
-      seg2_kernel<<<gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st>>>(c.hdr, c.row_ptr, c.rev, dz, c.Sbuf, W,
-                                                                            1);
-    }
+    segsum2(c, dz, W, 1, st);
     F0NodeGrad ng{node_rows_by_head(c), H, W, H, W, hL, c.Sbuf, HeadG{c.head_grads(), c.PH, wf0}};
     atb(ng, c, c.nsplit_node, st, c.Nc);
-    F0EdgeGrad eg{edge_rows_by_head(c), 2, W, H, W, c.dist, dz, HeadG{c.head_grads(), c.PH, wf0 + size_t(H) * W}};
-    atb(eg, c, c.nsplit_edge, st, c.Ec);
+    if (W % 4 == 0) {
+      colsum2(c, edge_rows_by_head(c), c.dist, 1, dz, W, c.head_grads() + wf0 + size_t(H) * W, c.PH, st);
+    } else {
+      F0EdgeGrad eg{edge_rows_by_head(c), 2, W, H, W, c.dist, dz, HeadG{c.head_grads(), c.PH, wf0 + size_t(H) * W}};
+      atb(eg, c, c.nsplit_edge, st, c.Ec);
+    }
     F0Dh dhq{node_rows_by_head(c), W, H, H, W, c.Sbuf, HeadW{c.head_params(), c.PH, wf0}, c.dh};
     ab(dhq, c.Nc, c.S, st, sm, c);
   }
@@ -1123,29 +1285,24 @@ void launch_backward(Ctx& c, cudaStream_t st) {
       L4Prob q{node_rows(c), H, 2 * H, H, c.dvz1, c.params + c.shared_off(p + "node.W1"), dh, dh2, c.dagg};
       ab(q, c.Nc, 1, st, sm, c);
     }
-    {
+    const bool fuse = c.store_a1;  // tensor-core shapes: dz2 is computed inside its consumers
+    if (!fuse) {
       Prof pr(c, "bwd.edge_dz2_gather", st);
       dz2_kernel<<<gridn(EH, 256, sm * 16), 256, 0, st>>>(c.hdr, c.edge_dst, c.dagg, z2, c.dzA, H);
     }
     {
       L6Prob q{edge_rows(c), H + 1, H, H, P, wd, b1, c.dzA, c.edge_dst, c.edge_src, c.geo,
-               c.grads + c.shared_off(p + "edge.W2"), c.store_a1 ? c.a1 + size_t(l) * EH : nullptr};
+               c.grads + c.shared_off(p + "edge.W2"), fuse ? c.a1 + size_t(l) * EH : nullptr,
+               fuse ? c.dagg : nullptr, z2};
       atb(q, c, c.nsplit_edge, st, c.Ec);
     }
     {
       L7Prob q{edge_rows(c), H, H, H, c.dzA, c.params + c.shared_off(p + "edge.W2"), P, wd, b1, c.edge_dst,
-               c.edge_src, c.geo, c.dzB};
+               c.edge_src, c.geo, c.dzB, fuse ? c.dagg : nullptr, z2};
       ab(q, c.Ec, 1, st, sm, c);
     }
-    {
-      Prof pr(c, "bwd.segsum_dst_src", st);
-      seg2_kernel<<<gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st>>>(c.hdr, c.row_ptr, c.rev, c.dzB, c.Sbuf,
-                                                                            H, 0);
-    }
-    {
-      L9Prob q{edge_rows(c), 2, H, H, c.geo, c.dzB, geW1 + size_t(2) * H * H};
-      atb(q, c, c.nsplit_edge, st, c.Ec);
-    }
+    segsum2(c, c.dzB, H, 0, st);
+    colsum2(c, edge_rows(c), &c.geo[0].w, 4, c.dzB, H, geW1 + size_t(2) * H * H, 0, st);
     {
       L10Prob q{node_rows(c), H, 2 * H, H, h, c.Sbuf, geW1};
       atb(q, c, c.nsplit_node, st, c.Nc);
@@ -1158,9 +1315,15 @@ void launch_backward(Ctx& c, cudaStream_t st) {
   }
   {
     Prof pr(c, "bwd.embed_grad", st);
-    embed_grad_kernel<<<gridn((long long)c.NS * H, 128, sm * 8), 128, 0, st>>>(c.hdr, c.species, dh,
-                                                                                 c.grads + c.shared_off("embed"), H,
-                                                                                 c.NS);
+    const size_t shm = size_t(c.NS) * H * 4;
+    if (shm <= 48 * 1024 && size_t(c.Nc + kEmbChunk - 1) / kEmbChunk * c.NS * H <= c.partial_cap) {
+      embed_grad_part<<<(c.Nc + kEmbChunk - 1) / kEmbChunk, 128, shm, st>>>(c.hdr, c.species, dh, c.partial, H, c.NS);
+      embed_grad_reduce<<<gridn((long long)c.NS * H, 256, sm), 256, 0, st>>>(c.hdr, c.partial,
+                                                                            c.grads + c.shared_off("embed"), H, c.NS);
+    } else {
+      embed_grad_kernel<<<gridn((long long)c.NS * H, 128, sm * 8), 128, 0, st>>>(
+          c.hdr, c.species, dh, c.grads + c.shared_off("embed"), H, c.NS);
+    }
   }
 }
 
