@@ -441,7 +441,7 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
     const int mtiles = (M + 127) / 128;
     const long long chunks = (rows_cap > 0 ? rows_cap : (long long)c.Ec) / tc::KC + 1;
     // enough CTAs to fill the GPU, >= 4 chunks each (bounded partial traffic)
-    long long want = std::max<long long>(1, (long long)c.sm_count * 2 / (mtiles * p.rows.nseg));
+    long long want = std::max<long long>(1, (long long)c.sm_count / (mtiles * p.rows.nseg));  // one wave
     int ns = int(std::max<long long>(1, std::min<long long>(want, chunks / 4)));
     while (ns > 1 && size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * p.Ncols > c.partial_cap) ns /= 2;
     if (size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * p.Ncols <= c.partial_cap) {
@@ -1097,7 +1097,22 @@ __global__ void __launch_bounds__(256) colsum2_kernel(RowSet rows, const float* 
   const int w0 = r0 + warp * sub, w1 = min(w0 + sub, re);
   for (int c = lane * 4, u = 0; c < C; c += 128, ++u) {
     float4 sw = f4z(), sx = f4z();
-    for (int v = w0; v < w1; ++v) {
+    int v = w0;
+    for (; v + 4 <= w1; v += 4) {
+      int r[4];
+      float4 xv[4];
+      float w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) r[q] = rows.row(v + q);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) xv[q] = ld4(x + size_t(r[q]) * C + c), w[q] = wvec[size_t(r[q]) * wstride];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        sw = make_float4(sw.x + w[q] * xv[q].x, sw.y + w[q] * xv[q].y, sw.z + w[q] * xv[q].z, sw.w + w[q] * xv[q].w);
+        sx = add4(sx, xv[q]);
+      }
+    }
+    for (; v < w1; ++v) {
       const int r = rows.row(v);
       const float4 xv = ld4(x + size_t(r) * C + c);
       const float w = wvec[size_t(r) * wstride];

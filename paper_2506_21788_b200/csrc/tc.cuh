@@ -372,13 +372,15 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
 // P must provide: RowSet rows; int M, Ncols, colsum;
 //   float4 x4(int seg, int row, int m) const;  float4 y4(int seg, int row, int n) const;
 // Output partial: [seg][split][Ncols][M + colsum] (transposed: coalesced stores).
-constexpr int kRedThreads = 160;
+constexpr int kRedProd = 8;                      // producer warps (warp w = k-group w of a chunk)
+constexpr int kRedThreads = (kRedProd + 1) * 32;  // + 1 MMA warp
 __host__ __device__ inline size_t red_stage_bytes(int N) { return size_t(2 * 128 * KC + 2 * N * KC) * 4; }
+constexpr size_t kRedCsum = size_t(kRedProd) * 256 * 4;
 inline int red_stages(int N) {
-  int s = int((kSmemLimit - 2048 - 8192) / red_stage_bytes(N));
+  int s = int((kSmemLimit - 2048 - kRedCsum) / red_stage_bytes(N));
   return s < 2 ? 2 : (s > kMaxStages ? kMaxStages : s);
 }
-inline size_t tc_red_smem(int N) { return red_stages(N) * red_stage_bytes(N) + 8192 + 2048; }
+inline size_t tc_red_smem(int N) { return red_stages(N) * red_stage_bytes(N) + kRedCsum + 2048; }
 
 __device__ __forceinline__ float4 col4(const float4* v, int j) {  // column j of a 4x4 block
   return j == 0 ? make_float4(v[0].x, v[1].x, v[2].x, v[3].x)
@@ -393,8 +395,8 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int N = p.Ncols;
   const size_t SB = red_stage_bytes(N);
-  float* csum_smem = reinterpret_cast<float*>(smem_raw + kStages * SB);  // [4 warps][N]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + kStages * SB + 8192);
+  float* csum_smem = reinterpret_cast<float*>(smem_raw + kStages * SB);  // [kRedProd][N]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + kStages * SB + kRedCsum);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* accfull = bars + 2 * kStages;
@@ -402,10 +404,11 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int mtile = blockIdx.x, split = blockIdx.y, seg = blockIdx.z;
   const uint32_t acc_cols = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
-  if (warp == 4) tmem_alloc(tmem_slot, acc_cols);
+  constexpr int kProdThreads = kRedProd * 32;
+  if (warp == kRedProd) tmem_alloc(tmem_slot, acc_cols);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 128);
+      mbar_init(&full[s], kProdThreads);
       mbar_init(&empty[s], 1);
     }
     mbar_init(&accfull[0], 1);
@@ -425,21 +428,21 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
   const int Mt = p.M - m0 < 128 ? p.M - m0 : 128;  // features of this m-tile (mult of 4)
   const bool do_colsum = p.colsum && mtile == 0;
 
-  if (warp < 4) {
+  if (warp < kRedProd) {
     float4 cs[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
     int stage = 0;
     uint32_t phase = 0;
     const int f = lane * 4;
     for (int c = split; c < nchunks; c += nsplit) {
-      // this warp's 8 rows of the chunk; lane j < 8 resolves row j, broadcast by shuffle
-      const int vj = rb + c * KC + warp * 8 + (lane & 7);
+      // this warp's 4 rows (k-group `warp` of the chunk)
+      const int vj = rb + c * KC + warp * 4 + (lane & 3);
       const int rj = vj < re ? p.rows.row(vj) : -1;
-      int rows[8];
+      int rows[4];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) rows[j] = __shfl_sync(0xffffffffu, rj, j);
-      float4 xa[8], yb[2][8];
+      for (int j = 0; j < 4; ++j) rows[j] = __shfl_sync(0xffffffffu, rj, j);
+      float4 xa[4], yb[2][4];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < 4; ++j) {
         xa[j] = (rows[j] >= 0 && f < Mt) ? p.x4(seg, rows[j], m0 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
+          for (int j = 0; j < 4; ++j)
             cs[u] = make_float4(cs[u].x + yb[u][j].x, cs[u].y + yb[u][j].y, cs[u].z + yb[u][j].z,
                                 cs[u].w + yb[u][j].w);
       mbar_wait(&empty[stage], phase ^ 1);
@@ -460,16 +463,12 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
       float* b_hi = a_lo + 128 * KC;
       float* b_lo = b_hi + N * KC;
 #pragma unroll
-      for (int qd = 0; qd < 2; ++qd) {  // row quads of this warp: k-group g = 2*warp + qd
-        const int g = 2 * warp + qd;
+      for (int i = 0; i < 4; ++i) {
+        const int jj = (i + lane) & 3;
+        put4(a_hi, a_lo, 128, warp, f + jj, col4(xa, jj));
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int jj = (i + lane) & 3;
-          put4(a_hi, a_lo, 128, g, f + jj, col4(&xa[4 * qd], jj));
-#pragma unroll
-          for (int u = 0; u < 2; ++u)
-            if (f + 128 * u < N) put4(b_hi, b_lo, N, g, f + 128 * u + jj, col4(&yb[u][4 * qd], jj));
-        }
+        for (int u = 0; u < 2; ++u)
+          if (f + 128 * u < N) put4(b_hi, b_lo, N, warp, f + 128 * u + jj, col4(yb[u], jj));
       }
       fence_proxy_async();
       mbar_arrive(&full[stage]);
@@ -480,29 +479,35 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
       for (int u = 0; u < 2; ++u)
         if (f + 128 * u < N) *reinterpret_cast<float4*>(csum_smem + warp * N + f + 128 * u) = cs[u];
     }
-    // epilogue: TMEM lane = feature m0 + tid; the partial is stored transposed ([n][m])
+    // epilogue: warp w reads TMEM lanes 32*(w%4) (features), column half w/4;
+    // the partial is stored transposed ([n][m]) so stores are coalesced
     if (my_chunks > 0) {
       mbar_wait(&accfull[0], 0);
       tc_fence_after();
     }
-    for (int n0 = 0; n0 < N; n0 += 32) {
+    const int q = warp & 3, half = warp >> 2;
+    const int nh = ((N / 32) + 1) / 2 * 32;  // columns of half 0
+    const int nb = half ? nh : 0, ne = half ? N : nh;
+    const int mloc = q * 32 + lane;
+    for (int n0 = nb; n0 < ne; n0 += 32) {
       float acc[32];
       __syncwarp();
-      tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + n0, acc);
-      if (tid < Mt) {
+      tmem_ld32(tmem + (uint32_t(q * 32) << 16) + n0, acc);
+      if (mloc < Mt) {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          if (n0 + i < N) out[size_t(n0 + i) * Mo + m0 + tid] = my_chunks ? acc[i] : 0.f;
+          if (n0 + i < N) out[size_t(n0 + i) * Mo + m0 + mloc] = my_chunks ? acc[i] : 0.f;
       }
     }
     if (do_colsum) {
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      for (int n = tid; n < N; n += 128) {
-        const float v = ((csum_smem[n] + csum_smem[N + n]) + csum_smem[2 * N + n]) + csum_smem[3 * N + n];
+      asm volatile("bar.sync 1, %0;" ::"r"(kProdThreads) : "memory");
+      for (int n = tid; n < N; n += kProdThreads) {
+        float v = 0.f;
+        for (int w = 0; w < kRedProd; ++w) v += csum_smem[w * N + n];
         out[size_t(n) * Mo + p.M] = v;
       }
     }
-  } else {  // warp 4: MMA issuer
+  } else {  // MMA issuer
     int stage = 0;
     uint32_t phase = 0;
     const uint32_t idesc = idesc_tf32(N);
@@ -525,7 +530,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) tmem_dealloc(tmem, acc_cols);
+  if (warp == kRedProd) tmem_dealloc(tmem, acc_cols);
 }
 
 // partial is [seg][split][n][Mo] (transposed); store C[m][n]
