@@ -183,6 +183,7 @@ int hmtl_profile_report(hmtl_ctx* ctx, char* json, size_t cap);
  * plain row-major matrices on device 0.  mode 0: C[rows x N] = X[rows x K] B[K x N]
  * (Y = B); mode 1: C[K x N] = X[rows x K]^T Y[rows x N].  variant: debug bits. */
 int hmtl_selftest_gemm(int mode, int variant, int rows, int K, int N, const float* X, const float* Y, float* C);
+int hmtl_selftest_time(int mode, int rows, int K, int N, int iters, float* ms);
 
 /* ------------------------------------------------------------ comm (NCCL) */
 /* collective::allreduce_mean over RankGroup (hmtl/mesh.hpp:276-278, 312-342),

@@ -106,6 +106,7 @@ SIGNATURES = {
     "hmtl_profile_enable": (C.c_int, [_P, C.c_int]),
     "hmtl_profile_report": (C.c_int, [_P, C.c_char_p, C.c_size_t]),
     "hmtl_selftest_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _FP, _FP, _FP]),
+    "hmtl_selftest_time": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _FP]),
     "hmtl_comm_unique_id": (C.c_int, [_U8P]),
     "hmtl_comm_init": (C.c_int, [_P, _U8P, C.c_int, C.c_int]),
     "hmtl_comm_sync_grads": (C.c_int, [_P, _P]),

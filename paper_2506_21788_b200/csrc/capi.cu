@@ -76,7 +76,7 @@ void free_ctx(Ctx& c) {
                   c.species, c.gslot, c.gperm, c.gnode_base, c.gedge_base, c.node_perm, c.edge_perm, c.hs, c.P,
                   c.z2, c.agg, c.vz1, c.pooled, c.ez, c.energy, c.Qf, c.zf, c.s, c.forces, c.dE, c.dF, c.dh,
                   c.dh2, c.dagg, c.dvz1, c.dzA, c.dzB, c.Sbuf, c.ds, c.dpooled, c.edA, c.edB, c.scratch,
-                  c.partial, c.bimg, c.a1, c.af0};
+                  c.partial, c.bimg, c.a1, c.af0, c.sf0};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto* p : c.pool) cudaFree(p);
@@ -232,9 +232,10 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   A(&c.bimg, c.bimg_cap);
   if (const char* e = std::getenv("HMTL_NO_TC")) c.use_tc = e[0] == '0';
   c.store_a1 = c.use_tc && H % 32 == 0;
-  c.store_af0 = c.use_tc && W % 32 == 0;
+  c.store_af0 = c.use_tc && W % 32 == 0 && H % 4 == 0;
   A(&c.a1, c.store_a1 ? L * E * H : 1);
   A(&c.af0, c.store_af0 ? E * W : 1);
+  A(&c.sf0, c.store_af0 ? E * W : 1);
   if (rc) {
     free_ctx(c);
     delete h;

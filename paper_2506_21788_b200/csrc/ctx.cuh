@@ -70,7 +70,7 @@ struct Ctx {
   bool use_tc = true;     // tcgen05 path for GEMMs whose shapes allow it
   bool store_a1 = false;  // forward producer materialises a1 = silu(z1) [L][E][H]
   bool store_af0 = false; // ... and silu(zf0) [E][W]
-  float *a1 = nullptr, *af0 = nullptr;
+  float *a1 = nullptr, *af0 = nullptr, *sf0 = nullptr;
   int nsplit_node = 1, nsplit_edge = 1, nsplit_graph = 1;
 
   // CUDA graph of a whole training step

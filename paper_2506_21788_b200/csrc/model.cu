@@ -97,12 +97,11 @@ struct MsgProb {
     int d, s;
     float w;
   };
-  __device__ RC rctx(int, int e) const { return RC{dst[e], src[e], geo[e].w}; }
+  __device__ RC rctx(int, int e) const { return a1out ? RC{0, 0, 0.f} : RC{dst[e], src[e], geo[e].w}; }
   __device__ float4 a4c(int, int e, const RC& r, int k) const {
-    const float4 a = silu4(pre4(ld4(P + size_t(r.d) * 2 * H + k), ld4(P + size_t(r.s) * 2 * H + H + k), r.w,
-                                ld4(wd + k), ld4(b1 + k)));
-    if (a1out) st4(a1out + size_t(e) * H + k, a);  // materialise a1 for the dW2 reduce GEMM
-    return a;
+    if (a1out) return ld4(a1out + size_t(e) * H + k);  // a1 materialised by edge_a1_kernel
+    return silu4(pre4(ld4(P + size_t(r.d) * 2 * H + k), ld4(P + size_t(r.s) * 2 * H + H + k), r.w, ld4(wd + k),
+                      ld4(b1 + k)));
   }
   __device__ void epi4c(int, int e, const RC&, int n, float4 acc) const {
     st4(z2 + size_t(e) * H + n, add4(acc, ld4(b2 + n)));
@@ -200,13 +199,14 @@ struct ForceProb {
     int d, s;
     float dist;
   };
-  __device__ RC rctx(int, int e) const { return RC{dst[e], src[e], dist[e]}; }
+  __device__ RC rctx(int, int e) const {
+    return (af0out || layer != 1) ? RC{0, 0, 0.f} : RC{dst[e], src[e], dist[e]};
+  }
   __device__ float4 a4c(int seg, int e, const RC& r, int k) const {
     if (layer == 1) {
-      const float4 a = silu4(pre4(ld4(Qf + size_t(r.d) * W + k), ld4(Qf + size_t(r.s) * W + k), r.dist,
-                                  ldu4(Wd.at(seg) + k), ldu4(B0.at(seg) + k)));
-      if (af0out) st4(af0out + size_t(e) * W + k, a);  // materialise silu(zf0) for the dWf1 reduce GEMM
-      return a;
+      if (af0out) return ld4(af0out + size_t(e) * W + k);  // silu(zf0) materialised by edge_af0_kernel
+      return silu4(pre4(ld4(Qf + size_t(r.d) * W + k), ld4(Qf + size_t(r.s) * W + k), r.dist,
+                        ldu4(Wd.at(seg) + k), ldu4(B0.at(seg) + k)));
     }
     return silu4(ld4(zf + size_t(layer - 2) * Ec * W + size_t(e) * W + k));
   }
@@ -385,10 +385,11 @@ __global__ void bimg_prob_kernel(P p, float* __restrict__ out, int nseg) {
     const int n = rem % N, k = rem / N;
     const float x = p.b(seg, k, n);
     const float h = tc::tf32_hi(x);
-    const int ch = k / tc::KC, g = (k % tc::KC) / 4, q = k % 4;
+    const int ch = k / tc::KC, c16 = (k % tc::KC) / 4, q = k % 4;
     float* o = out + size_t(seg) * 2 * K * N + size_t(ch) * 2 * tc::KC * N;
-    o[(size_t(g) * N + n) * 4 + q] = h;
-    o[size_t(tc::KC) * N + (size_t(g) * N + n) * 4 + q] = x - h;
+    const uint32_t off = tc::sw128(n, c16) / 4 + q;
+    o[off] = h;
+    o[size_t(tc::KC) * N + off] = x - h;
   }
 }
 template <class P>
@@ -500,6 +501,58 @@ RowSet graph_rows_by_head(Ctx& c) {
 namespace {
 __global__ void agg4_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const float* __restrict__ z2,
                             float* __restrict__ agg, int H);
+
+// ---- full-occupancy elementwise producers of the tensor-core A operands
+// a1 = silu(z1), z1 = (P_a[dst] + P_b[src]) + d2 w + b1   (one thread per 4 columns)
+__global__ void edge_a1_kernel(const DevHdr* hdr, const float* __restrict__ P, const int* __restrict__ dst,
+                               const int* __restrict__ src, const float4* __restrict__ geo,
+                               const float* __restrict__ wd, const float* __restrict__ b1, float* __restrict__ a1,
+                               int H) {
+  const int q = H / 4;
+  const long long total = (long long)hdr->E * q;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int e = int(t / q), c = int(t % q) * 4;
+    const int d = dst[e], s = src[e];
+    st4(a1 + size_t(e) * H + c, silu4(pre4(ld4(P + size_t(d) * 2 * H + c), ld4(P + size_t(s) * 2 * H + H + c),
+                                             geo[e].w, ld4(wd + c), ld4(b1 + c))));
+  }
+}
+// backward: dz2 = dagg[dst] * silu'(z2) and s1p = silu'(z1)
+__global__ void edge_bwd_prep_kernel(const DevHdr* hdr, const float* __restrict__ P, const int* __restrict__ dst,
+                                     const int* __restrict__ src, const float4* __restrict__ geo,
+                                     const float* __restrict__ wd, const float* __restrict__ b1,
+                                     const float* __restrict__ dagg, const float* __restrict__ z2,
+                                     float* __restrict__ dz2, float* __restrict__ s1p, int H) {
+  const int q = H / 4;
+  const long long total = (long long)hdr->E * q;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int e = int(t / q), c = int(t % q) * 4;
+    const int d = dst[e], s = src[e];
+    const size_t o = size_t(e) * H + c;
+    st4(dz2 + o, mul4(ld4(dagg + size_t(d) * H + c), sgrad4(ld4(z2 + o))));
+    st4(s1p + o, sgrad4(pre4(ld4(P + size_t(d) * 2 * H + c), ld4(P + size_t(s) * 2 * H + H + c), geo[e].w,
+                             ld4(wd + c), ld4(b1 + c))));
+  }
+}
+// force head layer 0: af0 = silu(zf0), sf0 = silu'(zf0) with the edge's head weights
+__global__ void edge_af0_kernel(const DevHdr* hdr, const float* __restrict__ Qf, const int* __restrict__ dst,
+                                const int* __restrict__ src, const float* __restrict__ dist,
+                                const int* __restrict__ node_graph, const int* __restrict__ gslot,
+                                const float* __restrict__ heads, size_t PH, size_t off_wd, size_t off_b0,
+                                float* __restrict__ af0, float* __restrict__ sf0, int W) {
+  const int q = W / 4;
+  const long long total = (long long)hdr->E * q;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int e = int(t / q), c = int(t % q) * 4;
+    const int d = dst[e], s = src[e];
+    const float* hb = heads + size_t(gslot[node_graph[d]]) * PH;
+    const float4 z = pre4(ld4(Qf + size_t(d) * W + c), ld4(Qf + size_t(s) * W + c), dist[e], ldu4(hb + off_wd + c),
+                          ldu4(hb + off_b0 + c));
+    const size_t o = size_t(e) * W + c;
+    st4(af0 + o, silu4(z));
+    st4(sf0 + o, sgrad4(z));
+  }
+}
 }
 
 void launch_forward(Ctx& c, cudaStream_t st) {
@@ -521,6 +574,12 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     {
       PProb q{node_rows(c), H, 2 * H, H, h, W1, P};
       ab(q, c.Nc, 1, st, sm, c);
+    }
+    if (c.store_a1) {
+      Prof pr(c, "fwd.edge_act", st);
+      edge_a1_kernel<<<gridn((long long)c.Ec * H / 4, 256, sm * 16), 256, 0, st>>>(
+          c.hdr, P, c.edge_dst, c.edge_src, c.geo, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
+          c.a1 + size_t(l) * EH, H);
     }
     {
       MsgProb q{edge_rows(c), H, H, H, P, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
@@ -565,6 +624,12 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     ab(q, c.Nc, c.S, st, sm, c);
   }
   const size_t wf0 = c.head_off("force.W0");
+  if (c.store_af0) {
+    Prof pr(c, "fwd.edge_act", st);
+    edge_af0_kernel<<<gridn((long long)c.Ec * W / 4, 256, sm * 16), 256, 0, st>>>(
+        c.hdr, c.Qf, c.edge_dst, c.edge_src, c.dist, c.node_graph, c.gslot, c.head_params(), c.PH,
+        wf0 + size_t(H) * W, c.head_off("force.b0"), c.af0, c.sf0, W);
+  }
   for (int i = 1; i < D; ++i) {
     const int last = i == D - 1;
     ForceProb q{edge_rows_by_head(c), W, last ? 1 : W, H, W, i, last, c.Ec, c.Qf, c.zf, c.dist, c.edge_dst,
@@ -711,9 +776,15 @@ struct FDxProb {  // dz_{i-1} = (dz_i W_i^T) * silu'(z_{i-1})
     int d, s;
     float dist;
   };
-  __device__ RC rctx(int, int e) const { return RC{dst[e], src[e], dist[e]}; }
+  __device__ RC rctx(int, int e) const {
+    return (sf0 || layer != 1) ? RC{0, 0, 0.f} : RC{dst[e], src[e], dist[e]};
+  }
   __device__ float4 a4c(int, int e, const RC&, int k) const { return ld4(dz + size_t(e) * ldz + k); }
   __device__ void epi4c(int seg, int e, const RC& r, int n, float4 acc) const {
+    if (layer == 1 && sf0) {
+      st4(out + size_t(e) * W + n, mul4(acc, ld4(sf0 + size_t(e) * W + n)));
+      return;
+    }
     const float4 zp = layer == 1 ? pre4(ld4(Qf + size_t(r.d) * W + n), ld4(Qf + size_t(r.s) * W + n), r.dist,
                                         ldu4(Wd.at(seg) + n), ldu4(B0.at(seg) + n))
                                  : ld4(zf + size_t(layer - 2) * Ec * W + size_t(e) * W + n);
@@ -734,6 +805,7 @@ struct FDxProb {  // dz_{i-1} = (dz_i W_i^T) * silu'(z_{i-1})
   const int *dst, *src;
   HeadW Wd, B0, Wt;
   float* out;
+  const float* sf0;  // non-null: silu'(zf0) materialised
   __device__ float a(int, int e, int k) const { return dz[size_t(e) * ldz + k]; }
   __device__ float b(int seg, int k, int n) const { return Wt.at(seg)[size_t(n) * K + k]; }
   __device__ void epi(int seg, int e, int n, float acc) const {
@@ -885,12 +957,16 @@ struct L7Prob {  // dz1 = (dz2 eW2^T) * silu'(z1)
     int d, s;
     float w;
   };
-  __device__ RC rctx(int, int e) const { return RC{dst[e], src[e], geo[e].w}; }
+  __device__ RC rctx(int, int e) const { return s1p ? RC{0, 0, 0.f} : RC{dst[e], src[e], geo[e].w}; }
   __device__ float4 a4c(int, int e, const RC& r, int k) const {
     if (dagg) return mul4(ld4(dagg + size_t(r.d) * H + k), sgrad4(ld4(z2s + size_t(e) * H + k)));
     return ld4(dz2 + size_t(e) * H + k);
   }
   __device__ void epi4c(int, int e, const RC& r, int n, float4 acc) const {
+    if (s1p) {  // silu'(z1) materialised by edge_bwd_prep_kernel
+      st4(dz1 + size_t(e) * H + n, mul4(acc, ld4(s1p + size_t(e) * H + n)));
+      return;
+    }
     const float4 z = pre4(ld4(P + size_t(r.d) * 2 * H + n), ld4(P + size_t(r.s) * 2 * H + H + n), r.w, ld4(wd + n),
                           ld4(b1 + n));
     st4(dz1 + size_t(e) * H + n, mul4(acc, sgrad4(z)));
@@ -908,6 +984,7 @@ struct L7Prob {  // dz1 = (dz2 eW2^T) * silu'(z1)
   const float4* geo;
   float* dz1;
   const float *dagg, *z2s;  // non-null: dz2 computed on the fly (tensor-core path)
+  const float* s1p;         // non-null: silu'(z1) materialised
   __device__ float a(int, int e, int k) const { return dz2[size_t(e) * H + k]; }
   __device__ float b(int, int k, int n) const { return W[size_t(n) * H + k]; }
   __device__ void epi(int, int e, int n, float acc) const {
@@ -1252,7 +1329,8 @@ void launch_backward(Ctx& c, cudaStream_t st) {
       atb(gq, c, c.nsplit_edge, st, c.Ec);
       float* nxt = bufs[i & 1];
       FDxProb dq{edge_rows_by_head(c), out, W, H, W, i, c.Ec, c.Qf, c.zf, c.dist, dz, ldz, c.edge_dst, c.edge_src,
-                 Wd, B0, HeadW{c.head_params(), c.PH, c.head_off("force.W" + std::to_string(i))}, nxt};
+                 Wd, B0, HeadW{c.head_params(), c.PH, c.head_off("force.W" + std::to_string(i))}, nxt,
+                 c.store_af0 ? c.sf0 : nullptr};
       ab(dq, c.Ec, c.S, st, sm, c);
       dz = nxt;
       ldz = W;
@@ -1300,20 +1378,23 @@ void launch_backward(Ctx& c, cudaStream_t st) {
       L4Prob q{node_rows(c), H, 2 * H, H, c.dvz1, c.params + c.shared_off(p + "node.W1"), dh, dh2, c.dagg};
       ab(q, c.Nc, 1, st, sm, c);
     }
-    const bool fuse = c.store_a1;  // tensor-core shapes: dz2 is computed inside its consumers
-    if (!fuse) {
+    const bool mat = c.store_a1;  // tensor-core shapes: gathered operands materialised elementwise
+    if (mat) {
+      Prof pr(c, "bwd.edge_act", st);
+      edge_bwd_prep_kernel<<<gridn((long long)c.Ec * H / 4, 256, sm * 16), 256, 0, st>>>(
+          c.hdr, P, c.edge_dst, c.edge_src, c.geo, wd, b1, c.dagg, z2, c.dzA, c.scratch, H);
+    } else {
       Prof pr(c, "bwd.edge_dz2_gather", st);
       dz2_kernel<<<gridn(EH, 256, sm * 16), 256, 0, st>>>(c.hdr, c.edge_dst, c.dagg, z2, c.dzA, H);
     }
     {
       L6Prob q{edge_rows(c), H + 1, H, H, P, wd, b1, c.dzA, c.edge_dst, c.edge_src, c.geo,
-               c.grads + c.shared_off(p + "edge.W2"), fuse ? c.a1 + size_t(l) * EH : nullptr,
-               fuse ? c.dagg : nullptr, z2};
+               c.grads + c.shared_off(p + "edge.W2"), mat ? c.a1 + size_t(l) * EH : nullptr, nullptr, z2};
       atb(q, c, c.nsplit_edge, st, c.Ec);
     }
     {
       L7Prob q{edge_rows(c), H, H, H, c.dzA, c.params + c.shared_off(p + "edge.W2"), P, wd, b1, c.edge_dst,
-               c.edge_src, c.geo, c.dzB, fuse ? c.dagg : nullptr, z2};
+               c.edge_src, c.geo, c.dzB, nullptr, z2, mat ? c.scratch : nullptr};
       ab(q, c.Ec, 1, st, sm, c);
     }
     segsum2(c, c.dzB, H, 0, st);

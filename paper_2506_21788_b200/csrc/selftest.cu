@@ -43,10 +43,11 @@ __global__ void st_bimg(const float* B, int K, int N, float* out) {  // B is [K]
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < K * N; t += gridDim.x * blockDim.x) {
     const int n = t % N, k = t / N;
     const float x = B[size_t(k) * N + n], h = tc::tf32_hi(x);
-    const int ch = k / tc::KC, g = (k % tc::KC) / 4, q = k % 4;
+    const int ch = k / tc::KC, c16 = (k % tc::KC) / 4, q = k % 4;
     float* o = out + size_t(ch) * 2 * tc::KC * N;
-    o[(size_t(g) * N + n) * 4 + q] = h;
-    o[size_t(tc::KC) * N + (size_t(g) * N + n) * 4 + q] = x - h;
+    const uint32_t off = tc::sw128(n, c16) / 4 + q;
+    o[off] = h;
+    o[size_t(tc::KC) * N + off] = x - h;
   }
 }
 
@@ -94,5 +95,68 @@ extern "C" int hmtl_selftest_gemm(int mode, int variant, int rows, int K, int N,
   if (e == cudaSuccess) cudaMemcpy(C, dC, (mode == 0 ? nc : size_t(K) * N) * 4, cudaMemcpyDeviceToHost);
   cudaFree(dX), cudaFree(dY), cudaFree(dC), cudaFree(img), cudaFree(part), cudaFree(dcnt);
   if (e != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("selftest: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+// Timed engine run on device-resident random matrices: returns the mean kernel
+// time (ms) of `iters` launches (CUDA events), for roofline work on the engine.
+namespace hmtl_b200 {
+namespace {
+__global__ void set_dbg(int v) { tc::g_tc_debug = v; }
+}  // namespace
+}  // namespace hmtl_b200
+
+extern "C" int hmtl_selftest_time(int mode, int rows, int K, int N, int iters, float* ms) {
+  cudaSetDevice(0);
+  const int dbg = mode >> 4;
+  mode &= 15;
+  set_dbg<<<1, 1>>>(dbg);
+  float *dX, *dY, *dC, *img, *part;
+  int* dcnt;
+  const size_t nx = size_t(rows) * K, ny = mode == 0 ? size_t(K) * N : size_t(rows) * N;
+  const size_t nc = mode == 0 ? size_t(rows) * N : size_t(K + 1) * N;
+  const int ns = mode == 0 ? 1 : 148 / ((K + 127) / 128);
+  HMTL_CUDA(cudaMalloc(&dX, nx * 4));
+  HMTL_CUDA(cudaMalloc(&dY, ny * 4));
+  HMTL_CUDA(cudaMalloc(&dC, nc * 4));
+  HMTL_CUDA(cudaMalloc(&img, 2 * size_t(K) * N * 4));
+  HMTL_CUDA(cudaMalloc(&part, size_t(ns) * (K + 1) * N * 4));
+  HMTL_CUDA(cudaMalloc(&dcnt, 4));
+  cudaMemset(dX, 0, nx * 4);
+  cudaMemset(dY, 0, ny * 4);
+  cudaMemcpy(dcnt, &rows, 4, cudaMemcpyHostToDevice);
+  RowSet rs;
+  rs.count = dcnt;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  auto launch = [&]() {
+    if (mode == 0) {
+      StRow p{rs, K, N, img, 0, dX, dC};
+      const tc::RowPlan plan = tc::row_plan(K, N);
+      cudaFuncSetAttribute(tc::tc_row_kernel<StRow>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan.smem));
+      const int tiles = (rows + 127) / 128;
+      tc::tc_row_kernel<StRow><<<tiles < 148 ? tiles : 148, tc::kRowThreads, plan.smem>>>(p, plan);
+    } else {
+      StRed p{rs, K, N, 0, dX, dY, dC};
+      const size_t smem = tc::tc_red_smem(N);
+      cudaFuncSetAttribute(tc::tc_red_kernel<StRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      dim3 grid((K + 127) / 128, ns, 1);
+      tc::tc_red_kernel<StRed><<<grid, tc::kRedThreads, smem>>>(p, part, ns, tc::red_stages(N));
+    }
+  };
+  launch();
+  cudaEventRecord(a);
+  for (int i = 0; i < iters; ++i) launch();
+  cudaEventRecord(b);
+  cudaError_t e = cudaEventSynchronize(b);
+  float t = 0.f;
+  cudaEventElapsedTime(&t, a, b);
+  *ms = t / iters;
+  cudaEventDestroy(a), cudaEventDestroy(b);
+  set_dbg<<<1, 1>>>(0);
+  cudaDeviceSynchronize();
+  cudaFree(dX), cudaFree(dY), cudaFree(dC), cudaFree(img), cudaFree(part), cudaFree(dcnt);
+  if (e != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("selftest_time: ") + cudaGetErrorString(e));
   return 0;
 }

@@ -5,13 +5,14 @@
 // FP32 accumulation in TMEM) -> ~FP32 accuracy (error ~2^-22 |a||b|), which
 // keeps the rel 1e-4 parity bar of the FP32 path.
 //
-// Operands live in shared memory in the canonical K-major SWIZZLE_NONE UMMA
-// layout: a K-chunk of 32 values is 8 "k-groups" of 4 fp32 (16 B); group g of
-// an R-row operand starts at g*R*16 B and row r sits at +r*16 B.  One MMA
-// (K = 8) covers two k-groups: LBO = R*16 B (k-group stride), SBO = 128 B
-// (8-row core-matrix stride).  Producer threads write A rows (thread t = row t,
-// 16 B stores, conflict-free); B comes from a pre-split global image with the
-// same byte layout (plain coalesced 16 B copies, L2-resident, shared by all CTAs).
+// Operands live in shared memory in the canonical K-major SWIZZLE_128B UMMA
+// layout: a K-chunk of 32 fp32 is one 128 B line per row (row r at r*128 B,
+// 1 KB atoms of 8 rows), its 16 B chunk c stored at chunk position c ^ (r % 8).
+// One MMA (K = 8 -> 32 B) advances the descriptor start by 32 B inside the
+// atom; SBO = 1024 B (8-row atom stride).  (The SWIZZLE_NONE "interleaved"
+// layout ran the MMAs at ~40% of the tensor floor -- measured with
+// hmtl_selftest_time.)  B comes from a pre-split global image with the same
+// byte layout (contiguous rows: plain coalesced 16 B copies, L2-resident).
 //
 // Two engines, both templated on a problem functor:
 //   tc_row_kernel : C[row, n] = epi(sum_k A(row,k) B(k,n)), 128-row tiles of a
@@ -88,10 +89,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// K-major, SWIZZLE_NONE shared-memory matrix descriptor (sm100 "version 1").
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
-         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46);
+// K-major, SWIZZLE_128B shared-memory matrix descriptor (sm100 "version 1",
+// layout type 2): LBO unused for swizzled K-major (set to 16 B), SBO = 1024 B.
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
 // instruction descriptor: kind::tf32, D f32, A/B tf32 K-major, M = 128, N
 __host__ __device__ constexpr uint32_t idesc_tf32(int N) {
@@ -100,27 +102,28 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int N) {
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
-// write 4 consecutive k-values of row r into the hi/lo chunk images
-__device__ __forceinline__ void put4(float* hi, float* lo, int R, int g, int r, float4 v) {
+// byte offset of 16 B chunk c (k = 4c..4c+3 of the 32-k chunk) of row r
+__host__ __device__ __forceinline__ uint32_t sw128(int r, int c) { return uint32_t(r * 128 + ((c ^ (r & 7)) << 4)); }
+// write 4 consecutive k-values (chunk c) of row r into the hi/lo operand tiles
+__device__ __forceinline__ void put4(float* hi, float* lo, int c, int r, float4 v) {
   float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
   float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-  reinterpret_cast<float4*>(hi)[g * R + r] = h;
-  reinterpret_cast<float4*>(lo)[g * R + r] = l;
+  const uint32_t o = sw128(r, c);
+  *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(hi) + o) = h;
+  *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(lo) + o) = l;
 }
 
 constexpr int KC = 32;  // k values per chunk (4 MMAs of K=8)
 
-// issue the 3xTF32 MMAs of one chunk (single thread)
-__device__ __forceinline__ void issue_chunk(uint32_t tmem, const float* a_hi, const float* a_lo, int RA,
-                                            const float* b_hi, const float* b_lo, int RB, uint32_t idesc,
-                                            bool first) {
+// issue the 3xTF32 MMAs of one chunk (single thread); operand tiles are SW128
+__device__ __forceinline__ void issue_chunk(uint32_t tmem, const float* a_hi, const float* a_lo, const float* b_hi,
+                                            const float* b_lo, uint32_t idesc, bool first) {
   const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
-  const uint32_t la = RA * 16, lb = RB * 16;
 #pragma unroll
   for (int j = 0; j < KC / 8; ++j) {
-    const uint32_t oa = j * 2 * RA * 16, ob = j * 2 * RB * 16;
-    const uint64_t dah = sdesc(ah + oa, la, 128), dal = sdesc(al + oa, la, 128);
-    const uint64_t dbh = sdesc(bh + ob, lb, 128), dbl = sdesc(bl + ob, lb, 128);
+    const uint32_t o = 32 * j;  // K = 8 fp32 = 32 B inside the 128 B swizzle atom row
+    const uint64_t dah = sdesc_sw128(ah + o), dal = sdesc_sw128(al + o);
+    const uint64_t dbh = sdesc_sw128(bh + o), dbl = sdesc_sw128(bl + o);
     mma_tf32(tmem, dal, dbh, idesc, (first && j == 0) ? 0u : 1u);
     mma_tf32(tmem, dah, dbl, idesc, 1u);
     mma_tf32(tmem, dah, dbh, idesc, 1u);
@@ -128,7 +131,7 @@ __device__ __forceinline__ void issue_chunk(uint32_t tmem, const float* a_hi, co
 }
 
 // B images (weights) are built per problem by bimg_prob_kernel (model.cu):
-// per 32-k chunk c, [hi | lo], each [8 k-groups][N rows][4] fp32.
+// per 32-k chunk c, [hi | lo], each N rows x 128 B in the SW128 layout above.
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -149,7 +152,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 //   float4 a4(int seg, int row, const RC&, int k) const;           // A(row, k..k+3)
 //   void epi4(int seg, int row, const RC&, int n, float4 acc) const;  // C(row, n..n+3)
 constexpr int kMaxStages = 4;
-constexpr int kProdWarps = 8;
+// engine ablation switches for hmtl_selftest_time (bit0: producers skip A loads/stores,
+// bit1: epilogue skips global stores); always 0 on the training path.
+static __device__ int g_tc_debug = 0;
+constexpr int kProdWarps = 16;  // 8 rows each (4 lanes per row)
 constexpr int kRowThreads = (kProdWarps + 5) * 32;  // producers, 1 MMA warp, 4 epilogue warps
 constexpr size_t kSmemLimit = 227 * 1024;
 constexpr int kEpiLd = 36;  // padded row stride (floats) of the epilogue transpose slab
@@ -165,19 +171,24 @@ inline RowPlan row_plan(int K, int Nt) {
   r.a_stage = size_t(2 * 128 * KC) * 4;  // hi + lo
   const size_t b_chunk = size_t(2 * Nt * KC) * 4;
   const size_t b_all = b_chunk * (K / KC);
-  r.resident = (b_all + 2 * r.a_stage + kEpiBytes + 256 <= kSmemLimit) ? 1 : 0;
+  r.resident = (b_all + 2 * r.a_stage + kEpiBytes + 256 + 1024 <= kSmemLimit) ? 1 : 0;
   r.b_res = r.resident ? b_all : 0;
   r.b_stage = r.resident ? 0 : b_chunk;
   const size_t per = r.a_stage + r.b_stage;
   int st = int((kSmemLimit - 256 - kEpiBytes - r.b_res) / per);
   r.stages = st < 2 ? 2 : (st > kMaxStages ? kMaxStages : st);
-  r.smem = r.b_res + r.stages * per + kEpiBytes + 128;
+  r.smem = r.b_res + r.stages * per + kEpiBytes + 128 + 1024;  // +1 KB: manual 1 KB alignment
   return r;
+}
+
+__device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
+  return p + ((1024 - (smem_u32(p) & 1023)) & 1023);
 }
 
 template <class P>
 __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan plan) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  extern __shared__ __align__(1024) uint8_t smem_dyn[];
+  uint8_t* smem_raw = align1k(smem_dyn);  // SW128 atoms need 1 KB alignment
   const int Nt = plan.Nt, kStages = plan.stages;
   const size_t SB = plan.a_stage + plan.b_stage;
   float* bres = reinterpret_cast<float*>(smem_raw);  // resident B (hi/lo per chunk)
@@ -230,11 +241,12 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
       const int tm = t / ntn, n0 = (t % ntn) * Nt;
       int seg = 0;
       while (tm >= mt_seg[seg + 1]) ++seg;
-      int rows_it[2];
-      typename P::RC rc[2];
+      constexpr int kIt = 128 / (kProdWarps * 8);  // row groups of 8 per warp
+      int rows_it[kIt];
+      typename P::RC rc[kIt];
 #pragma unroll
-      for (int it = 0; it < 2; ++it) {  // rows warp*16 + it*8 + rsub
-        const int v = p.rows.begin(seg) + (tm - mt_seg[seg]) * 128 + warp * 16 + it * 8 + rsub;
+      for (int it = 0; it < kIt; ++it) {  // rows warp*8*kIt + it*8 + rsub
+        const int v = p.rows.begin(seg) + (tm - mt_seg[seg]) * 128 + warp * 8 * kIt + it * 8 + rsub;
         rows_it[it] = v < p.rows.end(seg) ? p.rows.row(v) : -1;
         if (rows_it[it] >= 0) rc[it] = p.rctx(seg, rows_it[it]);
       }
@@ -246,41 +258,40 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
           uint32_t pph = stage == 0 ? (phase ^ 1) : phase;
           mbar_wait(&empty[ps], pph);
         }
+        // image rows n0..n0+Nt of every chunk/part are contiguous (SW128 rows of 128 B)
         float4* bd = reinterpret_cast<float4*>(bres);
-        for (int c = 0; c < nchunks; ++c) {
-          const float4* bc = bsrc + size_t(c) * 2 * KC * p.Ncols / 4;
-          for (int i = tid; i < 2 * (KC / 4) * Nt; i += kProdThreads) {
-            const int part = i / ((KC / 4) * Nt), rem = i % ((KC / 4) * Nt);
-            const int g = rem / Nt, n = rem % Nt;
-            bd[size_t(c) * 2 * (KC / 4) * Nt + i] = bc[size_t(part) * (KC / 4) * p.Ncols + size_t(g) * p.Ncols + n0 + n];
+        for (int c = 0; c < nchunks; ++c)
+          for (int part = 0; part < 2; ++part) {
+            const float4* bc = bsrc + (size_t(c) * 2 + part) * p.Ncols * 8 + size_t(n0) * 8;
+            float4* bo = bd + (size_t(c) * 2 + part) * Nt * 8;
+            for (int i = tid; i < Nt * 8; i += kProdThreads) bo[i] = bc[i];
           }
-        }
         fence_proxy_async();
         asm volatile("bar.sync 1, %0;" ::"r"(kProdThreads) : "memory");
         res_key = seg * 4096 + n0;
       }
       for (int c = 0; c < nchunks; ++c) {
-        float4 x[2][2];  // [row it][k-group half]
+        const bool skip = g_tc_debug & 1;
+        float4 x[kIt][2];  // [row it][k-group half]
 #pragma unroll
-        for (int it = 0; it < 2; ++it)
+        for (int it = 0; it < kIt; ++it)
 #pragma unroll
           for (int h = 0; h < 2; ++h)
-            x[it][h] = rows_it[it] >= 0 ? p.a4(seg, rows_it[it], rc[it], c * KC + 8 * kq + 4 * h)
-                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+            x[it][h] = (rows_it[it] >= 0 && !skip) ? p.a4(seg, rows_it[it], rc[it], c * KC + 8 * kq + 4 * h)
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
         mbar_wait(&empty[stage], phase ^ 1);
         float* a_hi = reinterpret_cast<float*>(stages + stage * SB);
         float* a_lo = a_hi + 128 * KC;
+        if (!skip)
 #pragma unroll
-        for (int it = 0; it < 2; ++it)
+          for (int it = 0; it < kIt; ++it)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) put4(a_hi, a_lo, 128, 2 * kq + h, warp * 16 + it * 8 + rsub, x[it][h]);
+            for (int h = 0; h < 2; ++h) put4(a_hi, a_lo, 2 * kq + h, warp * 8 * kIt + it * 8 + rsub, x[it][h]);
         if (!plan.resident) {
           float4* b_st = reinterpret_cast<float4*>(a_lo + 128 * KC);
-          const float4* bc = bsrc + size_t(c) * 2 * KC * p.Ncols / 4;
-          for (int i = tid; i < 2 * (KC / 4) * Nt; i += kProdThreads) {
-            const int part = i / ((KC / 4) * Nt), rem = i % ((KC / 4) * Nt);
-            const int g = rem / Nt, n = rem % Nt;
-            b_st[i] = bc[size_t(part) * (KC / 4) * p.Ncols + size_t(g) * p.Ncols + n0 + n];
+          for (int part = 0; part < 2; ++part) {
+            const float4* bc = bsrc + (size_t(c) * 2 + part) * p.Ncols * 8 + size_t(n0) * 8;
+            for (int i = tid; i < Nt * 8; i += kProdThreads) b_st[part * Nt * 8 + i] = bc[i];
           }
         }
         fence_proxy_async();
@@ -305,7 +316,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
           float* a_lo = a_hi + 128 * KC;
           float* b_hi = plan.resident ? bres + size_t(c) * 2 * KC * Nt : a_lo + 128 * KC;
           float* b_lo = b_hi + Nt * KC;
-          issue_chunk(tmem + ab * acc_cols, a_hi, a_lo, 128, b_hi, b_lo, Nt, idesc, c == 0);
+          issue_chunk(tmem + ab * acc_cols, a_hi, a_lo, b_hi, b_lo, idesc, c == 0);
           mma_commit(&empty[stage]);
           if (c == nchunks - 1) mma_commit(&accfull[ab]);
         }
@@ -346,7 +357,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
         for (int it = 0; it < 8; ++it) {
           const int rl = it * 4 + (lane >> 3), c4 = (lane & 7) * 4;
           const float4 a = reinterpret_cast<const float4*>(slab + rl * kEpiLd)[lane & 7];
-          if (rows_it[it] >= 0) p.epi4(seg, rows_it[it], rc[it], n0 + j + c4, a);
+          if (rows_it[it] >= 0 && !(g_tc_debug & 2)) p.epi4(seg, rows_it[it], rc[it], n0 + j + c4, a);
         }
       }
       tc_fence_before();
@@ -377,10 +388,10 @@ constexpr int kRedThreads = (kRedProd + 1) * 32;  // + 1 MMA warp
 __host__ __device__ inline size_t red_stage_bytes(int N) { return size_t(2 * 128 * KC + 2 * N * KC) * 4; }
 constexpr size_t kRedCsum = size_t(kRedProd) * 256 * 4;
 inline int red_stages(int N) {
-  int s = int((kSmemLimit - 2048 - kRedCsum) / red_stage_bytes(N));
+  int s = int((kSmemLimit - 2048 - 1024 - kRedCsum) / red_stage_bytes(N));
   return s < 2 ? 2 : (s > kMaxStages ? kMaxStages : s);
 }
-inline size_t tc_red_smem(int N) { return red_stages(N) * red_stage_bytes(N) + kRedCsum + 2048; }
+inline size_t tc_red_smem(int N) { return red_stages(N) * red_stage_bytes(N) + kRedCsum + 2048 + 1024; }
 
 __device__ __forceinline__ float4 col4(const float4* v, int j) {  // column j of a 4x4 block
   return j == 0 ? make_float4(v[0].x, v[1].x, v[2].x, v[3].x)
@@ -392,7 +403,8 @@ __device__ __forceinline__ float4 col4(const float4* v, int j) {  // column j of
 template <class P>
 __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __restrict__ partial, int nsplit,
                                                                 int kStages) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  extern __shared__ __align__(1024) uint8_t smem_dyn[];
+  uint8_t* smem_raw = align1k(smem_dyn);
   const int N = p.Ncols;
   const size_t SB = red_stage_bytes(N);
   float* csum_smem = reinterpret_cast<float*>(smem_raw + kStages * SB);  // [kRedProd][N]
@@ -463,12 +475,12 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
       float* b_hi = a_lo + 128 * KC;
       float* b_lo = b_hi + N * KC;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 4; ++i) {  // feature rows f+jj, k-chunk `warp` (rows 4w..4w+3 of the chunk)
         const int jj = (i + lane) & 3;
-        put4(a_hi, a_lo, 128, warp, f + jj, col4(xa, jj));
+        put4(a_hi, a_lo, warp, f + jj, col4(xa, jj));
 #pragma unroll
         for (int u = 0; u < 2; ++u)
-          if (f + 128 * u < N) put4(b_hi, b_lo, N, warp, f + 128 * u + jj, col4(yb[u], jj));
+          if (f + 128 * u < N) put4(b_hi, b_lo, warp, f + 128 * u + jj, col4(yb[u], jj));
       }
       fence_proxy_async();
       mbar_arrive(&full[stage]);
@@ -520,7 +532,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
         float* a_lo = a_hi + 128 * KC;
         float* b_hi = a_lo + 128 * KC;
         float* b_lo = b_hi + N * KC;
-        issue_chunk(tmem, a_hi, a_lo, 128, b_hi, b_lo, N, idesc, i == 0);
+        issue_chunk(tmem, a_hi, a_lo, b_hi, b_lo, idesc, i == 0);
         mma_commit(&empty[stage]);
         if (i == my_chunks - 1) mma_commit(&accfull[0]);
       }
