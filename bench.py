@@ -329,7 +329,7 @@ def run_b200(args, rank, world, local_rank, dist):
         dist.broadcast(t, 0)
         idb = (C.c_uint8 * 128)(*t.tolist())
         check(lib().hmtl_comm_init(model.ctx, idb, world, rank))
-    cfg = P.TrainConfig(use_graph=True)
+    cfg = P.TrainConfig(use_graph=os.environ.get("HMTL_BENCH_EAGER", "0") != "1")
     stream_ptr = lib().hmtl_ctx_stream(model.ctx)
     ext = torch.cuda.ExternalStream(stream_ptr, device=local_rank)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")  # > 126 MB L2
@@ -431,7 +431,7 @@ def run_b200(args, rank, world, local_rank, dist):
             "config": {"workload": WORKLOAD, **HYPER, "per_gpu_batch": {"structures": batches[0].G,
                                                                         "edges": E.value, "nodes": batches[0].N},
                        "batch_counts_1gpu": counts, "head_weights": list(WEIGHTS), "parallelism": par,
-                       "l2": "flushed (256 MB write) between timed steps", "cuda_graph": True,
+                       "l2": "flushed (256 MB write) between timed steps", "cuda_graph": cfg.use_graph,
                        "final_loss": final_loss},
             "e2e": {"value": round(e2e, 2), "unit": "structures/s",
                     "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": 240},

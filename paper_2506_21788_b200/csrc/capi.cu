@@ -76,7 +76,7 @@ void free_ctx(Ctx& c) {
                   c.species, c.gslot, c.gperm, c.gnode_base, c.gedge_base, c.node_perm, c.edge_perm, c.hs, c.P,
                   c.z2, c.agg, c.vz1, c.pooled, c.ez, c.energy, c.Qf, c.zf, c.s, c.forces, c.dE, c.dF, c.dh,
                   c.dh2, c.dagg, c.dvz1, c.dzA, c.dzB, c.Sbuf, c.ds, c.dpooled, c.edA, c.edB, c.scratch,
-                  c.partial, c.bimg, c.a1, c.af0, c.sf0};
+                  c.partial, c.bimg, c.a1, c.af0, c.sf0, c.bimg_all, c.d_bjobs};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto* p : c.pool) cudaFree(p);
@@ -88,6 +88,10 @@ void free_ctx(Ctx& c) {
 }
 
 int enqueue_step(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st) {
+  if (!c.bimg_ready && c.use_tc) {  // record this step's B-image jobs (call order is fixed)
+    c.bjobs.clear();
+    c.bimg_recording = true;
+  }
   launch_prep(c, st);
   launch_nbr(c, st);
   launch_forward(c, st);
@@ -294,6 +298,10 @@ int hmtl_set_block(hmtl_ctx* h, int which, const float* host) {
   if (int rc = block_span(h->c, which, &off, &n)) return rc;
   cudaSetDevice(h->c.device);
   HMTL_CUDA(cudaMemcpy(h->c.params + off, host, n * sizeof(float), cudaMemcpyHostToDevice));
+  if (h->c.bimg_ready) {  // prebuilt B images are stale now
+    launch_bimg_all(h->c, h->c.stream);
+    HMTL_CUDA(cudaStreamSynchronize(h->c.stream));
+  }
   return 0;
 }
 int hmtl_get_block(hmtl_ctx* h, int which, float* host) {
@@ -447,6 +455,11 @@ int hmtl_train_step(hmtl_ctx* h, const hmtl_train_cfg* cfg, void* stream) {
   if (c.step_exec && std::memcmp(&c.graph_cfg, cfg, sizeof *cfg) != 0) {
     cudaGraphExecDestroy(c.step_exec);
     c.step_exec = nullptr;
+  }
+  if (!c.bimg_ready && c.use_tc) {  // first step: eager, records the batched B-image jobs
+    if (int rc = enqueue_step(c, *cfg, st)) return rc;
+    HMTL_CUDA(cudaGetLastError());
+    return 0;
   }
   if (!c.step_exec) {
     cudaGraph_t g;

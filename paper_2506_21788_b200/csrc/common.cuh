@@ -57,6 +57,20 @@ __device__ __forceinline__ float silu_grad(float x) {
   return s * (1.f + x * (1.f - s));
 }
 
+// Sum of n values src[q*stride], q = 0..n-1, with 8 independent accumulators
+// (8 loads in flight) combined in a fixed tree: the association depends only on
+// n, so results are bit-reproducible run to run.
+__device__ __forceinline__ float sum_strided(const float* __restrict__ src, int n, size_t stride) {
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  int q = 0;
+  for (; q + 8 <= n; q += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] += src[size_t(q + j) * stride];
+  }
+  for (int j = 0; q < n; ++q, ++j) a[j] += src[size_t(q) * stride];
+  return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+}
+
 // ---- row sets: identity rows [0, *count) or head-sorted segments via a perm
 struct RowSet {
   const int* perm = nullptr;     // virtual -> actual row; nullptr = identity
@@ -211,10 +225,7 @@ __global__ void gemm_atb_reduce(P p, const float* __restrict__ partial, int nspl
        idx += size_t(gridDim.x) * blockDim.x) {
     const int seg = int(idx / KN);
     const size_t kn = idx % KN;
-    const float* src = partial + size_t(seg) * nsplit * KN + kn;
-    float s = 0.f;
-    for (int q = 0; q < nsplit; ++q) s += src[size_t(q) * KN];
-    p.store(seg, int(kn / p.Ncols), int(kn % p.Ncols), s);
+    p.store(seg, int(kn / p.Ncols), int(kn % p.Ncols), sum_strided(partial + size_t(seg) * nsplit * KN + kn, nsplit, KN));
   }
 }
 

@@ -12,6 +12,19 @@ namespace hmtl_b200 {
 
 struct Comm;  // comm.cu (NCCL)
 
+// Descriptor of a GEMM B operand B(k, n) read from a weight tensor:
+// base[seg*seg_stride + k*sk + n*sn], optionally split in two sources along n
+// (split 1) or k (split 2) at `at` (the second source sees n-at / k-at).
+struct BDesc {
+  const float* base0;
+  const float* base1;
+  int split, at;
+  long long sk, sn;
+  int K, N, nseg;
+  long long seg_stride;
+  float* out;  // image destination (filled in when batched)
+};
+
 // Optional per-launch CUDA-event timing (hmtl_profile); off in timed steps.
 struct ProfRec {
   std::string name;
@@ -68,6 +81,16 @@ struct Ctx {
   float* bimg = nullptr;  // tcgen05 B-operand images (hi/lo, K-major)
   size_t bimg_cap = 0;
   bool use_tc = true;     // tcgen05 path for GEMMs whose shapes allow it
+  // batched B-image builds: recorded in call order during the first step, rebuilt
+  // in one launch after every AdamW (weights only change there) and on set_block
+  std::vector<BDesc> bjobs;
+  bool bimg_ready = false;
+  bool bimg_recording = false;  // set by a train step before the images exist
+  int bimg_idx = 0;
+  float* bimg_all = nullptr;
+  size_t bimg_all_cap = 0;
+  BDesc* d_bjobs = nullptr;
+  int n_djobs = 0;
   bool store_a1 = false;  // forward producer materialises a1 = silu(z1) [L][E][H]
   bool store_af0 = false; // ... and silu(zf0) [E][W]
   float *a1 = nullptr, *af0 = nullptr, *sf0 = nullptr;
@@ -99,6 +122,7 @@ void launch_loss(Ctx& c, float w_e, float w_f, cudaStream_t st);
 void launch_backward(Ctx& c, cudaStream_t st);  // ModelT::backward (upstreams in c.dE/c.dF)
 void launch_adamw(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st);
 void launch_debug_z1(Ctx& c, int layer, float* out, cudaStream_t st);
+void launch_bimg_all(Ctx& c, cudaStream_t st);  // rebuild every recorded B image
 
 int comm_sync_grads(Ctx& c, cudaStream_t st);
 

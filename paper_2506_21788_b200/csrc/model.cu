@@ -78,6 +78,7 @@ struct HeadG {
 // ================================================================ forward
 // P = h [W1a | W1b]
 struct PProb {
+  BDesc bd() const { return BDesc{W1, W1 + size_t(H) * H, 1, H, H, 1, K, Ncols, 1, 0, nullptr}; }
   static constexpr const char* kName = "fwd.node_P";
   __device__ float4 a4(int, int r, int k) const { return ld4(h + size_t(r) * H + k); }
   __device__ void epi4(int, int r, int n, float4 acc) const { st4(P + size_t(r) * 2 * H + n, acc); }
@@ -92,6 +93,7 @@ struct PProb {
 
 // z2 = silu(z1) W2 + b2   (hmtl/model.hpp:398-404)
 struct MsgProb {
+  BDesc bd() const { return BDesc{W2, nullptr, 0, 0, H, 1, K, Ncols, 1, 0, nullptr}; }
   static constexpr const char* kName = "fwd.edge_msg_gemm";
   struct RC {
     int d, s;
@@ -126,6 +128,7 @@ struct MsgProb {
 
 // vz1 = [h, agg] nW1 + nb1   (hmtl/model.hpp:412-420)
 struct Node1Prob {
+  BDesc bd() const { return BDesc{W, nullptr, 0, 0, H, 1, K, Ncols, 1, 0, nullptr}; }
   static constexpr const char* kName = "fwd.node_mlp1";
   __device__ float4 a4(int, int r, int k) const {
     return k < H ? ld4(h + size_t(r) * H + k) : ld4(agg + size_t(r) * H + k - H);
@@ -142,6 +145,14 @@ struct Node1Prob {
 
 // h' = h + (silu(vz1) nW2 + nb2)   (hmtl/model.hpp:421-426, residual)
 struct Node2Prob {
+  struct Aux {
+    float4 h, b;
+  };
+  __device__ Aux epi_aux(int, int r, int n) const { return Aux{ld4(h + size_t(r) * H + n), ld4(bias + n)}; }
+  __device__ void epi4a(int, int r, int n, float4 acc, const Aux& a) const {
+    st4(hn + size_t(r) * H + n, add4(a.h, add4(acc, a.b)));  // h + (acc + b), as the SIMT path
+  }
+  BDesc bd() const { return BDesc{W, nullptr, 0, 0, H, 1, K, Ncols, 1, 0, nullptr}; }
   static constexpr const char* kName = "fwd.node_mlp2";
   __device__ float4 a4(int, int r, int k) const { return silu4(ld4(vz1 + size_t(r) * H + k)); }
   __device__ void epi4(int, int r, int n, float4 acc) const {
@@ -160,6 +171,7 @@ struct Node2Prob {
 
 // energy MLP layer i over graph rows of each head (mlp_forward_, :282-306)
 struct EnergyProb {
+  BDesc bd() const { return BDesc{Wt.base + Wt.off, nullptr, 0, 0, Ncols, 1, K, Ncols, rows.nseg, (long long)Wt.PH, nullptr}; }
   static constexpr const char* kName = "fwd.energy_mlp";
   RowSet rows;
   int K, Ncols, H, W, layer, last;
@@ -179,6 +191,7 @@ struct EnergyProb {
 
 // Qf = h_L Wf0[:H]  (node rows per head)
 struct QfProb {
+  BDesc bd() const { return BDesc{Wt.base + Wt.off, nullptr, 0, 0, W, 1, K, Ncols, rows.nseg, (long long)Wt.PH, nullptr}; }
   static constexpr const char* kName = "fwd.force_Qf";
   __device__ float4 a4(int, int r, int k) const { return ld4(h + size_t(r) * H + k); }
   __device__ void epi4(int, int r, int n, float4 acc) const { st4(Qf + size_t(r) * W + n, acc); }
@@ -194,6 +207,7 @@ struct QfProb {
 
 // force MLP layer i >= 1 over edge rows per head; last layer writes s_e
 struct ForceProb {
+  BDesc bd() const { return BDesc{Wt.base + Wt.off, nullptr, 0, 0, Ncols, 1, K, Ncols, rows.nseg, (long long)Wt.PH, nullptr}; }
   static constexpr const char* kName = "fwd.force_edge_gemm";
   struct RC {
     int d, s;
@@ -336,9 +350,22 @@ struct RCOf<P, std::void_t<typename P::RC>> {
   static constexpr bool has = true;
 };
 
+struct NoAux {};
+template <class P, class = void>
+struct AuxOf {
+  using type = NoAux;
+  static constexpr bool has = false;
+};
+template <class P>
+struct AuxOf<P, std::void_t<typename P::Aux>> {
+  using type = typename P::Aux;
+  static constexpr bool has = true;
+};
+
 template <class P>
 struct TcRow {
   using RC = typename RCOf<P>::type;
+  using Aux = typename AuxOf<P>::type;
   RowSet rows;
   int K, Ncols;
   const float* bimg;
@@ -353,8 +380,14 @@ struct TcRow {
     else if constexpr (HasA4<P>::value) return p.a4(seg, row, k);
     else return make_float4(p.a(seg, row, k), p.a(seg, row, k + 1), p.a(seg, row, k + 2), p.a(seg, row, k + 3));
   }
-  __device__ __forceinline__ void epi4(int seg, int row, const RC& rc, int n, float4 acc) const {
-    if constexpr (RCOf<P>::has) {
+  __device__ __forceinline__ Aux epi_aux(int seg, int row, const RC&, int n) const {
+    if constexpr (AuxOf<P>::has) return p.epi_aux(seg, row, n);
+    else return Aux{};
+  }
+  __device__ __forceinline__ void epi4(int seg, int row, const RC& rc, int n, float4 acc, const Aux& ax) const {
+    if constexpr (AuxOf<P>::has) {
+      p.epi4a(seg, row, n, acc, ax);
+    } else if constexpr (RCOf<P>::has) {
       p.epi4c(seg, row, rc, n, acc);
     } else if constexpr (HasEpi4<P>::value) {
       p.epi4(seg, row, n, acc);
@@ -408,6 +441,30 @@ struct TcRed {
   __device__ __forceinline__ void store(int seg, int k, int n, float v) const { p.store(seg, k, n, v); }
 };
 
+// one launch builds every B image of the step: blockIdx.y = job
+__global__ void bimg_all_kernel(const BDesc* __restrict__ jobs) {
+  const BDesc J = jobs[blockIdx.y];
+  const int K = J.K, N = J.N;
+  const size_t total = size_t(J.nseg) * K * N;
+  const bool kfast = J.sk == 1;  // walk the contiguous source dimension
+  for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < total; t += size_t(gridDim.x) * blockDim.x) {
+    const int seg = int(t / (size_t(K) * N));
+    const int rem = int(t % (size_t(K) * N));
+    const int k = kfast ? rem % K : rem / N, n = kfast ? rem / K : rem % N;
+    int kk = k, nn = n;
+    const float* b = J.base0;
+    if (J.split == 1 && n >= J.at) b = J.base1, nn = n - J.at;
+    if (J.split == 2 && k >= J.at) b = J.base1, kk = k - J.at;
+    const float x = b[size_t(seg) * J.seg_stride + size_t(kk) * J.sk + size_t(nn) * J.sn];
+    const float h = tc::tf32_hi(x);
+    const int ch = k / tc::KC, c16 = (k % tc::KC) / 4, q = k % 4;
+    float* o = J.out + size_t(seg) * 2 * K * N + size_t(ch) * 2 * tc::KC * N;
+    const uint32_t off = tc::sw128(n, c16) / 4 + q;
+    o[off] = h;
+    o[size_t(tc::KC) * N + off] = x - h;
+  }
+}
+
 template <class Kern>
 void set_smem(Kern k, size_t bytes) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
@@ -419,8 +476,19 @@ void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& 
   const bool use_tc = c.use_tc && p.K % tc::KC == 0 && p.Ncols % 32 == 0 && p.Ncols <= 256 &&
                       size_t(nseg) * 2 * p.K * p.Ncols <= c.bimg_cap;
   if (use_tc) {
-    bimg_prob_kernel<P><<<gridn((long long)nseg * p.K * p.Ncols, 256, sm * 4), 256, 0, st>>>(p, c.bimg, nseg);
-    TcRow<P> q{p.rows, p.K, p.Ncols, c.bimg, size_t(2) * p.K * p.Ncols, p};
+    const float* img = c.bimg;
+    const int idx = c.bimg_idx++;
+    if (c.bimg_ready && idx < int(c.bjobs.size())) {
+      img = c.bjobs[idx].out;  // prebuilt by the batched builder after the last weight update
+    } else {
+      bimg_prob_kernel<P><<<gridn((long long)nseg * p.K * p.Ncols, 256, sm * 4), 256, 0, st>>>(p, c.bimg, nseg);
+      if (c.bimg_recording) {
+        BDesc d = p.bd();
+        d.nseg = nseg;
+        c.bjobs.push_back(d);
+      }
+    }
+    TcRow<P> q{p.rows, p.K, p.Ncols, img, size_t(2) * p.K * p.Ncols, p};
     const long long mtiles = (rows_cap + 127) / 128 + nseg;
     // split N when there are too few row tiles to fill the GPU (node-row GEMMs)
     int Nt = p.Ncols;
@@ -555,7 +623,32 @@ __global__ void edge_af0_kernel(const DevHdr* hdr, const float* __restrict__ Qf,
 }
 }
 
+void launch_bimg_all(Ctx& c, cudaStream_t st) {
+  if (c.bjobs.empty()) return;
+  if (!c.d_bjobs || c.n_djobs < int(c.bjobs.size())) {  // lay out the image buffer once
+    size_t total = 0;
+    for (auto& j : c.bjobs) total += size_t(2) * j.K * j.N * j.nseg;
+    if (c.bimg_all) cudaFree(c.bimg_all);
+    if (c.d_bjobs) cudaFree(c.d_bjobs);
+    cudaMalloc(&c.bimg_all, total * 4);
+    c.bimg_all_cap = total;
+    size_t off = 0;
+    for (auto& j : c.bjobs) {
+      j.out = c.bimg_all + off;
+      off += size_t(2) * j.K * j.N * j.nseg;
+    }
+    cudaMalloc(&c.d_bjobs, c.bjobs.size() * sizeof(BDesc));
+    cudaMemcpy(c.d_bjobs, c.bjobs.data(), c.bjobs.size() * sizeof(BDesc), cudaMemcpyHostToDevice);
+    c.n_djobs = int(c.bjobs.size());
+  }
+  Prof pr(c, "bimg_all", st);
+  bimg_all_kernel<<<dim3(16, c.n_djobs), 256, 0, st>>>(c.d_bjobs);
+  c.bimg_ready = true;
+  c.bimg_recording = false;
+}
+
 void launch_forward(Ctx& c, cudaStream_t st) {
+  c.bimg_idx = 0;
   const int H = c.H, W = c.W, L = c.L, D = c.D, sm = c.sm_count;
   const size_t NH = size_t(c.Nc) * H, EH = size_t(c.Ec) * H;
   {
@@ -725,6 +818,7 @@ struct EGradProb {  // energy MLP layer i weight+bias
 };
 // dx = dz W^T, epilogue dz_prev = dx * silu'(z_prev) (or plain dpooled)
 struct EDxProb {
+  BDesc bd() const { return BDesc{Wt.base + Wt.off, nullptr, 0, 0, 1, K, K, Ncols, rows.nseg, (long long)Wt.PH, nullptr}; }
   static constexpr const char* kName = "bwd.energy_dx";
   RowSet rows;
   int K, Ncols, W, H;  // K = out_i, Ncols = in_i
@@ -771,6 +865,7 @@ struct FGradProb {  // force MLP layer i >= 1 weight+bias (edge rows per head)
   __device__ void store(int seg, int k, int n, float v) const { G.at(seg)[size_t(k) * Ncols + n] = v; }
 };
 struct FDxProb {  // dz_{i-1} = (dz_i W_i^T) * silu'(z_{i-1})
+  BDesc bd() const { return BDesc{Wt.base + Wt.off, nullptr, 0, 0, 1, K, K, Ncols, rows.nseg, (long long)Wt.PH, nullptr}; }
   static constexpr const char* kName = "bwd.force_edge_dx";
   struct RC {
     int d, s;
@@ -841,6 +936,12 @@ struct F0EdgeGrad {  // g_Wf0[H] (distance row) and g_bf0 (edge rows per head)
   __device__ void store(int seg, int k, int n, float v) const { G.at(seg)[size_t(k) * W + n] = v; }
 };
 struct F0Dh {  // dh += T Wf0[:H]^T  (node rows per head)
+  struct Aux {
+    float4 v;
+  };
+  __device__ Aux epi_aux(int, int r, int n) const { return Aux{ld4(dh + size_t(r) * H + n)}; }
+  __device__ void epi4a(int, int r, int n, float4 acc, const Aux& a) const { st4(dh + size_t(r) * H + n, add4(a.v, acc)); }
+  BDesc bd() const { return BDesc{Wt.base + Wt.off, nullptr, 0, 0, 1, W, K, Ncols, rows.nseg, (long long)Wt.PH, nullptr}; }
   static constexpr const char* kName = "bwd.force0_dh";
   __device__ float4 a4(int, int r, int k) const { return ld4(T + size_t(r) * W + k); }
   __device__ void epi4(int, int r, int n, float4 acc) const {
@@ -859,6 +960,12 @@ struct F0Dh {  // dh += T Wf0[:H]^T  (node rows per head)
 
 // ---- encoder layer backward problems (shared weights, identity rows)
 struct L1Prob {  // dvz1 = (dh nW2^T) * silu'(vz1)
+  struct Aux {
+    float4 v;
+  };
+  __device__ Aux epi_aux(int, int r, int n) const { return Aux{sgrad4(ld4(vz1 + size_t(r) * H + n))}; }
+  __device__ void epi4a(int, int r, int n, float4 acc, const Aux& a) const { st4(dvz1 + size_t(r) * H + n, mul4(acc, a.v)); }
+  BDesc bd() const { return BDesc{W, nullptr, 0, 0, 1, H, K, Ncols, 1, 0, nullptr}; }
   static constexpr const char* kName = "bwd.node_dvz1";
   __device__ float4 a4(int, int r, int k) const { return ld4(dh + size_t(r) * H + k); }
   __device__ void epi4(int, int r, int n, float4 acc) const {
@@ -907,6 +1014,17 @@ struct L3Prob {  // [g_nW1; g_nb1] = [h, agg, 1]^T dvz1
   __device__ void store(int, int k, int n, float v) const { G[size_t(k) * H + n] = v; }
 };
 struct L4Prob {  // dv = dvz1 nW1^T ; dh2 = dh + dv[:, :H] ; dagg = dv[:, H:]
+  struct Aux {
+    float4 v;
+  };
+  __device__ Aux epi_aux(int, int r, int n) const {
+    return Aux{n < H ? ld4(dh + size_t(r) * H + n) : make_float4(0.f, 0.f, 0.f, 0.f)};
+  }
+  __device__ void epi4a(int, int r, int n, float4 acc, const Aux& a) const {
+    if (n < H) st4(dh2 + size_t(r) * H + n, add4(a.v, acc));
+    else st4(dagg + size_t(r) * H + n - H, acc);
+  }
+  BDesc bd() const { return BDesc{W, nullptr, 0, 0, 1, H, K, Ncols, 1, 0, nullptr}; }
   static constexpr const char* kName = "bwd.node_dv";
   __device__ float4 a4(int, int r, int k) const { return ld4(dvz1 + size_t(r) * H + k); }
   __device__ void epi4(int, int r, int n, float4 acc) const {
@@ -952,6 +1070,12 @@ struct L6Prob {  // [g_eW2; g_eb2] = [silu(z1), 1]^T dz2   (E rows)
   __device__ void store(int, int k, int n, float v) const { G[size_t(k) * H + n] = v; }
 };
 struct L7Prob {  // dz1 = (dz2 eW2^T) * silu'(z1)
+  struct Aux {
+    float4 v;
+  };
+  __device__ Aux epi_aux(int, int e, int n) const { return Aux{ld4(s1p + size_t(e) * H + n)}; }
+  __device__ void epi4a(int, int e, int n, float4 acc, const Aux& a) const { st4(dz1 + size_t(e) * H + n, mul4(acc, a.v)); }
+  BDesc bd() const { return BDesc{W, nullptr, 0, 0, 1, H, K, Ncols, 1, 0, nullptr}; }
   static constexpr const char* kName = "bwd.edge_dz1_gemm";
   struct RC {
     int d, s;
@@ -1022,6 +1146,12 @@ struct L10Prob {  // g_W1a = h^T S_dst, g_W1b = h^T S_src
   }
 };
 struct L11Prob {  // dh2 += S_dst W1a^T + S_src W1b^T
+  struct Aux {
+    float4 v;
+  };
+  __device__ Aux epi_aux(int, int r, int n) const { return Aux{ld4(dh2 + size_t(r) * H + n)}; }
+  __device__ void epi4a(int, int r, int n, float4 acc, const Aux& a) const { st4(dh2 + size_t(r) * H + n, add4(a.v, acc)); }
+  BDesc bd() const { return BDesc{W1, W1 + size_t(H) * H, 2, H, 1, H, K, Ncols, 1, 0, nullptr}; }
   static constexpr const char* kName = "bwd.edge_dh_gemm";
   __device__ float4 a4(int, int r, int k) const { return ld4(S + size_t(r) * 2 * H + k); }
   __device__ void epi4(int, int r, int n, float4 acc) const {
@@ -1213,9 +1343,8 @@ __global__ void colsum2_reduce(RowSet rows, const float* __restrict__ partial, i
   const int seg = blockIdx.y;
   const int nchunks = (rows.end(seg) - rows.begin(seg) + kCs2Rows - 1) / kCs2Rows;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 2 * C; t += gridDim.x * blockDim.x) {
-    float acc = 0.f;
-    for (int k = 0; k < nchunks; ++k) acc += partial[(size_t(seg) * nchunk_cap + k) * 2 * C + t];
-    G[seg * seg_stride + t] = acc;  // rows [w; bias] are contiguous in the layout
+    // rows [w; bias] are contiguous in the layout
+    G[seg * seg_stride + t] = sum_strided(partial + size_t(seg) * nchunk_cap * 2 * C + t, nchunks, size_t(2) * C);
   }
 }
 
@@ -1231,8 +1360,18 @@ __global__ void embed_grad_part(const DevHdr* hdr, const uint8_t* __restrict__ s
   for (int t = threadIdx.x; t < NS * H; t += blockDim.x) acc[t] = 0.f;
   __syncthreads();
   const int i1 = min(i0 + kEmbChunk, N);
-  for (int c = threadIdx.x; c < H; c += blockDim.x)
-    for (int i = i0; i < i1; ++i) acc[species[i] * H + c] += dh[size_t(i) * H + c];
+  for (int c = threadIdx.x; c < H; c += blockDim.x) {
+    int i = i0;
+    for (; i + 8 <= i1; i += 8) {  // 8 loads in flight, updates in ascending node order
+      float v[8];
+      int sp[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = dh[size_t(i + j) * H + c], sp[j] = species[i + j];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[sp[j] * H + c] += v[j];
+    }
+    for (; i < i1; ++i) acc[species[i] * H + c] += dh[size_t(i) * H + c];
+  }
   __syncthreads();
   for (int t = threadIdx.x; t < NS * H; t += blockDim.x) partial[size_t(chunk) * NS * H + t] = acc[t];
 }
@@ -1240,9 +1379,7 @@ __global__ void embed_grad_reduce(const DevHdr* hdr, const float* __restrict__ p
                                   int NS) {
   const int nchunks = (hdr->N + kEmbChunk - 1) / kEmbChunk;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < NS * H; t += gridDim.x * blockDim.x) {
-    float a = 0.f;
-    for (int k = 0; k < nchunks; ++k) a += partial[size_t(k) * NS * H + t];
-    G[t] = a;
+    G[t] = sum_strided(partial + t, nchunks, size_t(NS) * H);
   }
 }
 
@@ -1470,6 +1607,11 @@ __global__ void adamw_kernel(const DevHdr* hdr, float* __restrict__ p, const flo
 }  // namespace
 
 void launch_adamw(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st) {
+  struct Rebuild {
+    Ctx& c;
+    cudaStream_t st;
+    ~Rebuild() { launch_bimg_all(c, st); }  // weights changed: refresh the B images (after the update)
+  } rebuild{c, st};
   adam_tick<<<1, 1, 0, st>>>(c.hdr);
   {
     Prof pr(c, "adamw", st);

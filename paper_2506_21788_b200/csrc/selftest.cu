@@ -18,11 +18,13 @@ struct StRow {
   const float* X;
   float* C;
   struct RC {};
+  struct Aux {};
   __device__ RC rctx(int, int) const { return RC{}; }
+  __device__ Aux epi_aux(int, int, const RC&, int) const { return Aux{}; }
   __device__ float4 a4(int, int r, const RC&, int k) const {
     return *reinterpret_cast<const float4*>(X + size_t(r) * K + k);
   }
-  __device__ void epi4(int, int r, const RC&, int n, float4 acc) const {
+  __device__ void epi4(int, int r, const RC&, int n, float4 acc, const Aux&) const {
     *reinterpret_cast<float4*>(C + size_t(r) * Ncols + n) = acc;
   }
 };

@@ -150,7 +150,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // P must provide: RowSet rows; int K, Ncols; const float* bimg; size_t bimg_seg;
 //   typename P::RC rctx(int seg, int row) const;                    // per-row gather context
 //   float4 a4(int seg, int row, const RC&, int k) const;           // A(row, k..k+3)
-//   void epi4(int seg, int row, const RC&, int n, float4 acc) const;  // C(row, n..n+3)
+//   typename P::Aux epi_aux(int seg, int row, const RC&, int n) const;  // prefetched epilogue inputs
+//   void epi4(int seg, int row, const RC&, int n, float4 acc, const Aux&) const;  // C(row, n..n+3)
 constexpr int kMaxStages = 4;
 // engine ablation switches for hmtl_selftest_time (bit0: producers skip A loads/stores,
 // bit1: epilogue skips global stores); always 0 on the training path.
@@ -342,12 +343,26 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
         rows_it[it] = v < p.rows.end(seg) ? p.rows.row(v) : -1;
         if (rows_it[it] >= 0) rc[it] = p.rctx(seg, rows_it[it]);
       }
+      // epilogue operands that do not depend on the accumulator (residuals, saved
+      // activations) are loaded one 32-column slab ahead -- the first slab's
+      // before waiting for the MMAs
+      typename P::Aux aux[2][8];
+      const int c4 = (lane & 7) * 4;
+#pragma unroll
+      for (int it = 0; it < 8; ++it)
+        if (rows_it[it] >= 0) aux[0][it] = p.epi_aux(seg, rows_it[it], rc[it], n0 + c4);
       mbar_wait(&accfull[ab], aphase);
       tc_fence_after();
       for (int j = 0; j < Nt; j += 32) {
+        const int cur = (j >> 5) & 1;
         float acc[32];
         __syncwarp();
         tmem_ld32(tmem + ab * acc_cols + (uint32_t(q * 32) << 16) + j, acc);
+        if (j + 32 < Nt) {
+#pragma unroll
+          for (int it = 0; it < 8; ++it)
+            if (rows_it[it] >= 0) aux[cur ^ 1][it] = p.epi_aux(seg, rows_it[it], rc[it], n0 + j + 32 + c4);
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           reinterpret_cast<float4*>(slab + lane * kEpiLd)[i] =
@@ -355,9 +370,9 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
         __syncwarp();
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
-          const int rl = it * 4 + (lane >> 3), c4 = (lane & 7) * 4;
+          const int rl = it * 4 + (lane >> 3);
           const float4 a = reinterpret_cast<const float4*>(slab + rl * kEpiLd)[lane & 7];
-          if (rows_it[it] >= 0 && !(g_tc_debug & 2)) p.epi4(seg, rows_it[it], rc[it], n0 + j + c4, a);
+          if (rows_it[it] >= 0 && !(g_tc_debug & 2)) p.epi4(seg, rows_it[it], rc[it], n0 + j + c4, a, aux[cur][it]);
         }
       }
       tc_fence_before();
@@ -555,10 +570,7 @@ __global__ void tc_red_reduce(P p, const float* __restrict__ partial, int nsplit
        idx += size_t(gridDim.x) * blockDim.x) {
     const int seg = int(idx / KN);
     const size_t nm = idx % KN;
-    const float* src = partial + size_t(seg) * nsplit * KN + nm;
-    float s = 0.f;
-    for (int q = 0; q < nsplit; ++q) s += src[size_t(q) * KN];
-    p.store(seg, int(nm % Mo), int(nm / Mo), s);
+    p.store(seg, int(nm % Mo), int(nm / Mo), sum_strided(partial + size_t(seg) * nsplit * KN + nm, nsplit, KN));
   }
 }
 
