@@ -231,6 +231,8 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   const size_t kn_head = std::max({(H + 1) * W, (W + 1) * W, H * W, 2 * W});
   c.partial_cap = std::max(size_t(64) * kn_shared, size_t(c.S) * 64 * kn_head);
   c.partial_cap = std::max(c.partial_cap, size_t(std::max(c.S, 1)) * 128 * (2 * std::max(H, W) + 1) * std::max(H, W));
+  // chunked column sums (colsum2, force output layer): [S][E/128 chunks][2*max(H,W)+1]
+  c.partial_cap = std::max(c.partial_cap, size_t(std::max(c.S, 1)) * size_t((E + 127) / 128 + 1) * (2 * std::max(H, W) + 1));
   A(&c.partial, c.partial_cap);
   c.bimg_cap = size_t(std::max(c.S, 2)) * 2 * (2 * std::max(H, W)) * (2 * std::max(H, W));
   A(&c.bimg, c.bimg_cap);

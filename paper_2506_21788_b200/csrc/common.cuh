@@ -71,6 +71,28 @@ __device__ __forceinline__ float sum_strided(const float* __restrict__ src, int 
   return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
 }
 
+// Deterministic split-partial reduction: out(seg, t) = sum_{q < f.count(seg)}
+// src[seg*seg_stride + q*stride + t] for t < T.  CTA = 32 consecutive t of one
+// segment (coalesced 128 B rows); warp w sums q = w, w+8, ... with sum_strided,
+// and the 8 warp sums combine in a fixed tree, so the association depends only
+// on the count.  8x the memory-level parallelism of one thread per output.
+template <class F>
+__global__ void __launch_bounds__(256) split_reduce_kernel(const float* __restrict__ src, size_t seg_stride,
+                                                           size_t stride, int T, F f) {
+  __shared__ float red[8][32];
+  const int seg = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 32 + lane;
+  const int n = f.count(seg);
+  float v = 0.f;
+  if (t < T && warp < n)
+    v = sum_strided(src + size_t(seg) * seg_stride + size_t(warp) * stride + t, (n - warp + 7) / 8, 8 * stride);
+  red[warp][lane] = v;
+  __syncthreads();
+  if (warp == 0 && t < T)
+    f.store(seg, t, ((red[0][lane] + red[1][lane]) + (red[2][lane] + red[3][lane])) +
+                        ((red[4][lane] + red[5][lane]) + (red[6][lane] + red[7][lane])));
+}
+
 // ---- row sets: identity rows [0, *count) or head-sorted segments via a perm
 struct RowSet {
   const int* perm = nullptr;     // virtual -> actual row; nullptr = identity

@@ -520,8 +520,7 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
       dim3 grid(mtiles, ns, p.rows.nseg);
       tc::tc_red_kernel<TcRed<P>><<<grid, tc::kRedThreads, smem, st>>>(q, c.partial, ns,
                                                                         tc::red_stages(p.Ncols));
-      const long long total = (long long)(M + P::kBias) * p.Ncols * p.rows.nseg;
-      tc::tc_red_reduce<TcRed<P>><<<gridn(total, 256, c.sm_count * 8), 256, 0, st>>>(q, c.partial, ns);
+      tc::tc_red_reduce(q, c.partial, ns, st);
       return;
     }
   }
@@ -622,6 +621,41 @@ __global__ void edge_af0_kernel(const DevHdr* hdr, const float* __restrict__ Qf,
   }
 }
 }
+
+namespace {
+// force MLP output layer (width 1; mlp_forward_'s last layer, hmtl/model.hpp:282-306):
+// s_e = x_e . w_slot + b_slot, x_e = silu(zf_{i-1}[e]) (act) or the materialised
+// silu(zf0).  8 lanes per edge, fixed lane split + xor tree: deterministic.
+__global__ void force_out_fwd_kernel(const DevHdr* hdr, const float* __restrict__ x, int act,
+                                     const int* __restrict__ dst, const int* __restrict__ node_graph,
+                                     const int* __restrict__ gslot, const float* __restrict__ heads, size_t PH,
+                                     size_t off_w, size_t off_b, float* __restrict__ s, int W) {
+  const int l8 = threadIdx.x & 7;
+  const unsigned gm = 0xffu << (threadIdx.x & 24);
+  const long long E = hdr->E;
+  const long long step = ((long long)gridDim.x * blockDim.x) >> 3;
+  for (long long e = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3; e < E; e += step) {
+    const float* hb = heads + size_t(gslot[node_graph[dst[e]]]) * PH;
+    const float* xr = x + size_t(e) * W;
+    float acc = 0.f;
+    for (int k = l8 * 4; k < W; k += 32) {
+      float4 v = ld4(xr + k);
+      if (act) v = silu4(v);
+      const float4 w = ldu4(hb + off_w + k);
+      acc += v.x * w.x + v.y * w.y + v.z * w.z + v.w * w.w;
+    }
+    acc += __shfl_xor_sync(gm, acc, 4);
+    acc += __shfl_xor_sync(gm, acc, 2);
+    acc += __shfl_xor_sync(gm, acc, 1);
+    if (l8 == 0) s[e] = acc + hb[off_b];
+  }
+}
+}  // namespace
+
+namespace {
+// width-1 force output layer through the dedicated kernels (x row = W floats, 16 B aligned)
+bool force_out_fast(const Ctx& c, int i) { return c.W % 4 == 0 && c.W <= 256 && (i >= 2 || c.store_af0); }
+}  // namespace
 
 void launch_bimg_all(Ctx& c, cudaStream_t st) {
   if (c.bjobs.empty()) return;
@@ -725,6 +759,14 @@ void launch_forward(Ctx& c, cudaStream_t st) {
   }
   for (int i = 1; i < D; ++i) {
     const int last = i == D - 1;
+    if (last && force_out_fast(c, i)) {
+      Prof pr(c, "fwd.force_out", st);
+      force_out_fwd_kernel<<<gridn((long long)c.Ec * 8, 256, sm * 16), 256, 0, st>>>(
+          c.hdr, i >= 2 ? c.zf + size_t(i - 2) * c.Ec * W : c.af0, i >= 2, c.edge_dst, c.node_graph, c.gslot,
+          c.head_params(), c.PH, c.head_off("force.W" + std::to_string(i)),
+          c.head_off("force.b" + std::to_string(i)), c.s, W);
+      continue;
+    }
     ForceProb q{edge_rows_by_head(c), W, last ? 1 : W, H, W, i, last, c.Ec, c.Qf, c.zf, c.dist, c.edge_dst,
                 c.edge_src, HeadW{c.head_params(), c.PH, wf0 + size_t(H) * W},
                 HeadW{c.head_params(), c.PH, c.head_off("force.b0")},
@@ -1292,7 +1334,7 @@ __global__ void seg2v_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr,
 // (the [distance-or-d2 ; bias] rows of a factorised first layer's gradient).
 // Deterministic: CTA (chunk, seg) owns a fixed row range, 8 warps split it in
 // fixed sub-ranges, smem combine in warp order; colsum2_reduce sums chunks in order.
-constexpr int kCs2Rows = 512;
+constexpr int kCs2Rows = 128;
 __global__ void __launch_bounds__(256) colsum2_kernel(RowSet rows, const float* __restrict__ wvec, int wstride,
                                                       const float* __restrict__ x, int C,
                                                       float* __restrict__ partial, int nchunk_cap) {
@@ -1300,6 +1342,7 @@ __global__ void __launch_bounds__(256) colsum2_kernel(RowSet rows, const float* 
   const int seg = blockIdx.y, chunk = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rb = rows.begin(seg), re = rows.end(seg);
   const int r0 = rb + chunk * kCs2Rows;
+  if (r0 >= re) return;  // beyond this segment: not counted by the reduce
   const int sub = kCs2Rows / 8;
   const int w0 = r0 + warp * sub, w1 = min(w0 + sub, re);
   for (int c = lane * 4, u = 0; c < C; c += 128, ++u) {
@@ -1338,15 +1381,93 @@ __global__ void __launch_bounds__(256) colsum2_kernel(RowSet rows, const float* 
     st4(out + which * C + cg * 4, acc);
   }
 }
-__global__ void colsum2_reduce(RowSet rows, const float* __restrict__ partial, int nchunk_cap, int C,
-                               float* __restrict__ G, size_t seg_stride) {
-  const int seg = blockIdx.y;
-  const int nchunks = (rows.end(seg) - rows.begin(seg) + kCs2Rows - 1) / kCs2Rows;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 2 * C; t += gridDim.x * blockDim.x) {
-    // rows [w; bias] are contiguous in the layout
-    G[seg * seg_stride + t] = sum_strided(partial + size_t(seg) * nchunk_cap * 2 * C + t, nchunks, size_t(2) * C);
+// force MLP output layer backward (width 1), for the edge rows of head segment seg:
+//   dz_{i-1}[e] = (ds_e w_seg) * silu'(z_{i-1}[e])                   (elementwise)
+//   partial[seg][chunk] = [sum_e ds_e silu(z_{i-1}[e]) ; sum_e ds_e]   (W and b grads)
+// Same fixed chunk / warp split as colsum2_kernel; split_reduce sums chunks in order.
+constexpr int kFoRows = 128;
+__global__ void __launch_bounds__(256) force_out_bwd_kernel(RowSet rows, const float* __restrict__ x,
+                                                            const float* __restrict__ xd, int act,
+                                                            const float* __restrict__ ds,
+                                                            const float* __restrict__ heads, size_t PH, size_t off_w,
+                                                            float* __restrict__ dzp, float* __restrict__ partial,
+                                                            int nchunk_cap, int W) {
+  __shared__ float red[8][257];
+  const int seg = blockIdx.y, chunk = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rb = rows.begin(seg), re = rows.end(seg);
+  const int r0 = rb + chunk * kFoRows;
+  if (r0 >= re) return;  // beyond this segment: not counted by the reduce
+  const int w0 = r0 + warp * (kFoRows / 8), w1 = min(w0 + kFoRows / 8, re);
+  const float* wv = heads + size_t(seg) * PH + off_w;
+  float4 wr[2], acc[2];
+  float accb = 0.f;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int c = lane * 4 + 128 * u;
+    wr[u] = c < W ? ldu4(wv + c) : f4z();
+    acc[u] = f4z();
+  }
+  for (int v = w0; v < w1; v += 2) {  // two rows per iteration, all loads issued before the math
+    int e[2];
+    float g[2];
+    float4 z[2][2], zd[2][2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      e[j] = v + j < w1 ? rows.row(v + j) : -1;
+      g[j] = e[j] >= 0 ? ds[e[j]] : 0.f;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int c = lane * 4 + 128 * u;
+        const bool ok = e[j] >= 0 && c < W;
+        z[j][u] = ok ? ld4(x + size_t(e[j]) * W + c) : f4z();
+        zd[j][u] = (ok && !act) ? ld4(xd + size_t(e[j]) * W + c) : f4z();
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int c = lane * 4 + 128 * u;
+        if (e[j] < 0 || c >= W) continue;
+        const float4 sg = act ? silu4(z[j][u]) : z[j][u];
+        const float4 sd = act ? sgrad4(z[j][u]) : zd[j][u];
+        const float4 gw = make_float4(g[j] * wr[u].x, g[j] * wr[u].y, g[j] * wr[u].z, g[j] * wr[u].w);
+        st4(dzp + size_t(e[j]) * W + c, mul4(gw, sd));
+        acc[u] = make_float4(acc[u].x + g[j] * sg.x, acc[u].y + g[j] * sg.y, acc[u].z + g[j] * sg.z,
+                             acc[u].w + g[j] * sg.w);
+      }
+      accb += g[j];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int c = lane * 4 + 128 * u;
+    if (c < W) {
+      red[warp][c] = acc[u].x;
+      red[warp][c + 1] = acc[u].y;
+      red[warp][c + 2] = acc[u].z;
+      red[warp][c + 3] = acc[u].w;
+    }
+  }
+  if (lane == 0) red[warp][W] = accb;
+  __syncthreads();
+  float* out = partial + (size_t(seg) * nchunk_cap + chunk) * (W + 1);
+  for (int t = threadIdx.x; t <= W; t += blockDim.x) {
+    float a = 0.f;
+    for (int w = 0; w < 8; ++w) a += red[w][t];
+    out[t] = a;
   }
 }
+
+// split_reduce functor: chunk partials of a head-segmented row set -> G + seg*seg_stride
+struct ChunkStore {
+  RowSet rows;
+  int rows_per_chunk;
+  float* G;
+  size_t seg_stride;
+  __device__ int count(int seg) const { return (rows.end(seg) - rows.begin(seg) + rows_per_chunk - 1) / rows_per_chunk; }
+  __device__ void store(int seg, int t, float v) const { G[seg * seg_stride + t] = v; }
+};
 
 // g_embed[s] = sum_{i: species_i = s} dh_i: CTA = 128-node chunk, thread = column,
 // smem accumulator [species][H] updated in ascending node order; chunks summed in order.
@@ -1375,13 +1496,12 @@ __global__ void embed_grad_part(const DevHdr* hdr, const uint8_t* __restrict__ s
   __syncthreads();
   for (int t = threadIdx.x; t < NS * H; t += blockDim.x) partial[size_t(chunk) * NS * H + t] = acc[t];
 }
-__global__ void embed_grad_reduce(const DevHdr* hdr, const float* __restrict__ partial, float* __restrict__ G, int H,
-                                  int NS) {
-  const int nchunks = (hdr->N + kEmbChunk - 1) / kEmbChunk;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < NS * H; t += gridDim.x * blockDim.x) {
-    G[t] = sum_strided(partial + t, nchunks, size_t(NS) * H);
-  }
-}
+struct EmbedStore {
+  const DevHdr* hdr;
+  float* G;
+  __device__ int count(int) const { return (hdr->N + kEmbChunk - 1) / kEmbChunk; }
+  __device__ void store(int, int t, float v) const { G[t] = v; }
+};
 
 // g_embed[s] = sum_{i: species_i = s} dh_i (ascending i; hmtl/model.hpp:619-622)
 __global__ void embed_grad_kernel(const DevHdr* hdr, const uint8_t* __restrict__ species, const float* __restrict__ dh,
@@ -1412,7 +1532,8 @@ void colsum2(Ctx& c, RowSet rows, const float* w, int wstride, const float* x, i
   const int chunk_cap = int((c.Ec + kCs2Rows - 1) / kCs2Rows);
   dim3 grid(chunk_cap, rows.nseg);
   colsum2_kernel<<<grid, 256, 0, st>>>(rows, w, wstride, x, C, c.partial, chunk_cap);
-  colsum2_reduce<<<dim3(1, rows.nseg), 256, 0, st>>>(rows, c.partial, chunk_cap, C, G, seg_stride);
+  split_reduce_kernel<<<dim3((2 * C + 31) / 32, rows.nseg), 256, 0, st>>>(
+      c.partial, size_t(chunk_cap) * 2 * C, size_t(2) * C, 2 * C, ChunkStore{rows, kCs2Rows, G, seg_stride});
 }
 }  // namespace
 
@@ -1460,11 +1581,25 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     float* bufs[2] = {c.dzA, c.dzB};
     for (int i = D - 1; i >= 1; --i) {
       const int out = i == D - 1 ? 1 : W;
+      float* nxt = bufs[i & 1];
+      if (i == D - 1 && force_out_fast(c, i)) {
+        Prof pr(c, "bwd.force_out", st);
+        const int cap = int((c.Ec + kFoRows - 1) / kFoRows);
+        const RowSet rows = edge_rows_by_head(c);
+        force_out_bwd_kernel<<<dim3(cap, rows.nseg), 256, 0, st>>>(
+            rows, i >= 2 ? c.zf + size_t(i - 2) * c.Ec * W : c.af0, c.sf0, i >= 2, c.ds, c.head_params(), c.PH,
+            c.head_off("force.W" + std::to_string(i)), nxt, c.partial, cap, W);
+        split_reduce_kernel<<<dim3((W + 1 + 31) / 32, rows.nseg), 256, 0, st>>>(
+            c.partial, size_t(cap) * (W + 1), size_t(W + 1), W + 1,
+            ChunkStore{rows, kFoRows, c.head_grads() + c.head_off("force.W" + std::to_string(i)), c.PH});
+        dz = nxt;
+        ldz = W;
+        continue;
+      }
       FGradProb gq{edge_rows_by_head(c), W + 1, out, H, W, i, c.Ec, c.Qf, c.zf, c.dist, dz, ldz, c.edge_dst,
                    c.edge_src, Wd, B0, HeadG{c.head_grads(), c.PH, c.head_off("force.W" + std::to_string(i))},
                    c.store_af0 ? c.af0 : nullptr};
       atb(gq, c, c.nsplit_edge, st, c.Ec);
-      float* nxt = bufs[i & 1];
       FDxProb dq{edge_rows_by_head(c), out, W, H, W, i, c.Ec, c.Qf, c.zf, c.dist, dz, ldz, c.edge_dst, c.edge_src,
                  Wd, B0, HeadW{c.head_params(), c.PH, c.head_off("force.W" + std::to_string(i))}, nxt,
                  c.store_af0 ? c.sf0 : nullptr};
@@ -1551,8 +1686,8 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     const size_t shm = size_t(c.NS) * H * 4;
     if (shm <= 48 * 1024 && size_t(c.Nc + kEmbChunk - 1) / kEmbChunk * c.NS * H <= c.partial_cap) {
       embed_grad_part<<<(c.Nc + kEmbChunk - 1) / kEmbChunk, 128, shm, st>>>(c.hdr, c.species, dh, c.partial, H, c.NS);
-      embed_grad_reduce<<<gridn((long long)c.NS * H, 256, sm), 256, 0, st>>>(c.hdr, c.partial,
-                                                                            c.grads + c.shared_off("embed"), H, c.NS);
+      split_reduce_kernel<<<dim3((c.NS * H + 31) / 32, 1), 256, 0, st>>>(
+          c.partial, 0, size_t(c.NS) * H, c.NS * H, EmbedStore{c.hdr, c.grads + c.shared_off("embed")});
     } else {
       embed_grad_kernel<<<gridn((long long)c.NS * H, 128, sm * 8), 128, 0, st>>>(
           c.hdr, c.species, dh, c.grads + c.shared_off("embed"), H, c.NS);

@@ -91,7 +91,7 @@ extern "C" int hmtl_selftest_gemm(int mode, int variant, int rows, int K, int N,
     cudaFuncSetAttribute(tc::tc_red_kernel<StRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     dim3 grid((K + 127) / 128, ns, 1);
     tc::tc_red_kernel<StRed><<<grid, tc::kRedThreads, smem>>>(p, part, ns, tc::red_stages(N));
-    tc::tc_red_reduce<StRed><<<64, 256>>>(p, part, ns);
+    tc::tc_red_reduce(p, part, ns, 0);
   }
   cudaError_t e = cudaDeviceSynchronize();
   if (e == cudaSuccess) cudaMemcpy(C, dC, (mode == 0 ? nc : size_t(K) * N) * 4, cudaMemcpyDeviceToHost);

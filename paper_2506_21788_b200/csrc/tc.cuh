@@ -460,14 +460,14 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
     int stage = 0;
     uint32_t phase = 0;
     const int f = lane * 4;
-    for (int c = split; c < nchunks; c += nsplit) {
-      // this warp's 4 rows (k-group `warp` of the chunk)
-      const int vj = rb + c * KC + warp * 4 + (lane & 3);
-      const int rj = vj < re ? p.rows.row(vj) : -1;
+    // register double buffer: chunk c+nsplit's loads are in flight while chunk c
+    // is transposed into shared memory
+    auto load = [&](int c, float4 (&xa)[4], float4 (&yb)[2][4]) {
+      const int vj = rb + c * KC + warp * 4 + (lane & 3);  // this warp's 4 rows (k-group `warp`)
+      const int rj = (c < nchunks && vj < re) ? p.rows.row(vj) : -1;
       int rows[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) rows[j] = __shfl_sync(0xffffffffu, rj, j);
-      float4 xa[4], yb[2][4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         xa[j] = (rows[j] >= 0 && f < Mt) ? p.x4(seg, rows[j], m0 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -477,6 +477,11 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
           yb[u][j] = (rows[j] >= 0 && n < N) ? p.y4(seg, rows[j], n) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
+    };
+    float4 xa[4], yb[2][4], xn[4], yn[2][4];
+    if (split < nchunks) load(split, xa, yb);
+    for (int c = split; c < nchunks; c += nsplit) {
+      if (c + nsplit < nchunks) load(c + nsplit, xn, yn);
       if (do_colsum)
 #pragma unroll
         for (int u = 0; u < 2; ++u)
@@ -500,6 +505,12 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
       fence_proxy_async();
       mbar_arrive(&full[stage]);
       if (++stage == kStages) stage = 0, phase ^= 1;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        xa[j] = xn[j];
+        yb[0][j] = yn[0][j];
+        yb[1][j] = yn[1][j];
+      }
     }
     if (do_colsum) {  // per-warp partial column sums -> fixed-order combine below
 #pragma unroll
@@ -562,16 +573,18 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
 
 // partial is [seg][split][n][Mo] (transposed); store C[m][n]
 template <class P>
-__global__ void tc_red_reduce(P p, const float* __restrict__ partial, int nsplit) {
+struct RedStore {
+  P p;
+  int nsplit, Mo;
+  __device__ int count(int) const { return nsplit; }
+  __device__ void store(int seg, int t, float v) const { p.store(seg, t % Mo, t / Mo, v); }
+};
+template <class P>
+inline void tc_red_reduce(const P& p, const float* partial, int nsplit, cudaStream_t st) {
   const int Mo = p.M + (p.colsum ? 1 : 0);
   const size_t KN = size_t(Mo) * p.Ncols;
-  const size_t total = KN * p.rows.nseg;
-  for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total;
-       idx += size_t(gridDim.x) * blockDim.x) {
-    const int seg = int(idx / KN);
-    const size_t nm = idx % KN;
-    p.store(seg, int(nm % Mo), int(nm / Mo), sum_strided(partial + size_t(seg) * nsplit * KN + nm, nsplit, KN));
-  }
+  dim3 grid(unsigned((KN + 31) / 32), p.rows.nseg);
+  split_reduce_kernel<<<grid, 256, 0, st>>>(partial, nsplit * KN, KN, int(KN), RedStore<P>{p, nsplit, Mo});
 }
 
 }  // namespace tc
