@@ -167,17 +167,20 @@ def load_peaks():
     return 6650.0, 1400.0, "fallback"
 
 
-def profile(model, cfg, slots, E, N, G, steps=3):
-    """Eager steps with per-kernel CUDA events (outside the timed region)."""
+def profile(model, cfg, slots, E, N, G, steps=3, flush=None):
+    """Per-scope device times from a profiled replay of the step's CUDA graph
+    (external event-record nodes around every kernel scope; outside the timed
+    region, L2 flushed between replays like the timed steps)."""
     import ctypes as C
 
     from paper_2506_21788_b200._lib import check, lib
 
     check(lib().hmtl_profile_enable(model.ctx, 1))
-    eager = type(cfg)(**{**cfg.__dict__, "use_graph": False})
     for i in range(steps):
+        if flush is not None:
+            flush()
         check(lib().hmtl_pool_bind(model.ctx, slots[i % len(slots)], None))
-        check(lib().hmtl_train_step(model.ctx, C.byref(eager.c()), None))
+        check(lib().hmtl_train_step(model.ctx, C.byref(cfg.c()), None))
     buf = C.create_string_buffer(1 << 16)
     check(lib().hmtl_profile_report(model.ctx, buf, len(buf)))
     check(lib().hmtl_profile_enable(model.ctx, 0))
@@ -399,8 +402,14 @@ def run_b200(args, rank, world, local_rank, dist):
     e2e = structs_per_step * args.steps / e2e_s
 
     # ---- per-kernel profile (eager, instrumented; outside the timed region)
-    rep = profile(model, cfg, slots, E.value, batches[0].N, batches[0].G)
-    launches_per_step = sum(r["calls"] * (2 if ("grad" in r["name"]) else 1) for r in rep) + 1  # + adam_tick
+    def do_flush():
+        with torch.cuda.stream(ext):
+            flush.zero_()
+
+    rep = profile(model, cfg, slots, E.value, batches[0].N, batches[0].G, flush=do_flush)
+    nk = C.c_int()
+    check(lib().hmtl_step_kernel_count(model.ctx, C.byref(nk)))
+    launches_per_step = nk.value  # kernel nodes of the step graph
     roof, roof_gs = roofline(rep, E.value, batches[0].N, batches[0].G, dev_ms / args.steps)
 
     cpu = None

@@ -173,11 +173,16 @@ int hmtl_train_step(hmtl_ctx* ctx, const hmtl_train_cfg* cfg, void* stream);
  * MLP layer >= 1), "s", "dE", "dF".  Returns #floats written in *n. */
 int hmtl_debug_fetch(hmtl_ctx* ctx, const char* name, int layer, float* host, size_t cap, size_t* n);
 
-/* Benchmark instrumentation: when enabled, every kernel launch site records
- * CUDA events on its stream (eager steps only; do not combine with graphs).
+/* Benchmark instrumentation: when enabled, every kernel scope records CUDA
+ * events on its stream.  Eager steps record plain events; graph steps
+ * (use_graph) replay a separately captured copy of the step graph whose
+ * scopes are external event-record nodes, synchronising after each replay.
  * report (syncs) writes a JSON array [{"name","calls","ms"}] and resets. */
 int hmtl_profile_enable(hmtl_ctx* ctx, int on);
 int hmtl_profile_report(hmtl_ctx* ctx, char* json, size_t cap);
+/* Kernel nodes in the captured step graph (= kernel launches per graph step),
+ * -1 before the first graph capture. */
+int hmtl_step_kernel_count(hmtl_ctx* ctx, int* n);
 
 /* Engine self-test (not on the training path): runs the tcgen05 engines on
  * plain row-major matrices on device 0.  mode 0: C[rows x N] = X[rows x K] B[K x N]

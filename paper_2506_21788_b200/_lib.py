@@ -105,6 +105,7 @@ SIGNATURES = {
     "hmtl_debug_fetch": (C.c_int, [_P, C.c_char_p, C.c_int, _FP, C.c_size_t, C.POINTER(C.c_size_t)]),
     "hmtl_profile_enable": (C.c_int, [_P, C.c_int]),
     "hmtl_profile_report": (C.c_int, [_P, C.c_char_p, C.c_size_t]),
+    "hmtl_step_kernel_count": (C.c_int, [_P, C.POINTER(C.c_int)]),
     "hmtl_selftest_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _FP, _FP, _FP]),
     "hmtl_selftest_time": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _FP]),
     "hmtl_comm_unique_id": (C.c_int, [_U8P]),

@@ -74,20 +74,48 @@ void free_ctx(Ctx& c) {
   void* ptrs[] = {c.params, c.grads, c.adam_m, c.adam_v, c.hdr, c.d_slot_of, c.arena, c.graph_offset, c.node_graph,
                   c.deg, c.row_ptr, c.edge_src, c.edge_dst, c.rev, c.edge_offset, c.pos32, c.geo, c.dist,
                   c.species, c.gslot, c.gperm, c.gnode_base, c.gedge_base, c.node_perm, c.edge_perm, c.hs, c.P,
-                  c.z2, c.agg, c.vz1, c.pooled, c.ez, c.energy, c.Qf, c.zf, c.s, c.forces, c.dE, c.dF, c.dh,
-                  c.dh2, c.dagg, c.dvz1, c.dzA, c.dzB, c.Sbuf, c.ds, c.dpooled, c.edA, c.edB, c.scratch,
-                  c.partial, c.bimg, c.a1, c.af0, c.sf0, c.bimg_all, c.d_bjobs};
+                  c.z2, c.agg, c.vz1, c.pooled, c.ez, c.energy, c.Qf, c.zf, c.s, c.forces, c.dE, c.dF,
+                  c.dagg, c.dhb, c.dvz1b, c.dzAb, c.dzBb, c.Sb, c.fzA, c.fzB, c.ds, c.dpooled, c.edA, c.edB,
+                  c.scratch, c.partial, c.partial_w, c.bimg, c.a1, c.af0, c.sf0, c.bimg_all, c.d_bjobs};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto* p : c.pool) cudaFree(p);
   if (c.h_arena) cudaFreeHost(c.h_arena);
   if (c.step_exec) cudaGraphExecDestroy(c.step_exec);
+  if (c.prof_exec) cudaGraphExecDestroy(c.prof_exec);
   comm_destroy(c.comm);
   c.comm = nullptr;
+  for (auto e : c.evs) cudaEventDestroy(e);
+  c.evs.clear();
+  if (c.s_e) cudaStreamDestroy(c.s_e);
+  if (c.s_w) cudaStreamDestroy(c.s_w);
   if (c.stream) cudaStreamDestroy(c.stream);
 }
 
+int count_kernel_nodes(cudaGraph_t g) {
+  size_t n = 0;
+  if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess) return -1;
+  std::vector<cudaGraphNode_t> nodes(n);
+  cudaGraphGetNodes(g, nodes.data(), &n);
+  int k = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+  }
+  return k;
+}
+
+// add the elapsed time of every recorded (start, end) pair to the scope totals
+void prof_harvest(Ctx& c) {
+  for (auto& r : c.prof)
+    for (size_t i = 0; i + 1 < r.used; i += 2) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, r.ev[i], r.ev[i + 1]) == cudaSuccess) r.acc_ms += t, r.calls += 1;
+    }
+}
+
 int enqueue_step(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st) {
+  c.ev_i = 0;
   if (!c.bimg_ready && c.use_tc) {  // record this step's B-image jobs (call order is fixed)
     c.bjobs.clear();
     c.bimg_recording = true;
@@ -170,7 +198,15 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   };
   const size_t H = c.H, W = c.W, L = c.L, D = c.D;
   const size_t N = c.Nc, E = c.Ec, G = c.Gc;
-  if (cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking) != cudaSuccess) rc = HMTL_ERR_INTERNAL;
+  {  // step stream at the highest priority: side-branch CTAs yield SMs to the critical path
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&c.stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c.s_e, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c.s_w, cudaStreamNonBlocking, lo) != cudaSuccess)
+      rc = HMTL_ERR_INTERNAL;
+  }
+  if (const char* e = std::getenv("HMTL_SINGLE_STREAM")) c.multi_stream = e[0] == '0';
   A(&c.params, c.PT);
   A(&c.grads, c.PT);
   A(&c.adam_m, c.PT);
@@ -211,13 +247,14 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   A(&c.forces, 3 * N);
   A(&c.dE, G);
   A(&c.dF, 3 * N);
-  A(&c.dh, N * H);
-  A(&c.dh2, N * H);
   A(&c.dagg, N * H);
-  A(&c.dvz1, N * H);
-  A(&c.dzA, E * std::max(H, W));
-  A(&c.dzB, E * std::max(H, W));
-  A(&c.Sbuf, N * 2 * std::max(H, W));
+  A(&c.dhb, (L + 1) * N * H);
+  A(&c.dvz1b, L * N * H);
+  A(&c.dzAb, L * E * H);
+  A(&c.dzBb, L * E * H);
+  A(&c.Sb, (L + 1) * N * 2 * std::max(H, W));
+  A(&c.fzA, E * W);
+  A(&c.fzB, E * W);
   A(&c.ds, E);
   A(&c.dpooled, G * H);
   A(&c.edA, G * W);
@@ -234,6 +271,7 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   // chunked column sums (colsum2, force output layer): [S][E/128 chunks][2*max(H,W)+1]
   c.partial_cap = std::max(c.partial_cap, size_t(std::max(c.S, 1)) * size_t((E + 127) / 128 + 1) * (2 * std::max(H, W) + 1));
   A(&c.partial, c.partial_cap);
+  A(&c.partial_w, c.partial_cap);
   c.bimg_cap = size_t(std::max(c.S, 2)) * 2 * (2 * std::max(H, W)) * (2 * std::max(H, W));
   A(&c.bimg, c.bimg_cap);
   if (const char* e = std::getenv("HMTL_NO_TC")) c.use_tc = e[0] == '0';
@@ -463,6 +501,23 @@ int hmtl_train_step(hmtl_ctx* h, const hmtl_train_cfg* cfg, void* stream) {
     HMTL_CUDA(cudaGetLastError());
     return 0;
   }
+  if (c.prof_on) {  // profiled replay (outside any timed region)
+    if (!c.prof_exec) {
+      for (auto& r : c.prof) r.used = 0;
+      cudaGraph_t g;
+      HMTL_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      int rc = enqueue_step(c, *cfg, st);
+      cudaError_t e = cudaStreamEndCapture(st, &g);
+      if (rc) return rc;
+      if (e != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("graph capture: ") + cudaGetErrorString(e));
+      HMTL_CUDA(cudaGraphInstantiate(&c.prof_exec, g, 0));
+      cudaGraphDestroy(g);
+    }
+    HMTL_CUDA(cudaGraphLaunch(c.prof_exec, st));
+    HMTL_CUDA(cudaStreamSynchronize(st));
+    prof_harvest(c);
+    return 0;
+  }
   if (!c.step_exec) {
     cudaGraph_t g;
     HMTL_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -470,6 +525,7 @@ int hmtl_train_step(hmtl_ctx* h, const hmtl_train_cfg* cfg, void* stream) {
     cudaError_t e = cudaStreamEndCapture(st, &g);
     if (rc) return rc;
     if (e != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("graph capture: ") + cudaGetErrorString(e));
+    c.step_kernels = count_kernel_nodes(g);
     HMTL_CUDA(cudaGraphInstantiate(&c.step_exec, g, 0));
     cudaGraphDestroy(g);
     c.graph_cfg = *cfg;
@@ -516,12 +572,22 @@ int hmtl_debug_fetch(hmtl_ctx* h, const char* name, int layer, float* host, size
   return 0;
 }
 
+int hmtl_step_kernel_count(hmtl_ctx* h, int* n) {
+  if (!n) return fail(HMTL_ERR_CONTRACT, "step_kernel_count: null argument");
+  *n = h->c.step_kernels;
+  return 0;
+}
+
 int hmtl_profile_enable(hmtl_ctx* h, int on) {
   Ctx& c = h->c;
   cudaSetDevice(c.device);
   HMTL_CUDA(cudaDeviceSynchronize());
   c.prof_on = on != 0;
-  for (auto& r : c.prof) r.used = 0;
+  if (c.prof_exec) {
+    cudaGraphExecDestroy(c.prof_exec);
+    c.prof_exec = nullptr;
+  }
+  for (auto& r : c.prof) r.used = 0, r.acc_ms = 0.0, r.calls = 0;
   return 0;
 }
 
@@ -529,18 +595,15 @@ int hmtl_profile_report(hmtl_ctx* h, char* json, size_t cap) {
   Ctx& c = h->c;
   cudaSetDevice(c.device);
   HMTL_CUDA(cudaDeviceSynchronize());
+  if (!c.prof_exec) prof_harvest(c);  // eager steps: events recorded once each
   std::string out = "[";
   for (auto& r : c.prof) {
-    double ms = 0.0;
-    for (size_t i = 0; i + 1 < r.used; i += 2) {
-      float t = 0.f;
-      cudaEventElapsedTime(&t, r.ev[i], r.ev[i + 1]);
-      ms += t;
-    }
     if (out.size() > 1) out += ",";
-    out += "{\"name\":\"" + r.name + "\",\"calls\":" + std::to_string(r.used / 2) + ",\"ms\":" +
-           std::to_string(ms) + "}";
-    r.used = 0;
+    out += "{\"name\":\"" + r.name + "\",\"calls\":" + std::to_string(r.calls) + ",\"ms\":" +
+           std::to_string(r.acc_ms) + "}";
+    if (!c.prof_exec) r.used = 0;
+    r.acc_ms = 0.0;
+    r.calls = 0;
   }
   out += "]";
   if (out.size() + 1 > cap) return fail(HMTL_ERR_CONTRACT, "profile_report: buffer too small");

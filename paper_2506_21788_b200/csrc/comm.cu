@@ -109,6 +109,10 @@ int hmtl_comm_init(hmtl_ctx* h, const uint8_t id_bytes[128], int world, int rank
     cudaGraphExecDestroy(c.step_exec);
     c.step_exec = nullptr;
   }
+  if (c.prof_exec) {
+    cudaGraphExecDestroy(c.prof_exec);
+    c.prof_exec = nullptr;
+  }
   c.comm = m;
   return 0;
 }

@@ -30,6 +30,8 @@ struct ProfRec {
   std::string name;
   std::vector<cudaEvent_t> ev;  // pairs (start, end)
   size_t used = 0;
+  double acc_ms = 0.0;  // harvested elapsed time
+  long calls = 0;
 };
 
 struct Ctx {
@@ -73,11 +75,25 @@ struct Ctx {
   float *pooled = nullptr, *ez = nullptr, *energy = nullptr, *Qf = nullptr, *zf = nullptr;
   float *s = nullptr, *forces = nullptr;
   // backward workspace
-  float *dE = nullptr, *dF = nullptr, *dh = nullptr, *dh2 = nullptr, *dagg = nullptr, *dvz1 = nullptr;
-  float *dzA = nullptr, *dzB = nullptr, *Sbuf = nullptr, *ds = nullptr, *dpooled = nullptr;
+  float *dE = nullptr, *dF = nullptr, *dagg = nullptr;
+  float *ds = nullptr, *dpooled = nullptr;
   float *edA = nullptr, *edB = nullptr, *scratch = nullptr;
-  float* partial = nullptr;
+  float* partial = nullptr;    // split-K partials of kernels on the main stream
+  float* partial_w = nullptr;  // ... and of the weight-gradient stream
   size_t partial_cap = 0;
+  // backward buffers that weight-gradient kernels read: one per layer, so the
+  // main stream never overwrites what the side stream has yet to read
+  float *dhb = nullptr;    // [L+1][N][H]: dL/dh_l
+  float *dvz1b = nullptr;  // [L][N][H]
+  float *dzAb = nullptr, *dzBb = nullptr;  // [L][E][H]
+  float *Sb = nullptr;     // [L+1][N][2max(H,W)] (slot L: force head)
+  float *fzA = nullptr, *fzB = nullptr;    // force head dz ping-pong [E][W]
+  // concurrency inside the step: s_e runs the energy head branch, s_w the
+  // weight gradients; both fork from / join into the step stream via events
+  cudaStream_t s_e = nullptr, s_w = nullptr;
+  std::vector<cudaEvent_t> evs;
+  size_t ev_i = 0;
+  bool multi_stream = true;
   float* bimg = nullptr;  // tcgen05 B-operand images (hi/lo, K-major)
   size_t bimg_cap = 0;
   bool use_tc = true;     // tcgen05 path for GEMMs whose shapes allow it
@@ -99,11 +115,15 @@ struct Ctx {
   // CUDA graph of a whole training step
   cudaGraphExec_t step_exec = nullptr;
   hmtl_train_cfg graph_cfg{};
+  int step_kernels = -1;  // kernel nodes in step_exec (launches per step)
 
   Comm* comm = nullptr;
   int sm_count = 148;
   bool prof_on = false;
   std::vector<ProfRec> prof;
+  // profiled copy of the step graph: every Prof scope is a pair of external
+  // event-record nodes, so per-scope times are taken inside a real graph replay
+  cudaGraphExec_t prof_exec = nullptr;
 
   // helpers
   float* shared_param(const char* name) const { return params + shared_lay.at(name).offset; }
@@ -112,6 +132,24 @@ struct Ctx {
   size_t head_off(const std::string& name) const { return head_lay.at(name).offset; }
   float* head_params() const { return params + PS; }
   float* head_grads() const { return grads + PS; }
+  float* part(cudaStream_t st) const { return st == s_w ? partial_w : partial; }
+  // stream for a side branch (the step stream itself while B images are being
+  // recorded: that eager step shares one image scratch buffer)
+  cudaStream_t side(cudaStream_t which, cudaStream_t st) const {
+    return (multi_stream && bimg_ready && which) ? which : st;
+  }
+  // make `to` wait for everything enqueued so far on `from`
+  void dep(cudaStream_t from, cudaStream_t to) {
+    if (from == to) return;
+    if (ev_i == evs.size()) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      evs.push_back(e);
+    }
+    cudaEvent_t e = evs[ev_i++];
+    cudaEventRecord(e, from);
+    cudaStreamWaitEvent(to, e, 0);
+  }
 };
 
 // launchers (stream-ordered; sizes come from the device header)
@@ -147,12 +185,18 @@ struct Prof {
       r->ev.push_back(a);
       r->ev.push_back(b);
     }
-    cudaEventRecord(r->ev[r->used], st);
+    rec(r->ev[r->used]);
     end = r->ev[r->used + 1];
     r->used += 2;
   }
+  void rec(cudaEvent_t e) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    else cudaEventRecord(e, st);
+  }
   ~Prof() {
-    if (end) cudaEventRecord(end, st);
+    if (end) rec(end);
   }
 };
 void comm_destroy(Comm* m);

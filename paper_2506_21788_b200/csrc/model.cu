@@ -512,23 +512,24 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
     // enough CTAs to fill the GPU, >= 4 chunks each (bounded partial traffic)
     long long want = std::max<long long>(1, (long long)c.sm_count / (mtiles * p.rows.nseg));  // one wave
     int ns = int(std::max<long long>(1, std::min<long long>(want, chunks / 4)));
+    float* partial = c.part(st);
     while (ns > 1 && size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * p.Ncols > c.partial_cap) ns /= 2;
     if (size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * p.Ncols <= c.partial_cap) {
       TcRed<P> q{p.rows, M, p.Ncols, P::kBias, p};
       const size_t smem = tc::tc_red_smem(p.Ncols);
       set_smem(tc::tc_red_kernel<TcRed<P>>, smem);
       dim3 grid(mtiles, ns, p.rows.nseg);
-      tc::tc_red_kernel<TcRed<P>><<<grid, tc::kRedThreads, smem, st>>>(q, c.partial, ns,
+      tc::tc_red_kernel<TcRed<P>><<<grid, tc::kRedThreads, smem, st>>>(q, partial, ns,
                                                                         tc::red_stages(p.Ncols));
-      tc::tc_red_reduce(q, c.partial, ns, st);
+      tc::tc_red_reduce(q, partial, ns, st);
       return;
     }
   }
   const int tiles = ((p.K + 63) / 64) * ((p.Ncols + 63) / 64);
   dim3 grid(tiles, nsplit, p.rows.nseg);
-  gemm_atb_kernel<P><<<grid, 256, 0, st>>>(p, c.partial, nsplit);
+  gemm_atb_kernel<P><<<grid, 256, 0, st>>>(p, c.part(st), nsplit);
   const long long total = (long long)p.K * p.Ncols * p.rows.nseg;
-  gemm_atb_reduce<P><<<gridn(total, 256, c.sm_count * 8), 256, 0, st>>>(p, c.partial, nsplit);
+  gemm_atb_reduce<P><<<gridn(total, 256, c.sm_count * 8), 256, 0, st>>>(p, c.part(st), nsplit);
 }
 
 RowSet node_rows(Ctx& c) {
@@ -731,10 +732,12 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     }
   }
   const float* hL = c.hs + size_t(L) * NH;
-  // energy branch
+  // energy branch (side stream; independent of the force branch until the loss)
+  cudaStream_t se = c.side(c.s_e, st);
+  c.dep(st, se);
   {
-    Prof pr(c, "fwd.pool", st);
-    pool_kernel<<<gridn((long long)c.Gc * 32, 256, sm * 8), 256, 0, st>>>(c.hdr, c.graph_offset, hL, c.pooled, H);
+    Prof pr(c, "fwd.pool", se);
+    pool_kernel<<<gridn((long long)c.Gc * 32, 256, sm * 8), 256, 0, se>>>(c.hdr, c.graph_offset, hL, c.pooled, H);
   }
   for (int i = 0; i < D; ++i) {
     const int last = i == D - 1;
@@ -743,7 +746,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
                  HeadW{c.head_params(), c.PH, c.head_off("energy.W" + std::to_string(i))},
                  HeadW{c.head_params(), c.PH, c.head_off("energy.b" + std::to_string(i))},
                  c.ez + size_t(i) * c.Gc * W, c.energy};
-    ab(q, c.Gc, c.S, st, sm, c);
+    ab(q, c.Gc, c.S, se, sm, c);
   }
   // force branch
   {
@@ -779,6 +782,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     Prof pr(c, "fwd.forces_segsum", st);
     forces_kernel<<<gridn(c.Nc, 256, sm * 8), 256, 0, st>>>(c.hdr, c.row_ptr, c.geo, c.s, c.forces);
   }
+  c.dep(se, st);
   {
     Prof pr(c, "fwd.finite", st);
     finite_kernel<<<gridn(c.Gc + 3LL * c.Nc, 256, sm * 4), 256, 0, st>>>(c.hdr, c.energy, c.forces);
@@ -1519,11 +1523,11 @@ __global__ void embed_grad_kernel(const DevHdr* hdr, const uint8_t* __restrict__
 }  // namespace
 
 namespace {
-void segsum2(Ctx& c, const float* x, int C, int fold, cudaStream_t st) {
+void segsum2(Ctx& c, const float* x, int C, int fold, float* out, cudaStream_t st) {
   Prof pr(c, "bwd.segsum_dst_src", st);
   const int blocks = gridn((long long)c.Nc * 32, 256, c.sm_count * 16);
-  if (C % 4 == 0) seg2v_kernel<<<blocks, 256, 0, st>>>(c.hdr, c.row_ptr, c.rev, x, c.Sbuf, C, fold);
-  else seg2_kernel<<<blocks, 256, 0, st>>>(c.hdr, c.row_ptr, c.rev, x, c.Sbuf, C, fold);
+  if (C % 4 == 0) seg2v_kernel<<<blocks, 256, 0, st>>>(c.hdr, c.row_ptr, c.rev, x, out, C, fold);
+  else seg2_kernel<<<blocks, 256, 0, st>>>(c.hdr, c.row_ptr, c.rev, x, out, C, fold);
 }
 // [sum w*x ; sum x] per head segment into G + seg*seg_stride (rows are contiguous)
 void colsum2(Ctx& c, RowSet rows, const float* w, int wstride, const float* x, int C, float* G, size_t seg_stride,
@@ -1531,40 +1535,47 @@ void colsum2(Ctx& c, RowSet rows, const float* w, int wstride, const float* x, i
   Prof pr(c, "bwd.colsum_tail", st);
   const int chunk_cap = int((c.Ec + kCs2Rows - 1) / kCs2Rows);
   dim3 grid(chunk_cap, rows.nseg);
-  colsum2_kernel<<<grid, 256, 0, st>>>(rows, w, wstride, x, C, c.partial, chunk_cap);
+  colsum2_kernel<<<grid, 256, 0, st>>>(rows, w, wstride, x, C, c.part(st), chunk_cap);
   split_reduce_kernel<<<dim3((2 * C + 31) / 32, rows.nseg), 256, 0, st>>>(
-      c.partial, size_t(chunk_cap) * 2 * C, size_t(2) * C, 2 * C, ChunkStore{rows, kCs2Rows, G, seg_stride});
+      c.part(st), size_t(chunk_cap) * 2 * C, size_t(2) * C, 2 * C, ChunkStore{rows, kCs2Rows, G, seg_stride});
 }
 }  // namespace
 
 void launch_backward(Ctx& c, cudaStream_t st) {
   const int H = c.H, W = c.W, L = c.L, D = c.D, sm = c.sm_count;
   const size_t NH = size_t(c.Nc) * H, EH = size_t(c.Ec) * H;
+  const size_t SBS = size_t(c.Nc) * 2 * std::max(H, W);  // one Sb slot
   const float* hL = c.hs + size_t(L) * NH;
   const size_t GW = size_t(c.Gc) * W;
+  // streams: st = critical path (dx chain), se = energy head branch, sw = weight
+  // gradients (consumed only by the gradient sync / AdamW after the final join)
+  cudaStream_t se = c.side(c.s_e, st), sw = c.side(c.s_w, st);
+  float* dhL = c.dhb + size_t(L) * NH;  // dL/dh_L, written by the heads
 
   // ---------------- energy heads (hmtl/model.hpp:512-524)
+  c.dep(st, se);
   {
     const float* dz = c.dE;
     int ldz = 1;
     float* bufs[2] = {c.edA, c.edB};
     for (int i = D - 1; i >= 0; --i) {
       const int in = i == 0 ? H : W, out = i == D - 1 ? 1 : W;
+      c.dep(se, sw);
       EGradProb gq{graph_rows_by_head(c), in + 1, out, H, W, i, c.pooled,
                    i ? c.ez + size_t(i - 1) * GW : nullptr, dz, ldz,
                    HeadG{c.head_grads(), c.PH, c.head_off("energy.W" + std::to_string(i))}};
-      atb(gq, c, c.nsplit_graph, st, c.Gc);
+      atb(gq, c, c.nsplit_graph, sw, c.Gc);
       float* nxt = i ? bufs[i & 1] : c.dpooled;
       EDxProb dq{graph_rows_by_head(c), out, in, W, H, dz, i ? c.ez + size_t(i - 1) * GW : nullptr, ldz,
                  HeadW{c.head_params(), c.PH, c.head_off("energy.W" + std::to_string(i))}, nxt, i ? W : H,
                  i ? 1 : 0};
-      ab(dq, c.Gc, c.S, st, sm, c);
+      ab(dq, c.Gc, c.S, se, sm, c);
       dz = nxt;
       ldz = W;
     }
     {
-      Prof pr(c, "bwd.pool", st);
-      dh_pool_kernel<<<gridn(NH, 256, sm * 16), 256, 0, st>>>(c.hdr, c.node_graph, c.graph_offset, c.dpooled, c.dh, H);
+      Prof pr(c, "bwd.pool", se);
+      dh_pool_kernel<<<gridn(NH, 256, sm * 16), 256, 0, se>>>(c.hdr, c.node_graph, c.graph_offset, c.dpooled, dhL, H);
     }
   }
   // ---------------- force heads (hmtl/model.hpp:526-549)
@@ -1578,7 +1589,7 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     const HeadW B0{c.head_params(), c.PH, c.head_off("force.b0")};
     const float* dz = c.ds;
     int ldz = 1;
-    float* bufs[2] = {c.dzA, c.dzB};
+    float* bufs[2] = {c.fzA, c.fzB};
     for (int i = D - 1; i >= 1; --i) {
       const int out = i == D - 1 ? 1 : W;
       float* nxt = bufs[i & 1];
@@ -1596,10 +1607,11 @@ void launch_backward(Ctx& c, cudaStream_t st) {
         ldz = W;
         continue;
       }
+      c.dep(st, sw);
       FGradProb gq{edge_rows_by_head(c), W + 1, out, H, W, i, c.Ec, c.Qf, c.zf, c.dist, dz, ldz, c.edge_dst,
                    c.edge_src, Wd, B0, HeadG{c.head_grads(), c.PH, c.head_off("force.W" + std::to_string(i))},
                    c.store_af0 ? c.af0 : nullptr};
-      atb(gq, c, c.nsplit_edge, st, c.Ec);
+      atb(gq, c, c.nsplit_edge, sw, c.Ec);
       FDxProb dq{edge_rows_by_head(c), out, W, H, W, i, c.Ec, c.Qf, c.zf, c.dist, dz, ldz, c.edge_dst, c.edge_src,
                  Wd, B0, HeadW{c.head_params(), c.PH, c.head_off("force.W" + std::to_string(i))}, nxt,
                  c.store_af0 ? c.sf0 : nullptr};
@@ -1608,21 +1620,22 @@ void launch_backward(Ctx& c, cudaStream_t st) {
       ldz = W;
     }
     // layer 0 (factorised): T = S_dst(dz0) + S_src(dz0)
-    segsum2(c, dz, W, 1, st);
-    F0NodeGrad ng{node_rows_by_head(c), H, W, H, W, hL, c.Sbuf, HeadG{c.head_grads(), c.PH, wf0}};
-    atb(ng, c, c.nsplit_node, st, c.Nc);
+    float* Sf = c.Sb + size_t(L) * SBS;
+    segsum2(c, dz, W, 1, Sf, st);
+    c.dep(st, sw);
+    F0NodeGrad ng{node_rows_by_head(c), H, W, H, W, hL, Sf, HeadG{c.head_grads(), c.PH, wf0}};
+    atb(ng, c, c.nsplit_node, sw, c.Nc);
     if (W % 4 == 0) {
-      colsum2(c, edge_rows_by_head(c), c.dist, 1, dz, W, c.head_grads() + wf0 + size_t(H) * W, c.PH, st);
+      colsum2(c, edge_rows_by_head(c), c.dist, 1, dz, W, c.head_grads() + wf0 + size_t(H) * W, c.PH, sw);
     } else {
       F0EdgeGrad eg{edge_rows_by_head(c), 2, W, H, W, c.dist, dz, HeadG{c.head_grads(), c.PH, wf0 + size_t(H) * W}};
-      atb(eg, c, c.nsplit_edge, st, c.Ec);
+      atb(eg, c, c.nsplit_edge, sw, c.Ec);
     }
-    F0Dh dhq{node_rows_by_head(c), W, H, H, W, c.Sbuf, HeadW{c.head_params(), c.PH, wf0}, c.dh};
+    c.dep(se, st);  // dL/dh_L = energy part (written) + force part (accumulated next)
+    F0Dh dhq{node_rows_by_head(c), W, H, H, W, Sf, HeadW{c.head_params(), c.PH, wf0}, dhL};
     ab(dhq, c.Nc, c.S, st, sm, c);
   }
   // ---------------- encoder layers in reverse (hmtl/model.hpp:552-617)
-  float* dh = c.dh;
-  float* dh2 = c.dh2;
   for (int l = L - 1; l >= 0; --l) {
     const std::string p = "layer" + std::to_string(l) + ".";
     const float* h = c.hs + size_t(l) * NH;
@@ -1634,65 +1647,76 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     const float* wd = eW1 + size_t(2) * H * H;
     const float* b1 = c.params + c.shared_off(p + "edge.b1");
     float* geW1 = c.grads + c.shared_off(p + "edge.W1");
-    {
-      L1Prob q{node_rows(c), H, H, H, dh, c.params + c.shared_off(p + "node.W2"), vz1, c.dvz1};
-      ab(q, c.Nc, 1, st, sm, c);
-    }
+    const float* dh = c.dhb + size_t(l + 1) * NH;  // dL/dh_{l+1}
+    float* dh2 = c.dhb + size_t(l) * NH;           // dL/dh_l
+    float* dvz1 = c.dvz1b + size_t(l) * NH;
+    float* dzA = c.dzAb + size_t(l) * EH;
+    float* dzB = c.dzBb + size_t(l) * EH;
+    float* Sl = c.Sb + size_t(l) * SBS;
+    c.dep(st, sw);  // dh ready
     {
       L2Prob q{node_rows(c), H + 1, H, H, vz1, dh, c.grads + c.shared_off(p + "node.W2")};
-      atb(q, c, c.nsplit_node, st, c.Nc);
+      atb(q, c, c.nsplit_node, sw, c.Nc);
     }
     {
-      L3Prob q{node_rows(c), 2 * H + 1, H, H, h, agg, c.dvz1, c.grads + c.shared_off(p + "node.W1")};
-      atb(q, c, c.nsplit_node, st, c.Nc);
+      L1Prob q{node_rows(c), H, H, H, dh, c.params + c.shared_off(p + "node.W2"), vz1, dvz1};
+      ab(q, c.Nc, 1, st, sm, c);
+    }
+    c.dep(st, sw);  // dvz1 ready
+    {
+      L3Prob q{node_rows(c), 2 * H + 1, H, H, h, agg, dvz1, c.grads + c.shared_off(p + "node.W1")};
+      atb(q, c, c.nsplit_node, sw, c.Nc);
     }
     {
-      L4Prob q{node_rows(c), H, 2 * H, H, c.dvz1, c.params + c.shared_off(p + "node.W1"), dh, dh2, c.dagg};
+      L4Prob q{node_rows(c), H, 2 * H, H, dvz1, c.params + c.shared_off(p + "node.W1"), dh, dh2, c.dagg};
       ab(q, c.Nc, 1, st, sm, c);
     }
     const bool mat = c.store_a1;  // tensor-core shapes: gathered operands materialised elementwise
     if (mat) {
       Prof pr(c, "bwd.edge_act", st);
       edge_bwd_prep_kernel<<<gridn((long long)c.Ec * H / 4, 256, sm * 16), 256, 0, st>>>(
-          c.hdr, P, c.edge_dst, c.edge_src, c.geo, wd, b1, c.dagg, z2, c.dzA, c.scratch, H);
+          c.hdr, P, c.edge_dst, c.edge_src, c.geo, wd, b1, c.dagg, z2, dzA, c.scratch, H);
     } else {
       Prof pr(c, "bwd.edge_dz2_gather", st);
-      dz2_kernel<<<gridn(EH, 256, sm * 16), 256, 0, st>>>(c.hdr, c.edge_dst, c.dagg, z2, c.dzA, H);
+      dz2_kernel<<<gridn(EH, 256, sm * 16), 256, 0, st>>>(c.hdr, c.edge_dst, c.dagg, z2, dzA, H);
     }
+    c.dep(st, sw);  // dz2 ready
     {
-      L6Prob q{edge_rows(c), H + 1, H, H, P, wd, b1, c.dzA, c.edge_dst, c.edge_src, c.geo,
+      L6Prob q{edge_rows(c), H + 1, H, H, P, wd, b1, dzA, c.edge_dst, c.edge_src, c.geo,
                c.grads + c.shared_off(p + "edge.W2"), mat ? c.a1 + size_t(l) * EH : nullptr, nullptr, z2};
-      atb(q, c, c.nsplit_edge, st, c.Ec);
+      atb(q, c, c.nsplit_edge, sw, c.Ec);
     }
     {
-      L7Prob q{edge_rows(c), H, H, H, c.dzA, c.params + c.shared_off(p + "edge.W2"), P, wd, b1, c.edge_dst,
-               c.edge_src, c.geo, c.dzB, nullptr, z2, mat ? c.scratch : nullptr};
+      L7Prob q{edge_rows(c), H, H, H, dzA, c.params + c.shared_off(p + "edge.W2"), P, wd, b1, c.edge_dst,
+               c.edge_src, c.geo, dzB, nullptr, z2, mat ? c.scratch : nullptr};
       ab(q, c.Ec, 1, st, sm, c);
     }
-    segsum2(c, c.dzB, H, 0, st);
-    colsum2(c, edge_rows(c), &c.geo[0].w, 4, c.dzB, H, geW1 + size_t(2) * H * H, 0, st);
+    segsum2(c, dzB, H, 0, Sl, st);
+    c.dep(st, sw);  // dz1 and its segment sums ready
+    colsum2(c, edge_rows(c), &c.geo[0].w, 4, dzB, H, geW1 + size_t(2) * H * H, 0, sw);
     {
-      L10Prob q{node_rows(c), H, 2 * H, H, h, c.Sbuf, geW1};
-      atb(q, c, c.nsplit_node, st, c.Nc);
+      L10Prob q{node_rows(c), H, 2 * H, H, h, Sl, geW1};
+      atb(q, c, c.nsplit_node, sw, c.Nc);
     }
     {
-      L11Prob q{node_rows(c), 2 * H, H, H, c.Sbuf, eW1, dh2};
+      L11Prob q{node_rows(c), 2 * H, H, H, Sl, eW1, dh2};
       ab(q, c.Nc, 1, st, sm, c);
     }
-    std::swap(dh, dh2);
   }
   {
+    const float* dh0 = c.dhb;
     Prof pr(c, "bwd.embed_grad", st);
     const size_t shm = size_t(c.NS) * H * 4;
     if (shm <= 48 * 1024 && size_t(c.Nc + kEmbChunk - 1) / kEmbChunk * c.NS * H <= c.partial_cap) {
-      embed_grad_part<<<(c.Nc + kEmbChunk - 1) / kEmbChunk, 128, shm, st>>>(c.hdr, c.species, dh, c.partial, H, c.NS);
+      embed_grad_part<<<(c.Nc + kEmbChunk - 1) / kEmbChunk, 128, shm, st>>>(c.hdr, c.species, dh0, c.partial, H, c.NS);
       split_reduce_kernel<<<dim3((c.NS * H + 31) / 32, 1), 256, 0, st>>>(
           c.partial, 0, size_t(c.NS) * H, c.NS * H, EmbedStore{c.hdr, c.grads + c.shared_off("embed")});
     } else {
       embed_grad_kernel<<<gridn((long long)c.NS * H, 128, sm * 8), 128, 0, st>>>(
-          c.hdr, c.species, dh, c.grads + c.shared_off("embed"), H, c.NS);
+          c.hdr, c.species, dh0, c.grads + c.shared_off("embed"), H, c.NS);
     }
   }
+  c.dep(sw, st);  // every weight gradient is final
 }
 
 // debug probe: z1 of layer l (the factorised pre-activation), [E x H]
