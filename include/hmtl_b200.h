@@ -188,6 +188,10 @@ int hmtl_step_kernel_count(hmtl_ctx* ctx, int* n);
  * plain row-major matrices on device 0.  mode 0: C[rows x N] = X[rows x K] B[K x N]
  * (Y = B); mode 1: C[K x N] = X[rows x K]^T Y[rows x N].  variant: debug bits. */
 int hmtl_selftest_gemm(int mode, int variant, int rows, int K, int N, const float* X, const float* Y, float* C);
+/* Tensor-pipe issue-rate probe (engine design; device 0): SM clocks per MMA of
+ * n back-to-back M=128 x N MMAs.  variant: 0 tf32 SS, 1 tf32 A-in-TMEM,
+ * 2 bf16 SS, 3 bf16 A-in-TMEM. */
+int hmtl_selftest_mma_rate(int variant, int N, int n, float* clk_per_mma);
 int hmtl_selftest_time(int mode, int rows, int K, int N, int iters, float* ms);
 
 /* ------------------------------------------------------------ comm (NCCL) */

@@ -146,11 +146,11 @@ struct Node1Prob {
 // h' = h + (silu(vz1) nW2 + nb2)   (hmtl/model.hpp:421-426, residual)
 struct Node2Prob {
   struct Aux {
-    float4 h, b;
+    float4 h;
   };
-  __device__ Aux epi_aux(int, int r, int n) const { return Aux{ld4(h + size_t(r) * H + n), ld4(bias + n)}; }
+  __device__ Aux epi_aux(int, int r, int n) const { return Aux{ld4(h + size_t(r) * H + n)}; }
   __device__ void epi4a(int, int r, int n, float4 acc, const Aux& a) const {
-    st4(hn + size_t(r) * H + n, add4(a.h, add4(acc, a.b)));  // h + (acc + b), as the SIMT path
+    st4(hn + size_t(r) * H + n, add4(a.h, add4(acc, ld4(bias + n))));  // h + (acc + b), as the SIMT path
   }
   BDesc bd() const { return BDesc{W, nullptr, 0, 0, H, 1, K, Ncols, 1, 0, nullptr}; }
   static constexpr const char* kName = "fwd.node_mlp2";
@@ -570,36 +570,67 @@ namespace {
 __global__ void agg4_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const float* __restrict__ z2,
                             float* __restrict__ agg, int H);
 
-// ---- full-occupancy elementwise producers of the tensor-core A operands
-// a1 = silu(z1), z1 = (P_a[dst] + P_b[src]) + d2 w + b1   (one thread per 4 columns)
-__global__ void edge_a1_kernel(const DevHdr* hdr, const float* __restrict__ P, const int* __restrict__ dst,
-                               const int* __restrict__ src, const float4* __restrict__ geo,
-                               const float* __restrict__ wd, const float* __restrict__ b1, float* __restrict__ a1,
-                               int H) {
-  const int q = H / 4;
-  const long long total = (long long)hdr->E * q;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int e = int(t / q), c = int(t % q) * 4;
-    const int d = dst[e], s = src[e];
-    st4(a1 + size_t(e) * H + c, silu4(pre4(ld4(P + size_t(d) * 2 * H + c), ld4(P + size_t(s) * 2 * H + H + c),
-                                             geo[e].w, ld4(wd + c), ld4(b1 + c))));
+// ---- elementwise producers of the tensor-core A operands.  Warp per group of
+// kEwU edges, lane = float4 column group: the per-edge indices are warp-uniform
+// loads and every row load of the group is issued before the math.
+constexpr int kEwU = 4;
+// a1 = silu(z1), z1 = (P_a[dst] + P_b[src]) + d2 w + b1
+__global__ void __launch_bounds__(256) edge_a1_kernel(const DevHdr* hdr, const float* __restrict__ P,
+                                                      const int* __restrict__ dst, const int* __restrict__ src,
+                                                      const float4* __restrict__ geo, const float* __restrict__ wd,
+                                                      const float* __restrict__ b1, float* __restrict__ a1, int H) {
+  const int E = hdr->E, lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int eb = gw * kEwU; eb < E; eb += nw * kEwU) {
+    for (int c = lane * 4; c < H; c += 128) {
+      const float4 w = ld4(wd + c), bb = ld4(b1 + c);
+      float4 pa[kEwU], pb[kEwU];
+      float d2[kEwU];
+#pragma unroll
+      for (int u = 0; u < kEwU; ++u) {
+        const int e = min(eb + u, E - 1);
+        pa[u] = ld4(P + size_t(dst[e]) * 2 * H + c);
+        pb[u] = ld4(P + size_t(src[e]) * 2 * H + H + c);
+        d2[u] = geo[e].w;
+      }
+#pragma unroll
+      for (int u = 0; u < kEwU; ++u)
+        if (eb + u < E) st4(a1 + size_t(eb + u) * H + c, silu4(pre4(pa[u], pb[u], d2[u], w, bb)));
+    }
   }
 }
 // backward: dz2 = dagg[dst] * silu'(z2) and s1p = silu'(z1)
-__global__ void edge_bwd_prep_kernel(const DevHdr* hdr, const float* __restrict__ P, const int* __restrict__ dst,
-                                     const int* __restrict__ src, const float4* __restrict__ geo,
-                                     const float* __restrict__ wd, const float* __restrict__ b1,
-                                     const float* __restrict__ dagg, const float* __restrict__ z2,
-                                     float* __restrict__ dz2, float* __restrict__ s1p, int H) {
-  const int q = H / 4;
-  const long long total = (long long)hdr->E * q;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int e = int(t / q), c = int(t % q) * 4;
-    const int d = dst[e], s = src[e];
-    const size_t o = size_t(e) * H + c;
-    st4(dz2 + o, mul4(ld4(dagg + size_t(d) * H + c), sgrad4(ld4(z2 + o))));
-    st4(s1p + o, sgrad4(pre4(ld4(P + size_t(d) * 2 * H + c), ld4(P + size_t(s) * 2 * H + H + c), geo[e].w,
-                             ld4(wd + c), ld4(b1 + c))));
+__global__ void __launch_bounds__(256) edge_bwd_prep_kernel(const DevHdr* hdr, const float* __restrict__ P,
+                                                            const int* __restrict__ dst, const int* __restrict__ src,
+                                                            const float4* __restrict__ geo,
+                                                            const float* __restrict__ wd, const float* __restrict__ b1,
+                                                            const float* __restrict__ dagg,
+                                                            const float* __restrict__ z2, float* __restrict__ dz2,
+                                                            float* __restrict__ s1p, int H) {
+  const int E = hdr->E, lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int eb = gw * kEwU; eb < E; eb += nw * kEwU) {
+    for (int c = lane * 4; c < H; c += 128) {
+      const float4 w = ld4(wd + c), bb = ld4(b1 + c);
+      float4 pa[kEwU], pb[kEwU], ga[kEwU], zz[kEwU];
+      float d2[kEwU];
+#pragma unroll
+      for (int u = 0; u < kEwU; ++u) {
+        const int e = min(eb + u, E - 1), d = dst[e];
+        pa[u] = ld4(P + size_t(d) * 2 * H + c);
+        pb[u] = ld4(P + size_t(src[e]) * 2 * H + H + c);
+        ga[u] = ld4(dagg + size_t(d) * H + c);
+        zz[u] = ld4(z2 + size_t(e) * H + c);
+        d2[u] = geo[e].w;
+      }
+#pragma unroll
+      for (int u = 0; u < kEwU; ++u)
+        if (eb + u < E) {
+          const size_t o = size_t(eb + u) * H + c;
+          st4(dz2 + o, mul4(ga[u], sgrad4(zz[u])));
+          st4(s1p + o, sgrad4(pre4(pa[u], pb[u], d2[u], w, bb)));
+        }
+    }
   }
 }
 // force head layer 0: af0 = silu(zf0), sf0 = silu'(zf0) with the edge's head weights
@@ -705,7 +736,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     }
     if (c.store_a1) {
       Prof pr(c, "fwd.edge_act", st);
-      edge_a1_kernel<<<gridn((long long)c.Ec * H / 4, 256, sm * 16), 256, 0, st>>>(
+      edge_a1_kernel<<<gridn((c.Ec + kEwU - 1) / kEwU * 32, 256, sm * 16), 256, 0, st>>>(
           c.hdr, P, c.edge_dst, c.edge_src, c.geo, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
           c.a1 + size_t(l) * EH, H);
     }
@@ -1281,49 +1312,62 @@ __global__ void seg2_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, 
 // 4 independent edge loads in flight; ascending-edge accumulation per column.
 __device__ __forceinline__ float4 f4z() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
-// agg_i = sum_{e in row i} silu(z2_e)
-__global__ void agg4_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const float* __restrict__ z2,
-                            float* __restrict__ agg, int H) {
+// agg_i = sum_{e in row i} silu(z2_e).  Warp per node, lane = float4 column
+// group; edges in batches of 8 with all 8 row loads issued before the
+// ascending-edge accumulation (high-degree inorganic nodes set the kernel time).
+constexpr int kAggU = 8;
+__global__ void __launch_bounds__(256) agg4_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr,
+                                                   const float* __restrict__ z2, float* __restrict__ agg, int H) {
   const int N = hdr->N, lane = threadIdx.x & 31;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += (gridDim.x * blockDim.x) >> 5) {
     const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
     for (int c = lane * 4; c < H; c += 128) {
       float4 acc = f4z();
-      int e = e0;
-      for (; e + 4 <= e1; e += 4) {
-        const float4 v0 = ld4(z2 + size_t(e) * H + c), v1 = ld4(z2 + size_t(e + 1) * H + c);
-        const float4 v2 = ld4(z2 + size_t(e + 2) * H + c), v3 = ld4(z2 + size_t(e + 3) * H + c);
-        acc = add4(acc, silu4(v0));
-        acc = add4(acc, silu4(v1));
-        acc = add4(acc, silu4(v2));
-        acc = add4(acc, silu4(v3));
+      for (int e = e0; e < e1; e += kAggU) {
+        float4 v[kAggU];
+#pragma unroll
+        for (int u = 0; u < kAggU; ++u) v[u] = e + u < e1 ? ld4(z2 + size_t(e + u) * H + c) : f4z();
+#pragma unroll
+        for (int u = 0; u < kAggU; ++u)
+          if (e + u < e1) acc = add4(acc, silu4(v[u]));
       }
-      for (; e < e1; ++e) acc = add4(acc, silu4(ld4(z2 + size_t(e) * H + c)));
       st4(agg + size_t(i) * H + c, acc);
     }
   }
 }
 
-// S[i] = [sum_{e in row i} x_e | sum_{e in row i} x_{rev(e)}] (or folded a + b)
-__global__ void seg2v_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const int* __restrict__ rev,
-                             const float* __restrict__ x, float* __restrict__ S, int C, int fold) {
+// S[i] = [sum_{e in row i} x_e | sum_{e in row i} x_{rev(e)}] (or folded a + b).
+// The row's rev indices are read once per 32-edge window (one per lane) and
+// broadcast by shuffle; 4 edges per batch -> 8 row loads in flight per lane.
+constexpr int kSegU = 4;
+__global__ void __launch_bounds__(256) seg2v_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr,
+                                                    const int* __restrict__ rev, const float* __restrict__ x,
+                                                    float* __restrict__ S, int C, int fold) {
   const int N = hdr->N, lane = threadIdx.x & 31;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += (gridDim.x * blockDim.x) >> 5) {
     const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
-    for (int c = lane * 4; c < C; c += 128) {
+    for (int c0 = 0; c0 < C; c0 += 128) {  // warp-uniform bound: the shuffles need every lane
+      const int c = c0 + lane * 4;
+      const bool col = c < C;
       float4 a = f4z(), b = f4z();
-      int e = e0;
-      for (; e + 2 <= e1; e += 2) {
-        const int r0 = rev[e], r1 = rev[e + 1];
-        const float4 a0 = ld4(x + size_t(e) * C + c), a1 = ld4(x + size_t(e + 1) * C + c);
-        const float4 b0 = ld4(x + size_t(r0) * C + c), b1 = ld4(x + size_t(r1) * C + c);
-        a = add4(add4(a, a0), a1);
-        b = add4(add4(b, b0), b1);
+      for (int w0 = e0; w0 < e1; w0 += 32) {
+        const int myrev = w0 + lane < e1 ? rev[w0 + lane] : 0;
+        const int cnt = min(32, e1 - w0);
+        for (int j = 0; j < cnt; j += kSegU) {
+          float4 va[kSegU], vb[kSegU];
+#pragma unroll
+          for (int u = 0; u < kSegU; ++u) {
+            const int r = __shfl_sync(0xffffffffu, myrev, (j + u) & 31);
+            const bool ok = col && j + u < cnt;
+            va[u] = ok ? ld4(x + size_t(w0 + j + u) * C + c) : f4z();
+            vb[u] = ok ? ld4(x + size_t(r) * C + c) : f4z();
+          }
+#pragma unroll
+          for (int u = 0; u < kSegU; ++u)
+            if (j + u < cnt) a = add4(a, va[u]), b = add4(b, vb[u]);
+        }
       }
-      for (; e < e1; ++e) {
-        a = add4(a, ld4(x + size_t(e) * C + c));
-        b = add4(b, ld4(x + size_t(rev[e]) * C + c));
-      }
+      if (!col) continue;
       if (fold) {
         st4(S + size_t(i) * C + c, add4(a, b));
       } else {
@@ -1674,7 +1718,7 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     const bool mat = c.store_a1;  // tensor-core shapes: gathered operands materialised elementwise
     if (mat) {
       Prof pr(c, "bwd.edge_act", st);
-      edge_bwd_prep_kernel<<<gridn((long long)c.Ec * H / 4, 256, sm * 16), 256, 0, st>>>(
+      edge_bwd_prep_kernel<<<gridn((c.Ec + kEwU - 1) / kEwU * 32, 256, sm * 16), 256, 0, st>>>(
           c.hdr, P, c.edge_dst, c.edge_src, c.geo, wd, b1, c.dagg, z2, dzA, c.scratch, H);
     } else {
       Prof pr(c, "bwd.edge_dz2_gather", st);

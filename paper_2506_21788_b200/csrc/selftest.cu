@@ -162,3 +162,82 @@ extern "C" int hmtl_selftest_time(int mode, int rows, int K, int N, int iters, f
   if (e != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("selftest_time: ") + cudaGetErrorString(e));
   return 0;
 }
+
+// Tensor-pipe issue-rate probe (engine design, not the training path): one CTA
+// per SM, lane 0 issues n back-to-back MMAs (M = 128, N, one K step each) into
+// one accumulator and reports SM clocks per MMA.  variant: 0 tf32 A,B in smem;
+// 1 tf32 A in TMEM; 2 bf16 (kind::f16) A,B in smem; 3 bf16 A in TMEM.
+namespace hmtl_b200 {
+namespace {
+__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int variant, int N, int n, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = tc::align1k(sm_raw);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < (16384 + 32768) / 16; i += blockDim.x) reinterpret_cast<float4*>(sm)[i] = make_float4(0, 0, 0, 0);
+  if (tid < 32) tc::tmem_alloc(&slot, 512);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_proxy_async();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = slot;
+  if (tid == 0) {
+    const bool f16 = variant >= 2, ts = variant & 1;
+    const uint32_t idesc = f16 ? ((1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24))
+                               : tc::idesc_tf32(N);
+    const uint32_t a_s = tc::smem_u32(sm), b_s = tc::smem_u32(sm + 16384);
+    const long long t0 = clock64();
+    for (int i = 0; i < n; ++i) {
+      const uint32_t o = 32 * (i & 3);
+      const uint64_t bd = tc::sdesc_sw128(b_s + o);
+      const uint32_t acc = i ? 1u : 0u;
+      if (!f16 && !ts) {
+        tc::mma_tf32(tmem, tc::sdesc_sw128(a_s + o), bd, idesc, acc);
+      } else if (!f16) {
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+                     "r"(tmem + 256 + 8 * (i & 3)), "l"(bd), "r"(idesc), "r"(acc));
+      } else if (!ts) {
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                     "l"(tc::sdesc_sw128(a_s + o)), "l"(bd), "r"(idesc), "r"(acc));
+      } else {
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+                     "r"(tmem + 256 + 8 * (i & 3)), "l"(bd), "r"(idesc), "r"(acc));
+      }
+    }
+    tc::mma_commit(&bar);
+    tc::mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (tid < 32) tc::tmem_dealloc(tmem, 512);
+}
+}  // namespace
+}  // namespace hmtl_b200
+
+extern "C" int hmtl_selftest_mma_rate(int variant, int N, int n, float* clk_per_mma) {
+  cudaSetDevice(0);
+  long long* d;
+  HMTL_CUDA(cudaMalloc(&d, 148 * sizeof(long long)));
+  const int smem = 16384 + 32768 + 1024;
+  cudaFuncSetAttribute(mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mma_rate_kernel<<<148, 128, smem>>>(variant, N, n, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[148] = {0};
+  if (e == cudaSuccess) cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("mma_rate: ") + cudaGetErrorString(e));
+  double s = 0;
+  for (long long v : h) s += double(v);
+  *clk_per_mma = float(s / 148 / n);
+  return 0;
+}

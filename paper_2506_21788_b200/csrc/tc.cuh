@@ -138,15 +138,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 // ================================================================ row GEMM
-// Warp-specialised, persistent.  Warps 0-3 produce A (8 lanes per row ->
-// coalesced 128 B row segments; the per-row gather context is loaded once per
-// tile, not per K-chunk) into a ring of smem stages; warp 4 allocates TMEM and
-// one lane issues the 3xTF32 MMAs; warps 5-8 drain a double-buffered TMEM
-// accumulator through the epilogue (warp w reads TMEM lanes 32*(w%4)..+31,
-// transposes each 32x32 slab through padded smem so stores are row-coalesced),
-// overlapping tile t's epilogue with tile t+1's MMAs.  When the whole B image
-// (hi+lo, K x Nt) fits next to two A stages it is loaded once per CTA
-// ("resident"), otherwise each stage carries its B slice.
+// Warp-specialised, persistent.  Warps 0-7 produce A: 4 lanes per row (32
+// contiguous bytes each -> coalesced 128 B row segments), 16 rows per warp;
+// the chunk sequence runs across tile boundaries with the next chunk's loads
+// in flight while the current one is split into tf32 hi/lo and stored (the
+// per-row gather context is computed once per tile).  Warp 8 issues the
+// 3xTF32 MMAs (one lane) and owns B: when the whole B image slice (hi+lo,
+// K x Nt) fits next to two A stages it is made resident by bulk async copies
+// (cp.async.bulk -> mbarrier tx count) and reloaded only when the tile's
+// (segment, n0) changes, after the MMAs that read it have completed;
+// otherwise an elected producer lane bulk-copies each stage's B slice.
+// Warps 9-16 drain a double-buffered TMEM accumulator (two warps per TMEM
+// lane quadrant, alternate 32-column slabs), transposing each 32x32 slab
+// through an XOR-swizzled 4 KB smem tile so global stores are row-coalesced,
+// overlapping tile t's epilogue with tile t+1's MMAs.
 // P must provide: RowSet rows; int K, Ncols; const float* bimg; size_t bimg_seg;
 //   typename P::RC rctx(int seg, int row) const;                    // per-row gather context
 //   float4 a4(int seg, int row, const RC&, int k) const;           // A(row, k..k+3)
@@ -156,11 +161,14 @@ constexpr int kMaxStages = 4;
 // engine ablation switches for hmtl_selftest_time (bit0: producers skip A loads/stores,
 // bit1: epilogue skips global stores); always 0 on the training path.
 static __device__ int g_tc_debug = 0;
-constexpr int kProdWarps = 16;  // 8 rows each (4 lanes per row)
-constexpr int kRowThreads = (kProdWarps + 5) * 32;  // producers, 1 MMA warp, 4 epilogue warps
+constexpr int kProdWarps = 8;                                  // 16 rows each
+constexpr int kRowIt = 128 / (kProdWarps * 8);                 // row groups of 8 per producer warp
+constexpr int kEpiWarps = 8;                                   // 2 per TMEM lane quadrant
+constexpr int kMmaWarp = kProdWarps, kEpiWarp0 = kProdWarps + 1;
+constexpr int kRowThreads = (kProdWarps + 1 + kEpiWarps) * 32;  // 544
 constexpr size_t kSmemLimit = 227 * 1024;
-constexpr int kEpiLd = 36;  // padded row stride (floats) of the epilogue transpose slab
-constexpr size_t kEpiBytes = size_t(128) * kEpiLd * 4;
+constexpr size_t kEpiBytes = size_t(kEpiWarps) * 32 * 32 * 4;  // one 4 KB slab per epilogue warp
+constexpr size_t kRowBars = 256;
 
 struct RowPlan {
   int Nt, stages, resident;
@@ -172,18 +180,28 @@ inline RowPlan row_plan(int K, int Nt) {
   r.a_stage = size_t(2 * 128 * KC) * 4;  // hi + lo
   const size_t b_chunk = size_t(2 * Nt * KC) * 4;
   const size_t b_all = b_chunk * (K / KC);
-  r.resident = (b_all + 2 * r.a_stage + kEpiBytes + 256 + 1024 <= kSmemLimit) ? 1 : 0;
+  r.resident = (b_all + 2 * r.a_stage + kEpiBytes + kRowBars + 1024 <= kSmemLimit) ? 1 : 0;
   r.b_res = r.resident ? b_all : 0;
   r.b_stage = r.resident ? 0 : b_chunk;
   const size_t per = r.a_stage + r.b_stage;
-  int st = int((kSmemLimit - 256 - kEpiBytes - r.b_res) / per);
+  int st = int((kSmemLimit - kRowBars - 1024 - kEpiBytes - r.b_res) / per);
   r.stages = st < 2 ? 2 : (st > kMaxStages ? kMaxStages : st);
-  r.smem = r.b_res + r.stages * per + kEpiBytes + 128 + 1024;  // +1 KB: manual 1 KB alignment
+  r.smem = r.b_res + r.stages * per + kEpiBytes + kRowBars + 1024;  // +1 KB: manual 1 KB alignment
   return r;
 }
 
 __device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
   return p + ((1024 - (smem_u32(p) & 1023)) & 1023);
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// bulk async copy global -> shared (16 B aligned, bytes % 16 == 0), completes on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
 template <class P>
@@ -196,14 +214,16 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   uint8_t* stages = smem_raw + plan.b_res;
   float* epi_smem = reinterpret_cast<float*>(stages + kStages * SB);
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kStages * SB + kEpiBytes);
-  uint64_t* full = bars;                        // [kStages], count = producer threads
+  uint64_t* full = bars;                        // [kStages], count = producer threads (+ tx)
   uint64_t* empty = bars + kStages;             // [kStages], count 1 (MMA commit)
   uint64_t* accfull = bars + 2 * kStages;       // [2], count 1
-  uint64_t* accempty = bars + 2 * kStages + 2;  // [2], count 128
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  uint64_t* accempty = bars + 2 * kStages + 2;  // [2], count = epilogue threads
+  uint64_t* bfull = bars + 2 * kStages + 4;     // resident B landed (tx)
+  uint64_t* bdone = bars + 2 * kStages + 5;     // MMAs reading the resident B completed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 6);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t acc_cols = Nt <= 32 ? 32 : (Nt <= 64 ? 64 : (Nt <= 128 ? 128 : 256));
-  constexpr int kMmaWarp = kProdWarps, kProdThreads = kProdWarps * 32;
+  constexpr int kProdThreads = kProdWarps * 32;
   if (warp == kMmaWarp) tmem_alloc(tmem_slot, 2 * acc_cols);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -212,8 +232,10 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accfull[b], 1);
-      mbar_init(&accempty[b], 128);
+      mbar_init(&accempty[b], kEpiWarps * 32);
     }
+    mbar_init(bfull, 1);
+    mbar_init(bdone, 1);
     fence_mbar_init();
   }
   int mt_seg[kMaxSlots + 1];
@@ -226,6 +248,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   const int ntn = p.Ncols / Nt;
   const int total = total_m * ntn;
   const int nchunks = p.K / KC;
+  const uint32_t b_slice = uint32_t(Nt) * 128;  // bytes of one (chunk, hi|lo) B slice
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -234,79 +257,120 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   if (warp < kProdWarps) {  // ------------------------------------- producers
     // 4 lanes per row, each lane two k-groups (32 contiguous bytes of the row):
     // 8 consecutive rows per store instruction -> all 8 16B bank groups, no conflicts
-    int stage = 0;
-    uint32_t phase = 0;
-    int res_key = -1;  // (seg, n0) of the resident B image
     const int kq = lane & 3, rsub = lane >> 2;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const int tm = t / ntn, n0 = (t % ntn) * Nt;
+    struct Cur {
+      int t, c, seg, n0;
+      int rows[kRowIt];
+      typename P::RC rc[kRowIt];
+    };
+    auto set_tile = [&](Cur& u) {
+      if (u.t >= total) return;
+      const int tm = u.t / ntn;
+      u.n0 = (u.t % ntn) * Nt;
       int seg = 0;
       while (tm >= mt_seg[seg + 1]) ++seg;
-      constexpr int kIt = 128 / (kProdWarps * 8);  // row groups of 8 per warp
-      int rows_it[kIt];
-      typename P::RC rc[kIt];
+      u.seg = seg;
 #pragma unroll
-      for (int it = 0; it < kIt; ++it) {  // rows warp*8*kIt + it*8 + rsub
-        const int v = p.rows.begin(seg) + (tm - mt_seg[seg]) * 128 + warp * 8 * kIt + it * 8 + rsub;
-        rows_it[it] = v < p.rows.end(seg) ? p.rows.row(v) : -1;
-        if (rows_it[it] >= 0) rc[it] = p.rctx(seg, rows_it[it]);
+      for (int it = 0; it < kRowIt; ++it) {  // rows warp*8*kRowIt + it*8 + rsub
+        const int v = p.rows.begin(seg) + (tm - mt_seg[seg]) * 128 + warp * 8 * kRowIt + it * 8 + rsub;
+        u.rows[it] = v < p.rows.end(seg) ? p.rows.row(v) : -1;
+        if (u.rows[it] >= 0) u.rc[it] = p.rctx(seg, u.rows[it]);
       }
-      const float4* bsrc = reinterpret_cast<const float4*>(p.bimg + seg * p.bimg_seg);
-      if (plan.resident && res_key != seg * 4096 + n0) {
-        asm volatile("bar.sync 1, %0;" ::"r"(kProdThreads) : "memory");
-        if (res_key >= 0) {  // the previous tile's last chunk must be consumed first
-          int ps = stage == 0 ? kStages - 1 : stage - 1;
-          uint32_t pph = stage == 0 ? (phase ^ 1) : phase;
-          mbar_wait(&empty[ps], pph);
-        }
-        // image rows n0..n0+Nt of every chunk/part are contiguous (SW128 rows of 128 B)
-        float4* bd = reinterpret_cast<float4*>(bres);
-        for (int c = 0; c < nchunks; ++c)
-          for (int part = 0; part < 2; ++part) {
-            const float4* bc = bsrc + (size_t(c) * 2 + part) * p.Ncols * 8 + size_t(n0) * 8;
-            float4* bo = bd + (size_t(c) * 2 + part) * Nt * 8;
-            for (int i = tid; i < Nt * 8; i += kProdThreads) bo[i] = bc[i];
-          }
-        fence_proxy_async();
-        asm volatile("bar.sync 1, %0;" ::"r"(kProdThreads) : "memory");
-        res_key = seg * 4096 + n0;
+    };
+    auto succ = [&](Cur& u) {
+      if (u.t >= total) return;
+      if (++u.c == nchunks) {
+        u.c = 0;
+        u.t += gridDim.x;
+        set_tile(u);
       }
-      for (int c = 0; c < nchunks; ++c) {
-        const bool skip = g_tc_debug & 1;
-        float4 x[kIt][2];  // [row it][k-group half]
+    };
+    auto load = [&](const Cur& u, float4 (&x)[kRowIt][2]) {
+      const bool skip = g_tc_debug & 1;
 #pragma unroll
-        for (int it = 0; it < kIt; ++it)
+      for (int it = 0; it < kRowIt; ++it)
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-            x[it][h] = (rows_it[it] >= 0 && !skip) ? p.a4(seg, rows_it[it], rc[it], c * KC + 8 * kq + 4 * h)
-                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-        mbar_wait(&empty[stage], phase ^ 1);
-        float* a_hi = reinterpret_cast<float*>(stages + stage * SB);
-        float* a_lo = a_hi + 128 * KC;
-        if (!skip)
-#pragma unroll
-          for (int it = 0; it < kIt; ++it)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) put4(a_hi, a_lo, 2 * kq + h, warp * 8 * kIt + it * 8 + rsub, x[it][h]);
-        if (!plan.resident) {
-          float4* b_st = reinterpret_cast<float4*>(a_lo + 128 * KC);
-          for (int part = 0; part < 2; ++part) {
-            const float4* bc = bsrc + (size_t(c) * 2 + part) * p.Ncols * 8 + size_t(n0) * 8;
-            for (int i = tid; i < Nt * 8; i += kProdThreads) b_st[part * Nt * 8 + i] = bc[i];
-          }
-        }
-        fence_proxy_async();
-        mbar_arrive(&full[stage]);
-        if (++stage == kStages) stage = 0, phase ^= 1;
-      }
-    }
-  } else if (warp == kMmaWarp) {  // --------------------------------- MMA issuer
+        for (int h = 0; h < 2; ++h)
+          x[it][h] = (u.rows[it] >= 0 && !skip) ? p.a4(u.seg, u.rows[it], u.rc[it], u.c * KC + 8 * kq + 4 * h)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
     int stage = 0;
     uint32_t phase = 0;
+    auto fill = [&](const Cur& u, const float4 (&x)[kRowIt][2]) {
+      mbar_wait(&empty[stage], phase ^ 1);
+      float* a_hi = reinterpret_cast<float*>(stages + stage * SB);
+      float* a_lo = a_hi + 128 * KC;
+      if (!(g_tc_debug & 1))
+#pragma unroll
+        for (int it = 0; it < kRowIt; ++it)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) put4(a_hi, a_lo, 2 * kq + h, warp * 8 * kRowIt + it * 8 + rsub, x[it][h]);
+      fence_proxy_async();
+      if (!plan.resident && tid == 0) {  // this stage's B slice rides on the same barrier
+        mbar_expect_tx(&full[stage], 2 * b_slice);
+        const float* bsrc = p.bimg + u.seg * p.bimg_seg;
+        for (int part = 0; part < 2; ++part)
+          bulk_g2s(reinterpret_cast<uint8_t*>(a_lo + 128 * KC) + part * b_slice,
+                   bsrc + (size_t(u.c) * 2 + part) * p.Ncols * KC + size_t(u.n0) * KC, b_slice, &full[stage]);
+      } else {
+        mbar_arrive(&full[stage]);
+      }
+      if (++stage == kStages) stage = 0, phase ^= 1;
+    };
+    Cur A, B;
+    A.t = blockIdx.x;
+    A.c = 0;
+    set_tile(A);
+    B = A;
+    succ(B);
+    float4 xa[kRowIt][2], xb[kRowIt][2];
+    if (A.t < total) load(A, xa);
+    if (B.t < total) load(B, xb);
+    while (A.t < total) {  // two chunks in registers: one being stored, the next in flight
+      fill(A, xa);
+      A = B;
+      succ(A);
+      if (A.t < total) load(A, xa);
+      if (B.t >= total) break;
+      fill(B, xb);
+      B = A;
+      succ(B);
+      if (B.t < total) load(B, xb);
+    }
+  } else if (warp == kMmaWarp) {  // --------------------------------- MMA issuer + resident B
+    int stage = 0;
+    uint32_t phase = 0, bphase = 0, dphase = 0;
     int ab = 0;
     uint32_t aphase = 0;
+    int res_key = -1;
     const uint32_t idesc = idesc_tf32(Nt);
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      if (plan.resident) {
+        const int tm = t / ntn, n0 = (t % ntn) * Nt;
+        int seg = 0;
+        while (tm >= mt_seg[seg + 1]) ++seg;
+        const int key = seg * 4096 + n0;
+        if (key != res_key) {
+          if (res_key >= 0) {  // every MMA that reads the old image must have completed
+            if (lane == 0) mma_commit(bdone);
+            __syncwarp();
+            mbar_wait(bdone, dphase);
+            dphase ^= 1;
+          }
+          if (lane == 0) {
+            mbar_expect_tx(bfull, uint32_t(nchunks) * 2 * b_slice);
+            const float* bsrc = p.bimg + seg * p.bimg_seg;
+            for (int c = 0; c < nchunks; ++c)
+              for (int part = 0; part < 2; ++part)
+                bulk_g2s(reinterpret_cast<uint8_t*>(bres) + (size_t(c) * 2 + part) * b_slice,
+                         bsrc + (size_t(c) * 2 + part) * p.Ncols * KC + size_t(n0) * KC, b_slice, bfull);
+          }
+          __syncwarp();
+          mbar_wait(bfull, bphase);
+          bphase ^= 1;
+          res_key = key;
+        }
+      }
       mbar_wait(&accempty[ab], aphase ^ 1);
       tc_fence_after();
       for (int c = 0; c < nchunks; ++c) {
@@ -327,10 +391,12 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
       if (++ab == 2) ab = 0, aphase ^= 1;
     }
   } else {  // ------------------------------------------------------- epilogue
-    const int q = warp & 3;
+    const int q = warp & 3;                 // TMEM lane quadrant this warp may access
+    const int half = (warp - kEpiWarp0) >> 2;  // which alternate 32-column slabs
     int ab = 0;
     uint32_t aphase = 0;
-    float* slab = epi_smem + q * 32 * kEpiLd;  // this warp's 32 rows x 32 cols (padded)
+    float* slab = epi_smem + (warp - kEpiWarp0) * 32 * 32;  // 32 rows x 32 cols, 16 B chunks XOR-swizzled
+    const int nslab = (Nt + 31) / 32;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const int tm = t / ntn, n0 = (t % ntn) * Nt;
       int seg = 0;
@@ -344,35 +410,37 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
         if (rows_it[it] >= 0) rc[it] = p.rctx(seg, rows_it[it]);
       }
       // epilogue operands that do not depend on the accumulator (residuals, saved
-      // activations) are loaded one 32-column slab ahead -- the first slab's
-      // before waiting for the MMAs
-      typename P::Aux aux[2][8];
-      const int c4 = (lane & 7) * 4;
+      // activations): the first slab's are loaded before waiting for the MMAs, later
+      // slabs' are issued ahead of their TMEM load and transpose
+      typename P::Aux aux[8];
+      const int cc = lane & 7, c4 = cc * 4;
+      if (half < nslab) {
 #pragma unroll
-      for (int it = 0; it < 8; ++it)
-        if (rows_it[it] >= 0) aux[0][it] = p.epi_aux(seg, rows_it[it], rc[it], n0 + c4);
+        for (int it = 0; it < 8; ++it)
+          if (rows_it[it] >= 0) aux[it] = p.epi_aux(seg, rows_it[it], rc[it], n0 + half * 32 + c4);
+      }
       mbar_wait(&accfull[ab], aphase);
       tc_fence_after();
-      for (int j = 0; j < Nt; j += 32) {
-        const int cur = (j >> 5) & 1;
-        float acc[32];
-        __syncwarp();
-        tmem_ld32(tmem + ab * acc_cols + (uint32_t(q * 32) << 16) + j, acc);
-        if (j + 32 < Nt) {
+      for (int sl = half; sl < nslab; sl += 2) {
+        const int j = sl * 32;
+        if (sl != half) {
 #pragma unroll
           for (int it = 0; it < 8; ++it)
-            if (rows_it[it] >= 0) aux[cur ^ 1][it] = p.epi_aux(seg, rows_it[it], rc[it], n0 + j + 32 + c4);
+            if (rows_it[it] >= 0) aux[it] = p.epi_aux(seg, rows_it[it], rc[it], n0 + j + c4);
         }
+        float acc[32];
+        tmem_ld32(tmem + ab * acc_cols + (uint32_t(q * 32) << 16) + j, acc);
+        __syncwarp();
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-          reinterpret_cast<float4*>(slab + lane * kEpiLd)[i] =
+          *reinterpret_cast<float4*>(slab + lane * 32 + ((i ^ (lane & 7)) << 2)) =
               make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
         __syncwarp();
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
           const int rl = it * 4 + (lane >> 3);
-          const float4 a = reinterpret_cast<const float4*>(slab + rl * kEpiLd)[lane & 7];
-          if (rows_it[it] >= 0 && !(g_tc_debug & 2)) p.epi4(seg, rows_it[it], rc[it], n0 + j + c4, a, aux[cur][it]);
+          const float4 a = *reinterpret_cast<const float4*>(slab + rl * 32 + ((cc ^ (rl & 7)) << 2));
+          if (rows_it[it] >= 0 && !(g_tc_debug & 2)) p.epi4(seg, rows_it[it], rc[it], n0 + j + c4, a, aux[it]);
         }
       }
       tc_fence_before();
