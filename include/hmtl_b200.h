@@ -170,7 +170,8 @@ int hmtl_train_step(hmtl_ctx* ctx, const hmtl_train_cfg* cfg, void* stream);
 /* Per-layer parity probe: copies a named device cache tensor to the host
  * (syncs). names: "h" (layer 0..L: input of layer l, L = final), "P", "z1",
  * "z2", "agg", "vz1", "pooled", "ez" (layer = MLP layer), "Qf", "zf" (layer =
- * MLP layer >= 1), "s", "dE", "dF".  Returns #floats written in *n. */
+ * MLP layer >= 1), "s", "dE", "dF", "grads" (the whole gradient buffer
+ * [shared | owned head slots] of the last backward).  Returns #floats written in *n. */
 int hmtl_debug_fetch(hmtl_ctx* ctx, const char* name, int layer, float* host, size_t cap, size_t* n);
 
 /* Benchmark instrumentation: when enabled, every kernel scope records CUDA
@@ -183,6 +184,9 @@ int hmtl_profile_report(hmtl_ctx* ctx, char* json, size_t cap);
 /* Kernel nodes in the captured step graph (= kernel launches per graph step),
  * -1 before the first graph capture. */
 int hmtl_step_kernel_count(hmtl_ctx* ctx, int* n);
+/* Engine tuning: per-CTA phase timestamps (SM clocks, [CTA][32]) written by the
+ * most recent fused node-chain launch; needs HMTL_CHAIN_STAMPS at ctx_create. */
+int hmtl_debug_chain_stamps(hmtl_ctx* ctx, long long* out, int n);
 
 /* Engine self-test (not on the training path): runs the tcgen05 engines on
  * plain row-major matrices on device 0.  mode 0: C[rows x N] = X[rows x K] B[K x N]

@@ -106,6 +106,7 @@ SIGNATURES = {
     "hmtl_profile_enable": (C.c_int, [_P, C.c_int]),
     "hmtl_profile_report": (C.c_int, [_P, C.c_char_p, C.c_size_t]),
     "hmtl_step_kernel_count": (C.c_int, [_P, C.POINTER(C.c_int)]),
+    "hmtl_debug_chain_stamps": (C.c_int, [_P, C.POINTER(C.c_longlong), C.c_int]),
     "hmtl_selftest_mma_rate": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "hmtl_selftest_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _FP, _FP, _FP]),
     "hmtl_selftest_time": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _FP]),

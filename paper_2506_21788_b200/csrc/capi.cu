@@ -76,7 +76,7 @@ void free_ctx(Ctx& c) {
                   c.species, c.gslot, c.gperm, c.gnode_base, c.gedge_base, c.node_perm, c.edge_perm, c.hs, c.P,
                   c.z2, c.agg, c.vz1, c.pooled, c.ez, c.energy, c.Qf, c.zf, c.s, c.forces, c.dE, c.dF,
                   c.dagg, c.dhb, c.dvz1b, c.dzAb, c.dzBb, c.Sb, c.fzA, c.fzB, c.ds, c.dpooled, c.edA, c.edB,
-                  c.scratch, c.partial, c.partial_w, c.bimg, c.a1, c.af0, c.sf0, c.bimg_all, c.d_bjobs};
+                  c.scratch, c.partial, c.partial_w, c.partial_w2, c.bimg, c.a1, c.af0, c.sf0, c.bimg_all, c.d_bjobs};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto* p : c.pool) cudaFree(p);
@@ -89,6 +89,7 @@ void free_ctx(Ctx& c) {
   c.evs.clear();
   if (c.s_e) cudaStreamDestroy(c.s_e);
   if (c.s_w) cudaStreamDestroy(c.s_w);
+  if (c.s_w2) cudaStreamDestroy(c.s_w2);
   if (c.stream) cudaStreamDestroy(c.stream);
 }
 
@@ -203,10 +204,14 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     if (cudaStreamCreateWithPriority(&c.stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c.s_e, cudaStreamNonBlocking, lo) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&c.s_w, cudaStreamNonBlocking, lo) != cudaSuccess)
+        cudaStreamCreateWithPriority(&c.s_w, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c.s_w2, cudaStreamNonBlocking, lo) != cudaSuccess)
       rc = HMTL_ERR_INTERNAL;
   }
   if (const char* e = std::getenv("HMTL_SINGLE_STREAM")) c.multi_stream = e[0] == '0';
+  if (const char* e = std::getenv("HMTL_NO_CHAIN")) c.fuse_chain = e[0] == '0';
+  if (std::getenv("HMTL_CHAIN_STAMPS")) A(&c.chain_stamps, size_t(4096) * 32);
+  if (const char* e = std::getenv("HMTL_CHAIN_DBG")) c.chain_dbg = std::atoi(e);
   A(&c.params, c.PT);
   A(&c.grads, c.PT);
   A(&c.adam_m, c.PT);
@@ -272,6 +277,7 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   c.partial_cap = std::max(c.partial_cap, size_t(std::max(c.S, 1)) * size_t((E + 127) / 128 + 1) * (2 * std::max(H, W) + 1));
   A(&c.partial, c.partial_cap);
   A(&c.partial_w, c.partial_cap);
+  A(&c.partial_w2, c.partial_cap);
   c.bimg_cap = size_t(std::max(c.S, 2)) * 2 * (2 * std::max(H, W)) * (2 * std::max(H, W));
   A(&c.bimg, c.bimg_cap);
   if (const char* e = std::getenv("HMTL_NO_TC")) c.use_tc = e[0] == '0';
@@ -556,6 +562,7 @@ int hmtl_debug_fetch(hmtl_ctx* h, const char* name, int layer, float* host, size
   else if (nm == "Qf") src = c.Qf, cnt = N * W;
   else if (nm == "zf" && lay_ok(1, c.D - 2)) src = c.zf + (layer - 1) * size_t(c.Ec) * W, cnt = E * W;
   else if (nm == "s") src = c.s, cnt = E;
+  else if (nm == "grads") src = c.grads, cnt = c.PT;  // [shared | owned head slots] of the last backward
   else if (nm == "dE") src = c.dE, cnt = G;
   else if (nm == "dF") src = c.dF, cnt = 3 * N;
   else if (nm == "z1" && lay_ok(0, c.L - 1)) {
@@ -569,6 +576,14 @@ int hmtl_debug_fetch(hmtl_ctx* h, const char* name, int layer, float* host, size
   if (!host) return 0;
   if (cap < cnt) return fail(HMTL_ERR_CONTRACT, "debug_fetch: buffer too small");
   HMTL_CUDA(cudaMemcpy(host, src, cnt * 4, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int hmtl_debug_chain_stamps(hmtl_ctx* h, long long* out, int n) {
+  Ctx& c = h->c;
+  if (!c.chain_stamps) return fail(HMTL_ERR_CONTRACT, "chain stamps: set HMTL_CHAIN_STAMPS before ctx_create");
+  HMTL_CUDA(cudaDeviceSynchronize());
+  HMTL_CUDA(cudaMemcpy(out, c.chain_stamps, size_t(n) * sizeof(long long), cudaMemcpyDeviceToHost));
   return 0;
 }
 

@@ -79,7 +79,8 @@ struct Ctx {
   float *ds = nullptr, *dpooled = nullptr;
   float *edA = nullptr, *edB = nullptr, *scratch = nullptr;
   float* partial = nullptr;    // split-K partials of kernels on the main stream
-  float* partial_w = nullptr;  // ... and of the weight-gradient stream
+  float* partial_w = nullptr;   // ... and of the weight-gradient streams
+  float* partial_w2 = nullptr;
   size_t partial_cap = 0;
   // backward buffers that weight-gradient kernels read: one per layer, so the
   // main stream never overwrites what the side stream has yet to read
@@ -90,10 +91,13 @@ struct Ctx {
   float *fzA = nullptr, *fzB = nullptr;    // force head dz ping-pong [E][W]
   // concurrency inside the step: s_e runs the energy head branch, s_w the
   // weight gradients; both fork from / join into the step stream via events
-  cudaStream_t s_e = nullptr, s_w = nullptr;
+  cudaStream_t s_e = nullptr, s_w = nullptr, s_w2 = nullptr;
   std::vector<cudaEvent_t> evs;
   size_t ev_i = 0;
   bool multi_stream = true;
+  bool fuse_chain = true;  // node-row GEMM chains in one launch (chain.cuh)
+  long long* chain_stamps = nullptr;
+  int chain_dbg = 0;  // engine tuning: phase timestamps of the last chain launch
   float* bimg = nullptr;  // tcgen05 B-operand images (hi/lo, K-major)
   size_t bimg_cap = 0;
   bool use_tc = true;     // tcgen05 path for GEMMs whose shapes allow it
@@ -132,7 +136,7 @@ struct Ctx {
   size_t head_off(const std::string& name) const { return head_lay.at(name).offset; }
   float* head_params() const { return params + PS; }
   float* head_grads() const { return grads + PS; }
-  float* part(cudaStream_t st) const { return st == s_w ? partial_w : partial; }
+  float* part(cudaStream_t st) const { return st == s_w ? partial_w : (st == s_w2 ? partial_w2 : partial); }
   // stream for a side branch (the step stream itself while B images are being
   // recorded: that eager step shares one image scratch buffer)
   cudaStream_t side(cudaStream_t which, cudaStream_t st) const {

@@ -18,6 +18,7 @@
 #include <type_traits>
 #include <utility>
 
+#include "chain.cuh"
 #include "ctx.cuh"
 #include "tc.cuh"
 
@@ -492,7 +493,8 @@ void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& 
     const long long mtiles = (rows_cap + 127) / 128 + nseg;
     // split N when there are too few row tiles to fill the GPU (node-row GEMMs)
     int Nt = p.Ncols;
-    while (Nt > 32 && mtiles * (p.Ncols / Nt) < sm && (Nt / 2) % 32 == 0) Nt /= 2;
+    // (one wave: the largest split whose tile count still fits the SMs)
+    while (Nt > 32 && mtiles * (p.Ncols / Nt) * 2 <= sm && (Nt / 2) % 32 == 0) Nt /= 2;
     const tc::RowPlan plan = tc::row_plan(p.K, Nt);
     set_smem(tc::tc_row_kernel<TcRow<P>>, plan.smem);
     tc::tc_row_kernel<TcRow<P>><<<gridn(mtiles * (p.Ncols / Nt), 1, sm), tc::kRowThreads, plan.smem, st>>>(q, plan);
@@ -530,6 +532,36 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
   gemm_atb_kernel<P><<<grid, 256, 0, st>>>(p, c.part(st), nsplit);
   const long long total = (long long)p.K * p.Ncols * p.rows.nseg;
   gemm_atb_reduce<P><<<gridn(total, 256, c.sm_count * 8), 256, 0, st>>>(p, c.part(st), nsplit);
+}
+
+// fused node-row GEMM chain (chain.cuh) over the prebuilt B images of the next
+// `G` tensor-core GEMMs in recorded call order; false = use the unfused path
+bool chain_ok(const Ctx& c) {
+  return c.use_tc && c.bimg_ready && c.fuse_chain && c.H % 32 == 0 && c.H <= 128;
+}
+void launch_chain(Ctx& c, const char* name, int G, const chain::Gemm* gs, cudaStream_t st) {
+  Prof pr(c, name, st);
+  chain::Chain q{};
+  q.count = &c.hdr->N;
+  q.G = G;
+  q.H = c.H;
+  for (int i = 0; i < G; ++i) {
+    q.g[i] = gs[i];
+    q.g[i].img = c.bjobs[c.bimg_idx++].out;
+  }
+  q.stamps = c.chain_stamps;
+  q.dbg = c.chain_dbg;
+  const int grid = int((c.Nc + 127) / 128);
+  auto go = [&](auto kern) {
+    set_smem(kern, chain::kSmem);
+    kern<<<grid, chain::kThreads, chain::kSmem, st>>>(q);
+  };
+  using namespace chain;
+  const int r0 = gs[0].role, r1 = G > 1 ? gs[1].role : -1, r2 = G > 2 ? gs[2].role : -1;
+  if (r0 == kFwdNode1 && r1 == kFwdNode2 && r2 == kFwdP) go(chain_kernel<kFwdNode1, kFwdNode2, kFwdP>);
+  else if (r0 == kFwdNode1 && r1 == kFwdNode2 && r2 < 0) go(chain_kernel<kFwdNode1, kFwdNode2, -1>);
+  else if (r0 == kBwdL11 && r1 == kBwdL1 && r2 == kBwdL4) go(chain_kernel<kBwdL11, kBwdL1, kBwdL4>);
+  else if (r0 == kBwdL1 && r1 == kBwdL4 && r2 < 0) go(chain_kernel<kBwdL1, kBwdL4, -1>);
 }
 
 RowSet node_rows(Ctx& c) {
@@ -721,6 +753,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     Prof pr(c, "fwd.embed", st);
     embed_kernel<<<gridn(NH, 256, sm * 16), 256, 0, st>>>(c.hdr, c.species, c.shared_param("embed"), c.hs, H);
   }
+  bool p_done = false;  // P of this layer already produced by the previous node chain
   for (int l = 0; l < L; ++l) {
     const std::string p = "layer" + std::to_string(l) + ".";
     const float* h = c.hs + size_t(l) * NH;
@@ -730,10 +763,11 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     float* agg = c.agg + size_t(l) * NH;
     float* vz1 = c.vz1 + size_t(l) * NH;
     const float* W1 = c.params + c.shared_off(p + "edge.W1");
-    {
+    if (!p_done) {
       PProb q{node_rows(c), H, 2 * H, H, h, W1, P};
       ab(q, c.Nc, 1, st, sm, c);
     }
+    p_done = false;
     if (c.store_a1) {
       Prof pr(c, "fwd.edge_act", st);
       edge_a1_kernel<<<gridn((c.Ec + kEwU - 1) / kEwU * 32, 256, sm * 16), 256, 0, st>>>(
@@ -750,6 +784,16 @@ void launch_forward(Ctx& c, cudaStream_t st) {
       Prof pr(c, "fwd.agg_segsum", st);
       if (H % 4 == 0) agg4_kernel<<<gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st>>>(c.hdr, c.row_ptr, z2, agg, H);
       else agg_kernel<<<gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st>>>(c.hdr, c.row_ptr, z2, agg, H);
+    }
+    if (chain_ok(c)) {  // node MLP + residual (+ the next layer's P) in one launch
+      const int G = l + 1 < L ? 3 : 2;
+      chain::Gemm gs[3] = {
+          {chain::kFwdNode1, 2 * H, H, nullptr, h, agg, c.params + c.shared_off(p + "node.b1"), vz1, nullptr},
+          {chain::kFwdNode2, H, H, nullptr, h, nullptr, c.params + c.shared_off(p + "node.b2"), hn, nullptr},
+          {chain::kFwdP, H, 2 * H, nullptr, nullptr, nullptr, nullptr, c.P + size_t(l + 1) * 2 * NH, nullptr}};
+      launch_chain(c, "fwd.node_chain", G, gs, st);
+      p_done = l + 1 < L;
+      continue;
     }
     {
       Node1Prob q{node_rows(c), 2 * H, H, H, h, agg, c.params + c.shared_off(p + "node.W1"),
@@ -1593,7 +1637,7 @@ void launch_backward(Ctx& c, cudaStream_t st) {
   const size_t GW = size_t(c.Gc) * W;
   // streams: st = critical path (dx chain), se = energy head branch, sw = weight
   // gradients (consumed only by the gradient sync / AdamW after the final join)
-  cudaStream_t se = c.side(c.s_e, st), sw = c.side(c.s_w, st);
+  cudaStream_t se = c.side(c.s_e, st), sw = c.side(c.s_w, st), sw2 = c.side(c.s_w2, st);
   float* dhL = c.dhb + size_t(L) * NH;  // dL/dh_L, written by the heads
 
   // ---------------- energy heads (hmtl/model.hpp:512-524)
@@ -1666,20 +1710,22 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     // layer 0 (factorised): T = S_dst(dz0) + S_src(dz0)
     float* Sf = c.Sb + size_t(L) * SBS;
     segsum2(c, dz, W, 1, Sf, st);
-    c.dep(st, sw);
+    c.dep(st, sw2);
     F0NodeGrad ng{node_rows_by_head(c), H, W, H, W, hL, Sf, HeadG{c.head_grads(), c.PH, wf0}};
-    atb(ng, c, c.nsplit_node, sw, c.Nc);
+    atb(ng, c, c.nsplit_node, sw2, c.Nc);
     if (W % 4 == 0) {
-      colsum2(c, edge_rows_by_head(c), c.dist, 1, dz, W, c.head_grads() + wf0 + size_t(H) * W, c.PH, sw);
+      colsum2(c, edge_rows_by_head(c), c.dist, 1, dz, W, c.head_grads() + wf0 + size_t(H) * W, c.PH, sw2);
     } else {
       F0EdgeGrad eg{edge_rows_by_head(c), 2, W, H, W, c.dist, dz, HeadG{c.head_grads(), c.PH, wf0 + size_t(H) * W}};
-      atb(eg, c, c.nsplit_edge, sw, c.Ec);
+      atb(eg, c, c.nsplit_edge, sw2, c.Ec);
     }
     c.dep(se, st);  // dL/dh_L = energy part (written) + force part (accumulated next)
     F0Dh dhq{node_rows_by_head(c), W, H, H, W, Sf, HeadW{c.head_params(), c.PH, wf0}, dhL};
     ab(dhq, c.Nc, c.S, st, sm, c);
   }
   // ---------------- encoder layers in reverse (hmtl/model.hpp:552-617)
+  const bool fused = chain_ok(c);
+  bool node_done = false;
   for (int l = L - 1; l >= 0; --l) {
     const std::string p = "layer" + std::to_string(l) + ".";
     const float* h = c.hs + size_t(l) * NH;
@@ -1697,23 +1743,28 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     float* dzA = c.dzAb + size_t(l) * EH;
     float* dzB = c.dzBb + size_t(l) * EH;
     float* Sl = c.Sb + size_t(l) * SBS;
-    c.dep(st, sw);  // dh ready
+    if (!node_done) {  // (else: the previous layer's chain produced dvz1, dh2, dagg)
+      if (fused && l == L - 1) {  // [L1, L4] of the top layer as one chain
+        chain::Gemm gs[2] = {
+            {chain::kBwdL1, H, H, nullptr, vz1, dh, nullptr, dvz1, nullptr},
+            {chain::kBwdL4, H, 2 * H, nullptr, dh, nullptr, nullptr, dh2, c.dagg}};
+        launch_chain(c, "bwd.node_chain", 2, gs, st);
+      } else {
+        L1Prob q1{node_rows(c), H, H, H, dh, c.params + c.shared_off(p + "node.W2"), vz1, dvz1};
+        ab(q1, c.Nc, 1, st, sm, c);
+        L4Prob q4{node_rows(c), H, 2 * H, H, dvz1, c.params + c.shared_off(p + "node.W1"), dh, dh2, c.dagg};
+        ab(q4, c.Nc, 1, st, sm, c);
+      }
+    }
+    node_done = false;
+    c.dep(st, sw);  // dh (input), dvz1 ready
     {
       L2Prob q{node_rows(c), H + 1, H, H, vz1, dh, c.grads + c.shared_off(p + "node.W2")};
       atb(q, c, c.nsplit_node, sw, c.Nc);
     }
     {
-      L1Prob q{node_rows(c), H, H, H, dh, c.params + c.shared_off(p + "node.W2"), vz1, dvz1};
-      ab(q, c.Nc, 1, st, sm, c);
-    }
-    c.dep(st, sw);  // dvz1 ready
-    {
       L3Prob q{node_rows(c), 2 * H + 1, H, H, h, agg, dvz1, c.grads + c.shared_off(p + "node.W1")};
       atb(q, c, c.nsplit_node, sw, c.Nc);
-    }
-    {
-      L4Prob q{node_rows(c), H, 2 * H, H, dvz1, c.params + c.shared_off(p + "node.W1"), dh, dh2, c.dagg};
-      ab(q, c.Nc, 1, st, sm, c);
     }
     const bool mat = c.store_a1;  // tensor-core shapes: gathered operands materialised elementwise
     if (mat) {
@@ -1736,11 +1787,23 @@ void launch_backward(Ctx& c, cudaStream_t st) {
       ab(q, c.Ec, 1, st, sm, c);
     }
     segsum2(c, dzB, H, 0, Sl, st);
-    c.dep(st, sw);  // dz1 and its segment sums ready
-    colsum2(c, edge_rows(c), &c.geo[0].w, 4, dzB, H, geW1 + size_t(2) * H * H, 0, sw);
+    c.dep(st, sw2);  // dz1 and its segment sums ready (second weight-gradient stream)
+    colsum2(c, edge_rows(c), &c.geo[0].w, 4, dzB, H, geW1 + size_t(2) * H * H, 0, sw2);
     {
       L10Prob q{node_rows(c), H, 2 * H, H, h, Sl, geW1};
-      atb(q, c, c.nsplit_node, sw, c.Nc);
+      atb(q, c, c.nsplit_node, sw2, c.Nc);
+    }
+    if (fused && l > 0) {  // L11 of this layer + [L1, L4] of the layer below
+      const std::string pb = "layer" + std::to_string(l - 1) + ".";
+      const float* vz1b = c.vz1 + size_t(l - 1) * NH;
+      float* dhb2 = c.dhb + size_t(l - 1) * NH;
+      chain::Gemm gs[3] = {
+          {chain::kBwdL11, 2 * H, H, nullptr, nullptr, Sl, nullptr, dh2, nullptr},
+          {chain::kBwdL1, H, H, nullptr, vz1b, nullptr, nullptr, c.dvz1b + size_t(l - 1) * NH, nullptr},
+          {chain::kBwdL4, H, 2 * H, nullptr, dh2, nullptr, nullptr, dhb2, c.dagg}};
+      launch_chain(c, "bwd.node_chain", 3, gs, st);
+      node_done = true;
+      continue;
     }
     {
       L11Prob q{node_rows(c), 2 * H, H, H, Sl, eW1, dh2};
@@ -1761,6 +1824,7 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     }
   }
   c.dep(sw, st);  // every weight gradient is final
+  c.dep(sw2, st);
 }
 
 // debug probe: z1 of layer l (the factorised pre-activation), [E x H]

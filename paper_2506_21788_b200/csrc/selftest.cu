@@ -186,7 +186,17 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int variant, int N, in
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = slot;
-  if (tid == 0) {
+  if (variant == 4) {  // warp-uniform 12-MMA blocks (the engine's issue path)
+    if (tid < 32) {
+      const uint32_t a_s = tc::smem_u32(sm), b_s = tc::smem_u32(sm + 16384);
+      const long long t0 = clock64();
+      for (int i = 0; i < n; i += 12) tc::issue_chunk_warp(tmem, a_s, a_s + 4096, b_s, b_s + 4096, tc::idesc_tf32(N), i ? 1u : 0u);
+      tc::commit_warp(&bar);
+      tc::mbar_wait(&bar, 0);
+      const long long t1 = clock64();
+      if (tid == 0) out[blockIdx.x] = t1 - t0;
+    }
+  } else if (tid == 0) {
     const bool f16 = variant >= 2, ts = variant & 1;
     const uint32_t idesc = f16 ? ((1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24))
                                : tc::idesc_tf32(N);

@@ -130,6 +130,46 @@ __device__ __forceinline__ void issue_chunk(uint32_t tmem, const float* a_hi, co
   }
 }
 
+// Warp-wide variant: called by all 32 lanes with warp-uniform arguments (the
+// descriptors stay in uniform registers); one elected lane issues the chunk's
+// 12 MMAs from a single asm block (K step = +32 B = +2 in the descriptor's
+// address field) and, when `commit_bar` is set, commits them to that mbarrier.
+__device__ __forceinline__ void issue_chunk_warp(uint32_t tmem, uint32_t a_hi, uint32_t a_lo, uint32_t b_hi,
+                                                 uint32_t b_lo, uint32_t idesc, uint32_t accumulate) {
+  const uint64_t dah = sdesc_sw128(a_hi), dal = sdesc_sw128(a_lo);
+  const uint64_t dbh = sdesc_sw128(b_hi), dbl = sdesc_sw128(b_lo);
+  asm volatile(
+      "{\n\t.reg .pred e, p0, pt;\n\t.reg .b64 ah, al, bh, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p0, %5, 0;\n\t"
+      "setp.ne.b32 pt, %6, 0;\n\t"
+      "mov.b64 ah, %1;\n\tmov.b64 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %7, p0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %7, pt;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %7, pt;\n\t"
+      "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %7, pt;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %7, pt;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %7, pt;\n\t"
+      "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %7, pt;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %7, pt;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %7, pt;\n\t"
+      "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %7, pt;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %7, pt;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %7, pt;\n\t"
+      "}" ::"r"(tmem),
+      "l"(dah), "l"(dal), "l"(dbh), "l"(dbl), "r"(accumulate), "r"(1u), "r"(idesc));
+}
+// warp-wide: the elected lane (the one that issued the MMAs) commits them to `bar`
+__device__ __forceinline__ void commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // B images (weights) are built per problem by bimg_prob_kernel (model.cu):
 // per 32-k chunk c, [hi | lo], each N rows x 128 B in the SW128 layout above.
 
@@ -352,7 +392,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
         const int key = seg * 4096 + n0;
         if (key != res_key) {
           if (res_key >= 0) {  // every MMA that reads the old image must have completed
-            if (lane == 0) mma_commit(bdone);
+            commit_warp(bdone);
             __syncwarp();
             mbar_wait(bdone, dphase);
             dphase ^= 1;
@@ -376,14 +416,13 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
       for (int c = 0; c < nchunks; ++c) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        if (lane == 0) {
-          float* a_hi = reinterpret_cast<float*>(stages + stage * SB);
-          float* a_lo = a_hi + 128 * KC;
-          float* b_hi = plan.resident ? bres + size_t(c) * 2 * KC * Nt : a_lo + 128 * KC;
-          float* b_lo = b_hi + Nt * KC;
-          issue_chunk(tmem + ab * acc_cols, a_hi, a_lo, b_hi, b_lo, idesc, c == 0);
-          mma_commit(&empty[stage]);
-          if (c == nchunks - 1) mma_commit(&accfull[ab]);
+        {
+          const uint32_t a_hi = smem_u32(stages + stage * SB), a_lo = a_hi + 128 * KC * 4;
+          const uint32_t b_hi = plan.resident ? smem_u32(bres) + uint32_t(c) * 2 * KC * Nt * 4 : a_lo + 128 * KC * 4;
+          const uint32_t b_lo = b_hi + Nt * KC * 4;
+          issue_chunk_warp(tmem + ab * acc_cols, a_hi, a_lo, b_hi, b_lo, idesc, c != 0);
+          commit_warp(&empty[stage]);
+          if (c == nchunks - 1) commit_warp(&accfull[ab]);
         }
         __syncwarp();
         if (++stage == kStages) stage = 0, phase ^= 1;

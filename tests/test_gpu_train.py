@@ -101,3 +101,52 @@ def test_loss_curve_100_steps_matches_fp64_oracle():
     assert ref[-1] < ref[0]  # it trains
     assert relerr.max() < 1e-3
     assert O.rel_vec_error(m.shared_block(), ot.sh) < 1e-3
+
+
+@pytest.mark.parametrize("H,L", [(128, 3), (64, 2)])
+def test_fused_graph_steps_match_oracle(H, L, monkeypatch):
+    """Steps 2+ of a graph-mode trainer run the fused node chains (chain.cuh),
+    the side-stream weight gradients and the batched B images: every step's
+    loss and the parameters after 3 AdamW steps must match the FP64 trainer
+    (FP32 tolerance), and the unfused single-stream engine closely."""
+    o = O.Oracle()
+    hp = P.ModelHyper(20, L, H, H, 3, 5, 5.0)
+    oh = O.Hyper(20, L, H, H, 3, 5, 5.0)
+    batches = [batch((4, 3, 3, 2, 1), 300 + i) for i in range(3)]
+    caps = P.Caps(64, 2048, max(b.edge_bound() for b in batches))
+    cfg = P.TrainConfig(use_graph=True)
+    m = P.ModelT(hp, 7, range(5), caps=caps)
+    ot = OracleTrainer(o, oh, 7, range(5))
+    for b in batches:
+        # FP64 gradients at the device's current parameters (isolates the engine's
+        # error from the FP32-vs-FP64 trajectory drift of earlier AdamW steps)
+        ob = O.batch_from_samples(dict(n_atoms=b.n_atoms, species=b.species, pos=b.positions, forces=b.forces,
+                                       energy=b.energy, dsid=b.dataset_id), 5.0, o.build_edges)
+        psh = m.shared_block().astype(np.float64)
+        phd = {k: m.head_block(k).astype(np.float64) for k in range(5)}
+        E, F, cache = o.forward(oh, psh, phd, ob)
+        _, dE, dF = o.loss(ob, E, F)
+        gs, gh = o.backward(oh, psh, phd, ob, cache, dE, dF)
+        L_dev, L_ref = m.train_step(b, cfg), ot.step(b)
+        assert abs(L_dev - L_ref) / abs(L_ref) < 1e-5
+        g = m.debug("grads")  # this step's gradients (fused engine from step 2 on)
+        PS = gs.size
+        assert O.rel_vec_error(g[:PS], gs) < 1e-4
+        for k in range(5):
+            assert O.rel_vec_error(g[PS + k * gh[k].size:PS + (k + 1) * gh[k].size], gh[k]) < 1e-4, k
+    fused = m.shared_block()
+    assert O.rel_vec_error(fused, ot.sh) < 1e-3  # trajectory drift bound, as the 100-step test
+    fused_heads = [m.head_block(k) for k in range(5)]
+    m.close()
+    monkeypatch.setenv("HMTL_NO_CHAIN", "1")
+    monkeypatch.setenv("HMTL_SINGLE_STREAM", "1")
+    u = P.ModelT(hp, 7, range(5), caps=caps)
+    for b in batches:
+        u.train_step(b, cfg)
+    unfused = u.shared_block()
+    for k in range(5):
+        assert O.rel_vec_error(fused_heads[k], u.head_block(k)) < 1e-5
+    u.close()
+    print("fused vs oracle", O.rel_vec_error(fused, ot.sh), "unfused vs oracle", O.rel_vec_error(unfused, ot.sh),
+          "fused vs unfused", O.rel_vec_error(fused, unfused))
+    assert O.rel_vec_error(fused, unfused) < 1e-5

@@ -1,0 +1,23 @@
+"""Phase timestamps of the fused node-chain kernel (last launch of an eager step).
+HMTL_CHAIN_STAMPS=1 python tools/chain_stamps.py"""
+import ctypes as C, os, sys
+os.environ.setdefault("HMTL_CHAIN_STAMPS", "1")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
+import bench
+import paper_2506_21788_b200 as P
+from paper_2506_21788_b200._lib import check, lib
+heads, batches, _ = bench.rank_batches(0, 1)
+caps = P.Caps.for_samples(batches[0])
+m = P.ModelT(P.ModelHyper(**bench.HYPER), 7, heads, caps=caps)
+cfg = P.TrainConfig(use_graph=False)
+for i in range(3):
+    m.train_step(batches[0], cfg)
+buf = (C.c_longlong * (32 * 32))()
+check(lib().hmtl_debug_chain_stamps(m.ctx, buf, 32 * 32))
+names = {0: "setup", 1: "prod_done", 2: "mma0_start", 3: "mma0_issued", 4: "mma1_start", 5: "mma1_issued",
+         6: "mma2_start", 7: "mma2_issued", 8: "epi0_start", 9: "epi0_end", 10: "epi1_start", 11: "epi1_end",
+         12: "epi2_start", 13: "epi2_end", 24: "e0s0_aux", 25: "e0s0_tmem", 26: "e0s0_done", 31: "exit"}
+for cta in (0, 13, 27):
+    row = buf[cta * 32:(cta + 1) * 32]
+    print(f"CTA {cta}: " + "  ".join(f"{names.get(i, 'b%d' % (i - 14))}={row[i] / 1.9e3:.2f}us" for i in range(32) if row[i]))
