@@ -10,6 +10,14 @@
 
 using namespace hmtl_b200;
 
+bool hmtl_b200::pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HMTL_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 namespace {
 
 template <class T>
@@ -212,6 +220,7 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   if (const char* e = std::getenv("HMTL_NO_CHAIN")) c.fuse_chain = e[0] == '0';
   if (std::getenv("HMTL_CHAIN_STAMPS")) A(&c.chain_stamps, size_t(4096) * 32);
   if (const char* e = std::getenv("HMTL_CHAIN_DBG")) c.chain_dbg = std::atoi(e);
+  if (const char* e = std::getenv("HMTL_DBG_SKIP_WGRAD")) c.dbg_skip_wgrad = e[0] == '1';
   A(&c.params, c.PT);
   A(&c.grads, c.PT);
   A(&c.adam_m, c.PT);

@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // setup above overlaps the previous kernel's tail
   if (tid == 0) CHAIN_STAMP(0);
 
   if (warp < kProdWarps) {  // ---------------------------- GEMM 1's A operand

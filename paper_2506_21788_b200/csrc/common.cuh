@@ -1,6 +1,8 @@
 // common.cuh -- device-side building blocks shared by every kernel file.
 #pragma once
 #include <cuda_runtime.h>
+
+#include <utility>
 #include <stdint.h>
 
 namespace hmtl_b200 {
@@ -57,6 +59,29 @@ __device__ __forceinline__ float silu_grad(float x) {
   return s * (1.f + x * (1.f - s));
 }
 
+// ---- programmatic dependent launch (PDL).  Every kernel calls pdl_wait()
+// before it touches memory an earlier kernel of the step wrote (a no-op when it
+// was launched without the attribute); kl() launches with the attribute, so the
+// next kernel's CTAs are scheduled as the current kernel's CTAs retire and its
+// launch latency / prologue overlap the tail.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void kl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // Sum of n values src[q*stride], q = 0..n-1, with 8 independent accumulators
 // (8 loads in flight) combined in a fixed tree: the association depends only on
 // n, so results are bit-reproducible run to run.
@@ -79,6 +104,7 @@ __device__ __forceinline__ float sum_strided(const float* __restrict__ src, int 
 template <class F>
 __global__ void __launch_bounds__(256) split_reduce_kernel(const float* __restrict__ src, size_t seg_stride,
                                                            size_t stride, int T, F f) {
+  pdl_wait();
   __shared__ float red[8][32];
   const int seg = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * 32 + lane;
@@ -110,6 +136,7 @@ struct RowSet {
 // 64x64x16 tiles, 256 threads, 4x4 outputs per thread; persistent over tiles.
 template <class P>
 __global__ void __launch_bounds__(256) gemm_ab_kernel(P p) {
+  pdl_wait();
   constexpr int BM = 64, BN = 64, BK = 16;
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
@@ -185,6 +212,7 @@ __global__ void __launch_bounds__(256) gemm_ab_kernel(P p) {
 // tile; gemm_atb_reduce sums the P partials in ascending p and stores.
 template <class P>
 __global__ void __launch_bounds__(256) gemm_atb_kernel(P p, float* __restrict__ partial, int nsplit) {
+  pdl_wait();
   constexpr int BK = 64, BN = 64, RC = 16;
   __shared__ float As[RC][BK + 4];
   __shared__ float Bs[RC][BN + 4];
@@ -241,6 +269,7 @@ __global__ void __launch_bounds__(256) gemm_atb_kernel(P p, float* __restrict__ 
 
 template <class P>
 __global__ void gemm_atb_reduce(P p, const float* __restrict__ partial, int nsplit) {
+  pdl_wait();
   const size_t KN = size_t(p.K) * p.Ncols;
   const size_t total = KN * p.rows.nseg;
   for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total;

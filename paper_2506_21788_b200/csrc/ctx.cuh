@@ -97,7 +97,8 @@ struct Ctx {
   bool multi_stream = true;
   bool fuse_chain = true;  // node-row GEMM chains in one launch (chain.cuh)
   long long* chain_stamps = nullptr;
-  int chain_dbg = 0;  // engine tuning: phase timestamps of the last chain launch
+  int chain_dbg = 0;
+  bool dbg_skip_wgrad = false;  // timing experiments: skip weight gradients (wrong training)  // engine tuning: phase timestamps of the last chain launch
   float* bimg = nullptr;  // tcgen05 B-operand images (hi/lo, K-major)
   size_t bimg_cap = 0;
   bool use_tc = true;     // tcgen05 path for GEMMs whose shapes allow it

@@ -262,6 +262,7 @@ struct ForceProb {
 
 __global__ void embed_kernel(const DevHdr* hdr, const uint8_t* __restrict__ species, const float* __restrict__ embed,
                              float* __restrict__ h, int H) {
+  pdl_wait();
   const long long total = (long long)hdr->N * H;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     const int i = int(t / H), k = int(t % H);
@@ -272,6 +273,7 @@ __global__ void embed_kernel(const DevHdr* hdr, const uint8_t* __restrict__ spec
 // agg_i = sum_{e: dst(e)=i, ascending e} silu(z2_e)   (segment_sum, hmtl/kernels.hpp:97-108)
 __global__ void agg_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const float* __restrict__ z2,
                            float* __restrict__ agg, int H) {
+  pdl_wait();
   const int N = hdr->N;
   const int lane = threadIdx.x & 31;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += (gridDim.x * blockDim.x) >> 5) {
@@ -287,6 +289,7 @@ __global__ void agg_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, c
 // mean pool: (sum_i h_i) * (S(1)/S(n))   (hmtl/model.hpp:444-453)
 __global__ void pool_kernel(const DevHdr* hdr, const int* __restrict__ graph_offset, const float* __restrict__ h,
                             float* __restrict__ pooled, int H) {
+  pdl_wait();
   const int G = hdr->G;
   const int lane = threadIdx.x & 31;
   for (int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < G; g += (gridDim.x * blockDim.x) >> 5) {
@@ -303,6 +306,7 @@ __global__ void pool_kernel(const DevHdr* hdr, const int* __restrict__ graph_off
 // F_i = sum_{e in row i} dvec_e * s_e   (hmtl/model.hpp:475-480)
 __global__ void forces_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const float4* __restrict__ geo,
                               const float* __restrict__ s, float* __restrict__ F) {
+  pdl_wait();
   const int N = hdr->N;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
     float fx = 0.f, fy = 0.f, fz = 0.f;
@@ -320,6 +324,7 @@ __global__ void forces_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr
 }
 
 __global__ void finite_kernel(DevHdr* hdr, const float* __restrict__ energy, const float* __restrict__ F) {
+  pdl_wait();
   const int G = hdr->G, N = hdr->N;
   bool bad = false;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < G + 3 * N; t += gridDim.x * blockDim.x) {
@@ -411,6 +416,7 @@ struct HasY4<P, std::void_t<decltype(std::declval<const P&>().y4(0, 0, 0))>> : s
 // B image of problem P: B(n, k) = p.b(seg, k, n), layout of tc::bimg_kernel
 template <class P>
 __global__ void bimg_prob_kernel(P p, float* __restrict__ out, int nseg) {
+  pdl_wait();
   const int K = p.K, N = p.Ncols;
   const size_t total = size_t(nseg) * K * N;
   for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < total; t += size_t(gridDim.x) * blockDim.x) {
@@ -444,6 +450,7 @@ struct TcRed {
 
 // one launch builds every B image of the step: blockIdx.y = job
 __global__ void bimg_all_kernel(const BDesc* __restrict__ jobs) {
+  pdl_wait();
   const BDesc J = jobs[blockIdx.y];
   const int K = J.K, N = J.N;
   const size_t total = size_t(J.nseg) * K * N;
@@ -482,7 +489,7 @@ void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& 
     if (c.bimg_ready && idx < int(c.bjobs.size())) {
       img = c.bjobs[idx].out;  // prebuilt by the batched builder after the last weight update
     } else {
-      bimg_prob_kernel<P><<<gridn((long long)nseg * p.K * p.Ncols, 256, sm * 4), 256, 0, st>>>(p, c.bimg, nseg);
+      kl(bimg_prob_kernel<P>, gridn((long long)nseg * p.K * p.Ncols, 256, sm * 4), 256, 0, st, p, c.bimg, nseg);
       if (c.bimg_recording) {
         BDesc d = p.bd();
         d.nseg = nseg;
@@ -497,15 +504,16 @@ void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& 
     while (Nt > 32 && mtiles * (p.Ncols / Nt) * 2 <= sm && (Nt / 2) % 32 == 0) Nt /= 2;
     const tc::RowPlan plan = tc::row_plan(p.K, Nt);
     set_smem(tc::tc_row_kernel<TcRow<P>>, plan.smem);
-    tc::tc_row_kernel<TcRow<P>><<<gridn(mtiles * (p.Ncols / Nt), 1, sm), tc::kRowThreads, plan.smem, st>>>(q, plan);
+    kl(tc::tc_row_kernel<TcRow<P>>, gridn(mtiles * (p.Ncols / Nt), 1, sm), tc::kRowThreads, plan.smem, st, q, plan);
     return;
   }
   const long long tiles = ((rows_cap + 63) / 64 + nseg) * ((p.Ncols + 63) / 64);
-  gemm_ab_kernel<P><<<gridn(tiles, 1, sm * 8), 256, 0, st>>>(p);
+  kl(gemm_ab_kernel<P>, gridn(tiles, 1, sm * 8), 256, 0, st, p);
 }
 
 template <class P>
 void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0) {
+  if (c.dbg_skip_wgrad) return;  // timing experiments only (HMTL_DBG_SKIP_WGRAD)
   Prof pr(c, P::kName, st);
   const int M = p.K - P::kBias;
   if (c.use_tc && P::kTc && p.Ncols % 32 == 0 && p.Ncols <= 256 && M % 4 == 0) {
@@ -521,7 +529,7 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
       const size_t smem = tc::tc_red_smem(p.Ncols);
       set_smem(tc::tc_red_kernel<TcRed<P>>, smem);
       dim3 grid(mtiles, ns, p.rows.nseg);
-      tc::tc_red_kernel<TcRed<P>><<<grid, tc::kRedThreads, smem, st>>>(q, partial, ns,
+      kl(tc::tc_red_kernel<TcRed<P>>, grid, tc::kRedThreads, smem, st, q, partial, ns,
                                                                         tc::red_stages(p.Ncols));
       tc::tc_red_reduce(q, partial, ns, st);
       return;
@@ -529,9 +537,9 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
   }
   const int tiles = ((p.K + 63) / 64) * ((p.Ncols + 63) / 64);
   dim3 grid(tiles, nsplit, p.rows.nseg);
-  gemm_atb_kernel<P><<<grid, 256, 0, st>>>(p, c.part(st), nsplit);
+  kl(gemm_atb_kernel<P>, grid, 256, 0, st, p, c.part(st), nsplit);
   const long long total = (long long)p.K * p.Ncols * p.rows.nseg;
-  gemm_atb_reduce<P><<<gridn(total, 256, c.sm_count * 8), 256, 0, st>>>(p, c.part(st), nsplit);
+  kl(gemm_atb_reduce<P>, gridn(total, 256, c.sm_count * 8), 256, 0, st, p, c.part(st), nsplit);
 }
 
 // fused node-row GEMM chain (chain.cuh) over the prebuilt B images of the next
@@ -554,7 +562,7 @@ void launch_chain(Ctx& c, const char* name, int G, const chain::Gemm* gs, cudaSt
   const int grid = int((c.Nc + 127) / 128);
   auto go = [&](auto kern) {
     set_smem(kern, chain::kSmem);
-    kern<<<grid, chain::kThreads, chain::kSmem, st>>>(q);
+    kl(kern, grid, chain::kThreads, chain::kSmem, st, q);
   };
   using namespace chain;
   const int r0 = gs[0].role, r1 = G > 1 ? gs[1].role : -1, r2 = G > 2 ? gs[2].role : -1;
@@ -611,6 +619,7 @@ __global__ void __launch_bounds__(256) edge_a1_kernel(const DevHdr* hdr, const f
                                                       const int* __restrict__ dst, const int* __restrict__ src,
                                                       const float4* __restrict__ geo, const float* __restrict__ wd,
                                                       const float* __restrict__ b1, float* __restrict__ a1, int H) {
+  pdl_wait();
   const int E = hdr->E, lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (int eb = gw * kEwU; eb < E; eb += nw * kEwU) {
@@ -639,6 +648,7 @@ __global__ void __launch_bounds__(256) edge_bwd_prep_kernel(const DevHdr* hdr, c
                                                             const float* __restrict__ dagg,
                                                             const float* __restrict__ z2, float* __restrict__ dz2,
                                                             float* __restrict__ s1p, int H) {
+  pdl_wait();
   const int E = hdr->E, lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (int eb = gw * kEwU; eb < E; eb += nw * kEwU) {
@@ -671,6 +681,7 @@ __global__ void edge_af0_kernel(const DevHdr* hdr, const float* __restrict__ Qf,
                                 const int* __restrict__ node_graph, const int* __restrict__ gslot,
                                 const float* __restrict__ heads, size_t PH, size_t off_wd, size_t off_b0,
                                 float* __restrict__ af0, float* __restrict__ sf0, int W) {
+  pdl_wait();
   const int q = W / 4;
   const long long total = (long long)hdr->E * q;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
@@ -694,6 +705,7 @@ __global__ void force_out_fwd_kernel(const DevHdr* hdr, const float* __restrict_
                                      const int* __restrict__ dst, const int* __restrict__ node_graph,
                                      const int* __restrict__ gslot, const float* __restrict__ heads, size_t PH,
                                      size_t off_w, size_t off_b, float* __restrict__ s, int W) {
+  pdl_wait();
   const int l8 = threadIdx.x & 7;
   const unsigned gm = 0xffu << (threadIdx.x & 24);
   const long long E = hdr->E;
@@ -740,7 +752,7 @@ void launch_bimg_all(Ctx& c, cudaStream_t st) {
     c.n_djobs = int(c.bjobs.size());
   }
   Prof pr(c, "bimg_all", st);
-  bimg_all_kernel<<<dim3(16, c.n_djobs), 256, 0, st>>>(c.d_bjobs);
+  kl(bimg_all_kernel, dim3(16, c.n_djobs), 256, 0, st, c.d_bjobs);
   c.bimg_ready = true;
   c.bimg_recording = false;
 }
@@ -751,7 +763,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
   const size_t NH = size_t(c.Nc) * H, EH = size_t(c.Ec) * H;
   {
     Prof pr(c, "fwd.embed", st);
-    embed_kernel<<<gridn(NH, 256, sm * 16), 256, 0, st>>>(c.hdr, c.species, c.shared_param("embed"), c.hs, H);
+    kl(embed_kernel, gridn(NH, 256, sm * 16), 256, 0, st, c.hdr, c.species, c.shared_param("embed"), c.hs, H);
   }
   bool p_done = false;  // P of this layer already produced by the previous node chain
   for (int l = 0; l < L; ++l) {
@@ -770,7 +782,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     p_done = false;
     if (c.store_a1) {
       Prof pr(c, "fwd.edge_act", st);
-      edge_a1_kernel<<<gridn((c.Ec + kEwU - 1) / kEwU * 32, 256, sm * 16), 256, 0, st>>>(
+      kl(edge_a1_kernel, gridn((c.Ec + kEwU - 1) / kEwU * 32, 256, sm * 16), 256, 0, st,
           c.hdr, P, c.edge_dst, c.edge_src, c.geo, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
           c.a1 + size_t(l) * EH, H);
     }
@@ -782,8 +794,8 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     }
     {
       Prof pr(c, "fwd.agg_segsum", st);
-      if (H % 4 == 0) agg4_kernel<<<gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st>>>(c.hdr, c.row_ptr, z2, agg, H);
-      else agg_kernel<<<gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st>>>(c.hdr, c.row_ptr, z2, agg, H);
+      if (H % 4 == 0) kl(agg4_kernel, gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st, c.hdr, c.row_ptr, z2, agg, H);
+      else kl(agg_kernel, gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st, c.hdr, c.row_ptr, z2, agg, H);
     }
     if (chain_ok(c)) {  // node MLP + residual (+ the next layer's P) in one launch
       const int G = l + 1 < L ? 3 : 2;
@@ -812,7 +824,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
   c.dep(st, se);
   {
     Prof pr(c, "fwd.pool", se);
-    pool_kernel<<<gridn((long long)c.Gc * 32, 256, sm * 8), 256, 0, se>>>(c.hdr, c.graph_offset, hL, c.pooled, H);
+    kl(pool_kernel, gridn((long long)c.Gc * 32, 256, sm * 8), 256, 0, se, c.hdr, c.graph_offset, hL, c.pooled, H);
   }
   for (int i = 0; i < D; ++i) {
     const int last = i == D - 1;
@@ -831,7 +843,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
   const size_t wf0 = c.head_off("force.W0");
   if (c.store_af0) {
     Prof pr(c, "fwd.edge_act", st);
-    edge_af0_kernel<<<gridn((long long)c.Ec * W / 4, 256, sm * 16), 256, 0, st>>>(
+    kl(edge_af0_kernel, gridn((long long)c.Ec * W / 4, 256, sm * 16), 256, 0, st,
         c.hdr, c.Qf, c.edge_dst, c.edge_src, c.dist, c.node_graph, c.gslot, c.head_params(), c.PH,
         wf0 + size_t(H) * W, c.head_off("force.b0"), c.af0, c.sf0, W);
   }
@@ -839,7 +851,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     const int last = i == D - 1;
     if (last && force_out_fast(c, i)) {
       Prof pr(c, "fwd.force_out", st);
-      force_out_fwd_kernel<<<gridn((long long)c.Ec * 8, 256, sm * 16), 256, 0, st>>>(
+      kl(force_out_fwd_kernel, gridn((long long)c.Ec * 8, 256, sm * 16), 256, 0, st,
           c.hdr, i >= 2 ? c.zf + size_t(i - 2) * c.Ec * W : c.af0, i >= 2, c.edge_dst, c.node_graph, c.gslot,
           c.head_params(), c.PH, c.head_off("force.W" + std::to_string(i)),
           c.head_off("force.b" + std::to_string(i)), c.s, W);
@@ -855,12 +867,12 @@ void launch_forward(Ctx& c, cudaStream_t st) {
   }
   {
     Prof pr(c, "fwd.forces_segsum", st);
-    forces_kernel<<<gridn(c.Nc, 256, sm * 8), 256, 0, st>>>(c.hdr, c.row_ptr, c.geo, c.s, c.forces);
+    kl(forces_kernel, gridn(c.Nc, 256, sm * 8), 256, 0, st, c.hdr, c.row_ptr, c.geo, c.s, c.forces);
   }
   c.dep(se, st);
   {
     Prof pr(c, "fwd.finite", st);
-    finite_kernel<<<gridn(c.Gc + 3LL * c.Nc, 256, sm * 4), 256, 0, st>>>(c.hdr, c.energy, c.forces);
+    kl(finite_kernel, gridn(c.Gc + 3LL * c.Nc, 256, sm * 4), 256, 0, st, c.hdr, c.energy, c.forces);
   }
 }
 
@@ -872,6 +884,7 @@ __global__ void __launch_bounds__(1024) loss_kernel(DevHdr* hdr, const uint8_t* 
                                                     const float* __restrict__ energy, const float* __restrict__ F,
                                                     float* __restrict__ dE, float* __restrict__ dF, float w_e,
                                                     float w_f) {
+  pdl_wait();
   __shared__ double wsum[32];
   const int G = hdr->G, N = hdr->N;
   const ArenaLayout al = arena_layout(G, N);
@@ -909,7 +922,7 @@ __global__ void __launch_bounds__(1024) loss_kernel(DevHdr* hdr, const uint8_t* 
 void launch_loss(Ctx& c, float w_e, float w_f, cudaStream_t st) {
   {
     Prof pr(c, "loss", st);
-    loss_kernel<<<1, 1024, 0, st>>>(c.hdr, c.arena, c.graph_offset, c.energy, c.forces, c.dE, c.dF, w_e, w_f);
+    kl(loss_kernel, 1, 1024, 0, st, c.hdr, c.arena, c.graph_offset, c.energy, c.forces, c.dE, c.dF, w_e, w_f);
   }
 }
 
@@ -1294,6 +1307,7 @@ struct L11Prob {  // dh2 += S_dst W1a^T + S_src W1b^T
 __global__ void dh_pool_kernel(const DevHdr* hdr, const int* __restrict__ node_graph,
                                const int* __restrict__ graph_offset, const float* __restrict__ dpooled,
                                float* __restrict__ dh, int H) {
+  pdl_wait();
   const long long total = (long long)hdr->N * H;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     const int i = int(t / H), k = int(t % H);
@@ -1306,6 +1320,7 @@ __global__ void dh_pool_kernel(const DevHdr* hdr, const int* __restrict__ node_g
 // ds_e = sum_c dF[dst,c] * dvec[e,c]  (hmtl/model.hpp:528-536)
 __global__ void ds_kernel(const DevHdr* hdr, const int* __restrict__ dst, const float4* __restrict__ geo,
                           const float* __restrict__ dF, float* __restrict__ ds) {
+  pdl_wait();
   const int E = hdr->E;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
     const int i = dst[e];
@@ -1321,6 +1336,7 @@ __global__ void ds_kernel(const DevHdr* hdr, const int* __restrict__ dst, const 
 // dz2 = dagg[dst] * silu'(z2)  (hmtl/model.hpp:590-597)
 __global__ void dz2_kernel(const DevHdr* hdr, const int* __restrict__ dst, const float* __restrict__ dagg,
                            const float* __restrict__ z2, float* __restrict__ dz2, int H) {
+  pdl_wait();
   const long long total = (long long)hdr->E * H;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     const int e = int(t / H), k = int(t % H);
@@ -1333,6 +1349,7 @@ __global__ void dz2_kernel(const DevHdr* hdr, const int* __restrict__ dst, const
 // reverses of row i.  If `fold`, the two halves are added (force head: T).
 __global__ void seg2_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const int* __restrict__ rev,
                             const float* __restrict__ x, float* __restrict__ S, int C, int fold) {
+  pdl_wait();
   const int N = hdr->N;
   const int lane = threadIdx.x & 31;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += (gridDim.x * blockDim.x) >> 5) {
@@ -1362,6 +1379,7 @@ __device__ __forceinline__ float4 f4z() { return make_float4(0.f, 0.f, 0.f, 0.f)
 constexpr int kAggU = 8;
 __global__ void __launch_bounds__(256) agg4_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr,
                                                    const float* __restrict__ z2, float* __restrict__ agg, int H) {
+  pdl_wait();
   const int N = hdr->N, lane = threadIdx.x & 31;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += (gridDim.x * blockDim.x) >> 5) {
     const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
@@ -1387,6 +1405,7 @@ constexpr int kSegU = 4;
 __global__ void __launch_bounds__(256) seg2v_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr,
                                                     const int* __restrict__ rev, const float* __restrict__ x,
                                                     float* __restrict__ S, int C, int fold) {
+  pdl_wait();
   const int N = hdr->N, lane = threadIdx.x & 31;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += (gridDim.x * blockDim.x) >> 5) {
     const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
@@ -1430,6 +1449,7 @@ constexpr int kCs2Rows = 128;
 __global__ void __launch_bounds__(256) colsum2_kernel(RowSet rows, const float* __restrict__ wvec, int wstride,
                                                       const float* __restrict__ x, int C,
                                                       float* __restrict__ partial, int nchunk_cap) {
+  pdl_wait();
   __shared__ float4 red[8][2][64];
   const int seg = blockIdx.y, chunk = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rb = rows.begin(seg), re = rows.end(seg);
@@ -1484,6 +1504,7 @@ __global__ void __launch_bounds__(256) force_out_bwd_kernel(RowSet rows, const f
                                                             const float* __restrict__ heads, size_t PH, size_t off_w,
                                                             float* __restrict__ dzp, float* __restrict__ partial,
                                                             int nchunk_cap, int W) {
+  pdl_wait();
   __shared__ float red[8][257];
   const int seg = blockIdx.y, chunk = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rb = rows.begin(seg), re = rows.end(seg);
@@ -1566,6 +1587,7 @@ struct ChunkStore {
 constexpr int kEmbChunk = 128;
 __global__ void embed_grad_part(const DevHdr* hdr, const uint8_t* __restrict__ species, const float* __restrict__ dh,
                                 float* __restrict__ partial, int H, int NS) {
+  pdl_wait();
   extern __shared__ float acc[];  // [NS][H]
   const int N = hdr->N, chunk = blockIdx.x;
   const int i0 = chunk * kEmbChunk;
@@ -1598,6 +1620,7 @@ struct EmbedStore {
 // g_embed[s] = sum_{i: species_i = s} dh_i (ascending i; hmtl/model.hpp:619-622)
 __global__ void embed_grad_kernel(const DevHdr* hdr, const uint8_t* __restrict__ species, const float* __restrict__ dh,
                                   float* __restrict__ G, int H, int NS) {
+  pdl_wait();
   const int N = hdr->N;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < NS * H; t += gridDim.x * blockDim.x) {
     const int s = t / H, k = t % H;
@@ -1614,17 +1637,18 @@ namespace {
 void segsum2(Ctx& c, const float* x, int C, int fold, float* out, cudaStream_t st) {
   Prof pr(c, "bwd.segsum_dst_src", st);
   const int blocks = gridn((long long)c.Nc * 32, 256, c.sm_count * 16);
-  if (C % 4 == 0) seg2v_kernel<<<blocks, 256, 0, st>>>(c.hdr, c.row_ptr, c.rev, x, out, C, fold);
-  else seg2_kernel<<<blocks, 256, 0, st>>>(c.hdr, c.row_ptr, c.rev, x, out, C, fold);
+  if (C % 4 == 0) kl(seg2v_kernel, blocks, 256, 0, st, c.hdr, c.row_ptr, c.rev, x, out, C, fold);
+  else kl(seg2_kernel, blocks, 256, 0, st, c.hdr, c.row_ptr, c.rev, x, out, C, fold);
 }
 // [sum w*x ; sum x] per head segment into G + seg*seg_stride (rows are contiguous)
 void colsum2(Ctx& c, RowSet rows, const float* w, int wstride, const float* x, int C, float* G, size_t seg_stride,
              cudaStream_t st) {
+  if (c.dbg_skip_wgrad) return;
   Prof pr(c, "bwd.colsum_tail", st);
   const int chunk_cap = int((c.Ec + kCs2Rows - 1) / kCs2Rows);
   dim3 grid(chunk_cap, rows.nseg);
-  colsum2_kernel<<<grid, 256, 0, st>>>(rows, w, wstride, x, C, c.part(st), chunk_cap);
-  split_reduce_kernel<<<dim3((2 * C + 31) / 32, rows.nseg), 256, 0, st>>>(
+  kl(colsum2_kernel, grid, 256, 0, st, rows, w, wstride, x, C, c.part(st), chunk_cap);
+  kl(split_reduce_kernel<ChunkStore>, dim3((2 * C + 31) / 32, rows.nseg), 256, 0, st,
       c.part(st), size_t(chunk_cap) * 2 * C, size_t(2) * C, 2 * C, ChunkStore{rows, kCs2Rows, G, seg_stride});
 }
 }  // namespace
@@ -1663,14 +1687,14 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     }
     {
       Prof pr(c, "bwd.pool", se);
-      dh_pool_kernel<<<gridn(NH, 256, sm * 16), 256, 0, se>>>(c.hdr, c.node_graph, c.graph_offset, c.dpooled, dhL, H);
+      kl(dh_pool_kernel, gridn(NH, 256, sm * 16), 256, 0, se, c.hdr, c.node_graph, c.graph_offset, c.dpooled, dhL, H);
     }
   }
   // ---------------- force heads (hmtl/model.hpp:526-549)
   {
     {
       Prof pr(c, "bwd.force_ds", st);
-      ds_kernel<<<gridn(c.Ec, 256, sm * 8), 256, 0, st>>>(c.hdr, c.edge_dst, c.geo, c.dF, c.ds);
+      kl(ds_kernel, gridn(c.Ec, 256, sm * 8), 256, 0, st, c.hdr, c.edge_dst, c.geo, c.dF, c.ds);
     }
     const size_t wf0 = c.head_off("force.W0");
     const HeadW Wd{c.head_params(), c.PH, wf0 + size_t(H) * W};
@@ -1685,10 +1709,10 @@ void launch_backward(Ctx& c, cudaStream_t st) {
         Prof pr(c, "bwd.force_out", st);
         const int cap = int((c.Ec + kFoRows - 1) / kFoRows);
         const RowSet rows = edge_rows_by_head(c);
-        force_out_bwd_kernel<<<dim3(cap, rows.nseg), 256, 0, st>>>(
+        kl(force_out_bwd_kernel, dim3(cap, rows.nseg), 256, 0, st,
             rows, i >= 2 ? c.zf + size_t(i - 2) * c.Ec * W : c.af0, c.sf0, i >= 2, c.ds, c.head_params(), c.PH,
             c.head_off("force.W" + std::to_string(i)), nxt, c.partial, cap, W);
-        split_reduce_kernel<<<dim3((W + 1 + 31) / 32, rows.nseg), 256, 0, st>>>(
+        kl(split_reduce_kernel<ChunkStore>, dim3((W + 1 + 31) / 32, rows.nseg), 256, 0, st,
             c.partial, size_t(cap) * (W + 1), size_t(W + 1), W + 1,
             ChunkStore{rows, kFoRows, c.head_grads() + c.head_off("force.W" + std::to_string(i)), c.PH});
         dz = nxt;
@@ -1769,11 +1793,11 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     const bool mat = c.store_a1;  // tensor-core shapes: gathered operands materialised elementwise
     if (mat) {
       Prof pr(c, "bwd.edge_act", st);
-      edge_bwd_prep_kernel<<<gridn((c.Ec + kEwU - 1) / kEwU * 32, 256, sm * 16), 256, 0, st>>>(
+      kl(edge_bwd_prep_kernel, gridn((c.Ec + kEwU - 1) / kEwU * 32, 256, sm * 16), 256, 0, st,
           c.hdr, P, c.edge_dst, c.edge_src, c.geo, wd, b1, c.dagg, z2, dzA, c.scratch, H);
     } else {
       Prof pr(c, "bwd.edge_dz2_gather", st);
-      dz2_kernel<<<gridn(EH, 256, sm * 16), 256, 0, st>>>(c.hdr, c.edge_dst, c.dagg, z2, dzA, H);
+      kl(dz2_kernel, gridn(EH, 256, sm * 16), 256, 0, st, c.hdr, c.edge_dst, c.dagg, z2, dzA, H);
     }
     c.dep(st, sw);  // dz2 ready
     {
@@ -1815,11 +1839,11 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     Prof pr(c, "bwd.embed_grad", st);
     const size_t shm = size_t(c.NS) * H * 4;
     if (shm <= 48 * 1024 && size_t(c.Nc + kEmbChunk - 1) / kEmbChunk * c.NS * H <= c.partial_cap) {
-      embed_grad_part<<<(c.Nc + kEmbChunk - 1) / kEmbChunk, 128, shm, st>>>(c.hdr, c.species, dh0, c.partial, H, c.NS);
-      split_reduce_kernel<<<dim3((c.NS * H + 31) / 32, 1), 256, 0, st>>>(
+      kl(embed_grad_part, (c.Nc + kEmbChunk - 1) / kEmbChunk, 128, shm, st, c.hdr, c.species, dh0, c.partial, H, c.NS);
+      kl(split_reduce_kernel<EmbedStore>, dim3((c.NS * H + 31) / 32, 1), 256, 0, st,
           c.partial, 0, size_t(c.NS) * H, c.NS * H, EmbedStore{c.hdr, c.grads + c.shared_off("embed")});
     } else {
-      embed_grad_kernel<<<gridn((long long)c.NS * H, 128, sm * 8), 128, 0, st>>>(
+      kl(embed_grad_kernel, gridn((long long)c.NS * H, 128, sm * 8), 128, 0, st,
           c.hdr, c.species, dh0, c.grads + c.shared_off("embed"), H, c.NS);
     }
   }
@@ -1832,6 +1856,7 @@ namespace {
 __global__ void z1_kernel(const DevHdr* hdr, const float* __restrict__ P, const int* __restrict__ dst,
                           const int* __restrict__ src, const float4* __restrict__ geo, const float* __restrict__ wd,
                           const float* __restrict__ b1, float* __restrict__ out, int H) {
+  pdl_wait();
   const long long total = (long long)hdr->E * H;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     const int e = int(t / H), k = int(t % H);
@@ -1843,18 +1868,20 @@ __global__ void z1_kernel(const DevHdr* hdr, const float* __restrict__ P, const 
 void launch_debug_z1(Ctx& c, int l, float* out, cudaStream_t st) {
   const std::string p = "layer" + std::to_string(l) + ".";
   const float* W1 = c.params + c.shared_off(p + "edge.W1");
-  z1_kernel<<<gridn((long long)c.Ec * c.H, 256, c.sm_count * 16), 256, 0, st>>>(
+  kl(z1_kernel, gridn((long long)c.Ec * c.H, 256, c.sm_count * 16), 256, 0, st,
       c.hdr, c.P + size_t(l) * 2 * c.Nc * c.H, c.edge_dst, c.edge_src, c.geo, W1 + size_t(2) * c.H * c.H,
       c.params + c.shared_off(p + "edge.b1"), out, c.H);
 }
 
 // ---------------------------------------------------------------- AdamW
 namespace {
-__global__ void adam_tick(DevHdr* hdr) { hdr->step += 1; }
+__global__ void adam_tick(DevHdr* hdr) {
+  pdl_wait(); hdr->step += 1; }
 // torch.optim.AdamW ordering (decision recorded in DESIGN.md)
 __global__ void adamw_kernel(const DevHdr* hdr, float* __restrict__ p, const float* __restrict__ g,
                              float* __restrict__ m, float* __restrict__ v, size_t n, float lr, float b1, float b2,
                              float eps, float wd) {
+  pdl_wait();
   const int t = hdr->step;
   const float bc1 = float(1.0 - pow(double(b1), double(t)));
   const float bc2s = float(sqrt(1.0 - pow(double(b2), double(t))));
@@ -1879,10 +1906,10 @@ void launch_adamw(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st) {
     cudaStream_t st;
     ~Rebuild() { launch_bimg_all(c, st); }  // weights changed: refresh the B images (after the update)
   } rebuild{c, st};
-  adam_tick<<<1, 1, 0, st>>>(c.hdr);
+  kl(adam_tick, 1, 1, 0, st, c.hdr);
   {
     Prof pr(c, "adamw", st);
-    adamw_kernel<<<gridn(c.PT, 256, c.sm_count * 8), 256, 0, st>>>(c.hdr, c.params, c.grads, c.adam_m, c.adam_v, c.PT,
+    kl(adamw_kernel, gridn(c.PT, 256, c.sm_count * 8), 256, 0, st, c.hdr, c.params, c.grads, c.adam_m, c.adam_v, c.PT,
                                                                    cfg.lr, cfg.beta1, cfg.beta2, cfg.eps,
                                                                    cfg.weight_decay);
   }

@@ -21,6 +21,7 @@ constexpr unsigned kFull = 0xffffffffu;
 __global__ void prep_kernel(const uint8_t* __restrict__ arena, DevHdr* hdr, const int* __restrict__ slot_of,
                             int* graph_offset, int* node_graph, uint8_t* species, float4* pos32, int* gslot,
                             int Gc, int Nc) {
+  pdl_wait();
   const int G = reinterpret_cast<const int*>(arena)[0];
   const int N = reinterpret_cast<const int*>(arena)[1];
   const ArenaLayout al = arena_layout(G, N);
@@ -67,6 +68,7 @@ __device__ __forceinline__ bool within(const double* __restrict__ pos, int i, in
 __global__ void nbr_count_kernel(const uint8_t* __restrict__ arena, const DevHdr* hdr,
                                  const int* __restrict__ graph_offset, const int* __restrict__ node_graph,
                                  int* __restrict__ deg, double rc2) {
+  pdl_wait();
   const int N = hdr->N, G = hdr->G;
   const double* pos = reinterpret_cast<const double*>(arena + arena_layout(G, N).pos);
   const int lane = threadIdx.x & 31;
@@ -87,6 +89,7 @@ __global__ void nbr_count_kernel(const uint8_t* __restrict__ arena, const DevHdr
 __global__ void __launch_bounds__(1024) scan_kernel(DevHdr* hdr, const int* __restrict__ deg, int* row_ptr,
                                                     const int* __restrict__ graph_offset, int* edge_offset,
                                                     long long Ec) {
+  pdl_wait();
   __shared__ int warp_sums[32];
   __shared__ int carry;
   const int N = hdr->N, G = hdr->G;
@@ -136,6 +139,7 @@ __global__ void nbr_write_kernel(const uint8_t* __restrict__ arena, const DevHdr
                                  const int* __restrict__ row_ptr, const float4* __restrict__ pos32,
                                  int* __restrict__ edge_src, int* __restrict__ edge_dst, float4* __restrict__ geo,
                                  float* __restrict__ dist, double rc2, long long Ec) {
+  pdl_wait();
   const int N = hdr->N, G = hdr->G;
   if (hdr->E > Ec) return;
   const double* pos = reinterpret_cast<const double*>(arena + arena_layout(G, N).pos);
@@ -168,6 +172,7 @@ __global__ void nbr_write_kernel(const uint8_t* __restrict__ arena, const DevHdr
 // symmetric bit-for-bit ((a-b)^2 == (b-a)^2), so (j,i) always exists.
 __global__ void rev_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const int* __restrict__ edge_src,
                            const int* __restrict__ edge_dst, int* __restrict__ rev, long long Ec) {
+  pdl_wait();
   const int E = hdr->E;
   if (E > Ec) return;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
@@ -190,6 +195,7 @@ __global__ void __launch_bounds__(1024) route_kernel(DevHdr* hdr, const int* __r
                                                      const int* __restrict__ graph_offset,
                                                      const int* __restrict__ edge_offset, int* gperm,
                                                      int* gnode_base, int* gedge_base, int S) {
+  pdl_wait();
   __shared__ int wsum[3][32];
   __shared__ int carry[3];
   const int G = hdr->G;
@@ -255,6 +261,7 @@ __global__ void perm_kernel(const DevHdr* hdr, const int* __restrict__ node_grap
                             const int* __restrict__ edge_offset, const int* __restrict__ edge_dst,
                             const int* __restrict__ gnode_base, const int* __restrict__ gedge_base, int* node_perm,
                             int* edge_perm) {
+  pdl_wait();
   const int N = hdr->N, E = hdr->E;
   const int M = N > E ? N : E;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < M; t += gridDim.x * blockDim.x) {
@@ -282,7 +289,7 @@ void launch_prep(Ctx& c, cudaStream_t st) {
   const int n = (c.Nc > c.Gc + 1 ? c.Nc : c.Gc + 1);
   {
     Prof pr(c, "prep", st);
-    prep_kernel<<<grid_for(n, 256, 1 << 20), 256, 0, st>>>(c.arena, c.hdr, c.d_slot_of, c.graph_offset, c.node_graph,
+    kl(prep_kernel, grid_for(n, 256, 1 << 20), 256, 0, st, c.arena, c.hdr, c.d_slot_of, c.graph_offset, c.node_graph,
                                                             c.species, c.pos32, c.gslot, c.Gc, c.Nc);
   }
 }
@@ -291,31 +298,31 @@ void launch_nbr(Ctx& c, cudaStream_t st) {
   const int warps_blocks = grid_for((long long)c.Nc * 32, 256, c.sm_count * 16);
   {
     Prof pr(c, "nbr.count", st);
-    nbr_count_kernel<<<warps_blocks, 256, 0, st>>>(c.arena, c.hdr, c.graph_offset, c.node_graph, c.deg, c.rc2);
+    kl(nbr_count_kernel, warps_blocks, 256, 0, st, c.arena, c.hdr, c.graph_offset, c.node_graph, c.deg, c.rc2);
   }
   {
     Prof pr(c, "nbr.scan", st);
-    scan_kernel<<<1, 1024, 0, st>>>(c.hdr, c.deg, c.row_ptr, c.graph_offset, c.edge_offset, c.Ec);
+    kl(scan_kernel, 1, 1024, 0, st, c.hdr, c.deg, c.row_ptr, c.graph_offset, c.edge_offset, c.Ec);
   }
   {
     Prof pr(c, "nbr.write", st);
-    nbr_write_kernel<<<warps_blocks, 256, 0, st>>>(c.arena, c.hdr, c.graph_offset, c.node_graph, c.row_ptr, c.pos32,
+    kl(nbr_write_kernel, warps_blocks, 256, 0, st, c.arena, c.hdr, c.graph_offset, c.node_graph, c.row_ptr, c.pos32,
                                                    c.edge_src, c.edge_dst, c.geo, c.dist, c.rc2, c.Ec);
   }
   {
     Prof pr(c, "nbr.rev", st);
-    rev_kernel<<<grid_for(c.Ec, 256, c.sm_count * 8), 256, 0, st>>>(c.hdr, c.row_ptr, c.edge_src, c.edge_dst, c.rev,
+    kl(rev_kernel, grid_for(c.Ec, 256, c.sm_count * 8), 256, 0, st, c.hdr, c.row_ptr, c.edge_src, c.edge_dst, c.rev,
                                                                      c.Ec);
   }
   {
     Prof pr(c, "route", st);
-    route_kernel<<<1, 1024, 0, st>>>(c.hdr, c.gslot, c.graph_offset, c.edge_offset, c.gperm, c.gnode_base,
+    kl(route_kernel, 1, 1024, 0, st, c.hdr, c.gslot, c.graph_offset, c.edge_offset, c.gperm, c.gnode_base,
                                      c.gedge_base, c.S);
   }
   const long long m = c.Nc > c.Ec ? c.Nc : c.Ec;
   {
     Prof pr(c, "route.perm", st);
-    perm_kernel<<<grid_for(m, 256, c.sm_count * 8), 256, 0, st>>>(c.hdr, c.node_graph, c.graph_offset, c.edge_offset,
+    kl(perm_kernel, grid_for(m, 256, c.sm_count * 8), 256, 0, st, c.hdr, c.node_graph, c.graph_offset, c.edge_offset,
                                                                    c.edge_dst, c.gnode_base, c.gedge_base, c.node_perm,
                                                                    c.edge_perm);
   }

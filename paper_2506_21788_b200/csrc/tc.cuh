@@ -293,6 +293,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // setup above overlaps the previous kernel's tail
 
   if (warp < kProdWarps) {  // ------------------------------------- producers
     // 4 lanes per row, each lane two k-groups (32 contiguous bytes of the row):
@@ -552,6 +553,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // setup above overlaps the previous kernel's tail
   const int rb = p.rows.begin(seg), re = p.rows.end(seg);
   const int nchunks = (re - rb + KC - 1) / KC;
   int my_chunks = 0;
@@ -691,7 +693,7 @@ inline void tc_red_reduce(const P& p, const float* partial, int nsplit, cudaStre
   const int Mo = p.M + (p.colsum ? 1 : 0);
   const size_t KN = size_t(Mo) * p.Ncols;
   dim3 grid(unsigned((KN + 31) / 32), p.rows.nseg);
-  split_reduce_kernel<<<grid, 256, 0, st>>>(partial, nsplit * KN, KN, int(KN), RedStore<P>{p, nsplit, Mo});
+  kl(split_reduce_kernel<RedStore<P>>, grid, 256, 0, st, partial, nsplit * KN, KN, int(KN), RedStore<P>{p, nsplit, Mo});
 }
 
 }  // namespace tc
