@@ -381,6 +381,12 @@ def run_b200(args, rank, world, local_rank, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    rank_ms = [dev_ms / args.steps]
+    if dist:
+        t = torch.zeros(world, dtype=torch.float64)
+        t[rank] = dev_ms / args.steps
+        dist.all_reduce(t)
+        rank_ms = [round(float(x), 4) for x in t]
     dev_ms = max_over_ranks(dev_ms)
     counts = batch_counts()
     structs_per_step = world * sum(counts)  # sum over ranks of their batches
@@ -446,7 +452,7 @@ def run_b200(args, rank, world, local_rank, dist):
                     "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": 240},
             "gpu_launches": int(round(launches_per_step * args.steps)),
             "roofline": roof, "roofline_gather_scatter": roof_gs, "clocks": clocks,
-            "cpu_baseline": cpu, **({"comm": nb} if nb else {}),
+            "cpu_baseline": cpu, **({"comm": nb, "rank_ms_per_step": rank_ms} if nb else {}),
             "kernel_ms_per_step": {r["name"]: round(r["ms"], 4) for r in sorted(rep, key=lambda r: -r["ms"])},
         }
         print(json.dumps(line), flush=True)

@@ -98,6 +98,7 @@ void free_ctx(Ctx& c) {
   if (c.s_e) cudaStreamDestroy(c.s_e);
   if (c.s_w) cudaStreamDestroy(c.s_w);
   if (c.s_w2) cudaStreamDestroy(c.s_w2);
+  if (c.s_c) cudaStreamDestroy(c.s_c);
   if (c.stream) cudaStreamDestroy(c.stream);
 }
 
@@ -133,8 +134,12 @@ int enqueue_step(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st) {
   launch_nbr(c, st);
   launch_forward(c, st);
   launch_loss(c, cfg.w_energy, cfg.w_force, st);
-  launch_backward(c, st);
-  if (c.comm) {
+  launch_backward(c, st, true);  // with a communicator: bucketed allreduces overlap it
+  if (c.comm_err) {
+    c.comm_err = 0;
+    return fail(HMTL_ERR_COMM, "NCCL: bucketed gradient allreduce failed");
+  }
+  if (c.comm && !comm_overlap(c)) {
     int rc = comm_sync_grads(c, st);
     if (rc) return rc;
   }
@@ -213,11 +218,13 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
     if (cudaStreamCreateWithPriority(&c.stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c.s_e, cudaStreamNonBlocking, lo) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c.s_w, cudaStreamNonBlocking, lo) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&c.s_w2, cudaStreamNonBlocking, lo) != cudaSuccess)
+        cudaStreamCreateWithPriority(&c.s_w2, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c.s_c, cudaStreamNonBlocking, hi) != cudaSuccess)
       rc = HMTL_ERR_INTERNAL;
   }
   if (const char* e = std::getenv("HMTL_SINGLE_STREAM")) c.multi_stream = e[0] == '0';
   if (const char* e = std::getenv("HMTL_NO_CHAIN")) c.fuse_chain = e[0] == '0';
+  if (const char* e = std::getenv("HMTL_NO_COMM_OVERLAP")) c.overlap_comm = e[0] == '0';
   if (std::getenv("HMTL_CHAIN_STAMPS")) A(&c.chain_stamps, size_t(4096) * 32);
   if (const char* e = std::getenv("HMTL_CHAIN_DBG")) c.chain_dbg = std::atoi(e);
   if (const char* e = std::getenv("HMTL_DBG_SKIP_WGRAD")) c.dbg_skip_wgrad = e[0] == '1';

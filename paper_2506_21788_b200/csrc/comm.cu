@@ -57,6 +57,34 @@ int comm_sync_grads(Ctx& c, cudaStream_t st) {
   return 0;
 }
 
+// ---- overlapped (bucketed) sync, issued from inside launch_backward on the
+// comm stream as soon as each bucket's gradients are final: the owned heads'
+// blocks (head groups) right after the heads' backward, then each encoder
+// layer's contiguous shared block, top layer first, and finally the rest of the
+// shared block (the embedding).  ncclAvg is elementwise, so bucketing gives
+// the same group means as one allreduce of the whole block.
+bool comm_overlap(const Ctx& c) { return c.comm && c.comm->world_size > 1 && c.overlap_comm; }
+
+void comm_heads_async(Ctx& c, cudaStream_t sc) {
+  Comm* m = c.comm;
+  for (int s = 0; s < c.S; ++s) {
+    const int k = c.owned[s];
+    if (m->head[k] && m->head_size[k] > 1) {
+      float* g = c.grads + c.PS + size_t(s) * c.PH;
+      if (ncclAllReduce(g, g, c.PH, ncclFloat32, ncclAvg, m->head[k], sc) != ncclSuccess) c.comm_err = 1;
+      m->bytes_head += c.PH * sizeof(float);
+    }
+  }
+}
+
+void comm_shared_async(Ctx& c, size_t off, size_t count, cudaStream_t sc) {
+  Comm* m = c.comm;
+  if (!count) return;
+  if (ncclAllReduce(c.grads + off, c.grads + off, count, ncclFloat32, ncclAvg, m->world, sc) != ncclSuccess)
+    c.comm_err = 1;
+  m->bytes_encoder += count * sizeof(float);
+}
+
 void comm_destroy(Comm* m) {
   if (!m) return;
   for (auto& h : m->head)

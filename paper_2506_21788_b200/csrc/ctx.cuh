@@ -92,6 +92,9 @@ struct Ctx {
   // concurrency inside the step: s_e runs the energy head branch, s_w the
   // weight gradients; both fork from / join into the step stream via events
   cudaStream_t s_e = nullptr, s_w = nullptr, s_w2 = nullptr;
+  cudaStream_t s_c = nullptr;  // gradient allreduces (high priority), overlapped with the backward
+  bool overlap_comm = true;
+  int comm_err = 0;
   std::vector<cudaEvent_t> evs;
   size_t ev_i = 0;
   bool multi_stream = true;
@@ -162,12 +165,15 @@ void launch_prep(Ctx& c, cudaStream_t st);      // arena -> node/graph tables, r
 void launch_nbr(Ctx& c, cudaStream_t st);       // neighbour list, CSR, rev, edge offsets
 void launch_forward(Ctx& c, cudaStream_t st);   // ModelT::forward
 void launch_loss(Ctx& c, float w_e, float w_f, cudaStream_t st);
-void launch_backward(Ctx& c, cudaStream_t st);  // ModelT::backward (upstreams in c.dE/c.dF)
+void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync = false);  // ModelT::backward (upstreams in c.dE/c.dF)
 void launch_adamw(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st);
 void launch_debug_z1(Ctx& c, int layer, float* out, cudaStream_t st);
 void launch_bimg_all(Ctx& c, cudaStream_t st);  // rebuild every recorded B image
 
 int comm_sync_grads(Ctx& c, cudaStream_t st);
+bool comm_overlap(const Ctx& c);                                    // bucketed sync inside the backward
+void comm_heads_async(Ctx& c, cudaStream_t sc);                     // owned heads, head groups
+void comm_shared_async(Ctx& c, size_t off, size_t count, cudaStream_t sc);  // shared range, world
 
 // RAII timing scope: records start/end events on `st` when profiling is on.
 struct Prof {

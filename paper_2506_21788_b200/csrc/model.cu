@@ -1653,7 +1653,7 @@ void colsum2(Ctx& c, RowSet rows, const float* w, int wstride, const float* x, i
 }
 }  // namespace
 
-void launch_backward(Ctx& c, cudaStream_t st) {
+void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
   const int H = c.H, W = c.W, L = c.L, D = c.D, sm = c.sm_count;
   const size_t NH = size_t(c.Nc) * H, EH = size_t(c.Ec) * H;
   const size_t SBS = size_t(c.Nc) * 2 * std::max(H, W);  // one Sb slot
@@ -1662,6 +1662,9 @@ void launch_backward(Ctx& c, cudaStream_t st) {
   // streams: st = critical path (dx chain), se = energy head branch, sw = weight
   // gradients (consumed only by the gradient sync / AdamW after the final join)
   cudaStream_t se = c.side(c.s_e, st), sw = c.side(c.s_w, st), sw2 = c.side(c.s_w2, st);
+  // gradient sync buckets (MTL-par), issued on the comm stream as they become final
+  const bool cs = comm_sync && comm_overlap(c);
+  cudaStream_t sc = c.side(c.s_c, st);
   float* dhL = c.dhb + size_t(L) * NH;  // dL/dh_L, written by the heads
 
   // ---------------- energy heads (hmtl/model.hpp:512-524)
@@ -1747,6 +1750,12 @@ void launch_backward(Ctx& c, cudaStream_t st) {
     F0Dh dhq{node_rows_by_head(c), W, H, H, W, Sf, HeadW{c.head_params(), c.PH, wf0}, dhL};
     ab(dhq, c.Nc, c.S, st, sm, c);
   }
+  if (cs) {  // every owned head's gradient block is final: head-group means
+    c.dep(st, sc);
+    c.dep(sw, sc);
+    c.dep(sw2, sc);
+    comm_heads_async(c, sc);
+  }
   // ---------------- encoder layers in reverse (hmtl/model.hpp:552-617)
   const bool fused = chain_ok(c);
   bool node_done = false;
@@ -1817,6 +1826,12 @@ void launch_backward(Ctx& c, cudaStream_t st) {
       L10Prob q{node_rows(c), H, 2 * H, H, h, Sl, geW1};
       atb(q, c, c.nsplit_node, sw2, c.Nc);
     }
+    if (cs) {  // layer l's shared block is final once its weight-gradient kernels finish
+      c.dep(sw, sc);
+      c.dep(sw2, sc);
+      const size_t o0 = c.shared_off(p + "edge.W1"), o1 = c.shared_off(p + "node.b2") + size_t(H);
+      comm_shared_async(c, o0, o1 - o0, sc);
+    }
     if (fused && l > 0) {  // L11 of this layer + [L1, L4] of the layer below
       const std::string pb = "layer" + std::to_string(l - 1) + ".";
       const float* vz1b = c.vz1 + size_t(l - 1) * NH;
@@ -1847,8 +1862,13 @@ void launch_backward(Ctx& c, cudaStream_t st) {
           c.hdr, c.species, dh0, c.grads + c.shared_off("embed"), H, c.NS);
     }
   }
-  c.dep(sw, st);  // every weight gradient is final
+  if (cs) {  // the rest of the shared block (the embedding)
+    c.dep(st, sc);
+    comm_shared_async(c, 0, c.shared_off("layer0.edge.W1"), sc);
+  }
+  c.dep(sw, st);  // every weight gradient is final (and, with MTL-par, averaged)
   c.dep(sw2, st);
+  if (cs) c.dep(sc, st);
 }
 
 // debug probe: z1 of layer l (the factorised pre-activation), [E x H]
