@@ -120,6 +120,17 @@ int hmtl_generate(const hmtl_dataset_spec* spec, uint64_t seed, int* G, int* N, 
  * Returns 0 or HMTL_ERR_CONFIG when the heads cannot be balanced. */
 int hmtl_head_placement(int world, int n_heads, const double* weights, double* share);
 
+/* Epoch plan, shuffle_epoch (hmtl/datastore.hpp:48-75, src/datastore.cpp:47-97):
+ * rank `rank`'s ordered (dataset, index) list for one epoch, steps * b_local
+ * items.  mode 0 = base (one permutation of the mixed set over all `world`
+ * ranks), 1 = taskpar (dataset ids[i] dealt only over its serving group
+ * members[member_off[i] .. member_off[i+1]), ascending ranks; the reference's
+ * Mesh is members of id g = g*M .. g*M+M-1).  Host-only, deterministic
+ * (reference RNG streams).  Pass null outputs to query *n_items. */
+int hmtl_epoch_plan(int mode, const uint8_t* ids, const uint64_t* counts, int n_datasets, const int* members,
+                    const int* member_off, int world, uint64_t seed, int b_local, int rank, uint8_t* out_ds,
+                    uint64_t* out_idx, size_t cap, int* steps, size_t* n_items);
+
 /* ------------------------------------------------------------ device */
 /* ModelT<float>(hp, seed, owned_heads), hmtl/model.hpp:158: creates the device
  * context on `device`, allocates capacity-padded buffers and initialises the
@@ -142,6 +153,18 @@ int hmtl_batch_upload(hmtl_ctx* ctx, const hmtl_samples* s, void* stream);
 int hmtl_pool_add(hmtl_ctx* ctx, const hmtl_samples* s, int* slot);
 /* ... and bind pool slot `slot` as the current batch (device-to-device). */
 int hmtl_pool_bind(hmtl_ctx* ctx, int slot, void* stream);
+
+/* Device-resident sample store (DataStore, hmtl/datastore.hpp:77-115): the
+ * pool (samples in order; per dataset, local index = order of appearance) is
+ * uploaded to HBM once; store_bind gathers a plan's batch (dataset ids[n],
+ * local indices[n]) into the context's batch arena on the device -- the same
+ * arena bytes hmtl_batch_upload would pack -- so only 4 B per graph (+ offsets)
+ * cross PCIe per step.  Errors as build_batch / fetch_samples. */
+typedef struct hmtl_store hmtl_store;
+int hmtl_store_create(int device, const hmtl_samples* pool, hmtl_store** out);
+int hmtl_store_counts(const hmtl_store* st, uint8_t* ids, uint64_t* counts, int cap, int* n);
+int hmtl_store_bind(hmtl_ctx* ctx, hmtl_store* st, const uint8_t* ds, const uint64_t* idx, int n, void* stream);
+int hmtl_store_destroy(hmtl_store* st);
 
 /* build_batch<float> on the device (hmtl/graph.hpp:46-83): bit-exact FP64
  * cutoff test, dst-major CSR, reverse-edge permutation, per-graph edge offsets. */

@@ -277,6 +277,25 @@ class Ref:
     def err(self) -> str:
         return self.lib.ref_last_error().decode()
 
+    def shuffle_epoch(self, counts: dict, n_groups: int, replicas: int, mode: int, seed: int, b_local: int,
+                      rank: int):
+        """The reference's shuffle_epoch (src/datastore.cpp:47-97) for one rank of Mesh{n_groups, replicas}."""
+        L = self.lib
+        L.ref_shuffle_epoch.restype = C.c_long
+        L.ref_shuffle_epoch.argtypes = [C.POINTER(_U8), C.POINTER(C.c_uint64), C.c_int, C.c_int, C.c_int, C.c_int,
+                                        C.c_uint64, C.c_int, C.c_int, C.POINTER(_U8), C.POINTER(C.c_uint64),
+                                        C.POINTER(_I)]
+        ids = np.array(sorted(counts), np.uint8)
+        cnt = np.array([counts[int(k)] for k in ids], np.uint64)
+        cap = int(cnt.sum()) + 1
+        ds, ix, st = np.zeros(cap, np.uint8), np.zeros(cap, np.uint64), _I()
+        n = L.ref_shuffle_epoch(_p(ids, _U8), cnt.ctypes.data_as(C.POINTER(C.c_uint64)), len(ids), n_groups,
+                                replicas, mode, seed, b_local, rank, _p(ds, _U8),
+                                ix.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(st))
+        if n < 0:
+            raise RuntimeError(self.err())
+        return st.value, ds[:n], ix[:n]
+
     def default5_spec(self, i: int) -> dict:
         el = (_U8 * 32)()
         ne, nmin, nmax = _I(), _I(), _I()

@@ -17,10 +17,12 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <map>
 #include <string>
 #include <thread>
 #include <vector>
 
+#include "hmtl/datastore.hpp"
 #include "hmtl/dataset.hpp"
 #include "hmtl/graph.hpp"
 #include "hmtl/model.hpp"
@@ -459,6 +461,27 @@ double ref_train_step(void* tp, int G, const int* n_atoms, const uint8_t* specie
           t->eps, t->wd);
   }
   return loss / double(G);
+}
+
+// shuffle_epoch (src/datastore.cpp:47-97) of the reference on Mesh{n_groups, replicas};
+// mode 0 base, 1 taskpar.  Writes rank `rank`'s plan; returns its item count.
+long ref_shuffle_epoch(const uint8_t* ids, const uint64_t* counts, int n, int n_groups, int replicas, int mode,
+                       uint64_t seed, int b_local, int rank, uint8_t* out_ds, uint64_t* out_idx, int* steps) {
+  try {
+    std::map<uint8_t, uint64_t> cnt;
+    for (int i = 0; i < n; ++i) cnt[ids[i]] = counts[i];
+    Mesh mesh;
+    mesh.n_groups = n_groups;
+    mesh.replicas = replicas;
+    EpochPlan p = shuffle_epoch(cnt, mesh, mode == 1 ? RunMode::taskpar : RunMode::base, seed, b_local);
+    *steps = p.steps;
+    const auto& v = p.per_rank[rank];
+    for (size_t i = 0; i < v.size(); ++i) out_ds[i] = v[i].dataset, out_idx[i] = v[i].index;
+    return long(v.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
 }
 
 }  // extern "C"

@@ -110,6 +110,13 @@ SIGNATURES = {
     "hmtl_selftest_mma_rate": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "hmtl_selftest_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _FP, _FP, _FP]),
     "hmtl_selftest_time": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _FP]),
+    "hmtl_epoch_plan": (C.c_int, [C.c_int, _U8P, C.POINTER(C.c_uint64), C.c_int, _IP, _IP, C.c_int, C.c_uint64,
+                                  C.c_int, C.c_int, _U8P, C.POINTER(C.c_uint64), C.c_size_t, _IP,
+                                  C.POINTER(C.c_size_t)]),
+    "hmtl_store_create": (C.c_int, [C.c_int, C.POINTER(CSamples), C.POINTER(_P)]),
+    "hmtl_store_counts": (C.c_int, [_P, _U8P, C.POINTER(C.c_uint64), C.c_int, _IP]),
+    "hmtl_store_bind": (C.c_int, [_P, _P, _U8P, C.POINTER(C.c_uint64), C.c_int, _P]),
+    "hmtl_store_destroy": (C.c_int, [_P]),
     "hmtl_comm_unique_id": (C.c_int, [_U8P]),
     "hmtl_comm_init": (C.c_int, [_P, _U8P, C.c_int, C.c_int]),
     "hmtl_comm_sync_grads": (C.c_int, [_P, _P]),

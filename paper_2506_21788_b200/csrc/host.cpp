@@ -392,3 +392,75 @@ int hmtl_head_placement(int world, int n_heads, const double* w, double* share) 
 }
 
 }  // extern "C"
+
+// ---- epoch plan: shuffle_epoch (src/datastore.cpp:47-97) -------------------
+// Per-rank ordered sample lists of one epoch.  taskpar: per dataset (ascending
+// id, as the reference's std::map), a seeded Fisher-Yates permutation
+// (seed_stream(seed, 0x700 + id)) of that dataset only, dealt in steps of
+// replicas x b_local over the dataset's serving group; steps = min over the
+// datasets of count / (replicas * b_local).  base: one permutation
+// (seed_stream(seed, 0x77)) of the mixed (dataset, index) set dealt over all
+// ranks.  The reference's Mesh (hmtl/mesh.hpp:21-31) is the special case
+// members[g] = {g*M .. g*M+M-1}; any placement's head groups are accepted.
+extern "C" int hmtl_epoch_plan(int mode, const uint8_t* ids, const uint64_t* counts, int n_datasets,
+                               const int* members, const int* member_off, int world, uint64_t seed, int b_local,
+                               int rank, uint8_t* out_ds, uint64_t* out_idx, size_t cap, int* steps_out,
+                               size_t* n_items) {
+  using namespace hmtl_b200;
+  if (b_local < 1) return fail(HMTL_ERR_CONTRACT, "b_local must be >= 1");
+  if (!ids || !counts || n_datasets < 1 || world < 1 || rank < 0 || rank >= world || !steps_out || !n_items)
+    return fail(HMTL_ERR_CONTRACT, "epoch_plan: bad arguments");
+  std::vector<int> order(n_datasets);  // ascending dataset id (std::map order)
+  for (int i = 0; i < n_datasets; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return ids[a] < ids[b]; });
+  for (int i = 1; i < n_datasets; ++i)
+    if (ids[order[i]] == ids[order[i - 1]]) return fail(HMTL_ERR_CONTRACT, "epoch_plan: duplicate dataset id");
+  std::vector<uint8_t> ds;
+  std::vector<uint64_t> ix;
+  int steps = 0;
+  if (mode == 1) {  // taskpar
+    if (!members || !member_off) return fail(HMTL_ERR_CONTRACT, "taskpar: dataset id without sub-group");
+    steps = -1;
+    for (int i : order) {
+      const int M = member_off[i + 1] - member_off[i];
+      if (M < 1) return fail(HMTL_ERR_CONTRACT, "taskpar: dataset id without sub-group");
+      const int g = int(counts[i] / (uint64_t(M) * uint64_t(b_local)));
+      steps = steps < 0 ? g : std::min(steps, g);
+    }
+    steps = std::max(steps, 0);
+    for (int i : order) {
+      const int M = member_off[i + 1] - member_off[i];
+      int slot = -1;
+      for (int s = 0; s < M; ++s)
+        if (members[member_off[i] + s] == rank) slot = s;
+      if (slot < 0) continue;
+      std::vector<uint64_t> idx(counts[i]);
+      for (uint64_t j = 0; j < counts[i]; ++j) idx[j] = j;
+      Rng rng(seed_stream(seed, 0x700 + ids[i]));
+      for (size_t j = idx.size(); j > 1; --j) std::swap(idx[j - 1], idx[size_t(rng.uniform_int(j))]);
+      for (int s = 0; s < steps; ++s) {
+        const uint64_t at = (uint64_t(s) * M + slot) * b_local;
+        for (int b = 0; b < b_local; ++b) ds.push_back(ids[i]), ix.push_back(idx[at + b]);
+      }
+    }
+  } else {  // base / serial
+    std::vector<std::pair<uint8_t, uint64_t>> all;
+    for (int i : order)
+      for (uint64_t j = 0; j < counts[i]; ++j) all.push_back({ids[i], j});
+    Rng rng(seed_stream(seed, 0x77));
+    for (size_t j = all.size(); j > 1; --j) std::swap(all[j - 1], all[size_t(rng.uniform_int(j))]);
+    steps = int(all.size() / (uint64_t(world) * uint64_t(b_local)));
+    for (int s = 0; s < steps; ++s) {
+      const uint64_t at = (uint64_t(s) * world + rank) * b_local;
+      for (int b = 0; b < b_local; ++b) ds.push_back(all[at + b].first), ix.push_back(all[at + b].second);
+    }
+  }
+  *steps_out = steps;
+  *n_items = ds.size();
+  if (out_ds || out_idx) {
+    if (cap < ds.size()) return fail(HMTL_ERR_CONTRACT, "epoch_plan: output buffer too small");
+    if (out_ds) std::copy(ds.begin(), ds.end(), out_ds);
+    if (out_idx) std::copy(ix.begin(), ix.end(), out_idx);
+  }
+  return HMTL_OK;
+}

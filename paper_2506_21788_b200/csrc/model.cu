@@ -842,7 +842,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
   }
   const size_t wf0 = c.head_off("force.W0");
   if (c.store_af0) {
-    Prof pr(c, "fwd.edge_act", st);
+    Prof pr(c, "fwd.force_act", st);
     kl(edge_af0_kernel, gridn((long long)c.Ec * W / 4, 256, sm * 16), 256, 0, st,
         c.hdr, c.Qf, c.edge_dst, c.edge_src, c.dist, c.node_graph, c.gslot, c.head_params(), c.PH,
         wf0 + size_t(H) * W, c.head_off("force.b0"), c.af0, c.sf0, W);
@@ -1380,8 +1380,12 @@ constexpr int kAggU = 8;
 __global__ void __launch_bounds__(256) agg4_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr,
                                                    const float* __restrict__ z2, float* __restrict__ agg, int H) {
   pdl_wait();
-  const int N = hdr->N, lane = threadIdx.x & 31;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += (gridDim.x * blockDim.x) >> 5) {
+  const int N = hdr->N, lane = threadIdx.x & 31, R = (N + 7) >> 3;
+  // node v of the grid-stride walk -> node (v % 8) * R + v / 8: a CTA's 8 warps take
+  // nodes from 8 regions of the batch, spreading the heavy (inorganic) degree tail
+  for (int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < 8 * R; v += (gridDim.x * blockDim.x) >> 5) {
+    const int i = (v & 7) * R + (v >> 3);
+    if (i >= N) continue;
     const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
     for (int c = lane * 4; c < H; c += 128) {
       float4 acc = f4z();
@@ -1406,8 +1410,10 @@ __global__ void __launch_bounds__(256) seg2v_kernel(const DevHdr* hdr, const int
                                                     const int* __restrict__ rev, const float* __restrict__ x,
                                                     float* __restrict__ S, int C, int fold) {
   pdl_wait();
-  const int N = hdr->N, lane = threadIdx.x & 31;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += (gridDim.x * blockDim.x) >> 5) {
+  const int N = hdr->N, lane = threadIdx.x & 31, R = (N + 7) >> 3;
+  for (int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < 8 * R; v += (gridDim.x * blockDim.x) >> 5) {
+    const int i = (v & 7) * R + (v >> 3);  // spread over the batch, as agg4_kernel
+    if (i >= N) continue;
     const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
     for (int c0 = 0; c0 < C; c0 += 128) {  // warp-uniform bound: the shuffles need every lane
       const int c = c0 + lane * 4;

@@ -363,3 +363,74 @@ def _fp(a):
 
 def _ip(a):
     return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+# ---------------------------------------------------------------- data plane
+def epoch_plan(mode: str, counts: dict, world: int, seed: int, b_local: int, rank: int,
+               members: dict | None = None):
+    """shuffle_epoch (hmtl/datastore.hpp:48-75, src/datastore.cpp:47-97) for one rank:
+    returns (steps, ds[steps*b_local] u8, idx[steps*b_local] u64).  mode 'base' or
+    'taskpar'; members = {dataset id: ascending serving ranks} (taskpar)."""
+    ids = np.array(sorted(counts), np.uint8)
+    cnt = np.array([counts[int(k)] for k in ids], np.uint64)
+    m = 1 if mode == "taskpar" else 0
+    if m:
+        if members is None:
+            raise ValueError("taskpar needs the serving group of every dataset")
+        off = np.zeros(len(ids) + 1, np.int32)
+        flat = []
+        for i, k in enumerate(ids):
+            grp = sorted(int(r) for r in members.get(int(k), []))
+            flat += grp
+            off[i + 1] = off[i] + len(grp)
+        mem = np.array(flat or [0], np.int32)
+        mp, op = _ip(mem), _ip(off)
+    else:
+        mp = op = None
+    u8 = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint8))
+    u64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint64))
+    steps, n = C.c_int(), C.c_size_t()
+    check(lib().hmtl_epoch_plan(m, u8(ids), u64(cnt), len(ids), mp, op, world, seed, b_local, rank, None, None, 0,
+                                C.byref(steps), C.byref(n)))
+    ds = np.zeros(max(n.value, 1), np.uint8)
+    ix = np.zeros(max(n.value, 1), np.uint64)
+    check(lib().hmtl_epoch_plan(m, u8(ids), u64(cnt), len(ids), mp, op, world, seed, b_local, rank, u8(ds), u64(ix),
+                                ds.size, C.byref(steps), C.byref(n)))
+    return steps.value, ds[: n.value], ix[: n.value]
+
+
+class SampleStore:
+    """Device-resident sample pool (DataStore, hmtl/datastore.hpp:77-115): upload once,
+    bind a plan's batch into a model's arena by a device gather."""
+
+    def __init__(self, pool: Samples, device: int = 0):
+        self._pool = pool  # keeps the host arrays alive for the upload
+        h = C.c_void_p()
+        check(lib().hmtl_store_create(device, C.byref(pool.as_c()), C.byref(h)))
+        self._h = h
+
+    def counts(self) -> dict:
+        n = C.c_int()
+        check(lib().hmtl_store_counts(self._h, None, None, 0, C.byref(n)))
+        ids = np.zeros(max(n.value, 1), np.uint8)
+        cnt = np.zeros(max(n.value, 1), np.uint64)
+        check(lib().hmtl_store_counts(self._h, ids.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                      cnt.ctypes.data_as(C.POINTER(C.c_uint64)), n.value, C.byref(n)))
+        return {int(i): int(c) for i, c in zip(ids[: n.value], cnt[: n.value])}
+
+    def bind(self, model: "ModelT", ds, idx, stream=None) -> None:
+        ds = np.ascontiguousarray(ds, np.uint8)
+        idx = np.ascontiguousarray(idx, np.uint64)
+        check(lib().hmtl_store_bind(model.ctx, self._h, ds.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                    idx.ctypes.data_as(C.POINTER(C.c_uint64)), len(ds), stream))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().hmtl_store_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

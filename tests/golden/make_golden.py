@@ -16,6 +16,8 @@ generator seeds 1234+k as in SURVEY.md 8(c)):
                      predictions/grads/h_final plus the reference's own FP32
                      (ModelT<float>) outputs = the FP32 noise floor
   train_ref.npz      5 steps of the reference CPU trainer (ModelT<float> + SPEC loss/AdamW)
+  epoch_plan.npz     shuffle_epoch (src/datastore.cpp:47-97) per-rank plans, base and
+                     taskpar, several meshes/seeds (`python make_golden.py epoch_plan`)
 
 The fixtures are small (< 2 MB total) and are committed; tests never read
 /root/reference at run time.
@@ -153,5 +155,29 @@ def main():
             print(f, os.path.getsize(os.path.join(HERE, f)))
 
 
+EPOCH_CASES = [  # (counts, n_groups, replicas, mode, seed, b_local)
+    ({0: 37, 1: 25, 2: 41, 3: 12, 4: 9}, 5, 1, 1, 11, 2),
+    ({0: 37, 1: 25, 2: 41, 3: 12, 4: 9}, 5, 2, 1, 12, 1),
+    ({0: 100, 1: 60}, 2, 3, 1, 13, 4),
+    ({0: 37, 1: 25, 2: 41, 3: 12, 4: 9}, 1, 4, 0, 14, 3),
+    ({0: 20, 3: 17}, 2, 2, 0, 15, 2),
+    ({2: 50}, 1, 1, 0, 16, 5),
+]
+
+
+def epoch_plans():
+    O.build(ref=True)
+    ref = O.Ref()
+    out = {}
+    for i, (counts, ng, rep, mode, seed, b) in enumerate(EPOCH_CASES):
+        for r in range(ng * rep):
+            steps, ds, ix = ref.shuffle_epoch(counts, ng, rep, mode, seed, b, r)
+            out[f"c{i}_r{r}_ds"], out[f"c{i}_r{r}_idx"], out[f"c{i}_r{r}_steps"] = ds, ix, np.array(steps)
+    np.savez_compressed(os.path.join(HERE, "epoch_plan.npz"), **out)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["epoch_plan"]:
+        epoch_plans()
+    else:
+        main()

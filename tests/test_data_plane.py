@@ -1,0 +1,104 @@
+"""Data plane on the hot path's input side: the epoch plan
+(shuffle_epoch, src/datastore.cpp:47-97) and the device-resident sample store
+that assembles each step's batch in HBM (DataStore, hmtl/datastore.hpp:77-115).
+
+The plan is host C++ behind the C ABI (no GPU needed) and must equal the
+reference's own shuffle_epoch item for item (tests/golden/epoch_plan.npz, made
+by tests/golden/make_golden.py from the unmodified reference)."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+import paper_2506_21788_b200 as P
+from paper_2506_21788_b200 import data
+
+sys.path.insert(0, os.path.join(os.path.dirname(GOLDEN)))
+from golden.make_golden import EPOCH_CASES  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    P.build()
+
+
+def mesh_members(counts, n_groups, replicas):
+    return {k: list(range(k * replicas, (k + 1) * replicas)) for k in counts}
+
+
+@pytest.mark.parametrize("case", range(len(EPOCH_CASES)))
+def test_epoch_plan_matches_reference(case):
+    g = np.load(os.path.join(GOLDEN, "epoch_plan.npz"))
+    counts, ng, rep, mode, seed, b = EPOCH_CASES[case]
+    members = mesh_members(counts, ng, rep) if mode == 1 else None
+    for r in range(ng * rep):
+        steps, ds, ix = P.epoch_plan("taskpar" if mode == 1 else "base", counts, ng * rep, seed, b, r, members)
+        assert steps == int(g[f"c{case}_r{r}_steps"])
+        assert np.array_equal(ds, g[f"c{case}_r{r}_ds"]), (case, r)
+        assert np.array_equal(ix, g[f"c{case}_r{r}_idx"]), (case, r)
+
+
+def test_taskpar_routing_and_coverage_general_placement():
+    """Placement groups of different sizes (5 heads on 8 ranks, shares {1,1,1,2,3}):
+    every rank draws only its group's dataset, replicas get disjoint samples,
+    and all groups take the same number of steps."""
+    share = data.head_placement(8, (1, 1, 1, 2, 3))
+    members = {k: [r for r in range(8) if share[r, k] > 0] for k in range(5)}
+    counts = {0: 400, 1: 300, 2: 350, 3: 500, 4: 600}
+    plans = [P.epoch_plan("taskpar", counts, 8, 99, 4, r, members) for r in range(8)]
+    assert len({p[0] for p in plans}) == 1
+    for k, grp in members.items():
+        seen = set()
+        for r in grp:
+            steps, ds, ix = plans[r]
+            assert set(ds.tolist()) <= {k}
+            items = set(ix.tolist())
+            assert not (seen & items)
+            seen |= items
+    for r in range(8):
+        assert set(plans[r][1].tolist()) <= {k for k, grp in members.items() if r in grp}
+
+
+def test_epoch_plan_errors():
+    with pytest.raises(P.HmtlError):
+        P.epoch_plan("base", {0: 10}, 1, 1, 0, 0)
+    with pytest.raises(P.HmtlError):
+        P.epoch_plan("taskpar", {0: 10, 1: 5}, 2, 1, 1, 0, {0: [0]})  # dataset 1 without a sub-group
+
+
+@pytest.mark.gpu
+def test_store_batch_equals_host_batch():
+    """A plan's batch gathered on the device from the HBM pool is the batch the
+    host would pack: same edges, and a train step gives a bit-identical loss."""
+    specs = data.default5_specs()
+    parts = [data.generate_dataset(sp, 1234 + k, count=c) for k, (sp, c) in enumerate(zip(specs, (30, 20, 20, 8, 6)))]
+    pool = P.Samples.concat(parts)
+    store = P.SampleStore(pool)
+    counts = store.counts()
+    assert counts == {k: c for k, c in enumerate((30, 20, 20, 8, 6))}
+    steps, ds, ix = P.epoch_plan("base", counts, 1, 5, 8, 0)
+    assert steps == 10
+    hp = P.ModelHyper(20, 2, 32, 32, 3, 5, 5.0)
+    offs = {k: np.cumsum([0] + [p.G for p in parts])[k] for k in range(5)}
+    cfg = P.TrainConfig(use_graph=False)
+    for s in range(3):
+        d, i = ds[s * 8:(s + 1) * 8], ix[s * 8:(s + 1) * 8]
+        host = pool.take([int(offs[int(a)] + int(b)) for a, b in zip(d, i)])
+        caps = P.Caps.for_samples(host)
+        m1 = P.ModelT(hp, 7, range(5), caps=caps)
+        m2 = P.ModelT(hp, 7, range(5), caps=caps)
+        store.bind(m1, d, i)
+        L1 = m1.train_step(None, cfg)
+        L2 = m2.train_step(host, cfg)
+        assert L1 == L2, (s, L1, L2)
+        assert np.array_equal(m1.shared_block(), m2.shared_block())
+        m1.close()
+        m2.close()
+    with pytest.raises(P.HmtlError):
+        store.bind(P.ModelT(hp, 7, [0], caps=P.Caps(64, 4096, 1 << 20)), np.array([1], np.uint8), np.array([0], np.uint64))
+    with pytest.raises(P.HmtlError):
+        store.bind(P.ModelT(hp, 7, [0], caps=P.Caps(64, 4096, 1 << 20)), np.array([0], np.uint8), np.array([30], np.uint64))
+    store.close()
