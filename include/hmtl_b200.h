@@ -165,6 +165,15 @@ int hmtl_store_create(int device, const hmtl_samples* pool, hmtl_store** out);
 int hmtl_store_counts(const hmtl_store* st, uint8_t* ids, uint64_t* counts, int cap, int* n);
 int hmtl_store_bind(hmtl_ctx* ctx, hmtl_store* st, const uint8_t* ds, const uint64_t* idx, int n, void* stream);
 int hmtl_store_destroy(hmtl_store* st);
+/* HMTD sample files (hmtl/sample_io.hpp:9-15) straight into a device store:
+ * structure checked on the host as read_sample_file_raw, the raw records
+ * uploaded as they are, per-record CRC-32 and the parse into the pool on the
+ * GPU.  Errors: io (open, magic, version, truncation, trailing bytes, CRC). */
+int hmtl_store_from_hmtd(int device, const char* const* paths, int n_files, hmtl_store** out);
+/* Host-side HMTD writer/header reader (write_sample_file / read_sample_header,
+ * src/sample_io.cpp:104-120, 173-189), byte-compatible with the reference. */
+int hmtl_hmtd_write(const char* path, uint8_t dataset_id, uint8_t aligned, const hmtl_samples* s);
+int hmtl_hmtd_read_header(const char* path, uint8_t* dataset_id, uint8_t* aligned, uint64_t* count);
 
 /* build_batch<float> on the device (hmtl/graph.hpp:46-83): bit-exact FP64
  * cutoff test, dst-major CSR, reverse-edge permutation, per-graph edge offsets. */

@@ -277,6 +277,21 @@ class Ref:
     def err(self) -> str:
         return self.lib.ref_last_error().decode()
 
+    def write_samples(self, path: str, dataset_id: int, aligned: int, s: dict) -> None:
+        """The reference's write_sample_file (src/sample_io.cpp:104-120)."""
+        L = self.lib
+        L.ref_write_samples.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_I), C.POINTER(_U8),
+                                        C.POINTER(_D), C.POINTER(_D), C.POINTER(_D), C.POINTER(_U8)]
+        n = np.ascontiguousarray(s["n_atoms"], np.int32)
+        sp = np.ascontiguousarray(s["species"], np.uint8)
+        pos = np.ascontiguousarray(s["pos"], np.float64)
+        en = np.ascontiguousarray(s["energy"], np.float64)
+        fo = np.ascontiguousarray(s["forces"], np.float64)
+        ds = np.ascontiguousarray(s["dsid"], np.uint8)
+        if L.ref_write_samples(path.encode(), dataset_id, aligned, len(n), _p(n, _I), _p(sp, _U8), _p(pos, _D),
+                               _p(en, _D), _p(fo, _D), _p(ds, _U8)) != 0:
+            raise RuntimeError(self.err())
+
     def shuffle_epoch(self, counts: dict, n_groups: int, replicas: int, mode: int, seed: int, b_local: int,
                       rank: int):
         """The reference's shuffle_epoch (src/datastore.cpp:47-97) for one rank of Mesh{n_groups, replicas}."""

@@ -27,6 +27,7 @@
 #include "hmtl/graph.hpp"
 #include "hmtl/model.hpp"
 #include "hmtl/rng.hpp"
+#include "hmtl/sample_io.hpp"
 
 using namespace hmtl;
 
@@ -478,6 +479,34 @@ long ref_shuffle_epoch(const uint8_t* ids, const uint64_t* counts, int n, int n_
     const auto& v = p.per_rank[rank];
     for (size_t i = 0; i < v.size(); ++i) out_ds[i] = v[i].dataset, out_idx[i] = v[i].index;
     return long(v.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// write_sample_file (src/sample_io.cpp:104-120) of G samples (flat arrays)
+int ref_write_samples(const char* path, int dataset_id, int aligned, int G, const int* n_atoms,
+                      const uint8_t* species, const double* pos, const double* energy, const double* forces,
+                      const uint8_t* dsid) {
+  try {
+    std::vector<AtomisticSample> v(G);
+    size_t a = 0;
+    for (int g = 0; g < G; ++g) {
+      const size_t n = size_t(n_atoms[g]);
+      v[g].species.assign(species + a, species + a + n);
+      v[g].positions.assign(pos + 3 * a, pos + 3 * (a + n));
+      v[g].forces.assign(forces + 3 * a, forces + 3 * (a + n));
+      v[g].energy_per_atom = energy[g];
+      v[g].dataset_id = dsid[g];
+      a += n;
+    }
+    io::FileHeader h;
+    h.dataset_id = uint8_t(dataset_id);
+    h.aligned = uint8_t(aligned);
+    h.count = uint64_t(G);
+    io::write_sample_file(path, h, v);
+    return 0;
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;

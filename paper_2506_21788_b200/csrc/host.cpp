@@ -464,3 +464,86 @@ extern "C" int hmtl_epoch_plan(int mode, const uint8_t* ids, const uint64_t* cou
   }
   return HMTL_OK;
 }
+
+// ---- HMTD sample files (hmtl/sample_io.hpp:9-15, src/sample_io.cpp) -----------
+// Little-endian: "HMTD", version u32 = 1, dataset_id u8, aligned u8, count u64,
+// then per record: n u32, species u8[n], positions f64[3n], energy_per_atom f64,
+// forces f64[3n], dataset_id u8, crc32 u32 (CRC-32 of the record before it).
+namespace hmtl_b200 {
+uint32_t crc32_ieee(const uint8_t* p, size_t n) {  // zlib crc32 (reflected 0xEDB88320)
+  static uint32_t table[256];
+  static bool init = false;
+  if (!init) {
+    for (uint32_t i = 0; i < 256; ++i) {
+      uint32_t c = i;
+      for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+      table[i] = c;
+    }
+    init = true;
+  }
+  uint32_t c = 0xFFFFFFFFu;
+  for (size_t i = 0; i < n; ++i) c = table[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+  return c ^ 0xFFFFFFFFu;
+}
+}  // namespace hmtl_b200
+
+namespace {
+void put_le(std::vector<uint8_t>& v, uint64_t x, int bytes) {
+  for (int i = 0; i < bytes; ++i) v.push_back(uint8_t(x >> (8 * i)));
+}
+}  // namespace
+
+extern "C" int hmtl_hmtd_write(const char* path, uint8_t dataset_id, uint8_t aligned, const hmtl_samples* s) {
+  using namespace hmtl_b200;
+  if (!path || !s || s->G < 0) return fail(HMTL_ERR_CONTRACT, "hmtd_write: bad arguments");
+  std::vector<uint8_t> buf;
+  put_le(buf, 0x44544d48u, 4);
+  put_le(buf, 1, 4);
+  buf.push_back(dataset_id);
+  buf.push_back(aligned);
+  put_le(buf, uint64_t(s->G), 8);
+  size_t a = 0;
+  for (int g = 0; g < s->G; ++g) {
+    const size_t n = size_t(s->n_atoms[g]), start = buf.size();
+    put_le(buf, n, 4);
+    buf.insert(buf.end(), s->species + a, s->species + a + n);
+    auto f64 = [&](double d) {
+      uint64_t x;
+      std::memcpy(&x, &d, 8);
+      put_le(buf, x, 8);
+    };
+    for (size_t i = 0; i < 3 * n; ++i) f64(s->positions[3 * a + i]);
+    f64(s->energy_per_atom ? s->energy_per_atom[g] : 0.0);
+    for (size_t i = 0; i < 3 * n; ++i) f64(s->forces ? s->forces[3 * a + i] : 0.0);
+    buf.push_back(s->dataset_id[g]);
+    put_le(buf, crc32_ieee(buf.data() + start, buf.size() - start), 4);
+    a += n;
+  }
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(HMTL_ERR_IO, std::string("cannot open for write: ") + path);
+  const size_t w = std::fwrite(buf.data(), 1, buf.size(), f);
+  std::fclose(f);
+  if (w != buf.size()) return fail(HMTL_ERR_IO, std::string("short write: ") + path);
+  return HMTL_OK;
+}
+
+extern "C" int hmtl_hmtd_read_header(const char* path, uint8_t* dataset_id, uint8_t* aligned, uint64_t* count) {
+  using namespace hmtl_b200;
+  FILE* f = path ? std::fopen(path, "rb") : nullptr;
+  if (!f) return fail(HMTL_ERR_IO, std::string("cannot open for read: ") + (path ? path : "(null)"));
+  uint8_t h[18];
+  const size_t got = std::fread(h, 1, sizeof h, f);
+  std::fclose(f);
+  if (got != sizeof h) return fail(HMTL_ERR_IO, std::string("short read: ") + path);
+  auto u32 = [&](int o) { return uint32_t(h[o]) | uint32_t(h[o + 1]) << 8 | uint32_t(h[o + 2]) << 16 | uint32_t(h[o + 3]) << 24; };
+  if (u32(0) != 0x44544d48u) return fail(HMTL_ERR_IO, std::string("bad magic: ") + path);
+  if (u32(4) != 1) return fail(HMTL_ERR_IO, std::string("bad version: ") + path);
+  if (dataset_id) *dataset_id = h[8];
+  if (aligned) *aligned = h[9];
+  if (count) {
+    uint64_t c = 0;
+    for (int i = 0; i < 8; ++i) c |= uint64_t(h[10 + i]) << (8 * i);
+    *count = c;
+  }
+  return HMTL_OK;
+}

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <string>
@@ -68,6 +69,66 @@ __global__ void store_gather_kernel(const int* __restrict__ sel, int G, const lo
     f[3LL * dst0 + t] = forces[3 * src0 + t];
   }
 }
+// CRC-32 (zlib's reflected 0xEDB88320) of each record body against its stored
+// value: one thread per record, table in shared memory (load-time check only).
+__global__ void hmtd_crc_kernel(const uint8_t* __restrict__ raw, const long long* __restrict__ rec_off, int R,
+                                int* __restrict__ bad) {
+  __shared__ uint32_t table[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    uint32_t c = uint32_t(i);
+    for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+    table[i] = c;
+  }
+  __syncthreads();
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+    const long long a = rec_off[r], b = rec_off[r + 1] - 4;
+    uint32_t c = 0xFFFFFFFFu;
+    for (long long i = a; i < b; ++i) c = table[(c ^ raw[i]) & 0xFF] ^ (c >> 8);
+    c ^= 0xFFFFFFFFu;
+    const uint32_t stored = uint32_t(raw[b]) | uint32_t(raw[b + 1]) << 8 | uint32_t(raw[b + 2]) << 16 |
+                            uint32_t(raw[b + 3]) << 24;
+    if (c != stored) atomicMin(bad, r);
+  }
+}
+__device__ __forceinline__ double le_f64(const uint8_t* p) {  // unaligned little-endian
+  unsigned long long x = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x |= static_cast<unsigned long long>(p[i]) << (8 * i);
+  return __longlong_as_double(static_cast<long long>(x));
+}
+// record r -> the pool's SoA (species, positions, energy, forces); CTA per record
+__global__ void hmtd_parse_kernel(const uint8_t* __restrict__ raw, const long long* __restrict__ rec_off,
+                                  const long long* __restrict__ atom_off, int R, uint8_t* __restrict__ species,
+                                  double* __restrict__ pos, double* __restrict__ energy,
+                                  double* __restrict__ forces) {
+  for (int r = blockIdx.x; r < R; r += gridDim.x) {
+    const uint8_t* rec = raw + rec_off[r];
+    const long long a0 = atom_off[r];
+    const int n = int(atom_off[r + 1] - a0);
+    const uint8_t* sp = rec + 4;
+    const uint8_t* ps = sp + n;
+    const uint8_t* en = ps + 24 * n;
+    const uint8_t* fs = en + 8;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) species[a0 + t] = sp[t];
+    for (int t = threadIdx.x; t < 3 * n; t += blockDim.x) {
+      pos[3 * a0 + t] = le_f64(ps + 8 * t);
+      forces[3 * a0 + t] = le_f64(fs + 8 * t);
+    }
+    if (threadIdx.x == 0) energy[r] = le_f64(en);
+  }
+}
+}  // namespace
+
+namespace {
+bool store_alloc(hmtl_store* st) {
+  return cudaMalloc(&st->d_atom_off, (size_t(st->G) + 1) * sizeof(long long)) == cudaSuccess &&
+         cudaMalloc(&st->d_ds, size_t(st->G)) == cudaSuccess &&
+         cudaMalloc(&st->d_species, size_t(st->N)) == cudaSuccess &&
+         cudaMalloc(&st->d_energy, size_t(st->G) * 8) == cudaSuccess &&
+         cudaMalloc(&st->d_pos, size_t(st->N) * 24) == cudaSuccess &&
+         cudaMalloc(&st->d_forces, size_t(st->N) * 24) == cudaSuccess &&
+         cudaEventCreateWithFlags(&st->staged, cudaEventDisableTiming) == cudaSuccess;
+}
 }  // namespace
 
 extern "C" {
@@ -101,13 +162,7 @@ int hmtl_store_create(int device, const hmtl_samples* s, hmtl_store** out) {
   const double* E = s->energy_per_atom;
   const double* F = s->forces;
   if (!E || !F) zeros.assign(size_t(3) * s->N + s->G, 0.0);
-  bool ok = cudaMalloc(&st->d_atom_off, off.size() * sizeof(long long)) == cudaSuccess &&
-            cudaMalloc(&st->d_ds, size_t(s->G)) == cudaSuccess &&
-            cudaMalloc(&st->d_species, size_t(s->N)) == cudaSuccess &&
-            cudaMalloc(&st->d_energy, size_t(s->G) * 8) == cudaSuccess &&
-            cudaMalloc(&st->d_pos, size_t(s->N) * 24) == cudaSuccess &&
-            cudaMalloc(&st->d_forces, size_t(s->N) * 24) == cudaSuccess &&
-            cudaEventCreateWithFlags(&st->staged, cudaEventDisableTiming) == cudaSuccess;
+  bool ok = store_alloc(st);
   if (ok)
     ok = cudaMemcpy(st->d_atom_off, off.data(), off.size() * sizeof(long long), cudaMemcpyHostToDevice) ==
              cudaSuccess &&
@@ -119,6 +174,96 @@ int hmtl_store_create(int device, const hmtl_samples* s, hmtl_store** out) {
   if (!ok) {
     hmtl_store_destroy(st);
     return fail(HMTL_ERR_INTERNAL, "store_create: device allocation/upload failed");
+  }
+  *out = st;
+  return HMTL_OK;
+}
+
+// HMTD files -> device pool.  The host reads each file once
+// and checks its structure as read_sample_file_raw (src/sample_io.cpp:122-160:
+// magic, version, `count` records, no trailing bytes); the raw record bytes go
+// to HBM as they are, and the per-record CRC check (parse_record,
+// src/sample_io.cpp:80-93) and the parse into the pool's SoA run on the GPU.
+int hmtl_store_from_hmtd(int device, const char* const* paths, int n_files, hmtl_store** out) {
+  if (!paths || n_files < 1 || !out) return fail(HMTL_ERR_CONTRACT, "store_from_hmtd: no files");
+  if (device < 0 || device >= hmtl_device_count())
+    return fail(HMTL_ERR_INTERNAL, "store_from_hmtd: no CUDA device (the B200 path has no CPU fallback)");
+  std::vector<uint8_t> raw;
+  std::vector<long long> rec_off{0}, atom_off{0};
+  std::vector<int> n_atoms;
+  std::vector<uint8_t> ds;
+  auto u32 = [](const uint8_t* p) { return uint32_t(p[0]) | uint32_t(p[1]) << 8 | uint32_t(p[2]) << 16 | uint32_t(p[3]) << 24; };
+  for (int fi = 0; fi < n_files; ++fi) {
+    const std::string path = paths[fi] ? paths[fi] : "";
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) return fail(HMTL_ERR_IO, "cannot open for read: " + path);
+    std::fseek(f, 0, SEEK_END);
+    const long len = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    std::vector<uint8_t> buf(len > 0 ? size_t(len) : 0);
+    const size_t got = std::fread(buf.data(), 1, buf.size(), f);
+    std::fclose(f);
+    if (len < 18) return fail(HMTL_ERR_IO, "sample file too short: " + path);
+    if (got != buf.size()) return fail(HMTL_ERR_IO, "short read: " + path);
+    if (u32(buf.data()) != 0x44544d48u) return fail(HMTL_ERR_IO, "bad magic (not a sample file): " + path);
+    if (u32(buf.data() + 4) != 1) return fail(HMTL_ERR_IO, "unsupported sample file version: " + path);
+    uint64_t count = 0;
+    for (int i = 0; i < 8; ++i) count |= uint64_t(buf[10 + i]) << (8 * i);
+    size_t off = 18;
+    for (uint64_t r = 0; r < count; ++r) {
+      if (off + 4 > buf.size()) return fail(HMTL_ERR_IO, "truncated record in " + path);
+      const uint32_t n = u32(buf.data() + off);
+      const size_t total = 4 + size_t(n) + 24 * size_t(n) + 8 + 24 * size_t(n) + 1 + 4;
+      if (off + total > buf.size()) return fail(HMTL_ERR_IO, "truncated record in " + path);
+      if (n < 1) return fail(HMTL_ERR_CONTRACT, "build_batch: empty graph rejected");
+      n_atoms.push_back(int(n));
+      ds.push_back(buf[off + total - 5]);
+      atom_off.push_back(atom_off.back() + n);
+      off += total;
+      rec_off.push_back(rec_off.back() + static_cast<long long>(total));
+    }
+    if (off != buf.size()) return fail(HMTL_ERR_IO, "trailing bytes in " + path);
+    raw.insert(raw.end(), buf.begin() + 18, buf.end());
+  }
+  const int R = int(n_atoms.size());
+  if (R < 1) return fail(HMTL_ERR_CONTRACT, "store_from_hmtd: no records");
+  HMTL_CUDA(cudaSetDevice(device));
+  auto* st = new hmtl_store;
+  st->device = device;
+  st->G = R;
+  st->N = atom_off.back();
+  st->n_atoms = n_atoms;
+  st->ds = ds;
+  for (int g = 0; g < R; ++g) st->by_dataset[ds[g]].push_back(g);
+  uint8_t* d_raw = nullptr;
+  long long* d_rec = nullptr;
+  int* d_bad = nullptr;
+  int bad = R;
+  bool ok = store_alloc(st) && cudaMalloc(&d_raw, raw.size()) == cudaSuccess &&
+            cudaMalloc(&d_rec, rec_off.size() * sizeof(long long)) == cudaSuccess &&
+            cudaMalloc(&d_bad, sizeof(int)) == cudaSuccess;
+  if (ok)
+    ok = cudaMemcpy(d_raw, raw.data(), raw.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(d_rec, rec_off.data(), rec_off.size() * sizeof(long long), cudaMemcpyHostToDevice) ==
+             cudaSuccess &&
+         cudaMemcpy(d_bad, &bad, sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(st->d_atom_off, atom_off.data(), atom_off.size() * sizeof(long long),
+                    cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(st->d_ds, ds.data(), ds.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+  if (ok) {
+    hmtd_crc_kernel<<<(R + 255) / 256, 256>>>(d_raw, d_rec, R, d_bad);
+    hmtd_parse_kernel<<<std::min(R, 148 * 16), 128>>>(d_raw, d_rec, st->d_atom_off, R, st->d_species, st->d_pos,
+                                                      st->d_energy, st->d_forces);
+    ok = cudaDeviceSynchronize() == cudaSuccess && cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess;
+  }
+  cudaFree(d_raw), cudaFree(d_rec), cudaFree(d_bad);
+  if (!ok) {
+    hmtl_store_destroy(st);
+    return fail(HMTL_ERR_INTERNAL, "store_from_hmtd: device upload/parse failed");
+  }
+  if (bad < R) {
+    hmtl_store_destroy(st);
+    return fail(HMTL_ERR_IO, "record: CRC mismatch (record " + std::to_string(bad) + ")");
   }
   *out = st;
   return HMTL_OK;

@@ -399,15 +399,38 @@ def epoch_plan(mode: str, counts: dict, world: int, seed: int, b_local: int, ran
     return steps.value, ds[: n.value], ix[: n.value]
 
 
+def hmtd_write(path: str, dataset_id: int, aligned: int, s: Samples) -> None:
+    """write_sample_file (src/sample_io.cpp:104-120), byte-compatible with the reference."""
+    check(lib().hmtl_hmtd_write(path.encode(), dataset_id, aligned, C.byref(s.as_c())))
+
+
+def hmtd_header(path: str) -> tuple:
+    """read_sample_header (src/sample_io.cpp:173-189): (dataset_id, aligned, count)."""
+    d, a, n = C.c_uint8(), C.c_uint8(), C.c_uint64()
+    check(lib().hmtl_hmtd_read_header(path.encode(), C.byref(d), C.byref(a), C.byref(n)))
+    return int(d.value), int(a.value), int(n.value)
+
+
 class SampleStore:
     """Device-resident sample pool (DataStore, hmtl/datastore.hpp:77-115): upload once,
     bind a plan's batch into a model's arena by a device gather."""
 
-    def __init__(self, pool: Samples, device: int = 0):
+    def __init__(self, pool: Samples | None, device: int = 0, _handle=None):
         self._pool = pool  # keeps the host arrays alive for the upload
+        if _handle is not None:
+            self._h = _handle
+            return
         h = C.c_void_p()
         check(lib().hmtl_store_create(device, C.byref(pool.as_c()), C.byref(h)))
         self._h = h
+
+    @staticmethod
+    def from_hmtd(paths, device: int = 0) -> "SampleStore":
+        """HMTD files straight to HBM: CRC check and parse on the GPU."""
+        arr = (C.c_char_p * len(paths))(*[p.encode() for p in paths])
+        h = C.c_void_p()
+        check(lib().hmtl_store_from_hmtd(device, arr, len(paths), C.byref(h)))
+        return SampleStore(None, device, _handle=h)
 
     def counts(self) -> dict:
         n = C.c_int()

@@ -16,6 +16,8 @@ generator seeds 1234+k as in SURVEY.md 8(c)):
                      predictions/grads/h_final plus the reference's own FP32
                      (ModelT<float>) outputs = the FP32 noise floor
   train_ref.npz      5 steps of the reference CPU trainer (ModelT<float> + SPEC loss/AdamW)
+  hmtd_ds{0,3}.bin   HMTD sample files written by the reference (src/sample_io.cpp:104-120)
+                     and hmtd.npz, their samples (`python make_golden.py hmtd`)
   epoch_plan.npz     shuffle_epoch (src/datastore.cpp:47-97) per-rank plans, base and
                      taskpar, several meshes/seeds (`python make_golden.py epoch_plan`)
 
@@ -176,8 +178,23 @@ def epoch_plans():
     np.savez_compressed(os.path.join(HERE, "epoch_plan.npz"), **out)
 
 
+def hmtd_files():
+    O.build(ref=True)
+    ref = O.Ref()
+    out = {}
+    for k, cnt in ((0, 8), (3, 4)):
+        spec = ref.default5_spec(k)
+        s = ref.generate(spec, 4321 + k, count=cnt)
+        ref.write_samples(os.path.join(HERE, f"hmtd_ds{k}.bin"), k, 1, s)
+        for key, v in s.items():
+            out[f"ds{k}_{key}"] = v
+    np.savez_compressed(os.path.join(HERE, "hmtd.npz"), **out)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["epoch_plan"]:
         epoch_plans()
+    elif sys.argv[1:] == ["hmtd"]:
+        hmtd_files()
     else:
         main()
