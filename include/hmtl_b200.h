@@ -87,6 +87,14 @@ typedef struct hmtl_train_cfg {
   int use_graph; /* capture the step in a CUDA graph and replay it */
 } hmtl_train_cfg;
 
+/* AdamW state of a checkpoint's blocks (the HMTP resume extension). */
+typedef struct hmtl_ckpt_opt {
+  uint64_t step;
+  const float *m_shared, *v_shared;
+  const float* const* m_heads; /* [n_heads] */
+  const float* const* v_heads;
+} hmtl_ckpt_opt;
+
 typedef struct hmtl_ctx hmtl_ctx;
 
 /* ------------------------------------------------------------ host-only */
@@ -127,6 +135,14 @@ int hmtl_head_placement(int world, int n_heads, const double* weights, double* s
  * members[member_off[i] .. member_off[i+1]), ascending ranks; the reference's
  * Mesh is members of id g = g*M .. g*M+M-1).  Host-only, deterministic
  * (reference RNG streams).  Pass null outputs to query *n_items. */
+/* HMTP checkpoints (save_checkpoint / load_checkpoint, src/model_io.cpp:62-118):
+ * the reference's v1 body (hyper record, shared + every head block as f64) plus
+ * an optional trailing "HMTO" section with the AdamW step and m/v of every
+ * block, which the reference's reader ignores.  heads = n_heads x P_h floats. */
+int hmtl_checkpoint_write(const char* path, const hmtl_hyper* hp, const float* shared, const float* heads,
+                          const hmtl_ckpt_opt* opt);
+int hmtl_checkpoint_read_hyper(const char* path, hmtl_hyper* hp, int* has_optimizer);
+
 int hmtl_epoch_plan(int mode, const uint8_t* ids, const uint64_t* counts, int n_datasets, const int* members,
                     const int* member_off, int world, uint64_t seed, int b_local, int rank, uint8_t* out_ds,
                     uint64_t* out_idx, size_t cap, int* steps, size_t* n_items);
@@ -145,6 +161,12 @@ int hmtl_set_block(hmtl_ctx* ctx, int which, const float* host);
 int hmtl_get_block(hmtl_ctx* ctx, int which, float* host);
 /* GradientBufferT (hmtl/model.hpp:98-115) of the last backward. */
 int hmtl_get_grad(hmtl_ctx* ctx, int which, float* host);
+/* Checkpoint a context (all heads owned: single rank or MTL-base) with or
+ * without its AdamW state; load the blocks this context owns (shared + owned
+ * heads, and the optimizer state when present) from any full checkpoint --
+ * every MTL-par rank resumes from one file.  Hyperparameters must match. */
+int hmtl_checkpoint_save(hmtl_ctx* ctx, const char* path, int with_optimizer);
+int hmtl_checkpoint_load(hmtl_ctx* ctx, const char* path);
 
 /* Batch upload: the samples are packed into one pinned staging arena and
  * copied with one cudaMemcpyAsync (build_batch input, hmtl/graph.hpp:46). */

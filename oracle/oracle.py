@@ -372,6 +372,13 @@ class RefModel:
         if getattr(self, "ptr", None):
             self.ref.lib.ref_model_free(self.ptr)
 
+    def save_checkpoint(self, path: str) -> None:
+        """The reference's save_checkpoint (src/model_io.cpp:62-84); FP64 model with all heads."""
+        L = self.ref.lib
+        L.ref_save_checkpoint.argtypes = [C.c_void_p, C.c_char_p]
+        if L.ref_save_checkpoint(self.ptr, path.encode()) != 0:
+            raise RuntimeError(self.ref.err())
+
     def block(self, which: int) -> np.ndarray:
         n = self.ref.lib.ref_model_shared_size(self.ptr) if which < 0 else self.ref.lib.ref_model_head_size(self.ptr)
         out = np.zeros(n, np.float64)

@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <stdexcept>
 #include <map>
 #include <string>
 #include <thread>
@@ -506,6 +507,21 @@ int ref_write_samples(const char* path, int dataset_id, int aligned, int G, cons
     h.aligned = uint8_t(aligned);
     h.count = uint64_t(G);
     io::write_sample_file(path, h, v);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// save_checkpoint (src/model_io.cpp:62-84) of a reference model's blocks
+int ref_save_checkpoint(void* m, const char* path) {
+  try {
+    auto* b = static_cast<ModelBox*>(m);
+    if (!b->md) throw std::runtime_error("ref_save_checkpoint: needs the FP64 model");
+    std::vector<std::vector<double>> heads;
+    for (int k = 0; k < b->md->hyper().n_heads; ++k) heads.push_back(b->md->head_block(k));
+    save_checkpoint(path, b->md->hyper(), b->md->shared_block(), heads);
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

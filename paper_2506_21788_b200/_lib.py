@@ -120,6 +120,10 @@ SIGNATURES = {
     "hmtl_store_from_hmtd": (C.c_int, [C.c_int, C.POINTER(C.c_char_p), C.c_int, C.POINTER(_P)]),
     "hmtl_hmtd_write": (C.c_int, [C.c_char_p, C.c_uint8, C.c_uint8, C.POINTER(CSamples)]),
     "hmtl_hmtd_read_header": (C.c_int, [C.c_char_p, _U8P, _U8P, C.POINTER(C.c_uint64)]),
+    "hmtl_checkpoint_write": (C.c_int, [C.c_char_p, C.POINTER(CHyper), _FP, _FP, _P]),
+    "hmtl_checkpoint_read_hyper": (C.c_int, [C.c_char_p, C.POINTER(CHyper), _IP]),
+    "hmtl_checkpoint_save": (C.c_int, [_P, C.c_char_p, C.c_int]),
+    "hmtl_checkpoint_load": (C.c_int, [_P, C.c_char_p]),
     "hmtl_comm_unique_id": (C.c_int, [_U8P]),
     "hmtl_comm_init": (C.c_int, [_P, _U8P, C.c_int, C.c_int]),
     "hmtl_comm_sync_grads": (C.c_int, [_P, _P]),

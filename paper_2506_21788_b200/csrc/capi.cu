@@ -383,6 +383,71 @@ int hmtl_get_grad(hmtl_ctx* h, int which, float* host) {
   return 0;
 }
 
+int hmtl_checkpoint_save(hmtl_ctx* h, const char* path, int with_optimizer) {
+  Ctx& c = h->c;
+  if (!path) return fail(HMTL_ERR_CONTRACT, "checkpoint: null path");
+  if (int(c.owned.size()) != c.hp.n_heads)
+    return fail(HMTL_ERR_CONTRACT, "checkpoint: need all head blocks in head-index order");
+  cudaSetDevice(c.device);
+  HMTL_CUDA(cudaDeviceSynchronize());
+  std::vector<float> p(c.PT), m, v;
+  HMTL_CUDA(cudaMemcpy(p.data(), c.params, c.PT * 4, cudaMemcpyDeviceToHost));
+  std::vector<const float*> hp(c.hp.n_heads), hm(c.hp.n_heads), hv(c.hp.n_heads);
+  for (int k = 0; k < c.hp.n_heads; ++k) hp[k] = p.data() + c.PS + size_t(c.slot_of[k]) * c.PH;
+  hmtl_ckpt_opt opt{};
+  if (with_optimizer) {
+    m.resize(c.PT), v.resize(c.PT);
+    DevHdr hd;
+    HMTL_CUDA(cudaMemcpy(m.data(), c.adam_m, c.PT * 4, cudaMemcpyDeviceToHost));
+    HMTL_CUDA(cudaMemcpy(v.data(), c.adam_v, c.PT * 4, cudaMemcpyDeviceToHost));
+    HMTL_CUDA(cudaMemcpy(&hd, c.hdr, sizeof hd, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < c.hp.n_heads; ++k) {
+      hm[k] = m.data() + c.PS + size_t(c.slot_of[k]) * c.PH;
+      hv[k] = v.data() + c.PS + size_t(c.slot_of[k]) * c.PH;
+    }
+    opt = hmtl_ckpt_opt{uint64_t(hd.step), m.data(), v.data(), hm.data(), hv.data()};
+  }
+  return hmtp_write(path, c.hp, p.data(), c.PS, hp.data(), c.PH, c.hp.n_heads, with_optimizer ? &opt : nullptr);
+}
+
+int hmtl_checkpoint_load(hmtl_ctx* h, const char* path) {
+  Ctx& c = h->c;
+  hmtl_hyper fh{};
+  std::vector<double> sh;
+  std::vector<std::vector<double>> hd, opt;
+  bool has_opt = false;
+  uint64_t step = 0;
+  if (int rc = hmtp_read(path, &fh, &sh, &hd, &has_opt, &step, &opt)) return rc;
+  if (fh.n_species != c.hp.n_species || fh.layers != c.hp.layers || fh.hidden != c.hp.hidden ||
+      fh.head_width != c.hp.head_width || fh.head_depth != c.hp.head_depth || fh.n_heads != c.hp.n_heads)
+    return fail(HMTL_ERR_CONFIG, "checkpoint: hyperparameters differ from the context's");
+  std::vector<float> p(c.PT), m(c.PT, 0.f), v(c.PT, 0.f);
+  auto put = [&](std::vector<float>& dst, size_t off, const std::vector<double>& src) {
+    for (size_t i = 0; i < src.size(); ++i) dst[off + i] = float(src[i]);  // exact: written from FP32
+  };
+  put(p, 0, sh);
+  if (has_opt) put(m, 0, opt[0]), put(v, 0, opt[1]);
+  for (size_t s = 0; s < c.owned.size(); ++s) {
+    const int k = c.owned[s];
+    put(p, c.PS + s * c.PH, hd[k]);
+    if (has_opt) put(m, c.PS + s * c.PH, opt[2 + 2 * k]), put(v, c.PS + s * c.PH, opt[3 + 2 * k]);
+  }
+  cudaSetDevice(c.device);
+  HMTL_CUDA(cudaDeviceSynchronize());
+  HMTL_CUDA(cudaMemcpy(c.params, p.data(), c.PT * 4, cudaMemcpyHostToDevice));
+  HMTL_CUDA(cudaMemcpy(c.adam_m, m.data(), c.PT * 4, cudaMemcpyHostToDevice));
+  HMTL_CUDA(cudaMemcpy(c.adam_v, v.data(), c.PT * 4, cudaMemcpyHostToDevice));
+  DevHdr hdr;
+  HMTL_CUDA(cudaMemcpy(&hdr, c.hdr, sizeof hdr, cudaMemcpyDeviceToHost));
+  hdr.step = has_opt ? int(step) : 0;
+  HMTL_CUDA(cudaMemcpy(c.hdr, &hdr, sizeof hdr, cudaMemcpyHostToDevice));
+  if (c.bimg_ready) {  // weights changed: rebuild the tensor-core B images
+    launch_bimg_all(c, c.stream);
+    HMTL_CUDA(cudaStreamSynchronize(c.stream));
+  }
+  return 0;
+}
+
 int hmtl_batch_upload(hmtl_ctx* h, const hmtl_samples* s, void* stream) {
   Ctx& c = h->c;
   cudaSetDevice(c.device);

@@ -66,11 +66,10 @@ constexpr size_t kSmem = size_t(kXSlots + kBSlots) * kSlot + kSlabBytes + 256 + 
 
 __device__ __forceinline__ float4 ld4c(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ void st4c(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
-__device__ __forceinline__ float silu1(float x) { return x / (1.f + __expf(-x)); }
-__device__ __forceinline__ float sgrad1(float x) {
-  const float s = 1.f / (1.f + __expf(-x));
-  return s * (1.f + x * (1.f - s));
-}
+// the same activation code as the unfused kernels (common.cuh), so a fused
+// chain is bit-identical to the separate launches it replaces
+__device__ __forceinline__ float silu1(float x) { return silu(x); }
+__device__ __forceinline__ float sgrad1(float x) { return silu_grad(x); }
 
 // GEMM 1's A operand, 4 consecutive k of row r
 template <int R>

@@ -547,3 +547,151 @@ extern "C" int hmtl_hmtd_read_header(const char* path, uint8_t* dataset_id, uint
   }
   return HMTL_OK;
 }
+
+// ---- HMTP checkpoints (src/model_io.cpp:7-13, 62-118) + optimizer section ----
+// v1 body exactly as save_checkpoint: "HMTP", version 1, hyper record (6 x u32,
+// cutoff f64), activation u8 = 1, then the shared block and every head block in
+// head order, each u64 count + f64 elements.  Resume extension (SURVEY.md
+// 8(f)3), appended after the v1 body so the reference's load_checkpoint (which
+// stops after the last head block) still reads the file: "HMTO", version u32 = 1,
+// AdamW step u64, then per block in the same order: u64 count, m f64[count],
+// v f64[count].  FP32 values are stored widened to f64 (exact both ways).
+namespace hmtl_b200 {
+namespace {
+struct Wr {
+  std::vector<uint8_t> b;
+  void raw(const void* p, size_t n) { b.insert(b.end(), (const uint8_t*)p, (const uint8_t*)p + n); }
+  void u32(uint32_t x) { raw(&x, 4); }
+  void u64(uint64_t x) { raw(&x, 8); }
+  void f64(double x) { raw(&x, 8); }
+  void block(const float* p, size_t n) {
+    u64(n);
+    for (size_t i = 0; i < n; ++i) f64(double(p[i]));
+  }
+};
+}  // namespace
+
+int hmtp_write(const char* path, const hmtl_hyper& hp, const float* shared, size_t ps, const float* const* heads,
+               size_t ph, int n_heads, const hmtl_ckpt_opt* opt) {
+  Wr w;
+  w.u32(0x50544d48u);
+  w.u32(1);
+  for (uint32_t x : {uint32_t(hp.n_species), uint32_t(hp.layers), uint32_t(hp.hidden), uint32_t(hp.head_width),
+                     uint32_t(hp.head_depth), uint32_t(hp.n_heads)})
+    w.u32(x);
+  w.f64(hp.cutoff);
+  const uint8_t act = 1;
+  w.raw(&act, 1);
+  w.block(shared, ps);
+  for (int k = 0; k < n_heads; ++k) w.block(heads[k], ph);
+  if (opt) {
+    w.u32(0x4f544d48u);  // "HMTO"
+    w.u32(1);
+    w.u64(opt->step);
+    w.block(opt->m_shared, ps);
+    w.block(opt->v_shared, ps);
+    for (int k = 0; k < n_heads; ++k) {
+      w.block(opt->m_heads[k], ph);
+      w.block(opt->v_heads[k], ph);
+    }
+  }
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(HMTL_ERR_IO, std::string("cannot open for write: ") + path);
+  const size_t n = std::fwrite(w.b.data(), 1, w.b.size(), f);
+  std::fclose(f);
+  if (n != w.b.size()) return fail(HMTL_ERR_IO, "checkpoint: short write");
+  return HMTL_OK;
+}
+
+// parse into host vectors: shared, heads[n_heads], optional optimizer section
+int hmtp_read(const char* path, hmtl_hyper* hp, std::vector<double>* shared, std::vector<std::vector<double>>* heads,
+              bool* has_opt, uint64_t* step, std::vector<std::vector<double>>* opt_blocks) {
+  FILE* f = path ? std::fopen(path, "rb") : nullptr;
+  if (!f) return fail(HMTL_ERR_IO, std::string("cannot open for read: ") + (path ? path : "(null)"));
+  std::vector<uint8_t> b;
+  std::fseek(f, 0, SEEK_END);
+  const long len = std::ftell(f);
+  std::fseek(f, 0, SEEK_SET);
+  b.resize(len > 0 ? size_t(len) : 0);
+  const size_t got = std::fread(b.data(), 1, b.size(), f);
+  std::fclose(f);
+  size_t o = 0;
+  bool short_read = got != b.size();
+  auto rd = [&](void* p, size_t n) {
+    if (o + n > b.size()) {
+      short_read = true;
+      std::memset(p, 0, n);
+      return;
+    }
+    std::memcpy(p, b.data() + o, n);
+    o += n;
+  };
+  auto u32 = [&] { uint32_t x; rd(&x, 4); return x; };
+  auto u64 = [&] { uint64_t x; rd(&x, 8); return x; };
+  auto blk = [&](std::vector<double>& v) -> bool {
+    const uint64_t n = u64();
+    if (short_read || n > (b.size() - o) / 8) return false;
+    v.resize(n);
+    rd(v.data(), 8 * n);
+    return true;
+  };
+  if (u32() != 0x50544d48u) return fail(HMTL_ERR_IO, std::string("not a checkpoint: ") + path);
+  if (u32() != 1) return fail(HMTL_ERR_IO, std::string("unsupported checkpoint version: ") + path);
+  hmtl_hyper h{};
+  h.n_species = int(u32());
+  h.layers = int(u32());
+  h.hidden = int(u32());
+  h.head_width = int(u32());
+  h.head_depth = int(u32());
+  h.n_heads = int(u32());
+  rd(&h.cutoff, 8);
+  uint8_t act = 0;
+  rd(&act, 1);
+  if (short_read) return fail(HMTL_ERR_IO, "checkpoint: short read");
+  if (act != 1) return fail(HMTL_ERR_IO, "unknown activation id in checkpoint");
+  const size_t ps = make_layout(h, true).total, ph = make_layout(h, false).total;
+  if (!blk(*shared)) return fail(HMTL_ERR_IO, "checkpoint: short read");
+  if (shared->size() != ps) return fail(HMTL_ERR_IO, "checkpoint: shared block size mismatch");
+  heads->assign(h.n_heads, {});
+  for (int k = 0; k < h.n_heads; ++k) {
+    if (!blk((*heads)[k])) return fail(HMTL_ERR_IO, "checkpoint: short read");
+    if ((*heads)[k].size() != ph) return fail(HMTL_ERR_IO, "checkpoint: head block size mismatch");
+  }
+  *hp = h;
+  *has_opt = false;
+  if (o + 8 <= b.size()) {
+    if (u32() != 0x4f544d48u || u32() != 1) return fail(HMTL_ERR_IO, "checkpoint: unknown trailing section");
+    *step = u64();
+    opt_blocks->assign(2 + 2 * size_t(h.n_heads), {});
+    for (size_t i = 0; i < opt_blocks->size(); ++i) {
+      if (!blk((*opt_blocks)[i])) return fail(HMTL_ERR_IO, "checkpoint: short read");
+      if ((*opt_blocks)[i].size() != (i < 2 ? ps : ph)) return fail(HMTL_ERR_IO, "checkpoint: optimizer block size mismatch");
+    }
+    *has_opt = true;
+  }
+  return HMTL_OK;
+}
+}  // namespace hmtl_b200
+
+extern "C" int hmtl_checkpoint_write(const char* path, const hmtl_hyper* hp, const float* shared,
+                                     const float* heads, const hmtl_ckpt_opt* opt) {
+  using namespace hmtl_b200;
+  if (!path || !hp || !shared || !heads) return fail(HMTL_ERR_CONTRACT, "checkpoint: need all head blocks in head-index order");
+  const size_t ps = make_layout(*hp, true).total, ph = make_layout(*hp, false).total;
+  std::vector<const float*> hs(hp->n_heads);
+  for (int k = 0; k < hp->n_heads; ++k) hs[k] = heads + size_t(k) * ph;
+  return hmtp_write(path, *hp, shared, ps, hs.data(), ph, hp->n_heads, opt);
+}
+
+extern "C" int hmtl_checkpoint_read_hyper(const char* path, hmtl_hyper* hp, int* has_optimizer) {
+  using namespace hmtl_b200;
+  std::vector<double> sh;
+  std::vector<std::vector<double>> hd, opt;
+  bool has = false;
+  uint64_t step = 0;
+  hmtl_hyper h{};
+  if (int rc = hmtp_read(path, &h, &sh, &hd, &has, &step, &opt)) return rc;
+  if (hp) *hp = h;
+  if (has_optimizer) *has_optimizer = has ? 1 : 0;
+  return HMTL_OK;
+}

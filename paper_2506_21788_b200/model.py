@@ -341,6 +341,14 @@ class ModelT:
         check(lib().hmtl_debug_fetch(self._ctx, name.encode(), layer, _fp(out), out.size, C.byref(n)))
         return out[: n.value]
 
+    def save_checkpoint(self, path: str, with_optimizer: bool = True) -> None:
+        """HMTP checkpoint (save_checkpoint, src/model_io.cpp:62-84) + AdamW resume section."""
+        check(lib().hmtl_checkpoint_save(self._ctx, path.encode(), int(with_optimizer)))
+
+    def load_checkpoint(self, path: str) -> None:
+        """Load the owned blocks (+ optimizer state when present) from a full HMTP checkpoint."""
+        check(lib().hmtl_checkpoint_load(self._ctx, path.encode()))
+
     def adamw(self, cfg: TrainConfig) -> None:
         check(lib().hmtl_adamw(self._ctx, C.byref(cfg.c()), None))
 
@@ -397,6 +405,20 @@ def epoch_plan(mode: str, counts: dict, world: int, seed: int, b_local: int, ran
     check(lib().hmtl_epoch_plan(m, u8(ids), u64(cnt), len(ids), mp, op, world, seed, b_local, rank, u8(ds), u64(ix),
                                 ds.size, C.byref(steps), C.byref(n)))
     return steps.value, ds[: n.value], ix[: n.value]
+
+
+def checkpoint_write(path: str, hp: ModelHyper, shared, heads) -> None:
+    """save_checkpoint (src/model_io.cpp:62-84) of host blocks (FP32, stored as f64)."""
+    sh = np.ascontiguousarray(shared, np.float32)
+    hd = np.ascontiguousarray(np.concatenate([np.asarray(h, np.float32) for h in heads]), np.float32)
+    check(lib().hmtl_checkpoint_write(path.encode(), C.byref(hp.c()), _fp(sh), _fp(hd), None))
+
+
+def checkpoint_hyper(path: str) -> tuple:
+    """(ModelHyper, has_optimizer_section) of an HMTP file."""
+    h, o = CHyper(), C.c_int()
+    check(lib().hmtl_checkpoint_read_hyper(path.encode(), C.byref(h), C.byref(o)))
+    return ModelHyper(h.n_species, h.layers, h.hidden, h.head_width, h.head_depth, h.n_heads, h.cutoff), bool(o.value)
 
 
 def hmtd_write(path: str, dataset_id: int, aligned: int, s: Samples) -> None:

@@ -18,6 +18,8 @@ generator seeds 1234+k as in SURVEY.md 8(c)):
   train_ref.npz      5 steps of the reference CPU trainer (ModelT<float> + SPEC loss/AdamW)
   hmtd_ds{0,3}.bin   HMTD sample files written by the reference (src/sample_io.cpp:104-120)
                      and hmtd.npz, their samples (`python make_golden.py hmtd`)
+  ckpt_ref.hmtp      save_checkpoint (src/model_io.cpp:62-84) of FP32-representable
+                     blocks (L2 H16 W16, 3 heads) + ckpt.npz (`python make_golden.py ckpt`)
   epoch_plan.npz     shuffle_epoch (src/datastore.cpp:47-97) per-rank plans, base and
                      taskpar, several meshes/seeds (`python make_golden.py epoch_plan`)
 
@@ -191,8 +193,25 @@ def hmtd_files():
     np.savez_compressed(os.path.join(HERE, "hmtd.npz"), **out)
 
 
+def ckpt_files():
+    O.build(ref=True)
+    ref = O.Ref()
+    h = O.Hyper(n_species=20, layers=2, hidden=16, head_width=16, head_depth=3, n_heads=3, cutoff=5.0)
+    m = O.RefModel(ref, h, 11, [0, 1, 2], dbl=True)
+    out = {}
+    for which in (-1, 0, 1, 2):
+        b = m.block(which).astype(np.float32).astype(np.float64)  # FP32-representable blocks
+        m.set_block(which, b)
+        out["shared" if which < 0 else f"head{which}"] = b.astype(np.float32)
+    m.save_checkpoint(os.path.join(HERE, "ckpt_ref.hmtp"))
+    out["hyper"] = np.array([20, 2, 16, 16, 3, 3], np.int32)
+    np.savez_compressed(os.path.join(HERE, "ckpt.npz"), **out)
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["epoch_plan"]:
+    if sys.argv[1:] == ["ckpt"]:
+        ckpt_files()
+    elif sys.argv[1:] == ["epoch_plan"]:
         epoch_plans()
     elif sys.argv[1:] == ["hmtd"]:
         hmtd_files()

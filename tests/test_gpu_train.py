@@ -145,8 +145,8 @@ def test_fused_graph_steps_match_oracle(H, L, monkeypatch):
         u.train_step(b, cfg)
     unfused = u.shared_block()
     for k in range(5):
-        assert O.rel_vec_error(fused_heads[k], u.head_block(k)) < 1e-5
+        assert np.array_equal(fused_heads[k], u.head_block(k))
     u.close()
     print("fused vs oracle", O.rel_vec_error(fused, ot.sh), "unfused vs oracle", O.rel_vec_error(unfused, ot.sh),
           "fused vs unfused", O.rel_vec_error(fused, unfused))
-    assert O.rel_vec_error(fused, unfused) < 1e-5
+    assert np.array_equal(fused, unfused)  # fusion and streams change no bit
