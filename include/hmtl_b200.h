@@ -172,6 +172,14 @@ int hmtl_checkpoint_load(hmtl_ctx* ctx, const char* path);
  * copied with one cudaMemcpyAsync (build_batch input, hmtl/graph.hpp:46). */
 int hmtl_batch_upload(hmtl_ctx* ctx, const hmtl_samples* s, void* stream);
 /* Device-resident batch pool: pack samples once into device memory ... */
+/* Periodic batch (no reference support): as batch_upload plus
+ * the lattice of every structure, cells[G][3][3] (rows a1, a2, a3, Angstrom).
+ * The next build_batch / train_step uses the cell-list neighbour list with
+ * periodic images; edges carry their source image (x_src + n1 a1 + n2 a2 +
+ * n3 a3), rows sorted by (src, image).  batch_upload switches back. */
+int hmtl_batch_upload_pbc(hmtl_ctx* ctx, const hmtl_samples* s, const double* cells, void* stream);
+/* image (n1, n2, n3) of every edge of the built batch, 3 ints per edge (syncs) */
+int hmtl_batch_edge_images(hmtl_ctx* ctx, int* img);
 int hmtl_pool_add(hmtl_ctx* ctx, const hmtl_samples* s, int* slot);
 /* ... and bind pool slot `slot` as the current batch (device-to-device). */
 int hmtl_pool_bind(hmtl_ctx* ctx, int slot, void* stream);

@@ -183,6 +183,110 @@ long ho_build_edges(int G, const int* n_atoms, const double* pos, double cutoff,
   return E;
 }
 
+static void* xmalloc(size_t n) {
+  void* p = calloc(n ? n : 1, 1);
+  if (!p) abort();
+  return p;
+}
+
+/* --------------------------------------------------------------- PBC ----- */
+static void lat_shift(const double* A, int n1, int n2, int n3, double* S) {
+  for (int k = 0; k < 3; ++k) S[k] = ((double)n1 * A[k] + (double)n2 * A[3 + k]) + (double)n3 * A[6 + k];
+}
+typedef struct { int j, key, n1, n2, n3; } pbc_hit;
+static int pbc_cmp(const void* a, const void* b) {
+  const pbc_hit *x = (const pbc_hit*)a, *y = (const pbc_hit*)b;
+  if (x->j != y->j) return x->j < y->j ? -1 : 1;
+  return x->key < y->key ? -1 : (x->key > y->key);
+}
+long ho_build_edges_pbc(int G, const int* n_atoms, const double* pos, const double* cells, double cutoff,
+                        int* graph_offset, int* edge_offset, int* edge_dst, int* edge_src, int* img, double* shift) {
+  const double rc2 = cutoff * cutoff;
+  long E = 0;
+  int base = 0;
+  if (graph_offset) graph_offset[0] = 0;
+  if (edge_offset) edge_offset[0] = 0;
+  for (int g = 0; g < G; ++g) {
+    const int n = n_atoms[g];
+    if (n < 1) return -1;
+    const double* A = cells + 9 * (size_t)g;
+    const double* P = pos + 3 * (size_t)base;
+    /* generous image range: |fractional displacement| + rc / width, from the
+       reciprocal rows (f = x A^-1) */
+    const double a[3][3] = {{A[0], A[1], A[2]}, {A[3], A[4], A[5]}, {A[6], A[7], A[8]}};
+    double c[3][3];
+    for (int k = 0; k < 3; ++k) {
+      const int u = (k + 1) % 3, v = (k + 2) % 3;
+      c[k][0] = a[u][1] * a[v][2] - a[u][2] * a[v][1];
+      c[k][1] = a[u][2] * a[v][0] - a[u][0] * a[v][2];
+      c[k][2] = a[u][0] * a[v][1] - a[u][1] * a[v][0];
+    }
+    const double V = a[0][0] * c[0][0] + a[0][1] * c[0][1] + a[0][2] * c[0][2];
+    /* per pair, the images whose fractional displacement can be within rc:
+       n_k in [floor(fd_k - rc/w_k) - 1, ceil(fd_k + rc/w_k) + 1], fd = f_i - f_j */
+    double span[3];
+    double* F = xmalloc(sizeof(double) * 3 * (size_t)n);
+    for (int k = 0; k < 3; ++k) {
+      const double cn = sqrt(c[k][0] * c[k][0] + c[k][1] * c[k][1] + c[k][2] * c[k][2]);
+      span[k] = cutoff * cn / fabs(V);
+      for (int i = 0; i < n; ++i)
+        F[3 * i + k] = (P[3 * i] * c[k][0] + P[3 * i + 1] * c[k][1] + P[3 * i + 2] * c[k][2]) / V;
+    }
+    size_t cap = 64;
+    pbc_hit* hits = xmalloc(sizeof(pbc_hit) * cap);
+    for (int i = 0; i < n; ++i) {
+      int h = 0;
+      for (int j = 0; j < n; ++j) {
+        int lo[3], hi[3];
+        for (int k = 0; k < 3; ++k) {
+          const double fd = F[3 * i + k] - F[3 * j + k];
+          lo[k] = (int)floor(fd - span[k]) - 1;
+          hi[k] = (int)ceil(fd + span[k]) + 1;
+        }
+        for (int n1 = lo[0]; n1 <= hi[0]; ++n1)
+          for (int n2 = lo[1]; n2 <= hi[1]; ++n2)
+            for (int n3 = lo[2]; n3 <= hi[2]; ++n3) {
+              if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
+              double S[3];
+              lat_shift(A, n1, n2, n3, S);
+              const double dx = (P[3 * i] - P[3 * j]) - S[0];
+              const double dy = (P[3 * i + 1] - P[3 * j + 1]) - S[1];
+              const double dz = (P[3 * i + 2] - P[3 * j + 2]) - S[2];
+              if ((dx * dx + dy * dy) + dz * dz <= rc2) {
+                if (abs(n1) > 7 || abs(n2) > 7 || abs(n3) > 7) {
+                  free(hits), free(F);
+                  return -2;
+                }
+                if ((size_t)h == cap) {
+                  pbc_hit* nh = xmalloc(sizeof(pbc_hit) * cap * 2);
+                  memcpy(nh, hits, sizeof(pbc_hit) * cap);
+                  free(hits);
+                  hits = nh, cap *= 2;
+                }
+                pbc_hit t = {j, (n1 + 8) * 256 + (n2 + 8) * 16 + (n3 + 8), n1, n2, n3};
+                hits[h++] = t;
+              }
+            }
+      }
+      qsort(hits, (size_t)h, sizeof(pbc_hit), pbc_cmp);
+      for (int q = 0; q < h; ++q) {
+        if (edge_dst) {
+          edge_dst[E] = base + i;
+          edge_src[E] = base + hits[q].j;
+          if (img) img[3 * E] = hits[q].n1, img[3 * E + 1] = hits[q].n2, img[3 * E + 2] = hits[q].n3;
+          if (shift) lat_shift(A, hits[q].n1, hits[q].n2, hits[q].n3, shift + 3 * E);
+        }
+        ++E;
+      }
+    }
+    free(hits), free(F);
+    base += n;
+    if (graph_offset) graph_offset[g + 1] = base;
+    if (edge_offset) edge_offset[g + 1] = (int)E;
+  }
+  return E;
+}
+
 /* ------------------------------------------------------------ numcore ----- */
 /* hmtl/kernels.hpp:19-32 */
 static void linear_forward(const double* x, size_t batch, size_t in, const double* W,
@@ -252,11 +356,7 @@ static void lay_make(const ho_hyper* hp, int shared, lay_t* L) {
   }
 }
 
-static void* xmalloc(size_t n) {
-  void* p = calloc(n ? n : 1, 1);
-  if (!p) abort();
-  return p;
-}
+
 
 /* head MLP forward, mlp_forward_ hmtl/model.hpp:282-306.  `first` is the
  * entry index of <prefix>.W0 in the head layout; entries alternate W,b. */
@@ -329,6 +429,9 @@ int ho_forward(const ho_hyper* hp, const double* shared, const double* const* he
     const double* pi = b->pos + 3 * (size_t)b->edge_dst[e];
     const double* pj = b->pos + 3 * (size_t)b->edge_src[e];
     double dx = pi[0] - pj[0], dy = pi[1] - pj[1], dz = pi[2] - pj[2];
+    if (b->edge_shift) { /* periodic image of the source (8(f)4) */
+      dx -= b->edge_shift[3 * e], dy -= b->edge_shift[3 * e + 1], dz -= b->edge_shift[3 * e + 2];
+    }
     dvec[3 * e] = dx;
     dvec[3 * e + 1] = dy;
     dvec[3 * e + 2] = dz;
@@ -512,6 +615,7 @@ int ho_backward(const ho_hyper* hp, const double* shared, const double* const* h
     const double* pi = b->pos + 3 * (size_t)b->edge_dst[e];
     const double* pj = b->pos + 3 * (size_t)b->edge_src[e];
     double dx = pi[0] - pj[0], dy = pi[1] - pj[1], dz = pi[2] - pj[2];
+    if (b->edge_shift) dx -= b->edge_shift[3 * e], dy -= b->edge_shift[3 * e + 1], dz -= b->edge_shift[3 * e + 2];
     dvec[3 * e] = dx, dvec[3 * e + 1] = dy, dvec[3 * e + 2] = dz;
     d[e] = sqrt(dx * dx + dy * dy + dz * dz);
   }

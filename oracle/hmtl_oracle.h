@@ -40,6 +40,7 @@ typedef struct {
   const int* edge_dst;            /* E   */
   const int* edge_src;            /* E   */
   const uint8_t* dataset_id;      /* G   */
+  const double* edge_shift;       /* 3E lattice shift S of the source image (PBC), NULL = none */
 } ho_batch;
 
 /* Forward cache (subset of ForwardCacheT, hmtl/model.hpp:117-151).  Every
@@ -67,6 +68,17 @@ int ho_layout_entries(const ho_hyper* hp, int shared, int i, char* name, size_t 
 uint64_t ho_seed_stream(uint64_t master, uint64_t stream_id);
 /* ModelT ctor / init_block_, hmtl/model.hpp:158-167, 211-225.  which=-1 shared, k>=0 head k */
 void ho_init_block(const ho_hyper* hp, uint64_t seed, int which, double* out);
+
+/* Periodic neighbour list (the reference has no PBC, so this
+ * FP64 brute force over lattice images is the builder's own oracle).  cells:
+ * [G][3][3], rows = lattice vectors a1, a2, a3.  Edge (i, j, n): source image
+ * x_j + S, S = (n1 a1 + n2 a2) + n3 a3 per component, test
+ * ((xi - xj) - S)^2 summed as (dx*dx + dy*dy) + dz*dz <= rc^2, self pair
+ * (i, i, 0) excluded.  Rows sorted by (src, image key (n1+8)*256+(n2+8)*16+(n3+8)),
+ * |n_k| <= 7.  Returns E (count when edge_dst == NULL), -1 empty graph, -2
+ * image range exceeded.  img: 3 ints per edge; shift: 3 doubles per edge. */
+long ho_build_edges_pbc(int G, const int* n_atoms, const double* pos, const double* cells, double cutoff,
+                        int* graph_offset, int* edge_offset, int* edge_dst, int* edge_src, int* img, double* shift);
 
 /* build_batch edge search, hmtl/graph.hpp:46-83. Returns E (count) when
  * edge_dst == NULL, else fills and returns E. -1 on empty graph. */

@@ -66,7 +66,7 @@ class _CBatch(C.Structure):
         ("graph_offset", C.POINTER(_I)), ("edge_offset", C.POINTER(_I)),
         ("pos", C.POINTER(_D)), ("species", C.POINTER(_U8)),
         ("edge_dst", C.POINTER(_I)), ("edge_src", C.POINTER(_I)),
-        ("dataset_id", C.POINTER(_U8)),
+        ("dataset_id", C.POINTER(_U8)), ("edge_shift", C.POINTER(_D)),
     ]
 
 
@@ -150,6 +150,27 @@ class Oracle:
         self.lib.ho_init_block(C.byref(_chyper(h)), seed, which, _p(out, _D))
         return out
 
+    def build_edges_pbc(self, n_atoms, pos, cells, cutoff):
+        """Periodic neighbour list (builder's FP64 oracle): returns
+        graph_offset, edge_offset, dst, src, img [E][3], shift [E][3]."""
+        L = self.lib
+        L.ho_build_edges_pbc.restype = C.c_long
+        L.ho_build_edges_pbc.argtypes = [C.c_int, C.POINTER(_I), C.POINTER(_D), C.POINTER(_D), C.c_double] + \
+            [C.POINTER(_I)] * 5 + [C.POINTER(_D)]
+        n = np.ascontiguousarray(n_atoms, np.int32)
+        p = np.ascontiguousarray(pos, np.float64).reshape(-1)
+        cl = np.ascontiguousarray(cells, np.float64).reshape(-1)
+        G = len(n)
+        E = L.ho_build_edges_pbc(G, _p(n, _I), _p(p, _D), _p(cl, _D), cutoff, None, None, None, None, None, None)
+        if E < 0:
+            raise ValueError("pbc: empty graph" if E == -1 else "pbc: image range exceeded")
+        go, eo = np.zeros(G + 1, np.int32), np.zeros(G + 1, np.int32)
+        dst, src = np.zeros(max(E, 1), np.int32), np.zeros(max(E, 1), np.int32)
+        img, sh = np.zeros((max(E, 1), 3), np.int32), np.zeros((max(E, 1), 3), np.float64)
+        L.ho_build_edges_pbc(G, _p(n, _I), _p(p, _D), _p(cl, _D), cutoff, _p(go, _I), _p(eo, _I), _p(dst, _I),
+                             _p(src, _I), _p(img, _I), _p(sh, _D))
+        return go, eo, dst[:E], src[:E], img[:E], sh[:E]
+
     def build_edges(self, n_atoms, pos, cutoff, species=None):
         n = np.ascontiguousarray(n_atoms, np.int32)
         pos = np.ascontiguousarray(pos, np.float64).reshape(-1)
@@ -171,9 +192,11 @@ class Oracle:
             dst=np.ascontiguousarray(b["edge_dst"], np.int32), src=np.ascontiguousarray(b["edge_src"], np.int32),
             ds=np.ascontiguousarray(b["dsid"], np.uint8),
         )
+        if b.get("edge_shift") is not None:
+            keep["sh"] = np.ascontiguousarray(b["edge_shift"], np.float64).reshape(-1)
         cb = _CBatch(len(keep["ds"]), len(keep["sp"]), len(keep["dst"]), _p(keep["go"], _I), _p(keep["eo"], _I),
                      _p(keep["pos"], _D), _p(keep["sp"], _U8), _p(keep["dst"], _I), _p(keep["src"], _I),
-                     _p(keep["ds"], _U8))
+                     _p(keep["ds"], _U8), _p(keep["sh"], _D) if "sh" in keep else None)
         return cb, keep
 
     @staticmethod

@@ -92,6 +92,8 @@ SIGNATURES = {
     "hmtl_get_grad": (C.c_int, [_P, C.c_int, _FP]),
     "hmtl_batch_upload": (C.c_int, [_P, C.POINTER(CSamples), _P]),
     "hmtl_pool_add": (C.c_int, [_P, C.POINTER(CSamples), _IP]),
+    "hmtl_batch_upload_pbc": (C.c_int, [_P, C.POINTER(CSamples), C.POINTER(C.c_double), _P]),
+    "hmtl_batch_edge_images": (C.c_int, [_P, _IP]),
     "hmtl_pool_bind": (C.c_int, [_P, C.c_int, _P]),
     "hmtl_build_batch": (C.c_int, [_P, _P]),
     "hmtl_batch_edges": (C.c_int, [_P, _IP, _IP, _IP, _IP]),

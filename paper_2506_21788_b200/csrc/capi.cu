@@ -41,7 +41,7 @@ int check_hdr(Ctx& c) {
 }
 
 // pack AtomisticSamples into the batch arena format (common.cuh: arena_layout)
-int pack(Ctx& c, const hmtl_samples* s, uint8_t* dst, size_t cap, size_t* bytes) {
+int pack(Ctx& c, const hmtl_samples* s, uint8_t* dst, size_t cap, size_t* bytes, bool pbc = false) {
   if (!s || s->G <= 0 || s->N <= 0) return fail(HMTL_ERR_CONTRACT, "model: empty batch rejected");
   if (s->G > c.Gc || s->N > c.Nc) return fail(HMTL_ERR_CONTRACT, "batch exceeds context capacity (graphs/nodes)");
   const ArenaLayout al = arena_layout(s->G, s->N);
@@ -57,7 +57,8 @@ int pack(Ctx& c, const hmtl_samples* s, uint8_t* dst, size_t cap, size_t* bytes)
                                          " (head not owned by this rank)");
   }
   if (n_sum != s->N) return fail(HMTL_ERR_CONTRACT, "samples: sum(n_atoms) != N");
-  if (bound > c.Ec) return fail(HMTL_ERR_CONTRACT, "batch may exceed the context's edge capacity");
+  // (periodic images can exceed n(n-1): that bound is checked on the device, kErrEdgeOverflow)
+  if (!pbc && bound > c.Ec) return fail(HMTL_ERR_CONTRACT, "batch may exceed the context's edge capacity");
   int* hdr = reinterpret_cast<int*>(dst);
   hdr[0] = s->G;
   hdr[1] = s->N;
@@ -84,11 +85,13 @@ void free_ctx(Ctx& c) {
                   c.species, c.gslot, c.gperm, c.gnode_base, c.gedge_base, c.node_perm, c.edge_perm, c.hs, c.P,
                   c.z2, c.agg, c.vz1, c.pooled, c.ez, c.energy, c.Qf, c.zf, c.s, c.forces, c.dE, c.dF,
                   c.dagg, c.dhb, c.dvz1b, c.dzAb, c.dzBb, c.Sb, c.fzA, c.fzB, c.ds, c.dpooled, c.edA, c.edB,
-                  c.scratch, c.partial, c.partial_w, c.partial_w2, c.bimg, c.a1, c.af0, c.sf0, c.bimg_all, c.d_bjobs};
+                  c.scratch, c.partial, c.partial_w, c.partial_w2, c.cells, c.eimg, c.pbc_meta, c.pbc_bins,
+                  c.pbc_order, c.pbc_acoord, c.pbc_w2, c.bimg, c.a1, c.af0, c.sf0, c.bimg_all, c.d_bjobs};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto* p : c.pool) cudaFree(p);
   if (c.h_arena) cudaFreeHost(c.h_arena);
+  if (c.h_cells) cudaFreeHost(c.h_cells);
   if (c.step_exec) cudaGraphExecDestroy(c.step_exec);
   if (c.prof_exec) cudaGraphExecDestroy(c.prof_exec);
   comm_destroy(c.comm);
@@ -247,6 +250,13 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   A(&c.pos32, N);
   A(&c.geo, E);
   A(&c.dist, E);
+  A(&c.cells, G * 9);
+  A(&c.eimg, E);
+  A(&c.pbc_meta, G);
+  A(&c.pbc_bins, G * 65);
+  A(&c.pbc_order, N);
+  A(&c.pbc_acoord, N);
+  A(&c.pbc_w2, N);
   A(&c.species, N);
   A(&c.gslot, G);
   A(&c.gperm, G);
@@ -450,6 +460,7 @@ int hmtl_checkpoint_load(hmtl_ctx* h, const char* path) {
 
 int hmtl_batch_upload(hmtl_ctx* h, const hmtl_samples* s, void* stream) {
   Ctx& c = h->c;
+  c.pbc = false;
   cudaSetDevice(c.device);
   cudaStream_t st = pick(c, stream);
   // the pinned staging buffer may still be read by a previous async copy
@@ -457,6 +468,39 @@ int hmtl_batch_upload(hmtl_ctx* h, const hmtl_samples* s, void* stream) {
   size_t bytes = 0;
   if (int rc = pack(c, s, c.h_arena, c.h_arena_cap, &bytes)) return rc;
   HMTL_CUDA(cudaMemcpyAsync(c.arena, c.h_arena, bytes, cudaMemcpyHostToDevice, st));
+  return 0;
+}
+
+int hmtl_batch_upload_pbc(hmtl_ctx* h, const hmtl_samples* s, const double* cells, void* stream) {
+  Ctx& c = h->c;
+  if (!cells) return fail(HMTL_ERR_CONTRACT, "pbc: null cell array");
+  cudaSetDevice(c.device);
+  cudaStream_t st = pick(c, stream);
+  HMTL_CUDA(cudaStreamSynchronize(st));  // the pinned staging buffers may still be read
+  size_t bytes = 0;
+  if (int rc = pack(c, s, c.h_arena, c.h_arena_cap, &bytes, true)) return rc;
+  if (!c.h_cells) HMTL_CUDA(cudaMallocHost(&c.h_cells, size_t(c.Gc) * 9 * sizeof(double)));
+  std::memcpy(c.h_cells, cells, size_t(s->G) * 9 * sizeof(double));
+  HMTL_CUDA(cudaMemcpyAsync(c.arena, c.h_arena, bytes, cudaMemcpyHostToDevice, st));
+  HMTL_CUDA(cudaMemcpyAsync(c.cells, c.h_cells, size_t(s->G) * 9 * sizeof(double), cudaMemcpyHostToDevice, st));
+  c.pbc = true;
+  return 0;
+}
+
+int hmtl_batch_edge_images(hmtl_ctx* h, int* img) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  HMTL_CUDA(cudaDeviceSynchronize());
+  if (int rc = check_hdr(c)) return rc;
+  DevHdr hd;
+  HMTL_CUDA(cudaMemcpy(&hd, c.hdr, sizeof hd, cudaMemcpyDeviceToHost));
+  std::vector<int> key(hd.E > 0 ? hd.E : 1, 2184);  // 2184 = image (0, 0, 0)
+  if (c.pbc && hd.E > 0) HMTL_CUDA(cudaMemcpy(key.data(), c.eimg, size_t(hd.E) * 4, cudaMemcpyDeviceToHost));
+  for (int e = 0; e < hd.E; ++e) {
+    img[3 * e] = (key[e] >> 8) - 8;
+    img[3 * e + 1] = ((key[e] >> 4) & 15) - 8;
+    img[3 * e + 2] = (key[e] & 15) - 8;
+  }
   return 0;
 }
 
@@ -579,7 +623,7 @@ int hmtl_train_step(hmtl_ctx* h, const hmtl_train_cfg* cfg, void* stream) {
     HMTL_CUDA(cudaGetLastError());
     return 0;
   }
-  if (c.step_exec && std::memcmp(&c.graph_cfg, cfg, sizeof *cfg) != 0) {
+  if (c.step_exec && (std::memcmp(&c.graph_cfg, cfg, sizeof *cfg) != 0 || c.graph_pbc != c.pbc)) {
     cudaGraphExecDestroy(c.step_exec);
     c.step_exec = nullptr;
   }
@@ -613,6 +657,7 @@ int hmtl_train_step(hmtl_ctx* h, const hmtl_train_cfg* cfg, void* stream) {
     if (rc) return rc;
     if (e != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("graph capture: ") + cudaGetErrorString(e));
     c.step_kernels = count_kernel_nodes(g);
+    c.graph_pbc = c.pbc;
     HMTL_CUDA(cudaGraphInstantiate(&c.step_exec, g, 0));
     cudaGraphDestroy(g);
     c.graph_cfg = *cfg;

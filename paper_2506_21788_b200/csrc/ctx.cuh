@@ -67,6 +67,13 @@ struct Ctx {
   float4 *pos32 = nullptr, *geo = nullptr;  // geo = (dx, dy, dz, d2) per edge, FP32
   float* dist = nullptr;
   uint8_t* species = nullptr;
+  // periodic cells: lattice [G][3][3] of the bound batch, per-edge
+  // image key, cell-list scratch; `pbc` selects the periodic neighbour list
+  double* cells = nullptr;
+  double* h_cells = nullptr;  // pinned staging
+  int *eimg = nullptr, *pbc_meta = nullptr, *pbc_bins = nullptr, *pbc_order = nullptr, *pbc_acoord = nullptr,
+      *pbc_w2 = nullptr;
+  bool pbc = false, graph_pbc = false;
   int *gslot = nullptr, *gperm = nullptr, *gnode_base = nullptr, *gedge_base = nullptr;
   int *node_perm = nullptr, *edge_perm = nullptr;
 
@@ -163,6 +170,8 @@ struct Ctx {
 // launchers (stream-ordered; sizes come from the device header)
 void launch_prep(Ctx& c, cudaStream_t st);      // arena -> node/graph tables, routing
 void launch_nbr(Ctx& c, cudaStream_t st);       // neighbour list, CSR, rev, edge offsets
+void launch_nbr_pbc(Ctx& c, cudaStream_t st);   // ... with periodic images (cell list)
+void launch_route(Ctx& c, cudaStream_t st);     // head routing + head-sorted permutations
 void launch_forward(Ctx& c, cudaStream_t st);   // ModelT::forward
 void launch_loss(Ctx& c, float w_e, float w_f, cudaStream_t st);
 void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync = false);  // ModelT::backward (upstreams in c.dE/c.dF)

@@ -9,6 +9,8 @@
 // in ascending-src order directly -- no sort, bit-exact edge set.  Graphs are
 // small (<= a few hundred atoms) so the per-graph all-pairs tile is the
 // cheapest exact search; rows of different graphs never interact.
+#include <cmath>
+
 #include "ctx.cuh"
 
 namespace hmtl_b200 {
@@ -295,6 +297,7 @@ void launch_prep(Ctx& c, cudaStream_t st) {
 }
 
 void launch_nbr(Ctx& c, cudaStream_t st) {
+  if (c.pbc) return launch_nbr_pbc(c, st), launch_route(c, st);
   const int warps_blocks = grid_for((long long)c.Nc * 32, 256, c.sm_count * 16);
   {
     Prof pr(c, "nbr.count", st);
@@ -314,6 +317,11 @@ void launch_nbr(Ctx& c, cudaStream_t st) {
     kl(rev_kernel, grid_for(c.Ec, 256, c.sm_count * 8), 256, 0, st, c.hdr, c.row_ptr, c.edge_src, c.edge_dst, c.rev,
                                                                      c.Ec);
   }
+  launch_route(c, st);
+}
+
+// head routing + head-sorted permutations (shared by both neighbour lists)
+void launch_route(Ctx& c, cudaStream_t st) {
   {
     Prof pr(c, "route", st);
     kl(route_kernel, 1, 1024, 0, st, c.hdr, c.gslot, c.graph_offset, c.edge_offset, c.gperm, c.gnode_base,
@@ -325,6 +333,283 @@ void launch_nbr(Ctx& c, cudaStream_t st) {
     kl(perm_kernel, grid_for(m, 256, c.sm_count * 8), 256, 0, st, c.hdr, c.node_graph, c.graph_offset, c.edge_offset,
                                                                    c.edge_dst, c.gnode_base, c.gedge_base, c.node_perm,
                                                                    c.edge_perm);
+  }
+}
+
+}  // namespace hmtl_b200
+
+// ============================================================================
+// Periodic cells (the reference has no PBC -- parity against
+// the builder's FP64 brute force, oracle ho_build_edges_pbc).  Cell list per
+// structure: fractional coordinates f = x A^-1 (A rows = lattice vectors),
+// nb_k = clamp(floor(width_k / rc), 1, 4) bins per axis (width = perpendicular
+// cell width), stencil of r_k bins each way (r_k >= ceil(rc / bin width), + a
+// rounding margin); a stencil bin b + o maps to wrapped bin b' and cell image
+// s.  Every (j, image) is visited once; the FP64 test is the oracle's,
+// ((xi - xj) - S)^2 with S = (n1 a1 + n2 a2) + n3 a3 per component.  Rows come
+// out sorted by (src, image key) after a per-warp bitonic sort in shared memory.
+namespace hmtl_b200 {
+namespace {
+
+constexpr int kPbcMaxDeg = 512;  // per-row sort buffer (cfg4-class crystals: <= ~200)
+constexpr int kPbcMaxImg = 7;    // |n_k| bound of the packed image key
+
+__device__ __forceinline__ int img_key(int n1, int n2, int n3) { return (n1 + 8) * 256 + (n2 + 8) * 16 + (n3 + 8); }
+__device__ __forceinline__ void img_of(int key, int& n1, int& n2, int& n3) {
+  n1 = (key >> 8) - 8, n2 = ((key >> 4) & 15) - 8, n3 = (key & 15) - 8;
+}
+__device__ __forceinline__ void lat_shift(const double* A, int n1, int n2, int n3, double* S) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    S[k] = __dadd_rn(__dadd_rn(__dmul_rn(double(n1), A[k]), __dmul_rn(double(n2), A[3 + k])), __dmul_rn(double(n3), A[6 + k]));
+}
+__device__ __forceinline__ bool within_pbc(const double* __restrict__ pos, int i, int j, const double* S, double rc2) {
+  const double dx = __dsub_rn(__dsub_rn(pos[3 * i], pos[3 * j]), S[0]);
+  const double dy = __dsub_rn(__dsub_rn(pos[3 * i + 1], pos[3 * j + 1]), S[1]);
+  const double dz = __dsub_rn(__dsub_rn(pos[3 * i + 2], pos[3 * j + 2]), S[2]);
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)) <= rc2;
+}
+
+// CTA per structure: geometry of the cell, per-atom wrap + bin, counting sort into bins
+// acoord[i] = bin coords (4 bits each) | (w0 + 128) << 12 | (w1 + 128) << 20; w2[i] = wrap 3
+__global__ void pbc_bin_kernel(const uint8_t* __restrict__ arena, const DevHdr* hdr, const int* __restrict__ go,
+                               const double* __restrict__ cells, double rc, int* __restrict__ meta,
+                               int* __restrict__ bin_start, int* __restrict__ order, int* __restrict__ acoord,
+                               int* __restrict__ w2) {
+  pdl_wait();
+  __shared__ double c[3][3];
+  __shared__ double invV;
+  __shared__ int nb[3], cnt[64], cur[64];
+  const int G = hdr->G, N = hdr->N;
+  const double* pos = reinterpret_cast<const double*>(arena + arena_layout(G, N).pos);
+  for (int g = blockIdx.x; g < G; g += gridDim.x) {
+    const double* A = cells + 9 * size_t(g);
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < 3; ++k) {
+        const int u = (k + 1) % 3, v = (k + 2) % 3;
+        c[k][0] = A[3 * u + 1] * A[3 * v + 2] - A[3 * u + 2] * A[3 * v + 1];
+        c[k][1] = A[3 * u + 2] * A[3 * v + 0] - A[3 * u + 0] * A[3 * v + 2];
+        c[k][2] = A[3 * u + 0] * A[3 * v + 1] - A[3 * u + 1] * A[3 * v + 0];
+      }
+      const double V = A[0] * c[0][0] + A[1] * c[0][1] + A[2] * c[0][2];
+      invV = 1.0 / V;
+      int packed = 0;
+      for (int k = 0; k < 3; ++k) {
+        const double width = fabs(V) / sqrt(c[k][0] * c[k][0] + c[k][1] * c[k][1] + c[k][2] * c[k][2]);
+        int n = int(width / rc);
+        n = n < 1 ? 1 : (n > 4 ? 4 : n);
+        int r = int(rc / (width / n) * (1.0 + 1e-9)) + 1;  // >= ceil(rc / bin width), rounding margin
+        r = r > 15 ? 15 : r;
+        nb[k] = n;
+        packed |= (n << (4 * k)) | (r << (12 + 4 * k));
+      }
+      meta[g] = packed;
+    }
+    if (threadIdx.x < 64) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int a0 = go[g], a1 = go[g + 1];
+    for (int i = a0 + threadIdx.x; i < a1; i += blockDim.x) {
+      int b[3], w[3];
+      for (int k = 0; k < 3; ++k) {
+        const double f = (pos[3 * i] * c[k][0] + pos[3 * i + 1] * c[k][1] + pos[3 * i + 2] * c[k][2]) * invV;
+        const double fl = floor(f);
+        w[k] = int(fl);
+        const int bb = int((f - fl) * nb[k]);
+        b[k] = bb < 0 ? 0 : (bb >= nb[k] ? nb[k] - 1 : bb);
+      }
+      acoord[i] = b[0] | (b[1] << 4) | (b[2] << 8) | ((w[0] + 128) << 12) | ((w[1] + 128) << 20);
+      w2[i] = w[2];
+      atomicAdd(&cnt[(b[0] * nb[1] + b[1]) * nb[2] + b[2]], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int s = a0;
+      const int nbin = nb[0] * nb[1] * nb[2];
+      for (int q = 0; q < nbin; ++q) bin_start[65 * g + q] = s, cur[q] = s, s += cnt[q];
+      bin_start[65 * g + nbin] = s;
+    }
+    __syncthreads();
+    for (int i = a0 + threadIdx.x; i < a1; i += blockDim.x) {  // order within a bin is irrelevant:
+      const int p = acoord[i];                                   // every row is sorted afterwards
+      order[atomicAdd(&cur[((p & 15) * nb[1] + ((p >> 4) & 15)) * nb[2] + ((p >> 8) & 15)], 1)] = i;
+    }
+    __syncthreads();
+  }
+}
+
+// warp per destination atom: visit the stencil; pass 1 counts, pass 2 collects,
+// sorts and writes its row
+template <bool kWrite>
+__global__ void __launch_bounds__(256) pbc_row_kernel(const uint8_t* __restrict__ arena, DevHdr* hdr,
+                                                      const int* __restrict__ node_graph,
+                                                      const double* __restrict__ cells, const int* __restrict__ meta,
+                                                      const int* __restrict__ bin_start, const int* __restrict__ order,
+                                                      const int* __restrict__ acoord, const int* __restrict__ w2,
+                                                      const int* __restrict__ row_ptr,
+                                                      const float4* __restrict__ pos32, int* __restrict__ deg,
+                                                      int* __restrict__ edge_src, int* __restrict__ edge_dst,
+                                                      int* __restrict__ eimg, float4* __restrict__ geo,
+                                                      float* __restrict__ dist, double rc2, long long Ec) {
+  pdl_wait();
+  __shared__ long long buf[8][kPbcMaxDeg];
+  const int N = hdr->N, G = hdr->G;
+  if (kWrite && hdr->E > Ec) return;
+  const double* pos = reinterpret_cast<const double*>(arena + arena_layout(G, N).pos);
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  long long* kb = buf[wl];
+  auto wrap_of = [&](int a) {
+    const int pa = acoord[a];
+    return make_int3(((pa >> 12) & 255) - 128, ((pa >> 20) & 255) - 128, w2[a]);
+  };
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += (gridDim.x * blockDim.x) >> 5) {
+    const int g = node_graph[i];
+    const int mt = meta[g];
+    const int nb0 = mt & 15, nb1 = (mt >> 4) & 15, nb2 = (mt >> 8) & 15;
+    const int r0 = (mt >> 12) & 15, r1 = (mt >> 16) & 15, r2 = (mt >> 20) & 15;
+    const double* A = cells + 9 * size_t(g);
+    const int pi = acoord[i];
+    const int bi0 = pi & 15, bi1 = (pi >> 4) & 15, bi2 = (pi >> 8) & 15;
+    const int3 wi = wrap_of(i);
+    int cntr = 0;
+    bool overflow = false;
+    for (int o0 = -r0; o0 <= r0; ++o0)
+      for (int o1 = -r1; o1 <= r1; ++o1)
+        for (int o2 = -r2; o2 <= r2; ++o2) {
+          const int b0 = bi0 + o0, b1 = bi1 + o1, b2 = bi2 + o2;
+          const int s0 = b0 >= 0 ? b0 / nb0 : -((nb0 - 1 - b0) / nb0);  // floor division
+          const int s1 = b1 >= 0 ? b1 / nb1 : -((nb1 - 1 - b1) / nb1);
+          const int s2 = b2 >= 0 ? b2 / nb2 : -((nb2 - 1 - b2) / nb2);
+          const int q = ((b0 - s0 * nb0) * nb1 + (b1 - s1 * nb1)) * nb2 + (b2 - s2 * nb2);
+          const int t0 = bin_start[65 * g + q], t1 = bin_start[65 * g + q + 1];
+          for (int t = t0; t < t1; t += 32) {
+            bool hit = false;
+            long long key = 0;
+            if (t + lane < t1) {
+              const int j = order[t + lane];
+              const int3 wj = wrap_of(j);
+              const int n1 = s0 - wj.x + wi.x, n2 = s1 - wj.y + wi.y, n3 = s2 - wj.z + wi.z;
+              if (!(j == i && n1 == 0 && n2 == 0 && n3 == 0)) {
+                double S[3];
+                lat_shift(A, n1, n2, n3, S);
+                hit = within_pbc(pos, i, j, S, rc2);
+                if (hit && (abs(n1) > kPbcMaxImg || abs(n2) > kPbcMaxImg || abs(n3) > kPbcMaxImg)) {
+                  atomicOr(&hdr->err, kErrEdgeOverflow);
+                  hit = false;
+                }
+                key = (long long)j * 4096 + img_key(n1, n2, n3);
+              }
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, hit);
+            if (kWrite && hit) {
+              const int at = cntr + __popc(m & ((1u << lane) - 1));
+              if (at < kPbcMaxDeg) kb[at] = key;
+              else overflow = true;
+            }
+            cntr += __popc(m);
+          }
+        }
+    if (!kWrite) {
+      if (lane == 0) deg[i] = cntr;
+      continue;
+    }
+    if (__any_sync(0xffffffffu, overflow) || cntr > kPbcMaxDeg) {
+      if (lane == 0) atomicOr(&hdr->err, kErrEdgeOverflow);
+      continue;
+    }
+    // bitonic sort of the row's keys (ascending (src, image))
+    int P2 = 1;
+    while (P2 < cntr) P2 <<= 1;
+    for (int t = cntr + lane; t < P2; t += 32) kb[t] = 0x7FFFFFFFFFFFFFFFLL;
+    __syncwarp();
+    for (int k = 2; k <= P2; k <<= 1)
+      for (int jj = k >> 1; jj > 0; jj >>= 1) {
+        for (int t = lane; t < P2; t += 32) {
+          const int u = t ^ jj;
+          if (u > t) {
+            const long long a = kb[t], b = kb[u];
+            if (((t & k) == 0) == (a > b)) kb[t] = b, kb[u] = a;
+          }
+        }
+        __syncwarp();
+      }
+    const int base = row_ptr[i];
+    const float4 p4 = pos32[i];
+    for (int t = lane; t < cntr; t += 32) {
+      const long long key = kb[t];
+      const int j = int(key >> 12), ik = int(key & 4095);
+      int n1, n2, n3;
+      img_of(ik, n1, n2, n3);
+      double S[3];
+      lat_shift(A, n1, n2, n3, S);
+      const float4 q4 = pos32[j];
+      // FP32 geometry as the open-boundary path (pos32 differences), minus the FP32 image shift
+      const float dx = __fsub_rn(__fsub_rn(p4.x, q4.x), float(S[0]));
+      const float dy = __fsub_rn(__fsub_rn(p4.y, q4.y), float(S[1]));
+      const float dz = __fsub_rn(__fsub_rn(p4.z, q4.z), float(S[2]));
+      const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+      const int e = base + t;
+      edge_src[e] = j;
+      edge_dst[e] = i;
+      eimg[e] = ik;
+      geo[e] = make_float4(dx, dy, dz, d2);
+      dist[e] = __fsqrt_rn(d2);
+    }
+    __syncwarp();
+  }
+}
+
+// reverse of (i, j, n) is (j, i, -n): binary search of row j on the (src, image) key
+__global__ void pbc_rev_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const int* __restrict__ edge_src,
+                               const int* __restrict__ edge_dst, const int* __restrict__ eimg, int* __restrict__ rev,
+                               long long Ec) {
+  pdl_wait();
+  const int E = hdr->E;
+  if (E > Ec) return;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    const int i = edge_dst[e], j = edge_src[e];
+    int n1, n2, n3;
+    img_of(eimg[e], n1, n2, n3);
+    const long long want = (long long)i * 4096 + img_key(-n1, -n2, -n3);
+    int lo = row_ptr[j], hi = row_ptr[j + 1];
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((long long)edge_src[mid] * 4096 + eimg[mid] < want) lo = mid + 1;
+      else hi = mid;
+    }
+    rev[e] = lo;
+  }
+}
+
+}  // namespace
+
+void launch_nbr_pbc(Ctx& c, cudaStream_t st) {
+  const int warps_blocks = grid_for((long long)c.Nc * 32, 256, c.sm_count * 16);
+  const double rc = std::sqrt(c.rc2);
+  {
+    Prof pr(c, "nbr.pbc_bin", st);
+    kl(pbc_bin_kernel, grid_for(c.Gc, 1, c.sm_count * 4), 256, 0, st, c.arena, c.hdr, c.graph_offset, c.cells, rc,
+       c.pbc_meta, c.pbc_bins, c.pbc_order, c.pbc_acoord, c.pbc_w2);
+  }
+  {
+    Prof pr(c, "nbr.count", st);
+    kl(pbc_row_kernel<false>, warps_blocks, 256, 0, st, c.arena, c.hdr, c.node_graph, c.cells, c.pbc_meta,
+       c.pbc_bins, c.pbc_order, c.pbc_acoord, c.pbc_w2, c.row_ptr, c.pos32, c.deg, c.edge_src, c.edge_dst, c.eimg, c.geo,
+       c.dist, c.rc2, c.Ec);
+  }
+  {
+    Prof pr(c, "nbr.scan", st);
+    kl(scan_kernel, 1, 1024, 0, st, c.hdr, c.deg, c.row_ptr, c.graph_offset, c.edge_offset, c.Ec);
+  }
+  {
+    Prof pr(c, "nbr.write", st);
+    kl(pbc_row_kernel<true>, warps_blocks, 256, 0, st, c.arena, c.hdr, c.node_graph, c.cells, c.pbc_meta,
+       c.pbc_bins, c.pbc_order, c.pbc_acoord, c.pbc_w2, c.row_ptr, c.pos32, c.deg, c.edge_src, c.edge_dst, c.eimg, c.geo,
+       c.dist, c.rc2, c.Ec);
+  }
+  {
+    Prof pr(c, "nbr.rev", st);
+    kl(pbc_rev_kernel, grid_for(c.Ec, 256, c.sm_count * 8), 256, 0, st, c.hdr, c.row_ptr, c.edge_src, c.edge_dst,
+       c.eimg, c.rev, c.Ec);
   }
 }
 

@@ -282,6 +282,23 @@ class ModelT:
         check(lib().hmtl_batch_upload(self._ctx, C.byref(s.as_c()), stream))
         self._G, self._N = s.G, s.N
 
+    def upload_pbc(self, s: Samples, cells, stream=None) -> None:
+        """Periodic batch: samples + lattice cells[G][3][3] (rows a1..a3)."""
+        self.reserve(s)
+        self._keep = s
+        self._cells = np.ascontiguousarray(cells, np.float64).reshape(s.G, 9)
+        check(lib().hmtl_batch_upload_pbc(self._ctx, C.byref(s.as_c()),
+                                          self._cells.ctypes.data_as(C.POINTER(C.c_double)), stream))
+        self._G, self._N = s.G, s.N
+
+    def edge_images(self) -> np.ndarray:
+        """[E][3] lattice image of every edge's source (zeros for open boundaries)."""
+        E = C.c_int()
+        check(lib().hmtl_batch_edges(self._ctx, C.byref(E), None, None, None))
+        img = np.zeros((max(E.value, 1), 3), np.int32)
+        check(lib().hmtl_batch_edge_images(self._ctx, _ip(img)))
+        return img[:E.value]
+
     def build_batch(self, s: Samples) -> GraphBatch:
         """build_batch<float> on the device; returns the edge view (syncs)."""
         self.upload(s)
