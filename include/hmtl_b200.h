@@ -238,8 +238,9 @@ int hmtl_debug_fetch(hmtl_ctx* ctx, const char* name, int layer, float* host, si
 
 /* Benchmark instrumentation: when enabled, every kernel scope records CUDA
  * events on its stream.  Eager steps record plain events; graph steps
- * (use_graph) replay a separately captured copy of the step graph whose
- * scopes are external event-record nodes, synchronising after each replay.
+ * (use_graph) replay a separately captured, single-stream copy of the step
+ * graph whose scopes are external event-record nodes, synchronising after
+ * each replay (per-scope times without side-stream contention).
  * report (syncs) writes a JSON array [{"name","calls","ms"}] and resets. */
 int hmtl_profile_enable(hmtl_ctx* ctx, int on);
 int hmtl_profile_report(hmtl_ctx* ctx, char* json, size_t cap);

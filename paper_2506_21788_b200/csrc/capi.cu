@@ -636,9 +636,14 @@ int hmtl_train_step(hmtl_ctx* h, const hmtl_train_cfg* cfg, void* stream) {
     if (!c.prof_exec) {
       for (auto& r : c.prof) r.used = 0;
       cudaGraph_t g;
+      // serialised copy of the step: every scope's time is its own kernels' time,
+      // not stretched by concurrent side-stream kernels competing for SMs
+      const bool ms = c.multi_stream;
+      c.multi_stream = false;
       HMTL_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       int rc = enqueue_step(c, *cfg, st);
       cudaError_t e = cudaStreamEndCapture(st, &g);
+      c.multi_stream = ms;
       if (rc) return rc;
       if (e != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("graph capture: ") + cudaGetErrorString(e));
       HMTL_CUDA(cudaGraphInstantiate(&c.prof_exec, g, 0));
