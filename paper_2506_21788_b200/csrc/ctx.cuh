@@ -106,6 +106,7 @@ struct Ctx {
   size_t ev_i = 0;
   bool multi_stream = true;
   bool fuse_chain = true;  // node-row GEMM chains in one launch (chain.cuh)
+  bool fuse_a1 = true;     // a1 = silu(z1) gathered in the message GEMM's producer (no edge_a1 launch)
   long long* chain_stamps = nullptr;
   int chain_dbg = 0;
   bool dbg_skip_wgrad = false;  // timing experiments: skip weight gradients (wrong training)  // engine tuning: phase timestamps of the last chain launch

@@ -103,8 +103,10 @@ struct MsgProb {
   __device__ RC rctx(int, int e) const { return a1out ? RC{0, 0, 0.f} : RC{dst[e], src[e], geo[e].w}; }
   __device__ float4 a4c(int, int e, const RC& r, int k) const {
     if (a1out) return ld4(a1out + size_t(e) * H + k);  // a1 materialised by edge_a1_kernel
-    return silu4(pre4(ld4(P + size_t(r.d) * 2 * H + k), ld4(P + size_t(r.s) * 2 * H + H + k), r.w, ld4(wd + k),
-                      ld4(b1 + k)));
+    const float4 v = silu4(pre4(ld4(P + size_t(r.d) * 2 * H + k), ld4(P + size_t(r.s) * 2 * H + H + k), r.w,
+                                ld4(wd + k), ld4(b1 + k)));
+    if (a1w) st4(a1w + size_t(e) * H + k, v);  // gathered in the producer; kept for the eW2 gradient
+    return v;
   }
   __device__ void epi4c(int, int e, const RC&, int n, float4 acc) const {
     st4(z2 + size_t(e) * H + n, add4(acc, ld4(b2 + n)));
@@ -122,6 +124,7 @@ struct MsgProb {
   const float4* geo;
   float* z2;
   float* a1out;
+  float* a1w = nullptr;
   __device__ float a(int, int e, int k) const { return silu(z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, k)); }
   __device__ float b(int, int k, int n) const { return W2[size_t(k) * H + n]; }
   __device__ void epi(int, int e, int n, float acc) const { z2[size_t(e) * H + n] = acc + b2[n]; }
@@ -780,7 +783,8 @@ void launch_forward(Ctx& c, cudaStream_t st) {
       ab(q, c.Nc, 1, st, sm, c);
     }
     p_done = false;
-    if (c.store_a1) {
+    const bool fuse_a1 = c.store_a1 && c.fuse_a1 && c.bimg_ready;  // a1 gathered in Msg's producer
+    if (c.store_a1 && !fuse_a1) {
       Prof pr(c, "fwd.edge_act", st);
       kl(edge_a1_kernel, gridn((c.Ec + kEwU - 1) / kEwU * 32, 256, sm * 16), 256, 0, st,
           c.hdr, P, c.edge_dst, c.edge_src, c.geo, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
@@ -789,7 +793,8 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     {
       MsgProb q{edge_rows(c), H, H, H, P, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
                 c.params + c.shared_off(p + "edge.W2"), c.params + c.shared_off(p + "edge.b2"), c.edge_dst,
-                c.edge_src, c.geo, z2, c.store_a1 ? c.a1 + size_t(l) * EH : nullptr};
+                c.edge_src, c.geo, z2, (c.store_a1 && !fuse_a1) ? c.a1 + size_t(l) * EH : nullptr,
+                fuse_a1 ? c.a1 + size_t(l) * EH : nullptr};
       ab(q, c.Ec, 1, st, sm, c);
     }
     {
