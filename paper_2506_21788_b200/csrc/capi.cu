@@ -85,7 +85,7 @@ void free_ctx(Ctx& c) {
                   c.species, c.gslot, c.gperm, c.gnode_base, c.gedge_base, c.node_perm, c.edge_perm, c.hs, c.P,
                   c.z2, c.agg, c.vz1, c.pooled, c.ez, c.energy, c.Qf, c.zf, c.s, c.forces, c.dE, c.dF,
                   c.dagg, c.dhb, c.dvz1b, c.dzAb, c.dzBb, c.Sb, c.fzA, c.fzB, c.ds, c.dpooled, c.edA, c.edB,
-                  c.scratch, c.partial, c.partial_w, c.partial_w2, c.cells, c.eimg, c.pbc_meta, c.pbc_bins,
+                  c.scratch, c.partial, c.partial_w, c.partial_w2, c.loss_terms, c.cells, c.eimg, c.pbc_meta, c.pbc_bins,
                   c.pbc_order, c.pbc_acoord, c.pbc_w2, c.bimg, c.a1, c.af0, c.sf0, c.bimg_all, c.d_bjobs};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -227,7 +227,7 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   }
   if (const char* e = std::getenv("HMTL_SINGLE_STREAM")) c.multi_stream = e[0] == '0';
   if (const char* e = std::getenv("HMTL_NO_CHAIN")) c.fuse_chain = e[0] == '0';
-  if (const char* e = std::getenv("HMTL_NO_FUSE_A1")) c.fuse_a1 = e[0] == '0';
+  if (const char* e = std::getenv("HMTL_TC_GRID")) c.tc_grid_mult = std::atoi(e);
   if (const char* e = std::getenv("HMTL_NO_COMM_OVERLAP")) c.overlap_comm = e[0] == '0';
   if (std::getenv("HMTL_CHAIN_STAMPS")) A(&c.chain_stamps, size_t(4096) * 32);
   if (const char* e = std::getenv("HMTL_CHAIN_DBG")) c.chain_dbg = std::atoi(e);
@@ -289,6 +289,7 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   A(&c.fzB, E * W);
   A(&c.ds, E);
   A(&c.dpooled, G * H);
+  A(&c.loss_terms, G);
   A(&c.edA, G * W);
   A(&c.edB, G * W);
   A(&c.scratch, E * std::max(H, W));

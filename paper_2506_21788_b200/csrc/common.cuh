@@ -20,7 +20,7 @@ struct DevHdr {
   int seg_node[kMaxSlots + 1];   // head-sorted node segments
   int seg_edge[kMaxSlots + 1];   // head-sorted edge segments
   int step;                      // AdamW step counter
-  int pad;
+  int loss_done;  // CTAs of the loss kernel finished (the last one reduces and resets it)
   double loss;
 };
 

@@ -84,6 +84,7 @@ struct Ctx {
   // backward workspace
   float *dE = nullptr, *dF = nullptr, *dagg = nullptr;
   float *ds = nullptr, *dpooled = nullptr;
+  double* loss_terms = nullptr;  // [G] per-graph loss terms
   float *edA = nullptr, *edB = nullptr, *scratch = nullptr;
   float* partial = nullptr;    // split-K partials of kernels on the main stream
   float* partial_w = nullptr;   // ... and of the weight-gradient streams
@@ -106,7 +107,7 @@ struct Ctx {
   size_t ev_i = 0;
   bool multi_stream = true;
   bool fuse_chain = true;  // node-row GEMM chains in one launch (chain.cuh)
-  bool fuse_a1 = true;     // a1 = silu(z1) gathered in the message GEMM's producer (no edge_a1 launch)
+  int tc_grid_mult = 1;    // row GEMM grid cap in SMs (0: one CTA per tile)
   long long* chain_stamps = nullptr;
   int chain_dbg = 0;
   bool dbg_skip_wgrad = false;  // timing experiments: skip weight gradients (wrong training)  // engine tuning: phase timestamps of the last chain launch

@@ -47,6 +47,7 @@ __device__ __forceinline__ float zf0_of(const float* __restrict__ Qf, int W, int
 }
 
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 f4z() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
 __device__ __forceinline__ float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
 __device__ __forceinline__ float4 silu4(float4 a) { return make_float4(silu(a.x), silu(a.y), silu(a.z), silu(a.w)); }
@@ -103,10 +104,8 @@ struct MsgProb {
   __device__ RC rctx(int, int e) const { return a1out ? RC{0, 0, 0.f} : RC{dst[e], src[e], geo[e].w}; }
   __device__ float4 a4c(int, int e, const RC& r, int k) const {
     if (a1out) return ld4(a1out + size_t(e) * H + k);  // a1 materialised by edge_a1_kernel
-    const float4 v = silu4(pre4(ld4(P + size_t(r.d) * 2 * H + k), ld4(P + size_t(r.s) * 2 * H + H + k), r.w,
-                                ld4(wd + k), ld4(b1 + k)));
-    if (a1w) st4(a1w + size_t(e) * H + k, v);  // gathered in the producer; kept for the eW2 gradient
-    return v;
+    return silu4(pre4(ld4(P + size_t(r.d) * 2 * H + k), ld4(P + size_t(r.s) * 2 * H + H + k), r.w, ld4(wd + k),
+                      ld4(b1 + k)));
   }
   __device__ void epi4c(int, int e, const RC&, int n, float4 acc) const {
     st4(z2 + size_t(e) * H + n, add4(acc, ld4(b2 + n)));
@@ -124,7 +123,6 @@ struct MsgProb {
   const float4* geo;
   float* z2;
   float* a1out;
-  float* a1w = nullptr;
   __device__ float a(int, int e, int k) const { return silu(z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, k)); }
   __device__ float b(int, int k, int n) const { return W2[size_t(k) * H + n]; }
   __device__ void epi(int, int e, int n, float acc) const { z2[size_t(e) * H + n] = acc + b2[n]; }
@@ -310,19 +308,26 @@ __global__ void pool_kernel(const DevHdr* hdr, const int* __restrict__ graph_off
 __global__ void forces_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const float4* __restrict__ geo,
                               const float* __restrict__ s, float* __restrict__ F) {
   pdl_wait();
-  const int N = hdr->N;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+  // warp per node: lane l sums edges l, l+32, ... of the row, then a fixed xor tree
+  // (the association depends only on the degree: deterministic)
+  const int N = hdr->N, lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += (gridDim.x * blockDim.x) >> 5) {
+    const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
     float fx = 0.f, fy = 0.f, fz = 0.f;
-    for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+    for (int e = e0 + lane; e < e1; e += 32) {
       const float4 g = geo[e];
       const float se = s[e];
       fx += g.x * se;
       fy += g.y * se;
       fz += g.z * se;
     }
-    F[3 * i] = fx;
-    F[3 * i + 1] = fy;
-    F[3 * i + 2] = fz;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      fx += __shfl_xor_sync(0xffffffffu, fx, o);
+      fy += __shfl_xor_sync(0xffffffffu, fy, o);
+      fz += __shfl_xor_sync(0xffffffffu, fz, o);
+    }
+    if (lane == 0) F[3 * i] = fx, F[3 * i + 1] = fy, F[3 * i + 2] = fz;
   }
 }
 
@@ -371,10 +376,30 @@ struct AuxOf<P, std::void_t<typename P::Aux>> {
   static constexpr bool has = true;
 };
 
+// optional two-phase A producer: raw4 issues the loads (kept in the producer's
+// prefetch registers), fin4 does the math (and any side store) when the chunk is
+// written to shared memory -- so gathered/elementwise A operands keep their loads
+// in flight across the previous chunk's stores
+template <class P, class = void>
+struct RawOf {
+  using type = float4;
+  static constexpr bool has = false;
+};
+template <class P>
+struct RawOf<P, std::void_t<typename P::Raw>> {
+  using type = typename P::Raw;
+  static constexpr bool has = true;
+};
+template <class P, class = void>
+struct HasAuxC : std::false_type {};
+template <class P>
+struct HasAuxC<P, std::void_t<decltype(&P::epi_auxc)>> : std::true_type {};
+
 template <class P>
 struct TcRow {
   using RC = typename RCOf<P>::type;
   using Aux = typename AuxOf<P>::type;
+  using Raw = typename RawOf<P>::type;
   RowSet rows;
   int K, Ncols;
   const float* bimg;
@@ -389,12 +414,23 @@ struct TcRow {
     else if constexpr (HasA4<P>::value) return p.a4(seg, row, k);
     else return make_float4(p.a(seg, row, k), p.a(seg, row, k + 1), p.a(seg, row, k + 2), p.a(seg, row, k + 3));
   }
-  __device__ __forceinline__ Aux epi_aux(int seg, int row, const RC&, int n) const {
-    if constexpr (AuxOf<P>::has) return p.epi_aux(seg, row, n);
+  __device__ __forceinline__ Raw raw4(int seg, int row, const RC& rc, int k) const {
+    if constexpr (RawOf<P>::has) return p.raw4(seg, row, rc, k);
+    else return a4(seg, row, rc, k);
+  }
+  __device__ __forceinline__ float4 fin4(int seg, int row, const RC& rc, int k, const Raw& r) const {
+    if constexpr (RawOf<P>::has) return p.fin4(seg, row, rc, k, r);
+    else return r;
+  }
+  __device__ __forceinline__ Aux epi_aux(int seg, int row, const RC& rc, int n) const {
+    if constexpr (HasAuxC<P>::value) return p.epi_auxc(seg, row, rc, n);
+    else if constexpr (AuxOf<P>::has) return p.epi_aux(seg, row, n);
     else return Aux{};
   }
   __device__ __forceinline__ void epi4(int seg, int row, const RC& rc, int n, float4 acc, const Aux& ax) const {
-    if constexpr (AuxOf<P>::has) {
+    if constexpr (HasAuxC<P>::value) {
+      p.epi4ac(seg, row, rc, n, acc, ax);
+    } else if constexpr (AuxOf<P>::has) {
       p.epi4a(seg, row, n, acc, ax);
     } else if constexpr (RCOf<P>::has) {
       p.epi4c(seg, row, rc, n, acc);
@@ -507,7 +543,9 @@ void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& 
     while (Nt > 32 && mtiles * (p.Ncols / Nt) * 2 <= sm && (Nt / 2) % 32 == 0) Nt /= 2;
     const tc::RowPlan plan = tc::row_plan(p.K, Nt);
     set_smem(tc::tc_row_kernel<TcRow<P>>, plan.smem);
-    kl(tc::tc_row_kernel<TcRow<P>>, gridn(mtiles * (p.Ncols / Nt), 1, sm), tc::kRowThreads, plan.smem, st, q, plan);
+    const int cap_ctas = c.tc_grid_mult > 0 ? sm * c.tc_grid_mult : (1 << 30);  // persistent when capped
+    kl(tc::tc_row_kernel<TcRow<P>>, gridn(mtiles * (p.Ncols / Nt), 1, cap_ctas), tc::kRowThreads, plan.smem, st, q,
+       plan);
     return;
   }
   const long long tiles = ((rows_cap + 63) / 64 + nseg) * ((p.Ncols + 63) / 64);
@@ -679,26 +717,50 @@ __global__ void __launch_bounds__(256) edge_bwd_prep_kernel(const DevHdr* hdr, c
   }
 }
 // force head layer 0: af0 = silu(zf0), sf0 = silu'(zf0) with the edge's head weights
-__global__ void edge_af0_kernel(const DevHdr* hdr, const float* __restrict__ Qf, const int* __restrict__ dst,
-                                const int* __restrict__ src, const float* __restrict__ dist,
-                                const int* __restrict__ node_graph, const int* __restrict__ gslot,
-                                const float* __restrict__ heads, size_t PH, size_t off_wd, size_t off_b0,
-                                float* __restrict__ af0, float* __restrict__ sf0, int W) {
+// (warp per group of kEwU edges, lane = float4 column group, as edge_a1_kernel)
+__global__ void __launch_bounds__(256) edge_af0_kernel(const DevHdr* hdr, const float* __restrict__ Qf,
+                                                       const int* __restrict__ dst, const int* __restrict__ src,
+                                                       const float* __restrict__ dist,
+                                                       const int* __restrict__ node_graph,
+                                                       const int* __restrict__ gslot, const float* __restrict__ heads,
+                                                       size_t PH, size_t off_wd, size_t off_b0,
+                                                       float* __restrict__ af0, float* __restrict__ sf0, int W) {
   pdl_wait();
-  const int q = W / 4;
-  const long long total = (long long)hdr->E * q;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int e = int(t / q), c = int(t % q) * 4;
-    const int d = dst[e], s = src[e];
-    const float* hb = heads + size_t(gslot[node_graph[d]]) * PH;
-    const float4 z = pre4(ld4(Qf + size_t(d) * W + c), ld4(Qf + size_t(s) * W + c), dist[e], ldu4(hb + off_wd + c),
-                          ldu4(hb + off_b0 + c));
-    const size_t o = size_t(e) * W + c;
-    st4(af0 + o, silu4(z));
-    st4(sf0 + o, sgrad4(z));
+  const int E = hdr->E, lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int eb = gw * kEwU; eb < E; eb += nw * kEwU) {
+    int d[kEwU], sl[kEwU];
+#pragma unroll
+    for (int u = 0; u < kEwU; ++u) {
+      const int e = min(eb + u, E - 1);
+      d[u] = dst[e];
+      sl[u] = gslot[node_graph[d[u]]];
+    }
+    for (int c = lane * 4; c < W; c += 128) {
+      float4 qa[kEwU], qb[kEwU], w[kEwU], b[kEwU];
+      float r[kEwU];
+#pragma unroll
+      for (int u = 0; u < kEwU; ++u) {
+        const int e = min(eb + u, E - 1);
+        const float* hb = heads + size_t(sl[u]) * PH;
+        qa[u] = ld4(Qf + size_t(d[u]) * W + c);
+        qb[u] = ld4(Qf + size_t(src[e]) * W + c);
+        w[u] = ldu4(hb + off_wd + c);
+        b[u] = ldu4(hb + off_b0 + c);
+        r[u] = dist[e];
+      }
+#pragma unroll
+      for (int u = 0; u < kEwU; ++u)
+        if (eb + u < E) {
+          const float4 z = pre4(qa[u], qb[u], r[u], w[u], b[u]);
+          const size_t o = size_t(eb + u) * W + c;
+          st4(af0 + o, silu4(z));
+          st4(sf0 + o, sgrad4(z));
+        }
+    }
   }
 }
-}
+}  // namespace
 
 namespace {
 // force MLP output layer (width 1; mlp_forward_'s last layer, hmtl/model.hpp:282-306):
@@ -783,8 +845,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
       ab(q, c.Nc, 1, st, sm, c);
     }
     p_done = false;
-    const bool fuse_a1 = c.store_a1 && c.fuse_a1 && c.bimg_ready;  // a1 gathered in Msg's producer
-    if (c.store_a1 && !fuse_a1) {
+    if (c.store_a1) {
       Prof pr(c, "fwd.edge_act", st);
       kl(edge_a1_kernel, gridn((c.Ec + kEwU - 1) / kEwU * 32, 256, sm * 16), 256, 0, st,
           c.hdr, P, c.edge_dst, c.edge_src, c.geo, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
@@ -793,8 +854,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     {
       MsgProb q{edge_rows(c), H, H, H, P, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
                 c.params + c.shared_off(p + "edge.W2"), c.params + c.shared_off(p + "edge.b2"), c.edge_dst,
-                c.edge_src, c.geo, z2, (c.store_a1 && !fuse_a1) ? c.a1 + size_t(l) * EH : nullptr,
-                fuse_a1 ? c.a1 + size_t(l) * EH : nullptr};
+                c.edge_src, c.geo, z2, c.store_a1 ? c.a1 + size_t(l) * EH : nullptr};
       ab(q, c.Ec, 1, st, sm, c);
     }
     {
@@ -848,7 +908,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
   const size_t wf0 = c.head_off("force.W0");
   if (c.store_af0) {
     Prof pr(c, "fwd.force_act", st);
-    kl(edge_af0_kernel, gridn((long long)c.Ec * W / 4, 256, sm * 16), 256, 0, st,
+    kl(edge_af0_kernel, gridn((c.Ec + kEwU - 1) / kEwU * 32, 256, sm * 16), 256, 0, st,
         c.hdr, c.Qf, c.edge_dst, c.edge_src, c.dist, c.node_graph, c.gslot, c.head_params(), c.PH,
         wf0 + size_t(H) * W, c.head_off("force.b0"), c.af0, c.sf0, W);
   }
@@ -872,7 +932,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
   }
   {
     Prof pr(c, "fwd.forces_segsum", st);
-    kl(forces_kernel, gridn(c.Nc, 256, sm * 8), 256, 0, st, c.hdr, c.row_ptr, c.geo, c.s, c.forces);
+    kl(forces_kernel, gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st, c.hdr, c.row_ptr, c.geo, c.s, c.forces);
   }
   c.dep(se, st);
   {
@@ -884,20 +944,20 @@ void launch_forward(Ctx& c, cudaStream_t st) {
 // ----------------------------------------------------------------- loss
 // SPEC.md:383-391; one CTA, warp per graph, fixed-order reductions.
 namespace {
-__global__ void __launch_bounds__(1024) loss_kernel(DevHdr* hdr, const uint8_t* __restrict__ arena,
-                                                    const int* __restrict__ graph_offset,
-                                                    const float* __restrict__ energy, const float* __restrict__ F,
-                                                    float* __restrict__ dE, float* __restrict__ dF, float w_e,
-                                                    float w_f) {
+__global__ void __launch_bounds__(256) loss_kernel(DevHdr* hdr, const uint8_t* __restrict__ arena,
+                                                   const int* __restrict__ graph_offset,
+                                                   const float* __restrict__ energy, const float* __restrict__ F,
+                                                   float* __restrict__ dE, float* __restrict__ dF, double* terms,
+                                                   float w_e, float w_f) {
   pdl_wait();
-  __shared__ double wsum[32];
+  __shared__ bool last;
   const int G = hdr->G, N = hdr->N;
   const ArenaLayout al = arena_layout(G, N);
   const double* le = reinterpret_cast<const double*>(arena + al.le);
   const double* lf = reinterpret_cast<const double*>(arena + al.lf);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double acc = 0.0;
-  for (int g = wid; g < G; g += 32) {
+  const int lane = threadIdx.x & 31;
+  // warp per graph: w_E (E^ - E)^2 + w_F mean_i |F^_i - F_i|^2 and the upstreams
+  for (int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < G; g += (gridDim.x * blockDim.x) >> 5) {
     const int lo = graph_offset[g], hi = graph_offset[g + 1];
     const double n = double(hi - lo);
     double fe = 0.0;
@@ -910,16 +970,27 @@ __global__ void __launch_bounds__(1024) loss_kernel(DevHdr* hdr, const uint8_t* 
     for (int o = 16; o; o >>= 1) fe += __shfl_xor_sync(0xffffffffu, fe, o);
     const double de = double(energy[g]) - le[g];
     if (lane == 0) {
-      acc += double(w_e) * de * de + double(w_f) * fe / n;
+      terms[g] = double(w_e) * de * de + double(w_f) * fe / n;
       dE[g] = float(2.0 * double(w_e) * de / double(G));
     }
   }
-  if (lane == 0) wsum[wid] = acc;
+  // the last CTA to finish sums the per-graph terms in graph order (deterministic)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&hdr->loss_done, 1) == int(gridDim.x) - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double part[256];
+  double a = 0.0;
+  for (int g = threadIdx.x; g < G; g += blockDim.x) a += terms[g];
+  part[threadIdx.x] = a;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < 32; ++w) s += wsum[w];
-    hdr->loss = s / double(G);
+    double t = 0.0;
+    for (int i = 0; i < int(blockDim.x); ++i) t += part[i];
+    hdr->loss = t / double(G);
+    hdr->loss_done = 0;
   }
 }
 }  // namespace
@@ -927,7 +998,8 @@ __global__ void __launch_bounds__(1024) loss_kernel(DevHdr* hdr, const uint8_t* 
 void launch_loss(Ctx& c, float w_e, float w_f, cudaStream_t st) {
   {
     Prof pr(c, "loss", st);
-    kl(loss_kernel, 1, 1024, 0, st, c.hdr, c.arena, c.graph_offset, c.energy, c.forces, c.dE, c.dF, w_e, w_f);
+    kl(loss_kernel, gridn((long long)c.Gc * 32, 256, c.sm_count * 2), 256, 0, st, c.hdr, c.arena, c.graph_offset, c.energy, c.forces,
+       c.dE, c.dF, c.loss_terms, w_e, w_f);
   }
 }
 
@@ -1376,7 +1448,6 @@ __global__ void seg2_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, 
 
 // ---- vectorised CSR segment sums: warp per node, lane = float4 column group,
 // 4 independent edge loads in flight; ascending-edge accumulation per column.
-__device__ __forceinline__ float4 f4z() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
 // agg_i = sum_{e in row i} silu(z2_e).  Warp per node, lane = float4 column
 // group; edges in batches of 8 with all 8 row loads issued before the
@@ -1801,15 +1872,6 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
       }
     }
     node_done = false;
-    c.dep(st, sw);  // dh (input), dvz1 ready
-    {
-      L2Prob q{node_rows(c), H + 1, H, H, vz1, dh, c.grads + c.shared_off(p + "node.W2")};
-      atb(q, c, c.nsplit_node, sw, c.Nc);
-    }
-    {
-      L3Prob q{node_rows(c), 2 * H + 1, H, H, h, agg, dvz1, c.grads + c.shared_off(p + "node.W1")};
-      atb(q, c, c.nsplit_node, sw, c.Nc);
-    }
     const bool mat = c.store_a1;  // tensor-core shapes: gathered operands materialised elementwise
     if (mat) {
       Prof pr(c, "bwd.edge_act", st);
@@ -1819,16 +1881,27 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
       Prof pr(c, "bwd.edge_dz2_gather", st);
       kl(dz2_kernel, gridn(EH, 256, sm * 16), 256, 0, st, c.hdr, c.edge_dst, c.dagg, z2, dzA, H);
     }
-    c.dep(st, sw);  // dz2 ready
-    {
-      L6Prob q{edge_rows(c), H + 1, H, H, P, wd, b1, dzA, c.edge_dst, c.edge_src, c.geo,
-               c.grads + c.shared_off(p + "edge.W2"), mat ? c.a1 + size_t(l) * EH : nullptr, nullptr, z2};
-      atb(q, c, c.nsplit_edge, sw, c.Ec);
-    }
     {
       L7Prob q{edge_rows(c), H, H, H, dzA, c.params + c.shared_off(p + "edge.W2"), P, wd, b1, c.edge_dst,
                c.edge_src, c.geo, dzB, nullptr, z2, mat ? c.scratch : nullptr};
       ab(q, c.Ec, 1, st, sm, c);
+    }
+    // this layer's node and eW2 weight gradients fork only now: they then overlap the
+    // segment sums and the 28-CTA node chain instead of competing with the persistent
+    // edge GEMM for SMs
+    c.dep(st, sw);
+    {
+      L2Prob q{node_rows(c), H + 1, H, H, vz1, dh, c.grads + c.shared_off(p + "node.W2")};
+      atb(q, c, c.nsplit_node, sw, c.Nc);
+    }
+    {
+      L3Prob q{node_rows(c), 2 * H + 1, H, H, h, agg, dvz1, c.grads + c.shared_off(p + "node.W1")};
+      atb(q, c, c.nsplit_node, sw, c.Nc);
+    }
+    {
+      L6Prob q{edge_rows(c), H + 1, H, H, P, wd, b1, dzA, c.edge_dst, c.edge_src, c.geo,
+               c.grads + c.shared_off(p + "edge.W2"), mat ? c.a1 + size_t(l) * EH : nullptr, nullptr, z2};
+      atb(q, c, c.nsplit_edge, sw, c.Ec);
     }
     segsum2(c, dzB, H, 0, Sl, st);
     c.dep(st, sw2);  // dz1 and its segment sums ready (second weight-gradient stream)

@@ -24,6 +24,9 @@ struct StRow {
   __device__ float4 a4(int, int r, const RC&, int k) const {
     return *reinterpret_cast<const float4*>(X + size_t(r) * K + k);
   }
+  using Raw = float4;
+  __device__ float4 raw4(int s, int r, const RC& rc, int k) const { return a4(s, r, rc, k); }
+  __device__ float4 fin4(int, int, const RC&, int, const float4& x) const { return x; }
   __device__ void epi4(int, int r, const RC&, int n, float4 acc, const Aux&) const {
     *reinterpret_cast<float4*>(C + size_t(r) * Ncols + n) = acc;
   }

@@ -194,7 +194,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // overlapping tile t's epilogue with tile t+1's MMAs.
 // P must provide: RowSet rows; int K, Ncols; const float* bimg; size_t bimg_seg;
 //   typename P::RC rctx(int seg, int row) const;                    // per-row gather context
-//   float4 a4(int seg, int row, const RC&, int k) const;           // A(row, k..k+3)
+//   typename P::Raw raw4(int seg, int row, const RC&, int k) const; // loads of A(row, k..k+3)
+//   float4 fin4(int seg, int row, const RC&, int k, const Raw&) const;  // -> A(row, k..k+3)
 //   typename P::Aux epi_aux(int seg, int row, const RC&, int n) const;  // prefetched epilogue inputs
 //   void epi4(int seg, int row, const RC&, int n, float4 acc, const Aux&) const;  // C(row, n..n+3)
 constexpr int kMaxStages = 4;
@@ -287,6 +288,10 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   mt_seg[p.rows.nseg] = total_m;
   const int ntn = p.Ncols / Nt;
   const int total = total_m * ntn;
+  // contiguous tile range per CTA: consecutive tiles share a head segment / column block,
+  // so the resident B image is reloaded only at segment boundaries
+  const int t_beg = int((long long)blockIdx.x * total / gridDim.x);
+  const int t_end = int((long long)(blockIdx.x + 1) * total / gridDim.x);
   const int nchunks = p.K / KC;
   const uint32_t b_slice = uint32_t(Nt) * 128;  // bytes of one (chunk, hi|lo) B slice
   tc_fence_before();
@@ -305,7 +310,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
       typename P::RC rc[kRowIt];
     };
     auto set_tile = [&](Cur& u) {
-      if (u.t >= total) return;
+      if (u.t >= t_end) return;
       const int tm = u.t / ntn;
       u.n0 = (u.t % ntn) * Nt;
       int seg = 0;
@@ -319,25 +324,33 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
       }
     };
     auto succ = [&](Cur& u) {
-      if (u.t >= total) return;
+      if (u.t >= t_end) return;
       if (++u.c == nchunks) {
         u.c = 0;
-        u.t += gridDim.x;
+        u.t += 1;
         set_tile(u);
       }
     };
-    auto load = [&](const Cur& u, float4 (&x)[kRowIt][2]) {
+    using Raw = typename P::Raw;  // raw A loads of a chunk; P::fin4 turns them into A values
+    auto load = [&](const Cur& u, Raw (&x)[kRowIt][2]) {
       const bool skip = g_tc_debug & 1;
 #pragma unroll
       for (int it = 0; it < kRowIt; ++it)
 #pragma unroll
         for (int h = 0; h < 2; ++h)
-          x[it][h] = (u.rows[it] >= 0 && !skip) ? p.a4(u.seg, u.rows[it], u.rc[it], u.c * KC + 8 * kq + 4 * h)
-                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (u.rows[it] >= 0 && !skip) x[it][h] = p.raw4(u.seg, u.rows[it], u.rc[it], u.c * KC + 8 * kq + 4 * h);
     };
     int stage = 0;
     uint32_t phase = 0;
-    auto fill = [&](const Cur& u, const float4 (&x)[kRowIt][2]) {
+    auto fill = [&](const Cur& u, const Raw (&x)[kRowIt][2]) {
+      float4 v[kRowIt][2];
+#pragma unroll
+      for (int it = 0; it < kRowIt; ++it)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          v[it][h] = (u.rows[it] >= 0 && !(g_tc_debug & 1))
+                         ? p.fin4(u.seg, u.rows[it], u.rc[it], u.c * KC + 8 * kq + 4 * h, x[it][h])
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
       mbar_wait(&empty[stage], phase ^ 1);
       float* a_hi = reinterpret_cast<float*>(stages + stage * SB);
       float* a_lo = a_hi + 128 * KC;
@@ -345,7 +358,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
 #pragma unroll
         for (int it = 0; it < kRowIt; ++it)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) put4(a_hi, a_lo, 2 * kq + h, warp * 8 * kRowIt + it * 8 + rsub, x[it][h]);
+          for (int h = 0; h < 2; ++h) put4(a_hi, a_lo, 2 * kq + h, warp * 8 * kRowIt + it * 8 + rsub, v[it][h]);
       fence_proxy_async();
       if (!plan.resident && tid == 0) {  // this stage's B slice rides on the same barrier
         mbar_expect_tx(&full[stage], 2 * b_slice);
@@ -359,24 +372,24 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
       if (++stage == kStages) stage = 0, phase ^= 1;
     };
     Cur A, B;
-    A.t = blockIdx.x;
+    A.t = t_beg;
     A.c = 0;
     set_tile(A);
     B = A;
     succ(B);
-    float4 xa[kRowIt][2], xb[kRowIt][2];
-    if (A.t < total) load(A, xa);
-    if (B.t < total) load(B, xb);
-    while (A.t < total) {  // two chunks in registers: one being stored, the next in flight
+    Raw xa[kRowIt][2], xb[kRowIt][2];
+    if (A.t < t_end) load(A, xa);
+    if (B.t < t_end) load(B, xb);
+    while (A.t < t_end) {  // two chunks in registers: one being stored, the next in flight
       fill(A, xa);
       A = B;
       succ(A);
-      if (A.t < total) load(A, xa);
-      if (B.t >= total) break;
+      if (A.t < t_end) load(A, xa);
+      if (B.t >= t_end) break;
       fill(B, xb);
       B = A;
       succ(B);
-      if (B.t < total) load(B, xb);
+      if (B.t < t_end) load(B, xb);
     }
   } else if (warp == kMmaWarp) {  // --------------------------------- MMA issuer + resident B
     int stage = 0;
@@ -385,7 +398,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
     uint32_t aphase = 0;
     int res_key = -1;
     const uint32_t idesc = idesc_tf32(Nt);
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = t_beg; t < t_end; ++t) {
       if (plan.resident) {
         const int tm = t / ntn, n0 = (t % ntn) * Nt;
         int seg = 0;
@@ -437,7 +450,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
     uint32_t aphase = 0;
     float* slab = epi_smem + (warp - kEpiWarp0) * 32 * 32;  // 32 rows x 32 cols, 16 B chunks XOR-swizzled
     const int nslab = (Nt + 31) / 32;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = t_beg; t < t_end; ++t) {
       const int tm = t / ntn, n0 = (t % ntn) * Nt;
       int seg = 0;
       while (tm >= mt_seg[seg + 1]) ++seg;

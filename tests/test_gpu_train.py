@@ -140,7 +140,6 @@ def test_fused_graph_steps_match_oracle(H, L, monkeypatch):
     m.close()
     monkeypatch.setenv("HMTL_NO_CHAIN", "1")
     monkeypatch.setenv("HMTL_SINGLE_STREAM", "1")
-    monkeypatch.setenv("HMTL_NO_FUSE_A1", "1")
     u = P.ModelT(hp, 7, range(5), caps=caps)
     for b in batches:
         u.train_step(b, cfg)
