@@ -311,9 +311,10 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   if (const char* e = std::getenv("HMTL_NO_TC")) c.use_tc = e[0] == '0';
   c.store_a1 = c.use_tc && H % 32 == 0;
   c.store_af0 = c.use_tc && W % 32 == 0 && H % 4 == 0;
+  c.store_sf0 = c.store_af0;  // (regathering silu'(zf0) from Qf in FDx's epilogue measured slower)
   A(&c.a1, c.store_a1 ? L * E * H : 1);
   A(&c.af0, c.store_af0 ? E * W : 1);
-  A(&c.sf0, c.store_af0 ? E * W : 1);
+  A(&c.sf0, c.store_sf0 ? E * W : 1);
   if (rc) {
     free_ctx(c);
     delete h;

@@ -147,8 +147,8 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
   uint64_t* bfull = bars + 8;               // [3] tx
   uint64_t* bempty = bars + 11;             // [3] MMA commit
   uint64_t* accd = bars + 14;               // [3] MMA commit: GEMM g complete
-  uint64_t* xrdy = bars + 17;               // [2] epilogue threads: X holds GEMM g+1's A
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
+  uint64_t* xrdy = bars + 17;               // [2][4] the 4 warps of a slab: X chunk c of GEMM g+1's A
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int H = p.H;
   uint32_t acc_off[3];
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
     for (int s = 0; s < kXSlots; ++s) mbar_init(&afull[s], kProdWarps * 32), mbar_init(&aempty[s], 1);
     for (int s = 0; s < kBSlots; ++s) mbar_init(&bfull[s], 1), mbar_init(&bempty[s], 1);
     for (int i = 0; i < 3; ++i) mbar_init(&accd[i], 1);
-    for (int i = 0; i < 2; ++i) mbar_init(&xrdy[i], kEpiWarps * 32);
+    for (int i = 0; i < 8; ++i) mbar_init(&xrdy[i], 4 * 32);
     fence_mbar_init();
   }
   tc_fence_before();
@@ -239,10 +239,6 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
     for (int gi = 0; gi < G; ++gi) {
       const Gemm& g = p.g[gi];
       const int nch = g.K / KC;
-      if (gi > 0) {
-        mbar_wait(&xrdy[gi - 1], 0);
-        tc_fence_after();
-      }
       if (lane == 0) CHAIN_STAMP(2 + 2 * gi);
       for (int n0 = 0; n0 < g.N; n0 += 128) {
         const int nr = g.N - n0 < 128 ? g.N - n0 : 128;
@@ -256,6 +252,9 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
               mbar_wait(&afull[xs], (c / kXSlots) & 1);
               tc_fence_after();
             }
+          } else if (n0 == 0) {  // chunk c of the chained operand, written slab by slab by
+            mbar_wait(&xrdy[(gi - 1) * 4 + c], 0);  // the previous epilogue: MMAs start early
+            tc_fence_after();
           }
           mbar_wait(&bfull[s], (q / kBSlots) & 1);
           tc_fence_after();
@@ -311,13 +310,13 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
           }
         }
         __syncwarp();
+        if (!last) {  // this warp's 32 rows of X chunk sl are written
+          fence_proxy_async();
+          tc_fence_before();
+          mbar_arrive(&xrdy[gi * 4 + sl]);
+        }
       }
       if (ew == 0 && lane == 0) CHAIN_STAMP(9 + 2 * gi);
-      if (!last) {
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(&xrdy[gi]);
-      }
     };
     phase(IC<R0>{}, IC<0>{});
     if constexpr (G > 1) phase(IC<R1>{}, IC<1>{});

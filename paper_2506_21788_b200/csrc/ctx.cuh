@@ -126,6 +126,9 @@ struct Ctx {
   int n_djobs = 0;
   bool store_a1 = false;  // forward producer materialises a1 = silu(z1) [L][E][H]
   bool store_af0 = false; // ... and silu(zf0) [E][W]
+  // silu'(zf0) [E][W] too only when the force output layer's backward needs it
+  // (head_depth 2); deeper heads regather it from the L2-resident Qf table
+  bool store_sf0 = false;
   float *a1 = nullptr, *af0 = nullptr, *sf0 = nullptr;
   int nsplit_node = 1, nsplit_edge = 1, nsplit_graph = 1;
 

@@ -755,7 +755,7 @@ __global__ void __launch_bounds__(256) edge_af0_kernel(const DevHdr* hdr, const 
           const float4 z = pre4(qa[u], qb[u], r[u], w[u], b[u]);
           const size_t o = size_t(eb + u) * W + c;
           st4(af0 + o, silu4(z));
-          st4(sf0 + o, sgrad4(z));
+          if (sf0) st4(sf0 + o, sgrad4(z));
         }
     }
   }
@@ -910,7 +910,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     Prof pr(c, "fwd.force_act", st);
     kl(edge_af0_kernel, gridn((c.Ec + kEwU - 1) / kEwU * 32, 256, sm * 16), 256, 0, st,
         c.hdr, c.Qf, c.edge_dst, c.edge_src, c.dist, c.node_graph, c.gslot, c.head_params(), c.PH,
-        wf0 + size_t(H) * W, c.head_off("force.b0"), c.af0, c.sf0, W);
+        wf0 + size_t(H) * W, c.head_off("force.b0"), c.af0, c.store_sf0 ? c.sf0 : nullptr, W);
   }
   for (int i = 1; i < D; ++i) {
     const int last = i == D - 1;
@@ -1086,15 +1086,22 @@ struct FDxProb {  // dz_{i-1} = (dz_i W_i^T) * silu'(z_{i-1})
     return (sf0 || layer != 1) ? RC{0, 0, 0.f} : RC{dst[e], src[e], dist[e]};
   }
   __device__ float4 a4c(int, int e, const RC&, int k) const { return ld4(dz + size_t(e) * ldz + k); }
-  __device__ void epi4c(int seg, int e, const RC& r, int n, float4 acc) const {
-    if (layer == 1 && sf0) {
-      st4(out + size_t(e) * W + n, mul4(acc, ld4(sf0 + size_t(e) * W + n)));
-      return;
-    }
+  // silu'(z_{i-1}) does not depend on the accumulator: prefetched by the epilogue (Aux)
+  struct Aux {
+    float4 v;
+  };
+  __device__ Aux epi_auxc(int seg, int e, const RC& r, int n) const {
+    if (layer == 1 && sf0) return Aux{ld4(sf0 + size_t(e) * W + n)};
     const float4 zp = layer == 1 ? pre4(ld4(Qf + size_t(r.d) * W + n), ld4(Qf + size_t(r.s) * W + n), r.dist,
                                         ldu4(Wd.at(seg) + n), ldu4(B0.at(seg) + n))
                                  : ld4(zf + size_t(layer - 2) * Ec * W + size_t(e) * W + n);
-    st4(out + size_t(e) * W + n, mul4(acc, sgrad4(zp)));
+    return Aux{sgrad4(zp)};
+  }
+  __device__ void epi4ac(int, int e, const RC&, int n, float4 acc, const Aux& a) const {
+    st4(out + size_t(e) * W + n, mul4(acc, a.v));
+  }
+  __device__ void epi4c(int seg, int e, const RC& r, int n, float4 acc) const {
+    epi4ac(seg, e, r, n, acc, epi_auxc(seg, e, r, n));
   }
   __device__ float4 a4(int, int e, int k) const { return ld4(dz + size_t(e) * ldz + k); }
   __device__ void epi4(int seg, int e, int n, float4 acc) const {
@@ -1811,7 +1818,7 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
       atb(gq, c, c.nsplit_edge, sw, c.Ec);
       FDxProb dq{edge_rows_by_head(c), out, W, H, W, i, c.Ec, c.Qf, c.zf, c.dist, dz, ldz, c.edge_dst, c.edge_src,
                  Wd, B0, HeadW{c.head_params(), c.PH, c.head_off("force.W" + std::to_string(i))}, nxt,
-                 c.store_af0 ? c.sf0 : nullptr};
+                 c.store_sf0 ? c.sf0 : nullptr};
       ab(dq, c.Ec, c.S, st, sm, c);
       dz = nxt;
       ldz = W;
