@@ -133,8 +133,18 @@ int enqueue_step(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st) {
     c.bjobs.clear();
     c.bimg_recording = true;
   }
+  // the previous step's AdamW left the tensor-core B images stale: rebuild them on a
+  // side stream while the batch preparation and neighbour list run (every graph replay
+  // does this; the images are needed from the first layer's GEMM on)
+  const bool images = c.bimg_ready && c.use_tc && !c.bimg_recording;
+  cudaStream_t sb = c.side(c.s_w, st);
+  if (images) {
+    c.dep(st, sb);
+    launch_bimg_all(c, sb);
+  }
   launch_prep(c, st);
   launch_nbr(c, st);
+  if (images) c.dep(sb, st);
   launch_forward(c, st);
   launch_loss(c, cfg.w_energy, cfg.w_force, st);
   launch_backward(c, st, true);  // with a communicator: bucketed allreduces overlap it
@@ -146,7 +156,16 @@ int enqueue_step(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st) {
     int rc = comm_sync_grads(c, st);
     if (rc) return rc;
   }
-  launch_adamw(c, cfg, st);
+  launch_adamw(c, cfg, st, /*defer_images=*/!c.bimg_recording);
+  return 0;
+}
+
+// standalone API calls after a train step: refresh the deferred B images first
+int fresh_images(Ctx& c, cudaStream_t st) {
+  if (c.bimg_stale) {
+    launch_bimg_all(c, st);
+    c.bimg_stale = false;
+  }
   return 0;
 }
 
@@ -558,6 +577,7 @@ int hmtl_batch_edges(hmtl_ctx* h, int* E, int* edge_dst, int* edge_src, int* edg
 int hmtl_forward(hmtl_ctx* h, void* stream) {
   Ctx& c = h->c;
   cudaSetDevice(c.device);
+  fresh_images(c, pick(c, stream));
   launch_forward(c, pick(c, stream));
   HMTL_CUDA(cudaGetLastError());
   return 0;
@@ -599,6 +619,7 @@ int hmtl_backward(hmtl_ctx* h, const float* dE, const float* dF, void* stream) {
   cudaSetDevice(c.device);
   cudaStream_t st = pick(c, stream);
   if ((dE == nullptr) != (dF == nullptr)) return fail(HMTL_ERR_CONTRACT, "model: upstream shape mismatch");
+  fresh_images(c, st);
   if (dE) {
     HMTL_CUDA(cudaMemcpyAsync(c.dE, dE, size_t(c.host_G) * 4, cudaMemcpyHostToDevice, st));
     HMTL_CUDA(cudaMemcpyAsync(c.dF, dF, size_t(c.host_N) * 12, cudaMemcpyHostToDevice, st));

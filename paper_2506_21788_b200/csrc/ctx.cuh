@@ -119,11 +119,13 @@ struct Ctx {
   std::vector<BDesc> bjobs;
   bool bimg_ready = false;
   bool bimg_recording = false;  // set by a train step before the images exist
+  bool bimg_stale = false;      // params updated by a train step's AdamW, images not yet rebuilt
   int bimg_idx = 0;
   float* bimg_all = nullptr;
   size_t bimg_all_cap = 0;
   BDesc* d_bjobs = nullptr;
   int n_djobs = 0;
+  int bimg_rows = 1;  // max (segments x K) over the recorded images: bimg_all grid.x
   bool store_a1 = false;  // forward producer materialises a1 = silu(z1) [L][E][H]
   bool store_af0 = false; // ... and silu(zf0) [E][W]
   // silu'(zf0) [E][W] too only when the force output layer's backward needs it
@@ -180,7 +182,7 @@ void launch_route(Ctx& c, cudaStream_t st);     // head routing + head-sorted pe
 void launch_forward(Ctx& c, cudaStream_t st);   // ModelT::forward
 void launch_loss(Ctx& c, float w_e, float w_f, cudaStream_t st);
 void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync = false);  // ModelT::backward (upstreams in c.dE/c.dF)
-void launch_adamw(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st);
+void launch_adamw(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st, bool defer_images = false);
 void launch_debug_z1(Ctx& c, int layer, float* out, cudaStream_t st);
 void launch_bimg_all(Ctx& c, cudaStream_t st);  // rebuild every recorded B image
 

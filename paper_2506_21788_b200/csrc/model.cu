@@ -488,15 +488,17 @@ struct TcRed {
 };
 
 // one launch builds every B image of the step: blockIdx.y = job
-__global__ void bimg_all_kernel(const BDesc* __restrict__ jobs) {
+// grid (blocks, jobs); elements walk the contiguous source dimension (coalesced
+// reads), 32-bit index math
+__global__ void __launch_bounds__(256) bimg_all_kernel(const BDesc* __restrict__ jobs) {
   pdl_wait();
   const BDesc J = jobs[blockIdx.y];
-  const int K = J.K, N = J.N;
-  const size_t total = size_t(J.nseg) * K * N;
+  const int K = J.K, N = J.N, KN = K * N;
+  const int total = J.nseg * KN;
   const bool kfast = J.sk == 1;  // walk the contiguous source dimension
-  for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < total; t += size_t(gridDim.x) * blockDim.x) {
-    const int seg = int(t / (size_t(K) * N));
-    const int rem = int(t % (size_t(K) * N));
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int seg = t / KN;
+    const int rem = t - seg * KN;
     const int k = kfast ? rem % K : rem / N, n = kfast ? rem / K : rem % N;
     int kk = k, nn = n;
     const float* b = J.base0;
@@ -505,7 +507,7 @@ __global__ void bimg_all_kernel(const BDesc* __restrict__ jobs) {
     const float x = b[size_t(seg) * J.seg_stride + size_t(kk) * J.sk + size_t(nn) * J.sn];
     const float h = tc::tf32_hi(x);
     const int ch = k / tc::KC, c16 = (k % tc::KC) / 4, q = k % 4;
-    float* o = J.out + size_t(seg) * 2 * K * N + size_t(ch) * 2 * tc::KC * N;
+    float* o = J.out + size_t(seg) * 2 * KN + size_t(ch) * 2 * tc::KC * N;
     const uint32_t off = tc::sw128(n, c16) / 4 + q;
     o[off] = h;
     o[size_t(tc::KC) * N + off] = x - h;
@@ -815,9 +817,11 @@ void launch_bimg_all(Ctx& c, cudaStream_t st) {
     cudaMalloc(&c.d_bjobs, c.bjobs.size() * sizeof(BDesc));
     cudaMemcpy(c.d_bjobs, c.bjobs.data(), c.bjobs.size() * sizeof(BDesc), cudaMemcpyHostToDevice);
     c.n_djobs = int(c.bjobs.size());
+    c.bimg_rows = 1;
+    for (auto& j : c.bjobs) c.bimg_rows = std::max(c.bimg_rows, j.K * j.N * j.nseg);  // elements
   }
   Prof pr(c, "bimg_all", st);
-  kl(bimg_all_kernel, dim3(16, c.n_djobs), 256, 0, st, c.d_bjobs);
+  kl(bimg_all_kernel, dim3((c.bimg_rows + 255) / 256, c.n_djobs), 256, 0, st, c.d_bjobs);
   c.bimg_ready = true;
   c.bimg_recording = false;
 }
@@ -2011,12 +2015,16 @@ __global__ void adamw_kernel(const DevHdr* hdr, float* __restrict__ p, const flo
 }
 }  // namespace
 
-void launch_adamw(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st) {
+void launch_adamw(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st, bool defer_images) {
   struct Rebuild {
     Ctx& c;
     cudaStream_t st;
-    ~Rebuild() { launch_bimg_all(c, st); }  // weights changed: refresh the B images (after the update)
-  } rebuild{c, st};
+    bool defer;
+    ~Rebuild() {  // weights changed: refresh the B images (after the update) -- or, inside a
+      if (defer && c.bimg_ready) c.bimg_stale = true;  // train step, at the start of the next
+      else launch_bimg_all(c, st);                     // step, overlapped with its batch prep
+    }
+  } rebuild{c, st, defer_images};
   kl(adam_tick, 1, 1, 0, st, c.hdr);
   {
     Prof pr(c, "adamw", st);
