@@ -1492,7 +1492,7 @@ __global__ void __launch_bounds__(256) agg4_kernel(const DevHdr* hdr, const int*
 // S[i] = [sum_{e in row i} x_e | sum_{e in row i} x_{rev(e)}] (or folded a + b).
 // The row's rev indices are read once per 32-edge window (one per lane) and
 // broadcast by shuffle; 4 edges per batch -> 8 row loads in flight per lane.
-constexpr int kSegU = 4;
+constexpr int kSegU = 8;
 __global__ void __launch_bounds__(256) seg2v_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr,
                                                     const int* __restrict__ rev, const float* __restrict__ x,
                                                     float* __restrict__ S, int C, int fold) {
