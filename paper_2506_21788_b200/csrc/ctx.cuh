@@ -107,7 +107,8 @@ struct Ctx {
   size_t ev_i = 0;
   bool multi_stream = true;
   bool fuse_chain = true;  // node-row GEMM chains in one launch (chain.cuh)
-  int tc_grid_mult = 1;    // row GEMM grid cap in SMs (0: one CTA per tile)
+  int tc_grid_mult = 1;
+  bool prefetch_l2 = true;  // L2 prefetch of re-read activations ahead of the critical path    // row GEMM grid cap in SMs (0: one CTA per tile)
   long long* chain_stamps = nullptr;
   int chain_dbg = 0;
   bool dbg_skip_wgrad = false;  // timing experiments: skip weight gradients (wrong training)  // engine tuning: phase timestamps of the last chain launch

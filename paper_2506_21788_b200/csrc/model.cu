@@ -1392,6 +1392,15 @@ struct L11Prob {  // dh2 += S_dst W1a^T + S_src W1b^T
 };
 
 // dh_i = dpooled_g * (1/n)  (first contribution; hmtl/model.hpp:517-524)
+// L2 prefetch of a tensor the critical path will read soon (it was written long
+// enough ago to have left L2): prefetch.global.L2 per 128 B line, no registers
+__global__ void l2_prefetch_kernel(const DevHdr* hdr, const float* __restrict__ x, int per_edge) {
+  pdl_wait();
+  const size_t bytes = size_t(hdr->E) * per_edge * sizeof(float);
+  const char* p = reinterpret_cast<const char*>(x);
+  for (size_t o = (blockIdx.x * size_t(blockDim.x) + threadIdx.x) * 128; o < bytes; o += size_t(gridDim.x) * blockDim.x * 128)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
+}
 __global__ void dh_pool_kernel(const DevHdr* hdr, const int* __restrict__ node_graph,
                                const int* __restrict__ graph_offset, const float* __restrict__ dpooled,
                                float* __restrict__ dh, int H) {
@@ -1760,6 +1769,13 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
   cudaStream_t sc = c.side(c.s_c, st);
   float* dhL = c.dhb + size_t(L) * NH;  // dL/dh_L, written by the heads
 
+  // silu'(zf0), written by the forward's force head long before, is re-read by the
+  // force-head dx GEMM on the critical path: pull it back into L2 from a side stream
+  if (c.store_sf0 && c.prefetch_l2) {
+    c.dep(st, sw2);
+    Prof pr(c, "bwd.l2_prefetch", sw2);
+    kl(l2_prefetch_kernel, sm * 4, 256, 0, sw2, static_cast<const DevHdr*>(c.hdr), static_cast<const float*>(c.sf0), W);
+  }
   // ---------------- energy heads (hmtl/model.hpp:512-524)
   c.dep(st, se);
   {

@@ -298,6 +298,8 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // ablation bits read once: a global load per chunk sat on the producer's critical path
+  const int dbg = g_tc_debug;
   pdl_wait();  // setup above overlaps the previous kernel's tail
 
   if (warp < kProdWarps) {  // ------------------------------------- producers
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
     };
     using Raw = typename P::Raw;  // raw A loads of a chunk; P::fin4 turns them into A values
     auto load = [&](const Cur& u, Raw (&x)[kRowIt][2]) {
-      const bool skip = g_tc_debug & 1;
+      const bool skip = dbg & 1;
 #pragma unroll
       for (int it = 0; it < kRowIt; ++it)
 #pragma unroll
@@ -348,13 +350,13 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
       for (int it = 0; it < kRowIt; ++it)
 #pragma unroll
         for (int h = 0; h < 2; ++h)
-          v[it][h] = (u.rows[it] >= 0 && !(g_tc_debug & 1))
+          v[it][h] = (u.rows[it] >= 0 && !(dbg & 1))
                          ? p.fin4(u.seg, u.rows[it], u.rc[it], u.c * KC + 8 * kq + 4 * h, x[it][h])
                          : make_float4(0.f, 0.f, 0.f, 0.f);
       mbar_wait(&empty[stage], phase ^ 1);
       float* a_hi = reinterpret_cast<float*>(stages + stage * SB);
       float* a_lo = a_hi + 128 * KC;
-      if (!(g_tc_debug & 1))
+      if (!(dbg & 1))
 #pragma unroll
         for (int it = 0; it < kRowIt; ++it)
 #pragma unroll
@@ -493,7 +495,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
         for (int it = 0; it < 8; ++it) {
           const int rl = it * 4 + (lane >> 3);
           const float4 a = *reinterpret_cast<const float4*>(slab + rl * 32 + ((cc ^ (rl & 7)) << 2));
-          if (rows_it[it] >= 0 && !(g_tc_debug & 2)) p.epi4(seg, rows_it[it], rc[it], n0 + j + c4, a, aux[it]);
+          if (rows_it[it] >= 0 && !(dbg & 2)) p.epi4(seg, rows_it[it], rc[it], n0 + j + c4, a, aux[it]);
         }
       }
       tc_fence_before();
