@@ -476,15 +476,17 @@ struct TcRed {
   RowSet rows;
   int M, Ncols, colsum;
   P p;
+  int n_off = 0;  // first output column of this launch (outputs wider than 256 go in slices)
   __device__ __forceinline__ float4 x4(int seg, int row, int m) const {
     if constexpr (HasX4<P>::value) return p.x4(seg, row, m);
     else return make_float4(p.a(seg, row, m), p.a(seg, row, m + 1), p.a(seg, row, m + 2), p.a(seg, row, m + 3));
   }
   __device__ __forceinline__ float4 y4(int seg, int row, int n) const {
+    n += n_off;
     if constexpr (HasY4<P>::value) return p.y4(seg, row, n);
     else return make_float4(p.b(seg, row, n), p.b(seg, row, n + 1), p.b(seg, row, n + 2), p.b(seg, row, n + 3));
   }
-  __device__ __forceinline__ void store(int seg, int k, int n, float v) const { p.store(seg, k, n, v); }
+  __device__ __forceinline__ void store(int seg, int k, int n, float v) const { p.store(seg, k, n + n_off, v); }
 };
 
 // one launch builds every B image of the step: blockIdx.y = job
@@ -522,8 +524,8 @@ void set_smem(Kern k, size_t bytes) {
 template <class P>
 void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& c) {
   Prof pr(c, P::kName, st);
-  const bool use_tc = c.use_tc && p.K % tc::KC == 0 && p.Ncols % 32 == 0 && p.Ncols <= 256 &&
-                      size_t(nseg) * 2 * p.K * p.Ncols <= c.bimg_cap;
+  const bool use_tc = c.use_tc && p.K % tc::KC == 0 && p.Ncols % 32 == 0 &&
+                      (p.Ncols <= 256 || p.Ncols % 256 == 0) && size_t(nseg) * 2 * p.K * p.Ncols <= c.bimg_cap;
   if (use_tc) {
     const float* img = c.bimg;
     const int idx = c.bimg_idx++;
@@ -540,7 +542,7 @@ void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& 
     TcRow<P> q{p.rows, p.K, p.Ncols, img, size_t(2) * p.K * p.Ncols, p};
     const long long mtiles = (rows_cap + 127) / 128 + nseg;
     // split N when there are too few row tiles to fill the GPU (node-row GEMMs)
-    int Nt = p.Ncols;
+    int Nt = p.Ncols <= 256 ? p.Ncols : 256;  // column block per tile (<= one 256-col accumulator)
     // (one wave: the largest split whose tile count still fits the SMs)
     while (Nt > 32 && mtiles * (p.Ncols / Nt) * 2 <= sm && (Nt / 2) % 32 == 0) Nt /= 2;
     const tc::RowPlan plan = tc::row_plan(p.K, Nt);
@@ -559,22 +561,24 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
   if (c.dbg_skip_wgrad) return;  // timing experiments only (HMTL_DBG_SKIP_WGRAD)
   Prof pr(c, P::kName, st);
   const int M = p.K - P::kBias;
-  if (c.use_tc && P::kTc && p.Ncols % 32 == 0 && p.Ncols <= 256 && M % 4 == 0) {
+  const int NW = p.Ncols <= 256 ? p.Ncols : 256;  // accumulator width; wider outputs in slices
+  if (c.use_tc && P::kTc && NW % 32 == 0 && p.Ncols % NW == 0 && M % 4 == 0) {
     const int mtiles = (M + 127) / 128;
     const long long chunks = (rows_cap > 0 ? rows_cap : (long long)c.Ec) / tc::KC + 1;
     // enough CTAs to fill the GPU, >= 4 chunks each (bounded partial traffic)
     long long want = std::max<long long>(1, (long long)c.sm_count / (mtiles * p.rows.nseg));  // one wave
     int ns = int(std::max<long long>(1, std::min<long long>(want, chunks / 4)));
     float* partial = c.part(st);
-    while (ns > 1 && size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * p.Ncols > c.partial_cap) ns /= 2;
-    if (size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * p.Ncols <= c.partial_cap) {
-      TcRed<P> q{p.rows, M, p.Ncols, P::kBias, p};
-      const size_t smem = tc::tc_red_smem(p.Ncols);
+    while (ns > 1 && size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * NW > c.partial_cap) ns /= 2;
+    if (size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * NW <= c.partial_cap) {
+      const size_t smem = tc::tc_red_smem(NW);
       set_smem(tc::tc_red_kernel<TcRed<P>>, smem);
-      dim3 grid(mtiles, ns, p.rows.nseg);
-      kl(tc::tc_red_kernel<TcRed<P>>, grid, tc::kRedThreads, smem, st, q, partial, ns,
-                                                                        tc::red_stages(p.Ncols));
-      tc::tc_red_reduce(q, partial, ns, st);
+      for (int n0 = 0; n0 < p.Ncols; n0 += NW) {
+        TcRed<P> q{p.rows, M, NW, P::kBias, p, n0};
+        dim3 grid(mtiles, ns, p.rows.nseg);
+        kl(tc::tc_red_kernel<TcRed<P>>, grid, tc::kRedThreads, smem, st, q, partial, ns, tc::red_stages(NW));
+        tc::tc_red_reduce(q, partial, ns, st);
+      }
       return;
     }
   }

@@ -136,3 +136,37 @@ def test_gpu_periodic_forward_backward_parity(orc):
     assert O.rel_vec_error(pred2.energy_per_atom, pred.energy_per_atom) < 1e-5
     assert O.rel_vec_error(pred2.forces, pred.forces) < 1e-5
     m.close()
+
+
+@pytest.mark.gpu
+def test_cfg4_shaped_periodic_crystal_parity(orc):
+    """BASELINE config 4 shape (parity case): a periodic inorganic cell of ~200
+    atoms at rc 6 with dense neighbour lists, hidden 256 (layers reduced to 2 so
+    the FP64 oracle stays fast); forward and gradients within 1e-4."""
+    rng = np.random.default_rng(44)
+    n, pos, cells = random_crystals(rng, 1, 200, 200, 13.0, tilt=0.15)
+    rc = 6.0
+    s = samples_for(n, pos, 4)
+    go, eo, dst, src, img, sh = orc.build_edges_pbc(n, pos, cells, rc)
+    assert len(dst) / n.sum() > 60  # dense: ~80 neighbours per atom
+    hp = P.ModelHyper(20, 2, 256, 256, 3, 1, rc)
+    oh = O.Hyper(20, 2, 256, 256, 3, 1, rc)
+    m = P.ModelT(hp, 7, [0], caps=P.Caps(2, int(n.sum()) + 8, len(dst) + 64))
+    m.upload_pbc(s, cells)
+    P.lib().hmtl_build_batch(m.ctx, None)
+    b_ = m.edges()
+    assert np.array_equal(b_.edge_dst, dst) and np.array_equal(b_.edge_src, src)
+    pred = m.forward()
+    b = dict(n_atoms=s.n_atoms, species=s.species, pos=s.positions, forces=s.forces, energy=s.energy,
+             dsid=s.dataset_id, graph_offset=go, edge_offset=eo, edge_dst=dst, edge_src=src, edge_shift=sh)
+    sh0 = orc.init_block(oh, 7, -1)
+    heads = {0: orc.init_block(oh, 7, 0)}
+    E, F, cache = orc.forward(oh, sh0, heads, b)
+    assert O.rel_vec_error(pred.energy_per_atom, E) < TOL
+    assert O.rel_vec_error(pred.forces, F) < TOL
+    L, dE, dF = orc.loss(b, E, F)
+    m.loss()
+    g = m.backward()
+    gs, gh = orc.backward(oh, sh0, heads, b, cache, dE, dF)
+    assert O.rel_vec_error(g.shared, gs) < TOL and O.rel_vec_error(g.heads[0], gh[0]) < TOL
+    m.close()
