@@ -216,6 +216,10 @@ KERNEL_SCOPES = [  # kernel-name pattern -> scope of kernel_work (first match wi
     (r"TcRed<.*::L6Prob>", "bwd.edge_w2grad"), (r"TcRed<.*::L2Prob>", "bwd.node_w2grad"),
     (r"TcRed<.*::L3Prob>", "bwd.node_w1grad"), (r"TcRed<.*::L10Prob>", "bwd.edge_w1ab_grad"),
     (r"TcRed<.*::FGradProb>", "bwd.force_edge_wgrad"),
+    (r"::EnergyProb>", "fwd.energy_mlp"), (r"::QfProb>", "fwd.force_Qf"), (r"::EGradProb>", "bwd.energy_wgrad"),
+    (r"::EDxProb>", "bwd.energy_dx"), (r"::F0NodeGrad>", "bwd.force0_node_wgrad"),
+    (r"::F0EdgeGrad>", "bwd.force0_edge_wgrad"), (r"::F0Dh>", "bwd.force0_dh"), (r"::Node1Prob>", "fwd.node_mlp1"),
+    (r"::Node2Prob>", "fwd.node_mlp2"), (r"::L1Prob>", "bwd.node_dvz1"), (r"::L4Prob>", "bwd.node_dv"),
 ]
 
 
@@ -232,6 +236,12 @@ def kernel_profile(model, cfg, slots, steps=3, flush=None):
 
     from paper_2506_21788_b200._lib import check, lib
 
+    # serialised step graph: each kernel's duration is its own (the view ncu's
+    # launch list gives), not stretched by side-stream kernels sharing the SMs
+    check(lib().hmtl_set_stream_mode(model.ctx, 0))
+    check(lib().hmtl_pool_bind(model.ctx, slots[0], None))
+    check(lib().hmtl_train_step(model.ctx, C.byref(cfg.c()), None))  # capture outside the profile
+    torch.cuda.synchronize()
     with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA], acc_events=True) as prof:
         for i in range(steps):
             if flush is not None:
@@ -239,6 +249,7 @@ def kernel_profile(model, cfg, slots, steps=3, flush=None):
             check(lib().hmtl_pool_bind(model.ctx, slots[i % len(slots)], None))
             check(lib().hmtl_train_step(model.ctx, C.byref(cfg.c()), None))
         torch.cuda.synchronize()
+    check(lib().hmtl_set_stream_mode(model.ctx, 1))
     with tempfile.NamedTemporaryFile(suffix=".json") as f:
         prof.export_chrome_trace(f.name)
         ev = [e for e in json.load(open(f.name))["traceEvents"] if e.get("cat") == "kernel"]
@@ -268,8 +279,9 @@ def roofline(rep, E, N, G, step_ms):
     known = [r for r in rep if kernel_work(r["name"], E, N, G, H, W, L, HEADS)]
     dom = max(known, key=lambda r: r["ms"])
     out = {"kernel": dom["name"], "share_of_step": round(dom["ms"] / total, 4), "peak_source": src,
-           "timing": "CUPTI kernel records (torch.profiler) of 3 replays of the step graph, outside the timed "
-                     "region; share = of the summed kernel time (streams overlap)"}
+           "timing": "CUPTI kernel records (torch.profiler) of 3 replays of a serialised (single-stream) copy "
+                     "of the step graph, L2 flushed between replays, outside the timed region; share = of the "
+                     "summed kernel time"}
     flops, byts = kernel_work(dom["name"], E, N, G, H, W, L, HEADS)
     per_launch_ms = dom["ms"] / max(dom["calls"], 1)
     tf = flops / (per_launch_ms * 1e-3) / 1e12
@@ -491,9 +503,9 @@ def run_b200(args, rank, world, local_rank, dist):
         with torch.cuda.stream(ext):
             flush.zero_()
 
-    rep = kernel_profile(model, cfg, slots, flush=do_flush)
     nk = C.c_int()
     check(lib().hmtl_step_kernel_count(model.ctx, C.byref(nk)))
+    rep = kernel_profile(model, cfg, slots, flush=do_flush)
     launches_per_step = nk.value  # kernel nodes of the step graph
     roof, roof_gs = roofline(rep, E.value, batches[0].N, batches[0].G, dev_ms / args.steps)
 

@@ -247,6 +247,11 @@ int hmtl_profile_report(hmtl_ctx* ctx, char* json, size_t cap);
 /* Kernel nodes in the captured step graph (= kernel launches per graph step),
  * -1 before the first graph capture. */
 int hmtl_step_kernel_count(hmtl_ctx* ctx, int* n);
+/* Step execution mode: 1 = multi-stream step graph (default: energy head,
+ * weight gradients and collectives on side streams), 0 = every kernel on the
+ * caller's stream (serialised; per-kernel times are then each kernel's own, as
+ * a profiler's launch list sees them).  Drops the captured graph; syncs. */
+int hmtl_set_stream_mode(hmtl_ctx* ctx, int multi);
 /* Engine tuning: per-CTA phase timestamps (SM clocks, [CTA][32]) written by the
  * most recent fused node-chain launch; needs HMTL_CHAIN_STAMPS at ctx_create. */
 int hmtl_debug_chain_stamps(hmtl_ctx* ctx, long long* out, int n);

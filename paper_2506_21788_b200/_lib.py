@@ -11,7 +11,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhmtl_b200.so")
+LIB_PATH = os.environ.get("HMTL_LIB") or os.path.join(HERE, "libhmtl_b200.so")  # HMTL_LIB: A/B builds
 CSRC = os.path.join(HERE, "csrc")
 
 ERR_NAMES = {1: "contract", 2: "io", 3: "comm", 4: "data", 5: "config", 6: "internal"}
@@ -108,6 +108,7 @@ SIGNATURES = {
     "hmtl_profile_enable": (C.c_int, [_P, C.c_int]),
     "hmtl_profile_report": (C.c_int, [_P, C.c_char_p, C.c_size_t]),
     "hmtl_step_kernel_count": (C.c_int, [_P, C.POINTER(C.c_int)]),
+    "hmtl_set_stream_mode": (C.c_int, [_P, C.c_int]),
     "hmtl_debug_chain_stamps": (C.c_int, [_P, C.POINTER(C.c_longlong), C.c_int]),
     "hmtl_selftest_mma_rate": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "hmtl_selftest_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _FP, _FP, _FP]),

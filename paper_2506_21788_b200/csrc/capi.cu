@@ -749,6 +749,18 @@ int hmtl_step_kernel_count(hmtl_ctx* h, int* n) {
   return 0;
 }
 
+int hmtl_set_stream_mode(hmtl_ctx* h, int multi) {
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  HMTL_CUDA(cudaDeviceSynchronize());
+  if (c.multi_stream != (multi != 0) && c.step_exec) {
+    cudaGraphExecDestroy(c.step_exec);
+    c.step_exec = nullptr;
+  }
+  c.multi_stream = multi != 0;
+  return 0;
+}
+
 int hmtl_profile_enable(hmtl_ctx* h, int on) {
   Ctx& c = h->c;
   cudaSetDevice(c.device);

@@ -304,6 +304,120 @@ __global__ void pool_kernel(const DevHdr* hdr, const int* __restrict__ graph_off
   }
 }
 
+// Energy head, whole (hmtl/model.hpp:440-452): pooled_g = mean_{i in g} h_L[i],
+// z_0 = pooled W0 + b0, z_i = silu(z_{i-1}) W_i + b_i, E_g = z_{D-1} (width 1).
+// One launch replaces pool + D GEMM launches of a few hundred rows each: CTA =
+// kEhRows graphs of one head segment; warp r pools graph r (float4 columns, 8
+// atom rows in flight, ascending atom order); each layer stages its weights in
+// shared memory in 64-row K chunks (one round of loads) and a thread
+// computes 4 rows x 1 column in exact FP32 (ascending k); the width-1 layer is a
+// warp dot product per graph.  Writes pooled and every z_i (the backward's inputs).
+constexpr int kEhRows = 8, kEhMaxD = 8, kEhKC = 64;
+struct EHeadArgs {
+  const float* hp;  // head block of slot 0; slot s at + s*PH
+  size_t PH;
+  size_t w[kEhMaxD], b[kEhMaxD];
+  int D, H, W;
+};
+__global__ void __launch_bounds__(256) energy_head_kernel(const DevHdr* hdr, RowSet rows, const int* __restrict__ go,
+                                                          const float* __restrict__ h, EHeadArgs a,
+                                                          float* __restrict__ pooled, float* __restrict__ ez, int Gc,
+                                                          float* __restrict__ energy) {
+  pdl_wait();
+  extern __shared__ float4 ehs4[];
+  float* smf = reinterpret_cast<float*>(ehs4);
+  const int KM = max(a.H, a.W);
+  float* X = smf;                    // [kEhRows][KM] layer input
+  float* Y = X + kEhRows * KM;       // [kEhRows][KM] next layer input
+  float* Ws = Y + kEhRows * KM;      // [kEhKC][W] weight chunk
+  const int seg = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rb = rows.begin(seg), re = rows.end(seg);
+  const float* hp = a.hp + size_t(seg) * a.PH;
+  for (int v0 = rb + blockIdx.x * kEhRows; v0 < re; v0 += gridDim.x * kEhRows) {
+    const int nr = min(kEhRows, re - v0);
+    if (warp < nr) {
+      const int g = rows.row(v0 + warp), lo = go[g], hi = go[g + 1];
+      const float inv = 1.f / float(hi - lo);
+      for (int c = lane * 4; c < a.H; c += 128) {
+        float4 acc = f4z();
+        for (int i = lo; i < hi; i += 8) {
+          float4 x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) x[u] = i + u < hi ? ld4(h + size_t(i + u) * a.H + c) : f4z();
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (i + u < hi) acc = add4(acc, x[u]);
+        }
+        const float4 m = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+        st4(pooled + size_t(g) * a.H + c, m);
+        *reinterpret_cast<float4*>(X + warp * KM + c) = m;
+      }
+    }
+    for (int l = 0; l < a.D; ++l) {
+      const int K = l ? a.W : a.H;
+      const float* Wt = hp + a.w[l];
+      const float* bt = hp + a.b[l];
+      float* ezl = ez + size_t(l) * Gc * a.W;
+      if (l == a.D - 1) {  // width-1 output: warp dot product per graph
+        __syncthreads();
+        if (warp < nr) {
+          const int g = rows.row(v0 + warp);
+          float acc = 0.f;
+          for (int k = lane; k < K; k += 32) acc = fmaf(X[warp * KM + k], Wt[k], acc);
+#pragma unroll
+          for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          if (lane == 0) {
+            const float z = acc + bt[0];
+            ezl[size_t(g) * a.W] = z;
+            energy[g] = z;
+          }
+        }
+        __syncthreads();
+        break;
+      }
+      const int n0 = tid & 127, r0 = (tid >> 7) * 4;  // 4 rows x 1 column per thread per 128-column block
+      float acc[4][2] = {};
+      for (int k0 = 0; k0 < K; k0 += kEhKC) {
+        const int kc = min(kEhKC, K - k0);
+        __syncthreads();  // X complete / previous chunk consumed
+        // (scalar: head tensors follow the reference's BlockLayout, not 16-byte aligned)
+#pragma unroll 8
+        for (int t = tid; t < kc * a.W; t += 256) Ws[t] = __ldg(Wt + size_t(k0) * a.W + t);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int n = n0 + 128 * j;
+          if (n < a.W) {
+            for (int k = 0; k < kc; ++k) {
+              const float w = Ws[k * a.W + n];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) acc[u][j] = fmaf(X[(r0 + u) * KM + k0 + k], w, acc[u][j]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int n = n0 + 128 * j;
+        if (n >= a.W) continue;
+        const float bn = bt[n];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (r0 + u >= nr) continue;
+          const float z = acc[u][j] + bn;
+          ezl[size_t(rows.row(v0 + r0 + u)) * a.W + n] = z;
+          Y[(r0 + u) * KM + n] = silu(z);
+        }
+      }
+      __syncthreads();
+      float* t = X;
+      X = Y;
+      Y = t;
+    }
+    __syncthreads();
+  }
+}
+
 // F_i = sum_{e in row i} dvec_e * s_e   (hmtl/model.hpp:475-480)
 __global__ void forces_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const float4* __restrict__ geo,
                               const float* __restrict__ s, float* __restrict__ F) {
@@ -895,18 +1009,32 @@ void launch_forward(Ctx& c, cudaStream_t st) {
   // energy branch (side stream; independent of the force branch until the loss)
   cudaStream_t se = c.side(c.s_e, st);
   c.dep(st, se);
-  {
-    Prof pr(c, "fwd.pool", se);
-    kl(pool_kernel, gridn((long long)c.Gc * 32, 256, sm * 8), 256, 0, se, c.hdr, c.graph_offset, hL, c.pooled, H);
-  }
-  for (int i = 0; i < D; ++i) {
-    const int last = i == D - 1;
-    EnergyProb q{graph_rows_by_head(c), i == 0 ? H : W, last ? 1 : W, H, W, i, last, c.pooled,
-                 i ? c.ez + size_t(i - 1) * c.Gc * W : nullptr,
-                 HeadW{c.head_params(), c.PH, c.head_off("energy.W" + std::to_string(i))},
-                 HeadW{c.head_params(), c.PH, c.head_off("energy.b" + std::to_string(i))},
-                 c.ez + size_t(i) * c.Gc * W, c.energy};
-    ab(q, c.Gc, c.S, se, sm, c);
+  if (D >= 2 && D <= kEhMaxD && H % 4 == 0 && W % 4 == 0 && W <= 256 && H <= 512) {
+    Prof pr(c, "fwd.energy_head", se);
+    EHeadArgs a{c.head_params(), c.PH, {}, {}, D, H, W};
+    for (int i = 0; i < D; ++i) {
+      a.w[i] = c.head_off("energy.W" + std::to_string(i));
+      a.b[i] = c.head_off("energy.b" + std::to_string(i));
+    }
+    const size_t smem = (size_t(2) * kEhRows * std::max(H, W) + size_t(kEhKC) * W) * sizeof(float);
+    set_smem(energy_head_kernel, smem);
+    const dim3 grid(std::min((c.Gc + kEhRows - 1) / kEhRows, 32), c.S);
+    kl(energy_head_kernel, grid, 256, smem, se, c.hdr, graph_rows_by_head(c), c.graph_offset, hL, a, c.pooled, c.ez,
+       c.Gc, c.energy);
+  } else {
+    {
+      Prof pr(c, "fwd.pool", se);
+      kl(pool_kernel, gridn((long long)c.Gc * 32, 256, sm * 8), 256, 0, se, c.hdr, c.graph_offset, hL, c.pooled, H);
+    }
+    for (int i = 0; i < D; ++i) {
+      const int last = i == D - 1;
+      EnergyProb q{graph_rows_by_head(c), i == 0 ? H : W, last ? 1 : W, H, W, i, last, c.pooled,
+                   i ? c.ez + size_t(i - 1) * c.Gc * W : nullptr,
+                   HeadW{c.head_params(), c.PH, c.head_off("energy.W" + std::to_string(i))},
+                   HeadW{c.head_params(), c.PH, c.head_off("energy.b" + std::to_string(i))},
+                   c.ez + size_t(i) * c.Gc * W, c.energy};
+      ab(q, c.Gc, c.S, se, sm, c);
+    }
   }
   // force branch
   {
