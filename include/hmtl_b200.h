@@ -195,6 +195,26 @@ int hmtl_store_create(int device, const hmtl_samples* pool, hmtl_store** out);
 int hmtl_store_counts(const hmtl_store* st, uint8_t* ids, uint64_t* counts, int cap, int* n);
 int hmtl_store_bind(hmtl_ctx* ctx, hmtl_store* st, const uint8_t* ds, const uint64_t* idx, int n, void* stream);
 int hmtl_store_destroy(hmtl_store* st);
+/* Sharded store: each rank keeps only its DataStore shard (make_partition +
+ * balanced_split, src/datastore.cpp:11-45 / :99-145) and fetch_samples'
+ * remote reads (request/response over TCP, src/datastore.cpp:192-248) become
+ * one grouped NCCL send/recv per step over NVLink/NVSwitch.
+ *   shard_range: balanced_split(count, n)[i] = [begin, end).
+ *   create_sharded: collective over the context's world communicator
+ *     (hmtl_comm_init first).  `shard` = this rank's samples of every dataset it
+ *     serves, dataset by dataset, each its range [begin, end) in index order;
+ *     ids/counts/members/member_off = the partition (serving ranks of dataset
+ *     d: members[member_off[d] .. member_off[d+1]], ascending).  The atom
+ *     counts of every shard are broadcast once (4 B per sample).
+ *   fetch: collective; plan_ds/plan_idx = this step's plan rows of EVERY rank
+ *     ([world][b_local], hmtl_epoch_plan output); owners push what their peers
+ *     need (no request message: the plan is known everywhere), then one kernel
+ *     assembles the batch arena -- the same bytes store_bind/batch_upload give. */
+int hmtl_shard_range(uint64_t count, int n, int i, uint64_t* begin, uint64_t* end);
+int hmtl_store_create_sharded(hmtl_ctx* ctx, const hmtl_samples* shard, const uint8_t* ids, const uint64_t* counts,
+                              const int* members, const int* member_off, int n_datasets, hmtl_store** out);
+int hmtl_store_fetch(hmtl_ctx* ctx, hmtl_store* st, const uint8_t* plan_ds, const uint64_t* plan_idx, int b_local,
+                     void* stream);
 /* HMTD sample files (hmtl/sample_io.hpp:9-15) straight into a device store:
  * structure checked on the host as read_sample_file_raw, the raw records
  * uploaded as they are, per-record CRC-32 and the parse into the pool on the
@@ -208,6 +228,8 @@ int hmtl_hmtd_read_header(const char* path, uint8_t* dataset_id, uint8_t* aligne
 /* build_batch<float> on the device (hmtl/graph.hpp:46-83): bit-exact FP64
  * cutoff test, dst-major CSR, reverse-edge permutation, per-graph edge offsets. */
 int hmtl_build_batch(hmtl_ctx* ctx, void* stream);
+/* n_graphs / n_nodes of the batch last bound (upload, pool, store bind/fetch). */
+int hmtl_batch_shape(hmtl_ctx* ctx, int* G, int* N);
 /* GraphBatchT edge view (syncs): *E, and optionally edge_dst/edge_src[E], edge_offset[G+1]. */
 int hmtl_batch_edges(hmtl_ctx* ctx, int* E, int* edge_dst, int* edge_src, int* edge_offset);
 

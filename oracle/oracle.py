@@ -334,6 +334,28 @@ class Ref:
             raise RuntimeError(self.err())
         return st.value, ds[:n], ix[:n]
 
+    def make_partition(self, counts: dict, n_groups: int, replicas: int, mode: int) -> dict:
+        """The reference's make_partition (src/datastore.cpp:25-45) on Mesh{n_groups, replicas}:
+        {dataset id: [(serving rank, begin, end), ...]}."""
+        L = self.lib
+        L.ref_make_partition.restype = C.c_long
+        L.ref_make_partition.argtypes = [C.POINTER(_U8), C.POINTER(C.c_uint64), C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.POINTER(_I), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(_I)]
+        ids = np.array(sorted(counts), np.uint8)
+        cnt = np.array([counts[int(k)] for k in ids], np.uint64)
+        cap = len(ids) * n_groups * replicas + 1
+        sv, b, e, ns = np.zeros(cap, np.int32), np.zeros(cap, np.uint64), np.zeros(cap, np.uint64), np.zeros(len(ids), np.int32)
+        u64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint64))
+        n = L.ref_make_partition(_p(ids, _U8), u64(cnt), len(ids), n_groups, replicas, mode, _p(sv, _I), u64(b), u64(e),
+                                 _p(ns, _I))
+        if n < 0:
+            raise RuntimeError(self.err())
+        out, k = {}, 0
+        for i, d in enumerate(ids):
+            out[int(d)] = [(int(sv[k + j]), int(b[k + j]), int(e[k + j])) for j in range(ns[i])]
+            k += ns[i]
+        return out
+
     def default5_spec(self, i: int) -> dict:
         el = (_U8 * 32)()
         ne, nmin, nmax = _I(), _I(), _I()

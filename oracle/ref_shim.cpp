@@ -486,6 +486,34 @@ long ref_shuffle_epoch(const uint8_t* ids, const uint64_t* counts, int n, int n_
   }
 }
 
+// make_partition (src/datastore.cpp:25-45) on Mesh{n_groups, replicas}: per
+// dataset (ascending id) its serving ranks and balanced_split ranges, flattened
+long ref_make_partition(const uint8_t* ids, const uint64_t* counts, int n, int n_groups, int replicas, int mode,
+                        int* serving, uint64_t* begin, uint64_t* end, int* n_serving) {
+  try {
+    std::map<uint8_t, uint64_t> cnt;
+    for (int i = 0; i < n; ++i) cnt[ids[i]] = counts[i];
+    Mesh mesh;
+    mesh.n_groups = n_groups;
+    mesh.replicas = replicas;
+    DataPartition p = make_partition(cnt, mesh, mode == 1 ? RunMode::taskpar : RunMode::base);
+    long k = 0;
+    int i = 0;
+    for (const auto& kv : p.datasets) {
+      n_serving[i++] = int(kv.second.serving_ranks.size());
+      for (size_t j = 0; j < kv.second.serving_ranks.size(); ++j, ++k) {
+        serving[k] = kv.second.serving_ranks[j];
+        begin[k] = kv.second.ranges[j].begin;
+        end[k] = kv.second.ranges[j].end;
+      }
+    }
+    return k;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // write_sample_file (src/sample_io.cpp:104-120) of G samples (flat arrays)
 int ref_write_samples(const char* path, int dataset_id, int aligned, int G, const int* n_atoms,
                       const uint8_t* species, const double* pos, const double* energy, const double* forces,

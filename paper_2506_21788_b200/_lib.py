@@ -120,6 +120,11 @@ SIGNATURES = {
     "hmtl_store_counts": (C.c_int, [_P, _U8P, C.POINTER(C.c_uint64), C.c_int, _IP]),
     "hmtl_store_bind": (C.c_int, [_P, _P, _U8P, C.POINTER(C.c_uint64), C.c_int, _P]),
     "hmtl_store_destroy": (C.c_int, [_P]),
+    "hmtl_batch_shape": (C.c_int, [_P, _IP, _IP]),
+    "hmtl_shard_range": (C.c_int, [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "hmtl_store_create_sharded": (C.c_int, [_P, C.POINTER(CSamples), _U8P, C.POINTER(C.c_uint64), _IP, _IP, C.c_int,
+                                            C.POINTER(_P)]),
+    "hmtl_store_fetch": (C.c_int, [_P, _P, _U8P, C.POINTER(C.c_uint64), C.c_int, _P]),
     "hmtl_store_from_hmtd": (C.c_int, [C.c_int, C.POINTER(C.c_char_p), C.c_int, C.POINTER(_P)]),
     "hmtl_hmtd_write": (C.c_int, [C.c_char_p, C.c_uint8, C.c_uint8, C.POINTER(CSamples)]),
     "hmtl_hmtd_read_header": (C.c_int, [C.c_char_p, _U8P, _U8P, C.POINTER(C.c_uint64)]),

@@ -743,6 +743,13 @@ int hmtl_debug_chain_stamps(hmtl_ctx* h, long long* out, int n) {
   return 0;
 }
 
+int hmtl_batch_shape(hmtl_ctx* h, int* G, int* N) {
+  if (!h || !G || !N) return fail(HMTL_ERR_CONTRACT, "batch_shape: null argument");
+  *G = h->c.host_G;
+  *N = h->c.host_N;
+  return 0;
+}
+
 int hmtl_step_kernel_count(hmtl_ctx* h, int* n) {
   if (!n) return fail(HMTL_ERR_CONTRACT, "step_kernel_count: null argument");
   *n = h->c.step_kernels;

@@ -93,6 +93,13 @@ void comm_destroy(Comm* m) {
   delete m;
 }
 
+ncclComm_t comm_world(Ctx& c, int* rank, int* size) {
+  if (!c.comm) return nullptr;
+  *rank = c.comm->rank;
+  *size = c.comm->world_size;
+  return c.comm->world;
+}
+
 }  // namespace hmtl_b200
 
 using namespace hmtl_b200;

@@ -12,6 +12,7 @@
 // offsets cross PCIe.  The arena it writes is byte-identical to the one
 // hmtl_batch_upload packs on the host.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -23,6 +24,32 @@
 #include "ctx.cuh"
 
 using namespace hmtl_b200;
+
+namespace hmtl_b200 {
+ncclComm_t comm_world(Ctx& c, int* rank, int* size);  // comm.cu
+}
+
+// DataPartition::Dataset (hmtl/datastore.hpp:25-40): serving ranks ascending,
+// one balanced contiguous range each
+struct StorePart {
+  uint64_t count = 0;
+  std::vector<int> serving;
+  std::vector<uint64_t> lo;  // range i = [lo[i], lo[i+1])
+  uint64_t my_begin = 0;     // this rank's range (sharded stores)
+  std::vector<int> n_atoms;  // every sample of the dataset (all shards), for batch offsets
+  int owner_of(uint64_t index) const {
+    for (size_t i = 0; i + 1 < lo.size(); ++i)
+      if (index >= lo[i] && index < lo[i + 1]) return serving[i];
+    return -1;
+  }
+};
+// one batch item of a sharded fetch: pool sample (kind 0) or byte offset in
+// the receive buffer (kind 1); pack items: pool sample -> send-buffer offset
+struct FetchItem {
+  long long src;
+  long long dst;
+  int n, kind, ds, pad;
+};
 
 struct hmtl_store {
   int device = 0;
@@ -41,6 +68,16 @@ struct hmtl_store {
   int* d_sel = nullptr;
   int stage_cap = 0;
   cudaEvent_t staged = nullptr;  // last bind's staging copy has been consumed
+  // sharded store (hmtl_store_create_sharded): only this rank's shard is in the
+  // pool; fetches exchange remote samples with NCCL send/recv
+  bool sharded = false;
+  int rank = 0, world = 1;
+  std::map<int, StorePart> part;
+  FetchItem* h_items = nullptr;  // pinned [pack items | assemble items]
+  FetchItem* d_items = nullptr;
+  int items_cap = 0;
+  uint8_t *d_send = nullptr, *d_recv = nullptr;
+  size_t send_cap = 0, recv_cap = 0;
 };
 
 namespace {
@@ -67,6 +104,67 @@ __global__ void store_gather_kernel(const int* __restrict__ sel, int G, const lo
   for (int t = threadIdx.x; t < 3 * n; t += blockDim.x) {
     p[3LL * dst0 + t] = pos[3 * src0 + t];
     f[3LL * dst0 + t] = forces[3 * src0 + t];
+  }
+}
+// sample wire format of a sharded fetch (8-byte aligned blocks):
+// [energy f64 | positions 3n f64 | forces 3n f64 | species n u8, padded to 8]
+__host__ __device__ inline long long wire_bytes(int n) { return 8 + 48LL * n + ((n + 7) & ~7); }
+__global__ void store_pack_kernel(const FetchItem* __restrict__ it, int n_items, const long long* __restrict__ atom_off,
+                                  const uint8_t* __restrict__ species, const double* __restrict__ energy,
+                                  const double* __restrict__ pos, const double* __restrict__ forces,
+                                  uint8_t* __restrict__ out) {
+  for (int k = blockIdx.x; k < n_items; k += gridDim.x) {
+    const FetchItem f = it[k];
+    const long long a0 = atom_off[f.src];
+    double* o = reinterpret_cast<double*>(out + f.dst);
+    if (threadIdx.x == 0) o[0] = energy[f.src];
+    for (int t = threadIdx.x; t < 3 * f.n; t += blockDim.x) {
+      o[1 + t] = pos[3 * a0 + t];
+      o[1 + 3 * f.n + t] = forces[3 * a0 + t];
+    }
+    uint8_t* sp = out + f.dst + 8 + 48LL * f.n;
+    for (int t = threadIdx.x; t < f.n; t += blockDim.x) sp[t] = species[a0 + t];
+  }
+}
+// batch item g -> the arena (same bytes as store_gather_kernel / batch_upload)
+__global__ void store_assemble_kernel(const FetchItem* __restrict__ it, int G, const long long* __restrict__ atom_off,
+                                      const uint8_t* __restrict__ species, const double* __restrict__ energy,
+                                      const double* __restrict__ pos, const double* __restrict__ forces,
+                                      const uint8_t* __restrict__ recv, uint8_t* __restrict__ arena) {
+  pdl_wait();
+  const int g = blockIdx.x;
+  if (g >= G) return;
+  const int* hdr = reinterpret_cast<const int*>(arena);
+  const ArenaLayout al = arena_layout(hdr[0], hdr[1]);
+  const int* go = reinterpret_cast<const int*>(arena + al.go);
+  const FetchItem f = it[g];
+  const int dst0 = go[g], n = f.n;
+  uint8_t* sp = arena + al.sp;
+  double* p = reinterpret_cast<double*>(arena + al.pos);
+  double* fo = reinterpret_cast<double*>(arena + al.lf);
+  if (f.kind == 0) {
+    const long long a0 = atom_off[f.src];
+    if (threadIdx.x == 0) {
+      arena[al.ds + g] = uint8_t(f.ds);
+      reinterpret_cast<double*>(arena + al.le)[g] = energy[f.src];
+    }
+    for (int t = threadIdx.x; t < n; t += blockDim.x) sp[dst0 + t] = species[a0 + t];
+    for (int t = threadIdx.x; t < 3 * n; t += blockDim.x) {
+      p[3LL * dst0 + t] = pos[3 * a0 + t];
+      fo[3LL * dst0 + t] = forces[3 * a0 + t];
+    }
+  } else {
+    const double* w = reinterpret_cast<const double*>(recv + f.src);
+    if (threadIdx.x == 0) {
+      arena[al.ds + g] = uint8_t(f.ds);
+      reinterpret_cast<double*>(arena + al.le)[g] = w[0];
+    }
+    const uint8_t* ws = recv + f.src + 8 + 48LL * n;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) sp[dst0 + t] = ws[t];
+    for (int t = threadIdx.x; t < 3 * n; t += blockDim.x) {
+      p[3LL * dst0 + t] = w[1 + t];
+      fo[3LL * dst0 + t] = w[1 + 3 * n + t];
+    }
   }
 }
 // CRC-32 (zlib's reflected 0xEDB88320) of each record body against its stored
@@ -343,14 +441,262 @@ int hmtl_store_bind(hmtl_ctx* h, hmtl_store* st, const uint8_t* ds, const uint64
   return HMTL_OK;
 }
 
+// ---- sharded store (remote samples over NVLink) ----
+
+// balanced_split (src/datastore.cpp:11-23): the first count % n shards get one extra
+int hmtl_shard_range(uint64_t count, int n, int i, uint64_t* begin, uint64_t* end) {
+  if (n < 1) return fail(HMTL_ERR_CONTRACT, "balanced_split: need at least one shard");
+  if (i < 0 || i >= n || !begin || !end) return fail(HMTL_ERR_CONTRACT, "shard_range: bad shard index");
+  const uint64_t base = count / uint64_t(n), extra = count % uint64_t(n);
+  *begin = base * uint64_t(i) + std::min<uint64_t>(uint64_t(i), extra);
+  *end = *begin + base + (uint64_t(i) < extra ? 1 : 0);
+  return HMTL_OK;
+}
+
+int hmtl_store_create_sharded(hmtl_ctx* h, const hmtl_samples* s, const uint8_t* ids, const uint64_t* counts,
+                              const int* members, const int* member_off, int n_datasets, hmtl_store** out) {
+  if (!h || !s || !out || !ids || !counts || !members || !member_off || n_datasets < 1)
+    return fail(HMTL_ERR_CONTRACT, "store_create_sharded: null argument");
+  Ctx& c = h->c;
+  int rank = 0, world = 1;
+  ncclComm_t comm = comm_world(c, &rank, &world);
+  if (!comm) return fail(HMTL_ERR_CONTRACT, "store_create_sharded: hmtl_comm_init first");
+  // the partition (make_partition, src/datastore.cpp:25-45) and this rank's expected shard
+  std::map<int, StorePart> part;
+  std::map<int, uint64_t> expect;
+  for (int d = 0; d < n_datasets; ++d) {
+    StorePart sp;
+    sp.count = counts[d];
+    sp.serving.assign(members + member_off[d], members + member_off[d + 1]);
+    if (sp.serving.empty() || !std::is_sorted(sp.serving.begin(), sp.serving.end()))
+      return fail(HMTL_ERR_CONTRACT, "store_create_sharded: serving ranks must be non-empty and ascending");
+    const int ns = int(sp.serving.size());
+    sp.lo.resize(ns + 1);
+    for (int i = 0; i < ns; ++i) {
+      uint64_t b, e;
+      hmtl_shard_range(sp.count, ns, i, &b, &e);
+      sp.lo[i] = b, sp.lo[i + 1] = e;
+      if (sp.serving[i] < 0 || sp.serving[i] >= world) return fail(HMTL_ERR_CONTRACT, "store_create_sharded: bad rank");
+      if (sp.serving[i] == rank) sp.my_begin = b, expect[ids[d]] = e - b;
+    }
+    if (part.count(ids[d])) return fail(HMTL_ERR_DATA, "duplicate dataset id across files");
+    part[ids[d]] = std::move(sp);
+  }
+  // the shard: per served dataset its range, in order; nothing else
+  std::map<int, uint64_t> have;
+  for (int g = 0; g < s->G; ++g) ++have[s->dataset_id[g]];
+  for (const auto& kv : have)
+    if (!expect.count(kv.first) || expect[kv.first] != kv.second)
+      return fail(HMTL_ERR_CONTRACT, "store_create_sharded: shard does not match this rank's ranges");
+  for (const auto& kv : expect)
+    if (kv.second && !have.count(kv.first))
+      return fail(HMTL_ERR_CONTRACT, "store_create_sharded: shard does not match this rank's ranges");
+  hmtl_store* st = nullptr;
+  if (int rc = hmtl_store_create(c.device, s, &st)) return rc;
+  st->sharded = true;
+  st->rank = rank;
+  st->world = world;
+  // every sample's atom count, all shards (one grouped broadcast per range
+  // owner, 4 B per sample): a fetch then needs no request round trip
+  size_t total = 0;
+  for (auto& kv : part) total += kv.second.count;
+  int* d_n = nullptr;
+  if (cudaMalloc(&d_n, std::max<size_t>(total, 1) * 4) != cudaSuccess) {
+    hmtl_store_destroy(st);
+    return fail(HMTL_ERR_INTERNAL, "store_create_sharded: allocation failed");
+  }
+  std::vector<int> h_n(total, 0);
+  {
+    size_t at = 0;
+    for (auto& kv : part) {  // my ranges from the shard (datasets appear in pool order)
+      const auto it = st->by_dataset.find(kv.first);
+      if (it != st->by_dataset.end())
+        for (size_t j = 0; j < it->second.size(); ++j) h_n[at + kv.second.my_begin + j] = st->n_atoms[it->second[j]];
+      at += kv.second.count;
+    }
+  }
+  cudaStream_t sm = c.stream;
+  bool ok = cudaMemcpy(d_n, h_n.data(), total * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok = ok && ncclGroupStart() == ncclSuccess;
+  {
+    size_t at = 0;
+    for (auto& kv : part) {
+      const StorePart& sp = kv.second;
+      for (size_t i = 0; i < sp.serving.size(); ++i) {
+        const size_t len = sp.lo[i + 1] - sp.lo[i];
+        if (len && ok)
+          ok = ncclBroadcast(d_n + at + sp.lo[i], d_n + at + sp.lo[i], len, ncclInt32, sp.serving[i], comm, sm) ==
+               ncclSuccess;
+      }
+      at += sp.count;
+    }
+  }
+  ok = (ncclGroupEnd() == ncclSuccess) && ok;
+  ok = ok && cudaStreamSynchronize(sm) == cudaSuccess &&
+       cudaMemcpy(h_n.data(), d_n, total * 4, cudaMemcpyDeviceToHost) == cudaSuccess;
+  cudaFree(d_n);
+  if (!ok) {
+    hmtl_store_destroy(st);
+    return fail(HMTL_ERR_COMM, "store_create_sharded: sample-size exchange failed");
+  }
+  size_t at = 0;
+  for (auto& kv : part) {
+    kv.second.n_atoms.assign(h_n.begin() + at, h_n.begin() + at + kv.second.count);
+    at += kv.second.count;
+  }
+  st->part = std::move(part);
+  *out = st;
+  return HMTL_OK;
+}
+
+// fetch_samples(plan, step) (src/datastore.cpp:192-248), B200 edition: the
+// step's plan rows of every rank are known to every rank (shuffle_epoch is
+// deterministic), so owners push what their peers need without a request
+// message; every pair's samples go in one ncclSend/ncclRecv of a grouped call
+// (NVLink/NVSwitch), and one kernel assembles the batch arena from the local
+// pool and the receive buffer.
+int hmtl_store_fetch(hmtl_ctx* h, hmtl_store* st, const uint8_t* plan_ds, const uint64_t* plan_idx, int b_local,
+                     void* stream) {
+  if (!h || !st || !plan_ds || !plan_idx || b_local < 1) return fail(HMTL_ERR_CONTRACT, "model: empty batch rejected");
+  if (!st->sharded) return fail(HMTL_ERR_CONTRACT, "store_fetch: not a sharded store (use store_bind)");
+  Ctx& c = h->c;
+  if (st->device != c.device) return fail(HMTL_ERR_CONTRACT, "store_fetch: store and context on different devices");
+  int rank = 0, world = 1;
+  ncclComm_t comm = comm_world(c, &rank, &world);
+  if (!comm || rank != st->rank || world != st->world)
+    return fail(HMTL_ERR_CONTRACT, "store_fetch: context communicator differs from the store's");
+  const int n = b_local;
+  if (n > c.Gc) return fail(HMTL_ERR_CONTRACT, "batch exceeds context capacity (graphs/nodes)");
+  cudaSetDevice(c.device);
+  cudaStream_t sm = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+  auto find = [&](uint8_t d, uint64_t i, const StorePart** sp) -> int {
+    auto it = st->part.find(d);
+    if (it == st->part.end() || i >= it->second.count) return -1;
+    *sp = &it->second;
+    return it->second.owner_of(i);
+  };
+  // plan walk: my items (local or from their owner), and what I owe each peer
+  std::vector<FetchItem> mine(n), pack;
+  std::vector<long long> send_b(world, 0), recv_b(world, 0), send_off(world + 1, 0), recv_off(world + 1, 0);
+  // pass 1: byte counts per peer
+  for (int r = 0; r < world; ++r)
+    for (int b = 0; b < n; ++b) {
+      const uint8_t d = plan_ds[size_t(r) * n + b];
+      const uint64_t i = plan_idx[size_t(r) * n + b];
+      const StorePart* sp = nullptr;
+      const int o = find(d, i, &sp);
+      if (o < 0) return fail(HMTL_ERR_CONTRACT, "owner_of: index out of range");
+      if (r == rank && o != rank) recv_b[o] += wire_bytes(sp->n_atoms[i]);
+      if (r != rank && o == rank) send_b[r] += wire_bytes(sp->n_atoms[i]);
+    }
+  for (int p = 0; p < world; ++p) send_off[p + 1] = send_off[p] + send_b[p], recv_off[p + 1] = recv_off[p] + recv_b[p];
+  // pass 2: descriptors (per peer in batch order, the order both sides walk)
+  std::vector<long long> sat(send_off.begin(), send_off.end() - 1), rat(recv_off.begin(), recv_off.end() - 1);
+  long long N = 0, bound = 0;
+  for (int r = 0; r < world; ++r)
+    for (int b = 0; b < n; ++b) {
+      const uint8_t d = plan_ds[size_t(r) * n + b];
+      const uint64_t i = plan_idx[size_t(r) * n + b];
+      const StorePart* sp = nullptr;
+      const int o = find(d, i, &sp);
+      const int na = sp->n_atoms[i];
+      if (r == rank) {
+        if (c.slot_of[d] < 0)
+          return fail(HMTL_ERR_CONTRACT, "model: unknown dataset id " + std::to_string(d) +
+                                             " (head not owned by this rank)");
+        FetchItem& f = mine[b];
+        f.n = na, f.ds = d, f.dst = 0, f.pad = 0;
+        if (o == rank) f.kind = 0, f.src = st->by_dataset[d][i - sp->my_begin];
+        else f.kind = 1, f.src = rat[o], rat[o] += wire_bytes(na);
+        N += na;
+        bound += (long long)na * (na - 1);
+      } else if (o == rank) {
+        pack.push_back(FetchItem{st->by_dataset[d][i - sp->my_begin], sat[r], na, 0, d, 0});
+        sat[r] += wire_bytes(na);
+      }
+    }
+  if (N > c.Nc) return fail(HMTL_ERR_CONTRACT, "batch exceeds context capacity (graphs/nodes)");
+  if (bound > c.Ec) return fail(HMTL_ERR_CONTRACT, "batch may exceed the context's edge capacity");
+  // staging: [G, N, 0, 0, graph_offset[G+1]] -> arena; items -> device
+  const int words = 4 + (n + 1);
+  const int n_items = int(pack.size()) + n;
+  if (words > st->stage_cap || n_items > st->items_cap) {
+    if (st->h_stage) cudaEventSynchronize(st->staged);
+    if (words > st->stage_cap) {
+      if (st->h_stage) cudaFreeHost(st->h_stage);
+      if (st->d_sel) cudaFree(st->d_sel);
+      st->stage_cap = std::max(words, 4096);
+      HMTL_CUDA(cudaMallocHost(&st->h_stage, size_t(st->stage_cap) * 4));
+      HMTL_CUDA(cudaMalloc(&st->d_sel, size_t(st->stage_cap) * 4));
+    }
+    if (n_items > st->items_cap) {
+      if (st->h_items) cudaFreeHost(st->h_items);
+      if (st->d_items) cudaFree(st->d_items);
+      st->items_cap = std::max(n_items, 1024);
+      HMTL_CUDA(cudaMallocHost(&st->h_items, size_t(st->items_cap) * sizeof(FetchItem)));
+      HMTL_CUDA(cudaMalloc(&st->d_items, size_t(st->items_cap) * sizeof(FetchItem)));
+    }
+  } else {
+    HMTL_CUDA(cudaEventSynchronize(st->staged));
+  }
+  auto grow = [&](uint8_t** p, size_t* cap, size_t need) -> bool {
+    if (need <= *cap) return true;
+    cudaStreamSynchronize(sm);
+    if (*p) cudaFree(*p);
+    *cap = std::max(need, size_t(1) << 20);
+    return cudaMalloc(p, *cap) == cudaSuccess;
+  };
+  if (!grow(&st->d_send, &st->send_cap, size_t(send_off[world])) ||
+      !grow(&st->d_recv, &st->recv_cap, size_t(recv_off[world])))
+    return fail(HMTL_ERR_INTERNAL, "store_fetch: exchange buffer allocation failed");
+  int* hs = st->h_stage;
+  hs[0] = n, hs[1] = int(N), hs[2] = hs[3] = 0;
+  int* go = hs + 4;
+  go[0] = 0;
+  for (int g = 0; g < n; ++g) go[g + 1] = go[g] + mine[g].n;
+  std::memcpy(st->h_items, pack.data(), pack.size() * sizeof(FetchItem));
+  std::memcpy(st->h_items + pack.size(), mine.data(), size_t(n) * sizeof(FetchItem));
+  HMTL_CUDA(cudaMemcpyAsync(c.arena, hs, size_t(4 + n + 1) * 4, cudaMemcpyHostToDevice, sm));
+  HMTL_CUDA(cudaMemcpyAsync(st->d_items, st->h_items, size_t(n_items) * sizeof(FetchItem), cudaMemcpyHostToDevice, sm));
+  if (!pack.empty())
+    store_pack_kernel<<<std::min<int>(int(pack.size()), 148 * 8), 128, 0, sm>>>(
+        st->d_items, int(pack.size()), st->d_atom_off, st->d_species, st->d_energy, st->d_pos, st->d_forces,
+        st->d_send);
+  HMTL_CUDA(cudaGetLastError());
+  if (world > 1) {
+    if (ncclGroupStart() != ncclSuccess) return fail(HMTL_ERR_COMM, "store_fetch: ncclGroupStart");
+    ncclResult_t r = ncclSuccess;
+    for (int p = 0; p < world && r == ncclSuccess; ++p) {
+      if (p == rank) continue;
+      if (send_b[p]) r = ncclSend(st->d_send + send_off[p], size_t(send_b[p]), ncclUint8, p, comm, sm);
+      if (r == ncclSuccess && recv_b[p]) r = ncclRecv(st->d_recv + recv_off[p], size_t(recv_b[p]), ncclUint8, p, comm, sm);
+    }
+    const ncclResult_t r2 = ncclGroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+      return fail(HMTL_ERR_COMM, std::string("store_fetch: NCCL send/recv: ") +
+                                     ncclGetErrorString(r != ncclSuccess ? r : r2));
+  }
+  kl(store_assemble_kernel, dim3(n), dim3(128), 0, sm, static_cast<const FetchItem*>(st->d_items + pack.size()), n,
+     static_cast<const long long*>(st->d_atom_off), static_cast<const uint8_t*>(st->d_species),
+     static_cast<const double*>(st->d_energy), static_cast<const double*>(st->d_pos),
+     static_cast<const double*>(st->d_forces), static_cast<const uint8_t*>(st->d_recv), c.arena);
+  HMTL_CUDA(cudaEventRecord(st->staged, sm));
+  HMTL_CUDA(cudaGetLastError());
+  c.host_G = n;
+  c.host_N = int(N);
+  return HMTL_OK;
+}
+
 int hmtl_store_destroy(hmtl_store* st) {
   if (!st) return HMTL_OK;
   cudaSetDevice(st->device);
   if (st->staged) cudaEventSynchronize(st->staged), cudaEventDestroy(st->staged);
-  void* ptrs[] = {st->d_atom_off, st->d_ds, st->d_species, st->d_energy, st->d_pos, st->d_forces, st->d_sel};
+  void* ptrs[] = {st->d_atom_off, st->d_ds,    st->d_species, st->d_energy, st->d_pos,
+                  st->d_forces,   st->d_sel,   st->d_items,   st->d_send,   st->d_recv};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (st->h_stage) cudaFreeHost(st->h_stage);
+  if (st->h_items) cudaFreeHost(st->h_items);
   delete st;
   return HMTL_OK;
 }

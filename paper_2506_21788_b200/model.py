@@ -358,6 +358,10 @@ class ModelT:
         check(lib().hmtl_debug_fetch(self._ctx, name.encode(), layer, _fp(out), out.size, C.byref(n)))
         return out[: n.value]
 
+    def comm_init(self, uid: bytes, world: int, rank: int) -> None:
+        """NCCL world communicator + per-head sub-groups (hmtl/mesh.hpp:322-334)."""
+        check(lib().hmtl_comm_init(self._ctx, (C.c_uint8 * 128)(*bytes(uid)), world, rank))
+
     def save_checkpoint(self, path: str, with_optimizer: bool = True) -> None:
         """HMTP checkpoint (save_checkpoint, src/model_io.cpp:62-84) + AdamW resume section."""
         check(lib().hmtl_checkpoint_save(self._ctx, path.encode(), int(with_optimizer)))
@@ -391,6 +395,36 @@ def _ip(a):
 
 
 # ---------------------------------------------------------------- data plane
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0 makes it; ship it to the others out of band)."""
+    b = (C.c_uint8 * 128)()
+    check(lib().hmtl_comm_unique_id(b))
+    return bytes(b)
+
+
+def shard_range(count: int, n: int, i: int) -> tuple:
+    """balanced_split(count, n)[i] (src/datastore.cpp:11-23): [begin, end)."""
+    b, e = C.c_uint64(), C.c_uint64()
+    check(lib().hmtl_shard_range(count, n, i, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+def make_partition(counts: dict, world: int, mode: str = "base", members: dict | None = None) -> dict:
+    """make_partition (src/datastore.cpp:25-45): {dataset id: (count, serving ranks
+    ascending, [(begin, end) per serving rank])}.  base: every rank serves every
+    dataset; taskpar: the dataset's head group (members[id], any placement)."""
+    out = {}
+    for d in sorted(counts):
+        if mode == "taskpar":
+            if members is None or d not in members:
+                raise ValueError(f"taskpar: dataset id {d} has no head sub-group")
+            serving = sorted(int(r) for r in members[d])
+        else:
+            serving = list(range(world))
+        out[int(d)] = (int(counts[d]), serving, [shard_range(int(counts[d]), len(serving), i) for i in range(len(serving))])
+    return out
+
+
 def epoch_plan(mode: str, counts: dict, world: int, seed: int, b_local: int, rank: int,
                members: dict | None = None):
     """shuffle_epoch (hmtl/datastore.hpp:48-75, src/datastore.cpp:47-97) for one rank:
@@ -485,6 +519,43 @@ class SampleStore:
         idx = np.ascontiguousarray(idx, np.uint64)
         check(lib().hmtl_store_bind(model.ctx, self._h, ds.ctypes.data_as(C.POINTER(C.c_uint8)),
                                     idx.ctypes.data_as(C.POINTER(C.c_uint64)), len(ds), stream))
+        self._bound(model)
+
+    @staticmethod
+    def sharded(model: "ModelT", shard: Samples, partition: dict) -> "SampleStore":
+        """This rank's shard only (DataStore, src/datastore.cpp:99-145); collective
+        over the model's communicator.  partition = {dataset id: (count, serving
+        ranks ascending)}; shard = the samples of this rank's ranges, dataset by
+        dataset in ascending id order (see shard_range)."""
+        ids = np.array(sorted(partition), np.uint8)
+        counts = np.array([partition[int(i)][0] for i in ids], np.uint64)
+        mem = [list(partition[int(i)][1]) for i in ids]
+        members = np.array([r for m in mem for r in m] or [0], np.int32)
+        off = np.zeros(len(ids) + 1, np.int32)
+        off[1:] = np.cumsum([len(m) for m in mem])
+        h = C.c_void_p()
+        check(lib().hmtl_store_create_sharded(model.ctx, C.byref(shard.as_c()), ids.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                              counts.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                              members.ctypes.data_as(C.POINTER(C.c_int)),
+                                              off.ctypes.data_as(C.POINTER(C.c_int)), len(ids), C.byref(h)))
+        st = SampleStore(None, model.device, _handle=h)
+        st._pool = shard
+        return st
+
+    def fetch(self, model: "ModelT", plan_ds, plan_idx, stream=None) -> None:
+        """fetch_samples(plan, step) (src/datastore.cpp:192-248): plan_ds/plan_idx are
+        this step's [world, b_local] plan rows of every rank; collective."""
+        ds = np.ascontiguousarray(plan_ds, np.uint8)
+        idx = np.ascontiguousarray(plan_idx, np.uint64)
+        check(lib().hmtl_store_fetch(model.ctx, self._h, ds.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                     idx.ctypes.data_as(C.POINTER(C.c_uint64)), ds.shape[-1], stream))
+        self._bound(model)
+
+    @staticmethod
+    def _bound(model: "ModelT") -> None:  # the model's host view of the batch the device now holds
+        G, N = C.c_int(), C.c_int()
+        check(lib().hmtl_batch_shape(model.ctx, C.byref(G), C.byref(N)))
+        model._G, model._N = G.value, N.value
 
     def close(self) -> None:
         if getattr(self, "_h", None):

@@ -180,6 +180,18 @@ def epoch_plans():
     np.savez_compressed(os.path.join(HERE, "epoch_plan.npz"), **out)
 
 
+def partitions():
+    """make_partition (src/datastore.cpp:25-45) of the reference for every EPOCH_CASES mesh."""
+    O.build(ref=True)
+    ref = O.Ref()
+    out = {}
+    for i, (counts, ng, rep, mode, seed, b) in enumerate(EPOCH_CASES):
+        part = ref.make_partition(counts, ng, rep, mode)
+        for d, rows in part.items():
+            out[f"c{i}_d{d}"] = np.array(rows, np.int64).reshape(-1, 3)
+    np.savez_compressed(os.path.join(HERE, "partition.npz"), **out)
+
+
 def hmtd_files():
     O.build(ref=True)
     ref = O.Ref()
@@ -213,6 +225,8 @@ if __name__ == "__main__":
         ckpt_files()
     elif sys.argv[1:] == ["epoch_plan"]:
         epoch_plans()
+    elif sys.argv[1:] == ["partition"]:
+        partitions()
     elif sys.argv[1:] == ["hmtd"]:
         hmtd_files()
     else:

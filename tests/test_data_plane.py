@@ -41,6 +41,28 @@ def test_epoch_plan_matches_reference(case):
         assert np.array_equal(ix, g[f"c{case}_r{r}_idx"]), (case, r)
 
 
+@pytest.mark.parametrize("case", range(len(EPOCH_CASES)))
+def test_partition_matches_reference(case):
+    """make_partition / balanced_split (src/datastore.cpp:11-45) vs the reference's own
+    (tests/golden/partition.npz): serving ranks and shard ranges per dataset."""
+    g = np.load(os.path.join(GOLDEN, "partition.npz"))
+    counts, ng, rep, mode, seed, b = EPOCH_CASES[case]
+    members = mesh_members(counts, ng, rep) if mode == 1 else None
+    part = P.make_partition(counts, ng * rep, "taskpar" if mode == 1 else "base", members)
+    for d, (cnt, serving, ranges) in part.items():
+        mine = np.array([(r, lo, hi) for r, (lo, hi) in zip(serving, ranges)], np.int64)
+        assert np.array_equal(mine, g[f"c{case}_d{d}"]), (case, d)
+        assert cnt == counts[d] and ranges[0][0] == 0 and ranges[-1][1] == cnt
+
+
+def test_shard_range_errors():
+    with pytest.raises(P.HmtlError):
+        P.shard_range(10, 0, 0)
+    with pytest.raises(P.HmtlError):
+        P.shard_range(10, 3, 3)
+    assert [P.shard_range(10, 4, i) for i in range(4)] == [(0, 3), (3, 6), (6, 8), (8, 10)]
+
+
 def test_taskpar_routing_and_coverage_general_placement():
     """Placement groups of different sizes (5 heads on 8 ranks, shares {1,1,1,2,3}):
     every rank draws only its group's dataset, replicas get disjoint samples,

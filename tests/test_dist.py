@@ -63,3 +63,25 @@ def test_nccl_matches_oracle_emulation(tmp_path):
         assert O.rel_vec_error(g[f"r{r}_shared"], o[f"r{r}_shared"]) < 1e-4
         for k in heads_of(g, r):
             assert O.rel_vec_error(g[f"r{r}_head{k}"], o[f"r{r}_head{k}"]) < 1e-4
+
+
+@pytest.mark.gpu
+def test_sharded_store_fetch(tmp_path):
+    """Sharded DataStore over NCCL: every rank keeps only its
+    make_partition shard; a fetched batch (local gather + NCCL send/recv of the
+    remote samples) gives forward predictions bit-identical to the same plan rows
+    bound from a replicated store, in base and taskpar partitions.  On a 1-GPU box
+    this runs world 1 (all samples local); with >= 2 GPUs, world 2."""
+    import torch
+
+    world = 2 if torch.cuda.device_count() >= 2 else 1
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29561", os.path.join(ROOT, "tests", "dist_store.py"),
+           str(tmp_path / "s.npz")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=dict(os.environ, OMP_NUM_THREADS="1"))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    d = dict(np.load(tmp_path / "s.npz"))
+    for rk in range(world):
+        assert d[f"r{rk}_base_ok"] and d[f"r{rk}_taskpar_ok"], rk
+    if world > 1:
+        assert sum(int(d[f"r{rk}_base_remote"]) for rk in range(world)) > 0  # the exchange was exercised
