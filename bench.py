@@ -39,6 +39,7 @@ UNIT_EDGES = 48000  # per-GPU edge budget of one step
 HYPER = dict(n_species=20, layers=4, hidden=128, head_width=128, head_depth=3, n_heads=5, cutoff=5.0)
 N_BATCHES = 4  # distinct batches cycled per rank
 WORKLOAD = "mtl5-weak"
+DEVHDR_BYTES = 240  # sizeof(DevHdr) (csrc/common.cuh): the per-step D2H result read (loss + error bits)
 
 
 def batch_counts():
@@ -483,18 +484,30 @@ def run_b200(args, rank, world, local_rank, dist):
     structs_per_step = world * sum(counts)  # sum over ranks of their batches
     value = structs_per_step * args.steps / (dev_ms / 1e3)
 
-    # ---- e2e through the public API: host samples -> pinned arena -> H2D -> step -> D2H loss
-    e2e_s = 0.0
+    # ---- e2e through the public API: host samples -> pinned arena -> H2D -> step -> D2H loss,
+    # every step; pipelined as a trainer loop runs it: the host packs step i+1 into the
+    # second pinned arena and launches it before blocking on step i's loss (pinned ring)
     h2d = 0
+    losses = []
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
     for i in range(args.steps):
         b = batches[i % len(batches)]
-        with torch.cuda.stream(ext):
-            flush.zero_()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        model.train_step(b, cfg, read_loss=True)
-        e2e_s += time.perf_counter() - t0
+        if args.e2e_flush:
+            with torch.cuda.stream(ext):
+                flush.zero_()
+        # (default: flushed, as the device-timed loop; --e2e-no-flush drops it -- a trainer
+        # loop has none, and a step streams ~2.7 GB of algorithmic traffic through L2)
+        model.train_step(b, cfg, read_loss=False)
+        model.post_loss(i)
         h2d += arena_bytes(b.G, b.N)
+        if i:
+            losses.append(model.wait_loss(i - 1))
+    losses.append(model.wait_loss(args.steps - 1))
+    e2e_s = time.perf_counter() - t0
+    assert all(np.isfinite(losses))
     e2e_s = max_over_ranks(e2e_s)
     e2e = structs_per_step * args.steps / e2e_s
 
@@ -540,7 +553,10 @@ def run_b200(args, rank, world, local_rank, dist):
                        "l2": "flushed (256 MB write) between timed steps", "cuda_graph": cfg.use_graph,
                        "final_loss": final_loss},
             "e2e": {"value": round(e2e, 2), "unit": "structures/s",
-                    "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": 240},
+                    "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": DEVHDR_BYTES,
+                    "timing": "wall clock over all steps, max over ranks; host pack + H2D of step i+1 overlap step i; "
+                              + ("L2 flushed between steps" if args.e2e_flush else
+                                 "no L2 flush (the step's own H2D inputs; ~2.7 GB/step through L2)")},
             "gpu_launches": int(round(launches_per_step * args.steps)),
             "roofline": roof, "roofline_gather_scatter": roof_gs, "clocks": clocks,
             "cpu_baseline": cpu, **({"comm": nb, "rank_ms_per_step": rank_ms} if nb else {}),
@@ -558,6 +574,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-no-flush", dest="e2e_flush", action="store_false",
+                    help="no L2 flush between the e2e loop's steps (default: flushed)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -240,6 +240,13 @@ int hmtl_predictions(hmtl_ctx* ctx, float* energy, float* forces);
 /* SPEC loss: loss on device + upstreams dE[G], dF[3N]. */
 int hmtl_loss(hmtl_ctx* ctx, float w_energy, float w_force, void* stream);
 int hmtl_read_loss(hmtl_ctx* ctx, float* loss); /* syncs */
+/* Pipelined trainer loop: loss_post enqueues the D2H read of the current
+ * step's result (loss + error bits, one DevHdr) into pinned ring slot
+ * `slot % 8` on `stream` without syncing; loss_wait blocks on that slot only and
+ * reports the reference's errors as read_loss does.  A loop can launch step
+ * i+1 before reading step i's loss. */
+int hmtl_loss_post(hmtl_ctx* ctx, int slot, void* stream);
+int hmtl_loss_wait(hmtl_ctx* ctx, int slot, float* loss);
 /* ModelT::backward, hmtl/model.hpp:490-625.  d_energy/d_forces are HOST
  * upstreams [G], [3N]; pass NULL for both to use the device upstreams of
  * hmtl_loss. */

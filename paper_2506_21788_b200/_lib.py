@@ -121,6 +121,8 @@ SIGNATURES = {
     "hmtl_store_bind": (C.c_int, [_P, _P, _U8P, C.POINTER(C.c_uint64), C.c_int, _P]),
     "hmtl_store_destroy": (C.c_int, [_P]),
     "hmtl_batch_shape": (C.c_int, [_P, _IP, _IP]),
+    "hmtl_loss_post": (C.c_int, [_P, C.c_int, _P]),
+    "hmtl_loss_wait": (C.c_int, [_P, C.c_int, C.POINTER(C.c_float)]),
     "hmtl_shard_range": (C.c_int, [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "hmtl_store_create_sharded": (C.c_int, [_P, C.POINTER(CSamples), _U8P, C.POINTER(C.c_uint64), _IP, _IP, C.c_int,
                                             C.POINTER(_P)]),

@@ -91,6 +91,12 @@ void free_ctx(Ctx& c) {
     if (p) cudaFree(p);
   for (auto* p : c.pool) cudaFree(p);
   if (c.h_arena) cudaFreeHost(c.h_arena);
+  if (c.h_arena2) cudaFreeHost(c.h_arena2);
+  for (auto& e : c.h_arena_ev)
+    if (e) cudaEventDestroy(e);
+  if (c.h_hdr_ring) cudaFreeHost(c.h_hdr_ring);
+  for (auto& e : c.hdr_ev)
+    if (e) cudaEventDestroy(e);
   if (c.h_cells) cudaFreeHost(c.h_cells);
   if (c.step_exec) cudaGraphExecDestroy(c.step_exec);
   if (c.prof_exec) cudaGraphExecDestroy(c.prof_exec);
@@ -351,7 +357,11 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   cudaMemset(c.hdr, 0, sizeof(DevHdr));
   cudaMemcpy(c.d_slot_of, c.slot_of, 256 * sizeof(int), cudaMemcpyHostToDevice);
   c.h_arena_cap = c.arena_cap;
-  if (cudaMallocHost(&c.h_arena, c.h_arena_cap) != cudaSuccess) {
+  bool pinned_ok = cudaMallocHost(&c.h_arena2, c.h_arena_cap) == cudaSuccess &&
+                   cudaMallocHost(&c.h_hdr_ring, sizeof(DevHdr) * Ctx::kLossRing) == cudaSuccess;
+  for (auto& e : c.h_arena_ev) pinned_ok = pinned_ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+  for (auto& e : c.hdr_ev) pinned_ok = pinned_ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+  if (!pinned_ok || cudaMallocHost(&c.h_arena, c.h_arena_cap) != cudaSuccess) {
     free_ctx(c);
     delete h;
     return fail(HMTL_ERR_INTERNAL, "cudaMallocHost failed");
@@ -486,11 +496,17 @@ int hmtl_batch_upload(hmtl_ctx* h, const hmtl_samples* s, void* stream) {
   c.pbc = false;
   cudaSetDevice(c.device);
   cudaStream_t st = pick(c, stream);
-  // the pinned staging buffer may still be read by a previous async copy
-  HMTL_CUDA(cudaStreamSynchronize(st));
+  // two pinned staging arenas used alternately: packing this batch waits only for
+  // the copy that last read this buffer, so the host packs step i+1 while the
+  // device still runs step i (the copy itself is stream-ordered after it)
+  const int k = c.h_arena_k;
+  uint8_t* buf = k ? c.h_arena2 : c.h_arena;
+  HMTL_CUDA(cudaEventSynchronize(c.h_arena_ev[k]));
   size_t bytes = 0;
-  if (int rc = pack(c, s, c.h_arena, c.h_arena_cap, &bytes)) return rc;
-  HMTL_CUDA(cudaMemcpyAsync(c.arena, c.h_arena, bytes, cudaMemcpyHostToDevice, st));
+  if (int rc = pack(c, s, buf, c.h_arena_cap, &bytes)) return rc;
+  HMTL_CUDA(cudaMemcpyAsync(c.arena, buf, bytes, cudaMemcpyHostToDevice, st));
+  HMTL_CUDA(cudaEventRecord(c.h_arena_ev[k], st));
+  c.h_arena_k = k ^ 1;
   return 0;
 }
 
@@ -500,6 +516,7 @@ int hmtl_batch_upload_pbc(hmtl_ctx* h, const hmtl_samples* s, const double* cell
   cudaSetDevice(c.device);
   cudaStream_t st = pick(c, stream);
   HMTL_CUDA(cudaStreamSynchronize(st));  // the pinned staging buffers may still be read
+  for (auto& e : c.h_arena_ev) HMTL_CUDA(cudaEventSynchronize(e));
   size_t bytes = 0;
   if (int rc = pack(c, s, c.h_arena, c.h_arena_cap, &bytes, true)) return rc;
   if (!c.h_cells) HMTL_CUDA(cudaMallocHost(&c.h_cells, size_t(c.Gc) * 9 * sizeof(double)));
@@ -612,6 +629,39 @@ int hmtl_read_loss(hmtl_ctx* h, float* loss) {
   DevHdr hd;
   HMTL_CUDA(cudaMemcpy(&hd, c.hdr, sizeof hd, cudaMemcpyDeviceToHost));
   *loss = float(hd.loss);
+  return 0;
+}
+
+namespace {
+int hdr_errors(const DevHdr& h) {  // the reference's errors for the device error bits (as check_hdr)
+  if (h.err & kErrUnowned) return fail(HMTL_ERR_CONTRACT, "model: unknown dataset id (head not owned by this rank)");
+  if (h.err & kErrEmptyGraph) return fail(HMTL_ERR_CONTRACT, "build_batch: empty graph rejected");
+  if (h.err & kErrEdgeOverflow) return fail(HMTL_ERR_CONTRACT, "build_batch: edge capacity exceeded");
+  if (h.err & kErrNonFinite) return fail(HMTL_ERR_CONTRACT, "model: non-finite prediction");
+  return 0;
+}
+}  // namespace
+
+int hmtl_loss_post(hmtl_ctx* h, int slot, void* stream) {
+  Ctx& c = h->c;
+  if (slot < 0) return fail(HMTL_ERR_CONTRACT, "loss_post: negative slot");
+  cudaSetDevice(c.device);
+  cudaStream_t st = pick(c, stream);
+  const int k = slot % Ctx::kLossRing;
+  HMTL_CUDA(cudaEventSynchronize(c.hdr_ev[k]));  // the slot's previous read has landed
+  HMTL_CUDA(cudaMemcpyAsync(c.h_hdr_ring + k, c.hdr, sizeof(DevHdr), cudaMemcpyDeviceToHost, st));
+  HMTL_CUDA(cudaEventRecord(c.hdr_ev[k], st));
+  return 0;
+}
+
+int hmtl_loss_wait(hmtl_ctx* h, int slot, float* loss) {
+  Ctx& c = h->c;
+  if (slot < 0 || !loss) return fail(HMTL_ERR_CONTRACT, "loss_wait: bad argument");
+  cudaSetDevice(c.device);
+  const int k = slot % Ctx::kLossRing;
+  HMTL_CUDA(cudaEventSynchronize(c.hdr_ev[k]));
+  if (int rc = hdr_errors(c.h_hdr_ring[k])) return rc;
+  *loss = float(c.h_hdr_ring[k].loss);
   return 0;
 }
 

@@ -57,6 +57,15 @@ struct Ctx {
   size_t arena_cap = 0;
   uint8_t* h_arena = nullptr;
   size_t h_arena_cap = 0;
+  // second pinned staging arena: batch_upload alternates and waits only for the
+  // copy that last read the buffer (two uploads back), not for the stream
+  uint8_t* h_arena2 = nullptr;
+  cudaEvent_t h_arena_ev[2] = {nullptr, nullptr};
+  int h_arena_k = 0;
+  // pinned ring of device headers for pipelined loss reads (hmtl_loss_post/wait)
+  static constexpr int kLossRing = 8;
+  DevHdr* h_hdr_ring = nullptr;
+  cudaEvent_t hdr_ev[kLossRing] = {};
   std::vector<uint8_t*> pool;
   std::vector<size_t> pool_bytes;
   int host_G = 0, host_N = 0;  // last bound batch (host view)

@@ -373,6 +373,16 @@ class ModelT:
     def adamw(self, cfg: TrainConfig) -> None:
         check(lib().hmtl_adamw(self._ctx, C.byref(cfg.c()), None))
 
+    def post_loss(self, slot: int, stream=None) -> None:
+        """Enqueue the D2H read of this step's loss into pinned ring slot `slot` (no sync)."""
+        check(lib().hmtl_loss_post(self._ctx, slot, stream))
+
+    def wait_loss(self, slot: int) -> float:
+        """Block on ring slot `slot` only; the loss posted there (errors as read_loss)."""
+        L = C.c_float()
+        check(lib().hmtl_loss_wait(self._ctx, slot, C.byref(L)))
+        return float(L.value)
+
     def train_step(self, s: Samples | None, cfg: TrainConfig, stream=None, read_loss: bool = True):
         """train_step -- uploads `s` (if given) and runs the whole
         stream-ordered step; returns the loss (syncs) when read_loss."""

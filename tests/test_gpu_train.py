@@ -79,6 +79,32 @@ def test_cuda_graph_step_equals_eager_step():
     assert np.array_equal(res[0][1], res[1][1])
 
 
+def test_pipelined_steps_equal_synchronous_steps():
+    """The trainer-loop pipeline (double-buffered pinned staging: batch i+1 packed and
+    launched before step i's loss is read from the pinned result ring) gives the
+    synchronous loop's losses and parameters bit for bit."""
+    hp = P.ModelHyper(20, 2, 32, 32, 3, 5, 5.0)
+    xs = [batch((3, 2, 2, 1, 1), 1), batch((4, 1, 3, 2, 1), 2), batch((2, 2, 2, 2, 2), 3)]
+    caps = P.Caps.for_samples(xs[0]).union(P.Caps.for_samples(xs[1])).union(P.Caps.for_samples(xs[2]))
+    cfg = P.TrainConfig(use_graph=True)
+    seq = xs * 3
+    m = P.ModelT(hp, 7, range(5), caps=caps)
+    sync = [m.train_step(x, cfg) for x in seq]
+    ref = m.shared_block()
+    m.close()
+    m = P.ModelT(hp, 7, range(5), caps=caps)
+    piped = []
+    for i, x in enumerate(seq):
+        m.train_step(x, cfg, read_loss=False)
+        m.post_loss(i)
+        if i:
+            piped.append(m.wait_loss(i - 1))
+    piped.append(m.wait_loss(len(seq) - 1))
+    assert piped == sync
+    assert np.array_equal(m.shared_block(), ref)
+    m.close()
+
+
 def test_loss_curve_100_steps_matches_fp64_oracle():
     """Loss curves over 100 steps (north star).  Same batches, same seeds; the
     FP32 B200 path vs the FP64 restatement of the reference."""
