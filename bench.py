@@ -213,7 +213,7 @@ KERNEL_SCOPES = [  # kernel-name pattern -> scope of kernel_work (first match wi
     (r"chain_kernel<0", "fwd.node_chain"), (r"chain_kernel<[34]", "bwd.node_chain"),
     (r"TcRow<.*::MsgProb>", "fwd.edge_msg_gemm"), (r"TcRow<.*::L7Prob>", "bwd.edge_dz1_gemm"),
     (r"TcRow<.*::PProb>", "fwd.node_P"), (r"TcRow<.*::L11Prob>", "bwd.edge_dh_gemm"),
-    (r"TcRow<.*::ForceProb>", "fwd.force_edge_gemm"), (r"TcRow<.*::FDxProb>", "bwd.force_edge_dx"),
+    (r"TcRow<.*::ForceProb>", "fwd.force_edge_gemm"), (r"TcRow<.*::FDxS?f?Prob>", "bwd.force_edge_dx"),
     (r"TcRed<.*::L6Prob>", "bwd.edge_w2grad"), (r"TcRed<.*::L2Prob>", "bwd.node_w2grad"),
     (r"TcRed<.*::L3Prob>", "bwd.node_w1grad"), (r"TcRed<.*::L10Prob>", "bwd.edge_w1ab_grad"),
     (r"TcRed<.*::FGradProb>", "bwd.force_edge_wgrad"),

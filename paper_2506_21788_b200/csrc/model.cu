@@ -1211,6 +1211,30 @@ struct FGradProb {  // force MLP layer i >= 1 weight+bias (edge rows per head)
   __device__ float b(int, int e, int n) const { return dz[size_t(e) * ldz + n]; }
   __device__ void store(int seg, int k, int n, float v) const { G.at(seg)[size_t(k) * Ncols + n] = v; }
 };
+// FDxProb's layer-1 case with silu'(zf0) materialised by edge_af0 (the TC
+// configuration): no row context, no gather branch -> no spills in the engine
+struct FDxSfProb {  // dz_0 = (dz_1 W_1^T) * sf0
+  BDesc bd() const { return BDesc{Wt.base + Wt.off, nullptr, 0, 0, 1, K, K, Ncols, rows.nseg, (long long)Wt.PH, nullptr}; }
+  static constexpr const char* kName = "bwd.force_edge_dx";
+  struct Aux {
+    float4 v;
+  };
+  __device__ float4 a4(int, int e, int k) const { return ld4(dz + size_t(e) * ldz + k); }
+  __device__ Aux epi_aux(int, int e, int n) const { return Aux{ld4(sf0 + size_t(e) * W + n)}; }
+  __device__ void epi4a(int, int e, int n, float4 acc, const Aux& a) const {
+    st4(out + size_t(e) * W + n, mul4(acc, a.v));
+  }
+  RowSet rows;
+  int K, Ncols, W;
+  const float* dz;
+  int ldz;
+  HeadW Wt;
+  float* out;
+  const float* sf0;
+  __device__ float a(int, int e, int k) const { return dz[size_t(e) * ldz + k]; }
+  __device__ float b(int seg, int k, int n) const { return Wt.at(seg)[size_t(n) * K + k]; }
+  __device__ void epi(int, int e, int n, float acc) const { out[size_t(e) * W + n] = acc * sf0[size_t(e) * W + n]; }
+};
 struct FDxProb {  // dz_{i-1} = (dz_i W_i^T) * silu'(z_{i-1})
   BDesc bd() const { return BDesc{Wt.base + Wt.off, nullptr, 0, 0, 1, K, K, Ncols, rows.nseg, (long long)Wt.PH, nullptr}; }
   static constexpr const char* kName = "bwd.force_edge_dx";
@@ -1968,10 +1992,15 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
                    c.edge_src, Wd, B0, HeadG{c.head_grads(), c.PH, c.head_off("force.W" + std::to_string(i))},
                    c.store_af0 ? c.af0 : nullptr};
       atb(gq, c, c.nsplit_edge, sw, c.Ec);
-      FDxProb dq{edge_rows_by_head(c), out, W, H, W, i, c.Ec, c.Qf, c.zf, c.dist, dz, ldz, c.edge_dst, c.edge_src,
-                 Wd, B0, HeadW{c.head_params(), c.PH, c.head_off("force.W" + std::to_string(i))}, nxt,
-                 c.store_sf0 ? c.sf0 : nullptr};
-      ab(dq, c.Ec, c.S, st, sm, c);
+      const HeadW Wi{c.head_params(), c.PH, c.head_off("force.W" + std::to_string(i))};
+      if (i == 1 && c.store_sf0) {
+        FDxSfProb dq{edge_rows_by_head(c), out, W, W, dz, ldz, Wi, nxt, c.sf0};
+        ab(dq, c.Ec, c.S, st, sm, c);
+      } else {
+        FDxProb dq{edge_rows_by_head(c), out, W, H, W, i, c.Ec, c.Qf, c.zf, c.dist, dz, ldz, c.edge_dst, c.edge_src,
+                   Wd, B0, Wi, nxt, c.store_sf0 ? c.sf0 : nullptr};
+        ab(dq, c.Ec, c.S, st, sm, c);
+      }
       dz = nxt;
       ldz = W;
     }
