@@ -585,6 +585,15 @@ __global__ void bimg_prob_kernel(P p, float* __restrict__ out, int nseg) {
     o[size_t(tc::KC) * N + off] = x - h;
   }
 }
+template <class P, class = void>
+struct HasTmaFin : std::false_type {};
+template <class P>
+struct HasTmaFin<P, std::void_t<decltype(std::declval<const P&>().xfin(float4{}))>> : std::true_type {};
+template <class P, class = void>
+struct HasTma : std::false_type {};
+template <class P>
+struct HasTma<P, std::void_t<decltype(&P::tma)>> : std::true_type {};
+
 template <class P>
 struct TcRed {
   RowSet rows;
@@ -601,6 +610,12 @@ struct TcRed {
     else return make_float4(p.b(seg, row, n), p.b(seg, row, n + 1), p.b(seg, row, n + 2), p.b(seg, row, n + 3));
   }
   __device__ __forceinline__ void store(int seg, int k, int n, float v) const { p.store(seg, k, n + n_off, v); }
+  // TMA operand path (tc_red_tma_kernel): elementwise transforms of the raw rows
+  __device__ __forceinline__ float4 xfin(float4 v) const {
+    if constexpr (HasTmaFin<P>::value) return p.xfin(v);
+    else return v;
+  }
+  __device__ __forceinline__ float4 yfin(float4 v) const { return v; }
 };
 
 // one launch builds every B image of the step: blockIdx.y = job
@@ -680,10 +695,31 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
     const int mtiles = (M + 127) / 128;
     const long long chunks = (rows_cap > 0 ? rows_cap : (long long)c.Ec) / tc::KC + 1;
     // enough CTAs to fill the GPU, >= 4 chunks each (bounded partial traffic)
-    long long want = std::max<long long>(1, (long long)c.sm_count / (mtiles * p.rows.nseg));  // one wave
-    int ns = int(std::max<long long>(1, std::min<long long>(want, chunks / 4)));
+    // one wave over red_sms SMs (side-stream weight gradients leave the rest to the critical path)
+    long long want = std::max<long long>(1, (long long)c.red_sms / (mtiles * p.rows.nseg));
+    int ns = int(std::max<long long>(1, std::min<long long>(want, chunks / c.red_min_chunks)));
     float* partial = c.part(st);
     while (ns > 1 && size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * NW > c.partial_cap) ns /= 2;
+    if constexpr (HasTma<P>::value) {  // plain row-major operands over contiguous rows: TMA path
+      const float *xb = nullptr, *yb = nullptr;
+      int ldx = 0, ldy = 0;
+      p.tma(&xb, &ldx, &yb, &ldy);
+      CUtensorMap mx, my;
+      const long long cap_rows = rows_cap > 0 ? rows_cap : (long long)c.Ec;
+      if (c.red_tma && xb && yb && !p.rows.perm && p.Ncols <= 128 && mtiles == 1 &&
+          size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * NW <= c.partial_cap && tc::tmap_2d(&mx, xb, cap_rows, ldx) &&
+          tc::tmap_2d(&my, yb, cap_rows, ldy)) {
+        const size_t SB = tc::red_stage_bytes(NW);
+        const int stages = int(std::min<size_t>(4, (tc::kSmemLimit - size_t(32) * NW * 4 - 4096) / SB));
+        const size_t smem = tc::tc_red_tma_smem(NW, stages);
+        set_smem(tc::tc_red_tma_kernel<TcRed<P>>, smem);
+        TcRed<P> q{p.rows, M, NW, P::kBias, p, 0};
+        kl(tc::tc_red_tma_kernel<TcRed<P>>, dim3(mtiles, ns, p.rows.nseg), tc::kRedTmaThreads, smem, st, q, mx, my,
+           partial, ns, stages);
+        tc::tc_red_reduce(q, partial, ns, st);
+        return;
+      }
+    }
     if (size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * NW <= c.partial_cap) {
       const size_t smem = tc::tc_red_smem(NW);
       set_smem(tc::tc_red_kernel<TcRed<P>>, smem);
@@ -1369,6 +1405,8 @@ struct L2Prob {  // [g_nW2; g_nb2] = [silu(vz1), 1]^T dh
   int K, Ncols, H;
   const float *vz1, *dh;
   float* G;
+  void tma(const float** x, int* ldx, const float** y, int* ldy) const { *x = vz1, *ldx = H, *y = dh, *ldy = H; }
+  __device__ float4 xfin(float4 v) const { return silu4(v); }
   __device__ float a(int, int r, int k) const { return k < H ? silu(vz1[size_t(r) * H + k]) : 1.f; }
   __device__ float b(int, int r, int n) const { return dh[size_t(r) * H + n]; }
   __device__ void store(int, int k, int n, float v) const { G[size_t(k) * H + n] = v; }
@@ -1441,6 +1479,9 @@ struct L6Prob {  // [g_eW2; g_eb2] = [silu(z1), 1]^T dz2   (E rows)
   float* G;
   const float* a1s;  // a1 materialised by the forward producer (nullable)
   const float *dagg, *z2s;  // non-null: dz2 = dagg[dst] * silu'(z2) computed on the fly
+  void tma(const float** x, int* ldx, const float** y, int* ldy) const {
+    *x = a1s, *ldx = H, *y = dagg ? nullptr : dz2, *ldy = H;
+  }
   __device__ float a(int, int e, int k) const {
     return k < H ? silu(z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, k)) : 1.f;
   }

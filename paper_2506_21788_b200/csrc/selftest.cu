@@ -42,6 +42,8 @@ struct StRed {
     return *reinterpret_cast<const float4*>(Y + size_t(r) * Ncols + n);
   }
   __device__ void store(int, int m, int n, float v) const { C[size_t(m) * Ncols + n] = v; }
+  __device__ float4 xfin(float4 v) const { return v; }
+  __device__ float4 yfin(float4 v) const { return v; }
 };
 
 __global__ void st_bimg(const float* B, int K, int N, float* out) {  // B is [K][N]
@@ -60,6 +62,12 @@ __global__ void st_bimg(const float* B, int K, int N, float* out) {  // B is [K]
 }  // namespace hmtl_b200
 
 using namespace hmtl_b200;
+
+namespace hmtl_b200 {
+namespace {
+__global__ void set_dbg(int v) { tc::g_tc_debug = v; }
+}  // namespace
+}  // namespace hmtl_b200
 
 extern "C" int hmtl_selftest_gemm(int mode, int variant, int rows, int K, int N, const float* X, const float* Y,
                                   float* C) {
@@ -90,10 +98,24 @@ extern "C" int hmtl_selftest_gemm(int mode, int variant, int rows, int K, int N,
   } else {
     StRed p{rs, K, N, 0, dX, dY, dC};
     const int ns = 4;
-    const size_t smem = tc::tc_red_smem(N);
-    cudaFuncSetAttribute(tc::tc_red_kernel<StRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     dim3 grid((K + 127) / 128, ns, 1);
-    tc::tc_red_kernel<StRed><<<grid, tc::kRedThreads, smem>>>(p, part, ns, tc::red_stages(N));
+    if (variant & 1) {  // TMA operand path; variant >> 1 -> g_tc_debug bits 8..
+      set_dbg<<<1, 1>>>((variant >> 1) << 8);
+      CUtensorMap mx, my;
+      if (!tc::tmap_2d(&mx, dX, rows, K) || !tc::tmap_2d(&my, dY, rows, N)) return fail(HMTL_ERR_INTERNAL, "tmap");
+      const size_t SB = tc::red_stage_bytes(N);
+      const int stages = int(std::min<size_t>(4, (tc::kSmemLimit - size_t(32) * N * 4 - 4096) / SB));
+      const size_t smem = tc::tc_red_tma_smem(N, stages);
+      cudaFuncSetAttribute(tc::tc_red_tma_kernel<StRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      tc::tc_red_tma_kernel<StRed><<<grid, tc::kRedTmaThreads, smem>>>(p, mx, my, part, ns, stages);
+      const cudaError_t le = cudaGetLastError();
+      if (le != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("tma launch: ") + cudaGetErrorString(le));
+      set_dbg<<<1, 1>>>(0);
+    } else {
+      const size_t smem = tc::tc_red_smem(N);
+      cudaFuncSetAttribute(tc::tc_red_kernel<StRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      tc::tc_red_kernel<StRed><<<grid, tc::kRedThreads, smem>>>(p, part, ns, tc::red_stages(N));
+    }
     tc::tc_red_reduce(p, part, ns, 0);
   }
   cudaError_t e = cudaDeviceSynchronize();
@@ -107,7 +129,6 @@ extern "C" int hmtl_selftest_gemm(int mode, int variant, int rows, int K, int N,
 // time (ms) of `iters` launches (CUDA events), for roofline work on the engine.
 namespace hmtl_b200 {
 namespace {
-__global__ void set_dbg(int v) { tc::g_tc_debug = v; }
 }  // namespace
 }  // namespace hmtl_b200
 

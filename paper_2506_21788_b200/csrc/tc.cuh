@@ -21,6 +21,8 @@
 //                   gradients: M-tile 128 features, the ROWS are the reduction
 //                   dim (K), statically split over CTAs; fixed-order reduce after.
 #pragma once
+#include <cuda.h>  // CUtensorMap (the TMA reduce GEMM's operand maps)
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -709,6 +711,224 @@ inline void tc_red_reduce(const P& p, const float* partial, int nsplit, cudaStre
   const size_t KN = size_t(Mo) * p.Ncols;
   dim3 grid(unsigned((KN + 31) / 32), p.rows.nseg);
   kl(split_reduce_kernel<RedStore<P>>, grid, 256, 0, st, partial, nsplit * KN, KN, int(KN), RedStore<P>{p, nsplit, Mo});
+}
+
+// ================================================================ reduce GEMM, TMA operands
+// Same contract as tc_red_kernel for problems whose X and Y are plain row-major
+// matrices over contiguous rows (identity RowSet): TMA brings each 32-row chunk
+// in as 32-feature x 32-row boxes swizzled in 32 B atoms -- exactly the
+// MN-major 128B_BASE32B canonical layout tcgen05 takes for tf32 (LBO = 4 KB
+// between 32-feature atoms, SBO = 512 B between 4-row groups), so neither
+// operand is transposed in registers.
+// Converter warps 0-7 then split each 16 B in place (raw -> tf32 hi, lo to the
+// lo tile at the same offset; rows past the segment end are zeroed; P::xfin /
+// P::yfin apply an elementwise transform such as silu), warp 8 issues the
+// 3xTF32 MMAs with A and B MN-major, warp 9 lane 0 keeps kStages chunks of TMA
+// loads in flight.  Deterministic: same chunk order and colsum order always.
+constexpr int kRedTmaThreads = (kRedProd + 2) * 32;
+// MN-major tf32 operands take the 128B_BASE32B layout (32 B granules of each
+// 128 B row XOR-swizzled by row % 4; atom = 4 rows x 128 B): LBO = 4 KB between
+// 32-feature boxes, SBO = 512 B between 4-row groups, layout type 1
+__device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t saddr, int dbg = 0) {
+  const uint64_t lbo = (dbg & 0x100) ? 512 : 4096, sbo = (dbg & 0x100) ? 4096 : 512;
+  return uint64_t((saddr >> 4) & 0x3FFF) | ((lbo >> 4) << 16) | ((sbo >> 4) << 32) | (uint64_t(1) << 46) |
+         (uint64_t(1) << 61);
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(m), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// 2-D tensor map over a row-major [rows x ld] fp32 matrix: 32 x 32 boxes, 128 B span
+// swizzled in 32 B atoms (the MN-major tf32 operand layout)
+inline bool tmap_2d(CUtensorMap* m, const float* base, long long rows, int ld,
+                    CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 4) % 16) return false;
+  cuuint64_t dims[2] = {cuuint64_t(ld), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(ld) * 4};
+  cuuint32_t box[2] = {32, 32}, es[2] = {1, 1};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+inline size_t tc_red_tma_smem(int N, int stages) {
+  return size_t(stages) * red_stage_bytes(N) + size_t(32) * N * 4 + 2048 + 1024;
+}
+
+template <class P>
+__global__ void __launch_bounds__(kRedTmaThreads, 1)
+    tc_red_tma_kernel(P p, const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap ty,
+                      float* __restrict__ partial, int nsplit, int kStages) {
+  extern __shared__ __align__(1024) uint8_t smem_dyn[];
+  uint8_t* smem_raw = align1k(smem_dyn);
+  const int N = p.Ncols;
+  const size_t SB = red_stage_bytes(N);
+  float* csum_smem = reinterpret_cast<float*>(smem_raw + kStages * SB);  // [32 rows][N]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + kStages * SB + size_t(32) * N * 4);
+  uint64_t* tfull = bars;                // TMA bytes landed
+  uint64_t* cfull = bars + kStages;      // converted (hi/lo) -> MMA
+  uint64_t* empty = bars + 2 * kStages;  // MMAs done -> TMA may refill
+  uint64_t* accfull = bars + 3 * kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kStages + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int mtile = blockIdx.x, split = blockIdx.y, seg = blockIdx.z;
+  const uint32_t acc_cols = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
+  constexpr int kProdThreads = kRedProd * 32;
+  if (warp == kRedProd) tmem_alloc(tmem_slot, acc_cols);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&cfull[s], kProdThreads);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&accfull[0], 1);
+    fence_mbar_init();
+  }
+  if (warp == kRedProd + 1 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tx) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&ty) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  const int rb = p.rows.begin(seg), re = p.rows.end(seg);
+  const int nchunks = (re - rb + KC - 1) / KC;
+  int my_chunks = 0;
+  for (int c = split; c < nchunks; c += nsplit) ++my_chunks;
+  const int Mo = p.M + (p.colsum ? 1 : 0);
+  float* out = partial + (size_t(seg) * nsplit + split) * size_t(Mo) * N;
+  const int m0 = mtile * 128;
+  const int Mt = p.M - m0 < 128 ? p.M - m0 : 128;
+  const int nxb = (Mt + 31) / 32, nyb = N / 32;  // 32-feature boxes per chunk
+  const bool do_colsum = p.colsum && mtile == 0;
+
+  if (warp == kRedProd + 1) {  // ------------------------------------ TMA
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int c = split; c < nchunks; c += nsplit) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        float* x_hi = reinterpret_cast<float*>(smem_raw + stage * SB);
+        float* y_hi = x_hi + 2 * 128 * KC;
+        mbar_expect_tx(&tfull[stage], uint32_t(nxb + nyb) * 32 * KC * 4);
+        const int r0 = rb + c * KC;
+        for (int b = 0; b < nxb; ++b) tma_2d(x_hi + b * 32 * KC, &tx, m0 + 32 * b, r0, &tfull[stage]);
+        for (int b = 0; b < nyb; ++b) tma_2d(y_hi + b * 32 * KC, &ty, 32 * b, r0, &tfull[stage]);
+        if (++stage == kStages) stage = 0, phase ^= 1;
+      }
+    }
+  } else if (warp < kRedProd) {  // ------------------------------- convert
+    // thread t owns 16 B slot t of every 4 KB box: row t/8 of the chunk; its 32 B
+    // granule (t%8)/2 holds logical granule ((t%8)/2) ^ (row%4) (128B_BASE32B)
+    const int row = tid >> 3, fq = (((((tid & 7) >> 1) ^ (row & 3)) << 1) | (tid & 1)) * 4;
+    float4 cs[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) cs[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int c = split; c < nchunks; c += nsplit) {
+      mbar_wait(&tfull[stage], phase);
+      float* x_hi = reinterpret_cast<float*>(smem_raw + stage * SB);
+      float* x_lo = x_hi + 128 * KC;
+      float* y_hi = x_lo + 128 * KC;
+      float* y_lo = y_hi + N * KC;
+      const bool live = rb + c * KC + row < re;
+      for (int b = 0; b < nxb; ++b) {
+        float4* h = reinterpret_cast<float4*>(x_hi + b * 32 * KC) + tid;
+        float4 v = live ? p.xfin(*h) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (m0 + 32 * b + fq >= p.M) v = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 hv = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+        *h = hv;
+        reinterpret_cast<float4*>(x_lo + b * 32 * KC)[tid] = make_float4(v.x - hv.x, v.y - hv.y, v.z - hv.z, v.w - hv.w);
+      }
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        if (b < nyb) {
+          float4* h = reinterpret_cast<float4*>(y_hi + b * 32 * KC) + tid;
+          const float4 v = live ? p.yfin(*h) : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (do_colsum) cs[b] = make_float4(cs[b].x + v.x, cs[b].y + v.y, cs[b].z + v.z, cs[b].w + v.w);
+          const float4 hv = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+          *h = hv;
+          reinterpret_cast<float4*>(y_lo + b * 32 * KC)[tid] =
+              make_float4(v.x - hv.x, v.y - hv.y, v.z - hv.z, v.w - hv.w);
+        }
+      }
+      fence_proxy_async();
+      mbar_arrive(&cfull[stage]);
+      if (++stage == kStages) stage = 0, phase ^= 1;
+    }
+    if (do_colsum)
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (b < nyb) *reinterpret_cast<float4*>(csum_smem + row * N + 32 * b + fq) = cs[b];
+    // epilogue (as tc_red_kernel): warp w reads TMEM lanes 32*(w%4), column half w/4
+    if (my_chunks > 0) {
+      mbar_wait(&accfull[0], 0);
+      tc_fence_after();
+    }
+    const int q = warp & 3, half = warp >> 2;
+    const int nh = ((N / 32) + 1) / 2 * 32;
+    const int nb = half ? nh : 0, ne = half ? N : nh;
+    const int mloc = q * 32 + lane;
+    for (int n0 = nb; n0 < ne; n0 += 32) {
+      float acc[32];
+      __syncwarp();
+      tmem_ld32(tmem + (uint32_t(q * 32) << 16) + n0, acc);
+      if (mloc < Mt) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (n0 + i < N) out[size_t(n0 + i) * Mo + m0 + mloc] = my_chunks ? acc[i] : 0.f;
+      }
+    }
+    if (do_colsum) {
+      asm volatile("bar.sync 1, %0;" ::"r"(kProdThreads) : "memory");
+      for (int n = tid; n < N; n += kProdThreads) {
+        float v = 0.f;
+        for (int r = 0; r < 32; ++r) v += csum_smem[r * N + n];
+        out[size_t(n) * Mo + p.M] = v;
+      }
+    }
+  } else {  // -------------------------------------------------------- MMA
+    int stage = 0;
+    uint32_t phase = 0;
+    const int dbg = g_tc_debug;
+    const uint32_t idesc = idesc_tf32(N) | ((dbg & 0x200) ? 0u : ((1u << 15) | (1u << 16)));  // A and B MN-major
+    int i = 0;
+    for (int c = split; c < nchunks; c += nsplit, ++i) {
+      mbar_wait(&cfull[stage], phase);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t ah = smem_u32(smem_raw + stage * SB), al = ah + 128 * KC * 4;
+        const uint32_t bh = al + 128 * KC * 4, bl = bh + uint32_t(N) * KC * 4;
+#pragma unroll
+        for (int j = 0; j < KC / 8; ++j) {
+          const uint32_t o = 1024 * j;  // 8-row group j of every box
+          mma_tf32(tmem, sdesc_sw128_mn(al + o, dbg), sdesc_sw128_mn(bh + o, dbg), idesc, (i == 0 && j == 0) ? 0u : 1u);
+          mma_tf32(tmem, sdesc_sw128_mn(ah + o, dbg), sdesc_sw128_mn(bl + o, dbg), idesc, 1u);
+          mma_tf32(tmem, sdesc_sw128_mn(ah + o, dbg), sdesc_sw128_mn(bh + o, dbg), idesc, 1u);
+        }
+        mma_commit(&empty[stage]);
+        if (i == my_chunks - 1) mma_commit(&accfull[0]);
+      }
+      __syncwarp();
+      if (++stage == kStages) stage = 0, phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kRedProd) tmem_dealloc(tmem, acc_cols);
 }
 
 }  // namespace tc
