@@ -589,6 +589,16 @@ template <class P, class = void>
 struct HasTmaFin : std::false_type {};
 template <class P>
 struct HasTmaFin<P, std::void_t<decltype(std::declval<const P&>().xfin(float4{}))>> : std::true_type {};
+// TMA reduce path operands (P::tma fills it; nullptr = computed on the fly):
+// X = x (or [x | x1], x1 from feature xsplit on), Y = y; row-major, ld floats
+struct TmaOps {
+  const float* x = nullptr;
+  int ldx = 0;
+  const float* x1 = nullptr;
+  int xsplit = 0;
+  const float* y = nullptr;
+  int ldy = 0;
+};
 template <class P, class = void>
 struct HasTma : std::false_type {};
 template <class P>
@@ -701,23 +711,29 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
     float* partial = c.part(st);
     while (ns > 1 && size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * NW > c.partial_cap) ns /= 2;
     if constexpr (HasTma<P>::value) {  // plain row-major operands over contiguous rows: TMA path
-      const float *xb = nullptr, *yb = nullptr;
-      int ldx = 0, ldy = 0;
-      p.tma(&xb, &ldx, &yb, &ldy);
-      CUtensorMap mx, my;
+      TmaOps o;
+      p.tma(o);
+      const int NT = p.Ncols <= 128 ? p.Ncols : 128;  // column slices of <= 128 (stage fits 3 in smem)
       const long long cap_rows = rows_cap > 0 ? rows_cap : (long long)c.Ec;
-      if (c.red_tma && xb && yb && !p.rows.perm && p.Ncols <= 128 && mtiles == 1 &&
-          size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * NW <= c.partial_cap && tc::tmap_2d(&mx, xb, cap_rows, ldx) &&
-          tc::tmap_2d(&my, yb, cap_rows, ldy)) {
-        const size_t SB = tc::red_stage_bytes(NW);
-        const int stages = int(std::min<size_t>(4, (tc::kSmemLimit - size_t(32) * NW * 4 - 4096) / SB));
-        const size_t smem = tc::tc_red_tma_smem(NW, stages);
+      CUtensorMap mx, mx1, my;
+      const bool split_ok = !o.x1 || (o.xsplit % 128 == 0 && o.xsplit > 0);
+      if (c.red_tma && o.x && o.y && split_ok && !p.rows.perm && p.Ncols % NT == 0 && NT % 32 == 0 &&
+          size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * NT <= c.partial_cap &&
+          tc::tmap_2d(&mx, o.x, cap_rows, o.ldx) && (!o.x1 || tc::tmap_2d(&mx1, o.x1, cap_rows, o.ldx))) {
+        const size_t SB = tc::red_stage_bytes(NT);
+        const int stages = int(std::min<size_t>(4, (tc::kSmemLimit - size_t(32) * NT * 4 - 4096) / SB));
+        const size_t smem = tc::tc_red_tma_smem(NT, stages);
         set_smem(tc::tc_red_tma_kernel<TcRed<P>>, smem);
-        TcRed<P> q{p.rows, M, NW, P::kBias, p, 0};
-        kl(tc::tc_red_tma_kernel<TcRed<P>>, dim3(mtiles, ns, p.rows.nseg), tc::kRedTmaThreads, smem, st, q, mx, my,
-           partial, ns, stages);
-        tc::tc_red_reduce(q, partial, ns, st);
-        return;
+        bool ok = true;
+        for (int n0 = 0; n0 < p.Ncols && ok; n0 += NT) {
+          ok = tc::tmap_2d(&my, o.y + n0, cap_rows, o.ldy);
+          if (!ok) break;
+          TcRed<P> q{p.rows, M, NT, P::kBias, p, n0};  // each slice sums its own bias columns
+          kl(tc::tc_red_tma_kernel<TcRed<P>>, dim3(mtiles, ns, p.rows.nseg), tc::kRedTmaThreads, smem, st, q, mx,
+             o.x1 ? mx1 : mx, my, o.x1 ? o.xsplit : 0, partial, ns, stages);
+          tc::tc_red_reduce(q, partial, ns, st);
+        }
+        if (ok) return;
       }
     }
     if (size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * NW <= c.partial_cap) {
@@ -1405,7 +1421,7 @@ struct L2Prob {  // [g_nW2; g_nb2] = [silu(vz1), 1]^T dh
   int K, Ncols, H;
   const float *vz1, *dh;
   float* G;
-  void tma(const float** x, int* ldx, const float** y, int* ldy) const { *x = vz1, *ldx = H, *y = dh, *ldy = H; }
+  void tma(TmaOps& o) const { o.x = vz1, o.ldx = H, o.y = dh, o.ldy = H; }
   __device__ float4 xfin(float4 v) const { return silu4(v); }
   __device__ float a(int, int r, int k) const { return k < H ? silu(vz1[size_t(r) * H + k]) : 1.f; }
   __device__ float b(int, int r, int n) const { return dh[size_t(r) * H + n]; }
@@ -1423,6 +1439,7 @@ struct L3Prob {  // [g_nW1; g_nb1] = [h, agg, 1]^T dvz1
   int K, Ncols, H;
   const float *h, *agg, *dvz1;
   float* G;
+  // (TMA path measured slower here in the overlapped step: the row-walking producer stays)
   __device__ float a(int, int r, int k) const {
     return k < H ? h[size_t(r) * H + k] : (k < 2 * H ? agg[size_t(r) * H + k - H] : 1.f);
   }
@@ -1479,9 +1496,7 @@ struct L6Prob {  // [g_eW2; g_eb2] = [silu(z1), 1]^T dz2   (E rows)
   float* G;
   const float* a1s;  // a1 materialised by the forward producer (nullable)
   const float *dagg, *z2s;  // non-null: dz2 = dagg[dst] * silu'(z2) computed on the fly
-  void tma(const float** x, int* ldx, const float** y, int* ldy) const {
-    *x = a1s, *ldx = H, *y = dagg ? nullptr : dz2, *ldy = H;
-  }
+  void tma(TmaOps& o) const { o.x = a1s, o.ldx = H, o.y = dagg ? nullptr : dz2, o.ldy = H; }
   __device__ float a(int, int e, int k) const {
     return k < H ? silu(z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, k)) : 1.f;
   }

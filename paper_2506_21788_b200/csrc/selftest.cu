@@ -107,7 +107,7 @@ extern "C" int hmtl_selftest_gemm(int mode, int variant, int rows, int K, int N,
       const int stages = int(std::min<size_t>(4, (tc::kSmemLimit - size_t(32) * N * 4 - 4096) / SB));
       const size_t smem = tc::tc_red_tma_smem(N, stages);
       cudaFuncSetAttribute(tc::tc_red_tma_kernel<StRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      tc::tc_red_tma_kernel<StRed><<<grid, tc::kRedTmaThreads, smem>>>(p, mx, my, part, ns, stages);
+      tc::tc_red_tma_kernel<StRed><<<grid, tc::kRedTmaThreads, smem>>>(p, mx, mx, my, 0, part, ns, stages);
       const cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("tma launch: ") + cudaGetErrorString(le));
       set_dbg<<<1, 1>>>(0);

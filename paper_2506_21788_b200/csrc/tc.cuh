@@ -767,8 +767,9 @@ inline size_t tc_red_tma_smem(int N, int stages) {
 
 template <class P>
 __global__ void __launch_bounds__(kRedTmaThreads, 1)
-    tc_red_tma_kernel(P p, const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap ty,
-                      float* __restrict__ partial, int nsplit, int kStages) {
+    tc_red_tma_kernel(P p, const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tx1,
+                      const __grid_constant__ CUtensorMap ty, int xsplit, float* __restrict__ partial, int nsplit,
+                      int kStages) {
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
   uint8_t* smem_raw = align1k(smem_dyn);
   const int N = p.Ncols;
@@ -796,6 +797,7 @@ __global__ void __launch_bounds__(kRedTmaThreads, 1)
   }
   if (warp == kRedProd + 1 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tx) : "memory");
+    if (xsplit) asm volatile("prefetch.tensormap [%0];" ::"l"(&tx1) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&ty) : "memory");
   }
   tc_fence_before();
@@ -816,6 +818,10 @@ __global__ void __launch_bounds__(kRedTmaThreads, 1)
 
   if (warp == kRedProd + 1) {  // ------------------------------------ TMA
     if (lane == 0) {
+      // X features >= xsplit (a multiple of 128) come from the second matrix
+      const bool second = xsplit && m0 >= xsplit;
+      const CUtensorMap* xm = second ? &tx1 : &tx;
+      const int xc = second ? m0 - xsplit : m0;
       int stage = 0;
       uint32_t phase = 0;
       for (int c = split; c < nchunks; c += nsplit) {
@@ -824,7 +830,7 @@ __global__ void __launch_bounds__(kRedTmaThreads, 1)
         float* y_hi = x_hi + 2 * 128 * KC;
         mbar_expect_tx(&tfull[stage], uint32_t(nxb + nyb) * 32 * KC * 4);
         const int r0 = rb + c * KC;
-        for (int b = 0; b < nxb; ++b) tma_2d(x_hi + b * 32 * KC, &tx, m0 + 32 * b, r0, &tfull[stage]);
+        for (int b = 0; b < nxb; ++b) tma_2d(x_hi + b * 32 * KC, xm, xc + 32 * b, r0, &tfull[stage]);
         for (int b = 0; b < nyb; ++b) tma_2d(y_hi + b * 32 * KC, &ty, 32 * b, r0, &tfull[stage]);
         if (++stage == kStages) stage = 0, phase ^= 1;
       }
