@@ -99,8 +99,7 @@ extern "C" int hmtl_selftest_gemm(int mode, int variant, int rows, int K, int N,
     StRed p{rs, K, N, 0, dX, dY, dC};
     const int ns = 4;
     dim3 grid((K + 127) / 128, ns, 1);
-    if (variant & 1) {  // TMA operand path; variant >> 1 -> g_tc_debug bits 8..
-      set_dbg<<<1, 1>>>((variant >> 1) << 8);
+    if (variant & 1) {  // TMA operand path (tc_red_tma_kernel)
       CUtensorMap mx, my;
       if (!tc::tmap_2d(&mx, dX, rows, K) || !tc::tmap_2d(&my, dY, rows, N)) return fail(HMTL_ERR_INTERNAL, "tmap");
       const size_t SB = tc::red_stage_bytes(N);
@@ -110,7 +109,6 @@ extern "C" int hmtl_selftest_gemm(int mode, int variant, int rows, int K, int N,
       tc::tc_red_tma_kernel<StRed><<<grid, tc::kRedTmaThreads, smem>>>(p, mx, mx, my, 0, part, ns, stages);
       const cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("tma launch: ") + cudaGetErrorString(le));
-      set_dbg<<<1, 1>>>(0);
     } else {
       const size_t smem = tc::tc_red_smem(N);
       cudaFuncSetAttribute(tc::tc_red_kernel<StRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -729,10 +729,9 @@ constexpr int kRedTmaThreads = (kRedProd + 2) * 32;
 // MN-major tf32 operands take the 128B_BASE32B layout (32 B granules of each
 // 128 B row XOR-swizzled by row % 4; atom = 4 rows x 128 B): LBO = 4 KB between
 // 32-feature boxes, SBO = 512 B between 4-row groups, layout type 1
-__device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t saddr, int dbg = 0) {
-  const uint64_t lbo = (dbg & 0x100) ? 512 : 4096, sbo = (dbg & 0x100) ? 4096 : 512;
-  return uint64_t((saddr >> 4) & 0x3FFF) | ((lbo >> 4) << 16) | ((sbo >> 4) << 32) | (uint64_t(1) << 46) |
-         (uint64_t(1) << 61);
+__device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t saddr) {
+  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(4096 >> 4) << 16) | (uint64_t(512 >> 4) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(1) << 61);
 }
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* bar) {
   asm volatile(
@@ -909,8 +908,7 @@ __global__ void __launch_bounds__(kRedTmaThreads, 1)
   } else {  // -------------------------------------------------------- MMA
     int stage = 0;
     uint32_t phase = 0;
-    const int dbg = g_tc_debug;
-    const uint32_t idesc = idesc_tf32(N) | ((dbg & 0x200) ? 0u : ((1u << 15) | (1u << 16)));  // A and B MN-major
+    const uint32_t idesc = idesc_tf32(N) | (1u << 15) | (1u << 16);  // A and B MN-major
     int i = 0;
     for (int c = split; c < nchunks; c += nsplit, ++i) {
       mbar_wait(&cfull[stage], phase);
@@ -920,10 +918,10 @@ __global__ void __launch_bounds__(kRedTmaThreads, 1)
         const uint32_t bh = al + 128 * KC * 4, bl = bh + uint32_t(N) * KC * 4;
 #pragma unroll
         for (int j = 0; j < KC / 8; ++j) {
-          const uint32_t o = 1024 * j;  // 8-row group j of every box
-          mma_tf32(tmem, sdesc_sw128_mn(al + o, dbg), sdesc_sw128_mn(bh + o, dbg), idesc, (i == 0 && j == 0) ? 0u : 1u);
-          mma_tf32(tmem, sdesc_sw128_mn(ah + o, dbg), sdesc_sw128_mn(bl + o, dbg), idesc, 1u);
-          mma_tf32(tmem, sdesc_sw128_mn(ah + o, dbg), sdesc_sw128_mn(bh + o, dbg), idesc, 1u);
+          const uint32_t o = 1024 * j;  // rows 8j..8j+7 (two 4-row groups) of every box
+          mma_tf32(tmem, sdesc_sw128_mn(al + o), sdesc_sw128_mn(bh + o), idesc, (i == 0 && j == 0) ? 0u : 1u);
+          mma_tf32(tmem, sdesc_sw128_mn(ah + o), sdesc_sw128_mn(bl + o), idesc, 1u);
+          mma_tf32(tmem, sdesc_sw128_mn(ah + o), sdesc_sw128_mn(bh + o), idesc, 1u);
         }
         mma_commit(&empty[stage]);
         if (i == my_chunks - 1) mma_commit(&accfull[0]);

@@ -39,3 +39,17 @@ def test_row_gemm_3xtf32(rows, K, N):
 @pytest.mark.parametrize("rows,M,N", [(1000, 128, 128), (333, 256, 128), (96, 32, 32), (500, 128, 256)])
 def test_reduce_gemm_3xtf32(rows, M, N):
     assert run(1, rows, M, N) < 1e-5
+
+
+@pytest.mark.parametrize("rows,M,N", [(1000, 128, 128), (77, 128, 64), (3509, 128, 128), (999, 64, 96), (333, 96, 32)])
+def test_reduce_gemm_tma_operands(rows, M, N):
+    """TMA operand path (tc_red_tma_kernel: MN-major 128B_BASE32B tiles, in-place hi/lo
+    split, partial last chunk zeroed) against FP64 and bit-equal to the register path."""
+    assert run(1, rows, M, N, variant=1) < 1e-5
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((rows, M)).astype(np.float32)
+    Y = rng.standard_normal((rows, N)).astype(np.float32)
+    a, b = np.zeros((M, N), np.float32), np.zeros((M, N), np.float32)
+    check(lib().hmtl_selftest_gemm(1, 0, rows, M, N, fp(X), fp(Y), fp(a)))
+    check(lib().hmtl_selftest_gemm(1, 1, rows, M, N, fp(X), fp(Y), fp(b)))
+    assert np.array_equal(a, b)
