@@ -220,6 +220,24 @@ int hmtl_store_fetch(hmtl_ctx* ctx, hmtl_store* st, const uint8_t* plan_ds, cons
  * uploaded as they are, per-record CRC-32 and the parse into the pool on the
  * GPU.  Errors: io (open, magic, version, truncation, trailing bytes, CRC). */
 int hmtl_store_from_hmtd(int device, const char* const* paths, int n_files, hmtl_store** out);
+/* Energy alignment (align_energies, src/dataset.cpp:263-356; hmtl/dataset.hpp:62-70),
+ * SURVEY.md 8(f)4.  store_align: in place on a device store -- per dataset the
+ * per-element offsets mu_hat (least squares of energy_per_atom on the element
+ * fractions of the present elements; normal equations accumulated on the GPU in
+ * FP64 in a fixed order, solved by the reference's GEPP with column dropping,
+ * hmtl/linalg.hpp:11-58), then energy -= sum_atoms (mu_d - mu_ref) / n.  ids[i],
+ * offsets[i*20 .. i*20+19] (NaN = absent or dropped element) per dataset in
+ * ascending id order (cap entries); skipped = dropped elements, n_skipped.
+ * align_energies: the reference's file-level call (HMTD in -> aligned HMTD out). */
+int hmtl_store_align(hmtl_store* st, uint8_t ref_dataset_id, uint8_t* ids, double* offsets, int cap,
+                     uint8_t* skipped, int* n_skipped);
+int hmtl_align_energies(int device, const char* const* files, int n_files, uint8_t ref_dataset_id,
+                        const char* const* out_files, uint8_t* ids, double* offsets, int cap, uint8_t* skipped,
+                        int* n_skipped);
+/* store contents back to host (store order) and its size */
+int hmtl_store_download(const hmtl_store* st, int* n_atoms, uint8_t* species, double* positions, double* forces,
+                        double* energy, uint8_t* dataset_id);
+int hmtl_store_shape(const hmtl_store* st, int* G, long long* N);
 /* Host-side HMTD writer/header reader (write_sample_file / read_sample_header,
  * src/sample_io.cpp:104-120, 173-189), byte-compatible with the reference. */
 int hmtl_hmtd_write(const char* path, uint8_t dataset_id, uint8_t aligned, const hmtl_samples* s);

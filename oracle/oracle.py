@@ -334,6 +334,20 @@ class Ref:
             raise RuntimeError(self.err())
         return st.value, ds[:n], ix[:n]
 
+    def align_energies(self, files, ref_id: int, out_files):
+        """The reference's align_energies (src/dataset.cpp:306-356): ({id: offsets[20]}, skipped)."""
+        L = self.lib
+        L.ref_align_energies.argtypes = [C.POINTER(C.c_char_p), C.c_int, C.c_int, C.POINTER(C.c_char_p),
+                                         C.POINTER(_U8), C.POINTER(_D), C.POINTER(_U8), C.POINTER(_I)]
+        n = len(files)
+        fa = (C.c_char_p * n)(*[f.encode() for f in files])
+        oa = (C.c_char_p * n)(*[f.encode() for f in out_files])
+        ids, off = np.zeros(n, np.uint8), np.zeros(n * 20, np.float64)
+        sk, ns = np.zeros(n * 20 + 1, np.uint8), _I()
+        if L.ref_align_energies(fa, n, ref_id, oa, _p(ids, _U8), _p(off, _D), _p(sk, _U8), C.byref(ns)) != 0:
+            raise RuntimeError(self.err())
+        return {int(i): off[20 * j:20 * j + 20] for j, i in enumerate(ids)}, list(sk[:ns.value])
+
     def make_partition(self, counts: dict, n_groups: int, replicas: int, mode: int) -> dict:
         """The reference's make_partition (src/datastore.cpp:25-45) on Mesh{n_groups, replicas}:
         {dataset id: [(serving rank, begin, end), ...]}."""

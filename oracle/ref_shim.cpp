@@ -542,6 +542,27 @@ int ref_write_samples(const char* path, int dataset_id, int aligned, int G, cons
   }
 }
 
+// align_energies (src/dataset.cpp:306-356): offsets per dataset (ascending id, 20 each)
+int ref_align_energies(const char* const* files, int n, int ref_id, const char* const* out_files, uint8_t* ids,
+                       double* offsets, uint8_t* skipped, int* n_skipped) {
+  try {
+    std::vector<std::string> in(files, files + n), out(out_files, out_files + n);
+    data::AlignResult r = data::align_energies(in, uint8_t(ref_id), out);
+    int i = 0;
+    for (const auto& kv : r.offsets) {
+      ids[i] = kv.first;
+      for (int e = 0; e < data::kNumElements; ++e) offsets[i * data::kNumElements + e] = kv.second[e];
+      ++i;
+    }
+    for (size_t j = 0; j < r.skipped_elements.size(); ++j) skipped[j] = r.skipped_elements[j];
+    *n_skipped = int(r.skipped_elements.size());
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // save_checkpoint (src/model_io.cpp:62-84) of a reference model's blocks
 int ref_save_checkpoint(void* m, const char* path) {
   try {

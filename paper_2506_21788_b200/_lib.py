@@ -123,6 +123,12 @@ SIGNATURES = {
     "hmtl_batch_shape": (C.c_int, [_P, _IP, _IP]),
     "hmtl_loss_post": (C.c_int, [_P, C.c_int, _P]),
     "hmtl_loss_wait": (C.c_int, [_P, C.c_int, C.POINTER(C.c_float)]),
+    "hmtl_store_align": (C.c_int, [_P, C.c_uint8, _U8P, C.POINTER(C.c_double), C.c_int, _U8P, _IP]),
+    "hmtl_align_energies": (C.c_int, [C.c_int, C.POINTER(C.c_char_p), C.c_int, C.c_uint8, C.POINTER(C.c_char_p), _U8P,
+                                      C.POINTER(C.c_double), C.c_int, _U8P, _IP]),
+    "hmtl_store_download": (C.c_int, [_P, _IP, _U8P, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double), _U8P]),
+    "hmtl_store_shape": (C.c_int, [_P, _IP, C.POINTER(C.c_longlong)]),
     "hmtl_shard_range": (C.c_int, [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "hmtl_store_create_sharded": (C.c_int, [_P, C.POINTER(CSamples), _U8P, C.POINTER(C.c_uint64), _IP, _IP, C.c_int,
                                             C.POINTER(_P)]),

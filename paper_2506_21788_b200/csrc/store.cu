@@ -15,7 +15,10 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
+#include <cmath>
 #include <cstdio>
+#include <limits>
 #include <cstring>
 #include <map>
 #include <string>
@@ -213,6 +216,70 @@ __global__ void hmtd_parse_kernel(const uint8_t* __restrict__ raw, const long lo
       forces[3 * a0 + t] = le_f64(fs + 8 * t);
     }
     if (threadIdx.x == 0) energy[r] = le_f64(en);
+  }
+}
+// ---- energy alignment (align_energies, src/dataset.cpp:263-356) on the device pool ----
+constexpr int kElems = 20;  // kNumElements (hmtl/dataset.hpp:14)
+// per-sample element fractions over the dataset's present elements (idx[z] = column or -1)
+__global__ void align_frac_kernel(const int* __restrict__ sel, int G, const long long* __restrict__ atom_off,
+                                  const uint8_t* __restrict__ species, const int* __restrict__ idx, int k,
+                                  double* __restrict__ F) {
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+    const int s = sel[g];
+    const long long a0 = atom_off[s], a1 = atom_off[s + 1];
+    const double inv = 1.0 / double(a1 - a0);
+    double f[kElems];
+#pragma unroll
+    for (int a = 0; a < kElems; ++a) f[a] = 0.0;
+    for (long long i = a0; i < a1; ++i) {
+      const int c = idx[species[i]];
+#pragma unroll
+      for (int a = 0; a < kElems; ++a)
+        if (a == c) f[a] += inv;  // frac[a] += 1/n per atom, atom order (as the reference)
+    }
+    for (int a = 0; a < k; ++a) F[size_t(g) * kElems + a] = f[a];
+  }
+}
+// normal equations X^T X | X^T y over a fixed chunk of samples per block (thread = entry),
+// then align_sum_kernel adds the chunk partials in chunk order: deterministic
+constexpr int kAlignChunk = 256;
+__global__ void align_normal_kernel(const double* __restrict__ F, const int* __restrict__ sel,
+                                    const double* __restrict__ energy, int G, int k, double* __restrict__ part) {
+  const int t = threadIdx.x, T = k * k + k;
+  if (t >= T) return;
+  const int g0 = blockIdx.x * kAlignChunk, g1 = min(G, g0 + kAlignChunk);
+  double acc = 0.0;
+  if (t < k * k) {
+    const int a = t / k, b = t % k;
+    for (int g = g0; g < g1; ++g) acc += F[size_t(g) * kElems + a] * F[size_t(g) * kElems + b];
+  } else {
+    const int a = t - k * k;
+    for (int g = g0; g < g1; ++g) acc += F[size_t(g) * kElems + a] * energy[sel[g]];
+  }
+  part[size_t(blockIdx.x) * T + t] = acc;
+}
+__global__ void align_sum_kernel(const double* __restrict__ part, int nb, int T, double* __restrict__ out) {
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    double acc = 0.0;
+    for (int b = 0; b < nb; ++b) acc += part[size_t(b) * T + t];
+    out[t] = acc;
+  }
+}
+// energy_per_atom -= sum over atoms (mu_d[z] - mu_ref[z]) / n (NaN offsets count as 0)
+__global__ void align_apply_kernel(const int* __restrict__ sel, int G, const long long* __restrict__ atom_off,
+                                   const uint8_t* __restrict__ species, const double* __restrict__ mu_d,
+                                   const double* __restrict__ mu_ref, double* __restrict__ energy) {
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+    const int s = sel[g];
+    const long long a0 = atom_off[s], a1 = atom_off[s + 1];
+    const double n = double(a1 - a0);
+    double corr = 0.0;
+    for (long long i = a0; i < a1; ++i) {
+      const int z = species[i];
+      const double d = isnan(mu_d[z]) ? 0.0 : mu_d[z], r = isnan(mu_ref[z]) ? 0.0 : mu_ref[z];
+      corr += (d - r) / n;
+    }
+    energy[s] -= corr;
   }
 }
 }  // namespace
@@ -684,6 +751,201 @@ int hmtl_store_fetch(hmtl_ctx* h, hmtl_store* st, const uint8_t* plan_ds, const 
   HMTL_CUDA(cudaGetLastError());
   c.host_G = n;
   c.host_N = int(N);
+  return HMTL_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// num::solve_gepp_dropping (hmtl/linalg.hpp:11-58): Gaussian elimination with partial
+// pivoting through a row permutation; a column whose best pivot is below
+// drop_tol * max |diag| is dropped (x = 0, index reported)
+std::vector<double> gepp_dropping(std::vector<double> A, size_t k, std::vector<double> b, double drop_tol,
+                                  std::vector<size_t>* dropped) {
+  double scale = 0.0;
+  for (size_t i = 0; i < k; ++i) scale = std::max(scale, std::fabs(A[i * k + i]));
+  if (scale == 0.0) scale = 1.0;
+  const double tol = drop_tol * scale;
+  std::vector<size_t> perm(k);
+  for (size_t i = 0; i < k; ++i) perm[i] = i;
+  std::vector<char> gone(k, 0);
+  for (size_t col = 0; col < k; ++col) {
+    size_t best = col;
+    double best_v = 0.0;
+    for (size_t r = col; r < k; ++r) {
+      const double v = std::fabs(A[perm[r] * k + col]);
+      if (v > best_v) best_v = v, best = r;
+    }
+    if (best_v < tol) {
+      gone[col] = 1;
+      dropped->push_back(col);
+      continue;
+    }
+    std::swap(perm[col], perm[best]);
+    const size_t pr = perm[col];
+    for (size_t r = col + 1; r < k; ++r) {
+      const size_t q = perm[r];
+      const double f = A[q * k + col] / A[pr * k + col];
+      if (f == 0.0) continue;
+      for (size_t c = col; c < k; ++c) A[q * k + c] -= f * A[pr * k + c];
+      b[q] -= f * b[pr];
+    }
+  }
+  std::vector<double> x(k, 0.0);
+  for (size_t ci = k; ci-- > 0;) {
+    if (gone[ci]) continue;
+    const size_t pr = perm[ci];
+    double acc = b[pr];
+    for (size_t c = ci + 1; c < k; ++c) acc -= A[pr * k + c] * x[c];
+    x[ci] = acc / A[pr * k + ci];
+  }
+  return x;
+}
+}  // namespace
+
+extern "C" {
+
+// align_energies (src/dataset.cpp:306-356) on a device store, in place: per dataset,
+// per-element offsets mu_hat by least squares of energy_per_atom on the element
+// fractions (normal equations accumulated on the GPU in FP64, deterministic chunk
+// order; the <= 20-column solve on the host), then energy -= sum_atoms (mu_d - mu_ref)/n.
+int hmtl_store_align(hmtl_store* st, uint8_t ref_dataset_id, uint8_t* ids, double* offsets, int cap,
+                     uint8_t* skipped, int* n_skipped) {
+  if (!st || !n_skipped) return fail(HMTL_ERR_CONTRACT, "store_align: null argument");
+  if (st->by_dataset.size() < 2) return fail(HMTL_ERR_DATA, "align: need at least two datasets");
+  if (!st->by_dataset.count(ref_dataset_id)) return fail(HMTL_ERR_DATA, "align: reference dataset not among inputs");
+  if (ids && cap < int(st->by_dataset.size())) return fail(HMTL_ERR_CONTRACT, "store_align: buffer too small");
+  HMTL_CUDA(cudaSetDevice(st->device));
+  // present elements per dataset (host copy of the species: counts are integers)
+  std::vector<uint8_t> sp(size_t(st->N));
+  HMTL_CUDA(cudaMemcpy(sp.data(), st->d_species, sp.size(), cudaMemcpyDeviceToHost));
+  std::vector<long long> off(size_t(st->G) + 1, 0);
+  for (int g = 0; g < st->G; ++g) off[g + 1] = off[g] + st->n_atoms[g];
+  std::map<int, std::array<double, kElems>> mu;
+  std::vector<uint8_t> skip;
+  int *d_sel = nullptr, *d_idx = nullptr;
+  double *d_F = nullptr, *d_part = nullptr, *d_out = nullptr, *d_mu = nullptr;
+  size_t maxg = 0;
+  for (const auto& kv : st->by_dataset) maxg = std::max(maxg, kv.second.size());
+  const int nbmax = int((maxg + kAlignChunk - 1) / kAlignChunk);
+  bool ok = cudaMalloc(&d_sel, maxg * 4) == cudaSuccess && cudaMalloc(&d_idx, 256 * 4) == cudaSuccess &&
+            cudaMalloc(&d_F, maxg * kElems * 8) == cudaSuccess &&
+            cudaMalloc(&d_part, size_t(nbmax) * (kElems * kElems + kElems) * 8) == cudaSuccess &&
+            cudaMalloc(&d_out, (kElems * kElems + kElems) * 8) == cudaSuccess &&
+            cudaMalloc(&d_mu, 2 * kElems * 8) == cudaSuccess;
+  for (const auto& kv : st->by_dataset) {
+    if (!ok) break;
+    const std::vector<int>& sel = kv.second;
+    const int G = int(sel.size());
+    std::array<long long, kElems> cnt{};
+    for (int s : sel)
+      for (long long i = off[s]; i < off[s + 1]; ++i) cnt[sp[i] < kElems ? sp[i] : 0]++;
+    std::vector<int> present, idx(256, -1);
+    for (int e = 0; e < kElems; ++e)
+      if (cnt[e] > 0) idx[e] = int(present.size()), present.push_back(e);
+    const int k = int(present.size()), T = k * k + k, nb = (G + kAlignChunk - 1) / kAlignChunk;
+    ok = cudaMemcpy(d_sel, sel.data(), size_t(G) * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(d_idx, idx.data(), 256 * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+    if (!ok) break;
+    align_frac_kernel<<<std::min((G + 255) / 256, 148 * 8), 256>>>(d_sel, G, st->d_atom_off, st->d_species, d_idx, k,
+                                                                     d_F);
+    align_normal_kernel<<<nb, 448>>>(d_F, d_sel, st->d_energy, G, k, d_part);
+    align_sum_kernel<<<1, 448>>>(d_part, nb, T, d_out);
+    std::vector<double> ne(T);
+    ok = cudaMemcpy(ne.data(), d_out, size_t(T) * 8, cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (!ok) break;
+    std::vector<double> xtx(ne.begin(), ne.begin() + size_t(k) * k), xty(ne.begin() + size_t(k) * k, ne.end());
+    std::vector<size_t> dropped;
+    const std::vector<double> x = gepp_dropping(xtx, size_t(k), xty, 1e-10, &dropped);
+    std::array<double, kElems> m;
+    m.fill(std::numeric_limits<double>::quiet_NaN());
+    for (int a = 0; a < k; ++a) m[present[a]] = x[a];
+    for (size_t d : dropped) m[present[d]] = std::numeric_limits<double>::quiet_NaN(), skip.push_back(uint8_t(present[d]));
+    mu[kv.first] = m;
+  }
+  const std::array<double, kElems> ref = ok ? mu[ref_dataset_id] : std::array<double, kElems>{};
+  for (const auto& kv : st->by_dataset) {
+    if (!ok) break;
+    const std::vector<int>& sel = kv.second;
+    const int G = int(sel.size());
+    double h_mu[2 * kElems];
+    std::copy(mu[kv.first].begin(), mu[kv.first].end(), h_mu);
+    std::copy(ref.begin(), ref.end(), h_mu + kElems);
+    ok = cudaMemcpy(d_sel, sel.data(), size_t(G) * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(d_mu, h_mu, sizeof h_mu, cudaMemcpyHostToDevice) == cudaSuccess;
+    if (!ok) break;
+    align_apply_kernel<<<std::min((G + 255) / 256, 148 * 8), 256>>>(d_sel, G, st->d_atom_off, st->d_species, d_mu,
+                                                                     d_mu + kElems, st->d_energy);
+    ok = cudaDeviceSynchronize() == cudaSuccess;
+  }
+  cudaFree(d_sel), cudaFree(d_idx), cudaFree(d_F), cudaFree(d_part), cudaFree(d_out), cudaFree(d_mu);
+  if (!ok) return fail(HMTL_ERR_INTERNAL, "store_align: device failure");
+  int i = 0;
+  for (const auto& kv : mu) {
+    if (ids) ids[i] = uint8_t(kv.first);
+    if (offsets) std::copy(kv.second.begin(), kv.second.end(), offsets + size_t(i) * kElems);
+    ++i;
+  }
+  if (skipped) std::copy(skip.begin(), skip.end(), skipped);
+  *n_skipped = int(skip.size());
+  return HMTL_OK;
+}
+
+// samples of the store back to host arrays (store order), e.g. to write aligned files
+int hmtl_store_download(const hmtl_store* st, int* n_atoms, uint8_t* species, double* positions, double* forces,
+                        double* energy, uint8_t* dataset_id) {
+  if (!st) return fail(HMTL_ERR_CONTRACT, "store_download: null store");
+  HMTL_CUDA(cudaSetDevice(st->device));
+  if (n_atoms) std::copy(st->n_atoms.begin(), st->n_atoms.end(), n_atoms);
+  if (dataset_id) std::copy(st->ds.begin(), st->ds.end(), dataset_id);
+  if (species) HMTL_CUDA(cudaMemcpy(species, st->d_species, size_t(st->N), cudaMemcpyDeviceToHost));
+  if (positions) HMTL_CUDA(cudaMemcpy(positions, st->d_pos, size_t(st->N) * 24, cudaMemcpyDeviceToHost));
+  if (forces) HMTL_CUDA(cudaMemcpy(forces, st->d_forces, size_t(st->N) * 24, cudaMemcpyDeviceToHost));
+  if (energy) HMTL_CUDA(cudaMemcpy(energy, st->d_energy, size_t(st->G) * 8, cudaMemcpyDeviceToHost));
+  return HMTL_OK;
+}
+
+// align_energies(files, ref, out_files) (hmtl/dataset.hpp:62-70): HMTD files -> device
+// store (CRC + parse on the GPU) -> hmtl_store_align -> one aligned file per input
+// (header aligned = 1, samples in input order).  offsets[i*20..] for dataset ids[i].
+int hmtl_align_energies(int device, const char* const* files, int n_files, uint8_t ref_dataset_id,
+                        const char* const* out_files, uint8_t* ids, double* offsets, int cap, uint8_t* skipped,
+                        int* n_skipped) {
+  if (!files || !out_files || !n_skipped) return fail(HMTL_ERR_CONTRACT, "align: null argument");
+  if (n_files < 2) return fail(HMTL_ERR_DATA, "align: need at least two datasets");
+  std::vector<uint8_t> file_ds(n_files);
+  std::vector<uint64_t> file_n(n_files);
+  for (int i = 0; i < n_files; ++i) {
+    uint8_t al = 0;
+    if (int rc = hmtl_hmtd_read_header(files[i], &file_ds[i], &al, &file_n[i])) return rc;
+    if (file_n[i] == 0) return fail(HMTL_ERR_DATA, std::string("align: empty dataset ") + files[i]);
+  }
+  hmtl_store* st = nullptr;
+  if (int rc = hmtl_store_from_hmtd(device, files, n_files, &st)) return rc;
+  int rc = hmtl_store_align(st, ref_dataset_id, ids, offsets, cap, skipped, n_skipped);
+  std::vector<int> na(st->G);
+  std::vector<uint8_t> sp(size_t(st->N)), dsv(st->G);
+  std::vector<double> pos(size_t(st->N) * 3), frc(size_t(st->N) * 3), en(st->G);
+  if (!rc) rc = hmtl_store_download(st, na.data(), sp.data(), pos.data(), frc.data(), en.data(), dsv.data());
+  // the pool holds the files back to back, in order
+  long long g0 = 0, a0 = 0;
+  for (int i = 0; i < n_files && !rc; ++i) {
+    const int G = int(file_n[i]);
+    long long n = 0;
+    for (int g = 0; g < G; ++g) n += na[g0 + g];
+    hmtl_samples smp{G, int(n), na.data() + g0, sp.data() + a0, pos.data() + 3 * a0, frc.data() + 3 * a0,
+                     en.data() + g0, dsv.data() + g0};
+    rc = hmtl_hmtd_write(out_files[i], file_ds[i], 1, &smp);
+    g0 += G, a0 += n;
+  }
+  hmtl_store_destroy(st);
+  return rc;
+}
+
+int hmtl_store_shape(const hmtl_store* st, int* G, long long* N) {
+  if (!st || !G || !N) return fail(HMTL_ERR_CONTRACT, "store_shape: null argument");
+  *G = st->G;
+  *N = st->N;
   return HMTL_OK;
 }
 

@@ -405,6 +405,22 @@ def _ip(a):
 
 
 # ---------------------------------------------------------------- data plane
+def align_energies(files, ref_dataset_id: int, out_files, device: int = 0):
+    """align_energies (hmtl/dataset.hpp:62-70, src/dataset.cpp:263-356) on the GPU:
+    HMTD files in, aligned HMTD files out; returns ({dataset id: offsets[20]}, skipped)."""
+    n = len(files)
+    fa = (C.c_char_p * n)(*[str(f).encode() for f in files])
+    oa = (C.c_char_p * len(out_files))(*[str(f).encode() for f in out_files])
+    if len(out_files) != n:
+        raise ValueError("align: out file count mismatch")
+    ids, off = np.zeros(n, np.uint8), np.zeros(n * 20, np.float64)
+    sk, ns = np.zeros(n * 20 + 1, np.uint8), C.c_int()
+    check(lib().hmtl_align_energies(device, fa, n, ref_dataset_id, oa, ids.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                    off.ctypes.data_as(C.POINTER(C.c_double)), n,
+                                    sk.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(ns)))
+    return {int(i): off[20 * j:20 * j + 20] for j, i in enumerate(ids)}, [int(x) for x in sk[:ns.value]]
+
+
 def comm_unique_id() -> bytes:
     """ncclGetUniqueId (rank 0 makes it; ship it to the others out of band)."""
     b = (C.c_uint8 * 128)()
@@ -551,6 +567,30 @@ class SampleStore:
         st = SampleStore(None, model.device, _handle=h)
         st._pool = shard
         return st
+
+    def download(self) -> Samples:
+        """The pool back in host memory (store order)."""
+        G, N = C.c_int(), C.c_longlong()
+        check(lib().hmtl_store_shape(self._h, C.byref(G), C.byref(N)))
+        na, sp = np.zeros(G.value, np.int32), np.zeros(N.value, np.uint8)
+        pos, frc = np.zeros(3 * N.value), np.zeros(3 * N.value)
+        en, ds = np.zeros(G.value), np.zeros(G.value, np.uint8)
+        dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+        u8 = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint8))
+        check(lib().hmtl_store_download(self._h, na.ctypes.data_as(C.POINTER(C.c_int)), u8(sp), dp(pos), dp(frc),
+                                        dp(en), u8(ds)))
+        return Samples(na, sp, pos, frc, en, ds)
+
+    def align(self, ref_dataset_id: int):
+        """Energy alignment of the pool in place (align_energies, src/dataset.cpp:306-356):
+        returns ({dataset id: offsets[20]}, skipped elements)."""
+        n = len(self.counts())
+        ids, off = np.zeros(n, np.uint8), np.zeros(n * 20, np.float64)
+        sk, ns = np.zeros(n * 20 + 1, np.uint8), C.c_int()
+        check(lib().hmtl_store_align(self._h, ref_dataset_id, ids.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                     off.ctypes.data_as(C.POINTER(C.c_double)), n,
+                                     sk.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(ns)))
+        return {int(i): off[20 * j:20 * j + 20] for j, i in enumerate(ids)}, [int(x) for x in sk[:ns.value]]
 
     def fetch(self, model: "ModelT", plan_ds, plan_idx, stream=None) -> None:
         """fetch_samples(plan, step) (src/datastore.cpp:192-248): plan_ds/plan_idx are

@@ -179,3 +179,46 @@ def test_store_from_hmtd_matches_reference_samples(tmp_path):
     trunc.write_bytes(bytes(raw[:-7]))
     with pytest.raises(P.HmtlError, match="truncated"):
         P.SampleStore.from_hmtd([str(trunc)])
+
+
+@pytest.mark.gpu
+def test_align_energies_matches_reference(tmp_path):
+    """align_energies (src/dataset.cpp:263-356) on the GPU vs the reference's
+    own (oracle/_ref): per-element offsets (NaN pattern exact, values to 1e-9), aligned labels
+    to 1e-10, structures byte-identical, output headers aligned = 1; planted offsets recovered."""
+    import oracle as O
+
+    O.build(ref=True)
+    ref = O.Ref()
+    files = []
+    for k, planted in ((0, None), (1, {0: 1.25, 1: -0.75}), (3, {2: 0.5})):
+        spec = ref.default5_spec(k)
+        if planted:
+            mu = list(spec["mu"])
+            for e, v in planted.items():
+                mu[e] += v
+            spec = dict(spec, mu=mu)
+        s = ref.generate(spec, 500 + k, count=60 + 10 * k)
+        f = str(tmp_path / f"in{k}.hmtd")
+        ref.write_samples(f, k, 0, s)
+        files.append(f)
+    out_r = [str(tmp_path / f"ref{k}.hmtd") for k in range(3)]
+    out_g = [str(tmp_path / f"gpu{k}.hmtd") for k in range(3)]
+    off_r, sk_r = ref.align_energies(files, 0, out_r)
+    off_g, sk_g = P.align_energies(files, 0, out_g)
+    assert sorted(off_r) == sorted(off_g) and sk_r == sk_g
+    for d in off_r:
+        a, b = off_r[d], off_g[d]
+        assert np.array_equal(np.isnan(a), np.isnan(b)), d
+        m = ~np.isnan(a)
+        assert np.all(np.abs(a[m] - b[m]) <= 1e-9 * np.maximum(1.0, np.abs(a[m]))), d
+    for fr, fg in zip(out_r, out_g):
+        assert P.hmtd_header(fg)[1] == 1
+        sr, sg = P.SampleStore.from_hmtd([fr]).download(), P.SampleStore.from_hmtd([fg]).download()
+        assert np.array_equal(sr.n_atoms, sg.n_atoms) and np.array_equal(sr.species, sg.species)
+        assert np.array_equal(sr.positions, sg.positions) and np.array_equal(sr.forces, sg.forces)
+        assert np.max(np.abs(sr.energy - sg.energy)) < 1e-10
+    with pytest.raises(P.HmtlError):
+        P.align_energies(files[:1], 0, out_g[:1])  # need at least two datasets
+    with pytest.raises(P.HmtlError):
+        P.align_energies(files[1:], 0, out_g[1:])  # reference dataset not among inputs
