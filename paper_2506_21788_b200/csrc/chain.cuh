@@ -126,17 +126,55 @@ __device__ __forceinline__ float4 epi_apply(const Gemm& g, int H, int r, int n, 
 template <int V>
 using IC = std::integral_constant<int, V>;
 
+// ---- 2-CTA cluster column split: rank r of a cluster computes columns
+// [r N/2, (r+1) N/2) of every GEMM of the same 128 rows and writes its slice of
+// the chained A operand into both CTAs' shared memory (DSMEM), arriving on both
+// CTAs' per-chunk barriers with cluster-scope release
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster4(uint32_t addr, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void arrive_cluster(uint32_t addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(tc::smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 // The role sequence is a compile-time parameter: a switch over roles in the
 // unrolled epilogue made every iteration distinct code (instruction-fetch bound).
-template <int R0, int R1, int R2>
+template <int R0, int R1, int R2, int CS = 1>
 __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
   constexpr int G = R2 >= 0 ? 3 : (R1 >= 0 ? 2 : 1);
   using namespace tc;
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
   const long long t_start = clock64();
   const int M = *p.count;
-  const int row0 = blockIdx.x * 128;
-  if (row0 >= M) return;  // whole CTA, before any barrier or TMEM use
+  const int row0 = (blockIdx.x / CS) * 128;
+  const uint32_t crank = CS > 1 ? cluster_rank() : 0;
+  if (row0 >= M) return;  // whole CTA (and its cluster peer), before any barrier or TMEM use
   uint8_t* sm = align1k(smem_dyn);
   uint8_t* X = sm;                          // kXSlots x kSlot
   uint8_t* Bq = sm + kXSlots * kSlot;       // kBSlots x kSlot
@@ -149,12 +187,17 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
   uint64_t* accd = bars + 14;               // [3] MMA commit: GEMM g complete
   uint64_t* xrdy = bars + 17;               // [2][4] the 4 warps of a slab: X chunk c of GEMM g+1's A
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
+  uint64_t* pd = bars + 26;                 // [3] cluster peer's GEMM g complete (CS > 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int H = p.H;
   uint32_t acc_off[3];
+  int nb_[3], ne_[3];  // this CTA's column range of GEMM i
   {
     uint32_t o = 0;
-    for (int i = 0; i < G; ++i) acc_off[i] = o, o += uint32_t(p.g[i].N);
+    for (int i = 0; i < G; ++i) {
+      nb_[i] = int(crank) * (p.g[i].N / CS), ne_[i] = nb_[i] + p.g[i].N / CS;
+      acc_off[i] = o, o += uint32_t(p.g[i].N / CS);
+    }
   }
   if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
   if (tid == 0) {
@@ -162,10 +205,12 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
     for (int s = 0; s < kBSlots; ++s) mbar_init(&bfull[s], 1), mbar_init(&bempty[s], 1);
     for (int i = 0; i < 3; ++i) mbar_init(&accd[i], 1);
     for (int i = 0; i < 8; ++i) mbar_init(&xrdy[i], 4 * 32);
+    for (int i = 0; i < 3; ++i) mbar_init(&pd[i], 1);
     fence_mbar_init();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CS > 1) cluster_sync();  // the peer's barriers exist before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // setup above overlaps the previous kernel's tail
@@ -219,8 +264,8 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
       int q = 0;
       for (int gi = 0; gi < G; ++gi) {
         const Gemm& g = p.g[gi];
-        for (int n0 = 0; n0 < g.N; n0 += 128) {
-          const int nr = g.N - n0 < 128 ? g.N - n0 : 128;
+        for (int n0 = nb_[gi]; n0 < ne_[gi]; n0 += 128) {
+          const int nr = ne_[gi] - n0 < 128 ? ne_[gi] - n0 : 128;
           const uint32_t bytes = uint32_t(nr) * 128;
           for (int c = 0; c < g.K / KC; ++c, ++q) {
             const int s = q % kBSlots;
@@ -240,28 +285,31 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
       const Gemm& g = p.g[gi];
       const int nch = g.K / KC;
       if (lane == 0) CHAIN_STAMP(2 + 2 * gi);
-      for (int n0 = 0; n0 < g.N; n0 += 128) {
-        const int nr = g.N - n0 < 128 ? g.N - n0 : 128;
+      for (int n0 = nb_[gi]; n0 < ne_[gi]; n0 += 128) {
+        const int nr = ne_[gi] - n0 < 128 ? ne_[gi] - n0 : 128;
         const uint32_t idesc = idesc_tf32(nr);
         for (int c = 0; c < nch; ++c, ++q) {
           const int s = q % kBSlots;
           int xs = c;
           if (gi == 0) {  // A ring slot c % 4 (chunks of GEMM 1 stream through X)
             xs = c % kXSlots;
-            if (n0 == 0) {
+            if (n0 == nb_[gi]) {
               mbar_wait(&afull[xs], (c / kXSlots) & 1);
               tc_fence_after();
             }
-          } else if (n0 == 0) {  // chunk c of the chained operand, written slab by slab by
-            mbar_wait(&xrdy[(gi - 1) * 4 + c], 0);  // the previous epilogue: MMAs start early
+          } else if (n0 == nb_[gi]) {  // chunk c of the chained operand, written slab by slab by
+            // the previous epilogue (of either CTA of the cluster): MMAs start early
+            if constexpr (CS > 1) wait_cluster(&xrdy[(gi - 1) * 4 + c], 0);
+            else mbar_wait(&xrdy[(gi - 1) * 4 + c], 0);
             tc_fence_after();
           }
           mbar_wait(&bfull[s], (q / kBSlots) & 1);
           tc_fence_after();
           const uint32_t ah = smem_u32(X + xs * kSlot), bh = smem_u32(Bq + s * kSlot);
-          issue_chunk_warp(tmem + acc_off[gi] + uint32_t(n0), ah, ah + 16384, bh, bh + 16384, idesc, c != 0);
+          issue_chunk_warp(tmem + acc_off[gi] + uint32_t(n0 - nb_[gi]), ah, ah + 16384, bh, bh + 16384, idesc,
+                           c != 0);
           commit_warp(&bempty[s]);
-          if (gi == 0 && n0 + 128 >= g.N) commit_warp(&aempty[xs]);
+          if (gi == 0 && n0 + 128 >= ne_[gi]) commit_warp(&aempty[xs]);
           __syncwarp();
         }
       }
@@ -278,13 +326,20 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
       const Gemm& g = p.g[gi];
       mbar_wait(&accd[gi], 0);
       tc_fence_after();
+      if constexpr (CS > 1) {
+        if (!last) {  // the peer writes into our X (and we into its) only once both CTAs'
+          // MMAs of GEMM gi -- which read X -- are complete
+          if (ew == 0 && lane == 0) arrive_cluster(mapa(smem_u32(&pd[gi]), crank ^ 1u));
+          wait_cluster(&pd[gi], 0);
+        }
+      }
       if (ew == 0 && lane == 0) CHAIN_STAMP(8 + 2 * gi);
       // per 32-column slab: TMEM (thread = row) -> XOR-swizzled smem tile -> read back
       // transposed (8 lanes x 16 B per row, 4 rows per instruction) so the operand
       // loads, output stores and next-operand writes are row-coalesced
       const int cc = lane & 7;
-      for (int sl = half; sl * 32 < g.N; sl += 2) {
-        const int j = sl * 32;
+      for (int sl = half; nb_[gi] + sl * 32 < ne_[gi]; sl += 2) {
+        const int j = nb_[gi] + sl * 32;
         float4 x[8];  // the slab's operand loads are in flight before the TMEM read
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
@@ -292,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
           x[it] = (rr < M && !(p.dbg & 4)) ? aux_load<R>(g, H, rr, j + 4 * cc) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
         float acc[32];
-        tmem_ld32(tmem + acc_off[gi] + (uint32_t(qd * 32) << 16) + uint32_t(j), acc);
+        tmem_ld32(tmem + acc_off[gi] + (uint32_t(qd * 32) << 16) + uint32_t(j - nb_[gi]), acc);
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < 8; ++i)
@@ -307,13 +362,28 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
           if (!last && !(p.dbg & 2)) {  // next GEMM's A: k = j + 4cc -> chunk j / 32, piece cc of row rl
             float* hi = reinterpret_cast<float*>(X + (j / KC) * kSlot);
             put4(hi, hi + 128 * KC, cc, qd * 32 + rl, v);
+            if constexpr (CS > 1) {  // the same 16 B pieces into the peer's X (DSMEM)
+              const float4 h4 = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+              const float4 l4 = make_float4(v.x - h4.x, v.y - h4.y, v.z - h4.z, v.w - h4.w);
+              const uint32_t o = smem_u32(hi) + sw128(qd * 32 + rl, cc);
+              const uint32_t peer = crank ^ 1u;
+              st_cluster4(mapa(o, peer), h4);
+              st_cluster4(mapa(o + 128 * KC * 4, peer), l4);
+            }
           }
         }
         __syncwarp();
-        if (!last) {  // this warp's 32 rows of X chunk sl are written
-          fence_proxy_async();
-          tc_fence_before();
-          mbar_arrive(&xrdy[gi * 4 + sl]);
+        if (!last) {  // this warp's 32 rows of X chunk j / 32 are written
+          if constexpr (CS > 1) {
+            asm volatile("fence.proxy.async;" ::: "memory");
+            tc_fence_before();
+            mbar_arrive(&xrdy[gi * 4 + j / KC]);
+            arrive_cluster(mapa(smem_u32(&xrdy[gi * 4 + j / KC]), crank ^ 1u));
+          } else {
+            fence_proxy_async();
+            tc_fence_before();
+            mbar_arrive(&xrdy[gi * 4 + sl]);
+          }
         }
       }
       if (ew == 0 && lane == 0) CHAIN_STAMP(9 + 2 * gi);
@@ -323,7 +393,8 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
     if constexpr (G > 2) phase(IC<R2>{}, IC<2>{});
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CS > 1) cluster_sync();  // no CTA leaves while its peer may still write into it
+  else __syncthreads();
   if (tid == 0) CHAIN_STAMP(31);
   if (warp == kMmaWarp) tmem_dealloc(tmem, 512);
 }

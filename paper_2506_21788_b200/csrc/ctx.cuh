@@ -141,9 +141,10 @@ struct Ctx {
   // silu'(zf0) [E][W] too only when the force output layer's backward needs it
   // (head_depth 2); deeper heads regather it from the L2-resident Qf table
   bool store_sf0 = false;
-  int red_sms = 0;
-  int red_min_chunks = 4;
-  bool red_tma = true;  // TMA operand path for plain row-major weight gradients (HMTL_NO_RED_TMA=1 off)  // >= this many 32-row chunks per weight-gradient CTA (HMTL_RED_MINCH)  // SMs a weight-gradient (tc_red) launch spreads over (HMTL_RED_SMS; default all)
+  int red_sms = 0;          // SMs a weight-gradient (tc_red) launch spreads over (HMTL_RED_SMS; default all)
+  int red_min_chunks = 4;   // >= this many 32-row chunks per weight-gradient CTA (HMTL_RED_MINCH)
+  bool red_tma = true;      // TMA operand path for plain row-major weight gradients (HMTL_NO_RED_TMA=1 off)
+  int chain_cs = 2;         // node-chain cluster size: 2 = column split over a CTA pair (HMTL_CHAIN_CS=1: one CTA)
   float *a1 = nullptr, *af0 = nullptr, *sf0 = nullptr;
   int nsplit_node = 1, nsplit_edge = 1, nsplit_graph = 1;
 

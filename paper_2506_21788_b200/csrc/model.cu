@@ -773,16 +773,45 @@ void launch_chain(Ctx& c, const char* name, int G, const chain::Gemm* gs, cudaSt
   q.stamps = c.chain_stamps;
   q.dbg = c.chain_dbg;
   const int grid = int((c.Nc + 127) / 128);
-  auto go = [&](auto kern) {
+  // 2-CTA clusters split every GEMM's columns (chained operand exchanged through DSMEM)
+  bool split = c.chain_cs == 2;
+  for (int i = 0; i < G; ++i) split = split && (gs[i].N / 2) % 32 == 0;
+  auto go = [&](auto kern, int cs) {
     set_smem(kern, chain::kSmem);
-    kl(kern, grid, chain::kThreads, chain::kSmem, st, q);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid * cs);
+    cfg.blockDim = dim3(chain::kThreads);
+    cfg.dynamicSmemBytes = chain::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int n = 0;
+    if (pdl_enabled()) {
+      at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[n++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    if (cs > 1) {
+      at[n].id = cudaLaunchAttributeClusterDimension;
+      at[n].val.clusterDim.x = cs, at[n].val.clusterDim.y = 1, at[n++].val.clusterDim.z = 1;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = n;
+    cudaLaunchKernelEx(&cfg, kern, q);
   };
   using namespace chain;
   const int r0 = gs[0].role, r1 = G > 1 ? gs[1].role : -1, r2 = G > 2 ? gs[2].role : -1;
-  if (r0 == kFwdNode1 && r1 == kFwdNode2 && r2 == kFwdP) go(chain_kernel<kFwdNode1, kFwdNode2, kFwdP>);
-  else if (r0 == kFwdNode1 && r1 == kFwdNode2 && r2 < 0) go(chain_kernel<kFwdNode1, kFwdNode2, -1>);
-  else if (r0 == kBwdL11 && r1 == kBwdL1 && r2 == kBwdL4) go(chain_kernel<kBwdL11, kBwdL1, kBwdL4>);
-  else if (r0 == kBwdL1 && r1 == kBwdL4 && r2 < 0) go(chain_kernel<kBwdL1, kBwdL4, -1>);
+  if (r0 == kFwdNode1 && r1 == kFwdNode2 && r2 == kFwdP) {
+    if (split) go(chain_kernel<kFwdNode1, kFwdNode2, kFwdP, 2>, 2);
+    else go(chain_kernel<kFwdNode1, kFwdNode2, kFwdP>, 1);
+  } else if (r0 == kFwdNode1 && r1 == kFwdNode2 && r2 < 0) {
+    if (split) go(chain_kernel<kFwdNode1, kFwdNode2, -1, 2>, 2);
+    else go(chain_kernel<kFwdNode1, kFwdNode2, -1>, 1);
+  } else if (r0 == kBwdL11 && r1 == kBwdL1 && r2 == kBwdL4) {
+    if (split) go(chain_kernel<kBwdL11, kBwdL1, kBwdL4, 2>, 2);
+    else go(chain_kernel<kBwdL11, kBwdL1, kBwdL4>, 1);
+  } else if (r0 == kBwdL1 && r1 == kBwdL4 && r2 < 0) {
+    if (split) go(chain_kernel<kBwdL1, kBwdL4, -1, 2>, 2);
+    else go(chain_kernel<kBwdL1, kBwdL4, -1>, 1);
+  }
 }
 
 RowSet node_rows(Ctx& c) {

@@ -18,6 +18,6 @@ check(lib().hmtl_debug_chain_stamps(m.ctx, buf, 32 * 32))
 names = {0: "setup", 1: "prod_done", 2: "mma0_start", 3: "mma0_issued", 4: "mma1_start", 5: "mma1_issued",
          6: "mma2_start", 7: "mma2_issued", 8: "epi0_start", 9: "epi0_end", 10: "epi1_start", 11: "epi1_end",
          12: "epi2_start", 13: "epi2_end", 24: "e0s0_aux", 25: "e0s0_tmem", 26: "e0s0_done", 31: "exit"}
-for cta in (0, 13, 27):
+for cta in [int(x) for x in os.environ.get("CTAS", "0,13,27").split(",")]:
     row = buf[cta * 32:(cta + 1) * 32]
     print(f"CTA {cta}: " + "  ".join(f"{names.get(i, 'b%d' % (i - 14))}={row[i] / 1.9e3:.2f}us" for i in range(32) if row[i]))
