@@ -18,7 +18,7 @@ def short(n):
     m = re.search(r"(TcRow|TcRed)<.*?::(\w+Prob|\w+Grad|F0Dh)>", n)
     if m:
         return f"{'tc_row' if m.group(1) == 'TcRow' else 'tc_red'}<{m.group(2)}>"
-    m = re.search(r"chain_kernel<(\d+), (\d+), \(?(?:int\))?(-?\d+)>", n)
+    m = re.search(r"chain_kernel<(\d+), (\d+), \(?(?:int\))?(-?\d+)(?:, \d+)?>", n)
     if m:
         return "chain<%s,%s,%s>" % m.groups()
     m = re.search(r"(gemm_ab_kernel|gemm_atb_kernel|gemm_atb_reduce|bimg_prob_kernel)<[^>]*?(\w+Prob|\w+Grad|F0Dh)\b", n)

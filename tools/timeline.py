@@ -11,7 +11,7 @@ from paper_2506_21788_b200._lib import check, lib
 
 
 def short(n):
-    for pat, fmt in ((r"(TcRow|TcRed)<.*?::(\w+Prob|\w+Grad|F0Dh)>", "{0}<{1}>"), (r"chain_kernel<(\d+), (\d+), \(?(?:int\))?(-?\d+)>", "chain<{0},{1},{2}>"),
+    for pat, fmt in ((r"(TcRow|TcRed)<.*?::(\w+Prob|\w+Grad|F0Dh)>", "{0}<{1}>"), (r"chain_kernel<(\d+), (\d+), \(?(?:int\))?(-?\d+)(?:, \d+)?>", "chain<{0},{1},{2}>"),
                      (r"split_reduce_kernel<.*?(ChunkStore|EmbedStore|RedStore)", "split<{0}>")):
         m = re.search(pat, n)
         if m:
