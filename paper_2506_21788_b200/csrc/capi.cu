@@ -256,6 +256,7 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   c.red_sms = c.sm_count;
   if (const char* e = std::getenv("HMTL_CHAIN_CS")) c.chain_cs = std::atoi(e) == 2 ? 2 : 1;
   if (const char* e = std::getenv("HMTL_NO_RED_TMA")) c.red_tma = e[0] == '0';
+  if (const char* e = std::getenv("HMTL_RED_SEGX")) c.red_seg_mult = std::max(1, std::min(8, std::atoi(e)));
   if (const char* e = std::getenv("HMTL_RED_MINCH")) c.red_min_chunks = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("HMTL_RED_SMS")) c.red_sms = std::max(1, std::min(c.sm_count, std::atoi(e)));
   if (const char* e = std::getenv("HMTL_NO_PREFETCH")) c.prefetch_l2 = e[0] == '0';

@@ -706,7 +706,10 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
     const long long chunks = (rows_cap > 0 ? rows_cap : (long long)c.Ec) / tc::KC + 1;
     // enough CTAs to fill the GPU, >= 4 chunks each (bounded partial traffic)
     // one wave over red_sms SMs (side-stream weight gradients leave the rest to the critical path)
-    long long want = std::max<long long>(1, (long long)c.red_sms / (mtiles * p.rows.nseg));
+    // head-segmented rows: segments differ in size (edge shares 1:1:1:2:3), so each gets up to
+    // red_seg_mult x its even share of CTAs; CTAs past a short segment's chunks store zeros
+    const long long segx = p.rows.nseg > 1 ? c.red_seg_mult : 1;
+    long long want = std::max<long long>(1, (long long)c.red_sms * segx / (mtiles * p.rows.nseg));
     int ns = int(std::max<long long>(1, std::min<long long>(want, chunks / c.red_min_chunks)));
     float* partial = c.part(st);
     while (ns > 1 && size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * NW > c.partial_cap) ns /= 2;
