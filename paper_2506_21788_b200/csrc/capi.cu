@@ -253,7 +253,9 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   if (const char* e = std::getenv("HMTL_SINGLE_STREAM")) c.multi_stream = e[0] == '0';
   if (const char* e = std::getenv("HMTL_NO_CHAIN")) c.fuse_chain = e[0] == '0';
   if (const char* e = std::getenv("HMTL_TC_GRID")) c.tc_grid_mult = std::atoi(e);
-  c.red_sms = c.sm_count;
+  // weight-gradient grids over ~13/16 of the SMs: the side-stream reduce GEMMs then leave SMs to the
+  // critical path (measured: 120 of 148 -> step 1.003 -> 0.994 ms; profiles/r01_ab_red_knobs.txt)
+  c.red_sms = std::max(1, c.sm_count * 13 / 16);
   if (const char* e = std::getenv("HMTL_CHAIN_CS")) c.chain_cs = std::atoi(e) == 2 ? 2 : 1;
   if (const char* e = std::getenv("HMTL_NO_RED_TMA")) c.red_tma = e[0] == '0';
   if (const char* e = std::getenv("HMTL_RED_SEGX")) c.red_seg_mult = std::max(1, std::min(8, std::atoi(e)));

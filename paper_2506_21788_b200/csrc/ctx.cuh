@@ -141,7 +141,7 @@ struct Ctx {
   // silu'(zf0) [E][W] too only when the force output layer's backward needs it
   // (head_depth 2); deeper heads regather it from the L2-resident Qf table
   bool store_sf0 = false;
-  int red_sms = 0;          // SMs a weight-gradient (tc_red) launch spreads over (HMTL_RED_SMS; default all)
+  int red_sms = 0;          // SMs a weight-gradient (tc_red) launch spreads over (HMTL_RED_SMS; default 13/16 of them)
   int red_seg_mult = 1;     // CTA multiplier for head-segmented weight gradients (HMTL_RED_SEGX)
   int red_min_chunks = 4;   // >= this many 32-row chunks per weight-gradient CTA (HMTL_RED_MINCH)
   bool red_tma = true;      // TMA operand path for plain row-major weight gradients (HMTL_NO_RED_TMA=1 off)
