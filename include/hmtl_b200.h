@@ -155,6 +155,11 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
                     int n_owned, const hmtl_caps* caps, hmtl_ctx** out);
 void hmtl_ctx_destroy(hmtl_ctx* ctx);
 void* hmtl_ctx_stream(hmtl_ctx* ctx);
+/* Grow the context's batch capacities to at least `need` in place: parameters,
+ * AdamW m/v and step counter, streams, the batch pool and an attached NCCL
+ * communicator all survive (the reference's ModelT has no capacities; this is
+ * what lets a growing batch keep training state).  No-op when `need` fits. */
+int hmtl_ctx_reserve(hmtl_ctx* ctx, const hmtl_caps* need);
 
 /* shared_block()/head_block(k) (hmtl/model.hpp:182-187): host <-> device. */
 int hmtl_set_block(hmtl_ctx* ctx, int which, const float* host);
@@ -246,6 +251,15 @@ int hmtl_hmtd_read_header(const char* path, uint8_t* dataset_id, uint8_t* aligne
 /* build_batch<float> on the device (hmtl/graph.hpp:46-83): bit-exact FP64
  * cutoff test, dst-major CSR, reverse-edge permutation, per-graph edge offsets. */
 int hmtl_build_batch(hmtl_ctx* ctx, void* stream);
+/* build_batch's edge set without a model context (hmtl/graph.hpp:46-83; SURVEY.md
+ * 8(b) hmtl_nbr_build): the same bit-exact FP64 cutoff search on `device` as the
+ * training step.  *E receives the edge count; edge_dst/edge_src[E] (dst-major,
+ * ascending src), edge_offset[G+1], row_ptr[N+1] (CSR by dst) and rev[E] (index
+ * of the reverse edge) are filled when non-NULL, provided E <= cap (else
+ * HMTL_ERR_CONTRACT with *E set, so a caller can size and retry).  Empty graphs
+ * are rejected as build_batch does (hmtl/graph.hpp:56). */
+int hmtl_nbr_build(int device, const hmtl_samples* s, double cutoff, long long cap, int* E, int* edge_dst,
+                   int* edge_src, int* edge_offset, int* row_ptr, int* rev);
 /* n_graphs / n_nodes of the batch last bound (upload, pool, store bind/fetch). */
 int hmtl_batch_shape(hmtl_ctx* ctx, int* G, int* N);
 /* GraphBatchT edge view (syncs): *E, and optionally edge_dst/edge_src[E], edge_offset[G+1]. */

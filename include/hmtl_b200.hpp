@@ -223,14 +223,11 @@ class ModelT<float> {
     if (need.max_graphs <= caps_.max_graphs && need.max_nodes <= caps_.max_nodes &&
         need.max_edges <= caps_.max_edges)
       return;
-    auto sh = shared_block();
-    std::map<int, std::vector<float>> hd;
-    for (int k : owned_) hd[k] = head_block(k);
-    const_cast<ModelT*>(this)->create({std::max(need.max_graphs, caps_.max_graphs),
-                                       std::max(need.max_nodes, caps_.max_nodes),
-                                       std::max(need.max_edges, caps_.max_edges)});
-    check(hmtl_set_block(ctx_->p, -1, sh.data()));
-    for (auto& kv : hd) check(hmtl_set_block(ctx_->p, kv.first, kv.second.data()));
+    // in place: parameters, AdamW state, step counter and communicator survive
+    const hmtl_caps grown{std::max(need.max_graphs, caps_.max_graphs), std::max(need.max_nodes, caps_.max_nodes),
+                          std::max(need.max_edges, caps_.max_edges)};
+    check(hmtl_ctx_reserve(ctx_->p, &grown));
+    const_cast<ModelT*>(this)->caps_ = grown;
   }
   void upload(const GraphBatchT<float>& b) const {
     reserve(detail::caps_for(b.n_atoms_));
@@ -282,28 +279,18 @@ inline GraphBatchT<float> build_batch<float>(const std::vector<AtomisticSample>&
     b.label_energy.push_back(float(s.energy_per_atom));
     b.energy64_.push_back(s.energy_per_atom);
   }
-  // device neighbour search (hmtl/graph.hpp:65-76 semantics, bit-exact)
-  ModelHyper hp;
-  hp.hidden = hp.head_width = 1;
-  hp.layers = 1;
-  hp.n_heads = 255;
-  hp.cutoff = cutoff;
-  std::vector<int> all;
-  for (const auto& s : samples) {
-    bool seen = false;
-    for (int a : all) seen |= a == s.dataset_id;
-    if (!seen) all.push_back(s.dataset_id);
-  }
-  if (all.size() > 16) all.resize(16);
-  ModelT<float> nb(hp, 0, all, device);
-  nb.upload(b);
-  check(hmtl_build_batch(nb.handle(), nullptr));
+  // device neighbour search (hmtl/graph.hpp:65-76 semantics, bit-exact), no model context
+  const hmtl_samples cs = b.c();
   int E = 0;
-  check(hmtl_batch_edges(nb.handle(), &E, nullptr, nullptr, nullptr));
+  long long cap = 0;
+  for (int n : b.n_atoms_) cap += (long long)n * (n - 1);
+  b.edge_dst.resize(size_t(cap));
+  b.edge_src.resize(size_t(cap));
+  b.edge_offset.resize(b.n_graphs + 1);
+  check(hmtl_nbr_build(device, &cs, cutoff, cap, &E, b.edge_dst.data(), b.edge_src.data(), b.edge_offset.data(),
+                       nullptr, nullptr));
   b.edge_dst.resize(E);
   b.edge_src.resize(E);
-  b.edge_offset.resize(b.n_graphs + 1);
-  check(hmtl_batch_edges(nb.handle(), &E, b.edge_dst.data(), b.edge_src.data(), b.edge_offset.data()));
   return b;
 }
 

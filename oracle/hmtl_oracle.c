@@ -288,9 +288,20 @@ long ho_build_edges_pbc(int G, const int* n_atoms, const double* pos, const doub
 }
 
 /* ------------------------------------------------------------ numcore ----- */
+/* Threading (OpenMP, the checker's only concession to full-size parity runs):
+ * every parallel loop below splits work so that each output element is still
+ * produced by ONE thread with the reference's operation sequence -- rows of y /
+ * dx are independent, and accumulations (dW, db, segment sums, scatters) are
+ * split by output element with the reduction loop (ascending batch row / edge)
+ * kept inside.  Results are therefore bit-identical to the serial loops for any
+ * thread count (pinned by tests/test_oracle_golden.py against the reference). */
+#define HO_PAR _Pragma("omp parallel for schedule(static)")
+#define HO_PAR_DYN _Pragma("omp parallel for schedule(dynamic, 1)")
+
 /* hmtl/kernels.hpp:19-32 */
 static void linear_forward(const double* x, size_t batch, size_t in, const double* W,
                            size_t out, const double* bias, double* y) {
+  HO_PAR
   for (size_t b = 0; b < batch; ++b) {
     double* yb = y + b * out;
     for (size_t o = 0; o < out; ++o) yb[o] = bias ? bias[o] : 0.0;
@@ -303,18 +314,35 @@ static void linear_forward(const double* x, size_t batch, size_t in, const doubl
   }
 }
 /* hmtl/kernels.hpp:37-59 (accumulates into dW/db) */
+/* (element (i,o) of dW receives xb[i]*ub[o] for b ascending exactly as the
+ * reference's row loop; rows are visited in blocks of 64 so a block of `up`
+ * stays cache-resident across a thread's dW rows) */
 static void linear_backward(const double* x, size_t batch, size_t in, const double* W,
                             size_t out, const double* up, double* dW, double* db, double* dx) {
-  for (size_t b = 0; b < batch; ++b) {
-    const double* xb = x + b * in;
-    const double* ub = up + b * out;
-    for (size_t i = 0; i < in; ++i) {
-      const double xi = xb[i];
-      double* dWi = dW + i * out;
-      for (size_t o = 0; o < out; ++o) dWi[o] += xi * ub[o];
+  const size_t BB = 64;
+  HO_PAR_DYN
+  for (size_t i0 = 0; i0 < in; i0 += 8) {
+    const size_t i1 = i0 + 8 < in ? i0 + 8 : in;
+    for (size_t b0 = 0; b0 < batch; b0 += BB) {
+      const size_t b1 = b0 + BB < batch ? b0 + BB : batch;
+      for (size_t i = i0; i < i1; ++i) {
+        double* dWi = dW + i * out;
+        for (size_t b = b0; b < b1; ++b) {
+          const double xi = x[b * in + i];
+          const double* ub = up + b * out;
+          for (size_t o = 0; o < out; ++o) dWi[o] += xi * ub[o];
+        }
+      }
     }
+  }
+  for (size_t b = 0; b < batch; ++b) {
+    const double* ub = up + b * out;
     for (size_t o = 0; o < out; ++o) db[o] += ub[o];
-    if (dx) {
+  }
+  if (dx) {
+    HO_PAR
+    for (size_t b = 0; b < batch; ++b) {
+      const double* ub = up + b * out;
       double* dxb = dx + b * in;
       for (size_t i = 0; i < in; ++i) {
         const double* Wi = W + i * out;
@@ -375,8 +403,10 @@ static void mlp_forward(const ho_hyper* hp, const double* block, const lay_t* L,
     linear_forward(cur, rows, in, block + L->off[we], od, block + L->off[be], z);
     z_out[i] = xmalloc(rows * od * sizeof(double));
     memcpy(z_out[i], z, rows * od * sizeof(double));
-    if (i + 1 < D)
+    if (i + 1 < D) {
+      HO_PAR
       for (size_t t = 0; t < rows * od; ++t) z[t] = silu(z[t]);
+    }
     cur = z;
     in = od;
   }
@@ -395,6 +425,7 @@ static double* mlp_backward(const ho_hyper* hp, const double* block, double* gbl
     int we = first + 2 * i, be = first + 2 * i + 1;
     size_t od = L->cols[we], in = L->rows[we];
     if (i + 1 < D) {
+      HO_PAR
       for (size_t t = 0; t < rows * od; ++t) up[t] = up[t] * silu_grad(z[i][t]);
     }
     double* dx = xmalloc(rows * in * sizeof(double));
@@ -463,6 +494,7 @@ int ho_forward(const ho_hyper* hp, const double* shared, const double* const* he
     const double *nW2 = shared + SL.off[base + 6], *nb2 = shared + SL.off[base + 7];
     if (c && c->h_in) memcpy(c->h_in + (size_t)l * N * H, h, N * H * sizeof(double));
     /* message m_ij = phi_e(h_i, h_j, d_ij^2), :388-406 */
+    HO_PAR
     for (size_t e = 0; e < E; ++e) {
       double* ue = u + e * K1;
       const double* hd = h + (size_t)b->edge_dst[e] * H;
@@ -472,15 +504,22 @@ int ho_forward(const ho_hyper* hp, const double* shared, const double* const* he
       ue[2 * H] = d2[e];
     }
     linear_forward(u, E, K1, eW1, H, eb1, z1);
+    HO_PAR
     for (size_t t = 0; t < E * H; ++t) a1[t] = silu(z1[t]);
     linear_forward(a1, E, H, eW2, H, eb2, z2);
+    HO_PAR
     for (size_t t = 0; t < E * H; ++t) m[t] = silu(z2[t]);
-    /* segment_sum over dst, ascending e: hmtl/kernels.hpp:97-108 */
+    /* segment_sum over dst, ascending e: hmtl/kernels.hpp:97-108 (columns split
+     * over threads, every column's sum in edge order) */
     memset(agg, 0, N * H * sizeof(double));
-    for (size_t e = 0; e < E; ++e) {
-      double* os = agg + (size_t)b->edge_dst[e] * H;
-      const double* vr = m + e * H;
-      for (size_t k = 0; k < H; ++k) os[k] += vr[k];
+    HO_PAR
+    for (size_t k0 = 0; k0 < H; k0 += 4) {
+      const size_t k1 = k0 + 4 < H ? k0 + 4 : H;
+      for (size_t e = 0; e < E; ++e) {
+        double* os = agg + (size_t)b->edge_dst[e] * H;
+        const double* vr = m + e * H;
+        for (size_t k = k0; k < k1; ++k) os[k] += vr[k];
+      }
     }
     /* node update with residual, :408-426 */
     for (size_t i = 0; i < N; ++i) {
@@ -490,6 +529,7 @@ int ho_forward(const ho_hyper* hp, const double* shared, const double* const* he
     linear_forward(v, N, 2 * H, nW1, H, nb1, vz1);
     for (size_t t = 0; t < N * H; ++t) vp1[t] = silu(vz1[t]);
     linear_forward(vp1, N, H, nW2, H, nb2, q);
+    HO_PAR
     for (size_t t = 0; t < N * H; ++t) h[t] += q[t];
     if (c) {
       const size_t oe = (size_t)l * E * H, on = (size_t)l * N * H;
@@ -551,6 +591,7 @@ int ho_forward(const ho_hyper* hp, const double* shared, const double* const* he
     for (size_t gi = 0; gi < Gk; ++gi)
       for (int e = b->edge_offset[graphs[gi]]; e < b->edge_offset[graphs[gi] + 1]; ++e) edges[Ek++] = e;
     double* psi = xmalloc((Ek ? Ek : 1) * (H + 1) * sizeof(double));
+    HO_PAR
     for (size_t ei = 0; ei < Ek; ++ei) {
       int e = edges[ei];
       const double* hd = h + (size_t)b->edge_dst[e] * H;
@@ -678,6 +719,7 @@ int ho_backward(const ho_hyper* hp, const double* shared, const double* const* h
       size_t od = HL.cols[ff_first + 2 * i], in = HL.rows[ff_first + 2 * i];
       fz[i] = xmalloc((Ek ? Ek : 1) * od * sizeof(double));
       fa[i] = xmalloc((Ek ? Ek : 1) * in * sizeof(double));
+      HO_PAR
       for (size_t ei = 0; ei < Ek; ++ei) {
         int e = edges[ei];
         for (size_t o = 0; o < od; ++o) fz[i][ei * od + o] = c->fz[((size_t)i * E + e) * W + o];
@@ -700,14 +742,18 @@ int ho_backward(const ho_hyper* hp, const double* shared, const double* const* h
       ds[ei] = acc;
     }
     double* dpsi = mlp_backward(hp, block, gblock, &HL, ff_first, Ek, fz, fa, ds);
-    for (size_t ei = 0; ei < Ek; ++ei) {
-      int e = edges[ei];
-      const double* dpe = dpsi + ei * (H + 1);
-      double* dhd = dh + (size_t)b->edge_dst[e] * H;
-      double* dhs = dh + (size_t)b->edge_src[e] * H;
-      for (size_t kk = 0; kk < H; ++kk) {
-        dhd[kk] += dpe[kk];
-        dhs[kk] += dpe[kk];
+    HO_PAR
+    for (size_t k0 = 0; k0 < H; k0 += 4) { /* columns split; each in edge order */
+      const size_t k1 = k0 + 4 < H ? k0 + 4 : H;
+      for (size_t ei = 0; ei < Ek; ++ei) {
+        int e = edges[ei];
+        const double* dpe = dpsi + ei * (H + 1);
+        double* dhd = dh + (size_t)b->edge_dst[e] * H;
+        double* dhs = dh + (size_t)b->edge_src[e] * H;
+        for (size_t kk = k0; kk < k1; ++kk) {
+          dhd[kk] += dpe[kk];
+          dhs[kk] += dpe[kk];
+        }
       }
     }
     for (int i = 0; i < D; ++i) free(fz[i]), free(fa[i]);
@@ -759,12 +805,15 @@ int ho_backward(const ho_hyper* hp, const double* shared, const double* const* h
         dagg[i * H + kk] = dv[i * 2 * H + H + kk];
       }
     /* edge path, :589-615 */
+    HO_PAR
     for (size_t e = 0; e < E; ++e) {
       const double* da = dagg + (size_t)b->edge_dst[e] * H;
       for (size_t kk = 0; kk < H; ++kk) dz2[e * H + kk] = da[kk] * silu_grad(z2[e * H + kk]);
     }
     linear_backward(a1, E, H, eW2, H, dz2, geW2, geb2, da1);
+    HO_PAR
     for (size_t t = 0; t < E * H; ++t) da1[t] = da1[t] * silu_grad(z1[t]);
+    HO_PAR
     for (size_t e = 0; e < E; ++e) {
       double* ue = u + e * K1;
       const double* hd = hin + (size_t)b->edge_dst[e] * H;
@@ -774,13 +823,17 @@ int ho_backward(const ho_hyper* hp, const double* shared, const double* const* h
       ue[2 * H] = d2[e];
     }
     linear_backward(u, E, K1, eW1, H, da1, geW1, geb1, du);
-    for (size_t e = 0; e < E; ++e) {
-      const double* due = du + e * K1;
-      double* dhd = dh_in + (size_t)b->edge_dst[e] * H;
-      double* dhs = dh_in + (size_t)b->edge_src[e] * H;
-      for (size_t kk = 0; kk < H; ++kk) {
-        dhd[kk] += due[kk];
-        dhs[kk] += due[H + kk];
+    HO_PAR
+    for (size_t k0 = 0; k0 < H; k0 += 4) { /* columns split; each in edge order */
+      const size_t k1 = k0 + 4 < H ? k0 + 4 : H;
+      for (size_t e = 0; e < E; ++e) {
+        const double* due = du + e * K1;
+        double* dhd = dh_in + (size_t)b->edge_dst[e] * H;
+        double* dhs = dh_in + (size_t)b->edge_src[e] * H;
+        for (size_t kk = k0; kk < k1; ++kk) {
+          dhd[kk] += due[kk];
+          dhs[kk] += due[H + kk];
+        }
       }
     }
     memcpy(dh, dh_in, N * H * sizeof(double));

@@ -87,6 +87,9 @@ SIGNATURES = {
                                   C.POINTER(_P)]),
     "hmtl_ctx_destroy": (None, [_P]),
     "hmtl_ctx_stream": (_P, [_P]),
+    "hmtl_ctx_reserve": (C.c_int, [_P, C.POINTER(CCaps)]),
+    "hmtl_nbr_build": (C.c_int, [C.c_int, C.POINTER(CSamples), C.c_double, C.c_longlong, _IP, _IP, _IP, _IP, _IP,
+                                 _IP]),
     "hmtl_set_block": (C.c_int, [_P, C.c_int, _FP]),
     "hmtl_get_block": (C.c_int, [_P, C.c_int, _FP]),
     "hmtl_get_grad": (C.c_int, [_P, C.c_int, _FP]),

@@ -394,6 +394,54 @@ void hmtl_ctx_destroy(hmtl_ctx* h) {
 
 void* hmtl_ctx_stream(hmtl_ctx* h) { return h ? h->c.stream : nullptr; }
 
+// Grow the capacity-padded batch buffers in place.  Everything that outlives a
+// batch -- parameters, gradients, AdamW m/v, the device header (step counter),
+// streams (callers may hold hmtl_ctx_stream), the NCCL communicators, the
+// recorded tensor-core B images and the batch pool -- stays with the handle; only
+// the capacity-sized buffers are replaced and the captured step graph dropped.
+int hmtl_ctx_reserve(hmtl_ctx* h, const hmtl_caps* need) {
+  if (!h || !need) return fail(HMTL_ERR_CONTRACT, "ctx_reserve: null argument");
+  Ctx& c = h->c;
+  if (need->max_graphs <= c.Gc && need->max_nodes <= c.Nc && need->max_edges <= c.Ec) return 0;
+  hmtl_caps caps{std::max(need->max_graphs, c.Gc), std::max(need->max_nodes, c.Nc), std::max(need->max_edges, c.Ec)};
+  cudaSetDevice(c.device);
+  HMTL_CUDA(cudaDeviceSynchronize());
+  hmtl_ctx* fresh = nullptr;
+  if (int rc = hmtl_ctx_create(c.device, &c.hp, 0, c.owned.data(), int(c.owned.size()), &caps, &fresh)) return rc;
+  Ctx& n = fresh->c;
+  std::swap(c, n);  // c: new capacity buffers; n: the old context
+  // state that outlives a batch goes back to the handle (n's copies are freed with it)
+  std::swap(c.params, n.params);
+  std::swap(c.grads, n.grads);
+  std::swap(c.adam_m, n.adam_m);
+  std::swap(c.adam_v, n.adam_v);
+  std::swap(c.hdr, n.hdr);
+  std::swap(c.stream, n.stream);
+  std::swap(c.s_e, n.s_e);
+  std::swap(c.s_w, n.s_w);
+  std::swap(c.s_w2, n.s_w2);
+  std::swap(c.s_c, n.s_c);
+  std::swap(c.comm, n.comm);
+  std::swap(c.pool, n.pool);
+  std::swap(c.pool_bytes, n.pool_bytes);
+  std::swap(c.bimg_all, n.bimg_all);
+  std::swap(c.bimg_all_cap, n.bimg_all_cap);
+  std::swap(c.d_bjobs, n.d_bjobs);
+  std::swap(c.bjobs, n.bjobs);
+  std::swap(c.n_djobs, n.n_djobs);
+  std::swap(c.bimg_rows, n.bimg_rows);
+  std::swap(c.bimg_ready, n.bimg_ready);
+  std::swap(c.bimg_stale, n.bimg_stale);
+  std::swap(c.prof_on, n.prof_on);
+  std::swap(c.host_G, n.host_G);
+  std::swap(c.host_N, n.host_N);
+  // tuning knobs set after creation
+  c.multi_stream = n.multi_stream;
+  c.overlap_comm = n.overlap_comm;
+  hmtl_ctx_destroy(fresh);  // frees the old capacity buffers and the old step graph
+  return 0;
+}
+
 static int block_span(Ctx& c, int which, size_t* off, size_t* n) {
   if (which < 0) {
     *off = 0;
@@ -583,6 +631,44 @@ int hmtl_build_batch(hmtl_ctx* h, void* stream) {
   launch_nbr(c, st);
   HMTL_CUDA(cudaGetLastError());
   return 0;
+}
+
+// build_batch's edge construction without a model (hmtl/graph.hpp:46-83): a
+// scratch context sized to the batch (every dataset id accepted), the same
+// kernels as the training step (bit-exact FP64 cutoff test, dst-major CSR).
+int hmtl_nbr_build(int device, const hmtl_samples* s, double cutoff, long long cap, int* E, int* edge_dst,
+                   int* edge_src, int* edge_offset, int* row_ptr, int* rev) {
+  if (!s || !E) return fail(HMTL_ERR_CONTRACT, "nbr_build: null argument");
+  if (s->G <= 0 || s->N <= 0) return fail(HMTL_ERR_CONTRACT, "build_batch: empty batch rejected");
+  long long bound = 0;
+  for (int g = 0; g < s->G; ++g) {
+    const long long n = s->n_atoms[g];
+    if (n < 1) return fail(HMTL_ERR_CONTRACT, "build_batch: empty graph rejected");
+    bound += n * (n - 1);
+  }
+  hmtl_hyper hp{1, 1, 1, 1, 2, 1, cutoff};
+  const int owned = 0;
+  const hmtl_caps caps{s->G, s->N, std::max(bound, 1LL)};
+  hmtl_ctx* h = nullptr;
+  if (int rc = hmtl_ctx_create(device, &hp, 0, &owned, 1, &caps, &h)) return rc;
+  Ctx& c = h->c;
+  std::fill(c.slot_of, c.slot_of + 256, 0);  // no heads here: every dataset id maps to slot 0
+  int rc = 0;
+  if (cudaMemcpy(c.d_slot_of, c.slot_of, 256 * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
+    rc = fail(HMTL_ERR_INTERNAL, "nbr_build: slot table upload failed");
+  if (!rc) rc = hmtl_batch_upload(h, s, nullptr);
+  if (!rc) rc = hmtl_build_batch(h, nullptr);
+  if (!rc) rc = hmtl_batch_edges(h, E, nullptr, nullptr, nullptr);
+  if (!rc && (edge_dst || edge_src || rev) && *E > cap)
+    rc = fail(HMTL_ERR_CONTRACT, "nbr_build: " + std::to_string(*E) + " edges exceed the output capacity");
+  if (!rc) rc = hmtl_batch_edges(h, E, edge_dst, edge_src, edge_offset);
+  const size_t ne = size_t(*E);
+  if (!rc && row_ptr && cudaMemcpy(row_ptr, c.row_ptr, (size_t(s->N) + 1) * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = fail(HMTL_ERR_INTERNAL, "nbr_build: row_ptr copy failed");
+  if (!rc && rev && ne && cudaMemcpy(rev, c.rev, ne * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = fail(HMTL_ERR_INTERNAL, "nbr_build: rev copy failed");
+  hmtl_ctx_destroy(h);
+  return rc;
 }
 
 int hmtl_batch_edges(hmtl_ctx* h, int* E, int* edge_dst, int* edge_src, int* edge_offset) {

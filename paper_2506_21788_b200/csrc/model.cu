@@ -2255,13 +2255,20 @@ void launch_debug_z1(Ctx& c, int l, float* out, cudaStream_t st) {
 
 // ---------------------------------------------------------------- AdamW
 namespace {
+// A step whose batch raised a device error (edge overflow, unowned head, empty
+// graph, non-finite prediction) leaves the parameters, m/v and the step counter
+// untouched: the reference throws before any update (hmtl/model.hpp:341-347,
+// 483-486) and the host raises the same error when it reads the step's result.
 __global__ void adam_tick(DevHdr* hdr) {
-  pdl_wait(); hdr->step += 1; }
+  pdl_wait();
+  if (hdr->err == 0) hdr->step += 1;
+}
 // torch.optim.AdamW ordering (decision recorded in DESIGN.md)
 __global__ void adamw_kernel(const DevHdr* hdr, float* __restrict__ p, const float* __restrict__ g,
                              float* __restrict__ m, float* __restrict__ v, size_t n, float lr, float b1, float b2,
                              float eps, float wd) {
   pdl_wait();
+  if (hdr->err != 0) return;  // see adam_tick
   const int t = hdr->step;
   const float bc1 = float(1.0 - pow(double(b1), double(t)));
   const float bc2s = float(sqrt(1.0 - pow(double(b2), double(t))));

@@ -9,6 +9,7 @@
 // in ascending-src order directly -- no sort, bit-exact edge set.  Graphs are
 // small (<= a few hundred atoms) so the per-graph all-pairs tile is the
 // cheapest exact search; rows of different graphs never interact.
+#include <algorithm>
 #include <cmath>
 
 #include "ctx.cuh"
@@ -172,11 +173,28 @@ __global__ void nbr_write_kernel(const uint8_t* __restrict__ arena, const DevHdr
 
 // reverse-edge permutation: rev[(i,j)] = index of (j,i).  The FP64 test is
 // symmetric bit-for-bit ((a-b)^2 == (b-a)^2), so (j,i) always exists.
-__global__ void rev_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const int* __restrict__ edge_src,
-                           const int* __restrict__ edge_dst, int* __restrict__ rev, long long Ec) {
+// Edge-capacity overflow (open boundaries: E > Ec; periodic: a row past the
+// per-row bound) leaves a partial edge set.  The reference throws in build_batch
+// (hmtl/graph.hpp:56 contract); the device step instead empties the batch's edge
+// structure (E = 0, every CSR row and graph edge range empty) so no later kernel
+// of the captured step reads past the Ec-sized buffers, and the error bit makes
+// the host raise and AdamW skip the update.  Returns true when it did.
+__device__ __forceinline__ bool overflow_guard(DevHdr* hdr, int* row_ptr, int* edge_offset) {
+  if (!(hdr->err & kErrEdgeOverflow)) return false;
+  const int N = hdr->N, G = hdr->G;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= N || t <= G; t += gridDim.x * blockDim.x) {
+    if (t <= N) row_ptr[t] = 0;
+    if (t <= G) edge_offset[t] = 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) hdr->E = 0;
+  return true;
+}
+
+__global__ void rev_kernel(DevHdr* hdr, int* __restrict__ row_ptr, const int* __restrict__ edge_src,
+                           const int* __restrict__ edge_dst, int* __restrict__ rev, int* __restrict__ edge_offset) {
   pdl_wait();
+  if (overflow_guard(hdr, row_ptr, edge_offset)) return;
   const int E = hdr->E;
-  if (E > Ec) return;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
     const int i = edge_dst[e], j = edge_src[e];
     int lo = row_ptr[j], hi = row_ptr[j + 1];
@@ -314,8 +332,8 @@ void launch_nbr(Ctx& c, cudaStream_t st) {
   }
   {
     Prof pr(c, "nbr.rev", st);
-    kl(rev_kernel, grid_for(c.Ec, 256, c.sm_count * 8), 256, 0, st, c.hdr, c.row_ptr, c.edge_src, c.edge_dst, c.rev,
-                                                                     c.Ec);
+    kl(rev_kernel, grid_for(std::max<long long>(c.Ec, c.Nc + 1), 256, c.sm_count * 8), 256, 0, st, c.hdr, c.row_ptr,
+       c.edge_src, c.edge_dst, c.rev, c.edge_offset);
   }
   launch_route(c, st);
 }
@@ -559,12 +577,12 @@ __global__ void __launch_bounds__(256) pbc_row_kernel(const uint8_t* __restrict_
 }
 
 // reverse of (i, j, n) is (j, i, -n): binary search of row j on the (src, image) key
-__global__ void pbc_rev_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const int* __restrict__ edge_src,
+__global__ void pbc_rev_kernel(DevHdr* hdr, int* __restrict__ row_ptr, const int* __restrict__ edge_src,
                                const int* __restrict__ edge_dst, const int* __restrict__ eimg, int* __restrict__ rev,
-                               long long Ec) {
+                               int* __restrict__ edge_offset) {
   pdl_wait();
+  if (overflow_guard(hdr, row_ptr, edge_offset)) return;
   const int E = hdr->E;
-  if (E > Ec) return;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
     const int i = edge_dst[e], j = edge_src[e];
     int n1, n2, n3;
@@ -608,8 +626,8 @@ void launch_nbr_pbc(Ctx& c, cudaStream_t st) {
   }
   {
     Prof pr(c, "nbr.rev", st);
-    kl(pbc_rev_kernel, grid_for(c.Ec, 256, c.sm_count * 8), 256, 0, st, c.hdr, c.row_ptr, c.edge_src, c.edge_dst,
-       c.eimg, c.rev, c.Ec);
+    kl(pbc_rev_kernel, grid_for(std::max<long long>(c.Ec, c.Nc + 1), 256, c.sm_count * 8), 256, 0, st, c.hdr,
+       c.row_ptr, c.edge_src, c.edge_dst, c.eimg, c.rev, c.edge_offset);
   }
 }
 

@@ -81,6 +81,7 @@ struct hmtl_store {
   int items_cap = 0;
   uint8_t *d_send = nullptr, *d_recv = nullptr;
   size_t send_cap = 0, recv_cap = 0;
+  int* d_flag = nullptr;  // fetch plan consensus (allreduce min)
 };
 
 namespace {
@@ -633,9 +634,18 @@ int hmtl_store_fetch(hmtl_ctx* h, hmtl_store* st, const uint8_t* plan_ds, const 
   if (!comm || rank != st->rank || world != st->world)
     return fail(HMTL_ERR_CONTRACT, "store_fetch: context communicator differs from the store's");
   const int n = b_local;
-  if (n > c.Gc) return fail(HMTL_ERR_CONTRACT, "batch exceeds context capacity (graphs/nodes)");
   cudaSetDevice(c.device);
   cudaStream_t sm = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+  // A rank that rejects its plan must not return while its peers enter the
+  // grouped send/recv (they would wait forever): every check below only records
+  // the first failure, and all ranks agree on the outcome with one tiny
+  // allreduce(min) before any exchange.
+  int bad_rc = 0;
+  std::string bad_msg;
+  auto reject = [&](int rc, const std::string& msg) {
+    if (!bad_rc) bad_rc = rc, bad_msg = msg;
+  };
+  if (n > c.Gc) reject(HMTL_ERR_CONTRACT, "batch exceeds context capacity (graphs/nodes)");
   auto find = [&](uint8_t d, uint64_t i, const StorePart** sp) -> int {
     auto it = st->part.find(d);
     if (it == st->part.end() || i >= it->second.count) return -1;
@@ -652,7 +662,10 @@ int hmtl_store_fetch(hmtl_ctx* h, hmtl_store* st, const uint8_t* plan_ds, const 
       const uint64_t i = plan_idx[size_t(r) * n + b];
       const StorePart* sp = nullptr;
       const int o = find(d, i, &sp);
-      if (o < 0) return fail(HMTL_ERR_CONTRACT, "owner_of: index out of range");
+      if (o < 0) {
+        if (r == rank) reject(HMTL_ERR_CONTRACT, "owner_of: index out of range");
+        continue;  // (a peer's bad row: that peer rejects it)
+      }
       if (r == rank && o != rank) recv_b[o] += wire_bytes(sp->n_atoms[i]);
       if (r != rank && o == rank) send_b[r] += wire_bytes(sp->n_atoms[i]);
     }
@@ -666,11 +679,12 @@ int hmtl_store_fetch(hmtl_ctx* h, hmtl_store* st, const uint8_t* plan_ds, const 
       const uint64_t i = plan_idx[size_t(r) * n + b];
       const StorePart* sp = nullptr;
       const int o = find(d, i, &sp);
+      if (o < 0) continue;
       const int na = sp->n_atoms[i];
       if (r == rank) {
         if (c.slot_of[d] < 0)
-          return fail(HMTL_ERR_CONTRACT, "model: unknown dataset id " + std::to_string(d) +
-                                             " (head not owned by this rank)");
+          reject(HMTL_ERR_CONTRACT, "model: unknown dataset id " + std::to_string(d) + " (head not owned by this rank)");
+        if (b >= int(mine.size())) continue;
         FetchItem& f = mine[b];
         f.n = na, f.ds = d, f.dst = 0, f.pad = 0;
         if (o == rank) f.kind = 0, f.src = st->by_dataset[d][i - sp->my_begin];
@@ -682,8 +696,20 @@ int hmtl_store_fetch(hmtl_ctx* h, hmtl_store* st, const uint8_t* plan_ds, const 
         sat[r] += wire_bytes(na);
       }
     }
-  if (N > c.Nc) return fail(HMTL_ERR_CONTRACT, "batch exceeds context capacity (graphs/nodes)");
-  if (bound > c.Ec) return fail(HMTL_ERR_CONTRACT, "batch may exceed the context's edge capacity");
+  if (N > c.Nc) reject(HMTL_ERR_CONTRACT, "batch exceeds context capacity (graphs/nodes)");
+  if (bound > c.Ec) reject(HMTL_ERR_CONTRACT, "batch may exceed the context's edge capacity");
+  if (world > 1) {  // consensus: every rank learns whether any rank rejected its plan
+    if (!st->d_flag) HMTL_CUDA(cudaMalloc(&st->d_flag, sizeof(int)));
+    const int mine_ok = bad_rc ? 0 : 1;
+    int all_ok = 0;
+    HMTL_CUDA(cudaMemcpyAsync(st->d_flag, &mine_ok, sizeof(int), cudaMemcpyHostToDevice, sm));
+    if (ncclAllReduce(st->d_flag, st->d_flag, 1, ncclInt32, ncclMin, comm, sm) != ncclSuccess)
+      return fail(HMTL_ERR_COMM, "store_fetch: plan consensus allreduce failed");
+    HMTL_CUDA(cudaMemcpyAsync(&all_ok, st->d_flag, sizeof(int), cudaMemcpyDeviceToHost, sm));
+    HMTL_CUDA(cudaStreamSynchronize(sm));
+    if (!all_ok && !bad_rc) reject(HMTL_ERR_CONTRACT, "store_fetch: a peer rank rejected its plan rows");
+  }
+  if (bad_rc) return fail(bad_rc, bad_msg);
   // staging: [G, N, 0, 0, graph_offset[G+1]] -> arena; items -> device
   const int words = 4 + (n + 1);
   const int n_items = int(pack.size()) + n;
@@ -954,7 +980,7 @@ int hmtl_store_destroy(hmtl_store* st) {
   cudaSetDevice(st->device);
   if (st->staged) cudaEventSynchronize(st->staged), cudaEventDestroy(st->staged);
   void* ptrs[] = {st->d_atom_off, st->d_ds,    st->d_species, st->d_energy, st->d_pos,
-                  st->d_forces,   st->d_sel,   st->d_items,   st->d_send,   st->d_recv};
+                  st->d_forces,   st->d_sel,   st->d_items,   st->d_send,   st->d_recv, st->d_flag};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (st->h_stage) cudaFreeHost(st->h_stage);

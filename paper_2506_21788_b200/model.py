@@ -142,6 +142,17 @@ class Caps:
     def for_samples(s: Samples, slack: float = 1.0) -> "Caps":
         return Caps(max(1, int(s.G * slack)), max(1, int(s.N * slack)), max(1, int(s.edge_bound() * slack)))
 
+    @staticmethod
+    def for_periodic(s: Samples, cells, cutoff: float, slack: float = 1.5) -> "Caps":
+        """Edge capacity for periodic structures, where the image
+        count, not n(n-1), bounds a row: n x (density x 4/3 pi rc^3 x slack + 16)."""
+        cells = np.asarray(cells, np.float64).reshape(s.G, 3, 3)
+        vol = np.abs(np.linalg.det(cells))
+        n = s.n_atoms.astype(np.float64)
+        per_atom = n / np.maximum(vol, 1e-12) * (4.0 / 3.0) * np.pi * cutoff ** 3
+        e = int(np.ceil((n * (per_atom * slack + 16.0)).sum()))
+        return Caps(max(1, s.G), max(1, s.N), max(1, e, s.edge_bound()))
+
     def covers(self, s: Samples) -> bool:
         return s.G <= self.max_graphs and s.N <= self.max_nodes and s.edge_bound() <= self.max_edges
 
@@ -218,13 +229,18 @@ class ModelT:
             for k, v in params.items():
                 check(lib().hmtl_set_block(self._ctx, k, _fp(v)))
 
-    def reserve(self, s: Samples) -> None:
-        """Grow the device capacities to fit `s` (keeps parameters, drops optimiser state)."""
-        if self.caps.covers(s):
+    def reserve(self, s: Samples, need: Caps | None = None) -> None:
+        """Grow the device capacities to fit `s` (or `need`) in place (hmtl_ctx_reserve):
+        parameters, AdamW state, step counter and an attached communicator all survive."""
+        if need is None:
+            if self.caps.covers(s):
+                return
+            need = Caps.for_samples(s, 1.25)
+        elif self.caps.union(need) == self.caps:
             return
-        params = {-1: self.shared_block(), **{k: self.head_block(k) for k in self.owned}}
-        self.close()
-        self._create(self.caps.union(Caps.for_samples(s, 1.25)), params)
+        caps = self.caps.union(need)
+        check(lib().hmtl_ctx_reserve(self._ctx, C.byref(CCaps(caps.max_graphs, caps.max_nodes, caps.max_edges))))
+        self.caps = caps
 
     def close(self):
         if self._ctx is not None:
@@ -284,7 +300,7 @@ class ModelT:
 
     def upload_pbc(self, s: Samples, cells, stream=None) -> None:
         """Periodic batch: samples + lattice cells[G][3][3] (rows a1..a3)."""
-        self.reserve(s)
+        self.reserve(s, Caps.for_samples(s, 1.25).union(Caps.for_periodic(s, cells, self.hp.cutoff)))
         self._keep = s
         self._cells = np.ascontiguousarray(cells, np.float64).reshape(s.G, 9)
         check(lib().hmtl_batch_upload_pbc(self._ctx, C.byref(s.as_c()),
@@ -394,6 +410,21 @@ class ModelT:
             check(lib().hmtl_read_loss(self._ctx, C.byref(L)))
             return float(L.value)
         return None
+
+
+def nbr_build(s: Samples, cutoff: float, device: int = 0) -> dict:
+    """build_batch's edge set without a model (hmtl_nbr_build; hmtl/graph.hpp:46-83):
+    edge_dst/edge_src[E], edge_offset[G+1], row_ptr[N+1] (CSR by dst), rev[E]."""
+    E = C.c_int()
+    cap = s.edge_bound()
+    out = {"edge_dst": np.zeros(max(cap, 1), np.int32), "edge_src": np.zeros(max(cap, 1), np.int32),
+           "edge_offset": np.zeros(s.G + 1, np.int32), "row_ptr": np.zeros(s.N + 1, np.int32),
+           "rev": np.zeros(max(cap, 1), np.int32)}
+    check(lib().hmtl_nbr_build(device, C.byref(s.as_c()), float(cutoff), cap, C.byref(E), _ip(out["edge_dst"]),
+                               _ip(out["edge_src"]), _ip(out["edge_offset"]), _ip(out["row_ptr"]), _ip(out["rev"])))
+    for k in ("edge_dst", "edge_src", "rev"):
+        out[k] = out[k][:E.value]
+    return out
 
 
 def _fp(a):
