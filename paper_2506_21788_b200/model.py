@@ -342,6 +342,13 @@ class ModelT:
         check(lib().hmtl_predictions(self._ctx, _fp(e), _fp(f)))
         return PredictionT(e, f.reshape(-1, 3))
 
+    def predictions(self) -> PredictionT:
+        """PredictionT of the last forward on the device (e.g. inside a train step), no recompute."""
+        e = np.zeros(self._G, np.float32)
+        f = np.zeros(3 * self._N, np.float32)
+        check(lib().hmtl_predictions(self._ctx, _fp(e), _fp(f)))
+        return PredictionT(e, f.reshape(-1, 3))
+
     def loss(self, w_energy: float = 1.0, w_force: float = 1.0) -> float:
         """SPEC loss on the device (also leaves dE/dF on the device for backward(None, None))."""
         check(lib().hmtl_loss(self._ctx, w_energy, w_force, None))
