@@ -286,6 +286,13 @@ def kernel_work(name, E, N, G, H, W, L, S, chain=True):
         "fwd.node_P": (2 * N * H * 2 * H, f4 * (N * H + N * 2 * H + 2 * H * H)),
         "fwd.edge_act": (0, f4 * (E * H + 2 * N * H) + 16 * E),
         "fwd.edge_msg_gemm": (2 * E * H * H, f4 * (2 * E * H + H * H)),
+        # fused gather -> GEMM -> segmented sum: writes a1, z2 (E x H), agg; node table P gathered (L2)
+        "fwd.edge_msg_fused": (2 * E * H * H, f4 * (2 * E * H + 3 * N * H + H * H) + 24 * E),
+        "bwd.edge_dz1_fused": (2 * E * H * H, f4 * (3 * E * H + 4 * N * H + H * H) + 24 * E),
+        "bwd.segsum_src": (E * H, f4 * (E * H + N * H) + 4 * E),
+        # cp.async gather producers: fwd writes a1, silu'(z1), z2; bwd reads z2, silu'(z1), writes dz2, dz1
+        "fwd.edge_msg_gather": (2 * E * H * H, f4 * (3 * E * H + 2 * N * H + H * H) + 24 * E),
+        "bwd.edge_dz1_gather": (2 * E * H * H, f4 * (4 * E * H + N * H + H * H) + 4 * E),
         "fwd.agg_segsum": (E * H, f4 * (E * H + N * H) + 4 * (N + 1)),
         "fwd.node_chain": (chain_f * N * H * H, f4 * (fchain_b * N * H + 5 * H * H)),
         "fwd.node_mlp1": (2 * N * 2 * H * H, f4 * (3 * N * H + 2 * H * H)),
@@ -322,7 +329,9 @@ def column_slices(name, H, W):
     return max(1, -(-n // per))
 
 
-GATHER_SCATTER = ("fwd.edge_act", "fwd.agg_segsum", "bwd.edge_act", "bwd.segsum_dst_src", "fwd.forces_segsum")
+GATHER_SCATTER = ("fwd.edge_act", "fwd.agg_segsum", "bwd.edge_act", "bwd.segsum_dst_src", "fwd.forces_segsum",
+                  "fwd.edge_msg_fused", "bwd.edge_dz1_fused", "bwd.segsum_src", "fwd.edge_msg_gather",
+                  "bwd.edge_dz1_gather")
 
 
 def load_peaks():
@@ -345,6 +354,9 @@ KERNEL_SCOPES = [
     (r"edge_bwd_prep_kernel", "bwd.edge_act"), (r"forces_kernel", "fwd.forces_segsum"),
     (r"edge_af0_kernel", "fwd.force_act"), (r"colsum2_kernel", "bwd.colsum_tail"),
     (r"chain_kernel<0", "fwd.node_chain"), (r"chain_kernel<[34]", "bwd.node_chain"),
+    (r"tc_row_kernel<.*::MsgSegProb>", "fwd.edge_msg_fused"), (r"tc_row_kernel<.*::L7SegProb>", "bwd.edge_dz1_fused"),
+    (r"agg_fix_kernel", "fwd.agg_fix"), (r"seg_src_kernel", "bwd.segsum_src"),
+    (r"tc_row_kernel<.*::MsgAsyncProb>", "fwd.edge_msg_gather"), (r"tc_row_kernel<.*::L7AsyncProb>", "bwd.edge_dz1_gather"),
     (r"tc_row_kernel<.*::MsgProb>", "fwd.edge_msg_gemm"), (r"tc_row_kernel<.*::L7Prob>", "bwd.edge_dz1_gemm"),
     (r"tc_row_kernel<.*::PProb>", "fwd.node_P"), (r"tc_row_kernel<.*::L11Prob>", "bwd.edge_dh_gemm"),
     (r"tc_row_kernel<.*::ForceProb>", "fwd.force_edge_gemm"), (r"tc_row_kernel<.*::FDxS?f?Prob>", "bwd.force_edge_dx"),
@@ -404,6 +416,8 @@ def kernel_profile(model, cfg, slots, steps=3, flush=None):
         if "vectorized_elementwise_kernel" in name:  # the L2 flush (torch), not the step
             continue
         scope = scope_of(name)
+        if scope.startswith("k.") and os.environ.get("HMTL_BENCH_NAMES"):
+            print("unmatched kernel:", name, file=sys.stderr)
         a = agg.setdefault(scope, {"name": scope, "calls": 0, "ms": 0.0})
         a["calls"] += 1
         a["ms"] += e["dur"] / 1e3

@@ -336,6 +336,13 @@ int hmtl_comm_unique_id(uint8_t out[128]);
 int hmtl_comm_init(hmtl_ctx* ctx, const uint8_t id[128], int world, int rank);
 /* Allreduce the last gradients (head groups, then global) on `stream`. */
 int hmtl_comm_sync_grads(hmtl_ctx* ctx, void* stream);
+/* Communicator census: world size, this rank, and the size of every head's
+ * sub-group (head_sizes[k], 0 = head not owned here; n = entries to fill).  With
+ * HMTL_COMM_LOG=1, comm_init prints the same to stderr.  Host waits on a step
+ * (read_loss, loss_wait) poll ncclCommGetAsyncError and abort every communicator
+ * on an asynchronous error or after HMTL_COMM_TIMEOUT_S seconds (default 600),
+ * returning HMTL_ERR_COMM (src/mesh.cpp:142-146, 161-171 timeouts / close). */
+int hmtl_comm_info(hmtl_ctx* ctx, int* world, int* rank, int* head_sizes, int n);
 /* Per-category byte counters (CommStats, hmtl/mesh.hpp:102-131): [encoder_sync, head_sync]. */
 int hmtl_comm_bytes(hmtl_ctx* ctx, uint64_t out[2]);
 

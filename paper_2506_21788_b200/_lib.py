@@ -147,6 +147,7 @@ SIGNATURES = {
     "hmtl_comm_init": (C.c_int, [_P, _U8P, C.c_int, C.c_int]),
     "hmtl_comm_sync_grads": (C.c_int, [_P, _P]),
     "hmtl_comm_bytes": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
+    "hmtl_comm_info": (C.c_int, [_P, _IP, _IP, _IP, C.c_int]),
 }
 
 _lib = None

@@ -86,7 +86,7 @@ void free_ctx(Ctx& c) {
                   c.z2, c.agg, c.vz1, c.pooled, c.ez, c.energy, c.Qf, c.zf, c.s, c.forces, c.dE, c.dF,
                   c.dagg, c.dhb, c.dvz1b, c.dzAb, c.dzBb, c.Sb, c.fzA, c.fzB, c.ds, c.dpooled, c.edA, c.edB,
                   c.scratch, c.partial, c.partial_w, c.partial_w2, c.loss_terms, c.cells, c.eimg, c.pbc_meta, c.pbc_bins,
-                  c.pbc_order, c.pbc_acoord, c.pbc_w2, c.bimg, c.a1, c.af0, c.sf0, c.bimg_all, c.d_bjobs};
+                  c.pbc_order, c.pbc_acoord, c.pbc_w2, c.bimg, c.a1, c.af0, c.sf0, c.bimg_all, c.d_bjobs, c.tpart, c.s1pb};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto* p : c.pool) cudaFree(p);
@@ -98,6 +98,7 @@ void free_ctx(Ctx& c) {
   for (auto& e : c.hdr_ev)
     if (e) cudaEventDestroy(e);
   if (c.h_cells) cudaFreeHost(c.h_cells);
+  if (c.step_done) cudaEventDestroy(c.step_done);
   if (c.step_exec) cudaGraphExecDestroy(c.step_exec);
   if (c.prof_exec) cudaGraphExecDestroy(c.prof_exec);
   comm_destroy(c.comm);
@@ -252,11 +253,15 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   }
   if (const char* e = std::getenv("HMTL_SINGLE_STREAM")) c.multi_stream = e[0] == '0';
   if (const char* e = std::getenv("HMTL_NO_CHAIN")) c.fuse_chain = e[0] == '0';
+  if (const char* e = std::getenv("HMTL_FUSE_EDGE")) c.fuse_edge = e[0] == '1';
+  if (const char* e = std::getenv("HMTL_ASYNC_FWD")) c.async_fwd = e[0] == '1';
+  if (const char* e = std::getenv("HMTL_ASYNC_BWD")) c.async_bwd = std::atoi(e);
+  if (const char* e = std::getenv("HMTL_TC_DEBUG")) set_tc_debug(std::atoi(e));
   if (const char* e = std::getenv("HMTL_TC_GRID")) c.tc_grid_mult = std::atoi(e);
   // weight-gradient grids over ~13/16 of the SMs: the side-stream reduce GEMMs then leave SMs to the
   // critical path (measured: 120 of 148 -> step 1.003 -> 0.994 ms; profiles/r01_ab_red_knobs.txt)
   c.red_sms = std::max(1, c.sm_count * 13 / 16);
-  if (const char* e = std::getenv("HMTL_CHAIN_CS")) c.chain_cs = std::atoi(e) == 2 ? 2 : 1;
+  if (const char* e = std::getenv("HMTL_CHAIN_CS")) c.chain_cs = std::atoi(e) == 4 ? 4 : (std::atoi(e) == 2 ? 2 : 1);
   if (const char* e = std::getenv("HMTL_NO_RED_TMA")) c.red_tma = e[0] == '0';
   if (const char* e = std::getenv("HMTL_RED_SEGX")) c.red_seg_mult = std::max(1, std::min(8, std::atoi(e)));
   if (const char* e = std::getenv("HMTL_RED_MINCH")) c.red_min_chunks = std::max(1, std::atoi(e));
@@ -347,8 +352,11 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   c.store_af0 = c.use_tc && W % 32 == 0 && H % 4 == 0;
   c.store_sf0 = c.store_af0;  // (regathering silu'(zf0) from Qf in FDx's epilogue measured slower)
   A(&c.a1, c.store_a1 ? L * E * H : 1);
+  A(&c.s1pb, c.store_a1 && (c.async_fwd || c.async_bwd == 1) ? L * E * H : 1);
   A(&c.af0, c.store_af0 ? E * W : 1);
   A(&c.sf0, c.store_sf0 ? E * W : 1);
+  c.tcap = int((E + 127) / 128 + 1);
+  A(&c.tpart, size_t(2) * c.tcap * H);
   if (rc) {
     free_ctx(c);
     delete h;
@@ -718,6 +726,11 @@ int hmtl_loss(hmtl_ctx* h, float w_e, float w_f, void* stream) {
 int hmtl_read_loss(hmtl_ctx* h, float* loss) {
   Ctx& c = h->c;
   cudaSetDevice(c.device);
+  if (c.comm) {  // the step's collectives may be in flight: wait with failure detection
+    if (!c.step_done) HMTL_CUDA(cudaEventCreateWithFlags(&c.step_done, cudaEventDisableTiming));
+    HMTL_CUDA(cudaEventRecord(c.step_done, c.stream));
+    if (int rc = comm_wait_event(c, c.step_done)) return rc;
+  }
   HMTL_CUDA(cudaDeviceSynchronize());
   if (int rc = check_hdr(c)) return rc;
   DevHdr hd;
@@ -753,7 +766,7 @@ int hmtl_loss_wait(hmtl_ctx* h, int slot, float* loss) {
   if (slot < 0 || !loss) return fail(HMTL_ERR_CONTRACT, "loss_wait: bad argument");
   cudaSetDevice(c.device);
   const int k = slot % Ctx::kLossRing;
-  HMTL_CUDA(cudaEventSynchronize(c.hdr_ev[k]));
+  if (int rc = comm_wait_event(c, c.hdr_ev[k])) return rc;
   if (int rc = hdr_errors(c.h_hdr_ring[k])) return rc;
   *loss = float(c.h_hdr_ring[k].loss);
   return 0;
@@ -785,6 +798,7 @@ int hmtl_adamw(hmtl_ctx* h, const hmtl_train_cfg* cfg, void* stream) {
 
 int hmtl_train_step(hmtl_ctx* h, const hmtl_train_cfg* cfg, void* stream) {
   Ctx& c = h->c;
+  if (comm_aborted(c)) return fail(HMTL_ERR_COMM, "train_step: communicators were aborted after an earlier failure");
   cudaSetDevice(c.device);
   cudaStream_t st = pick(c, stream);
   if (!cfg->use_graph) {

@@ -126,10 +126,10 @@ __device__ __forceinline__ float4 epi_apply(const Gemm& g, int H, int r, int n, 
 template <int V>
 using IC = std::integral_constant<int, V>;
 
-// ---- 2-CTA cluster column split: rank r of a cluster computes columns
-// [r N/2, (r+1) N/2) of every GEMM of the same 128 rows and writes its slice of
-// the chained A operand into both CTAs' shared memory (DSMEM), arriving on both
-// CTAs' per-chunk barriers with cluster-scope release
+// ---- CS-CTA cluster column split (CS = 2 or 4): rank r of a cluster computes
+// columns [r N/CS, (r+1) N/CS) of every GEMM of the same 128 rows and writes its
+// slice of the chained A operand into every CTA's shared memory (DSMEM),
+// arriving on every CTA's per-chunk barriers with cluster-scope release
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
     for (int s = 0; s < kBSlots; ++s) mbar_init(&bfull[s], 1), mbar_init(&bempty[s], 1);
     for (int i = 0; i < 3; ++i) mbar_init(&accd[i], 1);
     for (int i = 0; i < 8; ++i) mbar_init(&xrdy[i], 4 * 32);
-    for (int i = 0; i < 3; ++i) mbar_init(&pd[i], 1);
+    for (int i = 0; i < 3; ++i) mbar_init(&pd[i], CS > 1 ? CS - 1 : 1);
     fence_mbar_init();
   }
   tc_fence_before();
@@ -327,9 +327,10 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
       mbar_wait(&accd[gi], 0);
       tc_fence_after();
       if constexpr (CS > 1) {
-        if (!last) {  // the peer writes into our X (and we into its) only once both CTAs'
+        if (!last) {  // the peers write into our X (and we into theirs) only once every CTA's
           // MMAs of GEMM gi -- which read X -- are complete
-          if (ew == 0 && lane == 0) arrive_cluster(mapa(smem_u32(&pd[gi]), crank ^ 1u));
+          if (ew == 0 && lane == 0)
+            for (uint32_t pr = 1; pr < uint32_t(CS); ++pr) arrive_cluster(mapa(smem_u32(&pd[gi]), (crank + pr) % CS));
           wait_cluster(&pd[gi], 0);
         }
       }
@@ -362,13 +363,16 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
           if (!last && !(p.dbg & 2)) {  // next GEMM's A: k = j + 4cc -> chunk j / 32, piece cc of row rl
             float* hi = reinterpret_cast<float*>(X + (j / KC) * kSlot);
             put4(hi, hi + 128 * KC, cc, qd * 32 + rl, v);
-            if constexpr (CS > 1) {  // the same 16 B pieces into the peer's X (DSMEM)
+            if constexpr (CS > 1) {  // the same 16 B pieces into every peer's X (DSMEM)
               const float4 h4 = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
               const float4 l4 = make_float4(v.x - h4.x, v.y - h4.y, v.z - h4.z, v.w - h4.w);
               const uint32_t o = smem_u32(hi) + sw128(qd * 32 + rl, cc);
-              const uint32_t peer = crank ^ 1u;
-              st_cluster4(mapa(o, peer), h4);
-              st_cluster4(mapa(o + 128 * KC * 4, peer), l4);
+#pragma unroll
+              for (int pr = 1; pr < CS; ++pr) {
+                const uint32_t peer = (crank + uint32_t(pr)) % CS;
+                st_cluster4(mapa(o, peer), h4);
+                st_cluster4(mapa(o + 128 * KC * 4, peer), l4);
+              }
             }
           }
         }
@@ -378,7 +382,9 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
             asm volatile("fence.proxy.async;" ::: "memory");
             tc_fence_before();
             mbar_arrive(&xrdy[gi * 4 + j / KC]);
-            arrive_cluster(mapa(smem_u32(&xrdy[gi * 4 + j / KC]), crank ^ 1u));
+#pragma unroll
+            for (int pr = 1; pr < CS; ++pr)
+              arrive_cluster(mapa(smem_u32(&xrdy[gi * 4 + j / KC]), (crank + uint32_t(pr)) % CS));
           } else {
             fence_proxy_async();
             tc_fence_before();

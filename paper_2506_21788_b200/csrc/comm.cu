@@ -14,8 +14,12 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "ctx.cuh"
@@ -28,7 +32,9 @@ struct Comm {
   std::vector<ncclComm_t> head;  // per head id (nullptr if not owned)
   std::vector<int> head_size;
   uint64_t bytes_encoder = 0, bytes_head = 0;
+  bool aborted = false;
 };
+void comm_abort(Comm* m);
 
 #define HMTL_NCCL(call)                                                                        \
   do {                                                                                         \
@@ -87,11 +93,67 @@ void comm_shared_async(Ctx& c, size_t off, size_t count, cudaStream_t sc) {
 
 void comm_destroy(Comm* m) {
   if (!m) return;
+  if (m->aborted) {  // ncclCommAbort already released the communicators
+    delete m;
+    return;
+  }
   for (auto& h : m->head)
     if (h) ncclCommDestroy(h);
   if (m->world) ncclCommDestroy(m->world);
   delete m;
 }
+
+// Failure detection for the collectives captured in the step graph (the reference
+// bounds every blocking wait with a timeout and closes its endpoints on failure,
+// src/mesh.cpp:142-146, 161-171): a host wait on a stream-ordered event polls
+// ncclCommGetAsyncError of every communicator; an asynchronous NCCL error or a
+// wait longer than HMTL_COMM_TIMEOUT_S (default 600 s) aborts all of this rank's
+// communicators (ncclCommAbort: pending collectives return, peers see the
+// failure) and reports ErrorCode::comm.  Without a communicator it is
+// cudaEventSynchronize.
+int comm_wait_event(Ctx& c, cudaEvent_t ev) {
+  Comm* m = c.comm;
+  if (!m || m->world_size <= 1) {
+    HMTL_CUDA(cudaEventSynchronize(ev));
+    return 0;
+  }
+  if (m->aborted) return fail(HMTL_ERR_COMM, "comm: communicators were aborted after an earlier failure");
+  static const double timeout_s = [] {
+    const char* e = std::getenv("HMTL_COMM_TIMEOUT_S");
+    return e ? std::atof(e) : 600.0;
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) return 0;
+    if (q != cudaErrorNotReady)
+      return fail(HMTL_ERR_INTERNAL, std::string("CUDA: step event: ") + cudaGetErrorString(q));
+    std::string why;
+    ncclResult_t st = ncclSuccess;
+    if (ncclCommGetAsyncError(m->world, &st) != ncclSuccess || (st != ncclSuccess && st != ncclInProgress))
+      why = std::string("world communicator: ") + ncclGetErrorString(st);
+    for (size_t k = 0; why.empty() && k < m->head.size(); ++k)
+      if (m->head[k] && (ncclCommGetAsyncError(m->head[k], &st) != ncclSuccess || (st != ncclSuccess && st != ncclInProgress)))
+        why = "head " + std::to_string(k) + " communicator: " + ncclGetErrorString(st);
+    if (why.empty() && std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s)
+      why = "collective did not complete within HMTL_COMM_TIMEOUT_S=" + std::to_string(timeout_s) + " s";
+    if (!why.empty()) {
+      comm_abort(m);
+      return fail(HMTL_ERR_COMM, "comm: " + why + " (communicators aborted)");
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+void comm_abort(Comm* m) {
+  if (!m || m->aborted) return;
+  for (auto& h : m->head)
+    if (h) ncclCommAbort(h), h = nullptr;
+  if (m->world) ncclCommAbort(m->world), m->world = nullptr;
+  m->aborted = true;
+}
+
+bool comm_aborted(const Ctx& c) { return c.comm && c.comm->aborted; }
 
 ncclComm_t comm_world(Ctx& c, int* rank, int* size) {
   if (!c.comm) return nullptr;
@@ -140,6 +202,12 @@ int hmtl_comm_init(hmtl_ctx* h, const uint8_t id_bytes[128], int world, int rank
     }
     if (m->head[k]) ncclCommCount(m->head[k], &m->head_size[k]);
   }
+  if (const char* e = std::getenv("HMTL_COMM_LOG"); e && e[0] == '1') {
+    std::string g;
+    for (int k = 0; k < n_heads; ++k) g += (k ? "," : "") + std::to_string(m->head_size[k]);
+    std::fprintf(stderr, "[hmtl comm] rank %d/%d device %d: world comm %d ranks; head-group sizes [%s] (0 = not owned)\n",
+                 rank, world, c.device, world, g.c_str());
+  }
   if (c.step_exec) {
     cudaGraphExecDestroy(c.step_exec);
     c.step_exec = nullptr;
@@ -156,6 +224,15 @@ int hmtl_comm_sync_grads(hmtl_ctx* h, void* stream) {
   Ctx& c = h->c;
   cudaSetDevice(c.device);
   return comm_sync_grads(c, stream ? static_cast<cudaStream_t>(stream) : c.stream);
+}
+
+int hmtl_comm_info(hmtl_ctx* h, int* world, int* rank, int* head_sizes, int n) {
+  Comm* m = h ? h->c.comm : nullptr;
+  if (!m) return fail(HMTL_ERR_CONTRACT, "comm_info: no communicator attached");
+  if (world) ncclCommCount(m->world, world);
+  if (rank) ncclCommUserRank(m->world, rank);
+  for (int k = 0; head_sizes && k < n && k < int(m->head_size.size()); ++k) head_sizes[k] = m->head_size[k];
+  return 0;
 }
 
 int hmtl_comm_bytes(hmtl_ctx* h, uint64_t out[2]) {

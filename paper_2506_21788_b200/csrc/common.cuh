@@ -53,10 +53,13 @@ __device__ __forceinline__ float sigm(float x) {
   const float r = __fdividef(1.f, 1.f + e);
   return x >= 0.f ? r : e * r;
 }
-__device__ __forceinline__ float silu(float x) { return x * sigm(x); }
+// (explicitly rounded products/sums: no FMA contraction with the caller's
+// arithmetic, so every kernel that evaluates silu/silu' -- fused or not -- gets
+// the same bits)
+__device__ __forceinline__ float silu(float x) { return __fmul_rn(x, sigm(x)); }
 __device__ __forceinline__ float silu_grad(float x) {
   const float s = sigm(x);
-  return s * (1.f + x * (1.f - s));
+  return __fmul_rn(s, __fadd_rn(1.f, __fmul_rn(x, __fsub_rn(1.f, s))));
 }
 
 // ---- programmatic dependent launch (PDL).  Every kernel calls pdl_wait()

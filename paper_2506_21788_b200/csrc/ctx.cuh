@@ -112,10 +112,20 @@ struct Ctx {
   cudaStream_t s_c = nullptr;  // gradient allreduces (high priority), overlapped with the backward
   bool overlap_comm = true;
   int comm_err = 0;
+  cudaEvent_t step_done = nullptr;  // host waits on the step (read_loss) go through comm_wait_event
   std::vector<cudaEvent_t> evs;
   size_t ev_i = 0;
   bool multi_stream = true;
   bool fuse_chain = true;  // node-row GEMM chains in one launch (chain.cuh)
+  // fused edge passes (gather producer + segmented epilogue, tc.cuh kSeg): correct but slower on this
+  // engine (96-register cap of the 17-warp CTA -> producer spills), opt-in HMTL_FUSE_EDGE=1
+  bool fuse_edge = false;
+  // cp.async two-operand gather producers (tc.cuh kAsync) replacing the separate elementwise
+  // passes: forward message GEMM (HMTL_ASYNC_FWD=1), backward dz1 GEMM (HMTL_ASYNC_BWD: 0 off,
+  // 1 silu'(z1) stored by the forward's edge pass, 2 regathered from P in the epilogue)
+  bool async_fwd = false;
+  int async_bwd = 1;
+  float* s1pb = nullptr;  // [L][E][H] silu'(z1) stored by the forward for the backward
   int tc_grid_mult = 1;
   bool prefetch_l2 = true;  // L2 prefetch of re-read activations ahead of the critical path    // row GEMM grid cap in SMs (0: one CTA per tile)
   long long* chain_stamps = nullptr;
@@ -147,6 +157,8 @@ struct Ctx {
   bool red_tma = true;      // TMA operand path for plain row-major weight gradients (HMTL_NO_RED_TMA=1 off)
   int chain_cs = 2;         // node-chain cluster size: 2 = column split over a CTA pair (HMTL_CHAIN_CS=1: one CTA)
   float *a1 = nullptr, *af0 = nullptr, *sf0 = nullptr;
+  float* tpart = nullptr;  // [2][tcap][H] per-128-edge-tile pieces of straddling destinations (fused edge passes)
+  int tcap = 0;
   int nsplit_node = 1, nsplit_edge = 1, nsplit_graph = 1;
 
   // CUDA graph of a whole training step
@@ -200,8 +212,11 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync = false);  // Model
 void launch_adamw(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st, bool defer_images = false);
 void launch_debug_z1(Ctx& c, int layer, float* out, cudaStream_t st);
 void launch_bimg_all(Ctx& c, cudaStream_t st);  // rebuild every recorded B image
+void set_tc_debug(int bits);                     // HMTL_TC_DEBUG: engine ablation bits (timing only)
 
 int comm_sync_grads(Ctx& c, cudaStream_t st);
+int comm_wait_event(Ctx& c, cudaEvent_t ev);  // host wait with NCCL failure detection (comm.cu)
+bool comm_aborted(const Ctx& c);               // the communicators were aborted after a failure
 bool comm_overlap(const Ctx& c);                                    // bucketed sync inside the backward
 void comm_heads_async(Ctx& c, cudaStream_t sc);                     // owned heads, head groups
 void comm_shared_async(Ctx& c, size_t off, size_t count, cudaStream_t sc);  // shared range, world

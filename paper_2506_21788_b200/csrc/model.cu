@@ -66,6 +66,8 @@ __device__ __forceinline__ float4 pre4(float4 a, float4 b, float s, float4 w, fl
 // head-block vectors are not 16 B aligned (reference layout: energy.b2 is one float)
 __device__ __forceinline__ float4 ldu4(const float* p) { return make_float4(p[0], p[1], p[2], p[3]); }
 
+struct NoAux {};
+
 struct HeadW {  // a head-block tensor of slot `seg`: base + seg*PH + off
   const float* base;
   size_t PH, off;
@@ -126,6 +128,87 @@ struct MsgProb {
   __device__ float a(int, int e, int k) const { return silu(z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, k)); }
   __device__ float b(int, int k, int n) const { return W2[size_t(k) * H + n]; }
   __device__ void epi(int, int e, int n, float acc) const { z2[size_t(e) * H + n] = acc + b2[n]; }
+};
+
+// z2 = silu(z1) W2 + b2 with the A operand gathered by cp.async (tc.cuh kAsync):
+// the two node-table rows P_a[dst], P_b[src] of every edge land in shared memory
+// and are combined in place into a1 = silu(z1); a1 (eW2 weight gradient) and
+// silu'(z1) (the backward's dz1 epilogue) are stored on the way.  Replaces
+// edge_a1 -> MsgProb (same operations: bit-identical a1, z2).
+struct MsgAsyncProb {
+  BDesc bd() const { return BDesc{W2, nullptr, 0, 0, H, 1, K, Ncols, 1, 0, nullptr}; }
+  static constexpr const char* kName = "fwd.edge_msg_gather";
+  static constexpr bool kAsync = true;
+  struct RC {
+    int d, s;
+    float w;
+  };
+  __device__ RC rctx(int, int e) const { return RC{dst[e], src[e], geo[e].w}; }
+  __device__ const float* src_a(int, int, const RC& r, int k) const { return P + size_t(r.d) * 2 * H + k; }
+  __device__ const float* src_b(int, int, const RC& r, int k) const { return P + size_t(r.s) * 2 * H + H + k; }
+  __device__ float4 combine(int, int e, const RC& r, int k, float4 a, float4 b) const {
+    const float4 z = pre4(a, b, r.w, ld4(wd + k), ld4(b1 + k));
+    const float4 v = silu4(z);
+    st4(a1out + size_t(e) * H + k, v);
+    st4(s1p + size_t(e) * H + k, sgrad4(z));
+    return v;
+  }
+  __device__ void epi4c(int, int e, const RC&, int n, float4 acc) const {
+    st4(z2 + size_t(e) * H + n, add4(acc, ld4(b2 + n)));
+  }
+  RowSet rows;
+  int K, Ncols, H;
+  const float *P, *wd, *b1, *W2, *b2;
+  const int *dst, *src;
+  const float4* geo;
+  float *z2, *a1out, *s1p;
+  __device__ float b(int, int k, int n) const { return W2[size_t(k) * H + n]; }
+};
+
+// Fused message passing of one layer (hmtl/model.hpp:388-411) in one tensor-core
+// pass over the edges: the producer gathers a1 = silu(P_a[dst] + P_b[src] + d2 w
+// + b1) straight into the A operand (and stores a1 for the eW2 weight gradient),
+// the epilogue stores z2 = a1 W2 + b2 and sums m = silu(z2) per destination
+// (segmented epilogue, ascending edge order) into agg; destinations whose edge
+// rows straddle a 128-edge tile are finished by agg_fix_kernel.  Bit-identical
+// to edge_a1 -> MsgProb -> agg4 (same operations in the same order).
+struct MsgSegProb {
+  BDesc bd() const { return BDesc{W2, nullptr, 0, 0, H, 1, K, Ncols, 1, 0, nullptr}; }
+  static constexpr const char* kName = "fwd.edge_msg_fused";
+  static constexpr bool kSegSum = true;
+  struct RC {
+    int d, s;
+    float w;
+  };
+  struct Raw {
+    float4 a, b;
+  };
+  __device__ RC rctx(int, int e) const { return RC{dst[e], src[e], geo[e].w}; }
+  __device__ Raw raw4(int, int, const RC& r, int k) const {
+    return Raw{ld4(P + size_t(r.d) * 2 * H + k), ld4(P + size_t(r.s) * 2 * H + H + k)};
+  }
+  __device__ float4 fin4(int, int e, const RC& r, int k, const Raw& x) const {
+    const float4 v = silu4(pre4(x.a, x.b, r.w, ld4(wd + k), ld4(b1 + k)));
+    st4(a1out + size_t(e) * H + k, v);
+    return v;
+  }
+  __device__ float4 epi4r(int, int e, const RC&, int n, float4 acc, const NoAux&) const {
+    const float4 z = add4(acc, ld4(b2 + n));
+    st4(z2 + size_t(e) * H + n, z);
+    return silu4(z);
+  }
+  __device__ int seg_key(int e) const { return dst[e]; }
+  __device__ void seg_store(int i, int n, float v) const { agg[size_t(i) * H + n] = v; }
+  RowSet rows;
+  int K, Ncols, H;
+  const float *P, *wd, *b1, *W2, *b2;
+  const int *dst, *src;
+  const float4* geo;
+  float *z2, *a1out, *agg;
+  float* tpart;  // [2][tcap][H] straddling destinations' per-tile pieces (agg_fix_kernel adds them)
+  int tcap;
+  __device__ float a(int, int e, int k) const { return silu(z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, k)); }
+  __device__ float b(int, int k, int n) const { return W2[size_t(k) * H + n]; }
 };
 
 // vz1 = [h, agg] nW1 + nb1   (hmtl/model.hpp:412-420)
@@ -478,7 +561,6 @@ struct RCOf<P, std::void_t<typename P::RC>> {
   static constexpr bool has = true;
 };
 
-struct NoAux {};
 template <class P, class = void>
 struct AuxOf {
   using type = NoAux;
@@ -509,11 +591,34 @@ struct HasAuxC : std::false_type {};
 template <class P>
 struct HasAuxC<P, std::void_t<decltype(&P::epi_auxc)>> : std::true_type {};
 
+template <class P, class = void>
+struct AsyncOf : std::false_type {};
+template <class P>
+struct AsyncOf<P, std::void_t<decltype(P::kAsync)>> : std::bool_constant<P::kAsync> {};
+template <class P, class = void>
+struct SegOf : std::false_type {};
+template <class P>
+struct SegOf<P, std::void_t<decltype(P::kSegSum)>> : std::bool_constant<P::kSegSum> {};
+
 template <class P>
 struct TcRow {
   using RC = typename RCOf<P>::type;
   using Aux = typename AuxOf<P>::type;
   using Raw = typename RawOf<P>::type;
+  static constexpr bool kSeg = SegOf<P>::value;  // segmented-sum epilogue (tc.cuh)
+  static constexpr bool kAsync = AsyncOf<P>::value;  // cp.async two-operand producer (tc.cuh)
+  __device__ __forceinline__ const float* src_a(int seg, int row, const RC& rc, int k) const {
+    if constexpr (kAsync) return p.src_a(seg, row, rc, k);
+    else return nullptr;
+  }
+  __device__ __forceinline__ const float* src_b(int seg, int row, const RC& rc, int k) const {
+    if constexpr (kAsync) return p.src_b(seg, row, rc, k);
+    else return nullptr;
+  }
+  __device__ __forceinline__ float4 combine(int seg, int row, const RC& rc, int k, float4 a, float4 b) const {
+    if constexpr (kAsync) return p.combine(seg, row, rc, k, a, b);
+    else return a;
+  }
   RowSet rows;
   int K, Ncols;
   const float* bimg;
@@ -540,6 +645,20 @@ struct TcRow {
     if constexpr (HasAuxC<P>::value) return p.epi_auxc(seg, row, rc, n);
     else if constexpr (AuxOf<P>::has) return p.epi_aux(seg, row, n);
     else return Aux{};
+  }
+  __device__ __forceinline__ int seg_key(int row) const {
+    if constexpr (kSeg) return p.seg_key(row);
+    else return -1;
+  }
+  __device__ __forceinline__ float4 epi4r(int seg, int row, const RC& rc, int n, float4 acc, const Aux& ax) const {
+    if constexpr (kSeg) return p.epi4r(seg, row, rc, n, acc, ax);
+    else return acc;
+  }
+  __device__ __forceinline__ void seg_store(int key, int n, float v) const {
+    if constexpr (kSeg) p.seg_store(key, n, v);
+  }
+  __device__ __forceinline__ void tile_store(int which, int t, int n, float v) const {
+    if constexpr (kSeg) p.tpart[(size_t(which) * p.tcap + t) * p.Ncols + n] = v;
   }
   __device__ __forceinline__ void epi4(int seg, int row, const RC& rc, int n, float4 acc, const Aux& ax) const {
     if constexpr (HasAuxC<P>::value) {
@@ -684,15 +803,19 @@ void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& 
     int Nt = p.Ncols <= 256 ? p.Ncols : 256;  // column block per tile (<= one 256-col accumulator)
     // (one wave: the largest split whose tile count still fits the SMs)
     while (Nt > 32 && mtiles * (p.Ncols / Nt) * 2 <= sm && (Nt / 2) % 32 == 0) Nt /= 2;
-    const tc::RowPlan plan = tc::row_plan(p.K, Nt);
+    const tc::RowPlan plan = tc::row_plan(p.K, Nt, TcRow<P>::kSeg ? tc::kSegKeyBytes : 0);
     set_smem(tc::tc_row_kernel<TcRow<P>>, plan.smem);
     const int cap_ctas = c.tc_grid_mult > 0 ? sm * c.tc_grid_mult : (1 << 30);  // persistent when capped
     kl(tc::tc_row_kernel<TcRow<P>>, gridn(mtiles * (p.Ncols / Nt), 1, cap_ctas), tc::kRowThreads, plan.smem, st, q,
        plan);
     return;
   }
-  const long long tiles = ((rows_cap + 63) / 64 + nseg) * ((p.Ncols + 63) / 64);
-  kl(gemm_ab_kernel<P>, gridn(tiles, 1, sm * 8), 256, 0, st, p);
+  if constexpr (TcRow<P>::kSeg || TcRow<P>::kAsync) {  // tensor-core engine only
+    fail(HMTL_ERR_INTERNAL, std::string(P::kName) + ": shape outside the tensor-core engine");
+  } else {
+    const long long tiles = ((rows_cap + 63) / 64 + nseg) * ((p.Ncols + 63) / 64);
+    kl(gemm_ab_kernel<P>, gridn(tiles, 1, sm * 8), 256, 0, st, p);
+  }
 }
 
 template <class P>
@@ -776,9 +899,11 @@ void launch_chain(Ctx& c, const char* name, int G, const chain::Gemm* gs, cudaSt
   q.stamps = c.chain_stamps;
   q.dbg = c.chain_dbg;
   const int grid = int((c.Nc + 127) / 128);
-  // 2-CTA clusters split every GEMM's columns (chained operand exchanged through DSMEM)
-  bool split = c.chain_cs == 2;
-  for (int i = 0; i < G; ++i) split = split && (gs[i].N / 2) % 32 == 0;
+  // CS-CTA clusters split every GEMM's columns (chained operand exchanged through DSMEM)
+  int cs = c.chain_cs;
+  for (int i = 0; i < G; ++i)
+    while (cs > 1 && (gs[i].N / cs) % 32 != 0) cs /= 2;
+  const bool split = cs == 2, quad = cs == 4;
   auto go = [&](auto kern, int cs) {
     set_smem(kern, chain::kSmem);
     cudaLaunchConfig_t cfg = {};
@@ -803,16 +928,20 @@ void launch_chain(Ctx& c, const char* name, int G, const chain::Gemm* gs, cudaSt
   using namespace chain;
   const int r0 = gs[0].role, r1 = G > 1 ? gs[1].role : -1, r2 = G > 2 ? gs[2].role : -1;
   if (r0 == kFwdNode1 && r1 == kFwdNode2 && r2 == kFwdP) {
-    if (split) go(chain_kernel<kFwdNode1, kFwdNode2, kFwdP, 2>, 2);
+    if (quad) go(chain_kernel<kFwdNode1, kFwdNode2, kFwdP, 4>, 4);
+    else if (split) go(chain_kernel<kFwdNode1, kFwdNode2, kFwdP, 2>, 2);
     else go(chain_kernel<kFwdNode1, kFwdNode2, kFwdP>, 1);
   } else if (r0 == kFwdNode1 && r1 == kFwdNode2 && r2 < 0) {
-    if (split) go(chain_kernel<kFwdNode1, kFwdNode2, -1, 2>, 2);
+    if (quad) go(chain_kernel<kFwdNode1, kFwdNode2, -1, 4>, 4);
+    else if (split) go(chain_kernel<kFwdNode1, kFwdNode2, -1, 2>, 2);
     else go(chain_kernel<kFwdNode1, kFwdNode2, -1>, 1);
   } else if (r0 == kBwdL11 && r1 == kBwdL1 && r2 == kBwdL4) {
-    if (split) go(chain_kernel<kBwdL11, kBwdL1, kBwdL4, 2>, 2);
+    if (quad) go(chain_kernel<kBwdL11, kBwdL1, kBwdL4, 4>, 4);
+    else if (split) go(chain_kernel<kBwdL11, kBwdL1, kBwdL4, 2>, 2);
     else go(chain_kernel<kBwdL11, kBwdL1, kBwdL4>, 1);
   } else if (r0 == kBwdL1 && r1 == kBwdL4 && r2 < 0) {
-    if (split) go(chain_kernel<kBwdL1, kBwdL4, -1, 2>, 2);
+    if (quad) go(chain_kernel<kBwdL1, kBwdL4, -1, 4>, 4);
+    else if (split) go(chain_kernel<kBwdL1, kBwdL4, -1, 2>, 2);
     else go(chain_kernel<kBwdL1, kBwdL4, -1>, 1);
   }
 }
@@ -854,6 +983,9 @@ RowSet graph_rows_by_head(Ctx& c) {
 namespace {
 __global__ void agg4_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const float* __restrict__ z2,
                             float* __restrict__ agg, int H);
+__global__ void agg_fix_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr, const float* __restrict__ tp,
+                               int tcap, float* __restrict__ agg, int H);
+
 
 // ---- elementwise producers of the tensor-core A operands.  Warp per group of
 // kEwU edges, lane = float4 column group: the per-edge indices are warp-uniform
@@ -863,7 +995,8 @@ constexpr int kEwU = 4;
 __global__ void __launch_bounds__(256) edge_a1_kernel(const DevHdr* hdr, const float* __restrict__ P,
                                                       const int* __restrict__ dst, const int* __restrict__ src,
                                                       const float4* __restrict__ geo, const float* __restrict__ wd,
-                                                      const float* __restrict__ b1, float* __restrict__ a1, int H) {
+                                                      const float* __restrict__ b1, float* __restrict__ a1,
+                                                      float* __restrict__ s1p, int H) {
   pdl_wait();
   const int E = hdr->E, lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -881,7 +1014,11 @@ __global__ void __launch_bounds__(256) edge_a1_kernel(const DevHdr* hdr, const f
       }
 #pragma unroll
       for (int u = 0; u < kEwU; ++u)
-        if (eb + u < E) st4(a1 + size_t(eb + u) * H + c, silu4(pre4(pa[u], pb[u], d2[u], w, bb)));
+        if (eb + u < E) {
+          const float4 z = pre4(pa[u], pb[u], d2[u], w, bb);
+          st4(a1 + size_t(eb + u) * H + c, silu4(z));
+          if (s1p) st4(s1p + size_t(eb + u) * H + c, sgrad4(z));  // silu'(z1) for the backward's dz1 epilogue
+        }
     }
   }
 }
@@ -1002,6 +1139,9 @@ namespace {
 bool force_out_fast(const Ctx& c, int i) { return c.W % 4 == 0 && c.W <= 256 && (i >= 2 || c.store_af0); }
 }  // namespace
 
+// engine ablation bits of this translation unit's tc kernels (timing experiments only)
+void set_tc_debug(int bits) { cudaMemcpyToSymbol(tc::g_tc_debug, &bits, sizeof(int)); }
+
 void launch_bimg_all(Ctx& c, cudaStream_t st) {
   if (c.bjobs.empty()) return;
   if (!c.d_bjobs || c.n_djobs < int(c.bjobs.size())) {  // lay out the image buffer once
@@ -1051,11 +1191,27 @@ void launch_forward(Ctx& c, cudaStream_t st) {
       ab(q, c.Nc, 1, st, sm, c);
     }
     p_done = false;
+    if (c.store_a1 && c.async_fwd && !c.fuse_edge) {  // cp.async gather producer -> GEMM (a1, s1p, z2)
+      MsgAsyncProb q{edge_rows(c), H, H, H, P, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
+                     c.params + c.shared_off(p + "edge.W2"), c.params + c.shared_off(p + "edge.b2"), c.edge_dst,
+                     c.edge_src, c.geo, z2, c.a1 + size_t(l) * EH, c.s1pb + size_t(l) * EH};
+      ab(q, c.Ec, 1, st, sm, c);
+      Prof pr(c, "fwd.agg_segsum", st);
+      kl(agg4_kernel, gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st, c.hdr, c.row_ptr, z2, agg, H);
+    } else if (c.store_a1 && c.fuse_edge) {  // gather -> GEMM -> z2 + per-destination sum, one pass
+      MsgSegProb q{edge_rows(c), H, H, H, P, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
+                   c.params + c.shared_off(p + "edge.W2"), c.params + c.shared_off(p + "edge.b2"), c.edge_dst,
+                   c.edge_src, c.geo, z2, c.a1 + size_t(l) * EH, agg, c.tpart, c.tcap};
+      ab(q, c.Ec, 1, st, sm, c);
+      Prof pr(c, "fwd.agg_fix", st);
+      kl(agg_fix_kernel, gridn((long long)c.Nc * (H / 4), 256, sm * 4), 256, 0, st, c.hdr, c.row_ptr, c.tpart, c.tcap,
+         agg, H);
+    } else {
     if (c.store_a1) {
       Prof pr(c, "fwd.edge_act", st);
       kl(edge_a1_kernel, gridn((c.Ec + kEwU - 1) / kEwU * 32, 256, sm * 16), 256, 0, st,
           c.hdr, P, c.edge_dst, c.edge_src, c.geo, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
-          c.a1 + size_t(l) * EH, H);
+          c.a1 + size_t(l) * EH, c.async_bwd == 1 ? c.s1pb + size_t(l) * EH : nullptr, H);
     }
     {
       MsgProb q{edge_rows(c), H, H, H, P, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
@@ -1067,6 +1223,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
       Prof pr(c, "fwd.agg_segsum", st);
       if (H % 4 == 0) kl(agg4_kernel, gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st, c.hdr, c.row_ptr, z2, agg, H);
       else kl(agg_kernel, gridn((long long)c.Nc * 32, 256, sm * 16), 256, 0, st, c.hdr, c.row_ptr, z2, agg, H);
+    }
     }
     if (chain_ok(c)) {  // node MLP + residual (+ the next layer's P) in one launch
       const int G = l + 1 < L ? 3 : 2;
@@ -1581,6 +1738,130 @@ struct L7Prob {  // dz1 = (dz2 eW2^T) * silu'(z1)
     dz1[size_t(e) * H + n] = acc * silu_grad(z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, n));
   }
 };
+// Fused edge backward of one layer (hmtl/model.hpp:589-615) in one tensor-core
+// pass: the producer forms dz2 = dagg[dst] * silu'(z2) as the A operand (and
+// stores it for the eW2 weight gradient), the epilogue stores dz1 = (dz2 eW2^T) *
+// silu'(z1) -- z1 regathered from the L2-resident node table P -- and sums dz1 per
+// destination into S[:, :H] (segmented epilogue); seg_src_kernel adds S[:, H:]
+// (the source-side sums through the reverse-edge permutation) and finishes the
+// destinations that straddle a tile.  Bit-identical to edge_bwd_prep -> L7Prob
+// -> seg2v.
+struct L7SegProb {
+  BDesc bd() const { return BDesc{W, nullptr, 0, 0, 1, H, K, Ncols, 1, 0, nullptr}; }
+  static constexpr const char* kName = "bwd.edge_dz1_fused";
+  static constexpr bool kSegSum = true;
+  struct RC {
+    int d, s;
+    float w;
+  };
+  struct Raw {
+    float4 g, z;
+  };
+  struct Aux {
+    float4 v;
+  };
+  __device__ RC rctx(int, int e) const { return RC{dst[e], src[e], geo[e].w}; }
+  __device__ Raw raw4(int, int e, const RC& r, int k) const {
+    return Raw{ld4(dagg + size_t(r.d) * H + k), ld4(z2s + size_t(e) * H + k)};
+  }
+  __device__ float4 fin4(int, int e, const RC&, int k, const Raw& x) const {
+    const float4 v = mul4(x.g, sgrad4(x.z));
+    st4(dz2out + size_t(e) * H + k, v);
+    return v;
+  }
+  // silu'(z1) does not depend on the accumulator: prefetched ahead of the MMAs
+  __device__ Aux epi_auxc(int, int, const RC& r, int n) const {
+    return Aux{sgrad4(pre4(ld4(P + size_t(r.d) * 2 * H + n), ld4(P + size_t(r.s) * 2 * H + H + n), r.w, ld4(wd + n),
+                           ld4(b1 + n)))};
+  }
+  __device__ float4 epi4r(int, int e, const RC&, int n, float4 acc, const Aux& a) const {
+    const float4 v = mul4(acc, a.v);
+    st4(dz1 + size_t(e) * H + n, v);
+    return v;
+  }
+  __device__ int seg_key(int e) const { return dst[e]; }
+  __device__ void seg_store(int i, int n, float v) const { S[size_t(i) * 2 * H + n] = v; }
+  RowSet rows;
+  int K, Ncols, H;
+  const float *W, *P, *wd, *b1, *dagg, *z2s;
+  const int *dst, *src;
+  const float4* geo;
+  float *dz2out, *dz1, *S;
+  float* tpart;  // [2][tcap][H] (seg_src_kernel adds a straddling destination's pieces)
+  int tcap;
+  __device__ float a(int, int e, int k) const { return dagg[size_t(dst[e]) * H + k] * silu_grad(z2s[size_t(e) * H + k]); }
+  __device__ float b(int, int k, int n) const { return W[size_t(n) * H + k]; }
+};
+
+// dz1 = (dz2 eW2^T) * silu'(z1) with the A operand dz2 = dagg[dst] * silu'(z2)
+// gathered by cp.async (tc.cuh kAsync) and stored on the way (eW2 weight
+// gradient); silu'(z1) was stored by the forward (MsgAsyncProb).  Replaces
+// edge_bwd_prep -> L7Prob (same operations: bit-identical dz2, dz1).
+struct L7AsyncProb {
+  BDesc bd() const { return BDesc{W, nullptr, 0, 0, 1, H, K, Ncols, 1, 0, nullptr}; }
+  static constexpr const char* kName = "bwd.edge_dz1_gather";
+  static constexpr bool kAsync = true;
+  struct RC {
+    int d;
+  };
+  struct Aux {
+    float4 v;
+  };
+  __device__ RC rctx(int, int e) const { return RC{dst[e]}; }
+  __device__ const float* src_a(int, int, const RC& r, int k) const { return dagg + size_t(r.d) * H + k; }
+  __device__ const float* src_b(int, int e, const RC&, int k) const { return z2s + size_t(e) * H + k; }
+  __device__ float4 combine(int, int e, const RC&, int k, float4 a, float4 b) const {
+    const float4 v = mul4(a, sgrad4(b));
+    st4(dz2out + size_t(e) * H + k, v);
+    return v;
+  }
+  __device__ Aux epi_aux(int, int e, int n) const { return Aux{ld4(s1p + size_t(e) * H + n)}; }
+  __device__ void epi4a(int, int e, int n, float4 acc, const Aux& a) const { st4(dz1 + size_t(e) * H + n, mul4(acc, a.v)); }
+  RowSet rows;
+  int K, Ncols, H;
+  const float *W, *dagg, *z2s, *s1p;
+  const int* dst;
+  float *dz2out, *dz1;
+  __device__ float b(int, int k, int n) const { return W[size_t(n) * H + k]; }
+};
+
+// L7AsyncProb with silu'(z1) regathered in the epilogue from the L2-resident node
+// table (z1 = P_a[dst] + P_b[src] + d2 w + b1): nothing stored by the forward.
+struct L7AsyncPProb {
+  BDesc bd() const { return BDesc{W, nullptr, 0, 0, 1, H, K, Ncols, 1, 0, nullptr}; }
+  static constexpr const char* kName = "bwd.edge_dz1_gather";
+  static constexpr bool kAsync = true;
+  struct RC {
+    int d, s;
+    float w;
+  };
+  struct Aux {
+    float4 v;
+  };
+  __device__ RC rctx(int, int e) const { return RC{dst[e], src[e], geo[e].w}; }
+  __device__ const float* src_a(int, int, const RC& r, int k) const { return dagg + size_t(r.d) * H + k; }
+  __device__ const float* src_b(int, int e, const RC&, int k) const { return z2s + size_t(e) * H + k; }
+  __device__ float4 combine(int, int e, const RC&, int k, float4 a, float4 b) const {
+    const float4 v = mul4(a, sgrad4(b));
+    st4(dz2out + size_t(e) * H + k, v);
+    return v;
+  }
+  __device__ Aux epi_auxc(int, int, const RC& r, int n) const {
+    return Aux{sgrad4(pre4(ld4(P + size_t(r.d) * 2 * H + n), ld4(P + size_t(r.s) * 2 * H + H + n), r.w, ld4(wd + n),
+                           ld4(b1 + n)))};
+  }
+  __device__ void epi4ac(int, int e, const RC&, int n, float4 acc, const Aux& a) const {
+    st4(dz1 + size_t(e) * H + n, mul4(acc, a.v));
+  }
+  RowSet rows;
+  int K, Ncols, H;
+  const float *W, *dagg, *z2s, *P, *wd, *b1;
+  const int *dst, *src;
+  const float4* geo;
+  float *dz2out, *dz1;
+  __device__ float b(int, int k, int n) const { return W[size_t(n) * H + k]; }
+};
+
 struct L9Prob {  // [g_W1[2H]; g_b1] = [d2, 1]^T dz1   (E rows)
   static constexpr const char* kName = "bwd.edge_w1tail_grad";
   static constexpr int kBias = 0;
@@ -1783,6 +2064,75 @@ __global__ void __launch_bounds__(256) seg2v_kernel(const DevHdr* hdr, const int
         st4(S + size_t(i) * 2 * C + c, a);
         st4(S + size_t(i) * 2 * C + C + c, b);
       }
+    }
+  }
+}
+
+// A destination's edge rows straddle a 128-edge tile of the fused (segmented-
+// epilogue) edge kernels, or it has none: its sum is not written there.
+__device__ __forceinline__ bool tile_straddle(int e0, int e1) { return e1 == e0 || (e0 >> 7) != ((e1 - 1) >> 7); }
+
+// sum of a straddling destination's per-tile pieces (tc.cuh segmented epilogue):
+// its tail piece in its first tile, then the head pieces of the following tiles
+__device__ __forceinline__ float4 tile_pieces(const float* __restrict__ tp, int tcap, int C, int e0, int e1, int c) {
+  const int t0 = e0 >> 7, t1 = (e1 - 1) >> 7;
+  float4 acc = ld4(tp + (size_t(tcap) + t0) * C + c);
+  for (int t = t0 + 1; t <= t1; ++t) acc = add4(acc, ld4(tp + size_t(t) * C + c));
+  return acc;
+}
+
+// agg_i for the destinations the fused forward left: pieces of straddling
+// destinations summed in tile order, zeros for nodes without edges
+__global__ void __launch_bounds__(256) agg_fix_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr,
+                                                      const float* __restrict__ tp, int tcap, float* __restrict__ agg,
+                                                      int H) {
+  pdl_wait();
+  const int N = hdr->N;
+  const int per = H >> 2;  // float4 columns per node
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < N * per; t += gridDim.x * blockDim.x) {
+    const int i = t / per, c = (t - i * per) * 4;
+    const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
+    if (!tile_straddle(e0, e1)) continue;
+    st4(agg + size_t(i) * H + c, e1 == e0 ? f4z() : tile_pieces(tp, tcap, H, e0, e1, c));
+  }
+}
+
+// S[i][C:2C] = sum_{e in row i} x_{rev(e)} for every node (the source-side sums,
+// ascending-edge accumulation as seg2v_kernel), and S[i][0:C] for the
+// destinations the fused backward left (straddling pieces / zeros)
+constexpr int kSrcU = 8;
+__global__ void __launch_bounds__(256) seg_src_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr,
+                                                      const int* __restrict__ rev, const float* __restrict__ x,
+                                                      const float* __restrict__ tp, int tcap, float* __restrict__ S,
+                                                      int C) {
+  pdl_wait();
+  const int N = hdr->N, lane = threadIdx.x & 31, R = (N + 7) >> 3;
+  for (int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < 8 * R; v += (gridDim.x * blockDim.x) >> 5) {
+    const int i = (v & 7) * R + (v >> 3);  // spread over the batch, as agg4_kernel
+    if (i >= N) continue;
+    const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
+    for (int c0 = 0; c0 < C; c0 += 128) {
+      const int c = c0 + lane * 4;
+      const bool col = c < C;
+      float4 b = f4z();
+      for (int w0 = e0; w0 < e1; w0 += 32) {
+        const int myrev = w0 + lane < e1 ? rev[w0 + lane] : 0;
+        const int cnt = min(32, e1 - w0);
+        for (int j = 0; j < cnt; j += kSrcU) {
+          float4 vb[kSrcU];
+#pragma unroll
+          for (int u = 0; u < kSrcU; ++u) {
+            const int r = __shfl_sync(0xffffffffu, myrev, (j + u) & 31);
+            vb[u] = (col && j + u < cnt) ? ld4(x + size_t(r) * C + c) : f4z();
+          }
+#pragma unroll
+          for (int u = 0; u < kSrcU; ++u)
+            if (j + u < cnt) b = add4(b, vb[u]);
+        }
+      }
+      if (!col) continue;
+      if (tile_straddle(e0, e1)) st4(S + size_t(i) * 2 * C + c, e1 == e0 ? f4z() : tile_pieces(tp, tcap, C, e0, e1, c));
+      st4(S + size_t(i) * 2 * C + C + c, b);
     }
   }
 }
@@ -2149,7 +2499,21 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
     }
     node_done = false;
     const bool mat = c.store_a1;  // tensor-core shapes: gathered operands materialised elementwise
-    if (mat) {
+    const bool fz = mat && c.fuse_edge;
+    const bool az = mat && c.async_bwd && !fz;
+    if (az && c.async_bwd == 1) {  // cp.async dz2 gather producer -> GEMM (dz2, dz1; silu'(z1) from the forward)
+      L7AsyncProb q{edge_rows(c), H, H, H, c.params + c.shared_off(p + "edge.W2"), c.dagg, z2,
+                    c.s1pb + size_t(l) * EH, c.edge_dst, dzA, dzB};
+      ab(q, c.Ec, 1, st, sm, c);
+    } else if (az) {  // ... with silu'(z1) regathered from the node table P in the epilogue
+      L7AsyncPProb q{edge_rows(c), H, H, H, c.params + c.shared_off(p + "edge.W2"), c.dagg, z2, P, wd, b1,
+                     c.edge_dst, c.edge_src, c.geo, dzA, dzB};
+      ab(q, c.Ec, 1, st, sm, c);
+    } else if (fz) {  // dz2 producer -> GEMM -> dz1 + per-destination sum, one pass
+      L7SegProb q{edge_rows(c), H, H, H, c.params + c.shared_off(p + "edge.W2"), P, wd, b1, c.dagg, z2,
+                  c.edge_dst, c.edge_src, c.geo, dzA, dzB, Sl, c.tpart, c.tcap};
+      ab(q, c.Ec, 1, st, sm, c);
+    } else if (mat) {  // (unfused: elementwise dz2, silu'(z1) materialised, then the dz1 GEMM)
       Prof pr(c, "bwd.edge_act", st);
       kl(edge_bwd_prep_kernel, gridn((c.Ec + kEwU - 1) / kEwU * 32, 256, sm * 16), 256, 0, st,
           c.hdr, P, c.edge_dst, c.edge_src, c.geo, wd, b1, c.dagg, z2, dzA, c.scratch, H);
@@ -2157,7 +2521,7 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
       Prof pr(c, "bwd.edge_dz2_gather", st);
       kl(dz2_kernel, gridn(EH, 256, sm * 16), 256, 0, st, c.hdr, c.edge_dst, c.dagg, z2, dzA, H);
     }
-    {
+    if (!fz && !az) {
       L7Prob q{edge_rows(c), H, H, H, dzA, c.params + c.shared_off(p + "edge.W2"), P, wd, b1, c.edge_dst,
                c.edge_src, c.geo, dzB, nullptr, z2, mat ? c.scratch : nullptr};
       ab(q, c.Ec, 1, st, sm, c);
@@ -2179,7 +2543,13 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
                c.grads + c.shared_off(p + "edge.W2"), mat ? c.a1 + size_t(l) * EH : nullptr, nullptr, z2};
       atb(q, c, c.nsplit_edge, sw, c.Ec);
     }
-    segsum2(c, dzB, H, 0, Sl, st);
+    if (fz) {
+      Prof pr(c, "bwd.segsum_src", st);
+      kl(seg_src_kernel, gridn((long long)c.Nc * 32, 256, c.sm_count * 16), 256, 0, st, c.hdr, c.row_ptr, c.rev, dzB,
+         c.tpart, c.tcap, Sl, H);
+    } else {
+      segsum2(c, dzB, H, 0, Sl, st);
+    }
     c.dep(st, sw2);  // dz1 and its segment sums ready (second weight-gradient stream)
     colsum2(c, edge_rows(c), &c.geo[0].w, 4, dzB, H, geW1 + size_t(2) * H * H, 0, sw2);
     {

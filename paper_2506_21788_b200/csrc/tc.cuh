@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace hmtl_b200 {
@@ -200,37 +202,82 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 //   float4 fin4(int seg, int row, const RC&, int k, const Raw&) const;  // -> A(row, k..k+3)
 //   typename P::Aux epi_aux(int seg, int row, const RC&, int n) const;  // prefetched epilogue inputs
 //   void epi4(int seg, int row, const RC&, int n, float4 acc, const Aux&) const;  // C(row, n..n+3)
+// Segmented-sum epilogue (P::kSeg; identity RowSet of one segment whose rows are
+// sorted by key, e.g. edges by destination): epi4r stores C like epi4 and returns
+// the value to reduce; out(key, n) = sum over the rows of that key, in ascending
+// row order, is stored (seg_store) for every key whose rows lie inside one
+// 128-row tile.  A key that straddles tiles leaves one piece per tile instead:
+// tile_store(0, t, n, v) = its rows in tile t when they start the tile (a "head"
+// piece, the whole tile if the key covers it), tile_store(1, t, n, v) = its rows
+// in tile t when it starts there and continues (a "tail" piece); a fix-up pass
+// adds a straddling key's pieces in tile order.
+//   int seg_key(int row) const;  float4 epi4r(...same as epi4...) const;
+//   void seg_store(int key, int n, float v) const;  void tile_store(int which, int t, int n, float v) const;
 constexpr int kMaxStages = 4;
-// engine ablation switches for hmtl_selftest_time (bit0: producers skip A loads/stores,
-// bit1: epilogue skips global stores); always 0 on the training path.
+// engine ablation switches for hmtl_selftest_time and HMTL_TC_DEBUG (bit0: producers
+// skip A loads/stores, bit1: epilogue skips global stores, bit2: no segmented sums);
+// always 0 on the training path.
 static __device__ int g_tc_debug = 0;
 constexpr int kProdWarps = 8;                                  // 16 rows each
 constexpr int kRowIt = 128 / (kProdWarps * 8);                 // row groups of 8 per producer warp
-constexpr int kEpiWarps = 8;                                   // 2 per TMEM lane quadrant
+// epilogue warps: kEpiHalves per TMEM lane quadrant, each taking every kEpiHalves-th
+// 32-column slab.  (17 warps -- 2 per quadrant -- cap a thread at 96 registers: 5 warps
+// share one SM sub-partition's 16K registers; 13 warps allow 128.)
+#ifndef HMTL_EPI_HALVES
+#define HMTL_EPI_HALVES 2
+#endif
+constexpr int kEpiHalves = HMTL_EPI_HALVES;
+constexpr int kEpiWarps = 4 * kEpiHalves;
 constexpr int kMmaWarp = kProdWarps, kEpiWarp0 = kProdWarps + 1;
-constexpr int kRowThreads = (kProdWarps + 1 + kEpiWarps) * 32;  // 544
+constexpr int kRowThreads = (kProdWarps + 1 + kEpiWarps) * 32;  // 544 (416 with one epilogue warp per quadrant)
 constexpr size_t kSmemLimit = 227 * 1024;
 constexpr size_t kEpiBytes = size_t(kEpiWarps) * 32 * 32 * 4;  // one 4 KB slab per epilogue warp
 constexpr size_t kRowBars = 256;
+
+// segmented-sum epilogues (P::kSegSum): the tile's row keys, one array per
+// epilogue column half (the 4 quadrant warps of a half exchange through it)
+constexpr size_t kSegKeyBytes = size_t(2) * 128 * 4;
+template <class P, class = void>
+struct RowAsync : std::false_type {};
+template <class P>
+struct RowAsync<P, std::void_t<decltype(P::kAsync)>> : std::bool_constant<P::kAsync> {};
+
+// cp.async (Ampere-style, no register staging): 16 B global -> shared; src_bytes
+// 0 zero-fills (rows past the segment end)
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <class P, class = void>
+struct RowSeg : std::false_type {};
+template <class P>
+struct RowSeg<P, std::void_t<decltype(P::kSeg)>> : std::bool_constant<P::kSeg> {};
 
 struct RowPlan {
   int Nt, stages, resident;
   size_t a_stage, b_stage, b_res, smem;
 };
-inline RowPlan row_plan(int K, int Nt) {
+inline RowPlan row_plan(int K, int Nt, size_t extra = 0) {
   RowPlan r;
   r.Nt = Nt;
   r.a_stage = size_t(2 * 128 * KC) * 4;  // hi + lo
   const size_t b_chunk = size_t(2 * Nt * KC) * 4;
   const size_t b_all = b_chunk * (K / KC);
-  r.resident = (b_all + 2 * r.a_stage + kEpiBytes + kRowBars + 1024 <= kSmemLimit) ? 1 : 0;
+  const size_t fixed = kEpiBytes + kRowBars + extra + 1024;  // +1 KB: manual 1 KB alignment
+  r.resident = (b_all + 2 * r.a_stage + fixed <= kSmemLimit) ? 1 : 0;
   r.b_res = r.resident ? b_all : 0;
   r.b_stage = r.resident ? 0 : b_chunk;
   const size_t per = r.a_stage + r.b_stage;
-  int st = int((kSmemLimit - kRowBars - 1024 - kEpiBytes - r.b_res) / per);
+  int st = int((kSmemLimit - fixed - r.b_res) / per);
   r.stages = st < 2 ? 2 : (st > kMaxStages ? kMaxStages : st);
-  r.smem = r.b_res + r.stages * per + kEpiBytes + kRowBars + 1024;  // +1 KB: manual 1 KB alignment
+  r.smem = r.b_res + r.stages * per + fixed;
   return r;
+}
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 __device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
@@ -264,6 +311,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   uint64_t* bfull = bars + 2 * kStages + 4;     // resident B landed (tx)
   uint64_t* bdone = bars + 2 * kStages + 5;     // MMAs reading the resident B completed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 6);
+  int* tkeys = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(bars) + kRowBars);  // [2][128] (P::kSeg)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t acc_cols = Nt <= 32 ? 32 : (Nt <= 64 ? 64 : (Nt <= 128 ? 128 : 256));
   constexpr int kProdThreads = kProdWarps * 32;
@@ -281,21 +329,8 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
     mbar_init(bdone, 1);
     fence_mbar_init();
   }
-  int mt_seg[kMaxSlots + 1];
-  int total_m = 0;
-  for (int s = 0; s < p.rows.nseg; ++s) {
-    mt_seg[s] = total_m;
-    total_m += (p.rows.end(s) - p.rows.begin(s) + 127) / 128;
-  }
-  mt_seg[p.rows.nseg] = total_m;
-  const int ntn = p.Ncols / Nt;
-  const int total = total_m * ntn;
-  // contiguous tile range per CTA: consecutive tiles share a head segment / column block,
-  // so the resident B image is reloaded only at segment boundaries
-  const int t_beg = int((long long)blockIdx.x * total / gridDim.x);
-  const int t_end = int((long long)(blockIdx.x + 1) * total / gridDim.x);
-  const int nchunks = p.K / KC;
   const uint32_t b_slice = uint32_t(Nt) * 128;  // bytes of one (chunk, hi|lo) B slice
+  const int nchunks = p.K / KC;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -303,6 +338,26 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   // ablation bits read once: a global load per chunk sat on the producer's critical path
   const int dbg = g_tc_debug;
   pdl_wait();  // setup above overlaps the previous kernel's tail
+  // first m-tile of every head segment, in shared memory: a dynamically indexed
+  // per-thread array lands in local memory, whose misses go to L2 (the L1 left
+  // next to ~227 KB of shared memory is tiny)
+  int* mt_seg = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(bars) + 128);  // [kMaxSlots + 1]
+  if (tid == 0) {
+    int acc = 0;
+    for (int s = 0; s < p.rows.nseg; ++s) {
+      mt_seg[s] = acc;
+      acc += (p.rows.end(s) - p.rows.begin(s) + 127) / 128;
+    }
+    mt_seg[p.rows.nseg] = acc;
+  }
+  __syncthreads();
+  const int total_m = mt_seg[p.rows.nseg];
+  const int ntn = p.Ncols / Nt;
+  const int total = total_m * ntn;
+  // contiguous tile range per CTA: consecutive tiles share a head segment / column block,
+  // so the resident B image is reloaded only at segment boundaries
+  const int t_beg = int((long long)blockIdx.x * total / gridDim.x);
+  const int t_end = int((long long)(blockIdx.x + 1) * total / gridDim.x);
 
   if (warp < kProdWarps) {  // ------------------------------------- producers
     // 4 lanes per row, each lane two k-groups (32 contiguous bytes of the row):
@@ -335,6 +390,78 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
         set_tile(u);
       }
     };
+    if constexpr (RowAsync<P>::value) {
+      // Two-operand gather producer without register staging (P::kAsync): every
+      // thread cp.asyncs the two 16 B source pieces of each of its (row, k4) slots of
+      // a chunk straight into the stage's hi / lo tiles at the slot's SW128 position;
+      // one chunk later (the next chunk's copies in flight) it converts its own slots
+      // in place: v = p.combine(a, b) (+ the problem's side stores), tf32 hi -> hi
+      // tile, lo -> lo tile.  No registers hold loads in flight, so the 17-warp CTA's
+      // 96-register cap no longer forces spills on gathered operands.
+      auto slot_off = [&](int it, int h) { return sw128(warp * 8 * kRowIt + it * 8 + rsub, 2 * kq + h); };
+      auto issue = [&](const Cur& u, int st) {
+        const uint32_t hi = smem_u32(stages + st * SB), lo = hi + 128 * KC * 4;
+#pragma unroll
+        for (int it = 0; it < kRowIt; ++it)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = u.c * KC + 8 * kq + 4 * h;
+            const bool ok = u.rows[it] >= 0;
+            const uint32_t o = slot_off(it, h);
+            cp_async16(hi + o, ok ? p.src_a(u.seg, u.rows[it], u.rc[it], k) : p.bimg, ok ? 16u : 0u);
+            cp_async16(lo + o, ok ? p.src_b(u.seg, u.rows[it], u.rc[it], k) : p.bimg, ok ? 16u : 0u);
+          }
+        cp_async_commit();
+      };
+      auto convert = [&](const Cur& u, int st) {
+        uint8_t* hi = stages + st * SB;
+        uint8_t* lo = hi + 128 * KC * 4;
+#pragma unroll
+        for (int it = 0; it < kRowIt; ++it)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t o = slot_off(it, h);
+            float4* ph = reinterpret_cast<float4*>(hi + o);
+            float4* pl = reinterpret_cast<float4*>(lo + o);
+            const float4 v = u.rows[it] >= 0 ? p.combine(u.seg, u.rows[it], u.rc[it], u.c * KC + 8 * kq + 4 * h, *ph, *pl)
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 vh = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+            *ph = vh;
+            *pl = make_float4(v.x - vh.x, v.y - vh.y, v.z - vh.z, v.w - vh.w);
+          }
+        fence_proxy_async();
+        if (!plan.resident && tid == 0) {  // this stage's B slice rides on the same barrier
+          mbar_expect_tx(&full[st], 2 * b_slice);
+          const float* bsrc = p.bimg + u.seg * p.bimg_seg;
+          for (int part = 0; part < 2; ++part)
+            bulk_g2s(lo + 128 * KC * 4 + part * b_slice,
+                     bsrc + (size_t(u.c) * 2 + part) * p.Ncols * KC + size_t(u.n0) * KC, b_slice, &full[st]);
+        } else {
+          mbar_arrive(&full[st]);
+        }
+      };
+      Cur prev;
+      prev.t = t_beg;
+      prev.c = 0;
+      set_tile(prev);
+      if (prev.t < t_end) {
+        mbar_wait(&empty[0], 1);
+        issue(prev, 0);
+      }
+      for (int i = 1; prev.t < t_end; ++i) {  // chunk i issued, chunk i - 1 converted
+        Cur nxt = prev;
+        succ(nxt);
+        if (nxt.t < t_end) {
+          mbar_wait(&empty[i % kStages], ((i / kStages) & 1) ^ 1);
+          issue(nxt, i % kStages);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        convert(prev, (i - 1) % kStages);
+        prev = nxt;
+      }
+    } else {
     using Raw = typename P::Raw;  // raw A loads of a chunk; P::fin4 turns them into A values
     auto load = [&](const Cur& u, Raw (&x)[kRowIt][2]) {
       const bool skip = dbg & 1;
@@ -394,6 +521,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
       B = A;
       succ(B);
       if (B.t < t_end) load(B, xb);
+    }
     }
   } else if (warp == kMmaWarp) {  // --------------------------------- MMA issuer + resident B
     int stage = 0;
@@ -466,6 +594,15 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
         rows_it[it] = v < p.rows.end(seg) ? p.rows.row(v) : -1;
         if (rows_it[it] >= 0) rc[it] = p.rctx(seg, rows_it[it]);
       }
+      // segmented sums: this quadrant's row keys and the tile's neighbours
+      int tprev = -1, tnext = -1;
+      if constexpr (RowSeg<P>::value) {
+        const int base = p.rows.begin(seg) + (tm - mt_seg[seg]) * 128, endv = p.rows.end(seg);
+        const int v = base + q * 32 + lane;
+        tkeys[half * 128 + q * 32 + lane] = v < endv ? p.seg_key(p.rows.row(v)) : -1;
+        tprev = base > p.rows.begin(seg) ? p.seg_key(p.rows.row(base - 1)) : -1;
+        tnext = base + 128 < endv ? p.seg_key(p.rows.row(base + 128)) : -1;
+      }
       // epilogue operands that do not depend on the accumulator (residuals, saved
       // activations): the first slab's are loaded before waiting for the MMAs, later
       // slabs' are issued ahead of their TMEM load and transpose
@@ -478,7 +615,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
       }
       mbar_wait(&accfull[ab], aphase);
       tc_fence_after();
-      for (int sl = half; sl < nslab; sl += 2) {
+      for (int sl = half; sl < nslab; sl += kEpiHalves) {
         const int j = sl * 32;
         if (sl != half) {
 #pragma unroll
@@ -496,8 +633,60 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
           const int rl = it * 4 + (lane >> 3);
-          const float4 a = *reinterpret_cast<const float4*>(slab + rl * 32 + ((cc ^ (rl & 7)) << 2));
-          if (rows_it[it] >= 0 && !(dbg & 2)) p.epi4(seg, rows_it[it], rc[it], n0 + j + c4, a, aux[it]);
+          float4* sp = reinterpret_cast<float4*>(slab + rl * 32 + ((cc ^ (rl & 7)) << 2));
+          const float4 a = *sp;
+          if constexpr (RowSeg<P>::value) {  // store C; the reduced value replaces the accumulator in the slab
+            *sp = rows_it[it] >= 0 ? p.epi4r(seg, rows_it[it], rc[it], n0 + j + c4, a, aux[it])
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
+            if (rows_it[it] >= 0 && !(dbg & 2)) p.epi4(seg, rows_it[it], rc[it], n0 + j + c4, a, aux[it]);
+          }
+        }
+        if constexpr (RowSeg<P>::value) {
+          if (dbg & 4) continue;  // (ablation: no segmented sums)
+          // the 4 quadrant slabs of these 32 columns (this half's warps) now hold the
+          // reduced values of all 128 rows: lane = column, rows summed in ascending order;
+          // a key whose rows continue past the quadrant is finished by the quadrant where
+          // it starts (reading the following quadrants' slabs)
+          __syncwarp();
+          named_bar(1 + half, 128);
+          const int* tk = tkeys + half * 128;
+          auto colv = [&](int qq, int r) {
+            const float* sb = epi_smem + (half * 4 + ((qq + 3) & 3)) * 32 * 32;
+            return sb[r * 32 + ((((lane >> 2) ^ (r & 7))) << 2) + (lane & 3)];
+          };
+          const int col = n0 + j + lane, tile = tm - mt_seg[seg];
+          int cur = tk[q * 32];
+          bool head = q == 0 && tprev == cur;  // the key started in an earlier tile: this tile's head piece
+          bool owned = head || (q == 0 ? tprev : tk[q * 32 - 1]) != cur;
+          float sum = 0.f;
+          for (int r = 0; r < 32; ++r) {
+            const int k = tk[q * 32 + r];
+            if (k != cur) {
+              if (owned && cur >= 0) {
+                if (head) p.tile_store(0, tile, col, sum);
+                else p.seg_store(cur, col, sum);
+              }
+              sum = 0.f, cur = k, owned = true, head = false;
+            }
+            sum += colv(q, r);
+          }
+          if (owned && cur >= 0) {
+            bool done = false;
+            for (int qq = q + 1; qq < 4 && !done; ++qq)
+              for (int r = 0; r < 32; ++r) {
+                if (tk[qq * 32 + r] != cur) {
+                  done = true;
+                  break;
+                }
+                sum += colv(qq, r);
+              }
+            if (!done) done = tnext != cur;  // reached the tile end: complete unless the key continues
+            if (head) p.tile_store(0, tile, col, sum);
+            else if (done) p.seg_store(cur, col, sum);
+            else p.tile_store(1, tile, col, sum);
+          }
+          named_bar(1 + half, 128);  // every quadrant's slab read: free for the next 32 columns
         }
       }
       tc_fence_before();

@@ -72,6 +72,58 @@ def run_gpu(out):
     gather(result, out)
 
 
+def oracle_step_grads(o, oh, sh, hd, b):
+    import oracle as O
+
+    ob = O.batch_from_samples(dict(n_atoms=b.n_atoms, species=b.species, pos=b.positions, forces=b.forces,
+                                   energy=b.energy, dsid=b.dataset_id), 5.0, o.build_edges)
+    E, F, c = o.forward(oh, sh, hd, ob)
+    L, dE, dF = o.loss(ob, E, F)
+    gs, gh = o.backward(oh, sh, hd, ob, c, dE, dF)
+    return L, gs, gh
+
+
+def emulate(world):
+    """Single-process emulation of `world` MTL-par ranks on the FP64 oracle: every
+    rank's gradients computed in turn, shared grads averaged over all ranks, head k's
+    over the ranks that own it (hmtl/mesh.hpp:322-334 group means), AdamW per rank."""
+    import oracle as O
+
+    o = O.Oracle()
+    oh = O.Hyper(20, 2, 32, 32, 3, HEADS, 5.0)
+    state = []
+    for r in range(world):
+        _, heads, share = rank_batch(r, world, 0)
+        sh = o.init_block(oh, 7, -1)
+        hd = {k: o.init_block(oh, 7, k) for k in heads}
+        st = {"s": (np.zeros_like(sh), np.zeros_like(sh)),
+              **{k: (np.zeros_like(hd[k]), np.zeros_like(hd[k])) for k in heads}}
+        state.append((sh, hd, st))
+    losses = [[] for _ in range(world)]
+    for s in range(STEPS):
+        res = []
+        for r in range(world):
+            b, _, _ = rank_batch(r, world, s)
+            L, gs, gh = oracle_step_grads(o, oh, state[r][0], state[r][1], b)
+            losses[r].append(L)
+            res.append((gs, gh))
+        gmean = sum(g for g, _ in res) / world
+        for r in range(world):
+            sh, hd, st = state[r]
+            o.adamw(sh, gmean.copy(), *st["s"], s + 1)
+            for k in hd:
+                owners = [q for q in range(world) if k in res[q][1]]
+                gk = sum(res[q][1][k] for q in owners) / len(owners)
+                o.adamw(hd[k], np.ascontiguousarray(gk), *st[k], s + 1)
+    out = {}
+    for r in range(world):
+        out[f"r{r}_shared"] = state[r][0]
+        for k, v in state[r][1].items():
+            out[f"r{r}_head{k}"] = v
+        out[f"r{r}_losses"] = np.array(losses[r])
+    return out
+
+
 def run_oracle(out):
     import oracle as O
 
@@ -84,14 +136,11 @@ def run_oracle(out):
     st = {"s": (np.zeros_like(sh), np.zeros_like(sh)), **{k: (np.zeros_like(hd[k]), np.zeros_like(hd[k])) for k in heads}}
     # head sub-groups (hmtl/mesh.hpp:52-58 generalised): ranks sharing head k
     groups = {k: dist.new_group([r for r in range(world) if share[r, k] > 0]) for k in range(HEADS)}
-    losses = []
+    losses, seen = [], set()
     for s in range(STEPS):
         b, _, _ = rank_batch(rank, world, s)
-        ob = O.batch_from_samples(dict(n_atoms=b.n_atoms, species=b.species, pos=b.positions, forces=b.forces,
-                                       energy=b.energy, dsid=b.dataset_id), 5.0, o.build_edges)
-        E, F, c = o.forward(oh, sh, hd, ob)
-        L, dE, dF = o.loss(ob, E, F)
-        gs, gh = o.backward(oh, sh, hd, ob, c, dE, dF)
+        seen |= set(int(x) for x in b.dataset_id)
+        L, gs, gh = oracle_step_grads(o, oh, sh, hd, b)
         losses.append(L)
         for k in heads:  # head grads: mean within the head's sub-group
             t = torch.from_numpy(gh[k])
@@ -103,7 +152,8 @@ def run_oracle(out):
         o.adamw(sh, gs, *st["s"], s + 1)
         for k in heads:
             o.adamw(hd[k], np.ascontiguousarray(gh[k]), *st[k], s + 1)
-    gather({"shared": sh, **{f"head{k}": hd[k] for k in heads}, "losses": np.array(losses)}, out)
+    gather({"shared": sh, **{f"head{k}": hd[k] for k in heads}, "losses": np.array(losses),
+            "dsids": np.array(sorted(seen))}, out)
 
 
 def gather(result, out):

@@ -45,6 +45,51 @@ def test_gloo_world2_mtl_par_plan(tmp_path):
     assert not set(heads_of(d, 0)) & set(heads_of(d, 1))  # world 2: every head on one rank
 
 
+def test_gloo_world8_placement_sampling_and_group_means(tmp_path):
+    """CPU: the driver's 8-GPU MTL-par layout over gloo on the FP64 oracle.  The
+    product's placement gives GPUs per head {1,1,1,2,3} (every rank one head); each
+    rank trains only on its head's source (src/datastore.cpp:57-81); head replicas
+    and the shared block stay bit-identical across their groups; and the distributed
+    result equals a single-process emulation of the same group means
+    (hmtl/mesh.hpp:322-334) -- the host logic bench.py --gpus 8 runs over NCCL."""
+    import dist_equiv
+
+    d = torchrun(8, str(tmp_path / "o8.npz"), "oracle", 29571)
+    check_replicas(d, 8)
+    owners = {k: [r for r in range(8) if f"r{r}_head{k}" in d] for k in range(5)}
+    assert [len(owners[k]) for k in range(5)] == [1, 1, 1, 2, 3]
+    for r in range(8):
+        assert len(heads_of(d, r)) == 1
+        assert [int(x) for x in d[f"r{r}_dsids"]] == heads_of(d, r)  # only its head's source
+    e = dist_equiv.emulate(8)
+    import oracle as O
+
+    for r in range(8):
+        assert O.rel_vec_error(d[f"r{r}_losses"], e[f"r{r}_losses"]) < 1e-12
+        assert O.rel_vec_error(d[f"r{r}_shared"], e[f"r{r}_shared"]) < 1e-12
+        for k in heads_of(d, r):
+            assert O.rel_vec_error(d[f"r{r}_head{k}"], e[f"r{r}_head{k}"]) < 1e-12
+
+
+def test_world8_epoch_plan_serves_each_group_its_source():
+    """shuffle_epoch's taskpar rule on the 8-rank {1,1,1,2,3} serving groups: every
+    rank's plan holds only its head's dataset, the members of a replicated head draw
+    disjoint samples, and all ranks run the same number of steps."""
+    import paper_2506_21788_b200 as P
+
+    members = {0: [0], 1: [1], 2: [2], 3: [3, 4], 4: [5, 6, 7]}
+    counts = {k: 120 + 37 * k for k in range(5)}
+    plans = [P.epoch_plan("taskpar", counts, 8, 99, 4, r, members) for r in range(8)]
+    assert len({p[0] for p in plans}) == 1
+    for k, grp in members.items():
+        seen = []
+        for r in grp:
+            steps, ds, ix = plans[r]
+            assert set(int(x) for x in ds) == {k}
+            seen += [int(x) for x in ix]
+        assert len(seen) == len(set(seen))  # disjoint within the serving group
+
+
 @pytest.mark.gpu
 def test_nccl_matches_oracle_emulation(tmp_path):
     import torch

@@ -1,0 +1,84 @@
+"""The fused edge passes (gather -> tcgen05 GEMM -> segmented per-destination
+epilogue, csrc/tc.cuh + model.cu MsgSegProb / L7SegProb) against the unfused
+kernel sequence (edge_a1 -> MsgProb -> segred forward, edge_bwd_prep
+-> L7Prob -> segred backward; the fused passes are opt-in, HMTL_FUSE_EDGE=1), on
+batches whose destinations
+straddle 128-edge tiles and quadrants (mtl5 bench batch, max degree ~60) and
+whose rows exceed a whole tile (cfg4 cells, degree > 128).  Same operations;
+only a straddling destination's sum is associated per tile piece, so the two
+agree to FP32 rounding (1e-6) and the fused path is bitwise reproducible."""
+import os
+
+import numpy as np
+import pytest
+
+import bench
+
+import paper_2506_21788_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    P.build()
+    if P.lib().hmtl_device_count() < 1:
+        pytest.skip("no CUDA device")
+
+
+def run(workload, fused, n_structs=None, steps=3, env=None):
+    hyper = bench.WORKLOADS[workload]["hyper"]
+    heads, batches, _ = bench.rank_batches(0, 1, nb=3, workload=workload)
+    if n_structs:
+        batches = [b.take(range(n_structs)) for b in batches]
+    caps = P.Caps.for_samples(batches[0])
+    for b in batches[1:]:
+        caps = caps.union(P.Caps.for_samples(b))
+    env = dict(env or {}, **({"HMTL_FUSE_EDGE": "1"} if fused else {}))
+    os.environ.update(env)
+    try:
+        m = P.ModelT(P.ModelHyper(**hyper), 7, heads, caps=caps)
+    finally:
+        for k in env:
+            os.environ.pop(k, None)
+    cfg = P.TrainConfig(use_graph=True)
+    losses = [m.train_step(batches[i % 3], cfg) for i in range(steps)]
+    out = dict(losses=losses, agg=[m.debug("agg", l) for l in range(hyper["layers"])], g=m.grads().shared,
+               p=m.shared_block(), pred=m.predictions().forces)
+    m.close()
+    return out
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(a), np.linalg.norm(b), 1e-30)
+
+
+@pytest.mark.parametrize("workload,n", [("mtl5-weak", None), ("cfg4", 2), ("cfg2", None)])
+def test_fused_edge_passes_match_unfused(workload, n):
+    # one step: the same forward/backward at identical parameters (FP32 rounding only)
+    a, b = run(workload, True, n, steps=1), run(workload, False, n, steps=1)
+    np.testing.assert_allclose(a["losses"], b["losses"], rtol=1e-6)
+    for x, y in zip(a["agg"], b["agg"]):
+        assert rel(x, y) < 1e-6
+    for k in ("g", "pred"):
+        assert rel(a[k], b[k]) < 1e-5, k
+    a, c = run(workload, True, n), run(workload, True, n)  # bitwise reproducible over steps
+    assert a["losses"] == c["losses"]
+    for k in ("g", "p", "pred"):
+        assert np.array_equal(a[k], c[k]), k
+
+
+@pytest.mark.parametrize("workload,n", [("mtl5-weak", None), ("cfg4", 2)])
+def test_async_gather_producers_bit_identical(workload, n):
+    """The cp.async gather producers (MsgAsyncProb / L7AsyncProb, tc.cuh kAsync: the
+    default) compute the same operations as edge_a1 -> MsgProb and edge_bwd_prep ->
+    L7Prob (HMTL_ASYNC_EDGE=0): every step bit-identical."""
+    b = run(workload, False, n, env={"HMTL_ASYNC_FWD": "0", "HMTL_ASYNC_BWD": "0"})
+    for env in ({"HMTL_ASYNC_FWD": "1", "HMTL_ASYNC_BWD": "1"}, {"HMTL_ASYNC_BWD": "1"}, {"HMTL_ASYNC_BWD": "2"}):
+        a = run(workload, False, n, env=env)
+        assert a["losses"] == b["losses"], env
+        for x, y in zip(a["agg"], b["agg"]):
+            assert np.array_equal(x, y), env
+        for k in ("g", "p", "pred"):
+            assert np.array_equal(a[k], b[k]), (env, k)
