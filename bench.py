@@ -704,6 +704,12 @@ def run_b200(args, rank, world, local_rank, dist):
     rep = kernel_profile(model, cfg, slots, flush=do_flush)
     launches_per_step = nk.value  # kernel nodes of the step graph
     roof, roof_gs = roofline(rep, E.value, batches[0].N, batches[0].G, hyper, len(WORKLOADS[wl]["weights"]))
+    comm_census = None
+    if world > 1:  # communicator sizes as NCCL reports them (world, every head's sub-group)
+        cw, cr = C.c_int(), C.c_int()
+        hs = (C.c_int * hp.n_heads)()
+        check(lib().hmtl_comm_info(model.ctx, C.byref(cw), C.byref(cr), hs, hp.n_heads))
+        comm_census = {"world": cw.value, "head_group_sizes_rank0_view": list(hs)}
     model.close()
 
     # ---- reference CPU beside it (rank 0, N=1) + loss parity on the same batch sequence
@@ -736,9 +742,9 @@ def run_b200(args, rank, world, local_rank, dist):
     clocks = clk.summary(t_wall0, t_wall1)
     nb = {}
     if world > 1:
-        ub = (C.c_uint64 * 2)()
         nb = {"encoder_sync_bytes_per_step": model.shared_size() * 4,
-              "head_sync_bytes_per_step": int(sum(model.head_size() * 4 for k in heads if (share[:, k] > 0).sum() > 1))}
+              "head_sync_bytes_per_step": int(sum(model.head_size() * 4 for k in heads if (share[:, k] > 0).sum() > 1)),
+              "communicators": comm_census, "gpus_per_head": [int((share[:, k] > 0).sum()) for k in range(share.shape[1])]}
     if rank == 0:
         _, b1, _ = rank_batches(0, 1, nb=1, workload=wl) if world > 1 else (None, batches, None)
         E1 = E.value if world == 1 else None

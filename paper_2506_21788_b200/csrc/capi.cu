@@ -10,6 +10,11 @@
 
 using namespace hmtl_b200;
 
+hmtl_b200::LaunchPrio& hmtl_b200::launch_prio() {
+  static thread_local LaunchPrio p;
+  return p;
+}
+
 bool hmtl_b200::pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HMTL_NO_PDL");
@@ -39,6 +44,14 @@ int check_hdr(Ctx& c) {
   if (h.err & kErrNonFinite) return fail(HMTL_ERR_CONTRACT, "model: non-finite prediction");
   return 0;
 }
+
+}  // namespace
+bool hmtl_b200::sorted_by_slot(const Ctx& c, const uint8_t* ds, int G) {
+  for (int g = 1; g < G; ++g)
+    if (c.slot_of[ds[g]] < c.slot_of[ds[g - 1]]) return false;
+  return true;
+}
+namespace {
 
 // pack AtomisticSamples into the batch arena format (common.cuh: arena_layout)
 int pack(Ctx& c, const hmtl_samples* s, uint8_t* dst, size_t cap, size_t* bytes, bool pbc = false) {
@@ -76,6 +89,7 @@ int pack(Ctx& c, const hmtl_samples* s, uint8_t* dst, size_t cap, size_t* bytes,
   *bytes = al.total;
   c.host_G = s->G;
   c.host_N = s->N;
+  c.head_sorted = sorted_by_slot(c, s->dataset_id, s->G);
   return 0;
 }
 
@@ -136,6 +150,15 @@ void prof_harvest(Ctx& c) {
 
 int enqueue_step(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st) {
   c.ev_i = 0;
+  struct PrioScope {  // kernels on `st` high priority, side streams low, while this step is enqueued
+    explicit PrioScope(const Ctx& c, cudaStream_t st) {
+      LaunchPrio& p = launch_prio();
+      p.on = c.launch_prio;
+      p.hi_stream = st;
+      cudaDeviceGetStreamPriorityRange(&p.lo, &p.hi);
+    }
+    ~PrioScope() { launch_prio().on = false; }
+  } prio(c, st);
   if (!c.bimg_ready && c.use_tc) {  // record this step's B-image jobs (call order is fixed)
     c.bjobs.clear();
     c.bimg_recording = true;
@@ -255,6 +278,9 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   if (const char* e = std::getenv("HMTL_NO_CHAIN")) c.fuse_chain = e[0] == '0';
   if (const char* e = std::getenv("HMTL_FUSE_EDGE")) c.fuse_edge = e[0] == '1';
   if (const char* e = std::getenv("HMTL_ASYNC_FWD")) c.async_fwd = e[0] == '1';
+  if (const char* e = std::getenv("HMTL_FUSE_FORCE_OUT")) c.fuse_force_out = e[0] == '1';
+  if (const char* e = std::getenv("HMTL_LAUNCH_PRIO")) c.launch_prio = e[0] == '1';
+  if (const char* e = std::getenv("HMTL_BIMG_BLOCKS")) c.bimg_blocks = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("HMTL_ASYNC_BWD")) c.async_bwd = std::atoi(e);
   if (const char* e = std::getenv("HMTL_TC_DEBUG")) set_tc_debug(std::atoi(e));
   if (const char* e = std::getenv("HMTL_TC_GRID")) c.tc_grid_mult = std::atoi(e);
@@ -266,6 +292,8 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   if (const char* e = std::getenv("HMTL_RED_SEGX")) c.red_seg_mult = std::max(1, std::min(8, std::atoi(e)));
   if (const char* e = std::getenv("HMTL_RED_MINCH")) c.red_min_chunks = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("HMTL_RED_SMS")) c.red_sms = std::max(1, std::min(c.sm_count, std::atoi(e)));
+  c.row_sms = c.sm_count;
+  if (const char* e = std::getenv("HMTL_ROW_SMS")) c.row_sms = std::max(1, std::min(c.sm_count, std::atoi(e)));
   if (const char* e = std::getenv("HMTL_NO_PREFETCH")) c.prefetch_l2 = e[0] == '0';
   if (const char* e = std::getenv("HMTL_NO_COMM_OVERLAP")) c.overlap_comm = e[0] == '0';
   if (std::getenv("HMTL_CHAIN_STAMPS")) A(&c.chain_stamps, size_t(4096) * 32);
@@ -432,6 +460,8 @@ int hmtl_ctx_reserve(hmtl_ctx* h, const hmtl_caps* need) {
   std::swap(c.comm, n.comm);
   std::swap(c.pool, n.pool);
   std::swap(c.pool_bytes, n.pool_bytes);
+  std::swap(c.pool_sorted, n.pool_sorted);
+  c.head_sorted = n.head_sorted;
   std::swap(c.bimg_all, n.bimg_all);
   std::swap(c.bimg_all_cap, n.bimg_all_cap);
   std::swap(c.d_bjobs, n.d_bjobs);
@@ -619,6 +649,7 @@ int hmtl_pool_add(hmtl_ctx* h, const hmtl_samples* s, int* slot) {
   HMTL_CUDA(cudaMemcpy(d, tmp.data(), bytes, cudaMemcpyHostToDevice));
   c.pool.push_back(d);
   c.pool_bytes.push_back(bytes);
+  c.pool_sorted.push_back(c.head_sorted);
   if (slot) *slot = int(c.pool.size()) - 1;
   return 0;
 }
@@ -628,6 +659,7 @@ int hmtl_pool_bind(hmtl_ctx* h, int slot, void* stream) {
   if (slot < 0 || slot >= int(c.pool.size())) return fail(HMTL_ERR_CONTRACT, "pool_bind: bad slot");
   cudaSetDevice(c.device);
   HMTL_CUDA(cudaMemcpyAsync(c.arena, c.pool[slot], c.pool_bytes[slot], cudaMemcpyDeviceToDevice, pick(c, stream)));
+  c.head_sorted = c.pool_sorted[slot];
   return 0;
 }
 
@@ -806,7 +838,8 @@ int hmtl_train_step(hmtl_ctx* h, const hmtl_train_cfg* cfg, void* stream) {
     HMTL_CUDA(cudaGetLastError());
     return 0;
   }
-  if (c.step_exec && (std::memcmp(&c.graph_cfg, cfg, sizeof *cfg) != 0 || c.graph_pbc != c.pbc)) {
+  if (c.step_exec && (std::memcmp(&c.graph_cfg, cfg, sizeof *cfg) != 0 || c.graph_pbc != c.pbc ||
+                      c.graph_sorted != c.head_sorted)) {
     cudaGraphExecDestroy(c.step_exec);
     c.step_exec = nullptr;
   }
@@ -846,6 +879,7 @@ int hmtl_train_step(hmtl_ctx* h, const hmtl_train_cfg* cfg, void* stream) {
     if (e != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("graph capture: ") + cudaGetErrorString(e));
     c.step_kernels = count_kernel_nodes(g);
     c.graph_pbc = c.pbc;
+    c.graph_sorted = c.head_sorted;
     HMTL_CUDA(cudaGraphInstantiate(&c.step_exec, g, 0));
     cudaGraphDestroy(g);
     c.graph_cfg = *cfg;

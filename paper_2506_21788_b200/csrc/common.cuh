@@ -56,11 +56,19 @@ __device__ __forceinline__ float sigm(float x) {
 // (explicitly rounded products/sums: no FMA contraction with the caller's
 // arithmetic, so every kernel that evaluates silu/silu' -- fused or not -- gets
 // the same bits)
+#ifdef HMTL_SILU_FMA  // (A/B: contraction allowed)
+__device__ __forceinline__ float silu(float x) { return x * sigm(x); }
+__device__ __forceinline__ float silu_grad(float x) {
+  const float s = sigm(x);
+  return s * (1.f + x * (1.f - s));
+}
+#else
 __device__ __forceinline__ float silu(float x) { return __fmul_rn(x, sigm(x)); }
 __device__ __forceinline__ float silu_grad(float x) {
   const float s = sigm(x);
   return __fmul_rn(s, __fadd_rn(1.f, __fmul_rn(x, __fsub_rn(1.f, s))));
 }
+#endif
 
 // ---- programmatic dependent launch (PDL).  Every kernel calls pdl_wait()
 // before it touches memory an earlier kernel of the step wrote (a no-op when it
@@ -70,6 +78,18 @@ __device__ __forceinline__ float silu_grad(float x) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 bool pdl_enabled();
+// Launch priority of every kernel: the step's critical-path stream (set by the
+// context while it enqueues a step) gets the device's highest priority, side streams
+// the lowest, as a per-launch attribute so it survives CUDA-graph capture: when a
+// critical kernel and a weight-gradient kernel become ready together, the block
+// scheduler dispatches the critical kernel's CTAs first (both kinds need a whole
+// SM's shared memory, so whichever starts first holds the SMs).
+struct LaunchPrio {
+  cudaStream_t hi_stream = nullptr;
+  int hi = 0, lo = 0;
+  bool on = false;
+};
+LaunchPrio& launch_prio();
 template <typename... KArgs, typename... Args>
 inline void kl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
@@ -77,11 +97,19 @@ inline void kl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  const LaunchPrio& lp = launch_prio();
+  if (lp.on) {
+    at[n].id = cudaLaunchAttributePriority;
+    at[n++].val.priority = st == lp.hi_stream ? lp.hi : lp.lo;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = n;
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

@@ -83,6 +83,11 @@ struct Ctx {
   int *eimg = nullptr, *pbc_meta = nullptr, *pbc_bins = nullptr, *pbc_order = nullptr, *pbc_acoord = nullptr,
       *pbc_w2 = nullptr;
   bool pbc = false, graph_pbc = false;
+  // graphs of the bound batch grouped by owned head in ascending slot order (as a rank's
+  // batch of its heads' sources is): the head-sorted node/edge/graph orders are then the
+  // identity, so head-segmented row sets need no permutation (and can use TMA operands)
+  bool head_sorted = false, graph_sorted = false;
+  std::vector<char> pool_sorted;
   int *gslot = nullptr, *gperm = nullptr, *gnode_base = nullptr, *gedge_base = nullptr;
   int *node_perm = nullptr, *edge_perm = nullptr;
 
@@ -124,6 +129,8 @@ struct Ctx {
   // passes: forward message GEMM (HMTL_ASYNC_FWD=1), backward dz1 GEMM (HMTL_ASYNC_BWD: 0 off,
   // 1 silu'(z1) stored by the forward's edge pass, 2 regathered from P in the epilogue)
   bool async_fwd = false;
+  bool fuse_force_out = true;
+  bool launch_prio = false;  // per-launch priority attribute, critical path high (HMTL_LAUNCH_PRIO=1; measured no gain)  // force output layer's dz formed in the dx GEMM producer (HMTL_FUSE_FORCE_OUT=0: off)
   int async_bwd = 1;
   float* s1pb = nullptr;  // [L][E][H] silu'(z1) stored by the forward for the backward
   int tc_grid_mult = 1;
@@ -146,12 +153,14 @@ struct Ctx {
   BDesc* d_bjobs = nullptr;
   int n_djobs = 0;
   int bimg_rows = 1;  // max (segments x K) over the recorded images: bimg_all grid.x
+  int bimg_blocks = 1 << 20;  // CTA cap per image of the batched rebuild (HMTL_BIMG_BLOCKS; throttling it measured slower)
   bool store_a1 = false;  // forward producer materialises a1 = silu(z1) [L][E][H]
   bool store_af0 = false; // ... and silu(zf0) [E][W]
   // silu'(zf0) [E][W] too only when the force output layer's backward needs it
   // (head_depth 2); deeper heads regather it from the L2-resident Qf table
   bool store_sf0 = false;
   int red_sms = 0;          // SMs a weight-gradient (tc_red) launch spreads over (HMTL_RED_SMS; default 13/16 of them)
+  int row_sms = 148;        // persistent row-GEMM grid (HMTL_ROW_SMS; default every SM)
   int red_seg_mult = 1;     // CTA multiplier for head-segmented weight gradients (HMTL_RED_SEGX)
   int red_min_chunks = 4;   // >= this many 32-row chunks per weight-gradient CTA (HMTL_RED_MINCH)
   bool red_tma = true;      // TMA operand path for plain row-major weight gradients (HMTL_NO_RED_TMA=1 off)
@@ -202,6 +211,7 @@ struct Ctx {
 };
 
 // launchers (stream-ordered; sizes come from the device header)
+bool sorted_by_slot(const Ctx& c, const uint8_t* ds, int G);  // graphs grouped by ascending owned slot
 void launch_prep(Ctx& c, cudaStream_t st);      // arena -> node/graph tables, routing
 void launch_nbr(Ctx& c, cudaStream_t st);       // neighbour list, CSR, rev, edge offsets
 void launch_nbr_pbc(Ctx& c, cudaStream_t st);   // ... with periodic images (cell list)

@@ -592,6 +592,10 @@ template <class P>
 struct HasAuxC<P, std::void_t<decltype(&P::epi_auxc)>> : std::true_type {};
 
 template <class P, class = void>
+struct TcOnly : std::false_type {};  // problems without a SIMT fallback (P::kTcOnly)
+template <class P>
+struct TcOnly<P, std::void_t<decltype(P::kTcOnly)>> : std::bool_constant<P::kTcOnly> {};
+template <class P, class = void>
 struct AsyncOf : std::false_type {};
 template <class P>
 struct AsyncOf<P, std::void_t<decltype(P::kAsync)>> : std::bool_constant<P::kAsync> {};
@@ -805,12 +809,12 @@ void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& 
     while (Nt > 32 && mtiles * (p.Ncols / Nt) * 2 <= sm && (Nt / 2) % 32 == 0) Nt /= 2;
     const tc::RowPlan plan = tc::row_plan(p.K, Nt, TcRow<P>::kSeg ? tc::kSegKeyBytes : 0);
     set_smem(tc::tc_row_kernel<TcRow<P>>, plan.smem);
-    const int cap_ctas = c.tc_grid_mult > 0 ? sm * c.tc_grid_mult : (1 << 30);  // persistent when capped
+    const int cap_ctas = c.tc_grid_mult > 0 ? c.row_sms * c.tc_grid_mult : (1 << 30);  // persistent when capped
     kl(tc::tc_row_kernel<TcRow<P>>, gridn(mtiles * (p.Ncols / Nt), 1, cap_ctas), tc::kRowThreads, plan.smem, st, q,
        plan);
     return;
   }
-  if constexpr (TcRow<P>::kSeg || TcRow<P>::kAsync) {  // tensor-core engine only
+  if constexpr (TcRow<P>::kSeg || TcRow<P>::kAsync || TcOnly<P>::value) {  // tensor-core engine only
     fail(HMTL_ERR_INTERNAL, std::string(P::kName) + ": shape outside the tensor-core engine");
   } else {
     const long long tiles = ((rows_cap + 63) / 64 + nseg) * ((p.Ncols + 63) / 64);
@@ -911,11 +915,15 @@ void launch_chain(Ctx& c, const char* name, int G, const chain::Gemm* gs, cudaSt
     cfg.blockDim = dim3(chain::kThreads);
     cfg.dynamicSmemBytes = chain::kSmem;
     cfg.stream = st;
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[3];
     int n = 0;
     if (pdl_enabled()) {
       at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       at[n++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    if (launch_prio().on) {  // (as kl: critical-path kernels dispatch first)
+      at[n].id = cudaLaunchAttributePriority;
+      at[n++].val.priority = st == launch_prio().hi_stream ? launch_prio().hi : launch_prio().lo;
     }
     if (cs > 1) {
       at[n].id = cudaLaunchAttributeClusterDimension;
@@ -956,23 +964,24 @@ RowSet edge_rows(Ctx& c) {
   r.count = &c.hdr->E;
   return r;
 }
+// (head-sorted batches: the head-sorted orders are the identity -- no permutation)
 RowSet node_rows_by_head(Ctx& c) {
   RowSet r;
-  r.perm = c.node_perm;
+  r.perm = c.head_sorted ? nullptr : c.node_perm;
   r.seg_off = c.hdr->seg_node;
   r.nseg = c.S;
   return r;
 }
 RowSet edge_rows_by_head(Ctx& c) {
   RowSet r;
-  r.perm = c.edge_perm;
+  r.perm = c.head_sorted ? nullptr : c.edge_perm;
   r.seg_off = c.hdr->seg_edge;
   r.nseg = c.S;
   return r;
 }
 RowSet graph_rows_by_head(Ctx& c) {
   RowSet r;
-  r.perm = c.gperm;
+  r.perm = c.head_sorted ? nullptr : c.gperm;
   r.seg_off = c.hdr->seg_graph;
   r.nseg = c.S;
   return r;
@@ -1163,7 +1172,9 @@ void launch_bimg_all(Ctx& c, cudaStream_t st) {
     for (auto& j : c.bjobs) c.bimg_rows = std::max(c.bimg_rows, j.K * j.N * j.nseg);  // elements
   }
   Prof pr(c, "bimg_all", st);
-  kl(bimg_all_kernel, dim3((c.bimg_rows + 255) / 256, c.n_djobs), 256, 0, st, c.d_bjobs);
+  // a few CTAs per image (grid-stride): the rebuild overlaps the batch preparation and
+  // neighbour list without taking every SM from those small critical-path kernels
+  kl(bimg_all_kernel, dim3(std::min((c.bimg_rows + 255) / 256, c.bimg_blocks), c.n_djobs), 256, 0, st, c.d_bjobs);
   c.bimg_ready = true;
   c.bimg_recording = false;
 }
@@ -1444,6 +1455,10 @@ struct FGradProb {  // force MLP layer i >= 1 weight+bias (edge rows per head)
   HeadW Wd, B0;
   HeadG G;
   const float* af0s;  // silu(zf0) materialised by the forward producer (nullable)
+  // TMA operands when the head-segmented rows are contiguous (head-sorted batch): X = silu(zf0)
+  void tma(TmaOps& o) const {
+    if (layer == 1 && af0s) o.x = af0s, o.ldx = W, o.y = dz, o.ldy = ldz;
+  }
   __device__ float a(int seg, int e, int k) const {
     if (k == K - 1) return 1.f;
     if (layer == 1) return silu(zf0_of(Qf, W, dst[e], src[e], dist[e], Wd.at(seg), B0.at(seg), k));
@@ -1475,6 +1490,42 @@ struct FDxSfProb {  // dz_0 = (dz_1 W_1^T) * sf0
   __device__ float a(int, int e, int k) const { return dz[size_t(e) * ldz + k]; }
   __device__ float b(int seg, int k, int n) const { return Wt.at(seg)[size_t(n) * K + k]; }
   __device__ void epi(int, int e, int n, float acc) const { out[size_t(e) * W + n] = acc * sf0[size_t(e) * W + n]; }
+};
+// FDxSfProb with its A operand dz_1 = ds_e w_2 * silu'(zf1_e) -- the width-1 output
+// layer's backward (mlp_backward_, hmtl/model.hpp:308-336) -- formed by the producer
+// (and stored on the way for the W_1 weight gradient): the output layer's elementwise
+// pass leaves the critical path (its W_2/b_2 column sums run on a side stream).
+struct FDxDsProb {
+  BDesc bd() const { return BDesc{Wt.base + Wt.off, nullptr, 0, 0, 1, K, K, Ncols, rows.nseg, (long long)Wt.PH, nullptr}; }
+  static constexpr const char* kName = "bwd.force_edge_dx";
+  static constexpr bool kTcOnly = true;
+  struct RC {
+    float g;
+  };
+  using Raw = float4;
+  struct Aux {
+    float4 v;
+  };
+  __device__ RC rctx(int, int e) const { return RC{ds[e]}; }
+  __device__ Raw raw4(int, int e, const RC&, int k) const { return ld4(zf1 + size_t(e) * W + k); }
+  __device__ float4 fin4(int seg, int e, const RC& r, int k, const Raw& z) const {
+    const float4 w = ldu4(W2.at(seg) + k);
+    const float4 gw = make_float4(r.g * w.x, r.g * w.y, r.g * w.z, r.g * w.w);
+    const float4 v = mul4(gw, sgrad4(z));  // force_out_bwd_kernel's dz, same operations
+    st4(dz1out + size_t(e) * W + k, v);
+    return v;
+  }
+  __device__ Aux epi_aux(int, int e, int n) const { return Aux{ld4(sf0 + size_t(e) * W + n)}; }
+  __device__ void epi4a(int, int e, int n, float4 acc, const Aux& a) const {
+    st4(out + size_t(e) * W + n, mul4(acc, a.v));
+  }
+  RowSet rows;
+  int K, Ncols, W;
+  const float *zf1, *ds;
+  HeadW W2, Wt;
+  float *dz1out, *out;
+  const float* sf0;
+  __device__ float b(int seg, int k, int n) const { return Wt.at(seg)[size_t(n) * K + k]; }
 };
 struct FDxProb {  // dz_{i-1} = (dz_i W_i^T) * silu'(z_{i-1})
   BDesc bd() const { return BDesc{Wt.base + Wt.off, nullptr, 0, 0, 1, K, K, Ncols, rows.nseg, (long long)Wt.PH, nullptr}; }
@@ -2241,7 +2292,7 @@ __global__ void __launch_bounds__(256) force_out_bwd_kernel(RowSet rows, const f
         const float4 sg = act ? silu4(z[j][u]) : z[j][u];
         const float4 sd = act ? sgrad4(z[j][u]) : zd[j][u];
         const float4 gw = make_float4(g[j] * wr[u].x, g[j] * wr[u].y, g[j] * wr[u].z, g[j] * wr[u].w);
-        st4(dzp + size_t(e[j]) * W + c, mul4(gw, sd));
+        if (dzp) st4(dzp + size_t(e[j]) * W + c, mul4(gw, sd));  // (null: the next GEMM's producer forms it)
         acc[u] = make_float4(acc[u].x + g[j] * sg.x, acc[u].y + g[j] * sg.y, acc[u].z + g[j] * sg.z,
                              acc[u].w + g[j] * sg.w);
       }
@@ -2408,9 +2459,37 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
     const float* dz = c.ds;
     int ldz = 1;
     float* bufs[2] = {c.fzA, c.fzB};
+    // (head_depth 3: the output layer's dz is formed inside the next dx GEMM's producer)
+    const bool fuse_out = D == 3 && force_out_fast(c, 2) && c.store_sf0 && c.use_tc && c.fuse_force_out;
     for (int i = D - 1; i >= 1; --i) {
       const int out = i == D - 1 ? 1 : W;
       float* nxt = bufs[i & 1];
+      if (i == D - 1 && fuse_out) {  // W_2 / b_2 gradients only, off the critical path
+        c.dep(st, sw2);
+        Prof pr(c, "bwd.force_out", sw2);
+        const int cap = int((c.Ec + kFoRows - 1) / kFoRows);
+        const RowSet rows = edge_rows_by_head(c);
+        kl(force_out_bwd_kernel, dim3(cap, rows.nseg), 256, 0, sw2, rows, c.zf, c.sf0, 1, c.ds, c.head_params(), c.PH,
+           c.head_off("force.W2"), static_cast<float*>(nullptr), c.part(sw2), cap, W);
+        kl(split_reduce_kernel<ChunkStore>, dim3((W + 1 + 31) / 32, rows.nseg), 256, 0, sw2, c.part(sw2),
+           size_t(cap) * (W + 1), size_t(W + 1), W + 1,
+           ChunkStore{rows, kFoRows, c.head_grads() + c.head_off("force.W2"), c.PH});
+        continue;
+      }
+      if (i == 1 && fuse_out) {  // dz_1 (stored) and dz_0 in one GEMM, then W_1's gradient
+        const HeadW Wi{c.head_params(), c.PH, c.head_off("force.W1")};
+        FDxDsProb dq{edge_rows_by_head(c), W, W, W, c.zf, c.ds, HeadW{c.head_params(), c.PH, c.head_off("force.W2")},
+                     Wi, bufs[0], nxt, c.sf0};
+        ab(dq, c.Ec, c.S, st, sm, c);
+        c.dep(st, sw);
+        FGradProb gq{edge_rows_by_head(c), W + 1, W, H, W, 1, c.Ec, c.Qf, c.zf, c.dist, bufs[0], W, c.edge_dst,
+                     c.edge_src, Wd, B0, HeadG{c.head_grads(), c.PH, c.head_off("force.W1")},
+                     c.store_af0 ? c.af0 : nullptr};
+        atb(gq, c, c.nsplit_edge, sw, c.Ec);
+        dz = nxt;
+        ldz = W;
+        continue;
+      }
       if (i == D - 1 && force_out_fast(c, i)) {
         Prof pr(c, "bwd.force_out", st);
         const int cap = int((c.Ec + kFoRows - 1) / kFoRows);

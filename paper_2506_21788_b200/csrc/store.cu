@@ -505,6 +505,7 @@ int hmtl_store_bind(hmtl_ctx* h, hmtl_store* st, const uint8_t* ds, const uint64
   HMTL_CUDA(cudaGetLastError());
   (void)al;
   c.host_G = n;
+  c.head_sorted = sorted_by_slot(c, ds, n);
   c.host_N = int(N);
   return HMTL_OK;
 }
@@ -776,6 +777,11 @@ int hmtl_store_fetch(hmtl_ctx* h, hmtl_store* st, const uint8_t* plan_ds, const 
   HMTL_CUDA(cudaEventRecord(st->staged, sm));
   HMTL_CUDA(cudaGetLastError());
   c.host_G = n;
+  {
+    std::vector<uint8_t> dsm(n);
+    for (int g = 0; g < n; ++g) dsm[g] = mine[g].ds;
+    c.head_sorted = sorted_by_slot(c, dsm.data(), n);
+  }
   c.host_N = int(N);
   return HMTL_OK;
 }

@@ -82,3 +82,14 @@ def test_async_gather_producers_bit_identical(workload, n):
             assert np.array_equal(x, y), env
         for k in ("g", "p", "pred"):
             assert np.array_equal(a[k], b[k]), (env, k)
+
+
+def test_force_output_layer_fused_into_dx_producer_bit_identical():
+    """The force head's output-layer backward formed inside the dx GEMM's producer
+    (FDxDsProb; its W_2/b_2 column sums on a side stream) == the separate elementwise
+    pass (the default; the fused variant is opt-in, HMTL_FUSE_FORCE_OUT=1), every step bitwise."""
+    a = run("mtl5-weak", False, env={"HMTL_FUSE_FORCE_OUT": "1"})
+    b = run("mtl5-weak", False)
+    assert a["losses"] == b["losses"]
+    for k in ("g", "p", "pred"):
+        assert np.array_equal(a[k], b[k]), k

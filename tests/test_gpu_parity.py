@@ -262,3 +262,26 @@ def test_determinism_bitwise():
         m.close()
     for a, b in zip(outs[0], outs[1]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("order", ["interleaved", "reversed"])
+def test_parity_batch_not_grouped_by_head(orc, order):
+    """Graphs not grouped by head (head-sorted permutations in use: permuted row sets,
+    register-operand weight gradients) -- the grouped case takes identity row sets and
+    TMA operands; both must match the oracle."""
+    s = five_source_batch()
+    idx = np.arange(s.G)
+    idx = idx[::-1] if order == "reversed" else np.argsort(idx % 5, kind="stable")[::-1].copy()
+    rng = np.random.default_rng(5)
+    if order == "interleaved":
+        rng.shuffle(idx)
+    u = s.take(idx.tolist())
+    hp = P.ModelHyper(20, 2, 128, 128, 3, 5, 5.0)
+    oh = O.Hyper(20, 2, 128, 128, 3, 5, 5.0)
+    m, r, pred = run_both(orc, hp, oh, u, [0, 1, 2, 3, 4])
+    assert rel(pred.energy_per_atom, r["E"]) < TOL and rel(pred.forces, r["F"]) < TOL
+    gb = m.backward(r["dE"], r["dF"])
+    gs, gh = orc.backward(oh, r["sh"], r["heads"], r["b"], r["cache"], r["dE"], r["dF"])
+    assert rel(gb.shared, gs) < TOL
+    for k in range(5):
+        assert rel(gb.heads[k], gh[k]) < TOL, k

@@ -18,5 +18,5 @@ PY
 }
 for spec in ${AB_SPECS:-"base|HMTL_X=0"}; do
   IFS='|' read -r tag envs <<< "$spec"
-  run "$tag" $envs
+  run "$tag" ${envs//,/ }
 done
