@@ -129,8 +129,10 @@ struct Ctx {
   // passes: forward message GEMM (HMTL_ASYNC_FWD=1), backward dz1 GEMM (HMTL_ASYNC_BWD: 0 off,
   // 1 silu'(z1) stored by the forward's edge pass, 2 regathered from P in the epilogue)
   bool async_fwd = false;
-  bool fuse_force_out = true;
-  bool launch_prio = false;  // per-launch priority attribute, critical path high (HMTL_LAUNCH_PRIO=1; measured no gain)  // force output layer's dz formed in the dx GEMM producer (HMTL_FUSE_FORCE_OUT=0: off)
+  // force output layer's dz formed in the dx GEMM producer (HMTL_FUSE_FORCE_OUT=1; measured
+  // slower: its side-stream column sums contend with the critical path for SMs)
+  bool fuse_force_out = false;
+  bool launch_prio = false;  // per-launch priority attribute, critical path high (HMTL_LAUNCH_PRIO=1; no gain)
   int async_bwd = 1;
   float* s1pb = nullptr;  // [L][E][H] silu'(z1) stored by the forward for the backward
   int tc_grid_mult = 1;
