@@ -165,14 +165,18 @@ __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t phase) {
 
 // The role sequence is a compile-time parameter: a switch over roles in the
 // unrolled epilogue made every iteration distinct code (instruction-fetch bound).
-template <int R0, int R1, int R2, int CS = 1>
+// MR = node rows per CTA: 128 (M=128 MMAs, accumulator row r in TMEM lane r) or 64
+// (M=64 MMAs: twice the CTAs for the same rows; accumulator row r in TMEM lane
+// (r % 16) + 32 (r / 16), so each epilogue warp owns 16 rows of its lane quadrant).
+template <int R0, int R1, int R2, int CS = 1, int MR = 128>
 __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
   constexpr int G = R2 >= 0 ? 3 : (R1 >= 0 ? 2 : 1);
+  constexpr int QR = MR / 4;  // rows per TMEM lane quadrant (epilogue warp)
   using namespace tc;
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
   const long long t_start = clock64();
   const int M = *p.count;
-  const int row0 = (blockIdx.x / CS) * 128;
+  const int row0 = (blockIdx.x / CS) * MR;
   const uint32_t crank = CS > 1 ? cluster_rank() : 0;
   if (row0 >= M) return;  // whole CTA (and its cluster peer), before any barrier or TMEM use
   uint8_t* sm = align1k(smem_dyn);
@@ -219,10 +223,11 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
   if (warp < kProdWarps) {  // ---------------------------- GEMM 1's A operand
     const int kq = lane & 3, rsub = lane >> 2;
     const int nch = p.g[0].K / KC;
+    constexpr int kIt = MR / 64;  // 8-row groups per producer warp
     int rows[2];
     for (int it = 0; it < 2; ++it) {
-      const int v = row0 + warp * 16 + it * 8 + rsub;
-      rows[it] = v < M ? v : -1;
+      const int v = row0 + warp * 8 * kIt + it * 8 + rsub;
+      rows[it] = (it < kIt && v < M) ? v : -1;
     }
     // three chunk buffers: the one being stored and the next two in flight
     float4 x0[2][2], x1[2][2], x2[2][2];
@@ -240,9 +245,9 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
       float* hi = reinterpret_cast<float*>(X + s * kSlot);
       float* lo = hi + 128 * KC;
 #pragma unroll
-      for (int it = 0; it < 2; ++it)
+      for (int it = 0; it < kIt; ++it)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) put4(hi, lo, 2 * kq + h, warp * 16 + it * 8 + rsub, d[it][h]);
+        for (int h = 0; h < 2; ++h) put4(hi, lo, 2 * kq + h, warp * 8 * kIt + it * 8 + rsub, d[it][h]);
       fence_proxy_async();
       mbar_arrive(&afull[s]);
     };
@@ -287,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
       if (lane == 0) CHAIN_STAMP(2 + 2 * gi);
       for (int n0 = nb_[gi]; n0 < ne_[gi]; n0 += 128) {
         const int nr = ne_[gi] - n0 < 128 ? ne_[gi] - n0 : 128;
-        const uint32_t idesc = idesc_tf32(nr);
+        const uint32_t idesc = (idesc_tf32(nr) & ~(31u << 24)) | (uint32_t(MR >> 4) << 24);
         for (int c = 0; c < nch; ++c, ++q) {
           const int s = q % kBSlots;
           int xs = c;
@@ -341,10 +346,11 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
       const int cc = lane & 7;
       for (int sl = half; nb_[gi] + sl * 32 < ne_[gi]; sl += 2) {
         const int j = nb_[gi] + sl * 32;
-        float4 x[8];  // the slab's operand loads are in flight before the TMEM read
+        constexpr int kRit = QR / 4;  // rows of this warp's quadrant, 4 per read-back pass
+        float4 x[kRit];  // the slab's operand loads are in flight before the TMEM read
 #pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int rr = row0 + qd * 32 + it * 4 + (lane >> 3);
+        for (int it = 0; it < kRit; ++it) {
+          const int rr = row0 + qd * QR + it * 4 + (lane >> 3);
           x[it] = (rr < M && !(p.dbg & 4)) ? aux_load<R>(g, H, rr, j + 4 * cc) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
         float acc[32];
@@ -356,17 +362,17 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
               make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
         __syncwarp();
 #pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int rl = it * 4 + (lane >> 3), rr = row0 + qd * 32 + rl;
+        for (int it = 0; it < kRit; ++it) {  // (M=64: lanes 16-31 of the slab are not rows)
+          const int rl = it * 4 + (lane >> 3), rr = row0 + qd * QR + rl;
           const float4 a = *reinterpret_cast<const float4*>(slab + rl * 32 + ((cc ^ (rl & 7)) << 2));
           const float4 v = epi_apply<R>(g, H, rr < M ? rr : 0, j + 4 * cc, a, x[it], rr < M && !(p.dbg & 1));
           if (!last && !(p.dbg & 2)) {  // next GEMM's A: k = j + 4cc -> chunk j / 32, piece cc of row rl
             float* hi = reinterpret_cast<float*>(X + (j / KC) * kSlot);
-            put4(hi, hi + 128 * KC, cc, qd * 32 + rl, v);
+            put4(hi, hi + 128 * KC, cc, qd * QR + rl, v);
             if constexpr (CS > 1) {  // the same 16 B pieces into every peer's X (DSMEM)
               const float4 h4 = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
               const float4 l4 = make_float4(v.x - h4.x, v.y - h4.y, v.z - h4.z, v.w - h4.w);
-              const uint32_t o = smem_u32(hi) + sw128(qd * 32 + rl, cc);
+              const uint32_t o = smem_u32(hi) + sw128(qd * QR + rl, cc);
 #pragma unroll
               for (int pr = 1; pr < CS; ++pr) {
                 const uint32_t peer = (crank + uint32_t(pr)) % CS;

@@ -166,6 +166,7 @@ struct Ctx {
   int red_seg_mult = 1;     // CTA multiplier for head-segmented weight gradients (HMTL_RED_SEGX)
   int red_min_chunks = 4;   // >= this many 32-row chunks per weight-gradient CTA (HMTL_RED_MINCH)
   bool red_tma = true;      // TMA operand path for plain row-major weight gradients (HMTL_NO_RED_TMA=1 off)
+  int chain_mr = 128;       // node rows per chain CTA: 128 or 64 (HMTL_CHAIN_M; 64 only with the 2-CTA split)
   int chain_cs = 2;         // node-chain cluster size: 2 = column split over a CTA pair (HMTL_CHAIN_CS=1: one CTA)
   float *a1 = nullptr, *af0 = nullptr, *sf0 = nullptr;
   float* tpart = nullptr;  // [2][tcap][H] per-128-edge-tile pieces of straddling destinations (fused edge passes)

@@ -902,7 +902,8 @@ void launch_chain(Ctx& c, const char* name, int G, const chain::Gemm* gs, cudaSt
   }
   q.stamps = c.chain_stamps;
   q.dbg = c.chain_dbg;
-  const int grid = int((c.Nc + 127) / 128);
+  const int mr = c.chain_mr;  // node rows per CTA (128 or 64)
+  const int grid = int((c.Nc + mr - 1) / mr);
   // CS-CTA clusters split every GEMM's columns (chained operand exchanged through DSMEM)
   int cs = c.chain_cs;
   for (int i = 0; i < G; ++i)
@@ -935,23 +936,24 @@ void launch_chain(Ctx& c, const char* name, int G, const chain::Gemm* gs, cudaSt
   };
   using namespace chain;
   const int r0 = gs[0].role, r1 = G > 1 ? gs[1].role : -1, r2 = G > 2 ? gs[2].role : -1;
-  if (r0 == kFwdNode1 && r1 == kFwdNode2 && r2 == kFwdP) {
-    if (quad) go(chain_kernel<kFwdNode1, kFwdNode2, kFwdP, 4>, 4);
-    else if (split) go(chain_kernel<kFwdNode1, kFwdNode2, kFwdP, 2>, 2);
-    else go(chain_kernel<kFwdNode1, kFwdNode2, kFwdP>, 1);
-  } else if (r0 == kFwdNode1 && r1 == kFwdNode2 && r2 < 0) {
-    if (quad) go(chain_kernel<kFwdNode1, kFwdNode2, -1, 4>, 4);
-    else if (split) go(chain_kernel<kFwdNode1, kFwdNode2, -1, 2>, 2);
-    else go(chain_kernel<kFwdNode1, kFwdNode2, -1>, 1);
-  } else if (r0 == kBwdL11 && r1 == kBwdL1 && r2 == kBwdL4) {
-    if (quad) go(chain_kernel<kBwdL11, kBwdL1, kBwdL4, 4>, 4);
-    else if (split) go(chain_kernel<kBwdL11, kBwdL1, kBwdL4, 2>, 2);
-    else go(chain_kernel<kBwdL11, kBwdL1, kBwdL4>, 1);
-  } else if (r0 == kBwdL1 && r1 == kBwdL4 && r2 < 0) {
-    if (quad) go(chain_kernel<kBwdL1, kBwdL4, -1, 4>, 4);
-    else if (split) go(chain_kernel<kBwdL1, kBwdL4, -1, 2>, 2);
-    else go(chain_kernel<kBwdL1, kBwdL4, -1>, 1);
-  }
+  auto pick = [&](auto k128_1, auto k128_2, auto k128_4, auto k64_2) {
+    if (mr == 64 && split) go(k64_2, 2);
+    else if (quad) go(k128_4, 4);
+    else if (split) go(k128_2, 2);
+    else go(k128_1, 1);
+  };
+  if (r0 == kFwdNode1 && r1 == kFwdNode2 && r2 == kFwdP)
+    pick(chain_kernel<kFwdNode1, kFwdNode2, kFwdP>, chain_kernel<kFwdNode1, kFwdNode2, kFwdP, 2>,
+         chain_kernel<kFwdNode1, kFwdNode2, kFwdP, 4>, chain_kernel<kFwdNode1, kFwdNode2, kFwdP, 2, 64>);
+  else if (r0 == kFwdNode1 && r1 == kFwdNode2 && r2 < 0)
+    pick(chain_kernel<kFwdNode1, kFwdNode2, -1>, chain_kernel<kFwdNode1, kFwdNode2, -1, 2>,
+         chain_kernel<kFwdNode1, kFwdNode2, -1, 4>, chain_kernel<kFwdNode1, kFwdNode2, -1, 2, 64>);
+  else if (r0 == kBwdL11 && r1 == kBwdL1 && r2 == kBwdL4)
+    pick(chain_kernel<kBwdL11, kBwdL1, kBwdL4>, chain_kernel<kBwdL11, kBwdL1, kBwdL4, 2>,
+         chain_kernel<kBwdL11, kBwdL1, kBwdL4, 4>, chain_kernel<kBwdL11, kBwdL1, kBwdL4, 2, 64>);
+  else if (r0 == kBwdL1 && r1 == kBwdL4 && r2 < 0)
+    pick(chain_kernel<kBwdL1, kBwdL4, -1>, chain_kernel<kBwdL1, kBwdL4, -1, 2>, chain_kernel<kBwdL1, kBwdL4, -1, 4>,
+         chain_kernel<kBwdL1, kBwdL4, -1, 2, 64>);
 }
 
 RowSet node_rows(Ctx& c) {

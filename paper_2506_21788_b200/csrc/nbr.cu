@@ -338,6 +338,56 @@ void launch_nbr(Ctx& c, cudaStream_t st) {
   launch_route(c, st);
 }
 
+#ifdef HMTL_CHECKED
+namespace {
+// Checked builds (-DHMTL_CHECKED, tests/test_checked_build.py): every index structure the
+// gather / scatter / GEMM kernels of the step dereference, validated on the device after
+// the neighbour list and routing; a violation traps (sticky CUDA error -> the step fails).
+#define HMTL_REQUIRE(cond, what)                                                        \
+  do {                                                                                  \
+    if (!(cond)) {                                                                      \
+      printf("HMTL_CHECKED: %s violated (block %d thread %d)\n", what, blockIdx.x, threadIdx.x); \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
+__global__ void check_structure_kernel(const DevHdr* hdr, const int* __restrict__ row_ptr,
+                                       const int* __restrict__ dst, const int* __restrict__ src,
+                                       const int* __restrict__ rev, const int* __restrict__ graph_offset,
+                                       const int* __restrict__ edge_offset, const int* __restrict__ node_graph,
+                                       const int* __restrict__ node_perm, const int* __restrict__ edge_perm,
+                                       const int* __restrict__ gperm, int Gc, int Nc, long long Ec) {
+  pdl_wait();
+  const int G = hdr->G, N = hdr->N, E = hdr->E;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  if (tid == 0) {
+    HMTL_REQUIRE(G >= 1 && G <= Gc && N >= 1 && N <= Nc && E >= 0 && E <= Ec, "batch sizes within capacity");
+    HMTL_REQUIRE(row_ptr[0] == 0 && row_ptr[N] == E, "CSR row_ptr[0] = 0, row_ptr[N] = E");
+    HMTL_REQUIRE(graph_offset[0] == 0 && graph_offset[G] == N, "graph_offset spans the nodes");
+    HMTL_REQUIRE(edge_offset[0] == 0 && edge_offset[G] == E, "edge_offset spans the edges");
+    int prev = 0;
+    for (int s = 0; s <= hdr->n_slots; ++s) {
+      HMTL_REQUIRE(hdr->seg_edge[s] >= prev && hdr->seg_edge[s] <= E, "head edge segments monotone");
+      prev = hdr->seg_edge[s];
+    }
+  }
+  for (int i = tid; i < N; i += nth) {
+    HMTL_REQUIRE(row_ptr[i] <= row_ptr[i + 1], "CSR rows monotone");
+    HMTL_REQUIRE(node_graph[i] >= 0 && node_graph[i] < G, "node_graph in range");
+    HMTL_REQUIRE(node_perm[i] >= 0 && node_perm[i] < N, "node_perm in range");
+  }
+  for (int g = tid; g < G; g += nth) HMTL_REQUIRE(gperm[g] >= 0 && gperm[g] < G, "gperm in range");
+  for (int e = tid; e < E; e += nth) {
+    const int d = dst[e], s = src[e], r = rev[e];
+    HMTL_REQUIRE(d >= 0 && d < N && s >= 0 && s < N, "edge endpoints in range");
+    HMTL_REQUIRE(e >= row_ptr[d] && e < row_ptr[d + 1], "edge in its destination's CSR row");
+    HMTL_REQUIRE(r >= 0 && r < E && dst[r] == s && src[r] == d && rev[r] == e, "reverse edge");
+    HMTL_REQUIRE(node_graph[d] == node_graph[s], "edge within one graph");
+    HMTL_REQUIRE(edge_perm[e] >= 0 && edge_perm[e] < E, "edge_perm in range");
+  }
+}
+}  // namespace
+#endif
+
 // head routing + head-sorted permutations (shared by both neighbour lists)
 void launch_route(Ctx& c, cudaStream_t st) {
   {
@@ -352,6 +402,10 @@ void launch_route(Ctx& c, cudaStream_t st) {
                                                                    c.edge_dst, c.gnode_base, c.gedge_base, c.node_perm,
                                                                    c.edge_perm);
   }
+#ifdef HMTL_CHECKED
+  kl(check_structure_kernel, grid_for(m, 256, c.sm_count * 8), 256, 0, st, c.hdr, c.row_ptr, c.edge_dst, c.edge_src,
+     c.rev, c.graph_offset, c.edge_offset, c.node_graph, c.node_perm, c.edge_perm, c.gperm, c.Gc, c.Nc, c.Ec);
+#endif
 }
 
 }  // namespace hmtl_b200
