@@ -293,6 +293,12 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   if (const char* e = std::getenv("HMTL_RED_SEGX")) c.red_seg_mult = std::max(1, std::min(8, std::atoi(e)));
   if (const char* e = std::getenv("HMTL_RED_MINCH")) c.red_min_chunks = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("HMTL_RED_SMS")) c.red_sms = std::max(1, std::min(c.sm_count, std::atoi(e)));
+  c.red_sms_early = c.red_sms_now = c.red_sms;
+  if (const char* e = std::getenv("HMTL_RED_CLUSTER")) {
+    const int v = std::atoi(e);
+    c.red_cluster = v >= 8 ? 8 : (v >= 4 ? 4 : (v >= 2 ? 2 : 1));
+  }
+  if (const char* e = std::getenv("HMTL_RED_SMS_EARLY")) c.red_sms_early = std::max(1, std::min(c.sm_count, std::atoi(e)));
   c.row_sms = c.sm_count;
   if (const char* e = std::getenv("HMTL_ROW_SMS")) c.row_sms = std::max(1, std::min(c.sm_count, std::atoi(e)));
   if (const char* e = std::getenv("HMTL_NO_PREFETCH")) c.prefetch_l2 = e[0] == '0';
@@ -381,7 +387,9 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   c.store_af0 = c.use_tc && W % 32 == 0 && H % 4 == 0;
   c.store_sf0 = c.store_af0;  // (regathering silu'(zf0) from Qf in FDx's epilogue measured slower)
   A(&c.a1, c.store_a1 ? L * E * H : 1);
-  A(&c.s1pb, c.store_a1 && (c.async_fwd || c.async_bwd == 1) ? L * E * H : 1);
+  if (const char* e = std::getenv("HMTL_Z1_ONLY")) c.z1_only = e[0] == '1';
+  c.z1_only = c.z1_only && c.store_a1 && !c.fuse_edge && !c.async_fwd;
+  A(&c.s1pb, c.store_a1 && (c.async_fwd || (c.async_bwd == 1 && !c.z1_only)) ? L * E * H : 1);
   A(&c.af0, c.store_af0 ? E * W : 1);
   A(&c.sf0, c.store_sf0 ? E * W : 1);
   c.tcap = int((E + 127) / 128 + 1);

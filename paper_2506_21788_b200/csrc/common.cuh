@@ -113,6 +113,33 @@ inline void kl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// kl() with a thread-block cluster shape
+template <typename... KArgs, typename... Args>
+inline void kl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, dim3 cluster,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[3];
+  int n = 0;
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  at[n].id = cudaLaunchAttributeClusterDimension;
+  at[n].val.clusterDim.x = cluster.x, at[n].val.clusterDim.y = cluster.y, at[n++].val.clusterDim.z = cluster.z;
+  const LaunchPrio& lp = launch_prio();
+  if (lp.on) {
+    at[n].id = cudaLaunchAttributePriority;
+    at[n++].val.priority = st == lp.hi_stream ? lp.hi : lp.lo;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // Sum of n values src[q*stride], q = 0..n-1, with 8 independent accumulators
 // (8 loads in flight) combined in a fixed tree: the association depends only on
 // n, so results are bit-reproducible run to run.

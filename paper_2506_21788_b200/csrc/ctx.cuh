@@ -135,6 +135,9 @@ struct Ctx {
   bool launch_prio = false;  // per-launch priority attribute, critical path high (HMTL_LAUNCH_PRIO=1; no gain)
   int async_bwd = 1;
   float* s1pb = nullptr;  // [L][E][H] silu'(z1) stored by the forward for the backward
+  // the forward's edge pass stores z1 alone (in the a1 buffer); the message GEMM producer, the
+  // eW2 weight gradient and the dz1 epilogue apply silu / silu' to it (HMTL_Z1_ONLY=0: a1 + silu'(z1))
+  bool z1_only = false;  // (measured slower: silu' in the dz1 epilogue, silu in the eW2 gradient converter)
   int tc_grid_mult = 1;
   bool prefetch_l2 = true;  // L2 prefetch of re-read activations ahead of the critical path    // row GEMM grid cap in SMs (0: one CTA per tile)
   long long* chain_stamps = nullptr;
@@ -163,6 +166,9 @@ struct Ctx {
   bool store_sf0 = false;
   int red_sms = 0;          // SMs a weight-gradient (tc_red) launch spreads over (HMTL_RED_SMS; default 13/16 of them)
   int row_sms = 148;        // persistent row-GEMM grid (HMTL_ROW_SMS; default every SM)
+  int red_cluster = 1;      // split-K CTAs per cluster reducing partials through DSMEM (HMTL_RED_CLUSTER 1/2/4/8; opt-in, slower)
+  int red_sms_early = 0;    // ... for the weight gradients of the heads and layers >= 1 (HMTL_RED_SMS_EARLY)
+  int red_sms_now = 0;      // (the value atb() uses while the backward is enqueued)
   int red_seg_mult = 1;     // CTA multiplier for head-segmented weight gradients (HMTL_RED_SEGX)
   int red_min_chunks = 4;   // >= this many 32-row chunks per weight-gradient CTA (HMTL_RED_MINCH)
   bool red_tma = true;      // TMA operand path for plain row-major weight gradients (HMTL_NO_RED_TMA=1 off)

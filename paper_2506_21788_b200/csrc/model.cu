@@ -67,6 +67,7 @@ __device__ __forceinline__ float4 pre4(float4 a, float4 b, float s, float4 w, fl
 __device__ __forceinline__ float4 ldu4(const float* p) { return make_float4(p[0], p[1], p[2], p[3]); }
 
 struct NoAux {};
+struct NoRC {};
 
 struct HeadW {  // a head-block tensor of slot `seg`: base + seg*PH + off
   const float* base;
@@ -162,6 +163,25 @@ struct MsgAsyncProb {
   const int *dst, *src;
   const float4* geo;
   float *z2, *a1out, *s1p;
+  __device__ float b(int, int k, int n) const { return W2[size_t(k) * H + n]; }
+};
+
+// z2 = silu(z1) W2 + b2 from the stored pre-activation z1 (z1_only: the forward's edge
+// pass stores z1 alone; this producer, the eW2 weight gradient and the backward's dz1
+// epilogue apply silu / silu' themselves -- the same values as storing a1 and silu'(z1))
+struct MsgZ1Prob {
+  BDesc bd() const { return BDesc{W2, nullptr, 0, 0, H, 1, K, Ncols, 1, 0, nullptr}; }
+  static constexpr const char* kName = "fwd.edge_msg_gemm";
+  static constexpr bool kTcOnly = true;
+  using Raw = float4;
+  __device__ Raw raw4(int, int e, const NoRC&, int k) const { return ld4(z1 + size_t(e) * H + k); }
+  __device__ float4 fin4(int, int, const NoRC&, int, const Raw& z) const { return silu4(z); }
+  __device__ float4 a4(int, int e, int k) const { return silu4(ld4(z1 + size_t(e) * H + k)); }
+  __device__ void epi4(int, int e, int n, float4 acc) const { st4(z2 + size_t(e) * H + n, add4(acc, ld4(b2 + n))); }
+  RowSet rows;
+  int K, Ncols, H;
+  const float *z1, *W2, *b2;
+  float* z2;
   __device__ float b(int, int k, int n) const { return W2[size_t(k) * H + n]; }
 };
 
@@ -549,7 +569,6 @@ struct HasEpi4 : std::false_type {};
 template <class P>
 struct HasEpi4<P, std::void_t<decltype(std::declval<const P&>().epi4(0, 0, 0, float4{}))>> : std::true_type {};
 
-struct NoRC {};
 template <class P, class = void>
 struct RCOf {
   using type = NoRC;
@@ -836,10 +855,15 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
     // head-segmented rows: segments differ in size (edge shares 1:1:1:2:3), so each gets up to
     // red_seg_mult x its even share of CTAs; CTAs past a short segment's chunks store zeros
     const long long segx = p.rows.nseg > 1 ? c.red_seg_mult : 1;
-    long long want = std::max<long long>(1, (long long)c.red_sms * segx / (mtiles * p.rows.nseg));
+    long long want = std::max<long long>(1, (long long)c.red_sms_now * segx / (mtiles * p.rows.nseg));
     int ns = int(std::max<long long>(1, std::min<long long>(want, chunks / c.red_min_chunks)));
     float* partial = c.part(st);
     while (ns > 1 && size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * NW > c.partial_cap) ns /= 2;
+    // split clusters of `cl` CTAs reduce their partials through DSMEM first (tc.cuh)
+    int cl = c.red_cluster;
+    while (cl > 1 && ns < 2 * cl) cl /= 2;
+    ns = ns / cl * cl;
+    const dim3 cdim(1, unsigned(cl), 1);
     if constexpr (HasTma<P>::value) {  // plain row-major operands over contiguous rows: TMA path
       TmaOps o;
       p.tma(o);
@@ -859,9 +883,13 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
           ok = tc::tmap_2d(&my, o.y + n0, cap_rows, o.ldy);
           if (!ok) break;
           TcRed<P> q{p.rows, M, NT, P::kBias, p, n0};  // each slice sums its own bias columns
-          kl(tc::tc_red_tma_kernel<TcRed<P>>, dim3(mtiles, ns, p.rows.nseg), tc::kRedTmaThreads, smem, st, q, mx,
-             o.x1 ? mx1 : mx, my, o.x1 ? o.xsplit : 0, partial, ns, stages);
-          tc::tc_red_reduce(q, partial, ns, st);
+          if (cl > 1)
+            kl_cluster(tc::tc_red_tma_kernel<TcRed<P>>, dim3(mtiles, ns, p.rows.nseg), tc::kRedTmaThreads, smem, st,
+                       cdim, q, mx, o.x1 ? mx1 : mx, my, o.x1 ? o.xsplit : 0, partial, ns, stages);
+          else
+            kl(tc::tc_red_tma_kernel<TcRed<P>>, dim3(mtiles, ns, p.rows.nseg), tc::kRedTmaThreads, smem, st, q, mx,
+               o.x1 ? mx1 : mx, my, o.x1 ? o.xsplit : 0, partial, ns, stages);
+          tc::tc_red_reduce(q, partial, ns / cl, st);
         }
         if (ok) return;
       }
@@ -872,8 +900,12 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
       for (int n0 = 0; n0 < p.Ncols; n0 += NW) {
         TcRed<P> q{p.rows, M, NW, P::kBias, p, n0};
         dim3 grid(mtiles, ns, p.rows.nseg);
-        kl(tc::tc_red_kernel<TcRed<P>>, grid, tc::kRedThreads, smem, st, q, partial, ns, tc::red_stages(NW));
-        tc::tc_red_reduce(q, partial, ns, st);
+        if (cl > 1)
+          kl_cluster(tc::tc_red_kernel<TcRed<P>>, grid, tc::kRedThreads, smem, st, cdim, q, partial, ns,
+                     tc::red_stages(NW));
+        else
+          kl(tc::tc_red_kernel<TcRed<P>>, grid, tc::kRedThreads, smem, st, q, partial, ns, tc::red_stages(NW));
+        tc::tc_red_reduce(q, partial, ns / cl, st);
       }
       return;
     }
@@ -1007,7 +1039,7 @@ __global__ void __launch_bounds__(256) edge_a1_kernel(const DevHdr* hdr, const f
                                                       const int* __restrict__ dst, const int* __restrict__ src,
                                                       const float4* __restrict__ geo, const float* __restrict__ wd,
                                                       const float* __restrict__ b1, float* __restrict__ a1,
-                                                      float* __restrict__ s1p, int H) {
+                                                      float* __restrict__ s1p, int H, int pre) {
   pdl_wait();
   const int E = hdr->E, lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -1027,7 +1059,7 @@ __global__ void __launch_bounds__(256) edge_a1_kernel(const DevHdr* hdr, const f
       for (int u = 0; u < kEwU; ++u)
         if (eb + u < E) {
           const float4 z = pre4(pa[u], pb[u], d2[u], w, bb);
-          st4(a1 + size_t(eb + u) * H + c, silu4(z));
+          st4(a1 + size_t(eb + u) * H + c, pre ? z : silu4(z));  // (pre: z1 itself; consumers apply silu/silu')
           if (s1p) st4(s1p + size_t(eb + u) * H + c, sgrad4(z));  // silu'(z1) for the backward's dz1 epilogue
         }
     }
@@ -1224,9 +1256,14 @@ void launch_forward(Ctx& c, cudaStream_t st) {
       Prof pr(c, "fwd.edge_act", st);
       kl(edge_a1_kernel, gridn((c.Ec + kEwU - 1) / kEwU * 32, 256, sm * 16), 256, 0, st,
           c.hdr, P, c.edge_dst, c.edge_src, c.geo, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
-          c.a1 + size_t(l) * EH, c.async_bwd == 1 ? c.s1pb + size_t(l) * EH : nullptr, H);
+          c.a1 + size_t(l) * EH, c.async_bwd == 1 && !c.z1_only ? c.s1pb + size_t(l) * EH : nullptr, H,
+          c.z1_only ? 1 : 0);
     }
-    {
+    if (c.store_a1 && c.z1_only) {
+      MsgZ1Prob q{edge_rows(c), H, H, H, c.a1 + size_t(l) * EH, c.params + c.shared_off(p + "edge.W2"),
+                  c.params + c.shared_off(p + "edge.b2"), z2};
+      ab(q, c.Ec, 1, st, sm, c);
+    } else {
       MsgProb q{edge_rows(c), H, H, H, P, W1 + size_t(2) * H * H, c.params + c.shared_off(p + "edge.b1"),
                 c.params + c.shared_off(p + "edge.W2"), c.params + c.shared_off(p + "edge.b2"), c.edge_dst,
                 c.edge_src, c.geo, z2, c.store_a1 ? c.a1 + size_t(l) * EH : nullptr};
@@ -1722,7 +1759,7 @@ struct L6Prob {  // [g_eW2; g_eb2] = [silu(z1), 1]^T dz2   (E rows)
   static constexpr int kBias = 1;
   static constexpr bool kTc = true;
   __device__ float4 x4(int, int e, int m) const {
-    if (a1s) return ld4(a1s + size_t(e) * H + m);
+    if (a1s) return a1_is_z1 ? silu4(ld4(a1s + size_t(e) * H + m)) : ld4(a1s + size_t(e) * H + m);
     return silu4(pre4(ld4(P + size_t(dst[e]) * 2 * H + m), ld4(P + size_t(src[e]) * 2 * H + H + m), geo[e].w,
                       ld4(wd + m), ld4(b1 + m)));
   }
@@ -1738,7 +1775,9 @@ struct L6Prob {  // [g_eW2; g_eb2] = [silu(z1), 1]^T dz2   (E rows)
   float* G;
   const float* a1s;  // a1 materialised by the forward producer (nullable)
   const float *dagg, *z2s;  // non-null: dz2 = dagg[dst] * silu'(z2) computed on the fly
+  int a1_is_z1 = 0;         // a1s holds z1 (the forward stored the pre-activation): X = silu(z1)
   void tma(TmaOps& o) const { o.x = a1s, o.ldx = H, o.y = dagg ? nullptr : dz2, o.ldy = H; }
+  __device__ float4 xfin(float4 v) const { return a1_is_z1 ? silu4(v) : v; }
   __device__ float a(int, int e, int k) const {
     return k < H ? silu(z1_of(P, H, dst[e], src[e], geo[e].w, wd, b1, k)) : 1.f;
   }
@@ -1868,13 +1907,17 @@ struct L7AsyncProb {
     st4(dz2out + size_t(e) * H + k, v);
     return v;
   }
-  __device__ Aux epi_aux(int, int e, int n) const { return Aux{ld4(s1p + size_t(e) * H + n)}; }
+  __device__ Aux epi_aux(int, int e, int n) const {
+    const float4 v = ld4(s1p + size_t(e) * H + n);
+    return Aux{z1_only ? sgrad4(v) : v};  // (z1_only: the forward stored z1, silu'(z1) here)
+  }
   __device__ void epi4a(int, int e, int n, float4 acc, const Aux& a) const { st4(dz1 + size_t(e) * H + n, mul4(acc, a.v)); }
   RowSet rows;
   int K, Ncols, H;
-  const float *W, *dagg, *z2s, *s1p;
+  const float *W, *dagg, *z2s, *s1p;  // s1p: silu'(z1), or z1 itself when z1_only
   const int* dst;
   float *dz2out, *dz1;
+  int z1_only;
   __device__ float b(int, int k, int n) const { return W[size_t(n) * H + k]; }
 };
 
@@ -2423,6 +2466,10 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
     Prof pr(c, "bwd.l2_prefetch", sw2);
     kl(l2_prefetch_kernel, sm * 4, 256, 0, sw2, static_cast<const DevHdr*>(c.hdr), static_cast<const float*>(c.sf0), W);
   }
+  // weight gradients that have most of the backward left to finish in (heads, layers >= 1)
+  // spread over fewer SMs: they hold fewer SMs the critical path needs; layer 0's, which
+  // the optimizer waits on, spread over red_sms
+  c.red_sms_now = c.red_sms_early;
   // ---------------- energy heads (hmtl/model.hpp:512-524)
   c.dep(st, se);
   {
@@ -2565,6 +2612,7 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
     float* dzA = c.dzAb + size_t(l) * EH;
     float* dzB = c.dzBb + size_t(l) * EH;
     float* Sl = c.Sb + size_t(l) * SBS;
+    if (l == 0) c.red_sms_now = c.red_sms;
     if (!node_done) {  // (else: the previous layer's chain produced dvz1, dh2, dagg)
       if (fused && l == L - 1) {  // [L1, L4] of the top layer as one chain
         chain::Gemm gs[2] = {
@@ -2584,7 +2632,7 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
     const bool az = mat && c.async_bwd && !fz;
     if (az && c.async_bwd == 1) {  // cp.async dz2 gather producer -> GEMM (dz2, dz1; silu'(z1) from the forward)
       L7AsyncProb q{edge_rows(c), H, H, H, c.params + c.shared_off(p + "edge.W2"), c.dagg, z2,
-                    c.s1pb + size_t(l) * EH, c.edge_dst, dzA, dzB};
+                    (c.z1_only ? c.a1 : c.s1pb) + size_t(l) * EH, c.edge_dst, dzA, dzB, c.z1_only ? 1 : 0};
       ab(q, c.Ec, 1, st, sm, c);
     } else if (az) {  // ... with silu'(z1) regathered from the node table P in the epilogue
       L7AsyncPProb q{edge_rows(c), H, H, H, c.params + c.shared_off(p + "edge.W2"), c.dagg, z2, P, wd, b1,
@@ -2621,7 +2669,8 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
     }
     {
       L6Prob q{edge_rows(c), H + 1, H, H, P, wd, b1, dzA, c.edge_dst, c.edge_src, c.geo,
-               c.grads + c.shared_off(p + "edge.W2"), mat ? c.a1 + size_t(l) * EH : nullptr, nullptr, z2};
+               c.grads + c.shared_off(p + "edge.W2"), mat ? c.a1 + size_t(l) * EH : nullptr, nullptr, z2,
+               c.z1_only ? 1 : 0};
       atb(q, c, c.nsplit_edge, sw, c.Ec);
     }
     if (fz) {

@@ -276,6 +276,49 @@ inline RowPlan row_plan(int K, int Nt, size_t extra = 0) {
   r.smem = r.b_res + r.stages * per + fixed;
   return r;
 }
+// thread-block cluster helpers (split-K partial reduction through DSMEM)
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float ld_dsmem(uint32_t saddr, uint32_t rank) {
+  uint32_t a;
+  float v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(saddr), "r"(rank));
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+// Weight-gradient GEMMs launched as clusters of CL CTAs along the split dimension:
+// every CTA stages its accumulator tile T[n][m] (+ the column-sum column) in shared
+// memory, then CTA rank r sums rows [r N/CL, (r+1) N/CL) of all CL tiles in rank order
+// (DSMEM) and writes them as ONE partial: CL x fewer partials for split_reduce_kernel to
+// read, same fixed association for every run.
+constexpr int kRedTS = 129;  // T row stride: 128 m-tile features + the column-sum slot
+__device__ __forceinline__ void red_cluster_reduce(const float* T, float* partial, int seg, int split, int nsplit,
+                                                   int N, int Mo, int m0, int Mt, int M, bool do_colsum, int tid,
+                                                   int nthreads) {
+  const uint32_t CL = cl_size(), r = cl_rank();
+  float* out = partial + (size_t(seg) * (nsplit / CL) + split / CL) * size_t(Mo) * N;
+  const int nb = int(r) * N / int(CL), ne = int(r + 1) * N / int(CL);
+  const uint32_t tbase = smem_u32(T);
+  for (int idx = tid; idx < (ne - nb) * kRedTS; idx += nthreads) {
+    const int n = nb + idx / kRedTS, m = idx % kRedTS;
+    if (!(m < Mt || (m == kRedTS - 1 && do_colsum))) continue;
+    float sum = 0.f;
+    for (uint32_t q = 0; q < CL; ++q) sum += ld_dsmem(tbase + uint32_t(n * kRedTS + m) * 4, q);
+    out[size_t(n) * Mo + (m < kRedTS - 1 ? m0 + m : M)] = sum;
+  }
+}
+
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -766,6 +809,8 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
   for (int c = split; c < nchunks; c += nsplit) ++my_chunks;
   const int Mo = p.M + (p.colsum ? 1 : 0);
   float* out = partial + (size_t(seg) * nsplit + split) * size_t(Mo) * N;
+  const bool clustered = cl_size() > 1;  // (launched as split clusters: partials reduced in the cluster)
+  float* T = reinterpret_cast<float*>(smem_raw);  // [N][kRedTS] accumulator staging (stage memory, free by then)
   const int m0 = mtile * 128;
   const int Mt = p.M - m0 < 128 ? p.M - m0 : 128;  // features of this m-tile (mult of 4)
   const bool do_colsum = p.colsum && mtile == 0;
@@ -849,7 +894,11 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
       if (mloc < Mt) {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          if (n0 + i < N) out[size_t(n0 + i) * Mo + m0 + mloc] = my_chunks ? acc[i] : 0.f;
+          if (n0 + i < N) {
+            const float v = my_chunks ? acc[i] : 0.f;
+            if (clustered) T[(n0 + i) * kRedTS + mloc] = v;
+            else out[size_t(n0 + i) * Mo + m0 + mloc] = v;
+          }
       }
     }
     if (do_colsum) {
@@ -857,7 +906,8 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
       for (int n = tid; n < N; n += kProdThreads) {
         float v = 0.f;
         for (int w = 0; w < kRedProd; ++w) v += csum_smem[w * N + n];
-        out[size_t(n) * Mo + p.M] = v;
+        if (clustered) T[n * kRedTS + kRedTS - 1] = v;
+        else out[size_t(n) * Mo + p.M] = v;
       }
     }
   } else {  // MMA issuer
@@ -882,7 +932,13 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc_red_kernel(P p, float* __re
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (clustered) {
+    cl_sync();  // every CTA's accumulator tile staged
+    red_cluster_reduce(T, partial, seg, split, nsplit, N, Mo, m0, Mt, p.M, do_colsum, tid, blockDim.x);
+    cl_sync();  // peers done reading this CTA's tile
+  } else {
+    __syncthreads();
+  }
   if (warp == kRedProd) tmem_dealloc(tmem, acc_cols);
 }
 
@@ -999,6 +1055,8 @@ __global__ void __launch_bounds__(kRedTmaThreads, 1)
   for (int c = split; c < nchunks; c += nsplit) ++my_chunks;
   const int Mo = p.M + (p.colsum ? 1 : 0);
   float* out = partial + (size_t(seg) * nsplit + split) * size_t(Mo) * N;
+  const bool clustered = cl_size() > 1;  // (launched as split clusters: partials reduced in the cluster)
+  float* T = reinterpret_cast<float*>(smem_raw);  // [N][kRedTS] accumulator staging (stage memory, free by then)
   const int m0 = mtile * 128;
   const int Mt = p.M - m0 < 128 ? p.M - m0 : 128;
   const int nxb = (Mt + 31) / 32, nyb = N / 32;  // 32-feature boxes per chunk
@@ -1083,7 +1141,11 @@ __global__ void __launch_bounds__(kRedTmaThreads, 1)
       if (mloc < Mt) {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          if (n0 + i < N) out[size_t(n0 + i) * Mo + m0 + mloc] = my_chunks ? acc[i] : 0.f;
+          if (n0 + i < N) {
+            const float v = my_chunks ? acc[i] : 0.f;
+            if (clustered) T[(n0 + i) * kRedTS + mloc] = v;
+            else out[size_t(n0 + i) * Mo + m0 + mloc] = v;
+          }
       }
     }
     if (do_colsum) {
@@ -1091,7 +1153,8 @@ __global__ void __launch_bounds__(kRedTmaThreads, 1)
       for (int n = tid; n < N; n += kProdThreads) {
         float v = 0.f;
         for (int r = 0; r < 32; ++r) v += csum_smem[r * N + n];
-        out[size_t(n) * Mo + p.M] = v;
+        if (clustered) T[n * kRedTS + kRedTS - 1] = v;
+        else out[size_t(n) * Mo + p.M] = v;
       }
     }
   } else {  // -------------------------------------------------------- MMA
@@ -1120,7 +1183,13 @@ __global__ void __launch_bounds__(kRedTmaThreads, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (clustered) {
+    cl_sync();  // every CTA's accumulator tile staged
+    red_cluster_reduce(T, partial, seg, split, nsplit, N, Mo, m0, Mt, p.M, do_colsum, tid, blockDim.x);
+    cl_sync();  // peers done reading this CTA's tile
+  } else {
+    __syncthreads();
+  }
   if (warp == kRedProd) tmem_dealloc(tmem, acc_cols);
 }
 

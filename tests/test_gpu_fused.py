@@ -93,3 +93,30 @@ def test_force_output_layer_fused_into_dx_producer_bit_identical():
     assert a["losses"] == b["losses"]
     for k in ("g", "p", "pred"):
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_z1_only_storage_bit_identical():
+    """The forward's edge pass storing z1 alone (consumers apply silu / silu'; opt-in
+    HMTL_Z1_ONLY=1) == storing a1 and silu'(z1) (the default), every step bitwise."""
+    a = run("mtl5-weak", False, env={"HMTL_Z1_ONLY": "1"})
+    b = run("mtl5-weak", False)
+    assert a["losses"] == b["losses"]
+    for k in ("g", "p", "pred"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("cl", ["2", "4", "8"])
+def test_cluster_split_k_reduce_matches(cl):
+    """Weight-gradient split-K partials summed across a thread-block cluster through
+    DSMEM (tc.cuh red_cluster_reduce; opt-in HMTL_RED_CLUSTER) == one partial per CTA
+    reduced by split_reduce (the default): same sums in another order (FP32 rounding
+    only), and bitwise reproducible over steps."""
+    a = run("mtl5-weak", False, steps=1, env={"HMTL_RED_CLUSTER": cl})
+    b = run("mtl5-weak", False, steps=1)
+    np.testing.assert_allclose(a["losses"], b["losses"], rtol=1e-6)
+    for k in ("g", "pred"):
+        assert rel(a[k], b[k]) < 1e-5, k
+    a, c = run("mtl5-weak", False, env={"HMTL_RED_CLUSTER": cl}), run("mtl5-weak", False, env={"HMTL_RED_CLUSTER": cl})
+    assert a["losses"] == c["losses"]
+    for k in ("g", "p", "pred"):
+        assert np.array_equal(a[k], c[k]), k
