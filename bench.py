@@ -353,7 +353,7 @@ KERNEL_SCOPES = [
     (r"agg4_kernel", "fwd.agg_segsum"), (r"seg2v?_kernel", "bwd.segsum_dst_src"), (r"edge_a1_kernel", "fwd.edge_act"),
     (r"edge_bwd_prep_kernel", "bwd.edge_act"), (r"forces_kernel", "fwd.forces_segsum"),
     (r"edge_af0_kernel", "fwd.force_act"), (r"colsum2_kernel", "bwd.colsum_tail"),
-    (r"chain_kernel<0", "fwd.node_chain"), (r"chain_kernel<[34]", "bwd.node_chain"),
+    (r"(chain|pair)_kernel<0", "fwd.node_chain"), (r"(chain|pair)_kernel<[34]", "bwd.node_chain"),
     (r"tc_row_kernel<.*::MsgSegProb>", "fwd.edge_msg_fused"), (r"tc_row_kernel<.*::L7SegProb>", "bwd.edge_dz1_fused"),
     (r"agg_fix_kernel", "fwd.agg_fix"), (r"seg_src_kernel", "bwd.segsum_src"),
     (r"tc_row_kernel<.*::MsgAsyncProb>", "fwd.edge_msg_gather"), (r"tc_row_kernel<.*::L7AsyncProb>", "bwd.edge_dz1_gather"),

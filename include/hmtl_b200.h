@@ -325,6 +325,13 @@ int hmtl_selftest_gemm(int mode, int variant, int rows, int K, int N, const floa
  * n back-to-back M=128 x N MMAs.  variant: 0 tf32 SS, 1 tf32 A-in-TMEM,
  * 2 bf16 SS, 3 bf16 A-in-TMEM. */
 int hmtl_selftest_mma_rate(int variant, int N, int n, float* clk_per_mma);
+/* Engine design probe: bytes per SM clock moved into shared memory by bulk copies
+ * (mode 0 from global, `stride` bytes between CTAs' sources, 0 = shared source;
+ * mode 1 between the CTAs of 2-CTA clusters). */
+int hmtl_selftest_ingress(int mode, int grid, long long stride, int total, int chunk, int depth, float* bytes_per_clk);
+/* Engine design probe: TMEM accumulator layout of one CTA-pair (cta_group::2) MMA,
+ * out = [2 CTAs][128 lanes][32 columns]. */
+int hmtl_selftest_pair_layout(int M, int N, float* out);
 int hmtl_selftest_time(int mode, int rows, int K, int N, int iters, float* ms);
 
 /* ------------------------------------------------------------ comm (NCCL) */

@@ -114,6 +114,8 @@ SIGNATURES = {
     "hmtl_set_stream_mode": (C.c_int, [_P, C.c_int]),
     "hmtl_debug_chain_stamps": (C.c_int, [_P, C.POINTER(C.c_longlong), C.c_int]),
     "hmtl_selftest_mma_rate": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),
+    "hmtl_selftest_ingress": (C.c_int, [C.c_int, C.c_int, C.c_longlong, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),
+    "hmtl_selftest_pair_layout": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "hmtl_selftest_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _FP, _FP, _FP]),
     "hmtl_selftest_time": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _FP]),
     "hmtl_epoch_plan": (C.c_int, [C.c_int, _U8P, C.POINTER(C.c_uint64), C.c_int, _IP, _IP, C.c_int, C.c_uint64,

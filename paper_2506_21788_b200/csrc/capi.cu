@@ -1,6 +1,7 @@
 // capi.cu -- the C ABI (include/hmtl_b200.h): device context, batch upload,
 // and the stream-ordered training step.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -96,9 +97,9 @@ int pack(Ctx& c, const hmtl_samples* s, uint8_t* dst, size_t cap, size_t* bytes,
 void free_ctx(Ctx& c) {
   void* ptrs[] = {c.params, c.grads, c.adam_m, c.adam_v, c.hdr, c.d_slot_of, c.arena, c.graph_offset, c.node_graph,
                   c.deg, c.row_ptr, c.edge_src, c.edge_dst, c.rev, c.edge_offset, c.pos32, c.geo, c.dist,
-                  c.species, c.gslot, c.gperm, c.gnode_base, c.gedge_base, c.node_perm, c.edge_perm, c.hs, c.P,
-                  c.z2, c.agg, c.vz1, c.pooled, c.ez, c.energy, c.Qf, c.zf, c.s, c.forces, c.dE, c.dF,
-                  c.dagg, c.dhb, c.dvz1b, c.dzAb, c.dzBb, c.Sb, c.fzA, c.fzB, c.ds, c.dpooled, c.edA, c.edB,
+                  c.species, c.gslot, c.gperm, c.gnode_base, c.gedge_base, c.node_perm, c.edge_perm, c.node_arena,
+                  c.z2, c.pooled, c.ez, c.energy, c.Qf, c.zf, c.s, c.forces, c.dE, c.dF,
+                  c.dzAb, c.dzBb, c.Sb, c.fzA, c.fzB, c.ds, c.dpooled, c.edA, c.edB,
                   c.scratch, c.partial, c.partial_w, c.partial_w2, c.loss_terms, c.cells, c.eimg, c.pbc_meta, c.pbc_bins,
                   c.pbc_order, c.pbc_acoord, c.pbc_w2, c.bimg, c.a1, c.af0, c.sf0, c.bimg_all, c.d_bjobs, c.tpart, c.s1pb};
   for (void* p : ptrs)
@@ -212,6 +213,58 @@ int hmtl_device_count(void) {
   return n;
 }
 
+namespace {
+// persisting L2 window over the node tables on every step stream and (graph capture
+// keeps it per kernel node) in the captured step: the ~100 MB of edge tensors each
+// layer streams through the 126 MB L2 no longer evict the node rows the next
+// kernels gather and the node chains read
+cudaAccessPolicyWindow l2_window(const Ctx& c) {
+  cudaAccessPolicyWindow w{};
+  if (c.l2_persist_mb <= 0 || !c.node_arena) return w;
+  int dev = 0, max_win = 0, max_persist = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  const size_t persist = std::min(size_t(c.l2_persist_mb) << 20, size_t(max_persist));
+  w.base_ptr = c.node_arena;
+  w.num_bytes = std::min(c.node_arena_bytes, size_t(max_win));
+  w.hitRatio = w.num_bytes ? float(std::min(1.0, double(persist) / double(w.num_bytes))) : 0.f;
+  w.hitProp = cudaAccessPropertyPersisting;
+  w.missProp = cudaAccessPropertyStreaming;
+  return w;
+}
+void apply_l2_window(Ctx& c) {
+  const cudaAccessPolicyWindow w = l2_window(c);
+  if (!w.num_bytes) return;
+  int dev = 0, max_persist = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(size_t(c.l2_persist_mb) << 20, size_t(max_persist)));
+  cudaStreamAttrValue v{};
+  v.accessPolicyWindow = w;
+  for (cudaStream_t s : {c.stream, c.s_e, c.s_w, c.s_w2})
+    if (s) cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+  if (std::getenv("HMTL_COMM_LOG"))
+    std::fprintf(stderr, "hmtl: L2 persisting window %zu B, hit ratio %.2f (device max %d B)\n", w.num_bytes,
+                 double(w.hitRatio), max_persist);
+}
+void graph_l2_window(const Ctx& c, cudaGraph_t g) {
+  const cudaAccessPolicyWindow w = l2_window(c);
+  if (!w.num_bytes) return;
+  size_t n = 0;
+  cudaGraphGetNodes(g, nullptr, &n);
+  std::vector<cudaGraphNode_t> nodes(n);
+  cudaGraphGetNodes(g, nodes.data(), &n);
+  cudaKernelNodeAttrValue v{};
+  v.accessPolicyWindow = w;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel)
+      cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &v);
+  }
+}
+}  // namespace
+
 int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* owned, int n_owned,
                     const hmtl_caps* caps, hmtl_ctx** out) {
   if (!hp || !caps || !out) return fail(HMTL_ERR_CONTRACT, "ctx_create: null argument");
@@ -276,6 +329,9 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   }
   if (const char* e = std::getenv("HMTL_SINGLE_STREAM")) c.multi_stream = e[0] == '0';
   if (const char* e = std::getenv("HMTL_NO_CHAIN")) c.fuse_chain = e[0] == '0';
+  if (const char* e = std::getenv("HMTL_CHAIN_PAIR")) c.chain_pair = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HMTL_L2_PERSIST_MB")) c.l2_persist_mb = std::atoi(e);
+  if (const char* e = std::getenv("HMTL_CHAIN_PREFETCH")) c.chain_prefetch = std::atoi(e);
   if (const char* e = std::getenv("HMTL_FUSE_EDGE")) c.fuse_edge = e[0] == '1';
   if (const char* e = std::getenv("HMTL_ASYNC_FWD")) c.async_fwd = e[0] == '1';
   if (const char* e = std::getenv("HMTL_FUSE_FORCE_OUT")) c.fuse_force_out = e[0] == '1';
@@ -339,11 +395,19 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   A(&c.gedge_base, G);
   A(&c.node_perm, N);
   A(&c.edge_perm, E);
-  A(&c.hs, (L + 1) * N * H);
-  A(&c.P, L * N * 2 * H);
+  {  // node tables: one allocation (256 B aligned pieces), the L2 persisting window
+    const size_t parts[] = {(L + 1) * N * H, L * N * 2 * H, L * N * H, L * N * H, N * H, (L + 1) * N * H, L * N * H};
+    float** dst[] = {&c.hs, &c.P, &c.agg, &c.vz1, &c.dagg, &c.dhb, &c.dvz1b};
+    size_t tot = 0;
+    for (size_t n : parts) tot += (n + 63) & ~size_t(63);
+    A(&c.node_arena, tot);
+    if (!rc) {
+      size_t o = 0;
+      for (int i = 0; i < 7; ++i) *dst[i] = c.node_arena + o, o += (parts[i] + 63) & ~size_t(63);
+    }
+    c.node_arena_bytes = tot * sizeof(float);
+  }
   A(&c.z2, L * E * H);
-  A(&c.agg, L * N * H);
-  A(&c.vz1, L * N * H);
   A(&c.pooled, G * H);
   A(&c.ez, D * G * W);
   A(&c.energy, G);
@@ -353,9 +417,6 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   A(&c.forces, 3 * N);
   A(&c.dE, G);
   A(&c.dF, 3 * N);
-  A(&c.dagg, N * H);
-  A(&c.dhb, (L + 1) * N * H);
-  A(&c.dvz1b, L * N * H);
   A(&c.dzAb, L * E * H);
   A(&c.dzBb, L * E * H);
   A(&c.Sb, (L + 1) * N * 2 * std::max(H, W));
@@ -399,6 +460,7 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
     delete h;
     return rc;
   }
+  apply_l2_window(c);
   // parameters exactly as ModelT's ctor (hmtl/model.hpp:162-166)
   std::vector<float> host(c.PT);
   init_block(*hp, seed, -1, host.data());
@@ -485,6 +547,7 @@ int hmtl_ctx_reserve(hmtl_ctx* h, const hmtl_caps* need) {
   // tuning knobs set after creation
   c.multi_stream = n.multi_stream;
   c.overlap_comm = n.overlap_comm;
+  apply_l2_window(c);  // (the step streams came back from the old context: window over the new arena)
   hmtl_ctx_destroy(fresh);  // frees the old capacity buffers and the old step graph
   return 0;
 }
@@ -887,6 +950,7 @@ int hmtl_train_step(hmtl_ctx* h, const hmtl_train_cfg* cfg, void* stream) {
     if (rc) return rc;
     if (e != cudaSuccess) return fail(HMTL_ERR_INTERNAL, std::string("graph capture: ") + cudaGetErrorString(e));
     c.step_kernels = count_kernel_nodes(g);
+    graph_l2_window(c, g);
     c.graph_pbc = c.pbc;
     c.graph_sorted = c.head_sorted;
     HMTL_CUDA(cudaGraphInstantiate(&c.step_exec, g, 0));

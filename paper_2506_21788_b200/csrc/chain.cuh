@@ -50,6 +50,8 @@ struct Chain {
   Gemm g[3];
   long long* stamps;  // optional phase timestamps [CTA][32] (engine tuning; null on the training path)
   int dbg;            // engine ablation bits (0 on the training path): 1 no stores, 2 no X writes, 4 no aux loads
+  int rows_cap;       // allocated node rows of every operand table
+  int prefetch;       // L2 prefetch of the CTA's operands at launch
 };
 #define CHAIN_STAMP(i)                                                   \
   do {                                                                   \
@@ -89,6 +91,53 @@ __device__ __forceinline__ float4 aux_load(const Gemm& g, int H, int r, int n) {
   else if constexpr (R == kBwdL4) return n < H ? ld4c(g.x0 + size_t(r) * H + n) : make_float4(0.f, 0.f, 0.f, 0.f);
   else return make_float4(0.f, 0.f, 0.f, 0.f);
 }
+template <int V>
+using IC = std::integral_constant<int, V>;
+
+// L2 prefetch (bulk, fire and forget) of the row-major operands this CTA's rows
+// [r0, r0 + nr) will read -- GEMM 1's A and every epilogue operand -- plus slice
+// `part` of `parts` of the chain's B images.  The step streams ~100 MB of edge
+// tensors per layer through the 126 MB L2, so these node tables mostly come from
+// DRAM: issued before pdl_wait, the prefetches overlap the previous kernel's tail
+// and turn the chain's dependent loads into L2 hits.  (L2 is the coherence
+// point: a prefetch racing the previous kernel's writes is harmless.)
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+  for (size_t o = 0; o < bytes; o += 65536) {
+    const uint32_t n = uint32_t(bytes - o < 65536 ? bytes - o : 65536);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(p) + o), "r"(n)
+                 : "memory");
+  }
+}
+template <int R0, int R1, int R2>
+__device__ __forceinline__ void chain_prefetch(const Chain& p, int r0, int nr, int part, int parts) {
+  const int H = p.H;
+  if (r0 >= p.rows_cap) return;
+  if (nr > p.rows_cap - r0) nr = p.rows_cap - r0;
+  const size_t row = size_t(H) * 4, rows = size_t(nr) * row;
+  const Gemm& g0 = p.g[0];
+  if constexpr (R0 == kFwdNode1) {
+    prefetch_l2(g0.x0 + size_t(r0) * H, rows), prefetch_l2(g0.x1 + size_t(r0) * H, rows);
+  } else if constexpr (R0 == kFwdP) {
+    prefetch_l2(g0.x0 + size_t(r0) * H, rows);
+  } else if constexpr (R0 == kBwdL11) {
+    prefetch_l2(g0.x1 + size_t(r0) * 2 * H, 2 * rows), prefetch_l2(g0.y0 + size_t(r0) * H, rows);
+  } else if constexpr (R0 == kBwdL1) {
+    prefetch_l2(g0.x1 + size_t(r0) * H, rows), prefetch_l2(g0.x0 + size_t(r0) * H, rows);
+  }
+  auto aux = [&](auto rc, const Gemm& g) {
+    constexpr int R = decltype(rc)::value;
+    if constexpr (R == kFwdNode2 || R == kBwdL1 || R == kBwdL4) prefetch_l2(g.x0 + size_t(r0) * H, rows);
+  };
+  if constexpr (R1 >= 0) aux(IC<R1>{}, p.g[1]);
+  if constexpr (R2 >= 0) aux(IC<R2>{}, p.g[2]);
+  constexpr int G = R2 >= 0 ? 3 : (R1 >= 0 ? 2 : 1);
+  for (int i = 0; i < G; ++i) {  // this CTA's share of every B image (each image is read by all CTAs)
+    const size_t bytes = size_t(2) * p.g[i].K * p.g[i].N * 4, sl = (bytes / parts + 255) & ~size_t(255);
+    const size_t o = sl * size_t(part);
+    if (o < bytes) prefetch_l2(reinterpret_cast<const char*>(p.g[i].img) + o, bytes - o < sl ? bytes - o : sl);
+  }
+}
+
 // epilogue of one GEMM for row r, columns n..n+3 (acc a, operands x); stores the
 // outputs when `store` and returns the next GEMM's A values
 template <int R>
@@ -123,8 +172,6 @@ __device__ __forceinline__ float4 epi_apply(const Gemm& g, int H, int r, int n, 
   }
 }
 
-template <int V>
-using IC = std::integral_constant<int, V>;
 
 // ---- CS-CTA cluster column split (CS = 2 or 4): rank r of a cluster computes
 // columns [r N/CS, (r+1) N/CS) of every GEMM of the same 128 rows and writes its
@@ -409,6 +456,309 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(Chain p) {
   else __syncthreads();
   if (tid == 0) CHAIN_STAMP(31);
   if (warp == kMmaWarp) tmem_dealloc(tmem, 512);
+}
+
+// GEMM 1's A operand: address of 4 consecutive k of row r (the cp.async producer)
+template <int R>
+__device__ __forceinline__ const float* a1_src(const Gemm& g, int H, int r, int k) {
+  if constexpr (R == kFwdNode1) return k < H ? g.x0 + size_t(r) * H + k : g.x1 + size_t(r) * H + k - H;
+  else if constexpr (R == kFwdP) return g.x0 + size_t(r) * H + k;
+  else if constexpr (R == kBwdL11) return g.x1 + size_t(r) * 2 * H + k;
+  else return g.x1 + size_t(r) * H + k;  // kBwdL1
+}
+
+__device__ __forceinline__ float2 ld2c(const float* p) { return *reinterpret_cast<const float2*>(p); }
+__device__ __forceinline__ void st2c(float* p, float2 v) { *reinterpret_cast<float2*>(p) = v; }
+// aux_load / epi_apply for 2 consecutive columns n, n+1 (the pair kernel's .16x256b fragments)
+template <int R>
+__device__ __forceinline__ float2 aux_load2(const Gemm& g, int H, int r, int n) {
+  if constexpr (R == kFwdNode2) return ld2c(g.x0 + size_t(r) * H + n);
+  else if constexpr (R == kBwdL11) return ld2c(g.y0 + size_t(r) * H + n);
+  else if constexpr (R == kBwdL1) return ld2c(g.x0 + size_t(r) * H + n);
+  else if constexpr (R == kBwdL4) return n < H ? ld2c(g.x0 + size_t(r) * H + n) : make_float2(0.f, 0.f);
+  else return make_float2(0.f, 0.f);
+}
+template <int R>
+__device__ __forceinline__ float2 epi_apply2(const Gemm& g, int H, int r, int n, float2 a, float2 x, bool store) {
+  if constexpr (R == kFwdNode1) {
+    const float2 b = ld2c(g.bias + n);
+    const float2 v = make_float2(a.x + b.x, a.y + b.y);
+    if (store) st2c(g.y0 + size_t(r) * H + n, v);
+    return make_float2(silu1(v.x), silu1(v.y));
+  } else if constexpr (R == kFwdNode2) {
+    const float2 b = ld2c(g.bias + n);
+    const float2 v = make_float2(x.x + (a.x + b.x), x.y + (a.y + b.y));
+    if (store) st2c(g.y0 + size_t(r) * H + n, v);
+    return v;
+  } else if constexpr (R == kFwdP) {
+    if (store) st2c(g.y0 + size_t(r) * 2 * H + n, a);
+    return a;
+  } else if constexpr (R == kBwdL11) {
+    const float2 v = make_float2(x.x + a.x, x.y + a.y);
+    if (store) st2c(g.y0 + size_t(r) * H + n, v);
+    return v;
+  } else if constexpr (R == kBwdL1) {
+    const float2 v = make_float2(a.x * sgrad1(x.x), a.y * sgrad1(x.y));
+    if (store) st2c(g.y0 + size_t(r) * H + n, v);
+    return v;
+  } else {  // kBwdL4
+    if (store) {
+      if (n < H) st2c(g.y0 + size_t(r) * H + n, make_float2(x.x + a.x, x.y + a.y));
+      else st2c(g.y1 + size_t(r) * H + n - H, a);
+    }
+    return a;
+  }
+}
+// 2 consecutive k-values (k even, k < 32) of row r into the hi/lo operand tiles
+__device__ __forceinline__ void put2(uint8_t* hi, int r, int k, float2 v) {
+  const float2 h = make_float2(tc::tf32_hi(v.x), tc::tf32_hi(v.y));
+  const uint32_t o = tc::sw128(r, k >> 2) + uint32_t(k & 3) * 4;
+  *reinterpret_cast<float2*>(hi + o) = h;
+  *reinterpret_cast<float2*>(hi + 128 * tc::KC * 4 + o) = make_float2(v.x - h.x, v.y - h.y);
+}
+
+// ---- CTA-pair chain (cta_group::2).  A cluster of two CTAs runs every GEMM of
+// the chain as M = 256 MMAs issued by the leader (rank 0): CTA r owns node rows
+// [pair + 128 r, +128) -- its A operand and its accumulator rows (TMEM lanes 0-127,
+// all N columns) -- and holds columns [r N/2, (r+1) N/2) of every B operand, so
+// each weight byte crosses into the pair once and no activation crosses between
+// the two SMs (the column-split chain above pushed the chained operand through
+// DSMEM, ~21 B/clk).  B images use the pair layout (per half, per 32-k chunk,
+// [hi | lo] contiguous: one 32 KB bulk copy per ring slot).  Readiness of the
+// peer's operands reaches the leader by remote mbarrier arrivals; MMA completion
+// reaches both CTAs by multicast commits.
+namespace pairk {
+constexpr int kAWarp = kEpiWarp0 + kEpiWarps;               // GEMM 1's A tiles (TMA issue)
+constexpr int kThreads = (kProdWarps + 3 + kEpiWarps) * 32;  // 608 (still 5 warps per SMSP: 96 registers)
+constexpr uint32_t kBSlot = 32768;                           // one bulk copy: 1-4 chunks of one GEMM
+constexpr int kBRing = 3;
+constexpr size_t kSmem = size_t(kXSlots) * kSlot + size_t(kBRing) * kBSlot + 512 + 1024;
+}  // namespace pairk
+
+template <int R0, int R1, int R2>
+__global__ void __launch_bounds__(pairk::kThreads, 1)
+    pair_kernel(Chain p, const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUtensorMap ma1) {
+  constexpr int G = R2 >= 0 ? 3 : (R1 >= 0 ? 2 : 1);
+  using namespace tc;
+  using pairk::kBRing;
+  using pairk::kBSlot;
+  extern __shared__ __align__(1024) uint8_t smem_dyn[];
+  const long long t_start = clock64();
+  const int M = *p.count;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const int prow0 = (blockIdx.x / 2) * 256, row0 = prow0 + int(crank) * 128;
+  if (prow0 >= M) return;  // the whole pair, before any barrier or TMEM use
+  uint8_t* sm = align1k(smem_dyn);
+  uint8_t* X = sm;                            // kXSlots x kSlot
+  uint8_t* Bq = sm + kXSlots * kSlot;         // kBRing x kBSlot
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Bq + kBRing * kBSlot);
+  uint64_t* afull = bars;       // [4] leader: 8 producer warps of each CTA
+  uint64_t* aempty = bars + 4;  // [4] multicast commit
+  uint64_t* bfull = bars + 8;   // [3] tx (+ the peer's forwarded arrival on the leader)
+  uint64_t* bempty = bars + 11; // [3] multicast commit
+  uint64_t* accd = bars + 14;   // [3] multicast commit: GEMM g complete
+  uint64_t* xrdy = bars + 17;   // [2][4] leader: chunk c of GEMM g+1's A, 4 epilogue warps of each CTA
+  uint64_t* tfull = bars + 25;  // [4] tx: GEMM 1's A tile landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 29);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int H = p.H;
+  uint32_t acc_off[3];
+  {
+    uint32_t o = 0;
+    for (int i = 0; i < G; ++i) acc_off[i] = o, o += uint32_t(p.g[i].N);
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kXSlots; ++s) mbar_init(&afull[s], 2 * kProdWarps), mbar_init(&aempty[s], 1);
+    for (int s = 0; s < kBRing; ++s) mbar_init(&bfull[s], leader ? 2 : 1), mbar_init(&bempty[s], 1);
+    for (int i = 0; i < 3; ++i) mbar_init(&accd[i], 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&xrdy[i], 2 * 4);
+    for (int s = 0; s < kXSlots; ++s) mbar_init(&tfull[s], 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs exist before any remote arrive; TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (tid == pairk::kThreads - 1) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&ma0) : "memory");
+    if (R0 == kFwdNode1) asm volatile("prefetch.tensormap [%0];" ::"l"(&ma1) : "memory");
+  }
+  if (p.prefetch && tid == pairk::kThreads - 1) chain_prefetch<R0, R1, R2>(p, row0, 128, blockIdx.x, gridDim.x);
+  pdl_wait();
+  if (tid == 0) CHAIN_STAMP(0);
+  // this CTA's arrival on the leader's barrier (local when we are the leader)
+  auto arrive_leader = [&](uint64_t* bar) {
+    if (leader) mbar_arrive(bar);
+    else arrive_cluster(mapa(smem_u32(bar), 0));
+  };
+
+  if (warp == pairk::kAWarp) {  // ------------- GEMM 1's A: 32 k x 128 row TMA tiles (SW128) into the X ring
+    if (lane == 0) {
+      const int nch = p.g[0].K / KC;
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % kXSlots;
+        mbar_wait(&aempty[s], ((c / kXSlots) & 1) ^ 1);
+        mbar_expect_tx(&tfull[s], 128u * 128u);
+        int col = c * KC;
+        const CUtensorMap* m = &ma0;
+        if (R0 == kFwdNode1 && col >= H) m = &ma1, col -= H;
+        tma_2d(X + s * kSlot, m, col, row0, &tfull[s]);
+      }
+    }
+  } else if (warp < kProdWarps) {  // ------------- split the landed fp32 tiles into tf32 hi | lo in place
+    const int nch = p.g[0].K / KC;
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % kXSlots;
+      mbar_wait(&tfull[s], (c / kXSlots) & 1);
+      float4* hi = reinterpret_cast<float4*>(X + s * kSlot);
+      float4* lo = hi + 128 * KC / 4;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // (the same swizzled offset in both tiles)
+        const int o = tid + i * kProdWarps * 32;
+        const float4 v = hi[o];
+        const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+        hi[o] = h;
+        lo[o] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) arrive_leader(&afull[s]);
+      if (tid == 0 && (c == 0 || c == 3)) CHAIN_STAMP(26 + (c == 3));
+    }
+    if (tid == 0) CHAIN_STAMP(1);
+  } else if (warp == kBWarp) {  // ------------- B: this CTA's column half, 32 KB bulk copies
+    if (lane == 0) {
+      int q = 0;
+      for (int gi = 0; gi < G; ++gi) {
+        const Gemm& g = p.g[gi];
+        const int nch = g.K / KC;
+        const uint32_t cb = uint32_t(g.N) * 128;  // one chunk of this half: [hi | lo], N/2 rows x 128 B each
+        const int per = int(kBSlot / cb);
+        for (int c0 = 0; c0 < nch; c0 += per, ++q) {
+          const int s = q % kBRing;
+          mbar_wait(&bempty[s], ((q / kBRing) & 1) ^ 1);
+          const int n = nch - c0 < per ? nch - c0 : per;
+          mbar_expect_tx(&bfull[s], uint32_t(n) * cb);
+          bulk_g2s(Bq + s * kBSlot, g.img + (size_t(crank) * nch + c0) * KC * g.N, uint32_t(n) * cb, &bfull[s]);
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {  // ------------- MMA issuer (leader) / B-copy completion forwarder (peer)
+    if (!leader) {
+      if (lane == 0) {
+        int q = 0;
+        for (int gi = 0; gi < G; ++gi) {
+          const int nch = p.g[gi].K / KC, per = int(kBSlot / (uint32_t(p.g[gi].N) * 128));
+          for (int c0 = 0; c0 < nch; c0 += per, ++q) {
+            mbar_wait(&bfull[q % kBRing], (q / kBRing) & 1);
+            arrive_cluster(mapa(smem_u32(&bfull[q % kBRing]), 0));
+          }
+        }
+      }
+    } else {
+      int q = 0;
+      for (int gi = 0; gi < G; ++gi) {
+        const Gemm& g = p.g[gi];
+        const int nch = g.K / KC;
+        const uint32_t cb = uint32_t(g.N) * 128;
+        const int per = int(kBSlot / cb);
+        const uint32_t idesc = (idesc_tf32(g.N) & ~(31u << 24)) | (uint32_t(256 >> 4) << 24);
+        if (lane == 0) CHAIN_STAMP(2 + 2 * gi);
+        for (int c = 0; c < nch; ++c) {
+          const int s = q % kBRing;
+          if (c % per == 0) {
+            wait_cluster(&bfull[s], (q / kBRing) & 1);
+            tc_fence_after();
+          }
+          int xs = c;
+          if (gi == 0) {
+            xs = c % kXSlots;
+            wait_cluster(&afull[xs], (c / kXSlots) & 1);
+            if (lane == 0 && (c == 0 || c == 7)) CHAIN_STAMP(28 + (c == 7));
+          } else {
+            wait_cluster(&xrdy[(gi - 1) * 4 + c], 0);
+          }
+          tc_fence_after();
+          const uint32_t ah = smem_u32(X + xs * kSlot);
+          const uint32_t bh = smem_u32(Bq + s * kBSlot) + uint32_t(c % per) * cb;
+          issue_chunk_pair(tmem + acc_off[gi], ah, ah + 16384, bh, bh + cb / 2, idesc, c != 0);
+          if (gi == 0) commit_pair(&aempty[xs]);
+          if (c % per == per - 1 || c == nch - 1) {
+            commit_pair(&bempty[s]);
+            ++q;
+          }
+          __syncwarp();
+        }
+        commit_pair(&accd[gi]);
+        if (lane == 0) CHAIN_STAMP(3 + 2 * gi);
+        __syncwarp();
+      }
+    }
+  }
+  if (warp < kProdWarps || (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps)) {  // ---- epilogue: 16 warps,
+    // (the producer warps join once GEMM 1's A is staged).  .16x256b fragments: a warp
+    // owns slab sl (32 columns) of its quadrant's 32 rows; lane t holds rows t/4 and
+    // t/4 + 8 of each 16-lane half, 2 adjacent columns of each 8-column group, so the
+    // output stores and operand loads are full 32 B sectors and no shared-memory
+    // transpose is needed
+    const int qd = warp & 3, wq = warp < kProdWarps ? warp >> 2 : 2 + ((warp - kEpiWarp0) >> 2);
+    const int tr = lane >> 2, tc2 = 2 * (lane & 3);
+    auto phase = [&](auto role_c, auto gi_c) {
+      constexpr int R = decltype(role_c)::value, gi = decltype(gi_c)::value;
+      constexpr bool last = gi == G - 1;
+      const Gemm& g = p.g[gi];
+      mbar_wait(&accd[gi], 0);
+      tc_fence_after();
+      if (warp == kEpiWarp0 + 2 && lane == 0) CHAIN_STAMP(8 + 2 * gi);  // (quadrant 0)
+      for (int sl = wq; sl * 32 < g.N; sl += 4) {
+        const int j = sl * 32;
+        const bool stamp = warp == kEpiWarp0 + 2 && lane == 0 && sl == wq;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int rl0 = qd * 32 + 16 * h + tr;  // rows rl0 and rl0 + 8 of this CTA
+          float2 x[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {  // e = 2 jj + (second row)
+            const int rr = row0 + rl0 + 8 * (e & 1);
+            x[e] = (rr < M && !(p.dbg & 4)) ? aux_load2<R>(g, H, rr, j + 8 * (e >> 1) + tc2) : make_float2(0.f, 0.f);
+          }
+          float v[16];
+          tmem_ld16x32(tmem + acc_off[gi] + (uint32_t(qd * 32 + 16 * h) << 16) + uint32_t(j), v);
+          tmem_wait_ld();
+          if (stamp && h == 0) CHAIN_STAMP(14 + 4 * gi);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int jj = e >> 1, second = e & 1, rl = rl0 + 8 * second, rr = row0 + rl, col = j + 8 * jj + tc2;
+            const float2 a = make_float2(v[4 * jj + 2 * second], v[4 * jj + 2 * second + 1]);
+            const float2 y = epi_apply2<R>(g, H, rr < M ? rr : 0, col, a, x[e], rr < M && !(p.dbg & 1));
+            if (!last && !(p.dbg & 2)) put2(X + (j / KC) * kSlot, rl, 8 * jj + tc2, y);
+          }
+        }
+        if (stamp) CHAIN_STAMP(15 + 4 * gi);
+        if (!last) {  // this warp's 32 rows of X chunk j / 32 are written
+          fence_proxy_async();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_leader(&xrdy[gi * 4 + j / KC]);
+        }
+        if (stamp) CHAIN_STAMP(16 + 4 * gi);
+      }
+      if (warp == kEpiWarp0 + 2 && lane == 0) CHAIN_STAMP(9 + 2 * gi);
+    };
+    phase(IC<R0>{}, IC<0>{});
+    if constexpr (G > 1) phase(IC<R1>{}, IC<1>{});
+    if constexpr (G > 2) phase(IC<R2>{}, IC<2>{});
+  }
+  tc_fence_before();
+  cluster_sync();  // the leader's MMAs read both CTAs' shared memory: nobody leaves early
+  if (tid == 0) CHAIN_STAMP(31);
+  if (warp == kMmaWarp) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
 }  // namespace chain

@@ -23,6 +23,7 @@ struct BDesc {
   int K, N, nseg;
   long long seg_stride;
   float* out;  // image destination (filled in when batched)
+  int halves = 0;  // 2: CTA-pair chain layout (per column half, per 32-k chunk, [hi | lo] contiguous)
 };
 
 // Optional per-launch CUDA-event timing (hmtl_profile); off in timed steps.
@@ -93,6 +94,10 @@ struct Ctx {
 
   // forward cache (device)
   float *hs = nullptr, *P = nullptr, *z2 = nullptr, *agg = nullptr, *vz1 = nullptr;
+  // node tables (hs, P, agg, vz1, dagg, dhb, dvz1b) in one allocation: the L2 persisting window
+  float* node_arena = nullptr;
+  size_t node_arena_bytes = 0;
+  int l2_persist_mb = 0;  // persisting L2 set-aside for the node tables (HMTL_L2_PERSIST_MB; 0 = off)
   float *pooled = nullptr, *ez = nullptr, *energy = nullptr, *Qf = nullptr, *zf = nullptr;
   float *s = nullptr, *forces = nullptr;
   // backward workspace
@@ -122,6 +127,9 @@ struct Ctx {
   size_t ev_i = 0;
   bool multi_stream = true;
   bool fuse_chain = true;  // node-row GEMM chains in one launch (chain.cuh)
+  int chain_prefetch = 0;  // chains prefetch their operands into L2 at launch (HMTL_CHAIN_PREFETCH=1; measured neutral)
+  bool chain_pair = false;  // ... as CTA-pair (cta_group::2) kernels (HMTL_CHAIN_PAIR=1; measured slower)
+  int rec_halves = 0;      // B-image layout tag of the jobs being recorded (the pair chain's GEMMs)
   // fused edge passes (gather producer + segmented epilogue, tc.cuh kSeg): correct but slower on this
   // engine (96-register cap of the 17-warp CTA -> producer spills), opt-in HMTL_FUSE_EDGE=1
   bool fuse_edge = false;

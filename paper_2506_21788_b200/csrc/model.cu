@@ -15,6 +15,8 @@
 // Head-specific weights: rows are grouped per owned head (head-sorted
 // permutations built by route_kernel); GEMM tiles never straddle heads.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 #include <utility>
 
@@ -790,6 +792,14 @@ __global__ void __launch_bounds__(256) bimg_all_kernel(const BDesc* __restrict__
     const float x = b[size_t(seg) * J.seg_stride + size_t(kk) * J.sk + size_t(nn) * J.sn];
     const float h = tc::tf32_hi(x);
     const int ch = k / tc::KC, c16 = (k % tc::KC) / 4, q = k % 4;
+    if (J.halves) {  // pair layout: block (half, chunk) = [hi | lo] of N/2 rows
+      const int Nh = N / 2, hf = n / Nh, nl = n - hf * Nh;
+      float* o = J.out + size_t(seg) * 2 * KN + (size_t(hf) * (K / tc::KC) + ch) * 2 * tc::KC * Nh;
+      const uint32_t off = tc::sw128(nl, c16) / 4 + q;
+      o[off] = h;
+      o[size_t(tc::KC) * Nh + off] = x - h;
+      continue;
+    }
     float* o = J.out + size_t(seg) * 2 * KN + size_t(ch) * 2 * tc::KC * N;
     const uint32_t off = tc::sw128(n, c16) / 4 + q;
     o[off] = h;
@@ -810,13 +820,14 @@ void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& 
   if (use_tc) {
     const float* img = c.bimg;
     const int idx = c.bimg_idx++;
-    if (c.bimg_ready && idx < int(c.bjobs.size())) {
+    if (c.bimg_ready && idx < int(c.bjobs.size()) && !c.bjobs[idx].halves) {
       img = c.bjobs[idx].out;  // prebuilt by the batched builder after the last weight update
-    } else {
+    } else {  // (a pair-layout image -- recorded for a chain that did not run -- is rebuilt here)
       kl(bimg_prob_kernel<P>, gridn((long long)nseg * p.K * p.Ncols, 256, sm * 4), 256, 0, st, p, c.bimg, nseg);
       if (c.bimg_recording) {
         BDesc d = p.bd();
         d.nseg = nseg;
+        d.halves = c.rec_halves;
         c.bjobs.push_back(d);
       }
     }
@@ -922,6 +933,15 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
 bool chain_ok(const Ctx& c) {
   return c.use_tc && c.bimg_ready && c.fuse_chain && c.H % 32 == 0 && c.H <= 128;
 }
+// the recording step's GEMMs that later steps run inside CTA-pair chains get the pair image layout
+int chain_rec_halves(const Ctx& c) {
+  return c.use_tc && c.fuse_chain && c.chain_pair && c.H % 32 == 0 && c.H <= 128 ? 2 : 0;
+}
+struct RecHalves {  // scope: jobs recorded inside carry the pair layout tag
+  Ctx& c;
+  RecHalves(Ctx& c_, bool on) : c(c_) { c.rec_halves = on ? chain_rec_halves(c) : 0; }
+  ~RecHalves() { c.rec_halves = 0; }
+};
 void launch_chain(Ctx& c, const char* name, int G, const chain::Gemm* gs, cudaStream_t st) {
   Prof pr(c, name, st);
   chain::Chain q{};
@@ -932,8 +952,13 @@ void launch_chain(Ctx& c, const char* name, int G, const chain::Gemm* gs, cudaSt
     q.g[i] = gs[i];
     q.g[i].img = c.bjobs[c.bimg_idx++].out;
   }
-  q.stamps = c.chain_stamps;
+  {  // stamps of the chains named HMTL_CHAIN_STAMP_NAME (any chain when unset; the last launch wins)
+    static const char* sel = std::getenv("HMTL_CHAIN_STAMP_NAME");
+    q.stamps = (!sel || !std::strcmp(sel, name)) ? c.chain_stamps : nullptr;
+  }
   q.dbg = c.chain_dbg;
+  q.rows_cap = int(c.Nc);
+  q.prefetch = c.chain_prefetch;
   const int mr = c.chain_mr;  // node rows per CTA (128 or 64)
   const int grid = int((c.Nc + mr - 1) / mr);
   // CS-CTA clusters split every GEMM's columns (chained operand exchanged through DSMEM)
@@ -968,6 +993,51 @@ void launch_chain(Ctx& c, const char* name, int G, const chain::Gemm* gs, cudaSt
   };
   using namespace chain;
   const int r0 = gs[0].role, r1 = G > 1 ? gs[1].role : -1, r2 = G > 2 ? gs[2].role : -1;
+  if (c.chain_pair) {  // CTA-pair kernels over pair-layout B images
+    // GEMM 1's A operand as TMA tiles (32 k x 128 rows, 128 B swizzle = the K-major SW128 operand layout)
+    CUtensorMap ma0{}, ma1{};
+    {
+      const chain::Gemm& g = gs[0];
+      const float* a0 = g.role == kFwdNode1 || g.role == kFwdP ? g.x0 : g.x1;
+      const int ld0 = g.role == kBwdL11 ? 2 * c.H : c.H;
+      bool ok = tc::tmap_2d(&ma0, a0, c.Nc, ld0, CU_TENSOR_MAP_SWIZZLE_128B, 128);
+      if (g.role == kFwdNode1) ok = ok && tc::tmap_2d(&ma1, g.x1, c.Nc, c.H, CU_TENSOR_MAP_SWIZZLE_128B, 128);
+      else ma1 = ma0;
+      if (!ok) {
+        std::fprintf(stderr, "hmtl: chain A tensor map\n");
+        std::abort();
+      }
+    }
+    for (int i = 0; i < G; ++i)
+      if (!c.bjobs[c.bimg_idx - G + i].halves) {
+        std::fprintf(stderr, "hmtl: chain B image %d not in the pair layout\n", c.bimg_idx - G + i);
+        std::abort();
+      }
+    auto gop = [&](auto kern) {
+      set_smem(kern, pairk::kSmem);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(unsigned((c.Nc + 255) / 256 * 2));
+      cfg.blockDim = dim3(pairk::kThreads);
+      cfg.dynamicSmemBytes = pairk::kSmem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[2];
+      int n = 0;
+      if (pdl_enabled()) {
+        at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[n++].val.programmaticStreamSerializationAllowed = 1;
+      }
+      at[n].id = cudaLaunchAttributeClusterDimension;
+      at[n].val.clusterDim.x = 2, at[n].val.clusterDim.y = 1, at[n++].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = n;
+      cudaLaunchKernelEx(&cfg, kern, q, ma0, ma1);
+    };
+    if (r0 == kFwdNode1 && r1 == kFwdNode2 && r2 == kFwdP) gop(pair_kernel<kFwdNode1, kFwdNode2, kFwdP>);
+    else if (r0 == kFwdNode1 && r1 == kFwdNode2 && r2 < 0) gop(pair_kernel<kFwdNode1, kFwdNode2, -1>);
+    else if (r0 == kBwdL11 && r1 == kBwdL1 && r2 == kBwdL4) gop(pair_kernel<kBwdL11, kBwdL1, kBwdL4>);
+    else if (r0 == kBwdL1 && r1 == kBwdL4 && r2 < 0) gop(pair_kernel<kBwdL1, kBwdL4, -1>);
+    return;
+  }
   auto pick = [&](auto k128_1, auto k128_2, auto k128_4, auto k64_2) {
     if (mr == 64 && split) go(k64_2, 2);
     else if (quad) go(k128_4, 4);
@@ -1232,6 +1302,7 @@ void launch_forward(Ctx& c, cudaStream_t st) {
     float* vz1 = c.vz1 + size_t(l) * NH;
     const float* W1 = c.params + c.shared_off(p + "edge.W1");
     if (!p_done) {
+      RecHalves rh(c, l > 0);  // (layer 0's P is never inside a chain)
       PProb q{node_rows(c), H, 2 * H, H, h, W1, P};
       ab(q, c.Nc, 1, st, sm, c);
     }
@@ -1286,11 +1357,13 @@ void launch_forward(Ctx& c, cudaStream_t st) {
       continue;
     }
     {
+      RecHalves rh(c, true);
       Node1Prob q{node_rows(c), 2 * H, H, H, h, agg, c.params + c.shared_off(p + "node.W1"),
                   c.params + c.shared_off(p + "node.b1"), vz1};
       ab(q, c.Nc, 1, st, sm, c);
     }
     {
+      RecHalves rh(c, true);
       Node2Prob q{node_rows(c), H, H, H, vz1, c.params + c.shared_off(p + "node.W2"),
                   c.params + c.shared_off(p + "node.b2"), h, hn};
       ab(q, c.Nc, 1, st, sm, c);
@@ -2620,6 +2693,7 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
             {chain::kBwdL4, H, 2 * H, nullptr, dh, nullptr, nullptr, dh2, c.dagg}};
         launch_chain(c, "bwd.node_chain", 2, gs, st);
       } else {
+        RecHalves rh(c, true);
         L1Prob q1{node_rows(c), H, H, H, dh, c.params + c.shared_off(p + "node.W2"), vz1, dvz1};
         ab(q1, c.Nc, 1, st, sm, c);
         L4Prob q4{node_rows(c), H, 2 * H, H, dvz1, c.params + c.shared_off(p + "node.W1"), dh, dh2, c.dagg};
@@ -2705,6 +2779,7 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
       continue;
     }
     {
+      RecHalves rh(c, l > 0);  // (layer 0's L11 is never inside a chain)
       L11Prob q{node_rows(c), 2 * H, H, H, Sl, eW1, dh2};
       ab(q, c.Nc, 1, st, sm, c);
     }

@@ -93,6 +93,22 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 16 TMEM lanes x 32 consecutive columns (.16x256b, 4 repetitions): thread t holds
+// v[4j + {0, 1}] = lane t/4, columns 8j + 2(t%4) + {0, 1} and v[4j + {2, 3}] = lane
+// t/4 + 8, same columns (the m16n8 accumulator fragment, repeated along N)
+__device__ __forceinline__ void tmem_ld16x32(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 // K-major, SWIZZLE_128B shared-memory matrix descriptor (sm100 "version 1",
 // layout type 2): LBO unused for swizzled K-major (set to 16 B), SBO = 1024 B.
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
@@ -166,7 +182,46 @@ __device__ __forceinline__ void issue_chunk_warp(uint32_t tmem, uint32_t a_hi, u
       "}" ::"r"(tmem),
       "l"(dah), "l"(dal), "l"(dbh), "l"(dbl), "r"(accumulate), "r"(1u), "r"(idesc));
 }
+// CTA-pair variant (cta_group::2, issued by the pair's leader CTA): M = 256, A rows
+// split over the two CTAs, B columns split over them; same shared-memory offsets in both
+__device__ __forceinline__ void issue_chunk_pair(uint32_t tmem, uint32_t a_hi, uint32_t a_lo, uint32_t b_hi,
+                                                 uint32_t b_lo, uint32_t idesc, uint32_t accumulate) {
+  const uint64_t dah = sdesc_sw128(a_hi), dal = sdesc_sw128(a_lo);
+  const uint64_t dbh = sdesc_sw128(b_hi), dbl = sdesc_sw128(b_lo);
+  asm volatile(
+      "{\n\t.reg .pred e, p0, pt;\n\t.reg .b64 ah, al, bh, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p0, %5, 0;\n\t"
+      "setp.ne.b32 pt, %6, 0;\n\t"
+      "mov.b64 ah, %1;\n\tmov.b64 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], al, bh, %7, p0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bl, %7, pt;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %7, pt;\n\t"
+      "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], al, bh, %7, pt;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bl, %7, pt;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %7, pt;\n\t"
+      "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], al, bh, %7, pt;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bl, %7, pt;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %7, pt;\n\t"
+      "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], al, bh, %7, pt;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bl, %7, pt;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %7, pt;\n\t"
+      "}" ::"r"(tmem),
+      "l"(dah), "l"(dal), "l"(dbh), "l"(dbl), "r"(accumulate), "r"(1u), "r"(idesc));
+}
 // warp-wide: the elected lane (the one that issued the MMAs) commits them to `bar`
+// warp-wide, CTA pair: the elected lane's MMAs arrive on `bar` in both CTAs of the pair
+__device__ __forceinline__ void commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
 __device__ __forceinline__ void commit_warp(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
@@ -988,7 +1043,7 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* m, int c0, 
 // 2-D tensor map over a row-major [rows x ld] fp32 matrix: 32 x 32 boxes, 128 B span
 // swizzled in 32 B atoms (the MN-major tf32 operand layout)
 inline bool tmap_2d(CUtensorMap* m, const float* base, long long rows, int ld,
-                    CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) {
+                    CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, int box_rows = 32) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -1000,7 +1055,7 @@ inline bool tmap_2d(CUtensorMap* m, const float* base, long long rows, int ld,
   if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 4) % 16) return false;
   cuuint64_t dims[2] = {cuuint64_t(ld), cuuint64_t(rows)};
   cuuint64_t strides[1] = {cuuint64_t(ld) * 4};
-  cuuint32_t box[2] = {32, 32}, es[2] = {1, 1};
+  cuuint32_t box[2] = {32, cuuint32_t(box_rows)}, es[2] = {1, 1};
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;

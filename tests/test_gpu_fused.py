@@ -120,3 +120,31 @@ def test_cluster_split_k_reduce_matches(cl):
     assert a["losses"] == c["losses"]
     for k in ("g", "p", "pred"):
         assert np.array_equal(a[k], c[k]), k
+
+
+def test_cta_pair_chain_matches():
+    """Node-row chains as CTA-pair (cta_group::2, M = 256) kernels over pair-layout B
+    images (opt-in HMTL_CHAIN_PAIR=1; chain.cuh pair_kernel) == the column-split
+    cluster chains (the default): FP32 rounding only, bitwise reproducible."""
+    a = run("mtl5-weak", False, steps=1, env={"HMTL_CHAIN_PAIR": "1"})
+    b = run("mtl5-weak", False, steps=1)
+    np.testing.assert_allclose(a["losses"], b["losses"], rtol=1e-6)
+    for x, y in zip(a["agg"], b["agg"]):
+        assert rel(x, y) < 1e-6
+    for k in ("g", "pred"):
+        assert rel(a[k], b[k]) < 1e-5, k
+    a, c = run("mtl5-weak", False, env={"HMTL_CHAIN_PAIR": "1"}), run("mtl5-weak", False, env={"HMTL_CHAIN_PAIR": "1"})
+    assert a["losses"] == c["losses"]
+    for k in ("g", "p", "pred"):
+        assert np.array_equal(a[k], c[k]), k
+
+
+def test_l2_residency_knobs_bit_identical():
+    """The persisting L2 window over the node tables (HMTL_L2_PERSIST_MB) and the
+    chains' L2 prefetch (HMTL_CHAIN_PREFETCH) change only where bytes are cached:
+    every step bitwise equal to the default."""
+    a = run("mtl5-weak", False, env={"HMTL_L2_PERSIST_MB": "48", "HMTL_CHAIN_PREFETCH": "1"})
+    b = run("mtl5-weak", False)
+    assert a["losses"] == b["losses"]
+    for k in ("g", "p", "pred"):
+        assert np.array_equal(a[k], b[k]), k
