@@ -20,6 +20,7 @@
 #include <cstring>
 #include <string>
 #include <thread>
+#include <utility>
 #include <vector>
 
 #include "ctx.cuh"
@@ -33,6 +34,7 @@ struct Comm {
   std::vector<int> head_size;
   uint64_t bytes_encoder = 0, bytes_head = 0;
   bool aborted = false;
+  std::vector<std::pair<ncclComm_t, void*>> reg;  // user-buffer registrations (HMTL_NCCL_REG=1)
 };
 void comm_abort(Comm* m);
 
@@ -97,6 +99,7 @@ void comm_destroy(Comm* m) {
     delete m;
     return;
   }
+  for (auto& r : m->reg) ncclCommDeregister(r.first, r.second);
   for (auto& h : m->head)
     if (h) ncclCommDestroy(h);
   if (m->world) ncclCommDestroy(m->world);
@@ -201,6 +204,20 @@ int hmtl_comm_init(hmtl_ctx* h, const uint8_t id_bytes[128], int world, int rank
       return fail(HMTL_ERR_COMM, std::string("ncclCommSplit: ") + ncclGetErrorString(r));
     }
     if (m->head[k]) ncclCommCount(m->head[k], &m->head_size[k]);
+  }
+  if (const char* e = std::getenv("HMTL_NCCL_REG"); e && e[0] == '1') {
+    // the gradient buffer registered with every communicator that reduces it
+    // (zero-copy NVLink transfers / NVLS when the platform offers them)
+    int ok = 0, tried = 0;
+    auto reg = [&](ncclComm_t cm, void* p, size_t bytes) {
+      void* hd = nullptr;
+      ++tried;
+      if (ncclCommRegister(cm, p, bytes, &hd) == ncclSuccess && hd) m->reg.emplace_back(cm, hd), ++ok;
+    };
+    reg(m->world, c.grads, c.PS * sizeof(float));
+    for (int s = 0; s < c.S; ++s)
+      if (m->head[c.owned[s]]) reg(m->head[c.owned[s]], c.grads + c.PS + size_t(s) * c.PH, c.PH * sizeof(float));
+    std::fprintf(stderr, "[hmtl comm] rank %d: registered %d of %d gradient buffers with NCCL\n", rank, ok, tried);
   }
   if (const char* e = std::getenv("HMTL_COMM_LOG"); e && e[0] == '1') {
     std::string g;
