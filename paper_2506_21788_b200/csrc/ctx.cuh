@@ -166,7 +166,7 @@ struct Ctx {
   BDesc* d_bjobs = nullptr;
   int n_djobs = 0;
   int bimg_rows = 1;  // max (segments x K) over the recorded images: bimg_all grid.x
-  int bimg_blocks = 1 << 20;  // CTA cap per image of the batched rebuild (HMTL_BIMG_BLOCKS; throttling it measured slower)
+  int bimg_blocks = 32;  // CTAs per image of the batched rebuild (HMTL_BIMG_BLOCKS; 16-128 measured equal)
   bool store_a1 = false;  // forward producer materialises a1 = silu(z1) [L][E][H]
   bool store_af0 = false; // ... and silu(zf0) [E][W]
   // silu'(zf0) [E][W] too only when the force output layer's backward needs it

@@ -776,34 +776,45 @@ struct TcRed {
 // grid (blocks, jobs); elements walk the contiguous source dimension (coalesced
 // reads), 32-bit index math
 __global__ void __launch_bounds__(256) bimg_all_kernel(const BDesc* __restrict__ jobs) {
+  // one thread per 16 B piece of the image (4 consecutive k of one column n: one
+  // float4 store each for hi and lo); a few CTAs per job, grid-stride
   pdl_wait();
   const BDesc J = jobs[blockIdx.y];
-  const int K = J.K, N = J.N, KN = K * N;
-  const int total = J.nseg * KN;
+  const int K = J.K, N = J.N, K4 = K / 4, KN4 = K4 * N;
+  const int total = J.nseg * KN4;
   const bool kfast = J.sk == 1;  // walk the contiguous source dimension
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const int seg = t / KN;
-    const int rem = t - seg * KN;
-    const int k = kfast ? rem % K : rem / N, n = kfast ? rem / K : rem % N;
-    int kk = k, nn = n;
-    const float* b = J.base0;
-    if (J.split == 1 && n >= J.at) b = J.base1, nn = n - J.at;
-    if (J.split == 2 && k >= J.at) b = J.base1, kk = k - J.at;
-    const float x = b[size_t(seg) * J.seg_stride + size_t(kk) * J.sk + size_t(nn) * J.sn];
-    const float h = tc::tf32_hi(x);
-    const int ch = k / tc::KC, c16 = (k % tc::KC) / 4, q = k % 4;
+    const int seg = t / KN4;
+    const int rem = t - seg * KN4;
+    const int k4 = kfast ? rem % K4 : rem / N, n = kfast ? rem / K4 : rem % N;
+    const int k0 = 4 * k4;
+    float x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int kk = k0 + q, nn = n;
+      const float* b = J.base0;
+      if (J.split == 1 && n >= J.at) b = J.base1, nn = n - J.at;
+      if (J.split == 2 && kk >= J.at) b = J.base1, kk -= J.at;
+      x[q] = b[size_t(seg) * J.seg_stride + size_t(kk) * J.sk + size_t(nn) * J.sn];
+    }
+    const float4 h = make_float4(tc::tf32_hi(x[0]), tc::tf32_hi(x[1]), tc::tf32_hi(x[2]), tc::tf32_hi(x[3]));
+    const float4 l = make_float4(x[0] - h.x, x[1] - h.y, x[2] - h.z, x[3] - h.w);
+    const int ch = k0 / tc::KC, c16 = (k0 % tc::KC) / 4;
+    float* o;
+    uint32_t off;
+    size_t lo;
     if (J.halves) {  // pair layout: block (half, chunk) = [hi | lo] of N/2 rows
       const int Nh = N / 2, hf = n / Nh, nl = n - hf * Nh;
-      float* o = J.out + size_t(seg) * 2 * KN + (size_t(hf) * (K / tc::KC) + ch) * 2 * tc::KC * Nh;
-      const uint32_t off = tc::sw128(nl, c16) / 4 + q;
-      o[off] = h;
-      o[size_t(tc::KC) * Nh + off] = x - h;
-      continue;
+      o = J.out + size_t(seg) * 8 * KN4 + (size_t(hf) * (K / tc::KC) + ch) * 2 * tc::KC * Nh;
+      off = tc::sw128(nl, c16) / 4;
+      lo = size_t(tc::KC) * Nh;
+    } else {
+      o = J.out + size_t(seg) * 8 * KN4 + size_t(ch) * 2 * tc::KC * N;
+      off = tc::sw128(n, c16) / 4;
+      lo = size_t(tc::KC) * N;
     }
-    float* o = J.out + size_t(seg) * 2 * KN + size_t(ch) * 2 * tc::KC * N;
-    const uint32_t off = tc::sw128(n, c16) / 4 + q;
-    o[off] = h;
-    o[size_t(tc::KC) * N + off] = x - h;
+    *reinterpret_cast<float4*>(o + off) = h;
+    *reinterpret_cast<float4*>(o + lo + off) = l;
   }
 }
 
@@ -1278,7 +1289,8 @@ void launch_bimg_all(Ctx& c, cudaStream_t st) {
   Prof pr(c, "bimg_all", st);
   // a few CTAs per image (grid-stride): the rebuild overlaps the batch preparation and
   // neighbour list without taking every SM from those small critical-path kernels
-  kl(bimg_all_kernel, dim3(std::min((c.bimg_rows + 255) / 256, c.bimg_blocks), c.n_djobs), 256, 0, st, c.d_bjobs);
+  kl(bimg_all_kernel, dim3(std::min({(c.bimg_rows / 4 + 255) / 256, c.bimg_blocks}), c.n_djobs), 256, 0, st,
+     c.d_bjobs);
   c.bimg_ready = true;
   c.bimg_recording = false;
 }

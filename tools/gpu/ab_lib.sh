@@ -11,7 +11,7 @@ try:
 except Exception as e:
     print(t, "FAILED", e); sys.exit()
 k = d["kernel_ms_per_step"]
-top = ["fwd.edge_msg_gemm", "fwd.edge_msg_fused", "bwd.edge_dz1_gemm", "bwd.edge_dz1_fused", "fwd.node_chain",
+top = ["k.bimg_all_kernel", "fwd.edge_msg_gemm", "fwd.edge_msg_fused", "bwd.edge_dz1_gemm", "bwd.edge_dz1_fused", "fwd.node_chain",
        "bwd.node_chain", "bwd.segsum_dst_src", "bwd.segsum_src", "fwd.agg_segsum", "bwd.force_edge_dx", "fwd.force_Qf"]
 print(f"{t:10s} step {d['ms_per_step']:.4f} ms  e2e {d['e2e']['value']:.0f}", {x: k.get(x) for x in top if x in k})
 PY
