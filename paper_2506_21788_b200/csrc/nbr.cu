@@ -99,7 +99,38 @@ __global__ void __launch_bounds__(1024) scan_kernel(DevHdr* hdr, const int* __re
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) carry = 0;
   __syncthreads();
-  for (int base = 0; base < N; base += 1024) {
+  if (N <= 4 * 1024) {  // one pass: 4 consecutive degrees per thread, loads all in flight at once
+    int d[4], t = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d[q] = 4 * tid + q < N ? deg[4 * tid + q] : 0, t += d[q];
+    int x = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int w = warp_sums[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_sums[lane] = w;
+    }
+    __syncthreads();
+    int run = x - t + (wid ? warp_sums[wid - 1] : 0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (4 * tid + q < N) row_ptr[4 * tid + q] = run;
+      run += d[q];
+    }
+    if (tid == 1023) carry = run;
+    __syncthreads();
+  }
+  for (int base = 0; N > 4 * 1024 && base < N; base += 1024) {
     const int i = base + tid;
     const int v = i < N ? deg[i] : 0;
     int x = v;
@@ -226,6 +257,57 @@ __global__ void __launch_bounds__(1024) route_kernel(DevHdr* hdr, const int* __r
     hdr->seg_graph[0] = hdr->seg_node[0] = hdr->seg_edge[0] = 0;
   }
   __syncthreads();
+  if (G <= 1024) {  // one graph per thread: its slot, node and edge counts loaded once for every slot's pass
+    const int g = tid;
+    const int gs = g < G ? gslot[g] : -1;
+    const int nn = g < G ? graph_offset[g + 1] - graph_offset[g] : 0;
+    const int ne = g < G ? edge_offset[g + 1] - edge_offset[g] : 0;
+    for (int s = 0; s < S; ++s) {
+      const bool f = gs == s;
+      int v[3] = {f ? 1 : 0, f ? nn : 0, f ? ne : 0};
+      int x[3] = {v[0], v[1], v[2]};
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFull, x[q], o);
+          if (lane >= o) x[q] += y;
+        }
+        if (lane == 31) wsum[q][wid] = x[q];
+      }
+      __syncthreads();
+      if (wid < 3) {
+        int w = wsum[wid][lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFull, w, o);
+          if (lane >= o) w += y;
+        }
+        wsum[wid][lane] = w;
+      }
+      __syncthreads();
+      int excl[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) excl[q] = x[q] - v[q] + (wid ? wsum[q][wid - 1] : 0) + carry[q];
+      if (f) {
+        gperm[excl[0]] = g;
+        gnode_base[g] = excl[1];
+        gedge_base[g] = excl[2];
+      }
+      __syncthreads();
+      if (tid == 1023) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) carry[q] = excl[q] + v[q];
+      }
+      __syncthreads();
+      if (tid == 0) {
+        hdr->seg_graph[s + 1] = carry[0];
+        hdr->seg_node[s + 1] = carry[1];
+        hdr->seg_edge[s + 1] = carry[2];
+      }
+    }
+    return;
+  }
   for (int s = 0; s < S; ++s) {
     for (int base = 0; base < G; base += 1024) {
       const int g = base + tid;
