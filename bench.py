@@ -434,6 +434,8 @@ def roofline(rep, E, N, G, hyper, n_heads):
     total = sum(r["ms"] for r in rep)
     work = lambda name: kernel_work(name, E, N, G, H, W, L, n_heads)
     known = [r for r in rep if work(r["name"])]
+    if not known:  # no CUPTI kernel records (e.g. running under ncu, which holds the profiling interface)
+        return {"kernel": None, "unavailable": "no CUPTI kernel records in this process"}, None
     dom = max(known, key=lambda r: r["ms"])
     out = {"kernel": dom["name"], "share_of_step": round(dom["ms"] / total, 4), "peak_source": src,
            "timing": "CUPTI kernel records (torch.profiler) of 3 replays of a serialised (single-stream) copy "
