@@ -332,6 +332,7 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   if (const char* e = std::getenv("HMTL_CHAIN_PAIR")) c.chain_pair = std::atoi(e) != 0;
   if (const char* e = std::getenv("HMTL_L2_PERSIST_MB")) c.l2_persist_mb = std::atoi(e);
   if (const char* e = std::getenv("HMTL_CHAIN_PREFETCH")) c.chain_prefetch = std::atoi(e);
+  if (const char* e = std::getenv("HMTL_ROW_PREFETCH")) c.row_prefetch = std::atoi(e);
   if (const char* e = std::getenv("HMTL_FUSE_EDGE")) c.fuse_edge = e[0] == '1';
   if (const char* e = std::getenv("HMTL_ASYNC_FWD")) c.async_fwd = e[0] == '1';
   if (const char* e = std::getenv("HMTL_FUSE_FORCE_OUT")) c.fuse_force_out = e[0] == '1';

@@ -101,13 +101,7 @@ using IC = std::integral_constant<int, V>;
 // DRAM: issued before pdl_wait, the prefetches overlap the previous kernel's tail
 // and turn the chain's dependent loads into L2 hits.  (L2 is the coherence
 // point: a prefetch racing the previous kernel's writes is harmless.)
-__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
-  for (size_t o = 0; o < bytes; o += 65536) {
-    const uint32_t n = uint32_t(bytes - o < 65536 ? bytes - o : 65536);
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(p) + o), "r"(n)
-                 : "memory");
-  }
-}
+using tc::prefetch_l2;
 template <int R0, int R1, int R2>
 __device__ __forceinline__ void chain_prefetch(const Chain& p, int r0, int nr, int part, int parts) {
   const int H = p.H;

@@ -127,6 +127,7 @@ struct Ctx {
   size_t ev_i = 0;
   bool multi_stream = true;
   bool fuse_chain = true;  // node-row GEMM chains in one launch (chain.cuh)
+  int row_prefetch = 0;    // row GEMMs prefetch the next tile's forward-written rows into L2 (HMTL_ROW_PREFETCH=1; measured slower)
   int chain_prefetch = 0;  // chains prefetch their operands into L2 at launch (HMTL_CHAIN_PREFETCH=1; measured neutral)
   bool chain_pair = false;  // ... as CTA-pair (cta_group::2) kernels (HMTL_CHAIN_PAIR=1; measured slower)
   int rec_halves = 0;      // B-image layout tag of the jobs being recorded (the pair chain's GEMMs)

@@ -625,9 +625,18 @@ struct SegOf : std::false_type {};
 template <class P>
 struct SegOf<P, std::void_t<decltype(P::kSegSum)>> : std::bool_constant<P::kSegSum> {};
 
+template <class P, class = void>
+struct HasRowPrefetch : std::false_type {};
+template <class P>
+struct HasRowPrefetch<P, std::void_t<decltype(std::declval<const P&>().prefetch_rows(0, 0))>> : std::true_type {};
 template <class P>
 struct TcRow {
   using RC = typename RCOf<P>::type;
+  static constexpr bool kPrefetch = HasRowPrefetch<P>::value;
+  // L2 prefetch of the row-contiguous streams of rows [r0, r1) (tc.cuh: issued at launch)
+  __device__ __forceinline__ void prefetch_rows(int r0, int r1) const {
+    if constexpr (kPrefetch) p.prefetch_rows(r0, r1);
+  }
   using Aux = typename AuxOf<P>::type;
   using Raw = typename RawOf<P>::type;
   static constexpr bool kSeg = SegOf<P>::value;  // segmented-sum epilogue (tc.cuh)
@@ -848,7 +857,8 @@ void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& 
     int Nt = p.Ncols <= 256 ? p.Ncols : 256;  // column block per tile (<= one 256-col accumulator)
     // (one wave: the largest split whose tile count still fits the SMs)
     while (Nt > 32 && mtiles * (p.Ncols / Nt) * 2 <= sm && (Nt / 2) % 32 == 0) Nt /= 2;
-    const tc::RowPlan plan = tc::row_plan(p.K, Nt, TcRow<P>::kSeg ? tc::kSegKeyBytes : 0);
+    tc::RowPlan plan = tc::row_plan(p.K, Nt, TcRow<P>::kSeg ? tc::kSegKeyBytes : 0);
+    plan.prefetch = c.row_prefetch;
     set_smem(tc::tc_row_kernel<TcRow<P>>, plan.smem);
     const int cap_ctas = c.tc_grid_mult > 0 ? c.row_sms * c.tc_grid_mult : (1 << 30);  // persistent when capped
     kl(tc::tc_row_kernel<TcRow<P>>, gridn(mtiles * (p.Ncols / Nt), 1, cap_ctas), tc::kRowThreads, plan.smem, st, q,
@@ -1997,6 +2007,12 @@ struct L7AsyncProb {
     return Aux{z1_only ? sgrad4(v) : v};  // (z1_only: the forward stored z1, silu'(z1) here)
   }
   __device__ void epi4a(int, int e, int n, float4 acc, const Aux& a) const { st4(dz1 + size_t(e) * H + n, mul4(acc, a.v)); }
+  // z2 and silu'(z1) were written by the forward (long evicted from L2): stream this
+  // CTA's rows into L2 ahead of the pipeline (HMTL_ROW_PREFETCH)
+  __device__ void prefetch_rows(int e0, int e1) const {
+    tc::prefetch_l2(z2s + size_t(e0) * H, size_t(e1 - e0) * H * 4);
+    tc::prefetch_l2(s1p + size_t(e0) * H, size_t(e1 - e0) * H * 4);
+  }
   RowSet rows;
   int K, Ncols, H;
   const float *W, *dagg, *z2s, *s1p;  // s1p: silu'(z1), or z1 itself when z1_only

@@ -293,6 +293,10 @@ constexpr size_t kRowBars = 256;
 // epilogue column half (the 4 quadrant warps of a half exchange through it)
 constexpr size_t kSegKeyBytes = size_t(2) * 128 * 4;
 template <class P, class = void>
+struct RowPf : std::false_type {};
+template <class P>
+struct RowPf<P, std::void_t<decltype(P::kPrefetch)>> : std::bool_constant<P::kPrefetch> {};
+template <class P, class = void>
 struct RowAsync : std::false_type {};
 template <class P>
 struct RowAsync<P, std::void_t<decltype(P::kAsync)>> : std::bool_constant<P::kAsync> {};
@@ -311,8 +315,16 @@ struct RowSeg : std::false_type {};
 template <class P>
 struct RowSeg<P, std::void_t<decltype(P::kSeg)>> : std::bool_constant<P::kSeg> {};
 
+// L2 prefetch (bulk, fire and forget) of a contiguous byte range
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+  for (size_t o = 0; o < bytes; o += 65536) {
+    const uint32_t n = uint32_t(bytes - o < 65536 ? bytes - o : 65536) & ~15u;
+    if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(p) + o), "r"(n)
+                        : "memory");
+  }
+}
 struct RowPlan {
-  int Nt, stages, resident;
+  int Nt, stages, resident, prefetch = 0;
   size_t a_stage, b_stage, b_res, smem;
 };
 inline RowPlan row_plan(int K, int Nt, size_t extra = 0) {
@@ -435,6 +447,17 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   const uint32_t tmem = *tmem_slot;
   // ablation bits read once: a global load per chunk sat on the producer's critical path
   const int dbg = g_tc_debug;
+  if constexpr (RowPf<P>::value) {  // the first tile's rows of a plain row range, streamed into L2
+    // while the previous kernel drains (inputs written long before it: safe before pdl_wait);
+    // the producer prefetches each next tile as it starts one (below)
+    if (plan.prefetch && tid == kRowThreads - 1 && !p.rows.perm && !p.rows.seg_off) {
+      const int cnt = *p.rows.count, ntn = p.Ncols / Nt;
+      const int tot = (cnt + 127) / 128 * ntn;
+      const int tb = int((long long)blockIdx.x * tot / gridDim.x), te = int((long long)(blockIdx.x + 1) * tot / gridDim.x);
+      const int r0 = (tb / ntn) * 128;
+      if (te > tb && r0 < cnt) p.prefetch_rows(r0, r0 + 128 < cnt ? r0 + 128 : cnt);
+    }
+  }
   pdl_wait();  // setup above overlaps the previous kernel's tail
   // first m-tile of every head segment, in shared memory: a dynamically indexed
   // per-thread array lands in local memory, whose misses go to L2 (the L1 left
@@ -473,6 +496,12 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
       int seg = 0;
       while (tm >= mt_seg[seg + 1]) ++seg;
       u.seg = seg;
+      if constexpr (RowPf<P>::value) {  // the next tile's row streams into L2, one tile ahead
+        if (plan.prefetch && tid == 0 && !p.rows.perm && !p.rows.seg_off && u.t + 1 < t_end && (u.t + 1) / ntn != tm) {
+          const int r0 = (tm + 1) * 128, cnt = p.rows.end(0);
+          if (r0 < cnt) p.prefetch_rows(r0, r0 + 128 < cnt ? r0 + 128 : cnt);
+        }
+      }
 #pragma unroll
       for (int it = 0; it < kRowIt; ++it) {  // rows warp*8*kRowIt + it*8 + rsub
         const int v = p.rows.begin(seg) + (tm - mt_seg[seg]) * 128 + warp * 8 * kRowIt + it * 8 + rsub;
