@@ -954,7 +954,13 @@ int hmtl_train_step(hmtl_ctx* h, const hmtl_train_cfg* cfg, void* stream) {
     graph_l2_window(c, g);
     c.graph_pbc = c.pbc;
     c.graph_sorted = c.head_sorted;
-    HMTL_CUDA(cudaGraphInstantiate(&c.step_exec, g, 0));
+    // per-node priorities (the capturing streams' / launch attributes'): without this flag a
+    // graph runs every node at the priority of the stream it is launched into
+    static const unsigned long long inst_flags = [] {
+      const char* e = std::getenv("HMTL_NODE_PRIO");
+      return (e && e[0] == '0') ? 0ull : (unsigned long long)cudaGraphInstantiateFlagUseNodePriority;
+    }();
+    HMTL_CUDA(cudaGraphInstantiate(&c.step_exec, g, inst_flags));
     cudaGraphDestroy(g);
     c.graph_cfg = *cfg;
   }
