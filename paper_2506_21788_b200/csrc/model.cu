@@ -100,6 +100,7 @@ struct PProb {
 
 // z2 = silu(z1) W2 + b2   (hmtl/model.hpp:398-404)
 struct MsgProb {
+  static constexpr bool kSlabEpi = true;  // store-only epilogue: row-coalesced slab stores measured faster
   BDesc bd() const { return BDesc{W2, nullptr, 0, 0, H, 1, K, Ncols, 1, 0, nullptr}; }
   static constexpr const char* kName = "fwd.edge_msg_gemm";
   struct RC {
@@ -314,6 +315,7 @@ struct QfProb {
 
 // force MLP layer i >= 1 over edge rows per head; last layer writes s_e
 struct ForceProb {
+  static constexpr bool kSlabEpi = true;  // store-only epilogue: row-coalesced slab stores measured faster
   BDesc bd() const { return BDesc{Wt.base + Wt.off, nullptr, 0, 0, Ncols, 1, K, Ncols, rows.nseg, (long long)Wt.PH, nullptr}; }
   static constexpr const char* kName = "fwd.force_edge_gemm";
   struct RC {
@@ -633,6 +635,7 @@ template <class P>
 struct TcRow {
   using RC = typename RCOf<P>::type;
   static constexpr bool kPrefetch = HasRowPrefetch<P>::value;
+  static constexpr bool kSlabEpi = SegOf<P>::value || tc::RowSlab<P>::value;  // (tc.cuh: slab vs fragment epilogue)
   // L2 prefetch of the row-contiguous streams of rows [r0, r1) (tc.cuh: issued at launch)
   __device__ __forceinline__ void prefetch_rows(int r0, int r1) const {
     if constexpr (kPrefetch) p.prefetch_rows(r0, r1);
@@ -857,7 +860,7 @@ void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& 
     int Nt = p.Ncols <= 256 ? p.Ncols : 256;  // column block per tile (<= one 256-col accumulator)
     // (one wave: the largest split whose tile count still fits the SMs)
     while (Nt > 32 && mtiles * (p.Ncols / Nt) * 2 <= sm && (Nt / 2) % 32 == 0) Nt /= 2;
-    tc::RowPlan plan = tc::row_plan(p.K, Nt, TcRow<P>::kSeg ? tc::kSegKeyBytes : 0);
+    tc::RowPlan plan = tc::row_plan(p.K, Nt, TcRow<P>::kSeg ? tc::kSegKeyBytes : 0, TcRow<P>::kSlabEpi);
     plan.prefetch = c.row_prefetch;
     set_smem(tc::tc_row_kernel<TcRow<P>>, plan.smem);
     const int cap_ctas = c.tc_grid_mult > 0 ? c.row_sms * c.tc_grid_mult : (1 << 30);  // persistent when capped

@@ -314,6 +314,12 @@ template <class P, class = void>
 struct RowSeg : std::false_type {};
 template <class P>
 struct RowSeg<P, std::void_t<decltype(P::kSeg)>> : std::bool_constant<P::kSeg> {};
+// epilogue through shared-memory transpose slabs: segmented sums, and problems whose
+// store-only epilogue measured faster with row-coalesced 128 B stores (P::kSlabEpi)
+template <class P, class = void>
+struct RowSlab : std::bool_constant<RowSeg<P>::value> {};
+template <class P>
+struct RowSlab<P, std::void_t<decltype(P::kSlabEpi)>> : std::bool_constant<P::kSlabEpi || RowSeg<P>::value> {};
 
 // L2 prefetch (bulk, fire and forget) of a contiguous byte range
 __device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
@@ -326,14 +332,19 @@ __device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
 struct RowPlan {
   int Nt, stages, resident, prefetch = 0;
   size_t a_stage, b_stage, b_res, smem;
+  size_t epi_bytes;  // transpose slabs of the epilogue (0: register-fragment epilogue, no shared memory)
 };
-inline RowPlan row_plan(int K, int Nt, size_t extra = 0) {
+// slabs: the epilogue transposes through per-warp shared-memory slabs (segmented-sum
+// problems need them; every other problem reads .16x256b fragments and pairs lanes
+// with shuffles, leaving the 32 KB to one more A stage)
+inline RowPlan row_plan(int K, int Nt, size_t extra = 0, bool slabs = false) {
   RowPlan r;
   r.Nt = Nt;
+  r.epi_bytes = slabs ? kEpiBytes : 0;
   r.a_stage = size_t(2 * 128 * KC) * 4;  // hi + lo
   const size_t b_chunk = size_t(2 * Nt * KC) * 4;
   const size_t b_all = b_chunk * (K / KC);
-  const size_t fixed = kEpiBytes + kRowBars + extra + 1024;  // +1 KB: manual 1 KB alignment
+  const size_t fixed = r.epi_bytes + kRowBars + extra + 1024;  // +1 KB: manual 1 KB alignment
   r.resident = (b_all + 2 * r.a_stage + fixed <= kSmemLimit) ? 1 : 0;
   r.b_res = r.resident ? b_all : 0;
   r.b_stage = r.resident ? 0 : b_chunk;
@@ -413,7 +424,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   float* bres = reinterpret_cast<float*>(smem_raw);  // resident B (hi/lo per chunk)
   uint8_t* stages = smem_raw + plan.b_res;
   float* epi_smem = reinterpret_cast<float*>(stages + kStages * SB);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kStages * SB + kEpiBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kStages * SB + plan.epi_bytes);
   uint64_t* full = bars;                        // [kStages], count = producer threads (+ tx)
   uint64_t* empty = bars + kStages;             // [kStages], count 1 (MMA commit)
   uint64_t* accfull = bars + 2 * kStages;       // [2], count 1
@@ -713,6 +724,58 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
       const int tm = t / ntn, n0 = (t % ntn) * Nt;
       int seg = 0;
       while (tm >= mt_seg[seg + 1]) ++seg;
+      if constexpr (!RowSlab<P>::value) {
+        {  // ---- register-fragment epilogue (no shared memory; plan.epi_bytes == 0)
+          // .16x256b reads of this quadrant's two 16-lane halves; lane pairs (l, l^1) swap
+          // halves of their 8-column groups so lane l owns row 16h + l/4 + 8(l&1) of the
+          // quadrant, columns 8jj + 4((l>>1)&1) .. +3: the same float4 epi4 calls as the
+          // slab path (bit-identical), full 32 B sectors per store instruction
+          const int fr = (lane >> 2) + 8 * (lane & 1), fc = 4 * ((lane >> 1) & 1);
+          const bool odd = lane & 1;
+          int frow[2];
+          typename P::RC frc[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int v = p.rows.begin(seg) + (tm - mt_seg[seg]) * 128 + q * 32 + 16 * h + fr;
+            frow[h] = v < p.rows.end(seg) ? p.rows.row(v) : -1;
+            if (frow[h] >= 0) frc[h] = p.rctx(seg, frow[h]);
+          }
+          typename P::Aux fa[2][4];
+          auto load_aux = [&](int j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj)
+                if (frow[h] >= 0) fa[h][jj] = p.epi_aux(seg, frow[h], frc[h], n0 + j + 8 * jj + fc);
+          };
+          if (half < nslab) load_aux(half * 32);
+          mbar_wait(&accfull[ab], aphase);
+          tc_fence_after();
+          for (int sl = half; sl < nslab; sl += kEpiHalves) {
+            const int j = sl * 32;
+            if (sl != half) load_aux(j);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              float v[16];
+              tmem_ld16x32(tmem + ab * acc_cols + (uint32_t(q * 32 + 16 * h) << 16) + j, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                const float s0 = odd ? v[4 * jj] : v[4 * jj + 2], s1 = odd ? v[4 * jj + 1] : v[4 * jj + 3];
+                const float r0 = __shfl_xor_sync(0xffffffffu, s0, 1), r1 = __shfl_xor_sync(0xffffffffu, s1, 1);
+                const float4 a = odd ? make_float4(r0, r1, v[4 * jj + 2], v[4 * jj + 3])
+                                     : make_float4(v[4 * jj], v[4 * jj + 1], r0, r1);
+                if (frow[h] >= 0 && !(dbg & 2)) p.epi4(seg, frow[h], frc[h], n0 + j + 8 * jj + fc, a, fa[h][jj]);
+              }
+            }
+          }
+          tc_fence_before();
+          mbar_arrive(&accempty[ab]);
+          if (++ab == 2) ab = 0, aphase ^= 1;
+          continue;
+        }
+      }
+      if constexpr (RowSlab<P>::value) {  // ---- slab epilogue
       int rows_it[8];
       typename P::RC rc[8];
 #pragma unroll
@@ -819,6 +882,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
       tc_fence_before();
       mbar_arrive(&accempty[ab]);
       if (++ab == 2) ab = 0, aphase ^= 1;
+      }
     }
   }
   tc_fence_before();
