@@ -349,6 +349,8 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   if (const char* e = std::getenv("HMTL_NO_RED_TMA")) c.red_tma = e[0] == '0';
   if (const char* e = std::getenv("HMTL_RED_SEGX")) c.red_seg_mult = std::max(1, std::min(8, std::atoi(e)));
   if (const char* e = std::getenv("HMTL_RED_MINCH")) c.red_min_chunks = std::max(1, std::atoi(e));
+  c.red_min_tail = c.red_min_chunks;
+  if (const char* e = std::getenv("HMTL_RED_MINCH_TAIL")) c.red_min_tail = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("HMTL_RED_SMS")) c.red_sms = std::max(1, std::min(c.sm_count, std::atoi(e)));
   c.red_sms_early = c.red_sms_now = c.red_sms;
   if (const char* e = std::getenv("HMTL_RED_CLUSTER")) {

@@ -891,7 +891,7 @@ void atb(const P& p, Ctx& c, int nsplit, cudaStream_t st, long long rows_cap = 0
     // red_seg_mult x its even share of CTAs; CTAs past a short segment's chunks store zeros
     const long long segx = p.rows.nseg > 1 ? c.red_seg_mult : 1;
     long long want = std::max<long long>(1, (long long)c.red_sms_now * segx / (mtiles * p.rows.nseg));
-    int ns = int(std::max<long long>(1, std::min<long long>(want, chunks / c.red_min_chunks)));
+    int ns = int(std::max<long long>(1, std::min<long long>(want, chunks / c.red_min_now)));
     float* partial = c.part(st);
     while (ns > 1 && size_t(p.rows.nseg) * ns * size_t(M + P::kBias) * NW > c.partial_cap) ns /= 2;
     // split clusters of `cl` CTAs reduce their partials through DSMEM first (tc.cuh)
@@ -2574,6 +2574,7 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
   // spread over fewer SMs: they hold fewer SMs the critical path needs; layer 0's, which
   // the optimizer waits on, spread over red_sms
   c.red_sms_now = c.red_sms_early;
+  c.red_min_now = c.red_min_chunks;
   // ---------------- energy heads (hmtl/model.hpp:512-524)
   c.dep(st, se);
   {
@@ -2716,7 +2717,7 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
     float* dzA = c.dzAb + size_t(l) * EH;
     float* dzB = c.dzBb + size_t(l) * EH;
     float* Sl = c.Sb + size_t(l) * SBS;
-    if (l == 0) c.red_sms_now = c.red_sms;
+    if (l == 0) c.red_sms_now = c.red_sms, c.red_min_now = c.red_min_tail;
     if (!node_done) {  // (else: the previous layer's chain produced dvz1, dh2, dagg)
       if (fused && l == L - 1) {  // [L1, L4] of the top layer as one chain
         chain::Gemm gs[2] = {
