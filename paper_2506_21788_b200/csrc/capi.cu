@@ -101,7 +101,7 @@ void free_ctx(Ctx& c) {
                   c.z2, c.pooled, c.ez, c.energy, c.Qf, c.zf, c.s, c.forces, c.dE, c.dF,
                   c.dzAb, c.dzBb, c.Sb, c.fzA, c.fzB, c.ds, c.dpooled, c.edA, c.edB,
                   c.scratch, c.partial, c.partial_w, c.partial_w2, c.loss_terms, c.cells, c.eimg, c.pbc_meta, c.pbc_bins,
-                  c.pbc_order, c.pbc_acoord, c.pbc_w2, c.bimg, c.a1, c.af0, c.sf0, c.bimg_all, c.d_bjobs, c.tpart, c.s1pb};
+                  c.pbc_order, c.pbc_acoord, c.pbc_w2, c.bimg, c.a1, c.af0, c.sf0, c.bimg_all, c.d_bjobs, c.tpart, c.s1pb, c.ptab, c.d_ns};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto* p : c.pool) cudaFree(p);
@@ -169,14 +169,17 @@ int enqueue_step(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st) {
   // does this; the images are needed from the first layer's GEMM on)
   const bool images = c.bimg_ready && c.use_tc && !c.bimg_recording;
   cudaStream_t sb = c.side(c.s_w, st);
+  c.ptab_ready = false;
   if (images) {
     c.dep(st, sb);
     launch_bimg_all(c, sb);
+    launch_ptab(c, sb);
   }
   launch_prep(c, st);
   launch_nbr(c, st);
   if (images) c.dep(sb, st);
   launch_forward(c, st);
+  c.ptab_ready = false;  // (only this step's captured forward reads the table)
   launch_loss(c, cfg.w_energy, cfg.w_force, st);
   launch_backward(c, st, true);  // with a communicator: bucketed allreduces overlap it
   if (c.comm_err) {
@@ -458,6 +461,10 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   A(&c.sf0, c.store_sf0 ? E * W : 1);
   c.tcap = int((E + 127) / 128 + 1);
   A(&c.tpart, size_t(2) * c.tcap * H);
+  A(&c.ptab, size_t(std::max(c.NS, 1)) * 2 * H);
+  A(&c.d_ns, 1);
+  if (!rc) cudaMemcpy(c.d_ns, &c.NS, sizeof(int), cudaMemcpyHostToDevice);
+  if (const char* e = std::getenv("HMTL_PTAB")) c.ptab_on = e[0] != '0';
   if (rc) {
     free_ctx(c);
     delete h;

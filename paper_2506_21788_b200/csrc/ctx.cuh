@@ -127,6 +127,10 @@ struct Ctx {
   size_t ev_i = 0;
   bool multi_stream = true;
   bool fuse_chain = true;  // node-row GEMM chains in one launch (chain.cuh)
+  bool ptab_on = true;     // layer 0's P from a per-species table (HMTL_PTAB=0: the node-row GEMM)
+  bool ptab_ready = false;  // (this step's table was launched)
+  float* ptab = nullptr;    // [NS][2H]
+  int* d_ns = nullptr;      // device copy of NS (row count of the table GEMM)
   int row_prefetch = 0;    // row GEMMs prefetch the next tile's forward-written rows into L2 (HMTL_ROW_PREFETCH=1; measured slower)
   int chain_prefetch = 0;  // chains prefetch their operands into L2 at launch (HMTL_CHAIN_PREFETCH=1; measured neutral)
   bool chain_pair = false;  // ... as CTA-pair (cta_group::2) kernels (HMTL_CHAIN_PAIR=1; measured slower)
@@ -242,6 +246,7 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync = false);  // Model
 void launch_adamw(Ctx& c, const hmtl_train_cfg& cfg, cudaStream_t st, bool defer_images = false);
 void launch_debug_z1(Ctx& c, int layer, float* out, cudaStream_t st);
 void launch_bimg_all(Ctx& c, cudaStream_t st);  // rebuild every recorded B image
+void launch_ptab(Ctx& c, cudaStream_t st);      // layer 0's per-species P table (after launch_bimg_all)
 void set_tc_debug(int bits);                     // HMTL_TC_DEBUG: engine ablation bits (timing only)
 
 int comm_sync_grads(Ctx& c, cudaStream_t st);

@@ -369,12 +369,16 @@ struct ForceProb {
 };
 
 __global__ void embed_kernel(const DevHdr* hdr, const uint8_t* __restrict__ species, const float* __restrict__ embed,
-                             float* __restrict__ h, int H) {
+                             float* __restrict__ h, int H, const float* __restrict__ ptab, float* __restrict__ P0) {
   pdl_wait();
   const long long total = (long long)hdr->N * H;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int i = int(t / H), k = int(t % H);
-    h[t] = embed[size_t(species[i]) * H + k];
+    const int i = int(t / H), k = int(t % H), sp = species[i];
+    h[t] = embed[size_t(sp) * H + k];
+    if (ptab) {  // layer 0's P = h0 [W1a | W1b] is a per-species table (h0 = embed[species])
+      P0[size_t(i) * 2 * H + k] = ptab[size_t(sp) * 2 * H + k];
+      P0[size_t(i) * 2 * H + H + k] = ptab[size_t(sp) * 2 * H + H + k];
+    }
   }
 }
 
@@ -836,14 +840,16 @@ void set_smem(Kern k, size_t bytes) {
 }
 
 template <class P>
-void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& c) {
+void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& c, const float* img_fixed = nullptr) {
   Prof pr(c, P::kName, st);
   const bool use_tc = c.use_tc && p.K % tc::KC == 0 && p.Ncols % 32 == 0 &&
                       (p.Ncols <= 256 || p.Ncols % 256 == 0) && size_t(nseg) * 2 * p.K * p.Ncols <= c.bimg_cap;
   if (use_tc) {
     const float* img = c.bimg;
-    const int idx = c.bimg_idx++;
-    if (c.bimg_ready && idx < int(c.bjobs.size()) && !c.bjobs[idx].halves) {
+    const int idx = img_fixed ? -1 : c.bimg_idx++;  // (img_fixed: a prebuilt image, outside the call order)
+    if (img_fixed) {
+      img = img_fixed;
+    } else if (c.bimg_ready && idx < int(c.bjobs.size()) && !c.bjobs[idx].halves) {
       img = c.bjobs[idx].out;  // prebuilt by the batched builder after the last weight update
     } else {  // (a pair-layout image -- recorded for a chain that did not run -- is rebuilt here)
       kl(bimg_prob_kernel<P>, gridn((long long)nseg * p.K * p.Ncols, 256, sm * 4), 256, 0, st, p, c.bimg, nseg);
@@ -1308,15 +1314,33 @@ void launch_bimg_all(Ctx& c, cudaStream_t st) {
   c.bimg_recording = false;
 }
 
+// layer 0's P table per species: T = embed [W1a | W1b] (NS rows), from the weights alone,
+// on the B-image side stream at the step start; the embed kernel then gathers P0 = T[species]
+// (the same tensor-core GEMM per row as the node-row P GEMM it replaces)
+bool ptab_ok(const Ctx& c) {
+  return c.ptab_on && c.use_tc && c.bimg_ready && !c.bimg_recording && !c.bjobs.empty() && !c.bjobs[0].halves &&
+         c.H % 32 == 0 && c.ptab;
+}
+void launch_ptab(Ctx& c, cudaStream_t st) {
+  c.ptab_ready = ptab_ok(c);
+  if (!c.ptab_ready) return;
+  const int H = c.H;
+  RowSet rows{nullptr, nullptr, c.d_ns, 1};
+  PProb q{rows, H, 2 * H, H, c.shared_param("embed"), c.params + c.shared_off("layer0.edge.W1"), c.ptab};
+  ab(q, c.NS, 1, st, c.sm_count, c, c.bjobs[0].out);
+}
+
 void launch_forward(Ctx& c, cudaStream_t st) {
   c.bimg_idx = 0;
   const int H = c.H, W = c.W, L = c.L, D = c.D, sm = c.sm_count;
   const size_t NH = size_t(c.Nc) * H, EH = size_t(c.Ec) * H;
   {
     Prof pr(c, "fwd.embed", st);
-    kl(embed_kernel, gridn(NH, 256, sm * 16), 256, 0, st, c.hdr, c.species, c.shared_param("embed"), c.hs, H);
+    kl(embed_kernel, gridn(NH, 256, sm * 16), 256, 0, st, c.hdr, c.species, c.shared_param("embed"), c.hs, H,
+       c.ptab_ready ? c.ptab : nullptr, c.P);
   }
-  bool p_done = false;  // P of this layer already produced by the previous node chain
+  bool p_done = c.ptab_ready;  // P of this layer already produced (by the previous node chain / the species table)
+  if (c.ptab_ready) ++c.bimg_idx;  // (layer 0's P GEMM image, used by launch_ptab)
   for (int l = 0; l < L; ++l) {
     const std::string p = "layer" + std::to_string(l) + ".";
     const float* h = c.hs + size_t(l) * NH;
