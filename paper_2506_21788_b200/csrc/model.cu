@@ -2504,7 +2504,7 @@ struct ChunkStore {
 
 // g_embed[s] = sum_{i: species_i = s} dh_i: CTA = 128-node chunk, thread = column,
 // smem accumulator [species][H] updated in ascending node order; chunks summed in order.
-constexpr int kEmbChunk = 128;
+constexpr int kEmbChunk = 64;
 __global__ void embed_grad_part(const DevHdr* hdr, const uint8_t* __restrict__ species, const float* __restrict__ dh,
                                 float* __restrict__ partial, int H, int NS) {
   pdl_wait();
