@@ -100,7 +100,7 @@ void free_ctx(Ctx& c) {
                   c.species, c.gslot, c.gperm, c.gnode_base, c.gedge_base, c.node_perm, c.edge_perm, c.node_arena,
                   c.z2, c.pooled, c.ez, c.energy, c.Qf, c.zf, c.s, c.forces, c.dE, c.dF,
                   c.dzAb, c.dzBb, c.Sb, c.fzA, c.fzB, c.ds, c.dpooled, c.edA, c.edB,
-                  c.scratch, c.partial, c.partial_w, c.partial_w2, c.loss_terms, c.cells, c.eimg, c.pbc_meta, c.pbc_bins,
+                  c.scratch, c.partial, c.partial_w, c.partial_w2, c.partial_w3, c.loss_terms, c.cells, c.eimg, c.pbc_meta, c.pbc_bins,
                   c.pbc_order, c.pbc_acoord, c.pbc_w2, c.bimg, c.a1, c.af0, c.sf0, c.bimg_all, c.d_bjobs, c.tpart, c.s1pb, c.ptab, c.d_ns};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -123,6 +123,7 @@ void free_ctx(Ctx& c) {
   if (c.s_e) cudaStreamDestroy(c.s_e);
   if (c.s_w) cudaStreamDestroy(c.s_w);
   if (c.s_w2) cudaStreamDestroy(c.s_w2);
+  if (c.s_w3) cudaStreamDestroy(c.s_w3);
   if (c.s_c) cudaStreamDestroy(c.s_c);
   if (c.stream) cudaStreamDestroy(c.stream);
 }
@@ -245,7 +246,7 @@ void apply_l2_window(Ctx& c) {
   cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(size_t(c.l2_persist_mb) << 20, size_t(max_persist)));
   cudaStreamAttrValue v{};
   v.accessPolicyWindow = w;
-  for (cudaStream_t s : {c.stream, c.s_e, c.s_w, c.s_w2})
+  for (cudaStream_t s : {c.stream, c.s_e, c.s_w, c.s_w2, c.s_w3})
     if (s) cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
   if (std::getenv("HMTL_COMM_LOG"))
     std::fprintf(stderr, "hmtl: L2 persisting window %zu B, hit ratio %.2f (device max %d B)\n", w.num_bytes,
@@ -327,6 +328,7 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
         cudaStreamCreateWithPriority(&c.s_e, cudaStreamNonBlocking, lo) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c.s_w, cudaStreamNonBlocking, lo) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c.s_w2, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c.s_w3, cudaStreamNonBlocking, lo) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c.s_c, cudaStreamNonBlocking, hi) != cudaSuccess)
       rc = HMTL_ERR_INTERNAL;
   }
@@ -447,6 +449,7 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   A(&c.partial, c.partial_cap);
   A(&c.partial_w, c.partial_cap);
   A(&c.partial_w2, c.partial_cap);
+  A(&c.partial_w3, c.partial_cap);
   c.bimg_cap = size_t(std::max(c.S, 2)) * 2 * (2 * std::max(H, W)) * (2 * std::max(H, W));
   A(&c.bimg, c.bimg_cap);
   if (const char* e = std::getenv("HMTL_NO_TC")) c.use_tc = e[0] == '0';
@@ -465,6 +468,7 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   A(&c.d_ns, 1);
   if (!rc) cudaMemcpy(c.d_ns, &c.NS, sizeof(int), cudaMemcpyHostToDevice);
   if (const char* e = std::getenv("HMTL_PTAB")) c.ptab_on = e[0] != '0';
+  if (const char* e = std::getenv("HMTL_WGRAD3")) c.wgrad3 = std::atoi(e);
   if (rc) {
     free_ctx(c);
     delete h;
@@ -537,6 +541,7 @@ int hmtl_ctx_reserve(hmtl_ctx* h, const hmtl_caps* need) {
   std::swap(c.s_e, n.s_e);
   std::swap(c.s_w, n.s_w);
   std::swap(c.s_w2, n.s_w2);
+  std::swap(c.s_w3, n.s_w3);
   std::swap(c.s_c, n.s_c);
   std::swap(c.comm, n.comm);
   std::swap(c.pool, n.pool);

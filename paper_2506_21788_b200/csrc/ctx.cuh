@@ -107,6 +107,7 @@ struct Ctx {
   float *edA = nullptr, *edB = nullptr, *scratch = nullptr;
   float* partial = nullptr;    // split-K partials of kernels on the main stream
   float* partial_w = nullptr;   // ... and of the weight-gradient streams
+  float* partial_w3 = nullptr;
   float* partial_w2 = nullptr;
   size_t partial_cap = 0;
   // backward buffers that weight-gradient kernels read: one per layer, so the
@@ -118,7 +119,7 @@ struct Ctx {
   float *fzA = nullptr, *fzB = nullptr;    // force head dz ping-pong [E][W]
   // concurrency inside the step: s_e runs the energy head branch, s_w the
   // weight gradients; both fork from / join into the step stream via events
-  cudaStream_t s_e = nullptr, s_w = nullptr, s_w2 = nullptr;
+  cudaStream_t s_e = nullptr, s_w = nullptr, s_w2 = nullptr, s_w3 = nullptr;
   cudaStream_t s_c = nullptr;  // gradient allreduces (high priority), overlapped with the backward
   bool overlap_comm = true;
   int comm_err = 0;
@@ -131,6 +132,8 @@ struct Ctx {
   bool ptab_ready = false;  // (this step's table was launched)
   float* ptab = nullptr;    // [NS][2H]
   int* d_ns = nullptr;      // device copy of NS (row count of the table GEMM)
+  int wgrad3 = 0;          // edge eW2 weight gradient on a third side stream: 0 never, 1 layer 0 (the step's
+                           // tail), 2 every layer (HMTL_WGRAD3)
   int row_prefetch = 0;    // row GEMMs prefetch the next tile's forward-written rows into L2 (HMTL_ROW_PREFETCH=1; measured slower)
   int chain_prefetch = 0;  // chains prefetch their operands into L2 at launch (HMTL_CHAIN_PREFETCH=1; measured neutral)
   bool chain_pair = false;  // ... as CTA-pair (cta_group::2) kernels (HMTL_CHAIN_PAIR=1; measured slower)
@@ -214,7 +217,9 @@ struct Ctx {
   size_t head_off(const std::string& name) const { return head_lay.at(name).offset; }
   float* head_params() const { return params + PS; }
   float* head_grads() const { return grads + PS; }
-  float* part(cudaStream_t st) const { return st == s_w ? partial_w : (st == s_w2 ? partial_w2 : partial); }
+  float* part(cudaStream_t st) const {
+    return st == s_w ? partial_w : (st == s_w2 ? partial_w2 : (st == s_w3 ? partial_w3 : partial));
+  }
   // stream for a side branch (the step stream itself while B images are being
   // recorded: that eager step shares one image scratch buffer)
   cudaStream_t side(cudaStream_t which, cudaStream_t st) const {

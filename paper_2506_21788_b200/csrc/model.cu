@@ -2581,7 +2581,8 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
   const size_t GW = size_t(c.Gc) * W;
   // streams: st = critical path (dx chain), se = energy head branch, sw = weight
   // gradients (consumed only by the gradient sync / AdamW after the final join)
-  cudaStream_t se = c.side(c.s_e, st), sw = c.side(c.s_w, st), sw2 = c.side(c.s_w2, st);
+  cudaStream_t se = c.side(c.s_e, st), sw = c.side(c.s_w, st), sw2 = c.side(c.s_w2, st), sw3 = c.side(c.s_w3, st);
+  bool own3 = false, used3 = false;  // the eW2 gradient of this layer / of any layer on sw3
   // gradient sync buckets (MTL-par), issued on the comm stream as they become final
   const bool cs = comm_sync && comm_overlap(c);
   cudaStream_t sc = c.side(c.s_c, st);
@@ -2798,10 +2799,16 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
       atb(q, c, c.nsplit_node, sw, c.Nc);
     }
     {
+      // (on its own stream for layer 0: the step's tail runs the last layer's weight
+      // gradients side by side instead of one after another on sw)
+      own3 = sw3 != st && (c.wgrad3 >= 2 || (c.wgrad3 == 1 && l == 0));
+      used3 = used3 || own3;
+      cudaStream_t s6 = own3 ? sw3 : sw;
+      if (own3) c.dep(st, s6);
       L6Prob q{edge_rows(c), H + 1, H, H, P, wd, b1, dzA, c.edge_dst, c.edge_src, c.geo,
                c.grads + c.shared_off(p + "edge.W2"), mat ? c.a1 + size_t(l) * EH : nullptr, nullptr, z2,
                c.z1_only ? 1 : 0};
-      atb(q, c, c.nsplit_edge, sw, c.Ec);
+      atb(q, c, c.nsplit_edge, s6, c.Ec);
     }
     if (fz) {
       Prof pr(c, "bwd.segsum_src", st);
@@ -2819,6 +2826,7 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
     if (cs) {  // layer l's shared block is final once its weight-gradient kernels finish
       c.dep(sw, sc);
       c.dep(sw2, sc);
+      if (own3) c.dep(sw3, sc);  // (a stream joins the captured graph only once work was put on it)
       const size_t o0 = c.shared_off(p + "edge.W1"), o1 = c.shared_off(p + "node.b2") + size_t(H);
       comm_shared_async(c, o0, o1 - o0, sc);
     }
@@ -2859,6 +2867,7 @@ void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync) {
   }
   c.dep(sw, st);  // every weight gradient is final (and, with MTL-par, averaged)
   c.dep(sw2, st);
+  if (used3) c.dep(sw3, st);
   if (cs) c.dep(sc, st);
 }
 
