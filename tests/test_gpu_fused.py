@@ -148,3 +148,26 @@ def test_l2_residency_knobs_bit_identical():
     assert a["losses"] == b["losses"]
     for k in ("g", "p", "pred"):
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_species_table_layer0_p_bit_identical():
+    """Layer 0's P gathered from the per-species table T = embed [W1a | W1b] (built on the
+    B-image side stream; the default) == the node-row P GEMM (HMTL_PTAB=0): the same
+    tensor-core products per row, every step bitwise."""
+    a = run("mtl5-weak", False)
+    b = run("mtl5-weak", False, env={"HMTL_PTAB": "0"})
+    assert a["losses"] == b["losses"]
+    for k in ("g", "p", "pred"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_node_priority_and_wgrad_stream_bit_identical():
+    """Scheduling knobs change only when kernels run: graph node priorities off
+    (HMTL_NODE_PRIO=0) and the eW2 gradient on a third stream (HMTL_WGRAD3=2) give the
+    default's bits on every step."""
+    a = run("mtl5-weak", False)
+    for env in ({"HMTL_NODE_PRIO": "0"}, {"HMTL_WGRAD3": "2"}):
+        b = run("mtl5-weak", False, env=env)
+        assert a["losses"] == b["losses"], env
+        for k in ("g", "p", "pred"):
+            assert np.array_equal(a[k], b[k]), (env, k)
