@@ -1220,17 +1220,29 @@ __global__ void __launch_bounds__(256) edge_af0_kernel(const DevHdr* hdr, const 
       d[u] = dst[e];
       sl[u] = gslot[node_graph[d[u]]];
     }
+    bool uni = true;  // (head-sorted batches: the group's edges nearly always share one head)
+#pragma unroll
+    for (int u = 1; u < kEwU; ++u) uni = uni && sl[u] == sl[0];
     for (int c = lane * 4; c < W; c += 128) {
       float4 qa[kEwU], qb[kEwU], w[kEwU], b[kEwU];
       float r[kEwU];
+      if (uni) {
+        const float* hb = heads + size_t(sl[0]) * PH;
+        w[0] = ldu4(hb + off_wd + c);
+        b[0] = ldu4(hb + off_b0 + c);
+#pragma unroll
+        for (int u = 1; u < kEwU; ++u) w[u] = w[0], b[u] = b[0];
+      }
 #pragma unroll
       for (int u = 0; u < kEwU; ++u) {
         const int e = min(eb + u, E - 1);
-        const float* hb = heads + size_t(sl[u]) * PH;
         qa[u] = ld4(Qf + size_t(d[u]) * W + c);
         qb[u] = ld4(Qf + size_t(src[e]) * W + c);
-        w[u] = ldu4(hb + off_wd + c);
-        b[u] = ldu4(hb + off_b0 + c);
+        if (!uni) {
+          const float* hb = heads + size_t(sl[u]) * PH;
+          w[u] = ldu4(hb + off_wd + c);
+          b[u] = ldu4(hb + off_b0 + c);
+        }
         r[u] = dist[e];
       }
 #pragma unroll
