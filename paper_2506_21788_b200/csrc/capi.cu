@@ -469,6 +469,7 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   if (!rc) cudaMemcpy(c.d_ns, &c.NS, sizeof(int), cudaMemcpyHostToDevice);
   if (const char* e = std::getenv("HMTL_PTAB")) c.ptab_on = e[0] != '0';
   if (const char* e = std::getenv("HMTL_WGRAD3")) c.wgrad3 = std::atoi(e);
+  if (const char* e = std::getenv("HMTL_ROW_PAIR")) c.row_pair = e[0] == '1';
   if (rc) {
     free_ctx(c);
     delete h;

@@ -134,6 +134,7 @@ struct Ctx {
   int* d_ns = nullptr;      // device copy of NS (row count of the table GEMM)
   int wgrad3 = 0;          // edge eW2 weight gradient on a third side stream: 0 never, 1 layer 0 (the step's
                            // tail), 2 every layer (HMTL_WGRAD3)
+  bool row_pair = false;    // row GEMMs over one segment as CTA pairs (cta_group::2; HMTL_ROW_PAIR=1)
   int row_prefetch = 0;    // row GEMMs prefetch the next tile's forward-written rows into L2 (HMTL_ROW_PREFETCH=1; measured slower)
   int chain_prefetch = 0;  // chains prefetch their operands into L2 at launch (HMTL_CHAIN_PREFETCH=1; measured neutral)
   bool chain_pair = false;  // ... as CTA-pair (cta_group::2) kernels (HMTL_CHAIN_PAIR=1; measured slower)

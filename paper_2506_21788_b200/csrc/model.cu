@@ -866,10 +866,22 @@ void ab(const P& p, long long rows_cap, int nseg, cudaStream_t st, int sm, Ctx& 
     int Nt = p.Ncols <= 256 ? p.Ncols : 256;  // column block per tile (<= one 256-col accumulator)
     // (one wave: the largest split whose tile count still fits the SMs)
     while (Nt > 32 && mtiles * (p.Ncols / Nt) * 2 <= sm && (Nt / 2) % 32 == 0) Nt /= 2;
+    const int cap_ctas = c.tc_grid_mult > 0 ? c.row_sms * c.tc_grid_mult : (1 << 30);  // persistent when capped
+    if constexpr (!TcRow<P>::kSeg) {  // CTA pairs (cta_group::2): half of B per SM, more A stages
+      if (c.row_pair && nseg == 1 && !p.rows.perm && !p.rows.seg_off && Nt == p.Ncols && Nt % 32 == 0) {
+        tc::RowPlan pp = tc::row_plan(p.K, Nt, 0, TcRow<P>::kSlabEpi, true);
+        if (pp.resident) {
+          set_smem(tc::tc_row_kernel<TcRow<P>, true>, pp.smem);
+          const long long pairs = std::min<long long>((mtiles + 1) / 2, std::max(1, cap_ctas / 2));
+          kl_cluster(tc::tc_row_kernel<TcRow<P>, true>, dim3(unsigned(2 * pairs)), dim3(tc::kRowThreads), pp.smem, st,
+                     dim3(2, 1, 1), q, pp);
+          return;
+        }
+      }
+    }
     tc::RowPlan plan = tc::row_plan(p.K, Nt, TcRow<P>::kSeg ? tc::kSegKeyBytes : 0, TcRow<P>::kSlabEpi);
     plan.prefetch = c.row_prefetch;
     set_smem(tc::tc_row_kernel<TcRow<P>>, plan.smem);
-    const int cap_ctas = c.tc_grid_mult > 0 ? c.row_sms * c.tc_grid_mult : (1 << 30);  // persistent when capped
     kl(tc::tc_row_kernel<TcRow<P>>, gridn(mtiles * (p.Ncols / Nt), 1, cap_ctas), tc::kRowThreads, plan.smem, st, q,
        plan);
     return;

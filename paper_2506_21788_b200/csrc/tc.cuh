@@ -337,12 +337,12 @@ struct RowPlan {
 // slabs: the epilogue transposes through per-warp shared-memory slabs (segmented-sum
 // problems need them; every other problem reads .16x256b fragments and pairs lanes
 // with shuffles, leaving the 32 KB to one more A stage)
-inline RowPlan row_plan(int K, int Nt, size_t extra = 0, bool slabs = false) {
+inline RowPlan row_plan(int K, int Nt, size_t extra = 0, bool slabs = false, bool pair = false) {
   RowPlan r;
   r.Nt = Nt;
   r.epi_bytes = slabs ? kEpiBytes : 0;
   r.a_stage = size_t(2 * 128 * KC) * 4;  // hi + lo
-  const size_t b_chunk = size_t(2 * Nt * KC) * 4;
+  const size_t b_chunk = size_t(2 * (pair ? Nt / 2 : Nt) * KC) * 4;  // (pair: this CTA's column half)
   const size_t b_all = b_chunk * (K / KC);
   const size_t fixed = r.epi_bytes + kRowBars + extra + 1024;  // +1 KB: manual 1 KB alignment
   r.resident = (b_all + 2 * r.a_stage + fixed <= kSmemLimit) ? 1 : 0;
@@ -367,6 +367,24 @@ __device__ __forceinline__ uint32_t cl_size() {
 }
 __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// wait with cluster-scope acquire (arrivals may come from the cluster peer)
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// arrive on the same-offset barrier of cluster CTA `rank` (release at cluster scope)
+__device__ __forceinline__ void mbar_arrive_rank(uint64_t* bar, uint32_t rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
 }
 __device__ __forceinline__ float ld_dsmem(uint32_t saddr, uint32_t rank) {
   uint32_t a;
@@ -415,7 +433,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-template <class P>
+// kPair: CTA pairs (cta_group::2, 2-CTA clusters) -- M = 256 MMAs issued by the leader,
+// CTA r owning m-tile 2t + r of pair-tile t and columns [r Nt/2, (r+1) Nt/2) of the resident
+// B (half the shared memory for B: more A stages); one head segment, one column block
+template <class P, bool kPair = false>
 __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan plan) {
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
   uint8_t* smem_raw = align1k(smem_dyn);  // SW128 atoms need 1 KB alignment
@@ -436,29 +457,52 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t acc_cols = Nt <= 32 ? 32 : (Nt <= 64 ? 64 : (Nt <= 128 ? 128 : 256));
   constexpr int kProdThreads = kProdWarps * 32;
-  if (warp == kMmaWarp) tmem_alloc(tmem_slot, 2 * acc_cols);
+  const uint32_t crank = kPair ? cl_rank() : 0;
+  const bool leader = crank == 0;
+  if (warp == kMmaWarp) {
+    if constexpr (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(2 * acc_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      tmem_alloc(tmem_slot, 2 * acc_cols);
+    }
+  }
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], kProdThreads);
+      mbar_init(&full[s], kPair ? 2 * kProdWarps : kProdThreads);  // (pair: one arrival per warp of each CTA)
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accfull[b], 1);
-      mbar_init(&accempty[b], kEpiWarps * 32);
+      mbar_init(&accempty[b], kPair ? 2 * kEpiWarps : kEpiWarps * 32);
     }
-    mbar_init(bfull, 1);
+    mbar_init(bfull, kPair && leader ? 2 : 1);  // (pair leader: + the peer's forwarded completion)
     mbar_init(bdone, 1);
     fence_mbar_init();
   }
-  const uint32_t b_slice = uint32_t(Nt) * 128;  // bytes of one (chunk, hi|lo) B slice
+  const uint32_t b_slice = uint32_t(kPair ? Nt / 2 : Nt) * 128;  // bytes of one (chunk, hi|lo) B slice
   const int nchunks = p.K / KC;
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cl_sync();  // both CTAs' barriers exist before any remote arrival
+  else __syncthreads();
   tc_fence_after();
+  // this CTA's arrival on a barrier the pair leader waits on (pair: one elected lane per warp)
+  auto arrive_lead = [&](uint64_t* bar) {
+    if constexpr (kPair) {
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(bar);
+        else mbar_arrive_rank(bar, 0);
+      }
+    } else {
+      mbar_arrive(bar);
+    }
+  };
   const uint32_t tmem = *tmem_slot;
   // ablation bits read once: a global load per chunk sat on the producer's critical path
   const int dbg = g_tc_debug;
-  if constexpr (RowPf<P>::value) {  // the first tile's rows of a plain row range, streamed into L2
+  if constexpr (RowPf<P>::value && !kPair) {  // the first tile's rows of a plain row range, streamed into L2
     // while the previous kernel drains (inputs written long before it: safe before pdl_wait);
     // the producer prefetches each next tile as it starts one (below)
     if (plan.prefetch && tid == kRowThreads - 1 && !p.rows.perm && !p.rows.seg_off) {
@@ -485,11 +529,20 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
   __syncthreads();
   const int total_m = mt_seg[p.rows.nseg];
   const int ntn = p.Ncols / Nt;
-  const int total = total_m * ntn;
+  const int total = kPair ? (total_m + 1) / 2 : total_m * ntn;  // (pair: pair-tiles)
   // contiguous tile range per CTA: consecutive tiles share a head segment / column block,
   // so the resident B image is reloaded only at segment boundaries
-  const int t_beg = int((long long)blockIdx.x * total / gridDim.x);
-  const int t_end = int((long long)(blockIdx.x + 1) * total / gridDim.x);
+  const int units = kPair ? int(gridDim.x) / 2 : int(gridDim.x), unit = kPair ? int(blockIdx.x) / 2 : int(blockIdx.x);
+  const int t_beg = int((long long)unit * total / units);
+  const int t_end = int((long long)(unit + 1) * total / units);
+  // this CTA's m-tile of tile t (pair: m-tile 2t + rank of the single segment)
+  auto m_of = [&](int t) { return kPair ? 2 * t + int(crank) : t / ntn; };
+  auto seg_of = [&](int tm) {
+    int seg = 0;
+    if constexpr (!kPair)
+      while (tm >= mt_seg[seg + 1]) ++seg;
+    return seg;
+  };
 
   if (warp < kProdWarps) {  // ------------------------------------- producers
     // 4 lanes per row, each lane two k-groups (32 contiguous bytes of the row):
@@ -502,12 +555,11 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
     };
     auto set_tile = [&](Cur& u) {
       if (u.t >= t_end) return;
-      const int tm = u.t / ntn;
-      u.n0 = (u.t % ntn) * Nt;
-      int seg = 0;
-      while (tm >= mt_seg[seg + 1]) ++seg;
+      const int tm = m_of(u.t);
+      u.n0 = kPair ? 0 : (u.t % ntn) * Nt;
+      const int seg = seg_of(tm);
       u.seg = seg;
-      if constexpr (RowPf<P>::value) {  // the next tile's row streams into L2, one tile ahead
+      if constexpr (RowPf<P>::value && !kPair) {  // the next tile's row streams into L2, one tile ahead
         if (plan.prefetch && tid == 0 && !p.rows.perm && !p.rows.seg_off && u.t + 1 < t_end && (u.t + 1) / ntn != tm) {
           const int r0 = (tm + 1) * 128, cnt = p.rows.end(0);
           if (r0 < cnt) p.prefetch_rows(r0, r0 + 128 < cnt ? r0 + 128 : cnt);
@@ -575,7 +627,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
             bulk_g2s(lo + 128 * KC * 4 + part * b_slice,
                      bsrc + (size_t(u.c) * 2 + part) * p.Ncols * KC + size_t(u.n0) * KC, b_slice, &full[st]);
         } else {
-          mbar_arrive(&full[st]);
+          arrive_lead(&full[st]);
         }
       };
       Cur prev;
@@ -636,7 +688,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
           bulk_g2s(reinterpret_cast<uint8_t*>(a_lo + 128 * KC) + part * b_slice,
                    bsrc + (size_t(u.c) * 2 + part) * p.Ncols * KC + size_t(u.n0) * KC, b_slice, &full[stage]);
       } else {
-        mbar_arrive(&full[stage]);
+        arrive_lead(&full[stage]);
       }
       if (++stage == kStages) stage = 0, phase ^= 1;
     };
@@ -660,6 +712,46 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
       succ(B);
       if (B.t < t_end) load(B, xb);
     }
+    }
+  } else if (kPair && warp == kMmaWarp) {  // ------------------- pair: resident B half + MMA issue (leader)
+    // this CTA's column half of the single resident B image, once
+    if (t_beg < t_end) {
+      if (lane == 0) {
+        mbar_expect_tx(bfull, uint32_t(nchunks) * 2 * b_slice);
+        for (int c = 0; c < nchunks; ++c)
+          for (int part = 0; part < 2; ++part)
+            bulk_g2s(reinterpret_cast<uint8_t*>(bres) + (size_t(c) * 2 + part) * b_slice,
+                     p.bimg + (size_t(c) * 2 + part) * p.Ncols * KC + size_t(crank) * (Nt / 2) * KC, b_slice, bfull);
+      }
+      __syncwarp();
+      if (!leader) {  // the leader's MMAs read our half: forward its arrival
+        mbar_wait(bfull, 0);
+        if (lane == 0) mbar_arrive_rank(bfull, 0);
+      } else {
+        mbar_wait_cl(bfull, 0);
+        tc_fence_after();
+        int stage = 0;
+        uint32_t phase = 0;
+        int ab = 0;
+        uint32_t aphase = 0;
+        const uint32_t idesc = (idesc_tf32(Nt) & ~(31u << 24)) | (uint32_t(256 >> 4) << 24);
+        for (int t = t_beg; t < t_end; ++t) {
+          mbar_wait_cl(&accempty[ab], aphase ^ 1);
+          tc_fence_after();
+          for (int c = 0; c < nchunks; ++c) {
+            mbar_wait_cl(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t a_hi = smem_u32(stages + stage * SB), a_lo = a_hi + 128 * KC * 4;
+            const uint32_t b_hi = smem_u32(bres) + uint32_t(c) * 2 * b_slice, b_lo = b_hi + b_slice;
+            issue_chunk_pair(tmem + ab * acc_cols, a_hi, a_lo, b_hi, b_lo, idesc, c != 0);
+            commit_pair(&empty[stage]);
+            if (c == nchunks - 1) commit_pair(&accfull[ab]);
+            __syncwarp();
+            if (++stage == kStages) stage = 0, phase ^= 1;
+          }
+          if (++ab == 2) ab = 0, aphase ^= 1;
+        }
+      }
     }
   } else if (warp == kMmaWarp) {  // --------------------------------- MMA issuer + resident B
     int stage = 0;
@@ -721,9 +813,8 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
     float* slab = epi_smem + (warp - kEpiWarp0) * 32 * 32;  // 32 rows x 32 cols, 16 B chunks XOR-swizzled
     const int nslab = (Nt + 31) / 32;
     for (int t = t_beg; t < t_end; ++t) {
-      const int tm = t / ntn, n0 = (t % ntn) * Nt;
-      int seg = 0;
-      while (tm >= mt_seg[seg + 1]) ++seg;
+      const int tm = m_of(t), n0 = kPair ? 0 : (t % ntn) * Nt;
+      const int seg = seg_of(tm);
       if constexpr (!RowSlab<P>::value) {
         {  // ---- register-fragment epilogue (no shared memory; plan.epi_bytes == 0)
           // .16x256b reads of this quadrant's two 16-lane halves; lane pairs (l, l^1) swap
@@ -770,7 +861,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
             }
           }
           tc_fence_before();
-          mbar_arrive(&accempty[ab]);
+          arrive_lead(&accempty[ab]);
           if (++ab == 2) ab = 0, aphase ^= 1;
           continue;
         }
@@ -880,14 +971,20 @@ __global__ void __launch_bounds__(kRowThreads, 1) tc_row_kernel(P p, RowPlan pla
         }
       }
       tc_fence_before();
-      mbar_arrive(&accempty[ab]);
+      arrive_lead(&accempty[ab]);
       if (++ab == 2) ab = 0, aphase ^= 1;
       }
     }
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == kMmaWarp) tmem_dealloc(tmem, 2 * acc_cols);
+  if constexpr (kPair) {  // the leader's MMAs read both CTAs' shared memory: nobody leaves early
+    cl_sync();
+    if (warp == kMmaWarp)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * acc_cols));
+  } else {
+    __syncthreads();
+    if (warp == kMmaWarp) tmem_dealloc(tmem, 2 * acc_cols);
+  }
 }
 
 // ================================================================ reduce GEMM

@@ -171,3 +171,14 @@ def test_node_priority_and_wgrad_stream_bit_identical():
         assert a["losses"] == b["losses"], env
         for k in ("g", "p", "pred"):
             assert np.array_equal(a[k], b[k]), (env, k)
+
+
+def test_cta_pair_row_engine_bit_identical():
+    """Row GEMMs over one segment as CTA pairs (opt-in HMTL_ROW_PAIR=1; tc.cuh kPair:
+    tcgen05.mma.cta_group::2, M = 256, each CTA holding half of the resident B) == the
+    single-CTA engine: the same per-row products in the same order, every step bitwise."""
+    a = run("mtl5-weak", False, env={"HMTL_ROW_PAIR": "1"})
+    b = run("mtl5-weak", False)
+    assert a["losses"] == b["losses"]
+    for k in ("g", "p", "pred"):
+        assert np.array_equal(a[k], b[k]), k
