@@ -245,7 +245,7 @@ bool sorted_by_slot(const Ctx& c, const uint8_t* ds, int G);  // graphs grouped 
 void launch_prep(Ctx& c, cudaStream_t st);      // arena -> node/graph tables, routing
 void launch_nbr(Ctx& c, cudaStream_t st);       // neighbour list, CSR, rev, edge offsets
 void launch_nbr_pbc(Ctx& c, cudaStream_t st);   // ... with periodic images (cell list)
-void launch_route(Ctx& c, cudaStream_t st);     // head routing + head-sorted permutations
+void launch_route(Ctx& c, cudaStream_t st, bool routed);  // head routing (unless `routed`) + head-sorted permutations
 void launch_forward(Ctx& c, cudaStream_t st);   // ModelT::forward
 void launch_loss(Ctx& c, float w_e, float w_f, cudaStream_t st);
 void launch_backward(Ctx& c, cudaStream_t st, bool comm_sync = false);  // ModelT::backward (upstreams in c.dE/c.dF)

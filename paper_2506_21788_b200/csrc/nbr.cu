@@ -257,11 +257,14 @@ __global__ void __launch_bounds__(1024) route_kernel(DevHdr* hdr, const int* __r
     hdr->seg_graph[0] = hdr->seg_node[0] = hdr->seg_edge[0] = 0;
   }
   __syncthreads();
+  // (an edge overflow empties every edge range: the guard in rev_kernel may be rewriting
+  // edge_offset concurrently, this kernel running beside the neighbour-list writers)
+  const bool ovf = hdr->err & kErrEdgeOverflow;
   if (G <= 1024) {  // one graph per thread: its slot, node and edge counts loaded once for every slot's pass
     const int g = tid;
     const int gs = g < G ? gslot[g] : -1;
     const int nn = g < G ? graph_offset[g + 1] - graph_offset[g] : 0;
-    const int ne = g < G ? edge_offset[g + 1] - edge_offset[g] : 0;
+    const int ne = g < G && !ovf ? edge_offset[g + 1] - edge_offset[g] : 0;
     for (int s = 0; s < S; ++s) {
       const bool f = gs == s;
       int v[3] = {f ? 1 : 0, f ? nn : 0, f ? ne : 0};
@@ -313,7 +316,7 @@ __global__ void __launch_bounds__(1024) route_kernel(DevHdr* hdr, const int* __r
       const int g = base + tid;
       const bool f = g < G && gslot[g] == s;
       int v[3] = {f ? 1 : 0, f ? graph_offset[g + 1] - graph_offset[g] : 0,
-                  f ? edge_offset[g + 1] - edge_offset[g] : 0};
+                  f && !ovf ? edge_offset[g + 1] - edge_offset[g] : 0};
       int x[3] = {v[0], v[1], v[2]};
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
@@ -397,7 +400,7 @@ void launch_prep(Ctx& c, cudaStream_t st) {
 }
 
 void launch_nbr(Ctx& c, cudaStream_t st) {
-  if (c.pbc) return launch_nbr_pbc(c, st), launch_route(c, st);
+  if (c.pbc) return launch_nbr_pbc(c, st), launch_route(c, st, false);
   const int warps_blocks = grid_for((long long)c.Nc * 32, 256, c.sm_count * 16);
   {
     Prof pr(c, "nbr.count", st);
@@ -406,6 +409,15 @@ void launch_nbr(Ctx& c, cudaStream_t st) {
   {
     Prof pr(c, "nbr.scan", st);
     kl(scan_kernel, 1, 1024, 0, st, c.hdr, c.deg, c.row_ptr, c.graph_offset, c.edge_offset, c.Ec);
+  }
+  // the head routing (one CTA) needs only the graph and edge offsets: it runs on a side
+  // stream beside the edge writers instead of after them
+  cudaStream_t sr = c.side(c.s_e, st);
+  if (sr != st) {
+    c.dep(st, sr);
+    Prof pr(c, "route", sr);
+    kl(route_kernel, 1, 1024, 0, sr, c.hdr, c.gslot, c.graph_offset, c.edge_offset, c.gperm, c.gnode_base,
+       c.gedge_base, c.S);
   }
   {
     Prof pr(c, "nbr.write", st);
@@ -417,7 +429,8 @@ void launch_nbr(Ctx& c, cudaStream_t st) {
     kl(rev_kernel, grid_for(std::max<long long>(c.Ec, c.Nc + 1), 256, c.sm_count * 8), 256, 0, st, c.hdr, c.row_ptr,
        c.edge_src, c.edge_dst, c.rev, c.edge_offset);
   }
-  launch_route(c, st);
+  c.dep(sr, st);
+  launch_route(c, st, sr != st);
 }
 
 #ifdef HMTL_CHECKED
@@ -471,8 +484,8 @@ __global__ void check_structure_kernel(const DevHdr* hdr, const int* __restrict_
 #endif
 
 // head routing + head-sorted permutations (shared by both neighbour lists)
-void launch_route(Ctx& c, cudaStream_t st) {
-  {
+void launch_route(Ctx& c, cudaStream_t st, bool routed) {
+  if (!routed) {
     Prof pr(c, "route", st);
     kl(route_kernel, 1, 1024, 0, st, c.hdr, c.gslot, c.graph_offset, c.edge_offset, c.gperm, c.gnode_base,
                                      c.gedge_base, c.S);
