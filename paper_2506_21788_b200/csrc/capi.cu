@@ -350,6 +350,7 @@ int hmtl_ctx_create(int device, const hmtl_hyper* hp, uint64_t seed, const int* 
   // critical path (measured: 120 of 148 -> step 1.003 -> 0.994 ms; profiles/r01_ab_red_knobs.txt)
   c.red_sms = std::max(1, c.sm_count * 13 / 16);
   if (const char* e = std::getenv("HMTL_CHAIN_M")) c.chain_mr = std::atoi(e) == 64 ? 64 : 128;
+  if (const char* e = std::getenv("HMTL_CHAIN_M_FWD")) c.chain_mr_fwd = std::atoi(e) == 64 ? 64 : (std::atoi(e) == 128 ? 128 : 0);
   if (const char* e = std::getenv("HMTL_CHAIN_CS")) c.chain_cs = std::atoi(e) == 4 ? 4 : (std::atoi(e) == 2 ? 2 : 1);
   if (const char* e = std::getenv("HMTL_NO_RED_TMA")) c.red_tma = e[0] == '0';
   if (const char* e = std::getenv("HMTL_RED_SEGX")) c.red_seg_mult = std::max(1, std::min(8, std::atoi(e)));

@@ -191,6 +191,7 @@ struct Ctx {
   int red_min_tail = 4;     // ... for layer 0's weight gradients, the step's tail (HMTL_RED_MINCH_TAIL)
   int red_min_now = 4;      // (the value atb() uses while the backward is enqueued)
   bool red_tma = true;      // TMA operand path for plain row-major weight gradients (HMTL_NO_RED_TMA=1 off)
+  int chain_mr_fwd = 64;    // ... for the forward chains (HMTL_CHAIN_M_FWD; 0 = chain_mr)
   int chain_mr = 128;       // node rows per chain CTA: 128 or 64 (HMTL_CHAIN_M; 64 only with the 2-CTA split)
   int chain_cs = 2;         // node-chain cluster size: 2 = column split over a CTA pair (HMTL_CHAIN_CS=1: one CTA)
   float *a1 = nullptr, *af0 = nullptr, *sf0 = nullptr;

@@ -1001,7 +1001,10 @@ void launch_chain(Ctx& c, const char* name, int G, const chain::Gemm* gs, cudaSt
   q.dbg = c.chain_dbg;
   q.rows_cap = int(c.Nc);
   q.prefetch = c.chain_prefetch;
-  const int mr = c.chain_mr;  // node rows per CTA (128 or 64)
+  // node rows per CTA (128 or 64): the forward chains run alone on the GPU, so 64-row CTAs
+  // (twice the CTAs) pay off there; the backward's share the SMs with weight gradients
+  const bool fwd = name[0] == 'f';
+  const int mr = fwd && c.chain_mr_fwd ? c.chain_mr_fwd : c.chain_mr;
   const int grid = int((c.Nc + mr - 1) / mr);
   // CS-CTA clusters split every GEMM's columns (chained operand exchanged through DSMEM)
   int cs = c.chain_cs;

@@ -182,3 +182,13 @@ def test_cta_pair_row_engine_bit_identical():
     assert a["losses"] == b["losses"]
     for k in ("g", "p", "pred"):
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_forward_chain_row_count_bit_identical():
+    """Forward node chains in 64-row CTAs (M = 64 MMAs, twice the CTAs; the default) ==
+    128-row CTAs (HMTL_CHAIN_M_FWD=128): the same per-row products, every step bitwise."""
+    a = run("mtl5-weak", False)
+    b = run("mtl5-weak", False, env={"HMTL_CHAIN_M_FWD": "128"})
+    assert a["losses"] == b["losses"]
+    for k in ("g", "p", "pred"):
+        assert np.array_equal(a[k], b[k]), k
